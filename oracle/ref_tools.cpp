@@ -1,0 +1,446 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" shim over the *unmodified* reference sources (compiled from where
+// they lie under /root/reference/proj/core by oracle/Makefile into
+// oracle/_ref/libllspdz_ref.so).  It exists for three consumers only:
+//   * tests/golden/make_golden.py  — dumps golden vectors from the reference,
+//   * the oracle pin tests         — restatement (spdz_oracle.c) vs reference,
+//   * bench.py --impl reference / cpu_baseline — times the reference CPU path.
+//
+// Every function cites the reference entry point it forwards to.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <thread>
+#include <string>
+#include <vector>
+
+#include "mpc/backend.hpp"
+#include "mpc/circuit.hpp"
+#include "mpc/hash.hpp"
+#include "mpc/ir.hpp"
+#include "mpc/linear.hpp"
+#include "mpc/oracle.hpp"
+#include "mpc/preproc.hpp"
+#include "mpc/runtime.hpp"
+#include "mpc/spdz.hpp"
+#include "mpc/triple_store.hpp"
+
+using namespace mpc;
+using spdz::ShareVec;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Error codes mirror include/spdz_b200.h so tests can compare error behaviour.
+enum : int {
+    RC_OK = 0,
+    RC_LANE_MISMATCH = 1,
+    RC_TRIPLE_SHORTAGE = 2,
+    RC_BACKEND_UNAVAILABLE = 3,
+    RC_TRIPLE_EXHAUSTED = 4,
+    RC_TRIPLE_SHAPE_MISMATCH = 5,
+    RC_MASK_EXHAUSTED = 6,
+    RC_PEER_TIMEOUT = 7,
+    RC_LANE_COUNT_MISMATCH = 8,
+    RC_MALFORMED = 9,
+    RC_MAC_CHECK_FAILED = 10,
+    RC_SLICE_TOO_SMALL = 11,
+    RC_OTHER = 99,
+};
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return RC_OK;
+    } catch (const backend::LaneMismatch& e) {
+        g_err = e.what();
+        return RC_LANE_MISMATCH;
+    } catch (const backend::TripleShortage& e) {
+        g_err = e.what();
+        return RC_TRIPLE_SHORTAGE;
+    } catch (const backend::BackendUnavailable& e) {
+        g_err = e.what();
+        return RC_BACKEND_UNAVAILABLE;
+    } catch (const spdz::TripleExhausted& e) {
+        g_err = e.what();
+        return RC_TRIPLE_EXHAUSTED;
+    } catch (const spdz::TripleShapeMismatch& e) {
+        g_err = e.what();
+        return RC_TRIPLE_SHAPE_MISMATCH;
+    } catch (const spdz::MaskExhausted& e) {
+        g_err = e.what();
+        return RC_MASK_EXHAUSTED;
+    } catch (const net::PeerTimeout& e) {
+        g_err = e.what();
+        return RC_PEER_TIMEOUT;
+    } catch (const net::LaneCountMismatch& e) {
+        g_err = e.what();
+        return RC_LANE_COUNT_MISMATCH;
+    } catch (const net::MalformedShareMessage& e) {
+        g_err = e.what();
+        return RC_MALFORMED;
+    } catch (const spdz::MacCheckFailed& e) {
+        g_err = e.what();
+        return RC_MAC_CHECK_FAILED;
+    } catch (const linear::SliceTooSmall& e) {
+        g_err = e.what();
+        return RC_SLICE_TOO_SMALL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return RC_OTHER;
+    }
+}
+
+ShareVec sv(const uint32_t* v, const uint32_t* m, size_t n) {
+    ShareVec s;
+    s.vals.assign(v, v + n);
+    s.macs.assign(m, m + n);
+    return s;
+}
+
+void put(const ShareVec& s, uint32_t* v, uint32_t* m) {
+    std::memcpy(v, s.vals.data(), s.vals.size() * 4);
+    std::memcpy(m, s.macs.data(), s.macs.size() * 4);
+}
+
+circuit::CircuitGraph compile_text(const std::string& text) {
+    auto parsed = ir::parse_module(text);
+    if (!parsed.ok()) throw std::runtime_error("parse failed: " + parsed.diagnostics[0].message);
+    return circuit::compile_graph(ir::validate_entry(parsed.module, "main"));
+}
+
+preproc::Inputs make_inputs(int n_inputs, const char* const* names, const uint32_t* const* vals,
+                            const uint64_t* lens) {
+    preproc::Inputs in;
+    for (int i = 0; i < n_inputs; ++i) in[names[i]] = std::vector<uint32_t>(vals[i], vals[i] + lens[i]);
+    return in;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* reft_last_error() { return g_err.c_str(); }
+
+// test_util.hpp:46-51
+void reft_rand_field_vec(uint64_t n, uint64_t seed, uint32_t* out) {
+    std::mt19937_64 rng(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = uint32_t(rng() % kPrime);
+}
+
+uint64_t reft_splitmix64(uint64_t* state) { return splitmix64(*state); }  // hash.hpp:21-26
+uint64_t reft_fnv1a64(const void* data, uint64_t len, uint64_t seed) { return fnv1a64(data, len, seed); }
+
+// ---- Dealer (spdz.cpp:162-263) ----
+void* reft_dealer_new(int n, uint64_t seed, uint64_t prime) { return new spdz::Dealer(n, seed, prime); }
+void reft_dealer_free(void* h) { delete static_cast<spdz::Dealer*>(h); }
+uint32_t reft_dealer_alpha(void* h) { return static_cast<spdz::Dealer*>(h)->alpha(); }
+uint32_t reft_dealer_alpha_share(void* h, int i) { return static_cast<spdz::Dealer*>(h)->alpha_share(i); }
+uint32_t reft_dealer_random_element(void* h) { return static_cast<spdz::Dealer*>(h)->random_element(); }
+
+// out_vals/out_macs: n_parties * len, party-major.
+void reft_dealer_share(void* h, const uint32_t* xs, uint64_t len, uint32_t* out_vals, uint32_t* out_macs) {
+    auto* d = static_cast<spdz::Dealer*>(h);
+    auto s = d->share(std::vector<uint32_t>(xs, xs + len));
+    for (size_t i = 0; i < s.size(); ++i) put(s[i], out_vals + i * len, out_macs + i * len);
+}
+
+void reft_dealer_share_random(void* h, uint64_t len, uint32_t* clear, uint32_t* out_vals, uint32_t* out_macs) {
+    auto* d = static_cast<spdz::Dealer*>(h);
+    std::vector<uint32_t> c;
+    auto s = d->share_random(len, &c);
+    std::memcpy(clear, c.data(), len * 4);
+    for (size_t i = 0; i < s.size(); ++i) put(s[i], out_vals + i * len, out_macs + i * len);
+}
+
+// planes: 6 arrays (a.v a.m b.v b.m c.v c.m), each n_parties * lanes.
+void reft_dealer_triples(void* h, uint64_t lanes, uint32_t* const* planes) {
+    auto* d = static_cast<spdz::Dealer*>(h);
+    auto t = d->triples(lanes);
+    for (size_t i = 0; i < t.size(); ++i) {
+        size_t o = i * lanes;
+        put(t[i].a, planes[0] + o, planes[1] + o);
+        put(t[i].b, planes[2] + o, planes[3] + o);
+        put(t[i].c, planes[4] + o, planes[5] + o);
+    }
+}
+
+// planes: A.v A.m (n*rows*din), B.v B.m (n*din), C.v C.m (n*rows).
+void reft_dealer_matrix_triples(void* h, uint32_t din, uint32_t rows, uint32_t* const* planes) {
+    auto* d = static_cast<spdz::Dealer*>(h);
+    auto t = d->matrix_triples(din, rows);
+    size_t cells = size_t(din) * rows;
+    for (size_t i = 0; i < t.size(); ++i) {
+        put(t[i].a, planes[0] + i * cells, planes[1] + i * cells);
+        put(t[i].b, planes[2] + i * din, planes[3] + i * din);
+        put(t[i].c, planes[4] + i * rows, planes[5] + i * rows);
+    }
+}
+
+// ---- stores (triple_store.cpp:248-287) ----
+struct RefStores {
+    std::vector<std::shared_ptr<spdz::TripleStore>> s;
+};
+
+void* reft_make_stores(int n, uint64_t seed, uint64_t scalars, uint64_t n_mshapes, const uint32_t* mshapes,
+                       uint64_t masks) {
+    spdz::Dealer d(n, seed);
+    std::vector<std::pair<uint32_t, uint32_t>> shapes;
+    for (uint64_t i = 0; i < n_mshapes; ++i) shapes.emplace_back(mshapes[2 * i], mshapes[2 * i + 1]);
+    auto* r = new RefStores;
+    r->s = spdz::make_dealer_stores(d, scalars, shapes, masks);
+    return r;
+}
+void reft_free_stores(void* h) { delete static_cast<RefStores*>(h); }
+uint32_t reft_store_alpha_share(void* h, int p) { return static_cast<RefStores*>(h)->s.at(p)->alpha_share; }
+// planes: 6 arrays of `scalars` each
+void reft_store_scalars(void* h, int p, uint32_t* const* planes) {
+    auto& s = *static_cast<RefStores*>(h)->s.at(p);
+    const std::vector<uint32_t>* src[6] = {&s.a_vals, &s.a_macs, &s.b_vals, &s.b_macs, &s.c_vals, &s.c_macs};
+    for (int i = 0; i < 6; ++i) std::memcpy(planes[i], src[i]->data(), src[i]->size() * 4);
+}
+void reft_store_matrix(void* h, int p, uint64_t idx, uint32_t* const* planes) {
+    auto& m = static_cast<RefStores*>(h)->s.at(p)->matrix.at(idx);
+    put(m.a, planes[0], planes[1]);
+    put(m.b, planes[2], planes[3]);
+    put(m.c, planes[4], planes[5]);
+}
+void reft_store_masks(void* h, int p, uint32_t* val, uint32_t* mac, uint32_t* clear) {
+    auto& s = *static_cast<RefStores*>(h)->s.at(p);
+    for (size_t i = 0; i < s.masks.size(); ++i) {
+        val[i] = s.masks[i].val;
+        mac[i] = s.masks[i].mac;
+        clear[i] = s.masks[i].clear;
+    }
+}
+// triple_store.cpp:108-134 (consumption semantics)
+int reft_store_take_range(void* h, int p, uint64_t offset, uint64_t lanes) {
+    return guard([&] { static_cast<RefStores*>(h)->s.at(p)->take_range(offset, lanes); });
+}
+int reft_store_take_matrix_at(void* h, int p, uint64_t idx, uint32_t din, uint32_t rows) {
+    return guard([&] { static_cast<RefStores*>(h)->s.at(p)->take_matrix_at(idx, din, rows); });
+}
+
+// ---- CpuBackend (backend.cpp:25-84) ----
+int reft_cpu_add_batch(const uint32_t* xv, const uint32_t* xm, uint64_t nx, const uint32_t* yv,
+                       const uint32_t* ym, uint64_t ny, uint32_t* zv, uint32_t* zm) {
+    return guard([&] { put(backend::make_cpu_backend()->add_batch(sv(xv, xm, nx), sv(yv, ym, ny)), zv, zm); });
+}
+int reft_cpu_sub_batch(const uint32_t* xv, const uint32_t* xm, uint64_t nx, const uint32_t* yv,
+                       const uint32_t* ym, uint64_t ny, uint32_t* zv, uint32_t* zm) {
+    return guard([&] { put(backend::make_cpu_backend()->sub_batch(sv(xv, xm, nx), sv(yv, ym, ny)), zv, zm); });
+}
+// tri: 6 planes of tl lanes
+int reft_cpu_mul_mask(const uint32_t* xv, const uint32_t* xm, const uint32_t* yv, const uint32_t* ym,
+                      uint64_t n, const uint32_t* const* tri, uint64_t tl, uint32_t* d, uint32_t* e) {
+    return guard([&] {
+        spdz::TripleShares t{sv(tri[0], tri[1], tl), sv(tri[2], tri[3], tl), sv(tri[4], tri[5], tl)};
+        std::vector<uint32_t> dd, ee;
+        backend::make_cpu_backend()->mul_mask(sv(xv, xm, n), sv(yv, ym, n), t, dd, ee);
+        std::memcpy(d, dd.data(), dd.size() * 4);
+        std::memcpy(e, ee.data(), ee.size() * 4);
+    });
+}
+int reft_cpu_mul_combine(const uint32_t* const* tri, uint64_t tl, const uint32_t* d, const uint32_t* e,
+                         uint64_t n, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm) {
+    return guard([&] {
+        spdz::TripleShares t{sv(tri[0], tri[1], tl), sv(tri[2], tri[3], tl), sv(tri[4], tri[5], tl)};
+        put(backend::make_cpu_backend()->mul_combine(t, std::vector<uint32_t>(d, d + n),
+                                                      std::vector<uint32_t>(e, e + n), party, alpha),
+            zv, zm);
+    });
+}
+int reft_cpu_reduce_add(const uint32_t* xv, const uint32_t* xm, uint64_t n, uint32_t* zv, uint32_t* zm) {
+    return guard([&] { put(backend::make_cpu_backend()->reduce_add(sv(xv, xm, n)), zv, zm); });
+}
+// backend.cpp:90-121 + backend.hpp:58-76
+int reft_registry_routes_to_cpu(uint64_t stub_min, uint64_t lanes) {
+    backend::BackendRegistry reg;
+    reg.register_preferred(backend::make_gpu_stub(stub_min));
+    return &reg.select(lanes) == &reg.cpu();
+}
+
+// ---- public-constant rules (spdz.cpp:35-75); x is updated in place ----
+// op: 0 add_public 1 sub_public 2 rsub_public 3 mul_public 4 mul_public_scalar(k[0]) 5 share_of_public
+void reft_public_op(int op, uint32_t* xv, uint32_t* xm, uint64_t n, const uint32_t* k, int party,
+                    uint32_t alpha) {
+    ShareVec x = sv(xv, xm, n);
+    std::vector<uint32_t> kv(k, k + (op == 4 ? 1 : n));
+    switch (op) {
+        case 0: spdz::add_public(x, kv, party, alpha); break;
+        case 1: spdz::sub_public(x, kv, party, alpha); break;
+        case 2: spdz::rsub_public(x, kv, party, alpha); break;
+        case 3: spdz::mul_public(x, kv); break;
+        case 4: spdz::mul_public_scalar(x, kv[0]); break;
+        case 5: x = spdz::share_of_public(kv, party, alpha); break;
+    }
+    put(x, xv, xm);
+}
+
+// spdz.cpp:77-96
+void reft_beaver_combine(const uint32_t* const* tri, const uint32_t* d, const uint32_t* e, uint64_t n,
+                         int party, uint32_t alpha, uint32_t* zv, uint32_t* zm) {
+    spdz::TripleShares t{sv(tri[0], tri[1], n), sv(tri[2], tri[3], n), sv(tri[4], tri[5], n)};
+    put(spdz::beaver_combine(t, std::vector<uint32_t>(d, d + n), std::vector<uint32_t>(e, e + n), party, alpha),
+        zv, zm);
+}
+
+// spdz.cpp:98-124; mt planes: A.v A.m B.v B.m C.v C.m
+void reft_matrix_combine(uint32_t din, uint32_t rows, const uint32_t* const* mt, const uint32_t* D,
+                         const uint32_t* E, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm) {
+    spdz::MatrixTripleShares t;
+    t.din = din;
+    t.rows = rows;
+    size_t cells = size_t(din) * rows;
+    t.a = sv(mt[0], mt[1], cells);
+    t.b = sv(mt[2], mt[3], din);
+    t.c = sv(mt[4], mt[5], rows);
+    put(spdz::matrix_combine(t, std::vector<uint32_t>(D, D + cells), std::vector<uint32_t>(E, E + din), party,
+                             alpha),
+        zv, zm);
+}
+
+// spdz.cpp:126-138
+uint32_t reft_mac_sigma(uint64_t n, const uint64_t* batch, const uint32_t* lane, const uint32_t* value,
+                        const uint32_t* mac, uint64_t coin, uint32_t alpha) {
+    std::vector<spdz::OpenRecord> recs(n);
+    for (uint64_t i = 0; i < n; ++i) recs[i] = {batch[i], lane[i], value[i], mac[i]};
+    return spdz::mac_sigma(recs, coin, alpha);
+}
+uint64_t reft_commit_sigma(uint32_t sigma, uint64_t nonce) { return spdz::commit_sigma(sigma, nonce); }
+int reft_verify_sigmas(uint64_t n, const uint32_t* sig, const uint64_t* nonces, const uint64_t* commits) {
+    return guard([&] {
+        spdz::verify_sigmas(std::vector<uint32_t>(sig, sig + n), std::vector<uint64_t>(nonces, nonces + n),
+                            std::vector<uint64_t>(commits, commits + n));
+    });
+}
+
+// linear.cpp:7-21. Returns tile count, or -code on error.
+int64_t reft_plan_tiles(uint32_t din, uint32_t dout, uint64_t slice, uint32_t* starts, uint32_t* counts,
+                        uint64_t cap) {
+    linear::TilePlan plan;
+    int rc = guard([&] { plan = linear::plan_tiles(din, dout, slice); });
+    if (rc) return -rc;
+    for (size_t i = 0; i < plan.tiles.size() && i < cap; ++i) {
+        starts[i] = plan.tiles[i].row_start;
+        counts[i] = plan.tiles[i].row_count;
+    }
+    return int64_t(plan.tiles.size());
+}
+
+// ---- graph helpers (compile-time front end; only used to learn node ids) ----
+// Writes "id kind lanes private op0 op1 op2\n" lines. Returns bytes needed.
+uint64_t reft_graph_dump(const char* ir_text, char* buf, uint64_t cap) {
+    std::string out;
+    int rc = guard([&] {
+        auto g = compile_text(ir_text);
+        for (auto& n : g.nodes) {
+            out += std::to_string(n.id) + " " + circuit::kind_name(n.kind) + " " + std::to_string(n.lanes) + " " +
+                   (n.is_private ? "1" : "0");
+            for (auto o : n.operands) out += " " + std::to_string(o);
+            out += "\n";
+        }
+        out += "root " + std::to_string(g.root) + "\n";
+    });
+    if (rc) return 0;
+    if (buf && cap) std::strncpy(buf, out.c_str(), cap);
+    return out.size() + 1;
+}
+
+// oracle.cpp:25 — cleartext interpretation of the compiled graph.
+int reft_interpret(const char* ir_text, int n_inputs, const char* const* names, const uint32_t* const* vals,
+                   const uint64_t* lens, uint32_t* out, uint64_t cap, uint64_t* out_len) {
+    return guard([&] {
+        auto g = compile_text(ir_text);
+        auto r = oracle::interpret(g, make_inputs(n_inputs, names, vals, lens));
+        *out_len = r.size();
+        std::memcpy(out, r.data(), std::min<uint64_t>(cap, r.size()) * 4);
+    });
+}
+
+// runtime.cpp:586-613 — full n-party online phase over the simulated transport.
+// report: [setup_ms, online_ms, bytes_sent(p0), scalar_triples(p0), matrix_triples(p0), digest(p0) as double bits]
+int reft_run_local(const char* ir_text, int n_parties, int threads, uint64_t slice, uint64_t dealer_seed,
+                   uint64_t io_timeout_ms, int n_inputs, const char* const* names, const uint32_t* const* vals,
+                   const uint64_t* lens, uint32_t* out, uint64_t cap, uint64_t* out_len, double* report,
+                   uint64_t* digest) {
+    return guard([&] {
+        auto g = compile_text(ir_text);
+        runtime::RunOptions opts;
+        opts.threads = threads;
+        opts.slice = slice;
+        auto inputs = make_inputs(n_inputs, names, vals, lens);
+        std::vector<runtime::RunReport> reps;
+        if (io_timeout_ms == 0) {
+            reps = runtime::run_local(g, n_parties, inputs, opts, dealer_seed);
+        } else {
+            // run_local with a raised io_timeout: same steps as
+            // runtime.cpp:586-613 but sessions get a longer deadline.
+            const uint64_t loop_iters_hint = 64;
+            auto demand = preproc::compute_triple_demand(g, opts.slice, loop_iters_hint);
+            spdz::Dealer dealer(n_parties, dealer_seed);
+            auto stores = spdz::make_dealer_stores(dealer, demand.scalars, demand.matrix_shapes,
+                                                   demand.input_masks, loop_iters_hint);
+            auto sessions = net::make_sim_sessions(n_parties);
+            for (auto& s : sessions) s->io_timeout = std::chrono::milliseconds(io_timeout_ms);
+            reps.resize(n_parties);
+            std::vector<std::exception_ptr> errors(n_parties);
+            std::vector<std::thread> th;
+            for (int i = 0; i < n_parties; ++i)
+                th.emplace_back([&, i] {
+                    try {
+                        runtime::PartyRuntime rt(g, stores[i], sessions[i], opts);
+                        reps[i] = rt.run(inputs);
+                    } catch (...) {
+                        errors[i] = std::current_exception();
+                    }
+                });
+            for (auto& t : th) t.join();
+            for (auto& e : errors)
+                if (e) std::rethrow_exception(e);
+        }
+        double online = 0, setup = 0;
+        for (auto& r : reps) {
+            online = std::max(online, r.online_ms);
+            setup = std::max(setup, r.setup_ms);
+        }
+        auto& r0 = reps.at(0);
+        *out_len = r0.outputs.size();
+        std::memcpy(out, r0.outputs.data(), std::min<uint64_t>(cap, r0.outputs.size()) * 4);
+        report[0] = setup;
+        report[1] = online;
+        report[2] = double(r0.bytes_sent);
+        report[3] = double(r0.scalar_triples_consumed);
+        report[4] = double(r0.matrix_triples_consumed);
+        *digest = r0.output_digest;
+    });
+}
+
+// Kernel-level CPU timing (pattern of benchmarks/kernel_bench.cpp:33-58):
+// best-of-`reps` wall time of CpuBackend::mul_mask + mul_combine on `lanes`.
+double reft_time_beaver_kernels(uint64_t lanes, int reps) {
+    spdz::Dealer d(2, 1);
+    std::vector<uint32_t> xs(lanes), ys(lanes);
+    reft_rand_field_vec(lanes, 1, xs.data());
+    reft_rand_field_vec(lanes, 2, ys.data());
+    auto X = d.share(xs), Y = d.share(ys);
+    auto T = d.triples(lanes);
+    auto be = backend::make_cpu_backend();
+    double best = 1e30;
+    for (int r = 0; r < reps; ++r) {
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<uint32_t> dd, ee;
+        be->mul_mask(X[0], Y[0], T[0], dd, ee);
+        auto z = be->mul_combine(T[0], dd, ee, 0, d.alpha_share(0));
+        double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (z.vals.size() != lanes) return -1;
+        best = std::min(best, ms);
+    }
+    return best;
+}
+
+}  // extern "C"
