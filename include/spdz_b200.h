@@ -1,0 +1,332 @@
+/*
+ * spdz_b200.h — C ABI of the B200-native SPDZ online-phase back end.
+ *
+ * This is the drop-in boundary for the reference's back-end plugin
+ * `mpc::backend::Backend` (/root/reference/proj/core/include/mpc/backend.hpp:32-49),
+ * widened (SURVEY.md §8b "gaps to close") to the other online-phase ops that
+ * bypass `Backend` in the reference: public-constant ops (spdz.hpp:131-141),
+ * open/reveal (net.hpp:77-81 / net.cpp:61-111), the MAC check
+ * (spdz.hpp:168-176, runtime.cpp:467-506) and the linear layer
+ * (linear.hpp:248-265, runtime.cpp:283-358).
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types cross this boundary.
+ *  - Field F_p, p = 2^32 - 5 (field.hpp:10).  Elements are uint32 in [0, p).
+ *  - Share vectors are structure-of-arrays: one value plane + one MAC plane
+ *    (spdz.hpp:19-28).  `spdz_share_t` points at DEVICE memory.
+ *  - Device entry points are asynchronous on the context's CUDA stream and
+ *    never allocate on the hot path; caller owns every buffer.
+ *  - `spdz_host_*` entry points take HOST buffers (the exact call shape of the
+ *    reference's `Backend` virtuals) and copy in/out inside the call.
+ *  - Every function returns an `spdz_status` (0 = OK).  `spdz_last_error()`
+ *    returns the thread-local message; codes map 1:1 onto the reference's
+ *    exception types (listed per code).
+ *  - A context is owned by one party; distinct contexts may be driven from
+ *    distinct threads concurrently (kernels are pure).
+ */
+#ifndef SPDZ_B200_H
+#define SPDZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPDZ_PRIME 4294967291u /* field.hpp:10 */
+#define SPDZ_MAX_PARTIES 8
+
+typedef enum spdz_status {
+    SPDZ_OK = 0,
+    SPDZ_ERR_LANE_MISMATCH = 1,          /* backend::LaneMismatch        backend.hpp:11 */
+    SPDZ_ERR_TRIPLE_SHORTAGE = 2,        /* backend::TripleShortage      backend.hpp:14 */
+    SPDZ_ERR_BACKEND_UNAVAILABLE = 3,    /* backend::BackendUnavailable  backend.hpp:17 */
+    SPDZ_ERR_TRIPLE_EXHAUSTED = 4,       /* spdz::TripleExhausted        triple_store.hpp:14 */
+    SPDZ_ERR_TRIPLE_SHAPE_MISMATCH = 5,  /* spdz::TripleShapeMismatch    triple_store.hpp:17 */
+    SPDZ_ERR_MASK_EXHAUSTED = 6,         /* spdz::MaskExhausted          triple_store.hpp:20 */
+    SPDZ_ERR_PEER_TIMEOUT = 7,           /* net::PeerTimeout             net.hpp:25 */
+    SPDZ_ERR_LANE_COUNT_MISMATCH = 8,    /* net::LaneCountMismatch       net.hpp:31 */
+    SPDZ_ERR_MALFORMED_SHARE_MESSAGE = 9,/* net::MalformedShareMessage   net.hpp:34 */
+    SPDZ_ERR_MAC_CHECK_FAILED = 10,      /* spdz::MacCheckFailed         spdz.hpp:12 */
+    SPDZ_ERR_SLICE_TOO_SMALL = 11,       /* linear::SliceTooSmall        linear.hpp:10 */
+    SPDZ_ERR_INVALID_ARGUMENT = 20,
+    SPDZ_ERR_CUDA = 21,
+    SPDZ_ERR_DEALER_REJECTION = 22,      /* GPU dealer hit the 25/2^64 rejection branch */
+} spdz_status;
+
+/* One party's authenticated share of a lane vector (spdz.hpp:19-28), device memory. */
+typedef struct spdz_share {
+    uint32_t* vals;
+    uint32_t* macs;
+    uint64_t lanes;
+} spdz_share_t;
+
+/* Beaver triple shares (spdz.hpp:31-33). */
+typedef struct spdz_triple {
+    spdz_share_t a, b, c;
+} spdz_triple_t;
+
+/* Matrix triple for one linear-layer tile (spdz.hpp:35-43): A rows x din
+ * (row-major), B din, C rows. */
+typedef struct spdz_mtriple {
+    uint32_t din, rows;
+    spdz_share_t a, b, c;
+} spdz_mtriple_t;
+
+/* Backend capability record (backend.hpp:21-27). */
+typedef struct spdz_capability {
+    char name[32];
+    uint64_t min_kernel_size; /* 1: the GPU back end takes every request (no CPU fallback) */
+    uint32_t threads_per_block;
+    int32_t executable;
+    int32_t sm_count;
+    int32_t device;
+} spdz_capability_t;
+
+/* One contiguous run of opened records for the MAC check.  Record i of the
+ * segment is (opened x = value[i], mac share m = mac_a[i] - mac_b[i] (mac_b may
+ * be NULL), global rank j = j0 + i).  The rank is the record's position in
+ * (batch_id, lane) order over the whole run (spdz.cpp:127-129); the host
+ * assigns j0 by sorting segments by batch id (spdz_mac_assign_ranks). */
+typedef struct spdz_mac_segment {
+    const uint32_t* value;
+    const uint32_t* mac_a;
+    const uint32_t* mac_b;
+    uint64_t len;
+    uint64_t j0;       /* global rank of record 0 (filled by spdz_mac_assign_ranks) */
+    uint64_t batch_id; /* wire batch id of the opening (runtime.cpp:22-24) */
+    uint64_t lane0;    /* lane of record 0 inside its batch (log_open lane, runtime.cpp:115-116) */
+} spdz_mac_segment_t;
+
+typedef struct spdz_ctx spdz_ctx;
+
+/* ---------------- library / context ---------------- */
+const char* spdz_last_error(void);
+const char* spdz_version(void);
+/* Creates a party context on `device` (cudaSetDevice'd on every entry). */
+int spdz_ctx_create(int device, int party, int n_parties, uint32_t alpha_share, spdz_ctx** out);
+int spdz_ctx_destroy(spdz_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t passed as void*); NULL restores the owned stream. */
+int spdz_ctx_set_stream(spdz_ctx* ctx, void* stream);
+void* spdz_ctx_stream(spdz_ctx* ctx);
+int spdz_ctx_party(const spdz_ctx* ctx);
+int spdz_ctx_sync(spdz_ctx* ctx);
+/* backend.hpp:35 */
+int spdz_capability(const spdz_ctx* ctx, spdz_capability_t* out);
+/* Number of kernels this library launched on any context since load (evidence counter). */
+uint64_t spdz_kernel_launches(void);
+
+/* ---------------- Backend: batched share ops (device) ---------------- */
+/* backend.hpp:37 / backend.cpp:25-37: z = x + y on both planes */
+int spdz_add_batch(spdz_ctx* ctx, const spdz_share_t* x, const spdz_share_t* y, spdz_share_t* z);
+/* backend.hpp:38 / backend.cpp:39-51 */
+int spdz_sub_batch(spdz_ctx* ctx, const spdz_share_t* x, const spdz_share_t* y, spdz_share_t* z);
+/* backend.hpp:39-42 / backend.cpp:53-65: d = x.v - a.v, e = y.v - b.v (value planes only) */
+int spdz_mul_mask(spdz_ctx* ctx, const spdz_share_t* x, const spdz_share_t* y, const spdz_triple_t* t,
+                  uint32_t* d_out, uint32_t* e_out);
+/* backend.hpp:43-46 / spdz.cpp:77-96 with already-opened d, e */
+int spdz_mul_combine(spdz_ctx* ctx, const spdz_triple_t* t, const uint32_t* d, const uint32_t* e,
+                     spdz_share_t* z);
+/* backend.hpp:47-48 / backend.cpp:76-84: z (1 lane) = sum of lanes, both planes */
+int spdz_reduce_add(spdz_ctx* ctx, const spdz_share_t* x, spdz_share_t* z);
+
+/* ---------------- public-constant ops (spdz.cpp:35-75), in place ----------------
+ * `k` is a device vector of x->lanes elements, or of 1 element broadcast over
+ * the lanes (runtime.cpp:36-39). */
+int spdz_add_public(spdz_ctx* ctx, spdz_share_t* x, const uint32_t* k, uint64_t k_len);
+int spdz_sub_public(spdz_ctx* ctx, spdz_share_t* x, const uint32_t* k, uint64_t k_len);
+int spdz_rsub_public(spdz_ctx* ctx, spdz_share_t* x, const uint32_t* k, uint64_t k_len);
+int spdz_mul_public(spdz_ctx* ctx, spdz_share_t* x, const uint32_t* k, uint64_t k_len);
+int spdz_mul_public_scalar(spdz_ctx* ctx, spdz_share_t* x, uint32_t k);
+/* spdz.cpp:70-75: out = trivial sharing of public k (out->lanes lanes) */
+int spdz_share_of_public(spdz_ctx* ctx, const uint32_t* k, uint64_t k_len, spdz_share_t* out);
+
+/* ---------------- open / reveal (net.cpp:61-111, absorb 170-215) ----------------
+ * out[i] = own[i] + sum_p reduce(peers[p][i]) mod p.  Peer pointers may be on
+ * this device, on a peer device (P2P over NVLink) or IPC-mapped. */
+int spdz_open_sum(spdz_ctx* ctx, const uint32_t* own, const uint32_t* const* peers, int n_peers, uint64_t len,
+                  uint32_t* out);
+
+/* Fused Beaver open + combine: opened [d|e] = own_de + sum reduce(peer_de), then
+ * z = beaver_combine(t, d, e) (spdz.cpp:77-96).  `own_de`/`peer_de[p]` are the
+ * [d | e] payloads (2*lanes words, runtime.cpp:215-217).  If `opened_out` is not
+ * NULL the opened [d|e] is written there (the MAC log, runtime.cpp:224). */
+int spdz_beaver_open_combine(spdz_ctx* ctx, const spdz_triple_t* t, const uint32_t* own_de,
+                             const uint32_t* const* peer_de, int n_peers, spdz_share_t* z,
+                             uint32_t* opened_out);
+
+/* ---------------- MAC check (spdz.cpp:126-158, runtime.cpp:467-506) ---------------- */
+/* Assigns j0 to each segment: j0 = (records of all smaller batch ids) + lane0
+ * (host only). */
+int spdz_mac_assign_ranks(spdz_mac_segment_t* segs, uint64_t n_segs);
+/* sigma_i = sum_j r_j (m_ij - alpha_i x_j) mod p over the segments (device
+ * arrays referenced by host-side descriptors); blocks until the result is on the host. */
+int spdz_mac_sigma(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n_segs, uint64_t coin,
+                   uint32_t* sigma_out);
+/* spdz.hpp:168 record form: records in any order (device SoA arrays); ranks are
+ * assigned by sorting (batch_id, lane) on the host (compat path). */
+int spdz_mac_sigma_records(spdz_ctx* ctx, const uint64_t* host_batch, const uint32_t* host_lane,
+                           const uint32_t* dev_value, const uint32_t* dev_mac, uint64_t n, uint64_t coin,
+                           uint32_t* sigma_out);
+/* spdz.cpp:140-145 */
+uint64_t spdz_commit_sigma(uint32_t sigma, uint64_t nonce);
+/* spdz.cpp:147-158: SPDZ_OK or SPDZ_ERR_MAC_CHECK_FAILED */
+int spdz_verify_sigmas(const uint32_t* sigmas, const uint64_t* nonces, const uint64_t* commitments, uint64_t n);
+/* hash.hpp:11-19 */
+uint64_t spdz_fnv1a64(const void* data, uint64_t len, uint64_t seed);
+
+/* ---------------- linear layer ---------------- */
+/* linear.cpp:7-21.  Fills starts/counts (capacity `cap`), returns the tile
+ * count via *n_tiles; SPDZ_ERR_SLICE_TOO_SMALL like the reference. */
+int spdz_plan_tiles(uint32_t din, uint32_t dout, uint64_t slice, uint32_t* starts, uint32_t* counts, uint64_t cap,
+                    uint64_t* n_tiles);
+/* linear.cpp:30-49 value plane: payload = [D = W_tile.v - A.v (rows*din) | E = x.v - B.v (din)] */
+int spdz_matrix_mask(spdz_ctx* ctx, const spdz_share_t* w_tile, const spdz_share_t* x, const spdz_mtriple_t* mt,
+                     uint32_t* payload);
+/* linear.cpp:51-61 + spdz.cpp:98-124 fused with the open: opened [D|E] = own +
+ * sum reduce(peer); z = matrix_combine(mt, D, E) + b_slice.  b_slice may be NULL.
+ * opened_out (rows*din + din words) may be NULL. */
+int spdz_matrix_open_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t* own_payload,
+                             const uint32_t* const* peer_payload, int n_peers, const spdz_share_t* b_slice,
+                             spdz_share_t* z, uint32_t* opened_out);
+/* spdz.cpp:98-124 with already-opened D (rows*din) and E (din). */
+int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t* D, const uint32_t* E,
+                        spdz_share_t* z);
+/* runtime.cpp:303-334, batched: Y[dout x batch] = W[dout x din] * X[din x batch]
+ * on both planes.  w_public != 0: W public (w_vals), X secret (x->vals/x->macs,
+ * row-major din x batch).  w_public == 0: W secret (w->vals/w->macs), X public
+ * (x_pub).  Y row-major dout x batch.  Bias is a separate spdz_add_batch. */
+int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32_t batch, int w_public,
+                              const uint32_t* w_vals, const spdz_share_t* w_secret, const spdz_share_t* x_secret,
+                              const uint32_t* x_pub, spdz_share_t* y);
+
+/* ---------------- preprocessing: GPU fake dealer (spdz.cpp:162-249) ----------------
+ * The dealer is a splitmix64 stream; draw k (0-based after construction) is
+ * mix(seed + (k+1)*gamma), so every share is computed independently.  `draw0`
+ * is the stream position to start at (n after construction).  Outputs are the
+ * share planes of ALL parties, party-major (n * lanes).  Returns
+ * SPDZ_ERR_DEALER_REJECTION if any draw hit the rejection branch. */
+int spdz_dealer_alpha(int n_parties, uint64_t seed, uint32_t* alpha_shares_out, uint32_t* alpha_out);
+int spdz_dealer_triples(spdz_ctx* ctx, int n_parties, uint64_t seed, uint64_t draw0, uint64_t lanes,
+                        uint32_t* const planes[6]);
+int spdz_dealer_share(spdz_ctx* ctx, int n_parties, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                      const uint32_t* clear, uint64_t lanes, uint32_t* vals_out, uint32_t* macs_out);
+int spdz_dealer_matrix_triple(spdz_ctx* ctx, int n_parties, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                              uint32_t din, uint32_t rows, uint32_t* const planes[6], uint32_t* scratch);
+int spdz_dealer_masks(spdz_ctx* ctx, int n_parties, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count,
+                      uint32_t* vals_out, uint32_t* macs_out, uint32_t* clear_out);
+/* Number of draws each call consumes (to advance draw0). */
+uint64_t spdz_dealer_draws_triples(int n_parties, uint64_t lanes);
+uint64_t spdz_dealer_draws_share(int n_parties, uint64_t lanes);
+uint64_t spdz_dealer_draws_matrix(int n_parties, uint32_t din, uint32_t rows);
+uint64_t spdz_dealer_draws_masks(int n_parties, uint64_t count);
+
+/* ---------------- host-buffer Backend (the reference's call shape) ----------------
+ * Same semantics as CpuBackend (backend.cpp:16-88) with host vectors; the
+ * copies happen inside the call.  `t_lanes` is the triple count the request
+ * carries (TripleShortage when != lanes, backend.cpp:56-58). */
+int spdz_host_add_batch(spdz_ctx* ctx, const uint32_t* xv, const uint32_t* xm, uint64_t x_lanes, const uint32_t* yv,
+                        const uint32_t* ym, uint64_t y_lanes, uint32_t* zv, uint32_t* zm);
+int spdz_host_sub_batch(spdz_ctx* ctx, const uint32_t* xv, const uint32_t* xm, uint64_t x_lanes, const uint32_t* yv,
+                        const uint32_t* ym, uint64_t y_lanes, uint32_t* zv, uint32_t* zm);
+int spdz_host_mul_mask(spdz_ctx* ctx, const uint32_t* xv, const uint32_t* yv, uint64_t lanes,
+                       const uint32_t* const tri[6], uint64_t t_lanes, uint32_t* d_out, uint32_t* e_out);
+int spdz_host_mul_combine(spdz_ctx* ctx, const uint32_t* const tri[6], uint64_t t_lanes, const uint32_t* d,
+                          const uint32_t* e, uint64_t lanes, int party, uint32_t alpha_share, uint32_t* zv,
+                          uint32_t* zm);
+int spdz_host_reduce_add(spdz_ctx* ctx, const uint32_t* xv, const uint32_t* xm, uint64_t lanes, uint32_t* zv,
+                         uint32_t* zm);
+
+/* ---------------- local n-party online phase (runtime.cpp:508-613 shape) ----------------
+ * A straight-line circuit executed by n parties, each party on its own CUDA
+ * stream (and optionally its own device).  The opening exchange is the peer
+ * payload read fused into the combine kernels; per-party streams and events
+ * replace the reference's batch-id matching (net.cpp:61-95). */
+typedef enum spdz_node_kind {
+    SPDZ_NODE_INPUT = 0,   /* operand-free; bound by spdz_run_bind_input */
+    SPDZ_NODE_CONST = 1,   /* public constant (cvals) */
+    SPDZ_NODE_ADD = 2,     /* AddBatch/Adder      runtime.cpp:364-367 */
+    SPDZ_NODE_SUB = 3,     /* SubBatch/Subtract   runtime.cpp:368-371 */
+    SPDZ_NODE_MUL = 4,     /* MultBatch/Multiplier runtime.cpp:372-382 */
+    SPDZ_NODE_REDUCE_ADD = 5, /* runtime.cpp:383-396 */
+    SPDZ_NODE_REDUCE_MUL = 6, /* runtime.cpp:397-410 */
+    SPDZ_NODE_LINEAR = 7,  /* runtime.cpp:439-441, operands x, W, b */
+    SPDZ_NODE_ROOT = 8,    /* runtime.cpp:442-444 */
+    SPDZ_NODE_LOAD = 9,    /* runtime.cpp:419-438: operands (base, start const) -> lane slice view */
+    SPDZ_NODE_NOP = 10,    /* BlockLabel and other control nodes of a straight-line graph */
+} spdz_node_kind;
+
+typedef struct spdz_node {
+    int32_t kind;
+    int32_t is_private;   /* privacy tag (graph_builder.cpp:495) */
+    uint32_t lanes;       /* lane count of the node's value */
+    uint32_t n_operands;
+    uint32_t operands[3]; /* node ids (ids are the index in the node array) */
+    uint32_t din, dout;   /* LINEAR only */
+    uint32_t const_val;   /* CONST only (scalar broadcast) */
+} spdz_node_t;
+
+typedef struct spdz_run_options {
+    uint64_t slice;        /* RunOptions.slice (runtime.hpp:12), default 262140 */
+    uint64_t dealer_seed;  /* run_local dealer seed (runtime.hpp:54), default 1 */
+    int32_t fixed_coin;    /* 1: use `coin` instead of the commit-reveal nonces (tests) */
+    uint64_t coin;
+    int32_t use_graph;     /* reserved (CUDA-graph capture of the online phase) */
+    int32_t devices[SPDZ_MAX_PARTIES]; /* device of each party (-1: device 0) */
+    int32_t profile_kernels; /* 1: CUDA-event time every mask / combine / sigma launch */
+} spdz_run_options_t;
+
+/* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
+ * (SURVEY.md §8d contracts). */
+typedef struct spdz_kernel_stat {
+    uint64_t launches;
+    double ms;
+    uint64_t bytes;
+} spdz_kernel_stat_t;
+
+enum { SPDZ_KSTAT_MASK = 0, SPDZ_KSTAT_COMBINE = 1, SPDZ_KSTAT_SIGMA = 2, SPDZ_KSTAT_OPEN = 3, SPDZ_KSTAT_N = 4 };
+
+typedef struct spdz_run_report {
+    double setup_ms, online_ms;       /* host wall clock, as RunReport (runtime.hpp:20-31) */
+    double online_device_ms;          /* CUDA-event time of the online phase (max over parties) */
+    uint64_t scalar_triples_consumed, matrix_triples_consumed;
+    uint64_t bytes_exchanged;         /* payload bytes read from peers */
+    uint64_t output_digest;           /* fnv1a64 of the opened outputs (runtime.cpp:573) */
+    uint64_t kernel_launches;
+    uint32_t sigmas[SPDZ_MAX_PARTIES];
+    uint64_t coin;
+    spdz_kernel_stat_t kstat[SPDZ_KSTAT_N]; /* filled when profile_kernels = 1 */
+} spdz_run_report_t;
+
+typedef struct spdz_run spdz_run;
+
+/* Builds the run: computes the triple layout (preproc.cpp:124-163), runs the
+ * GPU dealer for every party (make_dealer_stores order, triple_store.cpp:248-287)
+ * and allocates every device buffer of the online phase. */
+int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
+                    const spdz_run_options_t* opts, spdz_run** out);
+int spdz_run_destroy(spdz_run* run);
+/* Re-runs the GPU dealer with `seed` (fresh preprocessing; inputs must be shared again). */
+int spdz_run_deal(spdz_run* run, uint64_t seed);
+/* Cleartext input for an INPUT node (host pointer).  Private inputs are shared
+ * with the dealer's input masks (preproc.cpp:205-243) during spdz_run_share_inputs. */
+int spdz_run_bind_input(spdz_run* run, uint32_t node, const uint32_t* host_vals, uint64_t len);
+/* Input sharing (setup, excluded from online time as in runtime.cpp:511-534). */
+int spdz_run_share_inputs(spdz_run* run);
+/* Online phase: node execution, root open, deferred MAC check.  Re-runnable
+ * (triple consumption is reset per call only when `reuse_preprocessing` = 1 —
+ * the bench re-times the same preprocessing; the reference semantics are 0). */
+int spdz_run_online(spdz_run* run, int reuse_preprocessing, spdz_run_report_t* report);
+/* Opened outputs (host).  *len receives the lane count. */
+int spdz_run_outputs(spdz_run* run, uint32_t* host_out, uint64_t cap, uint64_t* len);
+/* Device view of a node's share for party p (tests). */
+int spdz_run_node_share(spdz_run* run, int party, uint32_t node, spdz_share_t* out);
+/* Test hook: flip `bit` of the payload word `word` that party `receiver`
+ * reads from `sender` for node `node` (SimHub BitFlip, net.cpp:241-278). */
+int spdz_run_inject_bitflip(spdz_run* run, uint32_t node, int sender, int receiver, uint64_t word, uint32_t bit);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPDZ_B200_H */

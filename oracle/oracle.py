@@ -323,3 +323,63 @@ def np_add(a, b):
 
 def np_sub(a, b):
     return ((np.asarray(a, np.uint64) + P - np.asarray(b, np.uint64)) % P).astype(np.uint32)
+
+
+def sim_chain(kind: str, n: int, xs, ys, dealer_seed: int = 1, coin: int = 0):
+    """Share-level n-party simulation of the chain workloads through the
+    reference's run_local steps (runtime.cpp:508-577): dealer stores
+    (make_dealer_stores order), mask-based input sharing (preproc.cpp:205-243),
+    Beaver multiplies with per-node triple regions (preproc.cpp:124-163), root
+    open and the MAC sigma of every party for `coin` (spdz.cpp:126-138).
+    Node ids follow the reference graph: t1..t4 = 6..9, root = 10."""
+    ops = {"light": "++-+", "mixed": "*+*+", "heavy": "****"}[kind]
+    L = len(xs)
+    n_mul = ops.count("*")
+    st = dealer_stores(n, dealer_seed, n_mul * L, (), 2 * L)
+    al = st["alpha_shares"]
+    mv, mm, mc = st["masks"]
+    S = st["scalars"]  # (6, n, n_mul*L)
+
+    def share_input(vals, off):
+        diff = np_sub(np.asarray(vals, np.uint64) % P, mc[off:off + L])
+        out = []
+        for p in range(n):
+            out.append(public_op("add_public", mv[p, off:off + L], mm[p, off:off + L], diff, p, al[p]))
+        return out
+
+    X = share_input(xs, 0)
+    Y = share_input(ys, L)
+    logs = [[] for _ in range(n)]
+    vals = {4: X, 5: Y}
+    mul_i = 0
+    operands = [(4, 5), (6, 4), (7, 5), (8, 6)]
+    for k, (o0, o1) in enumerate(operands):
+        nid = 6 + k
+        A, B = vals[o0], vals[o1]
+        op = ops[k]
+        if op == "*":
+            base = mul_i * L
+            mul_i += 1
+            tri = [S[:, p, base:base + L] for p in range(n)]
+            ds, es = [], []
+            for p in range(n):
+                d, e = mul_mask(A[p][0], B[p][0], tri[p][0], tri[p][2])
+                ds.append(d)
+                es.append(e)
+            dop = open_sum(ds[0], ds[1:])
+            eop = open_sum(es[0], es[1:])
+            out = []
+            for p in range(n):
+                out.append(beaver_combine(tri[p], dop, eop, p, al[p]))
+                batch = make_batch(nid, 0, 0)
+                logs[p].append((batch, np.concatenate([dop, eop]),
+                                np.concatenate([np_sub(A[p][1], tri[p][1]), np_sub(B[p][1], tri[p][3])])))
+            vals[nid] = out
+        else:
+            vals[nid] = [add_batch(A[p][0], A[p][1], B[p][0], B[p][1], sub=(op == "-")) for p in range(n)]
+    R = vals[9]
+    outputs = open_sum(R[0][0], [R[p][0] for p in range(1, n)])
+    for p in range(n):
+        logs[p].append((make_batch(10, 1, 1), outputs, R[p][1]))
+    sigmas = [mac_sigma_segments(logs[p], coin, al[p]) for p in range(n)]
+    return dict(outputs=outputs, sigmas=sigmas, nodes=vals, alpha=st["alpha"], alpha_shares=al)

@@ -14,17 +14,19 @@ CHAINS = {
     "heavy": ("mul", "mul", "mul", "mul"),
 }
 
-_HDR = '@.str = private unnamed_addr constant [8 x i8] c"private\\00", align 1\n\n'
+_HDR = ('@.str = private unnamed_addr constant [8 x i8] c"private\\00", align 1\n'
+        '@.pub = private unnamed_addr constant [7 x i8] c"public\\00", align 1\n\n')
 _DECL = "declare void @llvm.var.annotation(ptr, ptr, ptr, i32, ptr)\n"
+
+
+def _ann(name: str, private: bool) -> str:
+    tag = "@.str" if private else "@.pub"
+    return f"  call void @llvm.var.annotation(ptr %{name}, ptr {tag}, ptr null, i32 0, ptr null)\n"
 
 
 def chain_ir(kind: str, n: int, x_private: bool = True, y_private: bool = True) -> str:
     ops = CHAINS[kind]
-    ann = ""
-    if x_private:
-        ann += "  call void @llvm.var.annotation(ptr %x, ptr @.str, ptr null, i32 0, ptr null)\n"
-    if y_private:
-        ann += "  call void @llvm.var.annotation(ptr %y, ptr @.str, ptr null, i32 0, ptr null)\n"
+    ann = _ann("x", x_private) + _ann("y", y_private)
     t = f"<{n} x i32>"
     body = (f"  %a = load {t}, ptr %x\n"
             f"  %b = load {t}, ptr %y\n"
@@ -38,10 +40,7 @@ def chain_ir(kind: str, n: int, x_private: bool = True, y_private: bool = True) 
 
 def linear_ir(din: int, dout: int, x_private=True, w_private=True, b_private=True) -> str:
     """tests/test_util.hpp:54-67 with per-operand privacy."""
-    ann = ""
-    for name, priv in (("x", x_private), ("W", w_private), ("b", b_private)):
-        if priv:
-            ann += f"  call void @llvm.var.annotation(ptr %{name}, ptr @.str, ptr null, i32 0, ptr null)\n"
+    ann = _ann("x", x_private) + _ann("W", w_private) + _ann("b", b_private)
     return (_HDR + "define ptr @main(ptr %x, ptr %W, ptr %b) {\nentry:\n" + ann +
             f"  %y = call ptr @mark_linear_layer(ptr %x, ptr %W, ptr %b, i32 {din}, i32 {dout})\n"
             "  ret ptr %y\n}\n")

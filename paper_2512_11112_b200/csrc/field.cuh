@@ -1,0 +1,97 @@
+// F_p arithmetic for p = 2^32 - 5 (reference: proj/core/include/mpc/field.hpp:10-46)
+// and the splitmix64 finaliser (proj/core/include/mpc/hash.hpp:21-26), as
+// device inline functions.
+//
+// Reduction: p is a pseudo-Mersenne prime, 2^32 == 5 (mod p), so a 64-bit
+// value v = hi*2^32 + lo folds to 5*hi + lo.  Two folds and one conditional
+// subtract give v mod p for every u64 (proof in DESIGN.md §3).  A Barrett
+// variant is kept for the ncu comparison the north star asks for
+// (`-DSPDZ_REDUCE_BARRETT`); every variant is bit-exact with `v % p`.
+#pragma once
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace spdzb200 {
+
+constexpr uint32_t kP = 4294967291u;
+constexpr uint64_t kP64 = 4294967291ull;
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+// t < 6 * 2^32 after one fold of any u64
+__host__ __device__ __forceinline__ uint64_t fold1(uint64_t v) {
+    return (v & 0xffffffffull) + 5ull * (v >> 32);
+}
+
+#if defined(SPDZ_REDUCE_BARRETT)
+// Barrett with mu = floor(2^64 / p): q = hi64(v * mu), r = v - q*p in [0, 2p).
+__host__ __device__ __forceinline__ uint32_t fp_reduce64(uint64_t v) {
+    constexpr uint64_t mu = 4294967301ull;  // floor(2^64 / (2^32 - 5)) = 2^32 + 5 (+0, remainder 25)
+#ifdef __CUDA_ARCH__
+    uint64_t q = __umul64hi(v, mu);
+#else
+    uint64_t q = (uint64_t)(((unsigned __int128)v * mu) >> 64);
+#endif
+    uint64_t r = v - q * kP64;
+    while (r >= kP64) r -= kP64;
+    return (uint32_t)r;
+}
+#else
+// v mod p for any u64: fold, fold, conditional subtract.
+__host__ __device__ __forceinline__ uint32_t fp_reduce64(uint64_t v) {
+    uint64_t t = fold1(v);     // < 6 * 2^32
+    t = fold1(t);              // < 2^32 + 25 < 2p
+    return (uint32_t)(t >= kP64 ? t - kP64 : t);
+}
+#endif
+
+// field.hpp:14 reduce() of a u32 (payload words from peers may be >= p)
+__host__ __device__ __forceinline__ uint32_t fp_reduce32(uint32_t v) { return v >= kP ? v - kP : v; }
+
+// field.hpp:16-20
+__host__ __device__ __forceinline__ uint32_t fp_add(uint32_t a, uint32_t b) {
+    uint32_t r = a + b;
+    // a, b < p: a + b < 2p; carry out of 32 bits implies >= p.
+    if (r < a || r >= kP) r -= kP;
+    return r;
+}
+
+// field.hpp:22-24
+__host__ __device__ __forceinline__ uint32_t fp_sub(uint32_t a, uint32_t b) {
+    uint32_t r = a - b;
+    if (a < b) r += kP;
+    return r;
+}
+
+// field.hpp:26
+__host__ __device__ __forceinline__ uint32_t fp_neg(uint32_t a) { return a == 0 ? 0u : kP - a; }
+
+__host__ __device__ __forceinline__ uint64_t mul_wide(uint32_t a, uint32_t b) { return (uint64_t)a * b; }
+
+// field.hpp:28-30
+__host__ __device__ __forceinline__ uint32_t fp_mul(uint32_t a, uint32_t b) { return fp_reduce64(mul_wide(a, b)); }
+
+// Lazy accumulation: acc += a*b folded once (< 6*2^32 per term), so 2^29 terms
+// fit in a u64 before a final fp_reduce64.
+__host__ __device__ __forceinline__ uint64_t mac_lazy(uint64_t acc, uint32_t a, uint32_t b) {
+    return acc + fold1(mul_wide(a, b));
+}
+
+// hash.hpp:21-26 finaliser; splitmix64(state) = mix64(state += gamma)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// MAC-check coefficient of global record rank j (spdz.cpp:131-135):
+// r_j = reduce(splitmix64 stream from coin, draw j) = reduce(mix(coin + (j+1) gamma)).
+__host__ __device__ __forceinline__ uint32_t mac_coeff(uint64_t coin, uint64_t j) {
+    return fp_reduce64(mix64(coin + (j + 1) * kGamma));
+}
+
+}  // namespace spdzb200

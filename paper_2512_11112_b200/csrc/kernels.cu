@@ -1,0 +1,912 @@
+// sm_100a kernels of the B200 SPDZ online-phase back end.
+//
+// All hot-path kernels here are HBM-bound integer streams over structure-of-
+// arrays share planes: 128-bit vector loads/stores when every
+// plane of a call is 16-byte aligned (scalar, still coalesced, otherwise), a
+// grid of (148 SMs x 8) 256-thread CTAs striding over the lanes, and modular
+// arithmetic by the pseudo-Mersenne fold of field.cuh.  The one dense
+// contraction (secret x public linear layer) is a CUDA-core modular GEMM.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "field.cuh"
+#include "kernels.cuh"
+
+namespace spdzb200 {
+
+unsigned long long g_kernel_launches = 0;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint4 ld4(const uint32_t* p, uint64_t g) {
+    return __ldcs(reinterpret_cast<const uint4*>(p) + g);
+}
+__device__ __forceinline__ uint4 ld4_peer(const uint32_t* p, uint64_t g) {
+    // peer payloads may live on another GPU (NVLink P2P / IPC): plain load
+    return reinterpret_cast<const uint4*>(p)[g];
+}
+__device__ __forceinline__ void st4(uint32_t* p, uint64_t g, const uint32_t (&v)[4]) {
+    reinterpret_cast<uint4*>(p)[g] = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int grid_for(uint64_t work, int sms, int per_sm = 8) {
+    uint64_t b = (work + kThreads - 1) / kThreads;
+    uint64_t cap = (uint64_t)sms * per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+inline cudaError_t launched() {
+    ++g_kernel_launches;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Generic lane-parallel map: NI input planes -> NO output planes, `op` applied
+// per lane.  Peer planes (NPI of the inputs, starting at PEER0) use plain loads.
+// ---------------------------------------------------------------------------
+template <int NI, int NO>
+struct IO {
+    const uint32_t* in[NI > 0 ? NI : 1];
+    uint32_t* out[NO];
+};
+
+template <int NI, int NO, class Op>
+__global__ void __launch_bounds__(kThreads) k_map(IO<NI, NO> io, uint64_t n, uint64_t n4, Op op) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint64_t g = t; g < n4; g += stride) {
+        uint32_t a[NI > 0 ? NI : 1][4];
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            uint4 v = Op::is_peer(k) ? ld4_peer(io.in[k], g) : ld4(io.in[k], g);
+            a[k][0] = v.x;
+            a[k][1] = v.y;
+            a[k][2] = v.z;
+            a[k][3] = v.w;
+        }
+        uint32_t o[NO][4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            uint32_t ai[NI > 0 ? NI : 1], oi[NO];
+#pragma unroll
+            for (int k = 0; k < NI; ++k) ai[k] = a[k][l];
+            op(ai, oi);
+#pragma unroll
+            for (int k = 0; k < NO; ++k) o[k][l] = oi[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NO; ++k) st4(io.out[k], g, o[k]);
+    }
+    for (uint64_t i = n4 * 4 + t; i < n; i += stride) {
+        uint32_t ai[NI > 0 ? NI : 1], oi[NO];
+#pragma unroll
+        for (int k = 0; k < NI; ++k) ai[k] = io.in[k][i];
+        op(ai, oi);
+#pragma unroll
+        for (int k = 0; k < NO; ++k) io.out[k][i] = oi[k];
+    }
+}
+
+template <int NI, int NO, class Op>
+cudaError_t run_map(cudaStream_t s, const IO<NI, NO>& io, uint64_t n, Op op, int sms) {
+    if (n == 0) return cudaSuccess;
+    bool al = true;
+    for (int k = 0; k < NI; ++k) al = al && aligned16(io.in[k]);
+    for (int k = 0; k < NO; ++k) al = al && aligned16(io.out[k]);
+    const uint64_t n4 = al ? n / 4 : 0;
+    const uint64_t work = n4 ? n4 : n;
+    k_map<NI, NO, Op><<<grid_for(work, sms), kThreads, 0, s>>>(io, n, n4, op);
+    return launched();
+}
+
+// ---- ops ----
+struct NoPeer {
+    __device__ static constexpr bool is_peer(int) { return false; }
+};
+
+struct OpAdd : NoPeer {  // backend.cpp:25-37
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        o[0] = fp_add(a[0], a[2]);
+        o[1] = fp_add(a[1], a[3]);
+    }
+};
+struct OpSub : NoPeer {  // backend.cpp:39-51
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        o[0] = fp_sub(a[0], a[2]);
+        o[1] = fp_sub(a[1], a[3]);
+    }
+};
+
+// spdz.cpp:35-75; inputs: xv, xm[, k].  KM: 0 vector k, 1 device scalar
+// broadcast (runtime.cpp:36-39), 2 immediate.
+template <int OPC, int KM>
+struct OpPublic : NoPeer {
+    int party;
+    uint32_t alpha;
+    uint32_t kk;
+    const uint32_t* kp;
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        const uint32_t k = KM == 0 ? a[2] : (KM == 1 ? __ldg(kp) : kk);
+        const uint32_t xv = a[0], xm = a[1];
+        if (OPC == 0) {  // add_public
+            o[0] = party == 0 ? fp_add(xv, k) : xv;
+            o[1] = fp_add(xm, fp_mul(alpha, k));
+        } else if (OPC == 1) {  // sub_public
+            o[0] = party == 0 ? fp_sub(xv, k) : xv;
+            o[1] = fp_sub(xm, fp_mul(alpha, k));
+        } else if (OPC == 2) {  // rsub_public
+            o[0] = party == 0 ? fp_sub(k, xv) : fp_neg(xv);
+            o[1] = fp_sub(fp_mul(alpha, k), xm);
+        } else {  // mul_public
+            o[0] = fp_mul(xv, k);
+            o[1] = fp_mul(xm, k);
+        }
+    }
+};
+// spdz.cpp:70-75 share_of_public; input: [k] (KM as OpPublic)
+template <int KM>
+struct OpShareOfPublic : NoPeer {
+    int party;
+    uint32_t alpha;
+    uint32_t kk;
+    const uint32_t* kp;
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        const uint32_t k = KM == 0 ? a[0] : (KM == 1 ? __ldg(kp) : kk);
+        o[0] = party == 0 ? k : 0u;
+        o[1] = fp_mul(alpha, k);
+    }
+};
+
+struct OpMask : NoPeer {  // backend.cpp:53-65: in xv yv av bv -> d e
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        o[0] = fp_sub(a[0], a[2]);
+        o[1] = fp_sub(a[1], a[3]);
+    }
+};
+
+// Fused open + Beaver combine.  Inputs: own_d, own_e, peer_d[NP], peer_e[NP],
+// a.v a.m b.v b.m c.v c.m.  Outputs: z.v z.m [open_d open_e].
+template <int NP, bool LOG>
+struct OpCombine {
+    int party;
+    uint32_t alpha;
+    __device__ static constexpr bool is_peer(int k) { return k >= 2 && k < 2 + 2 * NP; }
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        uint32_t d = in[0], e = in[1];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {  // net.cpp:188-189: acc = add(acc, reduce(peer))
+            d = fp_add(d, fp_reduce32(in[2 + p]));
+            e = fp_add(e, fp_reduce32(in[2 + NP + p]));
+        }
+        const uint32_t* t = in + 2 + 2 * NP;  // a.v a.m b.v b.m c.v c.m
+        // spdz.cpp:83-93, lazily reduced (exact mod p)
+        const uint32_t de = fp_mul(d, e);
+        uint64_t v = (uint64_t)t[4] + fold1(mul_wide(d, t[2])) + fold1(mul_wide(e, t[0]));
+        if (party == 0) v += de;
+        uint64_t m = (uint64_t)t[5] + fold1(mul_wide(d, t[3])) + fold1(mul_wide(e, t[1])) +
+                     fold1(mul_wide(alpha, de));
+        o[0] = fp_reduce64(v);
+        o[1] = fp_reduce64(m);
+        if (LOG) {
+            o[2] = d;
+            o[3] = e;
+        }
+    }
+};
+
+struct OpDiff : NoPeer {
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const { o[0] = fp_sub(a[0], a[1]); }
+};
+
+template <int NP>
+struct OpOpen {  // net.cpp:170-215
+    __device__ static constexpr bool is_peer(int k) { return k >= 1; }
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        uint32_t acc = in[0];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) acc = fp_add(acc, fp_reduce32(in[1 + p]));
+        o[0] = acc;
+    }
+};
+
+template <int NP>
+cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, const uint32_t* const* pd,
+                       const uint32_t* const* pe, const uint32_t* const tri[6], int party, uint32_t alpha,
+                       uint32_t* zv, uint32_t* zm, uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms) {
+    constexpr int NI = 8 + 2 * NP;
+    if (open_d) {
+        IO<NI, 4> io;
+        io.in[0] = od;
+        io.in[1] = oe;
+        for (int p = 0; p < NP; ++p) {
+            io.in[2 + p] = pd[p];
+            io.in[2 + NP + p] = pe[p];
+        }
+        for (int k = 0; k < 6; ++k) io.in[2 + 2 * NP + k] = tri[k];
+        io.out[0] = zv;
+        io.out[1] = zm;
+        io.out[2] = open_d;
+        io.out[3] = open_e;
+        return run_map(s, io, n, OpCombine<NP, true>{party, alpha}, sms);
+    }
+    IO<NI, 2> io;
+    io.in[0] = od;
+    io.in[1] = oe;
+    for (int p = 0; p < NP; ++p) {
+        io.in[2 + p] = pd[p];
+        io.in[2 + NP + p] = pe[p];
+    }
+    for (int k = 0; k < 6; ++k) io.in[2 + 2 * NP + k] = tri[k];
+    io.out[0] = zv;
+    io.out[1] = zm;
+    return run_map(s, io, n, OpCombine<NP, false>{party, alpha}, sms);
+}
+
+template <int NP>
+cudaError_t open_np(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, uint32_t* out, uint64_t n,
+                    int sms) {
+    IO<1 + NP, 1> io;
+    io.in[0] = own;
+    for (int p = 0; p < NP; ++p) io.in[1 + p] = peers[p];
+    io.out[0] = out;
+    return run_map(s, io, n, OpOpen<NP>{}, sms);
+}
+
+// ---------------------------------------------------------------------------
+// Reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block sum of NV u64 values; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(unsigned long long (&v)[NV]) {
+    __shared__ unsigned long long sh[NV][kThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sh[k][w] = v[k];
+    }
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            unsigned long long x = lane < (int)(blockDim.x >> 5) ? sh[k][lane] : 0ull;
+            v[k] = warp_sum(x);
+        }
+    }
+    __syncthreads();
+}
+
+// backend.cpp:76-84.  Per-thread u64 sums of u32 lanes (<= 2^32 terms safe),
+// block tree, fold to < p, one atomic per block.
+__global__ void __launch_bounds__(kThreads) k_reduce_add(const uint32_t* __restrict__ xv,
+                                                         const uint32_t* __restrict__ xm, uint64_t n,
+                                                         unsigned long long* acc) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    unsigned long long s[2] = {0ull, 0ull};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        s[0] += __ldcs(xv + i);
+        s[1] += __ldcs(xm + i);
+    }
+    s[0] = fp_reduce64(s[0]);
+    s[1] = fp_reduce64(s[1]);
+    block_sum<2>(s);
+    if (threadIdx.x == 0) {
+        atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
+        atomicAdd(acc + 1, (unsigned long long)fp_reduce64(s[1]));
+    }
+}
+
+__global__ void k_finish_reduce(const unsigned long long* acc, uint32_t* outv, uint32_t* outm) {
+    if (threadIdx.x == 0) {
+        outv[0] = fp_reduce64(acc[0]);
+        outm[0] = fp_reduce64(acc[1]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_pair_split(const uint32_t* __restrict__ cv,
+                                                         const uint32_t* __restrict__ cm, uint64_t pairs,
+                                                         uint32_t* xv, uint32_t* xm, uint32_t* yv, uint32_t* ym) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+        uint2 v = reinterpret_cast<const uint2*>(cv)[i];
+        uint2 m = reinterpret_cast<const uint2*>(cm)[i];
+        xv[i] = v.x;
+        yv[i] = v.y;
+        xm[i] = m.x;
+        ym[i] = m.y;
+    }
+}
+
+// MAC sigma (spdz.cpp:126-138) in closed form: record of rank j contributes
+// r_j * (m_j - alpha x_j), r_j = reduce(mix(coin + (j+1) gamma)).  Order-free.
+__global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restrict__ segs,
+                                                        const MacChunk* __restrict__ chunks, uint32_t n_chunks,
+                                                        uint64_t coin, uint32_t alpha, unsigned long long* acc) {
+    unsigned long long s[1] = {0ull};
+    for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const MacChunk ch = chunks[c];
+        const MacSegDev sg = segs[ch.seg];
+        const uint64_t base = ch.start;
+        for (uint32_t i = threadIdx.x; i < ch.count; i += blockDim.x) {
+            const uint64_t idx = base + i;
+            const uint32_t x = __ldcs(sg.value + idx);
+            uint32_t m = __ldcs(sg.mac_a + idx);
+            if (sg.mac_b) m = fp_sub(m, __ldcs(sg.mac_b + idx));
+            const uint32_t r = mac_coeff(coin, sg.j0 + idx);
+            const uint32_t diff = fp_sub(m, fp_mul(alpha, x));
+            s[0] += fold1(mul_wide(r, diff));  // < 6*2^32, count per thread << 2^29
+        }
+        s[0] = fold1(s[0]);
+    }
+    s[0] = fp_reduce64(s[0]);
+    block_sum<1>(s);
+    if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
+}
+
+__global__ void __launch_bounds__(kThreads) k_mac_sigma_ranked(const uint32_t* __restrict__ value,
+                                                               const uint32_t* __restrict__ mac,
+                                                               const uint64_t* __restrict__ rank, uint64_t n,
+                                                               uint64_t coin, uint32_t alpha,
+                                                               unsigned long long* acc) {
+    unsigned long long s[1] = {0ull};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t r = mac_coeff(coin, rank[i]);
+        const uint32_t diff = fp_sub(mac[i], fp_mul(alpha, value[i]));
+        s[0] = fold1(s[0] + fold1(mul_wide(r, diff)));
+    }
+    s[0] = fp_reduce64(s[0]);
+    block_sum<1>(s);
+    if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
+}
+
+// ---------------------------------------------------------------------------
+// Linear layer: matrix_combine fused with the open of the [D|E] payload.
+// One CTA per row (grid-strided); vectorised over the row when aligned.
+// E (opened, din words) must already be in opened[cells .. cells+din).
+// ---------------------------------------------------------------------------
+struct PeerPtrs {
+    const uint32_t* p[kMaxPeers];
+};
+
+template <int NP, bool V4>
+__global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint32_t rows, uint32_t rpt,
+                                                             const uint32_t* own,
+                                                             PeerPtrs peers_dev,
+                                                             const uint32_t* __restrict__ Av,
+                                                             const uint32_t* __restrict__ Am,
+                                                             const uint32_t* __restrict__ Bv_all,
+                                                             const uint32_t* __restrict__ Bm_all,
+                                                             const uint32_t* __restrict__ Cv,
+                                                             const uint32_t* __restrict__ Cm,
+                                                             const uint32_t* __restrict__ biasv,
+                                                             const uint32_t* __restrict__ biasm, int party,
+                                                             uint32_t alpha, uint32_t* zv, uint32_t* zm,
+                                                             uint32_t* opened) {
+    const uint64_t cells = (uint64_t)din * rows;
+    const uint32_t* peers[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) peers[p] = peers_dev.p[p];
+    for (uint32_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const uint64_t base = (uint64_t)r * din;
+        const uint64_t tile_off = (uint64_t)(r / rpt) * din;  // B_t / E_t of this row's tile
+        const uint32_t* E = opened + cells + tile_off;
+        const uint32_t* Bv = Bv_all + tile_off;
+        const uint32_t* Bm = Bm_all + tile_off;
+        unsigned long long acc[3] = {0ull, 0ull, 0ull};  // v, m, de
+        if (V4) {
+            const uint32_t n4 = din / 4;
+            for (uint32_t g = threadIdx.x; g < n4; g += blockDim.x) {
+                const uint64_t gg = base / 4 + g;
+                uint4 d4 = ld4(own, gg);
+                uint32_t d[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    uint4 q = ld4_peer(peers[p], gg);
+                    d[0] = fp_add(d[0], fp_reduce32(q.x));
+                    d[1] = fp_add(d[1], fp_reduce32(q.y));
+                    d[2] = fp_add(d[2], fp_reduce32(q.z));
+                    d[3] = fp_add(d[3], fp_reduce32(q.w));
+                }
+                st4(opened, gg, d);
+                uint4 av = ld4(Av, gg), am = ld4(Am, gg);
+                uint4 bv = reinterpret_cast<const uint4*>(Bv)[g], bm = reinterpret_cast<const uint4*>(Bm)[g];
+                uint4 e4 = reinterpret_cast<const uint4*>(E)[g];
+                const uint32_t A0[4] = {av.x, av.y, av.z, av.w}, A1[4] = {am.x, am.y, am.z, am.w};
+                const uint32_t B0[4] = {bv.x, bv.y, bv.z, bv.w}, B1[4] = {bm.x, bm.y, bm.z, bm.w};
+                const uint32_t Ee[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    acc[0] += fold1(mul_wide(d[l], B0[l])) + fold1(mul_wide(A0[l], Ee[l]));
+                    acc[1] += fold1(mul_wide(d[l], B1[l])) + fold1(mul_wide(A1[l], Ee[l]));
+                    acc[2] += fold1(mul_wide(d[l], Ee[l]));
+                }
+            }
+        } else {
+            for (uint32_t c = threadIdx.x; c < din; c += blockDim.x) {
+                uint32_t d = own[base + c];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) d = fp_add(d, fp_reduce32(peers[p][base + c]));
+                opened[base + c] = d;
+                const uint32_t e = E[c];
+                acc[0] += fold1(mul_wide(d, Bv[c])) + fold1(mul_wide(Av[base + c], e));
+                acc[1] += fold1(mul_wide(d, Bm[c])) + fold1(mul_wide(Am[base + c], e));
+                acc[2] += fold1(mul_wide(d, e));
+            }
+        }
+        // per-thread partial sums are < din/256 * 12 * 2^32: fold before the tree
+        acc[0] = fold1(acc[0]);
+        acc[1] = fold1(acc[1]);
+        acc[2] = fold1(acc[2]);
+        block_sum<3>(acc);
+        if (threadIdx.x == 0) {
+            // spdz.cpp:117-123
+            const uint32_t der = fp_reduce64(acc[2]);
+            uint32_t vr = fp_reduce64((unsigned long long)Cv[r] + fp_reduce64(acc[0]));
+            if (party == 0) vr = fp_add(vr, der);
+            uint32_t mr = fp_add(fp_reduce64((unsigned long long)Cm[r] + fp_reduce64(acc[1])), fp_mul(alpha, der));
+            if (biasv) {  // linear.cpp:59 add_local(z, b_slice)
+                vr = fp_add(vr, biasv[r]);
+                mr = fp_add(mr, biasm[r]);
+            }
+            zv[r] = vr;
+            zm[r] = mr;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-core modular GEMM: C (MxN) = A (MxK) * B (KxN) mod p, row-major.
+// A is split into 16-bit halves when staged to shared memory, so each MAC is
+// one IMAD.WIDE.U32 into a u64 (a_half*b < 2^48): 2^15 K-steps between folds.
+// 64x64 CTA tile, 16-deep K tile, 256 threads each owning 4x4 outputs.
+// ---------------------------------------------------------------------------
+constexpr int GT = 64, GK = 16;
+
+__global__ void __launch_bounds__(256) k_modgemm(uint32_t M, uint32_t N, uint32_t K, const uint32_t* A0,
+                                                 const uint32_t* A1, const uint32_t* B0, const uint32_t* B1,
+                                                 uint32_t* C0, uint32_t* C1) {
+    const uint32_t* A = blockIdx.z ? A1 : A0;
+    const uint32_t* B = blockIdx.z ? B1 : B0;
+    uint32_t* C = blockIdx.z ? C1 : C0;
+    __shared__ __align__(16) uint32_t sAl[GK][GT + 4];
+    __shared__ __align__(16) uint32_t sAh[GK][GT + 4];
+    __shared__ __align__(16) uint32_t sB[GK][GT + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const uint32_t m0 = blockIdx.y * GT, n0 = blockIdx.x * GT;
+    unsigned long long lo[4][4], hi[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) lo[i][j] = hi[i][j] = 0ull;
+    uint32_t since_fold = 0;
+    for (uint32_t k0 = 0; k0 < K; k0 += GK) {
+        // stage A tile (GT rows x GK cols) transposed, B tile (GK rows x GT cols)
+        for (int idx = threadIdx.x; idx < GT * GK; idx += 256) {
+            const int r = idx / GK, c = idx % GK;
+            const uint32_t gr = m0 + r, gc = k0 + c;
+            const uint32_t a = (gr < M && gc < K) ? A[(uint64_t)gr * K + gc] : 0u;
+            sAl[c][r] = a & 0xffffu;
+            sAh[c][r] = a >> 16;
+            const int br = idx / GT, bc = idx % GT;
+            const uint32_t gbr = k0 + br, gbc = n0 + bc;
+            sB[br][bc] = (gbr < K && gbc < N) ? B[(uint64_t)gbr * N + gbc] : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < GK; ++k) {
+            const uint4 al4 = *reinterpret_cast<const uint4*>(&sAl[k][ty * 4]);
+            const uint4 ah4 = *reinterpret_cast<const uint4*>(&sAh[k][ty * 4]);
+            const uint4 b4 = *reinterpret_cast<const uint4*>(&sB[k][tx * 4]);
+            const uint32_t al[4] = {al4.x, al4.y, al4.z, al4.w}, ah[4] = {ah4.x, ah4.y, ah4.z, ah4.w};
+            const uint32_t b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    lo[i][j] += mul_wide(al[i], b[j]);
+                    hi[i][j] += mul_wide(ah[i], b[j]);
+                }
+        }
+        since_fold += GK;
+        if (since_fold >= 32768) {  // keep the u64 accumulators from overflowing
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    lo[i][j] = fold1(lo[i][j]);
+                    hi[i][j] = fold1(hi[i][j]);
+                }
+            since_fold = 0;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t gr = m0 + ty * 4 + i;
+        if (gr >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t gc = n0 + tx * 4 + j;
+            if (gc >= N) continue;
+            const uint32_t h = fp_reduce64(hi[i][j]);
+            C[(uint64_t)gr * N + gc] = fp_reduce64((unsigned long long)fp_reduce64(lo[i][j]) + mul_wide(h, 65536u));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GPU dealer (spdz.cpp:162-249).  Draw k of the dealer stream (0-based after
+// construction) = reduce(mix(seed + (k+1) gamma)); the reference redraws when
+// the raw value is >= 2^64 - 25 (spdz.cpp:175-183): flagged, never silently
+// shifted.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kRejectBound = 0xFFFFFFFFFFFFFFE7ull;  // (2^64-1)/p*p = 2^64 - 25
+
+__device__ __forceinline__ uint32_t draw(uint64_t seed, uint64_t k, unsigned int* flag) {
+    const uint64_t v = mix64(seed + (k + 1) * kGamma);
+    if (v >= kRejectBound) atomicOr(flag, 1u);
+    return fp_reduce64(v);
+}
+
+// spdz.cpp:185-201 for one lane: party i>=1 gets (val, mac) draws at
+// base + 2(i-1), +1; party 0 the remainder.
+__device__ __forceinline__ void share_lane(int n, uint64_t seed, uint64_t base, uint32_t alpha, uint32_t x,
+                                           uint32_t* vals, uint32_t* macs, uint64_t pstride, uint64_t j,
+                                           unsigned int* flag) {
+    uint32_t vs = 0, ms = 0;
+    for (int i = 1; i < n; ++i) {
+        const uint32_t v = draw(seed, base + 2 * (i - 1), flag);
+        const uint32_t m = draw(seed, base + 2 * (i - 1) + 1, flag);
+        vals[(uint64_t)i * pstride + j] = v;
+        macs[(uint64_t)i * pstride + j] = m;
+        vs = fp_add(vs, v);
+        ms = fp_add(ms, m);
+    }
+    vals[j] = fp_sub(x, vs);
+    macs[j] = fp_sub(fp_mul(alpha, x), ms);
+}
+
+__global__ void k_dealer_triples(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t lanes,
+                                 uint32_t* av, uint32_t* am, uint32_t* bv, uint32_t* bm, uint32_t* cv, uint32_t* cm,
+                                 unsigned int* flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t per = 2ull * (n - 1);
+    const uint64_t sa = draw0 + 2 * lanes, sb = sa + per * lanes, sc = sb + per * lanes;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lanes; j += stride) {
+        const uint32_t a = draw(seed, draw0 + 2 * j, flag);
+        const uint32_t b = draw(seed, draw0 + 2 * j + 1, flag);
+        const uint32_t c = fp_mul(a, b);
+        share_lane(n, seed, sa + j * per, alpha, a, av, am, lanes, j, flag);
+        share_lane(n, seed, sb + j * per, alpha, b, bv, bm, lanes, j, flag);
+        share_lane(n, seed, sc + j * per, alpha, c, cv, cm, lanes, j, flag);
+    }
+}
+
+__global__ void k_dealer_share(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, const uint32_t* clear,
+                               uint64_t lanes, uint32_t* vals, uint32_t* macs, uint64_t pstride, unsigned int* flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t per = 2ull * (n - 1);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lanes; j += stride)
+        share_lane(n, seed, draw0 + j * per, alpha, clear[j], vals, macs, pstride, j, flag);
+}
+
+__global__ void k_dealer_uniform(uint64_t seed, uint64_t draw0, uint64_t count, uint32_t* out, unsigned int* flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride)
+        out[j] = draw(seed, draw0 + j, flag);
+}
+
+// C[r] = sum_c A[r,c] B[c] mod p (spdz.cpp:239-246)
+__global__ void __launch_bounds__(kThreads) k_dealer_matvec(const uint32_t* A, const uint32_t* B, uint32_t din,
+                                                            uint32_t rows, uint32_t* C) {
+    for (uint32_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        unsigned long long s[1] = {0ull};
+        for (uint32_t c = threadIdx.x; c < din; c += blockDim.x)
+            s[0] += fold1(mul_wide(A[(uint64_t)r * din + c], B[c]));
+        s[0] = fold1(s[0]);
+        block_sum<1>(s);
+        if (threadIdx.x == 0) C[r] = fp_reduce64(s[0]);
+    }
+}
+
+// triple_store.cpp:274-283: mask j = share_random(1): clear draw, then share draws.
+__global__ void k_dealer_masks(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count, uint32_t* vals,
+                               uint32_t* macs, uint32_t* clear, unsigned int* flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t per = 1 + 2ull * (n - 1);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+        const uint64_t base = draw0 + j * per;
+        const uint32_t x = draw(seed, base, flag);
+        clear[j] = x;
+        share_lane(n, seed, base + 1, alpha, x, vals, macs, count, j, flag);
+    }
+}
+
+// public (cleartext) lane ops with scalar broadcast (runtime.cpp:131-136, 168-172)
+__global__ void __launch_bounds__(kThreads) k_pub_binop(int op, const uint32_t* a, bool a_b, const uint32_t* b,
+                                                        bool b_b, uint32_t* out, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t a0 = a_b ? a[0] : 0u, b0 = b_b ? b[0] : 0u;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t x = a_b ? a0 : a[i], y = b_b ? b0 : b[i];
+        out[i] = op == 0 ? fp_add(x, y) : (op == 1 ? fp_sub(x, y) : fp_mul(x, y));
+    }
+}
+
+// bcast_share (runtime.cpp:41-47): every lane = lane 0 of the source
+__global__ void __launch_bounds__(kThreads) k_bcast2(const uint32_t* sv, const uint32_t* sm, uint32_t* ov,
+                                                     uint32_t* om, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t v = sv[0], m = sm ? sm[0] : 0u;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        ov[i] = v;
+        if (om) om[i] = m;
+    }
+}
+
+// E_t = x.v - B_t.v for every tile t (linear.cpp:44-47), B laid out n_tiles x din
+__global__ void __launch_bounds__(kThreads) k_tile_e(const uint32_t* __restrict__ xv, const uint32_t* __restrict__ bv,
+                                                     uint32_t din, uint64_t total, uint32_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+        out[i] = fp_sub(xv[i % din], bv[i]);
+}
+
+__global__ void k_xor_word(uint32_t* p, uint32_t mask) {
+    if (threadIdx.x == 0) *p ^= mask;
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
+                           const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms) {
+    IO<4, 2> io{{xv, xm, yv, ym}, {zv, zm}};
+    return sub ? run_map(s, io, n, OpSub{}, sms) : run_map(s, io, n, OpAdd{}, sms);
+}
+
+template <int OPC>
+static cudaError_t public_dispatch(cudaStream_t s, const uint32_t* xv, const uint32_t* xm, const uint32_t* k, int km,
+                                   uint32_t kk, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm, uint64_t n,
+                                   int sms) {
+    if (km == 0) {
+        IO<3, 2> io{{xv, xm, k}, {zv, zm}};
+        return run_map(s, io, n, OpPublic<OPC, 0>{{}, party, alpha, 0u, k}, sms);
+    }
+    IO<2, 2> io{{xv, xm}, {zv, zm}};
+    if (km == 1) return run_map(s, io, n, OpPublic<OPC, 1>{{}, party, alpha, 0u, k}, sms);
+    return run_map(s, io, n, OpPublic<OPC, 2>{{}, party, alpha, kk, k}, sms);
+}
+
+cudaError_t launch_public(cudaStream_t s, int op, const uint32_t* xv, const uint32_t* xm, const uint32_t* k,
+                          bool k_bcast, uint32_t k_imm, bool k_is_imm, int party, uint32_t alpha, uint32_t* zv,
+                          uint32_t* zm, uint64_t n, int sms) {
+    const int km = k_is_imm ? 2 : (k_bcast ? 1 : 0);
+    switch (op) {
+        case 0: return public_dispatch<0>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
+        case 1: return public_dispatch<1>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
+        case 2: return public_dispatch<2>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
+        case 3: return public_dispatch<3>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
+        case 4: {
+            if (km == 0) {
+                IO<1, 2> io{{k}, {zv, zm}};
+                return run_map(s, io, n, OpShareOfPublic<0>{{}, party, alpha, 0u, k}, sms);
+            }
+            IO<0, 2> io{{nullptr}, {zv, zm}};
+            if (km == 1) return run_map(s, io, n, OpShareOfPublic<1>{{}, party, alpha, 0u, k}, sms);
+            return run_map(s, io, n, OpShareOfPublic<2>{{}, party, alpha, k_imm, k}, sms);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* yv, const uint32_t* av,
+                            const uint32_t* bv, uint32_t* d, uint32_t* e, uint64_t n, int sms) {
+    IO<4, 2> io{{xv, yv, av, bv}, {d, e}};
+    return run_map(s, io, n, OpMask{}, sms);
+}
+
+cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                  const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
+                                  const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
+                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms) {
+    switch (n_peers) {
+#define CASE(NP) \
+    case NP: return combine_np<NP>(s, own_d, own_e, peer_d, peer_e, tri, party, alpha, zv, zm, open_d, open_e, n, sms);
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, int n_peers,
+                            uint32_t* out, uint64_t n, int sms) {
+    switch (n_peers) {
+#define CASE(NP) \
+    case NP: return open_np<NP>(s, own, peers, out, n, sms);
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reduce_add(cudaStream_t s, const uint32_t* xv, const uint32_t* xm, uint64_t n,
+                              unsigned long long* acc, int sms) {
+    k_reduce_add<<<grid_for(n, sms), kThreads, 0, s>>>(xv, xm, n, acc);
+    return launched();
+}
+
+cudaError_t launch_finish_reduce(cudaStream_t s, const unsigned long long* acc, uint32_t* outv, uint32_t* outm) {
+    k_finish_reduce<<<1, 32, 0, s>>>(acc, outv, outm);
+    return launched();
+}
+
+cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t* cm, uint64_t pairs, uint32_t* xv,
+                              uint32_t* xm, uint32_t* yv, uint32_t* ym, int sms) {
+    if (pairs == 0) return cudaSuccess;
+    k_pair_split<<<grid_for(pairs, sms), kThreads, 0, s>>>(cv, cm, pairs, xv, xm, yv, ym);
+    return launched();
+}
+
+cudaError_t launch_mac_sigma(cudaStream_t s, const MacSegDev* segs, const MacChunk* chunks, uint32_t n_chunks,
+                             uint64_t coin, uint32_t alpha, unsigned long long* acc, int sms) {
+    if (n_chunks == 0) return cudaSuccess;
+    int grid = (int)(n_chunks < (uint32_t)(sms * 8) ? n_chunks : (uint32_t)(sms * 8));
+    k_mac_sigma<<<grid, kThreads, 0, s>>>(segs, chunks, n_chunks, coin, alpha, acc);
+    return launched();
+}
+
+cudaError_t launch_mac_sigma_ranked(cudaStream_t s, const uint32_t* value, const uint32_t* mac,
+                                    const uint64_t* rank, uint64_t n, uint64_t coin, uint32_t alpha,
+                                    unsigned long long* acc, int sms) {
+    if (n == 0) return cudaSuccess;
+    k_mac_sigma_ranked<<<grid_for(n, sms), kThreads, 0, s>>>(value, mac, rank, n, coin, alpha, acc);
+    return launched();
+}
+
+cudaError_t launch_matrix_mask(cudaStream_t s, const uint32_t* wv, const uint32_t* av, uint64_t cells,
+                               const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t* payload, int sms) {
+    // D = W.v - A.v over the tile; E = x.v - B.v (linear.cpp:40-47, value plane)
+    IO<2, 1> io_d{{wv, av}, {payload}};
+    cudaError_t e = run_map(s, io_d, cells, OpDiff{}, sms);
+    if (e != cudaSuccess) return e;
+    IO<2, 1> io_e{{xv, bv}, {payload + cells}};
+    return run_map(s, io_e, din, OpDiff{}, sms);
+}
+
+template <int NP>
+static cudaError_t mc_np(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
+                         const PeerPtrs& peers_dev, const uint32_t* const mt[6], const uint32_t* biasv,
+                         const uint32_t* biasm, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
+                         uint32_t* opened, bool v4, int sms) {
+    const int grid = (int)(rows < (uint32_t)(sms * 8) ? rows : (uint32_t)(sms * 8));
+    if (rows == 0) return cudaSuccess;
+    if (v4)
+        k_matrix_combine<NP, true><<<grid, kThreads, 0, s>>>(din, rows, rpt, own, peers_dev, mt[0], mt[1], mt[2], mt[3],
+                                                             mt[4], mt[5], biasv, biasm, party, alpha, zv, zm, opened);
+    else
+        k_matrix_combine<NP, false><<<grid, kThreads, 0, s>>>(din, rows, rpt, own, peers_dev, mt[0], mt[1], mt[2], mt[3],
+                                                              mt[4], mt[5], biasv, biasm, party, alpha, zv, zm,
+                                                              opened);
+    return launched();
+}
+
+// `peers` is a HOST array of (device-accessible) peer payload pointers.
+cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
+                                  const uint32_t* const* peers, int n_peers, const uint32_t* const mt[6],
+                                  const uint32_t* biasv, const uint32_t* biasm, int party, uint32_t alpha,
+                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms) {
+    const uint64_t cells = (uint64_t)din * rows;
+    bool v4 = (din % 4 == 0) && aligned16(own) && aligned16(opened) && aligned16(mt[0]) && aligned16(mt[1]) &&
+              aligned16(mt[2]) && aligned16(mt[3]);
+    for (int p = 0; p < n_peers; ++p) v4 = v4 && aligned16(peers[p]);
+    if (rpt == 0) return cudaErrorInvalidValue;
+    (void)cells;
+    if (n_peers < 0 || n_peers > kMaxPeers) return cudaErrorInvalidValue;
+    PeerPtrs peer_table{};
+    for (int p = 0; p < n_peers; ++p) peer_table.p[p] = peers[p];
+    switch (n_peers) {
+#define CASE(NP) \
+    case NP: return mc_np<NP>(s, din, rows, rpt, own, peer_table, mt, biasv, biasm, party, alpha, zv, zm, opened, v4, sms);
+        CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,
+                           const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
+                           uint32_t* y0, uint32_t* y1) {
+    if (dout == 0 || batch == 0) return cudaSuccess;
+    dim3 grid((batch + GT - 1) / GT, (dout + GT - 1) / GT, 2);
+    if (mode == 0)  // W public shared by both planes of X
+        k_modgemm<<<grid, 256, 0, s>>>(dout, batch, din, w0, w0, x0, x1, y0, y1);
+    else  // W secret planes, X public
+        k_modgemm<<<grid, 256, 0, s>>>(dout, batch, din, w0, w1, x0, x0, y0, y1);
+    return launched();
+}
+
+cudaError_t launch_dealer_triples(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                  uint64_t lanes, uint32_t* const planes[6], unsigned int* flag, int sms) {
+    if (lanes == 0) return cudaSuccess;
+    k_dealer_triples<<<grid_for(lanes, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, lanes, planes[0], planes[1],
+                                                                    planes[2], planes[3], planes[4], planes[5], flag);
+    return launched();
+}
+
+cudaError_t launch_dealer_share(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                const uint32_t* clear, uint64_t lanes, uint32_t* vals, uint32_t* macs,
+                                uint64_t pstride, unsigned int* flag, int sms) {
+    if (lanes == 0) return cudaSuccess;
+    k_dealer_share<<<grid_for(lanes, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, clear, lanes, vals, macs,
+                                                                  pstride, flag);
+    return launched();
+}
+
+cudaError_t launch_dealer_uniform(cudaStream_t s, uint64_t seed, uint64_t draw0, uint64_t count, uint64_t,
+                                  uint32_t* out, unsigned int* flag, int sms) {
+    if (count == 0) return cudaSuccess;
+    k_dealer_uniform<<<grid_for(count, sms, 16), kThreads, 0, s>>>(seed, draw0, count, out, flag);
+    return launched();
+}
+
+cudaError_t launch_dealer_matvec(cudaStream_t s, const uint32_t* A, const uint32_t* B, uint32_t din, uint32_t rows,
+                                 uint32_t* C) {
+    if (rows == 0) return cudaSuccess;
+    k_dealer_matvec<<<rows < 4096 ? rows : 4096, kThreads, 0, s>>>(A, B, din, rows, C);
+    return launched();
+}
+
+cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count,
+                                uint32_t* vals, uint32_t* macs, uint32_t* clear, unsigned int* flag, int sms) {
+    if (count == 0) return cudaSuccess;
+    k_dealer_masks<<<grid_for(count, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, count, vals, macs, clear,
+                                                                  flag);
+    return launched();
+}
+
+cudaError_t launch_pub_binop(cudaStream_t s, int op, const uint32_t* a, bool a_bcast, const uint32_t* b, bool b_bcast,
+                             uint32_t* out, uint64_t n, int sms) {
+    if (n == 0) return cudaSuccess;
+    k_pub_binop<<<grid_for(n, sms), kThreads, 0, s>>>(op, a, a_bcast, b, b_bcast, out, n);
+    return launched();
+}
+
+cudaError_t launch_bcast(cudaStream_t s, const uint32_t* sv, const uint32_t* sm, uint32_t* ov, uint32_t* om,
+                         uint64_t n, int sms) {
+    if (n == 0) return cudaSuccess;
+    k_bcast2<<<grid_for(n, sms), kThreads, 0, s>>>(sv, sm, ov, om, n);
+    return launched();
+}
+
+cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t n_tiles,
+                          uint32_t* out, int sms) {
+    const uint64_t total = (uint64_t)din * n_tiles;
+    if (total == 0) return cudaSuccess;
+    k_tile_e<<<grid_for(total, sms), kThreads, 0, s>>>(xv, bv, din, total, out);
+    return launched();
+}
+
+cudaError_t launch_xor_word(cudaStream_t s, uint32_t* p, uint32_t mask) {
+    k_xor_word<<<1, 32, 0, s>>>(p, mask);
+    return launched();
+}
+
+}  // namespace spdzb200

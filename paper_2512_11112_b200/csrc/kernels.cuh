@@ -1,0 +1,108 @@
+// Kernel launchers of the B200 SPDZ back end (sm_100a).  Every launcher is
+// asynchronous on `stream` and returns cudaGetLastError() of its launch.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace spdzb200 {
+
+constexpr int kMaxPeers = 7;
+
+struct MacSegDev {            // device-side MAC segment descriptor
+    const uint32_t* value;
+    const uint32_t* mac_a;
+    const uint32_t* mac_b;    // may be null
+    uint64_t len;
+    uint64_t j0;
+};
+struct MacChunk {             // work item: [start, start+count) of segment `seg`
+    uint32_t seg;
+    uint32_t count;
+    uint64_t start;
+};
+
+struct LaunchInfo {
+    int sm_count = 148;
+};
+
+extern unsigned long long g_kernel_launches;  // evidence counter
+
+// elementwise (backend.cpp:25-51, spdz.cpp:35-75)
+cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
+                           const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms);
+// op: 0 add_public 1 sub_public 2 rsub_public 3 mul_public 4 share_of_public (xv/xm unused as inputs)
+cudaError_t launch_public(cudaStream_t s, int op, const uint32_t* xv, const uint32_t* xm, const uint32_t* k,
+                          bool k_bcast, uint32_t k_imm, bool k_is_imm, int party, uint32_t alpha, uint32_t* zv,
+                          uint32_t* zm, uint64_t n, int sms);
+// backend.cpp:53-65
+cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* yv, const uint32_t* av,
+                            const uint32_t* bv, uint32_t* d, uint32_t* e, uint64_t n, int sms);
+// spdz.cpp:77-96 fused with the open of net.cpp:170-215: d = own_d + sum reduce(peer_d) ...
+cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                  const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
+                                  const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
+                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms);
+// net.cpp:170-215
+cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, int n_peers,
+                            uint32_t* out, uint64_t n, int sms);
+// backend.cpp:76-84; result folded into acc[0..1] (u64, values < p each) — caller zeroes acc.
+cudaError_t launch_reduce_add(cudaStream_t s, const uint32_t* xv, const uint32_t* xm, uint64_t n,
+                              unsigned long long* acc, int sms);
+// acc (2 x u64) -> out[0] = acc[0] mod p, out[1] = acc[1] mod p
+cudaError_t launch_finish_reduce(cudaStream_t s, const unsigned long long* acc, uint32_t* outv, uint32_t* outm);
+// pairwise gather for reduce_mul (runtime.cpp:246-255): xs = cur[2i], ys = cur[2i+1]
+cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t* cm, uint64_t pairs, uint32_t* xv,
+                              uint32_t* xm, uint32_t* yv, uint32_t* ym, int sms);
+// MAC sigma partial over chunks; acc (u64) accumulates values < p per block.
+cudaError_t launch_mac_sigma(cudaStream_t s, const MacSegDev* segs, const MacChunk* chunks, uint32_t n_chunks,
+                             uint64_t coin, uint32_t alpha, unsigned long long* acc, int sms);
+// MAC sigma over explicit ranks (record form)
+cudaError_t launch_mac_sigma_ranked(cudaStream_t s, const uint32_t* value, const uint32_t* mac,
+                                    const uint64_t* rank, uint64_t n, uint64_t coin, uint32_t alpha,
+                                    unsigned long long* acc, int sms);
+
+// linear layer (linear.cpp:30-61, spdz.cpp:98-124)
+cudaError_t launch_matrix_mask(cudaStream_t s, const uint32_t* wv, const uint32_t* av, uint64_t cells,
+                               const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t* payload, int sms);
+// Layer-level: rows = all rows of the layer, tiles of `rpt` rows (last may be
+// short); A (rows x din), B (n_tiles x din), C (rows); opened = [D (rows*din) |
+// E (n_tiles*din)] with E already opened.  One CTA per row.
+cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
+                                  const uint32_t* const* peers, int n_peers, const uint32_t* const mt[6],
+                                  const uint32_t* biasv, const uint32_t* biasm, int party, uint32_t alpha,
+                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms);
+// E_t = x - B_t for all tiles (B: n_tiles x din)
+cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t n_tiles,
+                          uint32_t* out, int sms);
+// runtime.cpp:303-334 batched: Y (dout x batch) = W (dout x din) * X (din x batch), two planes.
+//   mode 0: W public (w0), X secret planes (x0 vals, x1 macs) -> y0 = W x0, y1 = W x1
+//   mode 1: W secret (w0 vals, w1 macs), X public (x0)        -> y0 = w0 X, y1 = w1 X
+cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,
+                           const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
+                           uint32_t* y0, uint32_t* y1);
+
+// GPU dealer (spdz.cpp:162-249), closed-form splitmix64 stream.
+cudaError_t launch_dealer_triples(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                  uint64_t lanes, uint32_t* const planes[6], unsigned int* reject_flag, int sms);
+// party p's share of lane j goes to vals[p * pstride + j]
+cudaError_t launch_dealer_share(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                const uint32_t* clear, uint64_t lanes, uint32_t* vals, uint32_t* macs,
+                                uint64_t pstride, unsigned int* reject_flag, int sms);
+cudaError_t launch_dealer_uniform(cudaStream_t s, uint64_t seed, uint64_t draw0, uint64_t count, uint64_t stride,
+                                  uint32_t* out, unsigned int* reject_flag, int sms);
+cudaError_t launch_dealer_matvec(cudaStream_t s, const uint32_t* A, const uint32_t* B, uint32_t din, uint32_t rows,
+                                 uint32_t* C);
+cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count,
+                                uint32_t* vals, uint32_t* macs, uint32_t* clear, unsigned int* reject_flag, int sms);
+
+// cleartext lane op (0 add 1 sub 2 mul) with scalar broadcast of either side
+cudaError_t launch_pub_binop(cudaStream_t s, int op, const uint32_t* a, bool a_bcast, const uint32_t* b, bool b_bcast,
+                             uint32_t* out, uint64_t n, int sms);
+// out[i] = src[0] (either plane pointer may be null for the MAC plane)
+cudaError_t launch_bcast(cudaStream_t s, const uint32_t* sv, const uint32_t* sm, uint32_t* ov, uint32_t* om,
+                         uint64_t n, int sms);
+
+// payload fault injection (test hook, net.cpp:241-278 BitFlip)
+cudaError_t launch_xor_word(cudaStream_t s, uint32_t* p, uint32_t mask);
+
+}  // namespace spdzb200

@@ -1,0 +1,1269 @@
+// Local n-party online phase over device-resident state: the batch executor
+// that replaces PartyRuntime::Impl's node drivers (runtime.cpp:129-506) for
+// straight-line circuits.  Parties are CUDA streams (optionally on distinct
+// devices); the opening exchange is a peer-buffer read fused into the combine
+// kernels, ordered by per-party events (the batch-id matching of
+// net.cpp:61-95 becomes stream/event ordering).  Every share, triple pool,
+// opened-value log and MAC record lives in HBM as structure-of-arrays.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "field.cuh"
+#include "internal.hpp"
+
+using namespace spdzb200;
+
+namespace {
+
+uint64_t make_batch(uint64_t node, uint64_t exec, uint64_t sub) {  // runtime.cpp:22-24
+    return (node << 32) | (exec << 12) | sub;
+}
+
+void lk(cudaError_t e, const char* what) { cuda_check(e, what); }
+
+// RtValue (runtime.cpp:28-34), device resident.
+struct Val {
+    bool is_public = true;
+    uint32_t* pub = nullptr;
+    uint32_t* v = nullptr;
+    uint32_t* m = nullptr;
+    uint64_t lanes = 0;
+};
+
+struct Region {  // preproc.hpp:44-53
+    uint64_t base = 0, stride = 0, max_execs = 1;
+};
+
+struct Fault {
+    uint32_t node;
+    int sender, receiver;
+    uint64_t word;
+    uint32_t bit;
+};
+
+struct RedLevel {
+    uint64_t in_lanes = 0, pairs = 0;
+    uint32_t *xv = nullptr, *xm = nullptr, *yv = nullptr, *ym = nullptr;
+    uint32_t *payload = nullptr, *opened = nullptr, *shadow = nullptr;
+    uint32_t *zv = nullptr, *zm = nullptr;  // pairs (+1 odd passthrough)
+    uint64_t out_lanes = 0;
+};
+
+struct NodeState {                  // per party, per node
+    Val out;
+    // Beaver
+    Val xa, xb;                     // operands after bcast_share
+    uint32_t* payload = nullptr;    // [d|e] or [D|E] sent to peers
+    uint32_t* opened = nullptr;     // opened values (MAC log)
+    uint32_t* shadow = nullptr;     // tampered copy of a peer payload (fault injection)
+    // reduce_mul
+    std::vector<RedLevel> levels;
+    // linear
+    uint32_t *bias_v = nullptr, *bias_m = nullptr;
+    uint32_t *mA[2] = {nullptr, nullptr}, *mB[2] = {nullptr, nullptr}, *mC[2] = {nullptr, nullptr};
+    uint32_t* lin_tmp = nullptr;    // public x public scratch
+};
+
+struct LinTiles {
+    std::vector<uint32_t> starts, counts;
+    uint32_t rpt = 1;
+};
+
+struct Party {
+    spdz_ctx* ctx = nullptr;
+    std::vector<NodeState> ns;
+    uint32_t* pool[6] = {};         // scalar triples (views)
+    uint32_t *mask_v = nullptr, *mask_m = nullptr, *mask_c = nullptr;
+    uint32_t* outputs = nullptr;
+    std::vector<spdz_mac_segment_t> maclog;
+    std::vector<cudaEvent_t> evs;   // open-slot events
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+struct DeviceDeal {                 // one dealer output per device (all parties' shares)
+    uint32_t* pool[6] = {};
+    uint32_t *mask_v = nullptr, *mask_m = nullptr, *mask_c = nullptr;
+    std::map<uint32_t, std::array<uint32_t*, 6>> layer;  // linear node -> A.v A.m B.v B.m C.v C.m (party-major)
+    uint32_t* scratch = nullptr;    // matrix dealer cleartext scratch
+};
+
+}  // namespace
+
+struct KTimer {  // CUDA-event timing of kernel classes (profile_kernels)
+    struct Rec {
+        int cls;
+        int dev;
+        cudaEvent_t a, b;
+        uint64_t bytes;
+    };
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<Rec> recs;
+    cudaEvent_t take(int dev) {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cuda_check(cudaSetDevice(dev), "dev");
+            cuda_check(cudaEventCreate(&e), "event");
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+};
+
+struct spdz_run {
+    KTimer kt;
+    std::vector<spdz_node_t> nodes;
+    uint32_t root = 0;
+    int n = 2;
+    spdz_run_options_t opts{};
+    std::vector<Party> parties;
+    std::vector<int> devices;
+    std::map<int, DeviceDeal> deals;
+    std::map<uint32_t, Region> scalar, matrix;
+    std::map<uint32_t, LinTiles> tiles;
+    uint64_t scalar_total = 0, matrix_total = 0, mask_total = 0;
+    std::vector<std::pair<uint32_t, uint32_t>> mshapes;  // (din, rows) per matrix triple (demand order)
+    std::map<uint32_t, uint64_t> input_mask_off;          // private input node -> first mask
+    std::map<uint32_t, std::vector<uint32_t>> inputs;     // cleartext (host)
+    std::map<uint32_t, uint32_t*> input_dev;              // cleartext staged on party 0's device
+    std::vector<void*> allocs;                            // (device, ptr)
+    std::vector<int> alloc_dev;
+    std::vector<Fault> faults;
+    bool consumed = false;
+    uint64_t dealer_seed = 1;
+    std::vector<uint32_t> host_out;
+    uint64_t exchanged = 0;
+    cudaEvent_t ev_input = nullptr;
+
+    uint32_t* alloc(int party, uint64_t words) {
+        const int dev = devices[party];
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, std::max<uint64_t>(words, 1) * 4), "cudaMalloc(run)");
+        allocs.push_back(p);
+        alloc_dev.push_back(dev);
+        return (uint32_t*)p;
+    }
+    uint32_t* alloc_dev_words(int dev, uint64_t words) {
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, std::max<uint64_t>(words, 1) * 4), "cudaMalloc(deal)");
+        allocs.push_back(p);
+        alloc_dev.push_back(dev);
+        return (uint32_t*)p;
+    }
+    const spdz_node_t& node(uint32_t id) const { return nodes.at(id); }
+    bool priv(uint32_t id) const { return nodes.at(id).is_private != 0; }
+};
+
+namespace {
+
+cudaStream_t S(spdz_run* r, int p) { return r->parties[p].ctx->stream; }
+int SMS(spdz_run* r, int p) { return r->parties[p].ctx->sms; }
+void dev(spdz_run* r, int p) { device_guard(r->parties[p].ctx); }
+
+cudaEvent_t new_event(spdz_run* r, int p) {
+    dev(r, p);
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    r->parties[p].evs.push_back(e);
+    return e;
+}
+
+// ---- planning (run creation) ----
+void plan_layout(spdz_run* r) {
+    // preproc.cpp:84-163 for straight-line graphs (no loops: mult = 1)
+    for (auto& n : r->nodes) {
+        const uint32_t id = (uint32_t)(&n - r->nodes.data());
+        switch (n.kind) {
+            case SPDZ_NODE_MUL:
+                if (r->priv(n.operands[0]) && r->priv(n.operands[1])) {
+                    r->scalar[id] = {r->scalar_total, n.lanes, 1};
+                    r->scalar_total += n.lanes;
+                }
+                break;
+            case SPDZ_NODE_REDUCE_MUL: {
+                const auto& src = r->node(n.operands[0]);
+                if (src.is_private && src.lanes >= 1) {
+                    r->scalar[id] = {r->scalar_total, src.lanes - 1ull, 1};
+                    r->scalar_total += src.lanes - 1ull;
+                }
+                break;
+            }
+            case SPDZ_NODE_LINEAR:
+                if (r->priv(n.operands[0]) && r->priv(n.operands[1])) {
+                    uint64_t nt = 0;
+                    LinTiles lt;
+                    lt.starts.resize(n.dout);
+                    lt.counts.resize(n.dout);
+                    int rc = spdz_plan_tiles(n.din, n.dout, r->opts.slice, lt.starts.data(), lt.counts.data(), n.dout,
+                                             &nt);
+                    if (rc) throw Error(rc, spdz_last_error());
+                    lt.starts.resize(nt);
+                    lt.counts.resize(nt);
+                    lt.rpt = lt.counts[0];
+                    r->matrix[id] = {r->matrix_total, nt, 1};
+                    r->matrix_total += nt;
+                    for (auto c : lt.counts) r->mshapes.emplace_back(n.din, c);
+                    r->tiles[id] = lt;
+                }
+                break;
+            default:
+                break;
+        }
+    }
+    for (uint32_t id = 0; id < r->nodes.size(); ++id) {  // preproc.cpp:119-121, g.inputs order
+        const auto& n = r->nodes[id];
+        if (n.kind == SPDZ_NODE_INPUT && n.is_private) {
+            r->input_mask_off[id] = r->mask_total;
+            r->mask_total += n.lanes;
+        }
+    }
+}
+
+uint32_t const_of(spdz_run* r, uint32_t id) {
+    const auto& n = r->node(id);
+    need(n.kind == SPDZ_NODE_CONST, SPDZ_ERR_INVALID_ARGUMENT, "load start must be a constant node");
+    return n.const_val;
+}
+
+// Allocates every device buffer of the online phase, per party.
+void plan_buffers(spdz_run* r) {
+    const uint32_t N = (uint32_t)r->nodes.size();
+    for (int p = 0; p < r->n; ++p) {
+        auto& P = r->parties[p];
+        P.ns.resize(N);
+        for (uint32_t id = 0; id < N; ++id) {
+            const auto& n = r->nodes[id];
+            auto& st = P.ns[id];
+            const uint64_t L = n.lanes;
+            auto priv_out = [&](uint64_t lanes) {
+                st.out.is_public = false;
+                st.out.lanes = lanes;
+                st.out.v = r->alloc(p, lanes);
+                st.out.m = r->alloc(p, lanes);
+            };
+            auto pub_out = [&](uint64_t lanes) {
+                st.out.is_public = true;
+                st.out.lanes = lanes;
+                st.out.pub = r->alloc(p, lanes);
+            };
+            auto opnd = [&](int k) -> const Val& { return P.ns[n.operands[k]].out; };
+            switch (n.kind) {
+                case SPDZ_NODE_INPUT:
+                    if (n.is_private) priv_out(L);
+                    else pub_out(L);
+                    break;
+                case SPDZ_NODE_CONST:
+                    pub_out(1);
+                    break;
+                case SPDZ_NODE_NOP:
+                    break;
+                case SPDZ_NODE_LOAD: {  // runtime.cpp:419-438 (zero-copy slice)
+                    const Val& base = opnd(0);
+                    const uint32_t start = const_of(r, n.operands[1]);
+                    need((uint64_t)start + L <= base.lanes, SPDZ_ERR_INVALID_ARGUMENT, "runtime: load out of bounds");
+                    st.out = base;
+                    st.out.lanes = L;
+                    if (base.is_public) st.out.pub = base.pub + start;
+                    else {
+                        st.out.v = base.v + start;
+                        st.out.m = base.m + start;
+                    }
+                    break;
+                }
+                case SPDZ_NODE_ADD:
+                case SPDZ_NODE_SUB:
+                    if (opnd(0).is_public && opnd(1).is_public) pub_out(L);
+                    else priv_out(L);
+                    break;
+                case SPDZ_NODE_MUL: {
+                    const Val &a = opnd(0), &b = opnd(1);
+                    if (a.is_public && b.is_public) {
+                        pub_out(L);
+                    } else if (!a.is_public && !b.is_public) {
+                        priv_out(L);
+                        st.xa = a;
+                        st.xb = b;
+                        if (a.lanes != L) st.xa = Val{false, nullptr, r->alloc(p, L), r->alloc(p, L), L};
+                        if (b.lanes != L) st.xb = Val{false, nullptr, r->alloc(p, L), r->alloc(p, L), L};
+                        st.payload = r->alloc(p, 2 * L);
+                        st.opened = r->alloc(p, 2 * L);
+                    } else {
+                        priv_out(L);
+                    }
+                    break;
+                }
+                case SPDZ_NODE_REDUCE_ADD:
+                    if (opnd(0).is_public) pub_out(1);
+                    else priv_out(1);
+                    break;
+                case SPDZ_NODE_REDUCE_MUL: {
+                    const Val& a = opnd(0);
+                    if (a.is_public) {
+                        pub_out(1);
+                        st.opened = r->alloc(p, std::max<uint64_t>(a.lanes, 1));  // scratch tree
+                        break;
+                    }
+                    uint64_t cur = a.lanes;
+                    while (cur > 1) {
+                        RedLevel lv;
+                        lv.in_lanes = cur;
+                        lv.pairs = cur / 2;
+                        lv.xv = r->alloc(p, lv.pairs);
+                        lv.xm = r->alloc(p, lv.pairs);
+                        lv.yv = r->alloc(p, lv.pairs);
+                        lv.ym = r->alloc(p, lv.pairs);
+                        lv.payload = r->alloc(p, 2 * lv.pairs);
+                        lv.opened = r->alloc(p, 2 * lv.pairs);
+                        lv.out_lanes = lv.pairs + (cur & 1);
+                        lv.zv = r->alloc(p, lv.out_lanes);
+                        lv.zm = r->alloc(p, lv.out_lanes);
+                        st.levels.push_back(lv);
+                        cur = lv.out_lanes;
+                    }
+                    if (st.levels.empty()) {
+                        priv_out(1);
+                    } else {
+                        st.out = Val{false, nullptr, st.levels.back().zv, st.levels.back().zm, 1};
+                    }
+                    break;
+                }
+                case SPDZ_NODE_LINEAR: {
+                    const Val &x = opnd(0), &w = opnd(1);
+                    need(x.lanes == n.din && w.lanes == (uint64_t)n.din * n.dout, SPDZ_ERR_INVALID_ARGUMENT,
+                         "ShapeMismatch: linear operands do not match din/dout");
+                    if (x.is_public && w.is_public) {
+                        pub_out(n.dout);
+                        st.lin_tmp = r->alloc(p, n.dout);
+                    } else if (x.is_public != w.is_public) {
+                        priv_out(n.dout);
+                        st.lin_tmp = r->alloc(p, 2ull * n.dout);
+                    } else {
+                        priv_out(n.dout);
+                        const auto& lt = r->tiles[id];
+                        const uint64_t cells = (uint64_t)n.din * n.dout, etot = (uint64_t)n.din * lt.starts.size();
+                        st.payload = r->alloc(p, cells + etot);
+                        st.opened = r->alloc(p, cells + etot);
+                        st.bias_v = r->alloc(p, n.dout);
+                        st.bias_m = r->alloc(p, n.dout);
+                        st.lin_tmp = r->alloc(p, 2ull * n.dout);
+                    }
+                    break;
+                }
+                case SPDZ_NODE_ROOT:
+                    st.out = opnd(0);
+                    break;
+                default:
+                    throw Error(SPDZ_ERR_INVALID_ARGUMENT, "runtime: unexpected node kind " + std::to_string(n.kind));
+            }
+        }
+        const Val& rv = P.ns[r->root].out;
+        P.outputs = r->alloc(p, std::max<uint64_t>(rv.lanes, 1));
+        cuda_check(cudaSetDevice(P.ctx->device), "dev");
+        cuda_check(cudaEventCreate(&P.t0), "ev");
+        cuda_check(cudaEventCreate(&P.t1), "ev");
+    }
+    // one open event per (party, node) plus reduce levels
+    for (int p = 0; p < r->n; ++p) {
+        size_t need_ev = r->nodes.size() + 1;
+        for (auto& st : r->parties[p].ns) need_ev += st.levels.size();
+        for (size_t k = 0; k < need_ev; ++k) new_event(r, p);
+    }
+    dev(r, 0);
+    cuda_check(cudaEventCreateWithFlags(&r->ev_input, cudaEventDisableTiming), "event");
+}
+
+// ---- preprocessing: GPU dealer in make_dealer_stores order (triple_store.cpp:248-287) ----
+void deal(spdz_run* r, uint64_t seed) {
+    const int n = r->n;
+    uint32_t alpha_sh[SPDZ_MAX_PARTIES], alpha;
+    dealer_alpha(n, seed, alpha_sh, &alpha);
+    for (int p = 0; p < n; ++p) r->parties[p].ctx->alpha = alpha_sh[p];
+    const uint64_t S = r->scalar_total, M = r->mask_total;
+    for (auto& [device, dd] : r->deals) {
+        int p0 = -1;
+        for (int p = 0; p < n; ++p)
+            if (r->devices[p] == device) { p0 = p; break; }
+        spdz_ctx* ctx = r->parties[p0].ctx;
+        device_guard(ctx);
+        cuda_check(cudaMemsetAsync(ctx->d_flag, 0, 4, ctx->stream), "memset flag");
+        uint64_t k = n;  // Dealer ctor consumed n draws (spdz.cpp:162-173)
+        lk(launch_dealer_triples(ctx->stream, n, seed, k, alpha, S, dd.pool, ctx->d_flag, ctx->sms), "deal triples");
+        k += dealer_draws_triples(n, S);
+        // matrix triples in demand order: linear nodes by id, tiles in order
+        for (auto& [id, reg] : r->matrix) {
+            const auto& nd = r->node(id);
+            const auto& lt = r->tiles[id];
+            auto& pl = dd.layer[id];
+            const uint64_t cells_all = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * lt.starts.size();
+            for (size_t t = 0; t < lt.starts.size(); ++t) {
+                const uint32_t rows = lt.counts[t];
+                const uint64_t cells = (uint64_t)nd.din * rows;
+                uint32_t* A = dd.scratch;
+                uint32_t* B = A + cells;
+                uint32_t* Cc = B + nd.din;
+                lk(launch_dealer_uniform(ctx->stream, seed, k, cells, 1, A, ctx->d_flag, ctx->sms), "deal A");
+                k += cells;
+                lk(launch_dealer_uniform(ctx->stream, seed, k, nd.din, 1, B, ctx->d_flag, ctx->sms), "deal B");
+                k += nd.din;
+                lk(launch_dealer_matvec(ctx->stream, A, B, nd.din, rows, Cc), "deal C");
+                const uint64_t aoff = (uint64_t)lt.starts[t] * nd.din;
+                lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, A, cells, pl[0] + aoff, pl[1] + aoff, cells_all,
+                                       ctx->d_flag, ctx->sms),
+                   "share A");
+                k += dealer_draws_share(n, cells);
+                const uint64_t boff = (uint64_t)t * nd.din;
+                lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, B, nd.din, pl[2] + boff, pl[3] + boff, etot,
+                                       ctx->d_flag, ctx->sms),
+                   "share B");
+                k += dealer_draws_share(n, nd.din);
+                lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, Cc, rows, pl[4] + lt.starts[t],
+                                       pl[5] + lt.starts[t], nd.dout, ctx->d_flag, ctx->sms),
+                   "share C");
+                k += dealer_draws_share(n, rows);
+                (void)reg;
+            }
+        }
+        lk(launch_dealer_masks(ctx->stream, n, seed, k, alpha, M, dd.mask_v, dd.mask_m, dd.mask_c, ctx->d_flag,
+                               ctx->sms),
+           "deal masks");
+        check_dealer_flag(ctx);
+    }
+    r->consumed = false;
+    r->dealer_seed = seed;
+}
+
+void alloc_deals(spdz_run* r) {
+    const int n = r->n;
+    const uint64_t S = r->scalar_total, M = r->mask_total;
+    uint64_t scratch = 1;
+    for (auto& [id, reg] : r->matrix) {
+        const auto& nd = r->node(id);
+        for (auto c : r->tiles[id].counts) scratch = std::max<uint64_t>(scratch, (uint64_t)nd.din * c + nd.din + c);
+    }
+    for (int p = 0; p < n; ++p) {
+        const int d = r->devices[p];
+        if (r->deals.count(d)) continue;
+        DeviceDeal dd;
+        for (int k = 0; k < 6; ++k) dd.pool[k] = r->alloc_dev_words(d, n * S);
+        dd.mask_v = r->alloc_dev_words(d, n * M);
+        dd.mask_m = r->alloc_dev_words(d, n * M);
+        dd.mask_c = r->alloc_dev_words(d, M);
+        for (auto& [id, reg] : r->matrix) {
+            const auto& nd = r->node(id);
+            const uint64_t cells = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * r->tiles[id].starts.size();
+            std::array<uint32_t*, 6> pl;
+            pl[0] = r->alloc_dev_words(d, n * cells);
+            pl[1] = r->alloc_dev_words(d, n * cells);
+            pl[2] = r->alloc_dev_words(d, n * etot);
+            pl[3] = r->alloc_dev_words(d, n * etot);
+            pl[4] = r->alloc_dev_words(d, n * (uint64_t)nd.dout);
+            pl[5] = r->alloc_dev_words(d, n * (uint64_t)nd.dout);
+            dd.layer[id] = pl;
+        }
+        dd.scratch = r->alloc_dev_words(d, scratch);
+        r->deals[d] = dd;
+    }
+    for (int p = 0; p < n; ++p) {  // per-party views (party-major planes)
+        auto& P = r->parties[p];
+        auto& dd = r->deals[r->devices[p]];
+        for (int k = 0; k < 6; ++k) P.pool[k] = dd.pool[k] + p * S;
+        P.mask_v = dd.mask_v + p * M;
+        P.mask_m = dd.mask_m + p * M;
+        P.mask_c = dd.mask_c;
+        for (auto& [id, reg] : r->matrix) {
+            const auto& nd = r->node(id);
+            const uint64_t cells = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * r->tiles[id].starts.size();
+            auto& pl = dd.layer[id];
+            auto& st = P.ns[id];
+            st.mA[0] = pl[0] + p * cells;
+            st.mA[1] = pl[1] + p * cells;
+            st.mB[0] = pl[2] + p * etot;
+            st.mB[1] = pl[3] + p * etot;
+            st.mC[0] = pl[4] + p * (uint64_t)nd.dout;
+            st.mC[1] = pl[5] + p * (uint64_t)nd.dout;
+        }
+    }
+}
+
+// ---- node execution (runtime.cpp:360-450) ----
+struct Exec {
+    spdz_run* r;
+    int ev_cursor[SPDZ_MAX_PARTIES] = {};
+
+    // kernel-class timing brackets on party p's stream
+    int tbegin(int p) {
+        if (!r->opts.profile_kernels) return -1;
+        cudaEvent_t a = r->kt.take(r->devices[p]);
+        dev(r, p);
+        lk(cudaEventRecord(a, S(r, p)), "record");
+        r->kt.recs.push_back({-1, r->devices[p], a, nullptr, 0});
+        return (int)r->kt.recs.size() - 1;
+    }
+    void tend(int p, int idx, int cls, uint64_t bytes) {
+        if (idx < 0) return;
+        cudaEvent_t b = r->kt.take(r->devices[p]);
+        lk(cudaEventRecord(b, S(r, p)), "record");
+        auto& rec = r->kt.recs[idx];
+        rec.cls = cls;
+        rec.b = b;
+        rec.bytes = bytes;
+    }
+
+    cudaEvent_t next_event(int p) { return r->parties[p].evs.at(ev_cursor[p]++); }
+
+    // bcast_share(s, lanes) into dst (runtime.cpp:41-47) when lanes differ
+    void bcast_into(int p, const Val& s, const Val& dst) {
+        if (s.v == dst.v) return;
+        lk(launch_bcast(S(r, p), s.v, s.m, dst.v, dst.m, dst.lanes, SMS(r, p)), "bcast");
+    }
+
+    // runtime.cpp:129-162
+    void add(int p, uint32_t id, bool sub) {
+        auto& P = r->parties[p];
+        const auto& n = r->node(id);
+        const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
+        Val& o = P.ns[id].out;
+        const uint64_t L = n.lanes;
+        spdz_ctx* c = P.ctx;
+        if (a.is_public && b.is_public) {
+            lk(launch_pub_binop(c->stream, sub ? 1 : 0, a.pub, a.lanes != L, b.pub, b.lanes != L, o.pub, L, c->sms),
+               "pub add");
+            return;
+        }
+        if (!a.is_public && !b.is_public) {
+            need(a.lanes == L || a.lanes == 1, SPDZ_ERR_LANE_MISMATCH, "LaneMismatch: add operand");
+            need(b.lanes == L || b.lanes == 1, SPDZ_ERR_LANE_MISMATCH, "LaneMismatch: add operand");
+            if (a.lanes != L && b.lanes != L) {  // both broadcast scalars: z[0] = a op b, then bcast
+                lk(launch_add_sub(c->stream, sub, a.v, a.m, b.v, b.m, o.v, o.m, 1, c->sms), "add 1");
+                if (L > 1) lk(launch_bcast(c->stream, o.v, o.m, o.v + 1, o.m + 1, L - 1, c->sms), "bcast");
+                return;
+            }
+            const uint32_t *av = a.v, *am = a.m, *bv = b.v, *bm = b.m;
+            if (a.lanes != L) {  // bcast_share(a) into the output, then z = z op b in place
+                bcast_into(p, a, o);
+                av = o.v;
+                am = o.m;
+            } else if (b.lanes != L) {
+                bcast_into(p, b, o);
+                bv = o.v;
+                bm = o.m;
+            }
+            lk(launch_add_sub(c->stream, sub, av, am, bv, bm, o.v, o.m, L, c->sms), "add_batch");
+            return;
+        }
+        // share op public / public op share (runtime.cpp:145-161)
+        const bool a_priv = !a.is_public;
+        const Val& sh = a_priv ? a : b;
+        const Val& pb = a_priv ? b : a;
+        const int op = a_priv ? (sub ? 1 : 0) : (sub ? 2 : 0);
+        const uint32_t* iv = sh.v;
+        const uint32_t* im = sh.m;
+        if (sh.lanes != L) {
+            bcast_into(p, sh, o);
+            iv = o.v;
+            im = o.m;
+        }
+        lk(launch_public(c->stream, op, iv, im, pb.pub, pb.lanes != L, 0u, false, c->party, c->alpha, o.v, o.m, L,
+                         c->sms),
+           "public op");
+    }
+
+    // runtime.cpp:166-183
+    void mul_local(int p, uint32_t id) {
+        auto& P = r->parties[p];
+        const auto& n = r->node(id);
+        const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
+        Val& o = P.ns[id].out;
+        const uint64_t L = n.lanes;
+        spdz_ctx* c = P.ctx;
+        if (a.is_public && b.is_public) {
+            lk(launch_pub_binop(c->stream, 2, a.pub, a.lanes != L, b.pub, b.lanes != L, o.pub, L, c->sms), "pub mul");
+            return;
+        }
+        const Val& sh = a.is_public ? b : a;
+        const Val& pb = a.is_public ? a : b;
+        const uint32_t* iv = sh.v;
+        const uint32_t* im = sh.m;
+        if (sh.lanes != L) {
+            bcast_into(p, sh, o);
+            iv = o.v;
+            im = o.m;
+        }
+        lk(launch_public(c->stream, 3, iv, im, pb.pub, pb.lanes != L, 0u, false, c->party, c->alpha, o.v, o.m, L,
+                         c->sms),
+           "mul_public");
+    }
+
+    const uint32_t* peer_payload(int p, int q, uint32_t id, const uint32_t* src, uint64_t words, uint32_t* shadow) {
+        // SimHub BitFlip (net.cpp:241-278): the receiver p sees a tampered copy of q's frame.
+        for (auto& f : r->faults) {
+            if (f.node == id && f.sender == q && f.receiver == p && shadow) {
+                lk(cudaMemcpyAsync(shadow, src, words * 4, cudaMemcpyDefault, S(r, p)), "shadow copy");
+                lk(launch_xor_word(S(r, p), shadow + (f.word % words), 1u << (f.bit % 32)), "bitflip");
+                return shadow;
+            }
+        }
+        return src;
+    }
+
+    // Beaver multiply (runtime.cpp:204-239): mask -> open [d|e] -> combine, all parties.
+    void beaver(uint32_t id, const Region& reg, uint64_t exec) {
+        const auto& n = r->node(id);
+        const uint64_t L = n.lanes;
+        const uint64_t off = reg.base + exec * reg.stride;  // runtime.cpp:197
+        std::vector<cudaEvent_t> sent(r->n);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            auto& st = P.ns[id];
+            const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
+            dev(r, p);
+            if (a.lanes != L) bcast_into(p, a, st.xa);
+            if (b.lanes != L) bcast_into(p, b, st.xb);
+            const int tk = tbegin(p);
+            lk(launch_mul_mask(S(r, p), st.xa.v, st.xb.v, P.pool[0] + off, P.pool[2] + off, st.payload,
+                               st.payload + L, L, SMS(r, p)),
+               "k_mul_mask");
+            tend(p, tk, SPDZ_KSTAT_MASK, 24 * L);
+            sent[p] = next_event(p);
+            lk(cudaEventRecord(sent[p], S(r, p)), "record");
+        }
+        const uint64_t batch = make_batch(id, exec, 0);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            auto& st = P.ns[id];
+            dev(r, p);
+            const uint32_t* pd[kMaxPeers];
+            const uint32_t* pe[kMaxPeers];
+            int k = 0;
+            for (int q = 0; q < r->n; ++q) {
+                if (q == p) continue;
+                lk(cudaStreamWaitEvent(S(r, p), sent[q], 0), "wait peer");
+                const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, 2 * L, st.shadow);
+                pd[k] = src;
+                pe[k] = src + L;
+                ++k;
+                r->exchanged += 2 * L * 4;
+            }
+            const uint32_t* tri[6];
+            for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
+            const int tk = tbegin(p);
+            lk(launch_beaver_combine(S(r, p), st.payload, st.payload + L, pd, pe, k, tri, P.ctx->party, P.ctx->alpha,
+                                     st.out.v, st.out.m, st.opened, st.opened + L, L, SMS(r, p)),
+               "k_combine");
+            // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
+            tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
+            // log_open (runtime.cpp:224): records [d | e] with mac shares [x.m - a.m | y.m - b.m]
+            P.maclog.push_back({st.opened, st.xa.m, P.pool[1] + off, L, 0, batch, 0});
+            P.maclog.push_back({st.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, L});
+        }
+    }
+
+    // runtime.cpp:242-281
+    void reduce_mul(uint32_t id, const Region& reg, uint64_t exec) {
+        const auto& n = r->node(id);
+        const size_t nlev = r->parties[0].ns[id].levels.size();
+        if (nlev == 0) {  // single lane: value passes through
+            for (int p = 0; p < r->n; ++p) {
+                auto& P = r->parties[p];
+                const Val& a = P.ns[n.operands[0]].out;
+                auto& o = P.ns[id].out;
+                dev(r, p);
+                lk(cudaMemcpyAsync(o.v, a.v, 4, cudaMemcpyDeviceToDevice, S(r, p)), "copy");
+                lk(cudaMemcpyAsync(o.m, a.m, 4, cudaMemcpyDeviceToDevice, S(r, p)), "copy");
+            }
+            return;
+        }
+        uint64_t used = 0, sub = 1;
+        for (size_t li = 0; li < nlev; ++li) {
+            std::vector<cudaEvent_t> sent(r->n);
+            const uint64_t off = reg.base + exec * reg.stride + used;
+            const uint64_t pairs = r->parties[0].ns[id].levels[li].pairs;
+            for (int p = 0; p < r->n; ++p) {
+                auto& P = r->parties[p];
+                auto& lv = P.ns[id].levels[li];
+                const uint32_t* cv = li == 0 ? P.ns[n.operands[0]].out.v : P.ns[id].levels[li - 1].zv;
+                const uint32_t* cm = li == 0 ? P.ns[n.operands[0]].out.m : P.ns[id].levels[li - 1].zm;
+                dev(r, p);
+                lk(launch_pair_split(S(r, p), cv, cm, pairs, lv.xv, lv.xm, lv.yv, lv.ym, SMS(r, p)), "pair split");
+                if (lv.in_lanes & 1) {  // odd element passes through (runtime.cpp:274-277)
+                    lk(cudaMemcpyAsync(lv.zv + pairs, cv + lv.in_lanes - 1, 4, cudaMemcpyDeviceToDevice, S(r, p)), "odd");
+                    lk(cudaMemcpyAsync(lv.zm + pairs, cm + lv.in_lanes - 1, 4, cudaMemcpyDeviceToDevice, S(r, p)), "odd");
+                }
+                lk(launch_mul_mask(S(r, p), lv.xv, lv.yv, P.pool[0] + off, P.pool[2] + off, lv.payload,
+                                   lv.payload + pairs, pairs, SMS(r, p)),
+                   "mask");
+                sent[p] = next_event(p);
+                lk(cudaEventRecord(sent[p], S(r, p)), "record");
+            }
+            const uint64_t batch = make_batch(id, exec, sub++);
+            for (int p = 0; p < r->n; ++p) {
+                auto& P = r->parties[p];
+                auto& lv = P.ns[id].levels[li];
+                dev(r, p);
+                const uint32_t* pd[kMaxPeers];
+                const uint32_t* pe[kMaxPeers];
+                int k = 0;
+                for (int q = 0; q < r->n; ++q) {
+                    if (q == p) continue;
+                    lk(cudaStreamWaitEvent(S(r, p), sent[q], 0), "wait");
+                    pd[k] = r->parties[q].ns[id].levels[li].payload;
+                    pe[k] = pd[k] + pairs;
+                    ++k;
+                    r->exchanged += 2 * pairs * 4;
+                }
+                const uint32_t* tri[6];
+                for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
+                lk(launch_beaver_combine(S(r, p), lv.payload, lv.payload + pairs, pd, pe, k, tri, P.ctx->party,
+                                         P.ctx->alpha, lv.zv, lv.zm, lv.opened, lv.opened + pairs, pairs, SMS(r, p)),
+                   "combine");
+                P.maclog.push_back({lv.opened, lv.xm, P.pool[1] + off, pairs, 0, batch, 0});
+                P.maclog.push_back({lv.opened + pairs, lv.ym, P.pool[3] + off, pairs, 0, batch, pairs});
+            }
+            used += pairs;
+        }
+    }
+
+    // runtime.cpp:283-358
+    void linear(uint32_t id, uint64_t exec) {
+        const auto& n = r->node(id);
+        const uint32_t din = n.din, dout = n.dout;
+        const bool xp = !r->parties[0].ns[n.operands[0]].out.is_public;
+        const bool wp = !r->parties[0].ns[n.operands[1]].out.is_public;
+        if (!xp || !wp) {
+            for (int p = 0; p < r->n; ++p) {
+                auto& P = r->parties[p];
+                auto& st = P.ns[id];
+                const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out, &b = P.ns[n.operands[2]].out;
+                spdz_ctx* c = P.ctx;
+                dev(r, p);
+                if (!xp && !wp) {  // public x public: y = W x, then exec_add(y, b)
+                    lk(launch_modgemm(c->stream, 1, dout, din, 1, w.pub, w.pub, x.pub, nullptr, st.lin_tmp,
+                                      st.out.pub),
+                       "modgemm");
+                    lk(launch_pub_binop(c->stream, 0, st.lin_tmp, false, b.pub, b.lanes != dout, st.out.pub, dout,
+                                        c->sms),
+                       "bias");
+                    continue;
+                }
+                uint32_t* yv = st.lin_tmp;
+                uint32_t* ym = st.lin_tmp + dout;
+                if (wp)  // x public, W secret: y.v = W.v x, y.m = W.m x
+                    lk(launch_modgemm(c->stream, 1, dout, din, 1, w.v, w.m, x.pub, nullptr, yv, ym), "modgemm");
+                else  // W public, x secret: y.v = W x.v, y.m = W x.m
+                    lk(launch_modgemm(c->stream, 0, dout, din, 1, w.pub, nullptr, x.v, x.m, yv, ym), "modgemm");
+                if (b.is_public)
+                    lk(launch_public(c->stream, 0, yv, ym, b.pub, b.lanes != dout, 0u, false, c->party, c->alpha,
+                                     st.out.v, st.out.m, dout, c->sms),
+                       "bias pub");
+                else if (b.lanes == dout)
+                    lk(launch_add_sub(c->stream, false, yv, ym, b.v, b.m, st.out.v, st.out.m, dout, c->sms), "bias");
+                else {
+                    lk(launch_bcast(c->stream, b.v, b.m, st.out.v, st.out.m, dout, c->sms), "bcast");
+                    lk(launch_add_sub(c->stream, false, yv, ym, st.out.v, st.out.m, st.out.v, st.out.m, dout, c->sms),
+                       "bias");
+                }
+            }
+            return;
+        }
+        // both private: matrix triples per tile (linear.cpp:75-130), all tiles batched per launch
+        const auto& reg = r->matrix.at(id);
+        const auto& lt = r->tiles.at(id);
+        (void)reg;
+        const uint64_t cells = (uint64_t)din * dout;
+        const uint32_t ntiles = (uint32_t)lt.starts.size();
+        const uint64_t etot = (uint64_t)din * ntiles;
+        const uint64_t batch0 = make_batch(id, exec, 0);
+        std::vector<cudaEvent_t> sent(r->n);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            auto& st = P.ns[id];
+            const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out, &b = P.ns[n.operands[2]].out;
+            spdz_ctx* c = P.ctx;
+            dev(r, p);
+            // bias shares bs (runtime.cpp:344-345)
+            if (b.is_public)
+                lk(launch_public(c->stream, 4, nullptr, nullptr, b.pub, b.lanes != dout, 0u, false, c->party, c->alpha,
+                                 st.bias_v, st.bias_m, dout, c->sms),
+                   "share_of_public");
+            else if (b.lanes == dout) {
+                lk(cudaMemcpyAsync(st.bias_v, b.v, dout * 4ull, cudaMemcpyDeviceToDevice, c->stream), "copy");
+                lk(cudaMemcpyAsync(st.bias_m, b.m, dout * 4ull, cudaMemcpyDeviceToDevice, c->stream), "copy");
+            } else
+                lk(launch_bcast(c->stream, b.v, b.m, st.bias_v, st.bias_m, dout, c->sms), "bcast");
+            // mask_tile for every tile: [D (all rows) | E_t for every tile]
+            lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
+            lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
+            sent[p] = next_event(p);
+            lk(cudaEventRecord(sent[p], c->stream), "record");
+        }
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            auto& st = P.ns[id];
+            const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out;
+            spdz_ctx* c = P.ctx;
+            dev(r, p);
+            const uint32_t* peers[kMaxPeers];
+            const uint32_t* peersE[kMaxPeers];
+            int k = 0;
+            for (int q = 0; q < r->n; ++q) {
+                if (q == p) continue;
+                lk(cudaStreamWaitEvent(c->stream, sent[q], 0), "wait");
+                const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, cells + etot, st.shadow);
+                peers[k] = src;
+                peersE[k] = src + cells;
+                ++k;
+                r->exchanged += (cells + etot) * 4;
+            }
+            lk(launch_open_sum(c->stream, st.payload + cells, peersE, k, st.opened + cells, etot, c->sms), "open E");
+            const uint32_t* m6[6] = {st.mA[0], st.mA[1], st.mB[0], st.mB[1], st.mC[0], st.mC[1]};
+            lk(launch_matrix_combine(c->stream, din, dout, lt.rpt, st.payload, peers, k, m6, st.bias_v, st.bias_m,
+                                     c->party, c->alpha, st.out.v, st.out.m, st.opened, c->sms),
+               "k_matrix_combine");
+            for (uint32_t t = 0; t < ntiles; ++t) {  // linear.cpp:113 log per tile: [D_t | E_t]
+                const uint64_t aoff = (uint64_t)lt.starts[t] * din, ct = (uint64_t)lt.counts[t] * din;
+                P.maclog.push_back({st.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0});
+                P.maclog.push_back({st.opened + cells + (uint64_t)t * din, x.m, st.mB[1] + (uint64_t)t * din, din, 0,
+                                    batch0 + t, ct});
+            }
+        }
+    }
+
+    void reduce_add(int p, uint32_t id) {
+        auto& P = r->parties[p];
+        const auto& n = r->node(id);
+        const Val& a = P.ns[n.operands[0]].out;
+        Val& o = P.ns[id].out;
+        spdz_ctx* c = P.ctx;
+        lk(cudaMemsetAsync(c->d_acc + 2, 0, 16, c->stream), "memset");
+        if (a.is_public) {
+            lk(launch_reduce_add(c->stream, a.pub, a.pub, a.lanes, c->d_acc + 2, c->sms), "reduce");
+            lk(launch_finish_reduce(c->stream, c->d_acc + 2, o.pub, o.pub), "finish");
+        } else {
+            lk(launch_reduce_add(c->stream, a.v, a.m, a.lanes, c->d_acc + 2, c->sms), "reduce");
+            lk(launch_finish_reduce(c->stream, c->d_acc + 2, o.v, o.m), "finish");
+        }
+    }
+
+    void reduce_mul_public(int p, uint32_t id) {
+        auto& P = r->parties[p];
+        const auto& n = r->node(id);
+        const Val& a = P.ns[n.operands[0]].out;
+        auto& st = P.ns[id];
+        spdz_ctx* c = P.ctx;
+        uint64_t len = a.lanes;
+        lk(cudaMemcpyAsync(st.opened, a.pub, len * 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
+        while (len > 1) {  // product is order-free: fold halves
+            const uint64_t half = len / 2;
+            lk(launch_pub_binop(c->stream, 2, st.opened, false, st.opened + (len - half), false, st.opened, half,
+                                c->sms),
+               "pub fold");
+            len -= half;
+        }
+        lk(cudaMemcpyAsync(st.out.pub, st.opened, 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
+    }
+
+    void run_nodes() {
+        for (uint32_t id = 0; id < r->nodes.size(); ++id) {
+            const auto& n = r->nodes[id];
+            switch (n.kind) {
+                case SPDZ_NODE_INPUT:
+                case SPDZ_NODE_CONST:
+                case SPDZ_NODE_NOP:
+                case SPDZ_NODE_LOAD:
+                case SPDZ_NODE_ROOT:
+                    break;
+                case SPDZ_NODE_ADD:
+                case SPDZ_NODE_SUB:
+                    for (int p = 0; p < r->n; ++p) {
+                        dev(r, p);
+                        add(p, id, n.kind == SPDZ_NODE_SUB);
+                    }
+                    break;
+                case SPDZ_NODE_MUL: {
+                    const bool a = r->parties[0].ns[n.operands[0]].out.is_public;
+                    const bool b = r->parties[0].ns[n.operands[1]].out.is_public;
+                    if (!a && !b) beaver(id, r->scalar.at(id), 0);
+                    else
+                        for (int p = 0; p < r->n; ++p) {
+                            dev(r, p);
+                            mul_local(p, id);
+                        }
+                    break;
+                }
+                case SPDZ_NODE_REDUCE_ADD:
+                    for (int p = 0; p < r->n; ++p) {
+                        dev(r, p);
+                        reduce_add(p, id);
+                    }
+                    break;
+                case SPDZ_NODE_REDUCE_MUL:
+                    if (r->parties[0].ns[n.operands[0]].out.is_public)
+                        for (int p = 0; p < r->n; ++p) {
+                            dev(r, p);
+                            reduce_mul_public(p, id);
+                        }
+                    else
+                        reduce_mul(id, r->scalar.at(id), 0);
+                    break;
+                case SPDZ_NODE_LINEAR:
+                    linear(id, 0);
+                    break;
+                default:
+                    throw Error(SPDZ_ERR_INVALID_ARGUMENT, "runtime: unexpected node kind");
+            }
+        }
+    }
+
+    // runtime.cpp:551-560 open the root (batch make_batch(root, 1, 1))
+    void open_root() {
+        const Val& rv0 = r->parties[0].ns[r->root].out;
+        const uint64_t L = rv0.lanes;
+        if (rv0.is_public) {
+            for (int p = 0; p < r->n; ++p) {
+                dev(r, p);
+                lk(cudaMemcpyAsync(r->parties[p].outputs, r->parties[p].ns[r->root].out.pub, L * 4,
+                                   cudaMemcpyDeviceToDevice, S(r, p)),
+                   "copy out");
+            }
+            return;
+        }
+        std::vector<cudaEvent_t> ready(r->n);
+        for (int p = 0; p < r->n; ++p) {
+            dev(r, p);
+            ready[p] = next_event(p);
+            lk(cudaEventRecord(ready[p], S(r, p)), "record");
+        }
+        const uint64_t batch = make_batch(r->root, 1, 1);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            const Val& rv = P.ns[r->root].out;
+            dev(r, p);
+            const uint32_t* peers[kMaxPeers];
+            int k = 0;
+            for (int q = 0; q < r->n; ++q) {
+                if (q == p) continue;
+                lk(cudaStreamWaitEvent(S(r, p), ready[q], 0), "wait");
+                peers[k++] = r->parties[q].ns[r->root].out.v;
+                r->exchanged += L * 4;
+            }
+            const int tk = tbegin(p);
+            lk(launch_open_sum(S(r, p), rv.v, peers, k, P.outputs, L, SMS(r, p)), "open root");
+            tend(p, tk, SPDZ_KSTAT_OPEN, (8ull + 4ull * k) * L);
+            P.maclog.push_back({P.outputs, rv.m, nullptr, L, 0, batch, 0});
+        }
+    }
+};
+
+uint64_t fresh_nonce() {
+    static thread_local std::mt19937_64 rng(std::random_device{}());
+    return rng();
+}
+
+// runtime.cpp:467-506
+void mac_check(spdz_run* r, spdz_run_report_t* rep, Exec& ex) {
+    const int n = r->n;
+    uint64_t coin = 0;
+    if (r->opts.fixed_coin) {
+        coin = r->opts.coin;
+    } else {  // commit to nonces, reveal, chain fnv1a64 (runtime.cpp:474-489)
+        std::vector<uint64_t> nonce(n), commit(n);
+        for (int p = 0; p < n; ++p) {
+            nonce[p] = fresh_nonce();
+            commit[p] = spdz_fnv1a64(&nonce[p], 8, 1469598103934665603ull);
+        }
+        for (int p = 0; p < n; ++p) {
+            if (spdz_fnv1a64(&nonce[p], 8, 1469598103934665603ull) != commit[p])
+                throw Error(SPDZ_ERR_MAC_CHECK_FAILED, "MacCheckFailed: coin commitment mismatch");
+            coin = spdz_fnv1a64(&nonce[p], 8, coin);
+        }
+    }
+    for (int p = 0; p < n; ++p) {
+        auto& P = r->parties[p];
+        dev(r, p);
+        assign_ranks(P.maclog.data(), P.maclog.size());
+        uint64_t sbytes = 0;
+        for (auto& sg : P.maclog) sbytes += sg.len * (sg.mac_b ? 12 : 8);
+        const int tk = ex.tbegin(p);
+        mac_sigma_launch(P.ctx, P.maclog.data(), P.maclog.size(), coin, 0);
+        ex.tend(p, tk, SPDZ_KSTAT_SIGMA, sbytes);
+        lk(cudaEventRecord(P.t1, P.ctx->stream), "t1");
+    }
+    std::vector<uint32_t> sig(n);
+    std::vector<uint64_t> nonce2(n), commits(n);
+    for (int p = 0; p < n; ++p) {
+        dev(r, p);
+        sig[p] = mac_sigma_collect(r->parties[p].ctx, 0);
+        nonce2[p] = fresh_nonce();
+        commits[p] = spdz_commit_sigma(sig[p], nonce2[p]);
+        if (rep) rep->sigmas[p] = sig[p];
+    }
+    if (rep) rep->coin = coin;
+    int rc = spdz_verify_sigmas(sig.data(), nonce2.data(), commits.data(), n);
+    if (rc) throw Error(rc, spdz_last_error());
+}
+
+void share_inputs(spdz_run* r) {
+    // preproc.cpp:205-243: party 0 opens x - mask, everyone adds the public difference
+    for (auto& [id, off] : r->input_mask_off) {
+        const auto& n = r->node(id);
+        auto it = r->input_dev.find(id);
+        need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
+             "ShapeMismatch: no values bound for input node " + std::to_string(id));
+        uint32_t* x0 = it->second;  // cleartext on party 0's device (reduced in place)
+        auto& P0 = r->parties[0];
+        dev(r, 0);
+        lk(launch_pub_binop(P0.ctx->stream, 1, x0, false, P0.mask_c + off, false, x0, n.lanes, P0.ctx->sms),
+           "x - r");
+        cudaEvent_t ev = r->ev_input;
+        lk(cudaEventRecord(ev, P0.ctx->stream), "record");
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            auto& o = P.ns[id].out;
+            dev(r, p);
+            if (p) lk(cudaStreamWaitEvent(P.ctx->stream, ev, 0), "wait");
+            lk(launch_public(P.ctx->stream, 0, P.mask_v + off, P.mask_m + off, x0, false, 0u, false, p, P.ctx->alpha,
+                             o.v, o.m, n.lanes, P.ctx->sms),
+               "add_public(diff)");
+        }
+        for (int p = 0; p < r->n; ++p) {
+            dev(r, p);
+            lk(cudaStreamSynchronize(S(r, p)), "sync");
+        }
+    }
+    for (uint32_t id = 0; id < r->nodes.size(); ++id) {  // public inputs and constants
+        const auto& n = r->nodes[id];
+        if (n.kind == SPDZ_NODE_INPUT && !n.is_private) {
+            auto it = r->inputs.find(id);
+            need(it != r->inputs.end(), SPDZ_ERR_INVALID_ARGUMENT,
+                 "ShapeMismatch: missing public input " + std::to_string(id));
+            std::vector<uint32_t> red(it->second.size());
+            for (size_t i = 0; i < red.size(); ++i) red[i] = it->second[i] % kP;
+            for (int p = 0; p < r->n; ++p) {
+                dev(r, p);
+                lk(cudaMemcpy(r->parties[p].ns[id].out.pub, red.data(), red.size() * 4, cudaMemcpyHostToDevice),
+                   "H2D pub");
+            }
+        }
+        if (n.kind == SPDZ_NODE_CONST) {
+            const uint32_t v = n.const_val % kP;
+            for (int p = 0; p < r->n; ++p) {
+                dev(r, p);
+                lk(cudaMemcpy(r->parties[p].ns[id].out.pub, &v, 4, cudaMemcpyHostToDevice), "H2D const");
+            }
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
+                    const spdz_run_options_t* opts, spdz_run** out) {
+    return guard([&] {
+        need(nodes && n_nodes > 0 && out, SPDZ_ERR_INVALID_ARGUMENT, "bad run arguments");
+        need(root < n_nodes, SPDZ_ERR_INVALID_ARGUMENT, "root out of range");
+        need(n_parties >= 1 && n_parties <= SPDZ_MAX_PARTIES, SPDZ_ERR_INVALID_ARGUMENT, "n_parties out of range");
+        auto r = std::make_unique<spdz_run>();
+        r->nodes.assign(nodes, nodes + n_nodes);
+        r->root = root;
+        r->n = n_parties;
+        if (opts) r->opts = *opts;
+        if (r->opts.slice == 0) r->opts.slice = 262140;
+        if (r->opts.dealer_seed == 0 && !opts) r->opts.dealer_seed = 1;
+        for (uint32_t id = 0; id < n_nodes; ++id)
+            for (uint32_t k = 0; k < nodes[id].n_operands; ++k)
+                need(nodes[id].operands[k] < id, SPDZ_ERR_INVALID_ARGUMENT,
+                     "graph must be topologically ordered (operand id < node id)");
+        r->devices.resize(n_parties);
+        for (int p = 0; p < n_parties; ++p) r->devices[p] = (opts && opts->devices[p] >= 0) ? opts->devices[p] : 0;
+        r->parties.resize(n_parties);
+        for (int p = 0; p < n_parties; ++p) {
+            int rc = spdz_ctx_create(r->devices[p], p, n_parties, 0, &r->parties[p].ctx);
+            if (rc) throw Error(rc, spdz_last_error());
+        }
+        for (int p = 0; p < n_parties; ++p)  // P2P between party devices (NVLink)
+            for (int q = 0; q < n_parties; ++q) {
+                if (r->devices[p] == r->devices[q]) continue;
+                cudaSetDevice(r->devices[p]);
+                cudaError_t e = cudaDeviceEnablePeerAccess(r->devices[q], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else cuda_check(e, "cudaDeviceEnablePeerAccess");
+            }
+        plan_layout(r.get());
+        plan_buffers(r.get());
+        alloc_deals(r.get());
+        deal(r.get(), r->opts.dealer_seed);
+        *out = r.release();
+    });
+}
+
+int spdz_run_destroy(spdz_run* r) {
+    return guard([&] {
+        if (!r) return;
+        for (auto& P : r->parties) {
+            if (!P.ctx) continue;
+            cudaSetDevice(P.ctx->device);
+            cudaStreamSynchronize(P.ctx->stream);
+            for (auto e : P.evs) cudaEventDestroy(e);
+            if (P.t0) cudaEventDestroy(P.t0);
+            if (P.t1) cudaEventDestroy(P.t1);
+        }
+        if (r->ev_input) {
+            cudaSetDevice(r->devices[0]);
+            cudaEventDestroy(r->ev_input);
+        }
+        for (auto e : r->kt.pool) cudaEventDestroy(e);
+        for (size_t i = 0; i < r->allocs.size(); ++i) {
+            cudaSetDevice(r->alloc_dev[i]);
+            cudaFree(r->allocs[i]);
+        }
+        for (auto& P : r->parties) spdz_ctx_destroy(P.ctx);
+        delete r;
+    });
+}
+
+int spdz_run_deal(spdz_run* r, uint64_t seed) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        deal(r, seed);
+    });
+}
+
+int spdz_run_bind_input(spdz_run* r, uint32_t node, const uint32_t* host_vals, uint64_t len) {
+    return guard([&] {
+        need(r && node < r->nodes.size(), SPDZ_ERR_INVALID_ARGUMENT, "bad input node");
+        const auto& n = r->node(node);
+        need(n.kind == SPDZ_NODE_INPUT, SPDZ_ERR_INVALID_ARGUMENT, "node is not an input");
+        need(len == n.lanes, SPDZ_ERR_INVALID_ARGUMENT,
+             "ShapeMismatch: input has " + std::to_string(len) + " elements, circuit expects " +
+                 std::to_string(n.lanes));
+        if (!n.is_private) {
+            r->inputs[node] = std::vector<uint32_t>(host_vals, host_vals + len);
+            return;
+        }
+        // party 0 owns every private input (preproc.cpp:146-150): stage on its device
+        auto it = r->input_dev.find(node);
+        uint32_t* d = it == r->input_dev.end() ? (r->input_dev[node] = r->alloc(0, len)) : it->second;
+        dev(r, 0);
+        auto& P0 = r->parties[0];
+        lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, P0.ctx->stream), "H2D input");
+        // reduce mod p (preproc.cpp:149 fp::reduce): x * 1 mod p
+        lk(launch_public(P0.ctx->stream, 3, d, d, nullptr, false, 1u, true, 0, 0, d, d, len, P0.ctx->sms),
+           "reduce input");
+    });
+}
+
+int spdz_run_share_inputs(spdz_run* r) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        share_inputs(r);
+    });
+}
+
+int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        if (r->consumed && !reuse)
+            throw Error(SPDZ_ERR_TRIPLE_EXHAUSTED,
+                        "TripleExhausted: preprocessing of this run was already consumed (deal again)");
+        const uint64_t launches0 = g_kernel_launches;
+        r->exchanged = 0;
+        auto t0 = std::chrono::steady_clock::now();
+        for (auto& P : r->parties) {
+            P.maclog.clear();
+            device_guard(P.ctx);
+            lk(cudaEventRecord(P.t0, P.ctx->stream), "t0");
+        }
+        r->kt.used = 0;
+        r->kt.recs.clear();
+        Exec ex{r};
+        ex.run_nodes();
+        ex.open_root();
+        r->consumed = true;
+        mac_check(r, rep, ex);  // also records t1 and synchronises
+        // outputs to host (party 0; all parties hold the same opened values)
+        const Val& rv = r->parties[0].ns[r->root].out;
+        r->host_out.resize(rv.lanes);
+        dev(r, 0);
+        lk(cudaMemcpy(r->host_out.data(), r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost), "D2H out");
+        auto t1 = std::chrono::steady_clock::now();
+        if (rep) {
+            rep->online_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+            double dmax = 0;
+            for (auto& P : r->parties) {
+                device_guard(P.ctx);
+                float ms = 0;
+                lk(cudaEventElapsedTime(&ms, P.t0, P.t1), "elapsed");
+                dmax = std::max(dmax, (double)ms);
+            }
+            rep->online_device_ms = dmax;
+            rep->scalar_triples_consumed = r->scalar_total;
+            rep->matrix_triples_consumed = r->matrix_total;
+            rep->bytes_exchanged = r->exchanged;
+            rep->output_digest = spdz_fnv1a64(r->host_out.data(), r->host_out.size() * 4, 1469598103934665603ull);
+            rep->kernel_launches = g_kernel_launches - launches0;
+            for (int c = 0; c < SPDZ_KSTAT_N; ++c) rep->kstat[c] = spdz_kernel_stat_t{0, 0.0, 0};
+            for (auto& rec : r->kt.recs) {
+                if (rec.cls < 0 || !rec.b) continue;
+                cuda_check(cudaSetDevice(rec.dev), "dev");
+                float ms = 0;
+                lk(cudaEventSynchronize(rec.b), "sync ev");
+                lk(cudaEventElapsedTime(&ms, rec.a, rec.b), "elapsed");
+                rep->kstat[rec.cls].launches += 1;
+                rep->kstat[rec.cls].ms += ms;
+                rep->kstat[rec.cls].bytes += rec.bytes;
+            }
+        }
+    });
+}
+
+int spdz_run_outputs(spdz_run* r, uint32_t* host_out, uint64_t cap, uint64_t* len) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        if (len) *len = r->host_out.size();
+        if (host_out) std::memcpy(host_out, r->host_out.data(), std::min<uint64_t>(cap, r->host_out.size()) * 4);
+    });
+}
+
+int spdz_run_node_share(spdz_run* r, int party, uint32_t node, spdz_share_t* out) {
+    return guard([&] {
+        need(r && party >= 0 && party < r->n && node < r->nodes.size() && out, SPDZ_ERR_INVALID_ARGUMENT,
+             "bad node_share args");
+        const Val& v = r->parties[party].ns[node].out;
+        out->vals = v.is_public ? v.pub : v.v;
+        out->macs = v.is_public ? nullptr : v.m;
+        out->lanes = v.lanes;
+    });
+}
+
+int spdz_run_inject_bitflip(spdz_run* r, uint32_t node, int sender, int receiver, uint64_t word, uint32_t bit) {
+    return guard([&] {
+        need(r && node < r->nodes.size(), SPDZ_ERR_INVALID_ARGUMENT, "bad node");
+        need(sender >= 0 && sender < r->n && receiver >= 0 && receiver < r->n && sender != receiver,
+             SPDZ_ERR_INVALID_ARGUMENT, "bad sender/receiver");
+        auto& st = r->parties[receiver].ns[node];
+        need(st.payload != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "node has no opening to tamper with");
+        if (!st.shadow) {
+            const auto& n = r->node(node);
+            uint64_t words = 2ull * n.lanes;
+            if (n.kind == SPDZ_NODE_LINEAR)
+                words = (uint64_t)n.din * n.dout + (uint64_t)n.din * r->tiles[node].starts.size();
+            st.shadow = r->alloc(receiver, words);
+        }
+        r->faults.push_back({node, sender, receiver, word, bit});
+    });
+}
+
+}  // extern "C"

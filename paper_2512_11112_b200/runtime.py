@@ -1,0 +1,252 @@
+"""Local n-party online phase on B200 (runtime::run_local shape,
+/root/reference/proj/core/src/runtime.cpp:586-613).
+
+A ``Graph`` is the lowered straight-line circuit the reference's runtime
+executes (node kinds of runtime.cpp:360-450; ids in topological order, as
+``circuit::compile_graph`` finalises them).  ``LocalRun`` owns the device
+state of every party (C ABI ``spdz_run_*``): GPU-dealt preprocessing in
+``make_dealer_stores`` order, input sharing (preproc.cpp:205-243), node
+execution with Beaver openings fused into the combine kernels, root open and
+the deferred MAC check (runtime.cpp:467-506).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+INPUT, CONST, ADD, SUB, MUL, REDUCE_ADD, REDUCE_MUL, LINEAR, ROOT, LOAD, NOP = range(11)
+KIND_NAMES = {"Input": INPUT, "Const": CONST, "Adder": ADD, "AddBatch": ADD, "Subtract": SUB, "SubBatch": SUB,
+              "Multiplier": MUL, "MultBatch": MUL, "ReduceAdd": REDUCE_ADD, "ReduceMul": REDUCE_MUL,
+              "LinearLayer": LINEAR, "Root": ROOT, "Load": LOAD, "BlockLabel": NOP}
+
+
+@dataclass
+class NodeSpec:
+    kind: int
+    lanes: int = 1
+    operands: tuple = ()
+    is_private: bool = False
+    din: int = 0
+    dout: int = 0
+    const_val: int = 0
+    name: str = ""
+
+
+@dataclass
+class Graph:
+    nodes: list = field(default_factory=list)
+    root: int = -1
+    inputs: dict = field(default_factory=dict)  # name -> node id (g.inputs order)
+
+    def add(self, spec: NodeSpec) -> int:
+        self.nodes.append(spec)
+        return len(self.nodes) - 1
+
+    def input(self, name: str, count: int, private: bool) -> int:
+        nid = self.add(NodeSpec(INPUT, count, (), private, name=name))
+        self.inputs[name] = nid
+        return nid
+
+    def to_c(self):
+        arr = (_lib.Node * len(self.nodes))()
+        for i, n in enumerate(self.nodes):
+            c = arr[i]
+            c.kind = n.kind
+            c.is_private = int(bool(n.is_private))
+            c.lanes = n.lanes
+            c.n_operands = len(n.operands)
+            for k, o in enumerate(n.operands):
+                c.operands[k] = o
+            c.din, c.dout, c.const_val = n.din, n.dout, n.const_val
+        return arr
+
+
+# ---- graph builders mirroring the reference front end's lowered output ----
+CHAINS = {"light": ("add", "add", "sub", "add"), "mixed": ("mul", "add", "mul", "add"),
+          "heavy": ("mul", "mul", "mul", "mul")}
+_OPK = {"add": ADD, "sub": SUB, "mul": MUL}
+
+
+def chain_graph(kind: str, n: int, x_private=True, y_private=True) -> Graph:
+    """t1 = op0 a,b; t2 = op1 t1,a; t3 = op2 t2,b; t4 = op3 t3,t1; ret t4 — node
+    ids identical to the reference's compile_graph of the same IR (Input, Input,
+    Const, BlockLabel, Load, Load, 4 ops, Root)."""
+    g = Graph()
+    x = g.input("x", n, x_private)
+    y = g.input("y", n, y_private)
+    c0 = g.add(NodeSpec(CONST, 1, (), False, const_val=0))
+    g.add(NodeSpec(NOP))
+    a = g.add(NodeSpec(LOAD, n, (x, c0), x_private))
+    b = g.add(NodeSpec(LOAD, n, (y, c0), y_private))
+    ops = CHAINS[kind]
+    priv = lambda *ids: any(g.nodes[i].is_private for i in ids)
+    t1 = g.add(NodeSpec(_OPK[ops[0]], n, (a, b), priv(a, b)))
+    t2 = g.add(NodeSpec(_OPK[ops[1]], n, (t1, a), priv(t1, a)))
+    t3 = g.add(NodeSpec(_OPK[ops[2]], n, (t2, b), priv(t2, b)))
+    t4 = g.add(NodeSpec(_OPK[ops[3]], n, (t3, t1), priv(t3, t1)))
+    g.root = g.add(NodeSpec(ROOT, n, (t4,), priv(t4)))
+    return g
+
+
+def linear_graph(din: int, dout: int, x_private=True, w_private=True, b_private=True) -> Graph:
+    """mark_linear_layer idiom (tests/test_util.hpp:54-67): Input x, W, b; consts; LinearLayer; Root."""
+    g = Graph()
+    x = g.input("x", din, x_private)
+    w = g.input("W", din * dout, w_private)
+    b = g.input("b", dout, b_private)
+    g.add(NodeSpec(CONST, 1, (), False, const_val=0))
+    g.add(NodeSpec(CONST, 1, (), False, const_val=1))
+    g.add(NodeSpec(NOP))
+    lin = g.add(NodeSpec(LINEAR, dout, (x, w, b), x_private or w_private or b_private, din=din, dout=dout))
+    g.root = g.add(NodeSpec(ROOT, dout, (lin,), g.nodes[lin].is_private))
+    return g
+
+
+def reduce_graph(kind: str, n: int) -> Graph:
+    """llvm.vector.reduce.{add,mul} over a private <n x i32> (fixtures/reduce_mul.ll)."""
+    g = Graph()
+    x = g.input("x", n, True)
+    c0 = g.add(NodeSpec(CONST, 1, (), False, const_val=0))
+    g.add(NodeSpec(NOP))
+    a = g.add(NodeSpec(LOAD, n, (x, c0), True))
+    r = g.add(NodeSpec(REDUCE_ADD if kind == "add" else REDUCE_MUL, 1, (a,), True))
+    g.root = g.add(NodeSpec(ROOT, 1, (r,), True))
+    return g
+
+
+def graph_from_reference_dump(dump: str, inputs_private: dict, din_dout=None) -> Graph:
+    """Builds a Graph from oracle/ref.py:graph_dump text (tests only)."""
+    g = Graph()
+    lines = [l.split() for l in dump.strip().splitlines()]
+    root = None
+    in_names = list(inputs_private)
+    k = 0
+    for t in lines:
+        if t[0] == "root":
+            root = int(t[1])
+            continue
+        nid, kind, lanes, priv = int(t[0]), t[1], int(t[2]), t[3] == "1"
+        ops = tuple(int(o) for o in t[4:])
+        spec = NodeSpec(KIND_NAMES[kind], lanes, ops, priv)
+        if spec.kind == INPUT:
+            spec.name = in_names[k]
+            k += 1
+        g.nodes.append(spec)
+        if spec.kind == INPUT:
+            g.inputs[spec.name] = nid
+    g.root = root
+    return g
+
+
+@dataclass
+class RunReport:
+    """runtime::RunReport (runtime.hpp:20-31) + device timing."""
+    outputs: np.ndarray
+    online_ms: float
+    online_device_ms: float
+    scalar_triples_consumed: int
+    matrix_triples_consumed: int
+    bytes_exchanged: int
+    output_digest: int
+    kernel_launches: int
+    sigmas: list
+    coin: int
+    kstat: dict = None  # kernel class -> {launches, ms, bytes} (profile_kernels)
+
+
+class LocalRun:
+    """All n parties of one online phase, device resident.
+
+    ``devices[p]`` is party p's GPU (all 0 on a single B200)."""
+
+    def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
+                 devices=None, coin: int | None = None, profile_kernels: bool = False):
+        self.graph, self.n = graph, n_parties
+        o = _lib.RunOptions()
+        o.slice = slice_
+        o.dealer_seed = dealer_seed
+        o.fixed_coin = 1 if coin is not None else 0
+        o.coin = coin or 0
+        o.profile_kernels = int(profile_kernels)
+        for p in range(_lib.MAX_PARTIES):
+            o.devices[p] = (devices[p] if devices and p < len(devices) else 0)
+        self._nodes = graph.to_c()
+        h = C.c_void_p()
+        check(lib().spdz_run_create(self._nodes, len(graph.nodes), graph.root, n_parties, C.byref(o), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().spdz_run_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def deal(self, seed: int):
+        check(lib().spdz_run_deal(self.h, seed))
+
+    def bind_inputs(self, inputs: dict):
+        for name, vals in inputs.items():
+            v = np.ascontiguousarray(vals, dtype=np.uint32)
+            check(lib().spdz_run_bind_input(self.h, self.graph.inputs[name], v.ctypes.data, v.size))
+
+    def share_inputs(self):
+        check(lib().spdz_run_share_inputs(self.h))
+
+    def online(self, reuse: bool = False) -> RunReport:
+        rep = _lib.RunReport()
+        check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
+        n = C.c_uint64()
+        check(lib().spdz_run_outputs(self.h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.uint32)
+        check(lib().spdz_run_outputs(self.h, out.ctypes.data, n.value, C.byref(n)))
+        return RunReport(out, rep.online_ms, rep.online_device_ms, rep.scalar_triples_consumed,
+                         rep.matrix_triples_consumed, rep.bytes_exchanged, rep.output_digest, rep.kernel_launches,
+                         list(rep.sigmas)[: self.n], rep.coin,
+                         {name: dict(launches=rep.kstat[i].launches, ms=rep.kstat[i].ms, bytes=rep.kstat[i].bytes)
+                          for i, name in enumerate(_lib.KSTAT_NAMES)})
+
+    def node_share(self, party: int, node: int):
+        s = _lib.Share()
+        check(lib().spdz_run_node_share(self.h, party, node, C.byref(s)))
+        return s
+
+    def node_share_host(self, party: int, node: int):
+        """Copies a node's share planes to host (tests)."""
+        s = self.node_share(party, node)
+        return [device_to_host(ptr, s.lanes) if ptr else None for ptr in (s.vals, s.macs)]
+
+    def inject_bitflip(self, node: int, sender: int, receiver: int, word: int, bit: int):
+        check(lib().spdz_run_inject_bitflip(self.h, node, sender, receiver, word, bit))
+
+
+def device_to_host(ptr: int, n: int) -> np.ndarray:
+    """Copies n uint32 words at a device pointer (owned by the library) to host."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<u4", "data": (int(ptr), False), "version": 3}
+
+    torch.cuda.synchronize()
+    return torch.as_tensor(_CAI(), device="cuda").cpu().numpy().copy()
+
+
+def run_local(graph: Graph, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,
+              coin: int | None = None, devices=None) -> RunReport:
+    """runtime::run_local (runtime.cpp:586-613) on B200: deal, share inputs, online phase."""
+    r = LocalRun(graph, n_parties, slice_, dealer_seed, devices, coin)
+    try:
+        r.bind_inputs(inputs)
+        r.share_inputs()
+        return r.online()
+    finally:
+        r.close()

@@ -1,0 +1,159 @@
+"""End-to-end online phase on the GPU against the reference's run_local
+outputs (tests/golden) and the share-level oracle simulation (oracle.sim_chain):
+opened outputs, per-party node shares and MAC sigmas are bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+P = O.P
+
+
+@pytest.mark.parametrize("kind", ["light", "mixed", "heavy"])
+def test_chain_outputs_match_reference_run_local(gpu, golden, kind):
+    from paper_2512_11112_b200 import chain_graph, run_local
+    rep = run_local(chain_graph(kind, 64), 2, {"x": golden["e2e_x"], "y": golden["e2e_y"]})
+    np.testing.assert_array_equal(rep.outputs, golden[f"e2e_{kind}_out"])
+    assert rep.output_digest == golden[f"e2e_{kind}_digest"]  # runtime.cpp:573-574
+    assert rep.scalar_triples_consumed == golden[f"e2e_{kind}_triples"]
+    assert sum(rep.sigmas) % P == 0
+
+
+@pytest.mark.parametrize("kind", ["heavy", "mixed"])
+def test_three_parties(gpu, golden, kind):
+    from paper_2512_11112_b200 import chain_graph, run_local
+    rep = run_local(chain_graph(kind, 64), 3, {"x": golden["e2e_x"], "y": golden["e2e_y"]})
+    np.testing.assert_array_equal(rep.outputs, golden[f"e2e3_{kind}_out"])
+
+
+@pytest.mark.parametrize("kind,n_parties", [("heavy", 2), ("mixed", 2), ("light", 2), ("heavy", 4)])
+def test_share_level_parity_and_sigma(gpu, golden, kind, n_parties):
+    """Every node share of every party and every party's MAC sigma (fixed coin)
+    equal the oracle's simulation of the reference protocol."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    coin = 0xDEADBEEF12345678
+    x, y = golden["e2e_x"], golden["e2e_y"]
+    want = O.sim_chain(kind, n_parties, x, y, 1, coin)
+    r = LocalRun(chain_graph(kind, 64), n_parties, coin=coin)
+    r.bind_inputs({"x": x, "y": y})
+    r.share_inputs()
+    rep = r.online()
+    np.testing.assert_array_equal(rep.outputs, want["outputs"])
+    assert rep.sigmas == want["sigmas"]
+    for nid in (6, 7, 8, 9):
+        for p in range(n_parties):
+            v, m = r.node_share_host(p, nid)
+            np.testing.assert_array_equal(v, want["nodes"][nid][p][0], err_msg=f"node {nid} party {p} vals")
+            np.testing.assert_array_equal(m, want["nodes"][nid][p][1], err_msg=f"node {nid} party {p} macs")
+    r.close()
+
+
+@pytest.mark.parametrize("slice_", [262140, 200])
+def test_linear_secret_secret_matches_reference(gpu, golden, slice_):
+    from paper_2512_11112_b200 import linear_graph, run_local
+    inp = {"x": golden["lin_x"], "W": golden["lin_W"], "b": golden["lin_b"]}
+    rep = run_local(linear_graph(64, 32), 2, inp, slice_=slice_)
+    np.testing.assert_array_equal(rep.outputs, golden[f"lin_ss_{slice_}_out"])
+    assert rep.matrix_triples_consumed == golden[f"lin_ss_{slice_}_mtriples"]
+
+
+@pytest.mark.parametrize("wpriv,xpriv,key", [(False, True, "lin_wpub_out"), (True, False, "lin_xpub_out")])
+def test_linear_one_public_matches_reference(gpu, golden, wpriv, xpriv, key):
+    from paper_2512_11112_b200 import linear_graph, run_local
+    inp = {"x": golden["lin_x"], "W": golden["lin_W"], "b": golden["lin_b"]}
+    rep = run_local(linear_graph(64, 32, x_private=xpriv, w_private=wpriv), 2, inp)
+    np.testing.assert_array_equal(rep.outputs, golden[key])
+
+
+@pytest.mark.parametrize("kind", ["add", "mul"])
+def test_reduce_matches_reference(gpu, golden, kind):
+    from paper_2512_11112_b200 import reduce_graph, run_local
+    rep = run_local(reduce_graph(kind, 7), 2, {"x": golden["red_x"]})
+    np.testing.assert_array_equal(rep.outputs, golden[f"red_{kind}_out"])
+    assert sum(rep.sigmas) % P == 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 33, 1000])
+def test_reduce_mul_sizes(gpu, n):
+    from paper_2512_11112_b200 import reduce_graph, run_local
+    x = O.rand_field_vec(n, 5)
+    rep = run_local(reduce_graph("mul", n), 2, {"x": x})
+    want = 1
+    for v in x.tolist():
+        want = want * v % P
+    assert int(rep.outputs[0]) == want
+
+
+def test_bitflip_aborts_with_mac_check_failed(gpu, golden):
+    """acceptance.cpp:112-139: a flipped payload bit on any opening aborts the run."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph, errors
+    rng = np.random.default_rng(7)
+    aborted = 0
+    trials = 10
+    for t in range(trials):
+        r = LocalRun(chain_graph("heavy", 64), 2)
+        r.bind_inputs({"x": golden["e2e_x"], "y": golden["e2e_y"]})
+        r.share_inputs()
+        node = int(rng.integers(6, 10))
+        sender = int(rng.integers(0, 2))
+        r.inject_bitflip(node, sender, 1 - sender, int(rng.integers(0, 128)), int(rng.integers(0, 32)))
+        try:
+            r.online()
+        except errors.MacCheckFailed:
+            aborted += 1
+        r.close()
+    assert aborted == trials
+    # and no false aborts
+    from paper_2512_11112_b200 import run_local
+    for s in range(5):
+        run_local(chain_graph("heavy", 64), 2, {"x": golden["e2e_x"], "y": golden["e2e_y"]}, dealer_seed=100 + s)
+
+
+def test_triple_reuse_is_rejected_until_redeal(gpu, golden):
+    from paper_2512_11112_b200 import LocalRun, chain_graph, errors
+    r = LocalRun(chain_graph("heavy", 64), 2)
+    r.bind_inputs({"x": golden["e2e_x"], "y": golden["e2e_y"]})
+    r.share_inputs()
+    r.online()
+    with pytest.raises(errors.TripleExhausted):
+        r.online()
+    r.deal(2)
+    r.share_inputs()
+    rep = r.online()
+    np.testing.assert_array_equal(rep.outputs, golden["e2e_heavy_out"])
+    r.close()
+
+
+@pytest.mark.parametrize("kind,n", [("heavy", 1 << 20), ("mixed", (1 << 18) + 7)])
+def test_large_chain_vs_cleartext(gpu, kind, n):
+    """Full-size property: opened outputs equal the cleartext chain and the MAC check passes."""
+    from paper_2512_11112_b200 import chain_graph, run_local
+    x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+    rep = run_local(chain_graph(kind, n), 2, {"x": x, "y": y})
+    ops = {"light": "++-+", "mixed": "*+*+", "heavy": "****"}[kind]
+    f = {"+": O.np_add, "-": O.np_sub, "*": O.np_mul}
+    t1 = f[ops[0]](x, y)
+    t2 = f[ops[1]](t1, x)
+    t3 = f[ops[2]](t2, y)
+    np.testing.assert_array_equal(rep.outputs, f[ops[3]](t3, t1))
+    assert sum(rep.sigmas) % P == 0
+
+
+def test_linear_4096_secret_secret_property(gpu):
+    """C4 shape (4096x4096, slice 262140 -> 64 tiles): opened output equals W x + b."""
+    from paper_2512_11112_b200 import linear_graph, run_local
+    din = dout = 4096
+    x, W, b = O.rand_field_vec(din, 1), O.rand_field_vec(din * dout, 2), O.rand_field_vec(dout, 3)
+    rep = run_local(linear_graph(din, dout), 2, {"x": x, "W": W, "b": b})
+    import torch
+    Wt = torch.from_numpy(W.astype(np.int64)).cuda().view(dout, din)
+    xt = torch.from_numpy(x.astype(np.int64)).cuda()
+    # exact W x mod p in int64 chunks: split x into 16-bit halves to stay below 2^63 per partial sum
+    lo, hi = xt & 0xFFFF, xt >> 16
+    acc_lo = ((Wt * lo) % P).sum(1) % P
+    acc_hi = ((Wt * hi) % P).sum(1) % P
+    want = ((acc_lo + acc_hi * 65536 % P) % P + torch.from_numpy(b.astype(np.int64)).cuda()) % P
+    np.testing.assert_array_equal(rep.outputs, want.cpu().numpy().astype(np.uint32))
+    assert rep.matrix_triples_consumed == 64
+    assert sum(rep.sigmas) % P == 0
