@@ -1,0 +1,171 @@
+"""Sweep over BASELINE.json's configs (the non-headline bench lines), with the
+reference CPU implementation (oracle/_ref, runtime::run_local) timed beside
+where it finishes in seconds.  Writes one JSON document.
+
+  python bench_configs.py [--out gpurun_out/sweep.json] [--quick]
+
+C1  2-party Beaver multiply, 2^16..2^26 lanes (single MultBatch node graph)
+C2  light / mixed / heavy chains, 2^16, 2^20, 2^24
+C3  linear secret x public 1024x1024, batch 256 (modular GEMM, both planes)
+C4  linear secret x secret 4096x4096 (+ MAC check), slice 262140 (64 tiles) and 1 tile
+    + the paper's 8192x8192 layer (slice 262140, 265 tiles)
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+P = 4294967291
+
+
+def rnd(n, seed):
+    return np.random.default_rng(seed).integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+
+
+def gpu_online(graph, inputs, reps=5, slice_=262140, profile=True):
+    from paper_2512_11112_b200 import LocalRun
+    r = LocalRun(graph, 2, slice_=slice_, profile_kernels=profile)
+    dev, wall, reps_out = [], [], None
+    for k in range(reps + 1):
+        r.deal(10 + k)
+        r.bind_inputs(inputs)
+        r.share_inputs()
+        t0 = time.perf_counter()
+        rep = r.online()
+        t1 = time.perf_counter()
+        assert sum(rep.sigmas) % P == 0
+        if k:
+            dev.append(rep.online_device_ms)
+            wall.append((t1 - t0) * 1e3)
+            reps_out = rep
+    r.close()
+    ks = {n: {"ms": v["ms"], "GBs": (v["bytes"] / v["ms"] / 1e6) if v["ms"] else None, "launches": v["launches"]}
+          for n, v in reps_out.kstat.items() if v["launches"]}
+    return {"online_device_ms": float(np.median(dev)), "online_wall_ms": float(np.median(wall)),
+            "kernel_launches": reps_out.kernel_launches, "kernels": ks}
+
+
+def ref_online(ir, inputs, threads, slice_=262140, reps=1):
+    from oracle import ref
+    if not ref.available():
+        return None
+    best = None
+    for _ in range(reps):
+        _, rep = ref.run_local(ir, 2, inputs, threads=threads, slice_=slice_, io_timeout_ms=600000)
+        best = rep["online_ms"] if best is None else min(best, rep["online_ms"])
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "sweep.json"))
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--no-ref", action="store_true")
+    args = ap.parse_args()
+    import torch
+
+    from oracle import workloads
+    from paper_2512_11112_b200 import Graph, NodeSpec, chain_graph, linear_graph
+    from paper_2512_11112_b200 import runtime as rt
+    threads = os.cpu_count() or 1
+    out = {"host_cores": threads, "gpu": torch.cuda.get_device_name(0), "configs": {}}
+    res = out["configs"]
+
+    # C1: single Beaver multiply node
+    c1 = []
+    for lg in ([16, 20, 24] if args.quick else [16, 18, 20, 22, 24, 26]):
+        n = 1 << lg
+        g = Graph()
+        x = g.input("x", n, True)
+        y = g.input("y", n, True)
+        c0 = g.add(NodeSpec(rt.CONST, 1, (), False, const_val=0))
+        g.add(NodeSpec(rt.NOP))
+        a = g.add(NodeSpec(rt.LOAD, n, (x, c0), True))
+        b = g.add(NodeSpec(rt.LOAD, n, (y, c0), True))
+        m = g.add(NodeSpec(rt.MUL, n, (a, b), True))
+        g.root = g.add(NodeSpec(rt.ROOT, n, (m,), True))
+        gr = gpu_online(g, {"x": rnd(n, 1), "y": rnd(n, 2)})
+        gr.update(lanes=n, mults_per_s=n / (gr["online_device_ms"] / 1e3))
+        c1.append(gr)
+        print("C1", lg, gr["online_device_ms"], flush=True)
+    res["C1_beaver_multiply"] = c1
+
+    # C2: chains
+    c2 = []
+    for kind in ("light", "mixed", "heavy"):
+        for lg in (16, 20, 24):
+            n = 1 << lg
+            inp = {"x": rnd(n, 1), "y": rnd(n, 2)}
+            gr = gpu_online(chain_graph(kind, n), inp)
+            gr.update(kind=kind, lanes=n)
+            if not args.no_ref and lg <= (16 if args.quick else 20):
+                gr["reference_online_ms"] = ref_online(workloads.chain_ir(kind, n), inp, threads)
+                gr["reference_threads_per_party"] = threads
+            c2.append(gr)
+            print("C2", kind, lg, gr["online_device_ms"], gr.get("reference_online_ms"), flush=True)
+    res["C2_chains"] = c2
+
+    # C3: secret x public 1024x1024 batch 256 (modular GEMM on both planes)
+    from paper_2512_11112_b200 import Context, DeviceShare
+    from paper_2512_11112_b200._lib import check, lib
+    from paper_2512_11112_b200.backend import dshare
+    din = dout = 1024
+    batch = 256
+    ctx = Context(0, 0, 2, 12345)
+    ctx.use_torch_stream()
+    W = torch.from_numpy(rnd(din * dout, 1)).cuda()
+    xs = DeviceShare(torch.from_numpy(rnd(din * batch, 2)).cuda(), torch.from_numpy(rnd(din * batch, 3)).cuda())
+    ys = DeviceShare.empty(dout * batch)
+    args_c = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
+    for _ in range(3):
+        check(lib().spdz_linear_secret_public(*args_c))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 20
+    e0.record()
+    for _ in range(iters):
+        check(lib().spdz_linear_secret_public(*args_c))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    modmacs = 2 * din * dout * batch  # two planes
+    c3 = {"shape": [dout, din, batch], "kernel_ms": ms, "modmac_per_s": modmacs / (ms / 1e3),
+          "int_ops_per_s": 2 * modmacs / (ms / 1e3), "path": "CUDA-core k_modgemm (2 IMAD.WIDE per modMAC)"}
+    if not args.no_ref:
+        lin = {"x": rnd(din, 4), "W": rnd(din * dout, 5), "b": rnd(dout, 6)}
+        one = ref_online(workloads.linear_ir(din, dout, w_private=False), lin, threads)
+        c3["reference_batch1_online_ms"] = one
+        c3["reference_batch256_online_ms_est"] = one * batch if one else None
+    res["C3_linear_secret_public"] = c3
+    print("C3", c3, flush=True)
+
+    # C4: secret x secret 4096x4096 with MAC check
+    c4 = []
+    shapes = [(4096, 4096, 262140), (4096, 4096, 4096 * 4096)]
+    if not args.quick:
+        shapes.append((8192, 8192, 262140))
+    for din, dout, sl in shapes:
+        inp = {"x": rnd(din, 1), "W": rnd(din * dout, 2), "b": rnd(dout, 3)}
+        gr = gpu_online(linear_graph(din, dout), inp, reps=3, slice_=sl)
+        gr.update(din=din, dout=dout, slice=sl)
+        if not args.no_ref and din == 4096 and sl == 262140 and not args.quick:
+            gr["reference_online_ms"] = ref_online(workloads.linear_ir(din, dout), inp, threads, slice_=sl)
+        c4.append(gr)
+        print("C4", din, sl, gr["online_device_ms"], gr.get("reference_online_ms"), flush=True)
+    res["C4_linear_secret_secret"] = c4
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(out, indent=1))
+    print(json.dumps(out)[:2000])
+
+
+if __name__ == "__main__":
+    main()

@@ -107,8 +107,11 @@ const char* spdz_version(void);
 /* Creates a party context on `device` (cudaSetDevice'd on every entry). */
 int spdz_ctx_create(int device, int party, int n_parties, uint32_t alpha_share, spdz_ctx** out);
 int spdz_ctx_destroy(spdz_ctx* ctx);
-/* Use an external CUDA stream (cudaStream_t passed as void*); NULL restores the owned stream. */
+/* Launch on an external CUDA stream (cudaStream_t passed as void*; NULL = the
+ * legacy default stream), e.g. the caller's framework stream. */
 int spdz_ctx_set_stream(spdz_ctx* ctx, void* stream);
+/* Back to the context's own non-blocking stream (the default after create). */
+int spdz_ctx_use_own_stream(spdz_ctx* ctx);
 void* spdz_ctx_stream(spdz_ctx* ctx);
 int spdz_ctx_party(const spdz_ctx* ctx);
 int spdz_ctx_sync(spdz_ctx* ctx);
@@ -275,6 +278,8 @@ typedef struct spdz_run_options {
     int32_t use_graph;     /* reserved (CUDA-graph capture of the online phase) */
     int32_t devices[SPDZ_MAX_PARTIES]; /* device of each party (-1: device 0) */
     int32_t profile_kernels; /* 1: CUDA-event time every mask / combine / sigma launch */
+    int32_t stream_per_party; /* 0 (default): parties on one device share its stream (kernels
+                                 serialise, each gets the full HBM); 1: one stream per party */
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
@@ -318,6 +323,10 @@ int spdz_run_share_inputs(spdz_run* run);
  * (triple consumption is reset per call only when `reuse_preprocessing` = 1 —
  * the bench re-times the same preprocessing; the reference semantics are 0). */
 int spdz_run_online(spdz_run* run, int reuse_preprocessing, spdz_run_report_t* report);
+/* Registers the host buffer the next online phases write the opened outputs
+ * into (D2H straight from the open kernel's buffer; pinned memory recommended).
+ * Without one, outputs land in an internal pinned buffer (spdz_run_outputs). */
+int spdz_run_bind_output(spdz_run* run, uint32_t* host_out, uint64_t cap);
 /* Opened outputs (host).  *len receives the lane count. */
 int spdz_run_outputs(spdz_run* run, uint32_t* host_out, uint64_t cap, uint64_t* len);
 /* Device view of a node's share for party p (tests). */

@@ -48,7 +48,8 @@ class Node(C.Structure):  # spdz_node_t
 
 class RunOptions(C.Structure):  # spdz_run_options_t
     _fields_ = [("slice", C.c_uint64), ("dealer_seed", C.c_uint64), ("fixed_coin", C.c_int32), ("coin", C.c_uint64),
-                ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32)]
+                ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32),
+                ("stream_per_party", C.c_int32)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t
@@ -72,6 +73,7 @@ _SIGS = {
     "spdz_ctx_destroy": (C.c_int, [vp]),
     "spdz_ctx_set_stream": (C.c_int, [vp, vp]),
     "spdz_ctx_stream": (vp, [vp]),
+    "spdz_ctx_use_own_stream": (C.c_int, [vp]),
     "spdz_ctx_party": (C.c_int, [vp]),
     "spdz_ctx_sync": (C.c_int, [vp]),
     "spdz_capability": (C.c_int, [vp, C.POINTER(Capability)]),
@@ -126,6 +128,7 @@ _SIGS = {
     "spdz_run_share_inputs": (C.c_int, [vp]),
     "spdz_run_online": (C.c_int, [vp, C.c_int, C.POINTER(RunReport)]),
     "spdz_run_outputs": (C.c_int, [vp, vp, C.c_uint64, u64p]),
+    "spdz_run_bind_output": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_node_share": (C.c_int, [vp, C.c_int, C.c_uint32, C.POINTER(Share)]),
     "spdz_run_inject_bitflip": (C.c_int, [vp, C.c_uint32, C.c_int, C.c_int, C.c_uint64, C.c_uint32]),
 }

@@ -76,11 +76,15 @@ def _u32(a) -> np.ndarray:
 class Context:
     """One party's device context (spdz_ctx): device, stream, party index, alpha share."""
 
-    def __init__(self, device: int = 0, party: int = 0, n_parties: int = 2, alpha_share: int = 0):
+    def __init__(self, device: int = 0, party: int = 0, n_parties: int = 2, alpha_share: int = 0,
+                 use_torch_stream: bool = True):
         self.device, self.party, self.n_parties, self.alpha_share = device, party, n_parties, alpha_share
         h = C.c_void_p()
         check(lib().spdz_ctx_create(device, party, n_parties, alpha_share, C.byref(h)))
         self.h = h
+        if use_torch_stream:
+            # device tensors come from torch: order our kernels on torch's current stream
+            self.use_torch_stream()
 
     def close(self):
         if getattr(self, "h", None):
@@ -94,7 +98,11 @@ class Context:
             pass
 
     def set_stream(self, stream_handle: int | None):
+        """Launch on a raw cudaStream_t (0/None = the legacy default stream)."""
         check(lib().spdz_ctx_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
+
+    def use_own_stream(self):
+        check(lib().spdz_ctx_use_own_stream(self.h))
 
     def use_torch_stream(self, stream=None):
         import torch
@@ -204,7 +212,7 @@ class GpuBackend:
     path is the CUDA library (spdz_host_* entry points)."""
 
     def __init__(self, device: int = 0, min_kernel_size: int = 1):
-        self.ctx = Context(device, 0, 2, 0)
+        self.ctx = Context(device, 0, 2, 0, use_torch_stream=False)
         cap = self.ctx.capability()
         cap.min_kernel_size = max(1, min_kernel_size)
         self._cap = cap

@@ -204,7 +204,14 @@ int spdz_ctx_destroy(spdz_ctx* ctx) {
 int spdz_ctx_set_stream(spdz_ctx* ctx, void* stream) {
     return guard([&] {
         need_ctx(ctx);
-        ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+        ctx->stream = (cudaStream_t)stream;  // NULL = the legacy default stream
+    });
+}
+
+int spdz_ctx_use_own_stream(spdz_ctx* ctx) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->stream = ctx->own_stream;
     });
 }
 void* spdz_ctx_stream(spdz_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }

@@ -140,7 +140,9 @@ struct spdz_run {
     std::vector<Fault> faults;
     bool consumed = false;
     uint64_t dealer_seed = 1;
-    std::vector<uint32_t> host_out;
+    uint32_t* host_out = nullptr;   // pinned (internal) or user-bound output buffer
+    uint64_t host_out_len = 0, host_out_cap = 0;
+    bool host_out_owned = false;
     uint64_t exchanged = 0;
     cudaEvent_t ev_input = nullptr;
 
@@ -1092,6 +1094,12 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
         for (int p = 0; p < n_parties; ++p) {
             int rc = spdz_ctx_create(r->devices[p], p, n_parties, 0, &r->parties[p].ctx);
             if (rc) throw Error(rc, spdz_last_error());
+            if (!r->opts.stream_per_party)  // parties sharing a device share its stream
+                for (int q = 0; q < p; ++q)
+                    if (r->devices[q] == r->devices[p]) {
+                        r->parties[p].ctx->stream = r->parties[q].ctx->stream;
+                        break;
+                    }
         }
         for (int p = 0; p < n_parties; ++p)  // P2P between party devices (NVLink)
             for (int q = 0; q < n_parties; ++q) {
@@ -1129,7 +1137,11 @@ int spdz_run_destroy(spdz_run* r) {
             cudaSetDevice(r->alloc_dev[i]);
             cudaFree(r->allocs[i]);
         }
-        for (auto& P : r->parties) spdz_ctx_destroy(P.ctx);
+        if (r->host_out && r->host_out_owned) cudaFreeHost(r->host_out);
+        for (auto& P : r->parties) {
+            if (P.ctx && P.ctx->stream != P.ctx->own_stream) P.ctx->stream = P.ctx->own_stream;
+            spdz_ctx_destroy(P.ctx);
+        }
         delete r;
     });
 }
@@ -1195,9 +1207,18 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
         mac_check(r, rep, ex);  // also records t1 and synchronises
         // outputs to host (party 0; all parties hold the same opened values)
         const Val& rv = r->parties[0].ns[r->root].out;
-        r->host_out.resize(rv.lanes);
         dev(r, 0);
-        lk(cudaMemcpy(r->host_out.data(), r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost), "D2H out");
+        if (!r->host_out || r->host_out_cap < rv.lanes) {
+            need(r->host_out_owned || !r->host_out, SPDZ_ERR_INVALID_ARGUMENT, "bound output buffer too small");
+            if (r->host_out) cudaFreeHost(r->host_out);
+            cuda_check(cudaMallocHost(&r->host_out, std::max<uint64_t>(rv.lanes, 1) * 4), "cudaMallocHost(out)");
+            r->host_out_cap = rv.lanes;
+            r->host_out_owned = true;
+        }
+        r->host_out_len = rv.lanes;
+        lk(cudaMemcpyAsync(r->host_out, r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost, S(r, 0)),
+           "D2H out");
+        lk(cudaStreamSynchronize(S(r, 0)), "sync out");
         auto t1 = std::chrono::steady_clock::now();
         if (rep) {
             rep->online_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -1212,7 +1233,7 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
             rep->scalar_triples_consumed = r->scalar_total;
             rep->matrix_triples_consumed = r->matrix_total;
             rep->bytes_exchanged = r->exchanged;
-            rep->output_digest = spdz_fnv1a64(r->host_out.data(), r->host_out.size() * 4, 1469598103934665603ull);
+            rep->output_digest = spdz_fnv1a64(r->host_out, r->host_out_len * 4, 1469598103934665603ull);
             rep->kernel_launches = g_kernel_launches - launches0;
             for (int c = 0; c < SPDZ_KSTAT_N; ++c) rep->kstat[c] = spdz_kernel_stat_t{0, 0.0, 0};
             for (auto& rec : r->kt.recs) {
@@ -1232,8 +1253,19 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
 int spdz_run_outputs(spdz_run* r, uint32_t* host_out, uint64_t cap, uint64_t* len) {
     return guard([&] {
         need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
-        if (len) *len = r->host_out.size();
-        if (host_out) std::memcpy(host_out, r->host_out.data(), std::min<uint64_t>(cap, r->host_out.size()) * 4);
+        if (len) *len = r->host_out_len;
+        if (host_out && host_out != r->host_out)
+            std::memcpy(host_out, r->host_out, std::min<uint64_t>(cap, r->host_out_len) * 4);
+    });
+}
+
+int spdz_run_bind_output(spdz_run* r, uint32_t* host_out, uint64_t cap) {
+    return guard([&] {
+        need(r != nullptr && host_out != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "bad bind_output");
+        if (r->host_out && r->host_out_owned) cudaFreeHost(r->host_out);
+        r->host_out = host_out;
+        r->host_out_cap = cap;
+        r->host_out_owned = false;
     });
 }
 

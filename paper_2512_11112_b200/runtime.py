@@ -165,7 +165,8 @@ class LocalRun:
     ``devices[p]`` is party p's GPU (all 0 on a single B200)."""
 
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
-                 devices=None, coin: int | None = None, profile_kernels: bool = False):
+                 devices=None, coin: int | None = None, profile_kernels: bool = False,
+                 stream_per_party: bool = False):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -173,6 +174,7 @@ class LocalRun:
         o.fixed_coin = 1 if coin is not None else 0
         o.coin = coin or 0
         o.profile_kernels = int(profile_kernels)
+        o.stream_per_party = int(stream_per_party)
         for p in range(_lib.MAX_PARTIES):
             o.devices[p] = (devices[p] if devices and p < len(devices) else 0)
         self._nodes = graph.to_c()
@@ -202,13 +204,22 @@ class LocalRun:
     def share_inputs(self):
         check(lib().spdz_run_share_inputs(self.h))
 
+    def bind_output(self, out: np.ndarray):
+        """Opened outputs of the next online phases are written straight into `out` (pin it for speed)."""
+        assert out.dtype == np.uint32 and out.flags.c_contiguous
+        self._out = out
+        check(lib().spdz_run_bind_output(self.h, out.ctypes.data, out.size))
+
     def online(self, reuse: bool = False) -> RunReport:
         rep = _lib.RunReport()
         check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
         n = C.c_uint64()
         check(lib().spdz_run_outputs(self.h, None, 0, C.byref(n)))
-        out = np.empty(n.value, np.uint32)
-        check(lib().spdz_run_outputs(self.h, out.ctypes.data, n.value, C.byref(n)))
+        if getattr(self, "_out", None) is not None:
+            out = self._out[: n.value]
+        else:
+            out = np.empty(n.value, np.uint32)
+            check(lib().spdz_run_outputs(self.h, out.ctypes.data, n.value, C.byref(n)))
         return RunReport(out, rep.online_ms, rep.online_device_ms, rep.scalar_triples_consumed,
                          rep.matrix_triples_consumed, rep.bytes_exchanged, rep.output_digest, rep.kernel_launches,
                          list(rep.sigmas)[: self.n], rep.coin,

@@ -1,0 +1,21 @@
+"""The reference's own Backend interface driven by the B200 back end: the
+drop-in shim integration/gpu_b200_backend.cpp, compiled against the
+reference headers and linked with the unmodified reference core, runs the
+protocol_tests.cpp:280-330 scenario and compares bit-for-bit with the
+reference CpuBackend (integration/check_drop_in.cpp)."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BIN = ROOT / "integration" / "_build" / "check_drop_in"
+
+
+@pytest.mark.gpu
+def test_reference_backend_interface_drop_in(gpu):
+    if not BIN.exists():
+        pytest.skip("integration/_build/check_drop_in not built (needs /root/reference at build time)")
+    r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout

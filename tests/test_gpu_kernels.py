@@ -302,7 +302,8 @@ def test_linear_secret_public_vs_oracle(gpu, din, dout, batch):
     c = ctx()
     y = DeviceShare.empty(dout * batch)
     x = share(Xv, Xm)
-    check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 1, T(W).data_ptr(), None, C.byref(dshare(x)), None,
+    Wd = T(W)  # keep device operands alive until the stream-ordered read below
+    check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 1, Wd.data_ptr(), None, C.byref(dshare(x)), None,
                                           C.byref(dshare(y))))
     yv, ym = H(y.vals).reshape(dout, batch), H(y.macs).reshape(dout, batch)
     cols = range(batch) if batch <= 8 else (0, 17, batch - 1)
@@ -314,7 +315,8 @@ def test_linear_secret_public_vs_oracle(gpu, din, dout, batch):
     # x public, W secret
     Wm = O.rand_field_vec(din * dout, 4)
     w = share(W, Wm)
-    check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 0, None, C.byref(dshare(w)), None, T(Xv).data_ptr(),
+    Xd = T(Xv)
+    check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 0, None, C.byref(dshare(w)), None, Xd.data_ptr(),
                                           C.byref(dshare(y))))
     yv, ym = H(y.vals).reshape(dout, batch), H(y.macs).reshape(dout, batch)
     for j in list(cols)[:2]:
