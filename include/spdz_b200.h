@@ -97,6 +97,7 @@ typedef struct spdz_mac_segment {
     uint64_t j0;       /* global rank of record 0 (filled by spdz_mac_assign_ranks) */
     uint64_t batch_id; /* wire batch id of the opening (runtime.cpp:22-24) */
     uint64_t lane0;    /* lane of record 0 inside its batch (log_open lane, runtime.cpp:115-116) */
+    uint64_t batch_len;/* records of the whole batch across all shards (0: infer from the local segments) */
 } spdz_mac_segment_t;
 
 typedef struct spdz_ctx spdz_ctx;
@@ -280,6 +281,13 @@ typedef struct spdz_run_options {
     int32_t profile_kernels; /* 1: CUDA-event time every mask / combine / sigma launch */
     int32_t stream_per_party; /* 0 (default): parties on one device share its stream (kernels
                                  serialise, each gets the full HBM); 1: one stream per party */
+    /* Lane sharding (multi-GPU): this run holds lanes [shard_offset, shard_offset + L) of
+     * every vector node of a global circuit with shard_total lanes (L = the nodes' lanes).
+     * Preprocessing is exactly that slice of the global dealer output and MAC ranks are
+     * global, so sigma partials of all shards sum to the unsharded sigma.  0 = unsharded. */
+    uint64_t shard_offset;
+    uint64_t shard_total;
+    int32_t external_mac_verify; /* 1: report per-party (partial) sigmas, caller verifies */
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
@@ -297,7 +305,7 @@ typedef struct spdz_run_report {
     double online_device_ms;          /* CUDA-event time of the online phase (max over parties) */
     uint64_t scalar_triples_consumed, matrix_triples_consumed;
     uint64_t bytes_exchanged;         /* payload bytes read from peers */
-    uint64_t output_digest;           /* fnv1a64 of the opened outputs (runtime.cpp:573) */
+    uint64_t output_digest;           /* 0 here; see spdz_run_output_digest (kept off the online phase) */
     uint64_t kernel_launches;
     uint32_t sigmas[SPDZ_MAX_PARTIES];
     uint64_t coin;
@@ -327,6 +335,16 @@ int spdz_run_online(spdz_run* run, int reuse_preprocessing, spdz_run_report_t* r
  * into (D2H straight from the open kernel's buffer; pinned memory recommended).
  * Without one, outputs land in an internal pinned buffer (spdz_run_outputs). */
 int spdz_run_bind_output(spdz_run* run, uint32_t* host_out, uint64_t cap);
+/* The online phase in two steps, so that the MAC-check coin can be agreed
+ * after the openings (runtime.cpp:467-489) — e.g. across the ranks of a
+ * lane-sharded run: begin = node execution + root open (+ async D2H of the
+ * outputs); mac_check = sigma with `coin` (use_coin = 1) or the run's own
+ * coin, then verification (unless external_mac_verify) and the report.
+ * spdz_run_online = begin + mac_check(use_coin = 0). */
+int spdz_run_online_begin(spdz_run* run, int reuse_preprocessing);
+int spdz_run_mac_check(spdz_run* run, int use_coin, uint64_t coin, spdz_run_report_t* report);
+/* fnv1a64 digest of the last opened outputs (RunReport.output_digest, runtime.cpp:573). */
+int spdz_run_output_digest(spdz_run* run, uint64_t* digest);
 /* Opened outputs (host).  *len receives the lane count. */
 int spdz_run_outputs(spdz_run* run, uint32_t* host_out, uint64_t cap, uint64_t* len);
 /* Device view of a node's share for party p (tests). */

@@ -63,6 +63,7 @@ void assign_ranks(spdz_mac_segment_t* segs, uint64_t n) {
         const uint64_t b = segs[idx[i]].batch_id;
         while (j < idx.size() && segs[idx[j]].batch_id == b) {
             batch_records = std::max(batch_records, segs[idx[j]].lane0 + segs[idx[j]].len);
+            batch_records = std::max(batch_records, segs[idx[j]].batch_len);
             segs[idx[j]].j0 = off + segs[idx[j]].lane0;
             ++j;
         }
@@ -596,7 +597,8 @@ int spdz_dealer_triples(spdz_ctx* ctx, int n, uint64_t seed, uint64_t draw0, uin
         uint32_t sh[SPDZ_MAX_PARTIES], alpha;
         dealer_alpha(n, seed, sh, &alpha);
         cuda_check(cudaMemsetAsync(ctx->d_flag, 0, 4, ctx->stream), "memset");
-        launch_ok(launch_dealer_triples(ctx->stream, n, seed, draw0, alpha, lanes, planes, ctx->d_flag, ctx->sms),
+        launch_ok(launch_dealer_triples(ctx->stream, n, seed, draw0, alpha, lanes, 0, lanes, lanes, planes, ctx->d_flag,
+                                        ctx->sms),
                   "k_dealer_triples");
         check_dealer_flag(ctx);
     });
@@ -653,7 +655,7 @@ int spdz_dealer_masks(spdz_ctx* ctx, int n, uint64_t seed, uint64_t draw0, uint3
         need_ctx(ctx);
         device_guard(ctx);
         cuda_check(cudaMemsetAsync(ctx->d_flag, 0, 4, ctx->stream), "memset");
-        launch_ok(launch_dealer_masks(ctx->stream, n, seed, draw0, alpha, count, vals, macs, clear, ctx->d_flag,
+        launch_ok(launch_dealer_masks(ctx->stream, n, seed, draw0, alpha, 0, count, count, vals, macs, clear, ctx->d_flag,
                                       ctx->sms),
                   "k_dealer_masks");
         check_dealer_flag(ctx);

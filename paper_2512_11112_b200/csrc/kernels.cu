@@ -332,27 +332,61 @@ __global__ void __launch_bounds__(kThreads) k_pair_split(const uint32_t* __restr
 }
 
 // MAC sigma (spdz.cpp:126-138) in closed form: record of rank j contributes
-// r_j * (m_j - alpha x_j), r_j = reduce(mix(coin + (j+1) gamma)).  Order-free.
+// r_j * (m_j - alpha x_j), r_j = reduce(mix(coin + (j+1) gamma)).  Order-free, so
+// sigma = S_m - alpha * S_x with S_m = sum r_j m_j and S_x = sum r_j x_j (two
+// lazily folded accumulators, one alpha-multiply per CTA instead of per record).
+// Four records per thread per step from 128-bit loads issued before the math.
+__device__ __forceinline__ void sigma_rec(uint64_t z, uint32_t x, uint32_t m, unsigned long long& sm,
+                                          unsigned long long& sx) {
+    const uint32_t r = fp_reduce64(mix64(z));
+    sm += fold1(mul_wide(r, m));
+    sx += fold1(mul_wide(r, x));
+}
+
 __global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restrict__ segs,
                                                         const MacChunk* __restrict__ chunks, uint32_t n_chunks,
                                                         uint64_t coin, uint32_t alpha, unsigned long long* acc) {
-    unsigned long long s[1] = {0ull};
+    unsigned long long sm = 0ull, sx = 0ull;
     for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
         const MacChunk ch = chunks[c];
         const MacSegDev sg = segs[ch.seg];
-        const uint64_t base = ch.start;
-        for (uint32_t i = threadIdx.x; i < ch.count; i += blockDim.x) {
-            const uint64_t idx = base + i;
-            const uint32_t x = __ldcs(sg.value + idx);
-            uint32_t m = __ldcs(sg.mac_a + idx);
-            if (sg.mac_b) m = fp_sub(m, __ldcs(sg.mac_b + idx));
-            const uint32_t r = mac_coeff(coin, sg.j0 + idx);
-            const uint32_t diff = fp_sub(m, fp_mul(alpha, x));
-            s[0] += fold1(mul_wide(r, diff));  // < 6*2^32, count per thread << 2^29
+        const uint32_t* xv = sg.value + ch.start;
+        const uint32_t* ma = sg.mac_a + ch.start;
+        const uint32_t* mb = sg.mac_b ? sg.mac_b + ch.start : nullptr;
+        const uint64_t z0 = coin + (sg.j0 + ch.start + 1) * kGamma;  // z of record 0 of the chunk
+        const bool v4 = ((reinterpret_cast<uintptr_t>(xv) | reinterpret_cast<uintptr_t>(ma) |
+                          reinterpret_cast<uintptr_t>(mb)) & 15u) == 0;
+        uint32_t done = 0;
+        if (v4) {
+            const uint32_t n4 = ch.count / 4;
+            for (uint32_t g = threadIdx.x; g < n4; g += blockDim.x) {
+                const uint4 x = __ldcs(reinterpret_cast<const uint4*>(xv) + g);
+                uint4 m = __ldcs(reinterpret_cast<const uint4*>(ma) + g);
+                if (mb) {
+                    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(mb) + g);
+                    m.x = fp_sub(m.x, b.x);
+                    m.y = fp_sub(m.y, b.y);
+                    m.z = fp_sub(m.z, b.z);
+                    m.w = fp_sub(m.w, b.w);
+                }
+                const uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
+                sigma_rec(z, x.x, m.x, sm, sx);
+                sigma_rec(z + kGamma, x.y, m.y, sm, sx);
+                sigma_rec(z + 2 * kGamma, x.z, m.z, sm, sx);
+                sigma_rec(z + 3 * kGamma, x.w, m.w, sm, sx);
+            }
+            done = n4 * 4;
         }
-        s[0] = fold1(s[0]);
+        for (uint32_t i = done + threadIdx.x; i < ch.count; i += blockDim.x) {
+            uint32_t m = __ldcs(ma + i);
+            if (mb) m = fp_sub(m, __ldcs(mb + i));
+            sigma_rec(z0 + (uint64_t)i * kGamma, __ldcs(xv + i), m, sm, sx);
+        }
+        sm = fold1(sm);  // per chunk a thread adds <= 64 terms < 6*2^32
+        sx = fold1(sx);
     }
-    s[0] = fp_reduce64(s[0]);
+    // sigma partial of this thread: S_m - alpha * S_x (mod p)
+    unsigned long long s[1] = {fp_sub(fp_reduce64(sm), fp_mul(alpha, fp_reduce64(sx)))};
     block_sum<1>(s);
     if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
 }
@@ -581,19 +615,22 @@ __device__ __forceinline__ void share_lane(int n, uint64_t seed, uint64_t base, 
     macs[j] = fp_sub(fp_mul(alpha, x), ms);
 }
 
-__global__ void k_dealer_triples(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t lanes,
-                                 uint32_t* av, uint32_t* am, uint32_t* bv, uint32_t* bm, uint32_t* cv, uint32_t* cm,
-                                 unsigned int* flag) {
+// Lanes [j_first, j_first+count) of dealer.triples(S_total) (spdz.cpp:210-225);
+// party p's share of local lane j goes to plane[p * pstride + j].
+__global__ void k_dealer_triples(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t S_total,
+                                 uint64_t j_first, uint64_t count, uint64_t pstride, uint32_t* av, uint32_t* am,
+                                 uint32_t* bv, uint32_t* bm, uint32_t* cv, uint32_t* cm, unsigned int* flag) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t per = 2ull * (n - 1);
-    const uint64_t sa = draw0 + 2 * lanes, sb = sa + per * lanes, sc = sb + per * lanes;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lanes; j += stride) {
-        const uint32_t a = draw(seed, draw0 + 2 * j, flag);
-        const uint32_t b = draw(seed, draw0 + 2 * j + 1, flag);
+    const uint64_t sa = draw0 + 2 * S_total, sb = sa + per * S_total, sc = sb + per * S_total;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+        const uint64_t g = j_first + j;
+        const uint32_t a = draw(seed, draw0 + 2 * g, flag);
+        const uint32_t b = draw(seed, draw0 + 2 * g + 1, flag);
         const uint32_t c = fp_mul(a, b);
-        share_lane(n, seed, sa + j * per, alpha, a, av, am, lanes, j, flag);
-        share_lane(n, seed, sb + j * per, alpha, b, bv, bm, lanes, j, flag);
-        share_lane(n, seed, sc + j * per, alpha, c, cv, cm, lanes, j, flag);
+        share_lane(n, seed, sa + g * per, alpha, a, av, am, pstride, j, flag);
+        share_lane(n, seed, sb + g * per, alpha, b, bv, bm, pstride, j, flag);
+        share_lane(n, seed, sc + g * per, alpha, c, cv, cm, pstride, j, flag);
     }
 }
 
@@ -625,15 +662,17 @@ __global__ void __launch_bounds__(kThreads) k_dealer_matvec(const uint32_t* A, c
 }
 
 // triple_store.cpp:274-283: mask j = share_random(1): clear draw, then share draws.
-__global__ void k_dealer_masks(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count, uint32_t* vals,
-                               uint32_t* macs, uint32_t* clear, unsigned int* flag) {
+// Masks [m_first, m_first+count) (triple_store.cpp:274-283): mask m = share_random(1):
+// one clear draw, then the share draws.  Party p's share of local mask j -> [p * pstride + j].
+__global__ void k_dealer_masks(int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t m_first, uint64_t count,
+                               uint64_t pstride, uint32_t* vals, uint32_t* macs, uint32_t* clear, unsigned int* flag) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t per = 1 + 2ull * (n - 1);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
-        const uint64_t base = draw0 + j * per;
+        const uint64_t base = draw0 + (m_first + j) * per;
         const uint32_t x = draw(seed, base, flag);
         clear[j] = x;
-        share_lane(n, seed, base + 1, alpha, x, vals, macs, count, j, flag);
+        share_lane(n, seed, base + 1, alpha, x, vals, macs, pstride, j, flag);
     }
 }
 
@@ -844,10 +883,12 @@ cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din
 }
 
 cudaError_t launch_dealer_triples(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
-                                  uint64_t lanes, uint32_t* const planes[6], unsigned int* flag, int sms) {
-    if (lanes == 0) return cudaSuccess;
-    k_dealer_triples<<<grid_for(lanes, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, lanes, planes[0], planes[1],
-                                                                    planes[2], planes[3], planes[4], planes[5], flag);
+                                  uint64_t S_total, uint64_t j_first, uint64_t count, uint64_t pstride,
+                                  uint32_t* const planes[6], unsigned int* flag, int sms) {
+    if (count == 0) return cudaSuccess;
+    k_dealer_triples<<<grid_for(count, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, S_total, j_first, count,
+                                                                    pstride, planes[0], planes[1], planes[2],
+                                                                    planes[3], planes[4], planes[5], flag);
     return launched();
 }
 
@@ -874,11 +915,12 @@ cudaError_t launch_dealer_matvec(cudaStream_t s, const uint32_t* A, const uint32
     return launched();
 }
 
-cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count,
-                                uint32_t* vals, uint32_t* macs, uint32_t* clear, unsigned int* flag, int sms) {
+cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                uint64_t m_first, uint64_t count, uint64_t pstride, uint32_t* vals, uint32_t* macs,
+                                uint32_t* clear, unsigned int* flag, int sms) {
     if (count == 0) return cudaSuccess;
-    k_dealer_masks<<<grid_for(count, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, count, vals, macs, clear,
-                                                                  flag);
+    k_dealer_masks<<<grid_for(count, sms, 16), kThreads, 0, s>>>(n, seed, draw0, alpha, m_first, count, pstride,
+                                                                  vals, macs, clear, flag);
     return launched();
 }
 

@@ -82,9 +82,11 @@ cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din
                            uint32_t* y0, uint32_t* y1);
 
 // GPU dealer (spdz.cpp:162-249), closed-form splitmix64 stream.
+// lanes [j_first, j_first+count) of Dealer::triples(S_total); party p's share of
+// local lane j at planes[k][p * pstride + j]
 cudaError_t launch_dealer_triples(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
-                                  uint64_t lanes, uint32_t* const planes[6], unsigned int* reject_flag, int sms);
-// party p's share of lane j goes to vals[p * pstride + j]
+                                  uint64_t S_total, uint64_t j_first, uint64_t count, uint64_t pstride,
+                                  uint32_t* const planes[6], unsigned int* reject_flag, int sms);
 cudaError_t launch_dealer_share(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
                                 const uint32_t* clear, uint64_t lanes, uint32_t* vals, uint32_t* macs,
                                 uint64_t pstride, unsigned int* reject_flag, int sms);
@@ -92,8 +94,10 @@ cudaError_t launch_dealer_uniform(cudaStream_t s, uint64_t seed, uint64_t draw0,
                                   uint32_t* out, unsigned int* reject_flag, int sms);
 cudaError_t launch_dealer_matvec(cudaStream_t s, const uint32_t* A, const uint32_t* B, uint32_t din, uint32_t rows,
                                  uint32_t* C);
-cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha, uint64_t count,
-                                uint32_t* vals, uint32_t* macs, uint32_t* clear, unsigned int* reject_flag, int sms);
+// masks [m_first, m_first+count); party p's share of local mask j at [p * pstride + j]
+cudaError_t launch_dealer_masks(cudaStream_t s, int n, uint64_t seed, uint64_t draw0, uint32_t alpha,
+                                uint64_t m_first, uint64_t count, uint64_t pstride, uint32_t* vals, uint32_t* macs,
+                                uint32_t* clear, unsigned int* reject_flag, int sms);
 
 // cleartext lane op (0 add 1 sub 2 mul) with scalar broadcast of either side
 cudaError_t launch_pub_binop(cudaStream_t s, int op, const uint32_t* a, bool a_bcast, const uint32_t* b, bool b_bcast,

@@ -41,6 +41,7 @@ struct Val {
 
 struct Region {  // preproc.hpp:44-53
     uint64_t base = 0, stride = 0, max_execs = 1;
+    uint64_t gbase = 0;  // global triple index of the region's first local lane (sharding)
 };
 
 struct Fault {
@@ -132,9 +133,13 @@ struct spdz_run {
     std::map<uint32_t, LinTiles> tiles;
     uint64_t scalar_total = 0, matrix_total = 0, mask_total = 0;
     std::vector<std::pair<uint32_t, uint32_t>> mshapes;  // (din, rows) per matrix triple (demand order)
-    std::map<uint32_t, uint64_t> input_mask_off;          // private input node -> first mask
+    std::map<uint32_t, uint64_t> input_mask_off;          // private input node -> first mask (local)
+    std::map<uint32_t, uint64_t> input_mask_gfirst;       // ... global index of that mask
+    uint64_t scalar_total_global = 0, mask_total_global = 0;
+    uint64_t shard_off = 0, shard_total = 0, shard_L = 0;  // shard_total == 0: unsharded
     std::map<uint32_t, std::vector<uint32_t>> inputs;     // cleartext (host)
     std::map<uint32_t, uint32_t*> input_dev;              // cleartext staged on party 0's device
+    std::map<uint32_t, uint32_t*> input_diff;             // opened x - mask (party 0's device)
     std::vector<void*> allocs;                            // (device, ptr)
     std::vector<int> alloc_dev;
     std::vector<Fault> faults;
@@ -145,6 +150,11 @@ struct spdz_run {
     bool host_out_owned = false;
     uint64_t exchanged = 0;
     cudaEvent_t ev_input = nullptr;
+    cudaEvent_t ev_opened = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    bool in_flight = false;
+    uint64_t launches0 = 0;
+    std::chrono::steady_clock::time_point wall0;
 
     uint32_t* alloc(int party, uint64_t words) {
         const int dev = devices[party];
@@ -183,25 +193,39 @@ cudaEvent_t new_event(spdz_run* r, int p) {
 
 // ---- planning (run creation) ----
 void plan_layout(spdz_run* r) {
-    // preproc.cpp:84-163 for straight-line graphs (no loops: mult = 1)
+    // preproc.cpp:84-163 for straight-line graphs (no loops: mult = 1).  With lane
+    // sharding every vector node holds shard_L of shard_total global lanes; regions
+    // are laid out globally and this run keeps its slice (local compact pools).
+    const bool sh = r->shard_total != 0;
+    const uint64_t G = r->shard_total, off = r->shard_off;
     for (auto& n : r->nodes) {
         const uint32_t id = (uint32_t)(&n - r->nodes.data());
+        if (sh && n.lanes != 1 && n.lanes != r->shard_L && n.kind != SPDZ_NODE_NOP)
+            throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: every vector node must have the shard's lanes");
         switch (n.kind) {
             case SPDZ_NODE_MUL:
                 if (r->priv(n.operands[0]) && r->priv(n.operands[1])) {
-                    r->scalar[id] = {r->scalar_total, n.lanes, 1};
+                    Region g{r->scalar_total, n.lanes, 1, sh ? r->scalar_total_global + off : r->scalar_total};
+                    r->scalar[id] = g;
                     r->scalar_total += n.lanes;
+                    r->scalar_total_global += sh ? G : n.lanes;
                 }
                 break;
             case SPDZ_NODE_REDUCE_MUL: {
                 const auto& src = r->node(n.operands[0]);
+                if (sh) throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: reduce_mul is not lane-parallel");
                 if (src.is_private && src.lanes >= 1) {
-                    r->scalar[id] = {r->scalar_total, src.lanes - 1ull, 1};
+                    r->scalar[id] = {r->scalar_total, src.lanes - 1ull, 1, r->scalar_total};
                     r->scalar_total += src.lanes - 1ull;
+                    r->scalar_total_global += src.lanes - 1ull;
                 }
                 break;
             }
+            case SPDZ_NODE_REDUCE_ADD:
+                if (sh) throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: reduce_add is not lane-parallel");
+                break;
             case SPDZ_NODE_LINEAR:
+                if (sh) throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: linear layers are row-sharded separately");
                 if (r->priv(n.operands[0]) && r->priv(n.operands[1])) {
                     uint64_t nt = 0;
                     LinTiles lt;
@@ -227,7 +251,9 @@ void plan_layout(spdz_run* r) {
         const auto& n = r->nodes[id];
         if (n.kind == SPDZ_NODE_INPUT && n.is_private) {
             r->input_mask_off[id] = r->mask_total;
+            r->input_mask_gfirst[id] = sh ? r->mask_total_global + off : r->mask_total;
             r->mask_total += n.lanes;
+            r->mask_total_global += sh ? G : n.lanes;
         }
     }
 }
@@ -383,6 +409,8 @@ void plan_buffers(spdz_run* r) {
     }
     dev(r, 0);
     cuda_check(cudaEventCreateWithFlags(&r->ev_input, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&r->ev_opened, cudaEventDisableTiming), "event");
+    cuda_check(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking), "copy stream");
 }
 
 // ---- preprocessing: GPU dealer in make_dealer_stores order (triple_store.cpp:248-287) ----
@@ -400,8 +428,16 @@ void deal(spdz_run* r, uint64_t seed) {
         device_guard(ctx);
         cuda_check(cudaMemsetAsync(ctx->d_flag, 0, 4, ctx->stream), "memset flag");
         uint64_t k = n;  // Dealer ctor consumed n draws (spdz.cpp:162-173)
-        lk(launch_dealer_triples(ctx->stream, n, seed, k, alpha, S, dd.pool, ctx->d_flag, ctx->sms), "deal triples");
-        k += dealer_draws_triples(n, S);
+        // Dealer::triples(S_global); this run keeps each region's slice (compact local pool)
+        for (auto& [id, reg] : r->scalar) {
+            const uint64_t cnt = reg.stride * reg.max_execs;
+            uint32_t* planes[6];
+            for (int q = 0; q < 6; ++q) planes[q] = dd.pool[q] + reg.base;
+            lk(launch_dealer_triples(ctx->stream, n, seed, k, alpha, r->scalar_total_global, reg.gbase, cnt, S, planes,
+                                     ctx->d_flag, ctx->sms),
+               "deal triples");
+        }
+        k += dealer_draws_triples(n, r->scalar_total_global);
         // matrix triples in demand order: linear nodes by id, tiles in order
         for (auto& [id, reg] : r->matrix) {
             const auto& nd = r->node(id);
@@ -436,9 +472,12 @@ void deal(spdz_run* r, uint64_t seed) {
                 (void)reg;
             }
         }
-        lk(launch_dealer_masks(ctx->stream, n, seed, k, alpha, M, dd.mask_v, dd.mask_m, dd.mask_c, ctx->d_flag,
-                               ctx->sms),
-           "deal masks");
+        for (auto& [id, moff] : r->input_mask_off) {
+            const uint64_t cnt = r->node(id).lanes;
+            lk(launch_dealer_masks(ctx->stream, n, seed, k, alpha, r->input_mask_gfirst[id], cnt, M,
+                                   dd.mask_v + moff, dd.mask_m + moff, dd.mask_c + moff, ctx->d_flag, ctx->sms),
+               "deal masks");
+        }
         check_dealer_flag(ctx);
     }
     r->consumed = false;
@@ -498,29 +537,32 @@ void alloc_deals(spdz_run* r) {
     }
 }
 
+// kernel-class timing brackets on party p's stream (profile_kernels)
+int ktimer_begin(spdz_run* r, int p) {
+    if (!r->opts.profile_kernels) return -1;
+    cudaEvent_t a = r->kt.take(r->devices[p]);
+    dev(r, p);
+    lk(cudaEventRecord(a, S(r, p)), "record");
+    r->kt.recs.push_back({-1, r->devices[p], a, nullptr, 0});
+    return (int)r->kt.recs.size() - 1;
+}
+void ktimer_end(spdz_run* r, int p, int idx, int cls, uint64_t bytes) {
+    if (idx < 0) return;
+    cudaEvent_t b = r->kt.take(r->devices[p]);
+    lk(cudaEventRecord(b, S(r, p)), "record");
+    auto& rec = r->kt.recs[idx];
+    rec.cls = cls;
+    rec.b = b;
+    rec.bytes = bytes;
+}
+
 // ---- node execution (runtime.cpp:360-450) ----
 struct Exec {
     spdz_run* r;
     int ev_cursor[SPDZ_MAX_PARTIES] = {};
 
-    // kernel-class timing brackets on party p's stream
-    int tbegin(int p) {
-        if (!r->opts.profile_kernels) return -1;
-        cudaEvent_t a = r->kt.take(r->devices[p]);
-        dev(r, p);
-        lk(cudaEventRecord(a, S(r, p)), "record");
-        r->kt.recs.push_back({-1, r->devices[p], a, nullptr, 0});
-        return (int)r->kt.recs.size() - 1;
-    }
-    void tend(int p, int idx, int cls, uint64_t bytes) {
-        if (idx < 0) return;
-        cudaEvent_t b = r->kt.take(r->devices[p]);
-        lk(cudaEventRecord(b, S(r, p)), "record");
-        auto& rec = r->kt.recs[idx];
-        rec.cls = cls;
-        rec.b = b;
-        rec.bytes = bytes;
-    }
+    int tbegin(int p) { return ktimer_begin(r, p); }
+    void tend(int p, int idx, int cls, uint64_t bytes) { ktimer_end(r, p, idx, cls, bytes); }
 
     cudaEvent_t next_event(int p) { return r->parties[p].evs.at(ev_cursor[p]++); }
 
@@ -666,8 +708,9 @@ struct Exec {
             // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
             tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
             // log_open (runtime.cpp:224): records [d | e] with mac shares [x.m - a.m | y.m - b.m]
-            P.maclog.push_back({st.opened, st.xa.m, P.pool[1] + off, L, 0, batch, 0});
-            P.maclog.push_back({st.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, L});
+            const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
+            P.maclog.push_back({st.opened, st.xa.m, P.pool[1] + off, L, 0, batch, so, 2 * G});
+            P.maclog.push_back({st.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
         }
     }
 
@@ -729,8 +772,8 @@ struct Exec {
                 lk(launch_beaver_combine(S(r, p), lv.payload, lv.payload + pairs, pd, pe, k, tri, P.ctx->party,
                                          P.ctx->alpha, lv.zv, lv.zm, lv.opened, lv.opened + pairs, pairs, SMS(r, p)),
                    "combine");
-                P.maclog.push_back({lv.opened, lv.xm, P.pool[1] + off, pairs, 0, batch, 0});
-                P.maclog.push_back({lv.opened + pairs, lv.ym, P.pool[3] + off, pairs, 0, batch, pairs});
+                P.maclog.push_back({lv.opened, lv.xm, P.pool[1] + off, pairs, 0, batch, 0, 0});
+                P.maclog.push_back({lv.opened + pairs, lv.ym, P.pool[3] + off, pairs, 0, batch, pairs, 0});
             }
             used += pairs;
         }
@@ -804,8 +847,10 @@ struct Exec {
             } else
                 lk(launch_bcast(c->stream, b.v, b.m, st.bias_v, st.bias_m, dout, c->sms), "bcast");
             // mask_tile for every tile: [D (all rows) | E_t for every tile]
+            const int tk = tbegin(p);
             lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
             lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
+            tend(p, tk, SPDZ_KSTAT_MASK, 12 * cells + 12 * etot);
             sent[p] = next_event(p);
             lk(cudaEventRecord(sent[p], c->stream), "record");
         }
@@ -827,16 +872,19 @@ struct Exec {
                 ++k;
                 r->exchanged += (cells + etot) * 4;
             }
+            const int tk = tbegin(p);
             lk(launch_open_sum(c->stream, st.payload + cells, peersE, k, st.opened + cells, etot, c->sms), "open E");
             const uint32_t* m6[6] = {st.mA[0], st.mA[1], st.mB[0], st.mB[1], st.mC[0], st.mC[1]};
             lk(launch_matrix_combine(c->stream, din, dout, lt.rpt, st.payload, peers, k, m6, st.bias_v, st.bias_m,
                                      c->party, c->alpha, st.out.v, st.out.m, st.opened, c->sms),
                "k_matrix_combine");
+            // own D 4 + peer D 4k + A.v A.m 8 + opened D 4 per cell (B, E from cache)
+            tend(p, tk, SPDZ_KSTAT_COMBINE, (16 + 4ull * k) * cells);
             for (uint32_t t = 0; t < ntiles; ++t) {  // linear.cpp:113 log per tile: [D_t | E_t]
                 const uint64_t aoff = (uint64_t)lt.starts[t] * din, ct = (uint64_t)lt.counts[t] * din;
-                P.maclog.push_back({st.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0});
+                P.maclog.push_back({st.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
                 P.maclog.push_back({st.opened + cells + (uint64_t)t * din, x.m, st.mB[1] + (uint64_t)t * din, din, 0,
-                                    batch0 + t, ct});
+                                    batch0 + t, ct, 0});
             }
         }
     }
@@ -962,7 +1010,8 @@ struct Exec {
             const int tk = tbegin(p);
             lk(launch_open_sum(S(r, p), rv.v, peers, k, P.outputs, L, SMS(r, p)), "open root");
             tend(p, tk, SPDZ_KSTAT_OPEN, (8ull + 4ull * k) * L);
-            P.maclog.push_back({P.outputs, rv.m, nullptr, L, 0, batch, 0});
+            P.maclog.push_back({P.outputs, rv.m, nullptr, L, 0, batch, r->shard_off,
+                                r->shard_total ? r->shard_total : L});
         }
     }
 };
@@ -973,10 +1022,12 @@ uint64_t fresh_nonce() {
 }
 
 // runtime.cpp:467-506
-void mac_check(spdz_run* r, spdz_run_report_t* rep, Exec& ex) {
+void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t given_coin) {
     const int n = r->n;
     uint64_t coin = 0;
-    if (r->opts.fixed_coin) {
+    if (have_coin) {
+        coin = given_coin;
+    } else if (r->opts.fixed_coin) {
         coin = r->opts.coin;
     } else {  // commit to nonces, reveal, chain fnv1a64 (runtime.cpp:474-489)
         std::vector<uint64_t> nonce(n), commit(n);
@@ -996,9 +1047,9 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, Exec& ex) {
         assign_ranks(P.maclog.data(), P.maclog.size());
         uint64_t sbytes = 0;
         for (auto& sg : P.maclog) sbytes += sg.len * (sg.mac_b ? 12 : 8);
-        const int tk = ex.tbegin(p);
+        const int tk = ktimer_begin(r, p);
         mac_sigma_launch(P.ctx, P.maclog.data(), P.maclog.size(), coin, 0);
-        ex.tend(p, tk, SPDZ_KSTAT_SIGMA, sbytes);
+        ktimer_end(r, p, tk, SPDZ_KSTAT_SIGMA, sbytes);
         lk(cudaEventRecord(P.t1, P.ctx->stream), "t1");
     }
     std::vector<uint32_t> sig(n);
@@ -1011,6 +1062,7 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, Exec& ex) {
         if (rep) rep->sigmas[p] = sig[p];
     }
     if (rep) rep->coin = coin;
+    if (r->opts.external_mac_verify) return;  // partial sigmas: the caller sums shards and verifies
     int rc = spdz_verify_sigmas(sig.data(), nonce2.data(), commits.data(), n);
     if (rc) throw Error(rc, spdz_last_error());
 }
@@ -1022,10 +1074,12 @@ void share_inputs(spdz_run* r) {
         auto it = r->input_dev.find(id);
         need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
              "ShapeMismatch: no values bound for input node " + std::to_string(id));
-        uint32_t* x0 = it->second;  // cleartext on party 0's device (reduced in place)
+        uint32_t* x0 = it->second;  // reduced cleartext on party 0's device
+        uint32_t*& diff = r->input_diff[id];
+        if (!diff) diff = r->alloc(0, n.lanes);
         auto& P0 = r->parties[0];
         dev(r, 0);
-        lk(launch_pub_binop(P0.ctx->stream, 1, x0, false, P0.mask_c + off, false, x0, n.lanes, P0.ctx->sms),
+        lk(launch_pub_binop(P0.ctx->stream, 1, x0, false, P0.mask_c + off, false, diff, n.lanes, P0.ctx->sms),
            "x - r");
         cudaEvent_t ev = r->ev_input;
         lk(cudaEventRecord(ev, P0.ctx->stream), "record");
@@ -1034,8 +1088,8 @@ void share_inputs(spdz_run* r) {
             auto& o = P.ns[id].out;
             dev(r, p);
             if (p) lk(cudaStreamWaitEvent(P.ctx->stream, ev, 0), "wait");
-            lk(launch_public(P.ctx->stream, 0, P.mask_v + off, P.mask_m + off, x0, false, 0u, false, p, P.ctx->alpha,
-                             o.v, o.m, n.lanes, P.ctx->sms),
+            lk(launch_public(P.ctx->stream, 0, P.mask_v + off, P.mask_m + off, diff, false, 0u, false, p,
+                             P.ctx->alpha, o.v, o.m, n.lanes, P.ctx->sms),
                "add_public(diff)");
         }
         for (int p = 0; p < r->n; ++p) {
@@ -1109,6 +1163,13 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
                 if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
                 else cuda_check(e, "cudaDeviceEnablePeerAccess");
             }
+        if (r->opts.shard_total) {
+            r->shard_off = r->opts.shard_offset;
+            r->shard_total = r->opts.shard_total;
+            for (auto& nd : r->nodes)
+                if (nd.lanes > 1) r->shard_L = std::max<uint64_t>(r->shard_L, nd.lanes);
+            need(r->shard_off + r->shard_L <= r->shard_total, SPDZ_ERR_INVALID_ARGUMENT, "shard outside the circuit");
+        }
         plan_layout(r.get());
         plan_buffers(r.get());
         alloc_deals(r.get());
@@ -1131,6 +1192,9 @@ int spdz_run_destroy(spdz_run* r) {
         if (r->ev_input) {
             cudaSetDevice(r->devices[0]);
             cudaEventDestroy(r->ev_input);
+            cudaEventDestroy(r->ev_opened);
+            cudaStreamSynchronize(r->copy_stream);
+            cudaStreamDestroy(r->copy_stream);
         }
         for (auto e : r->kt.pool) cudaEventDestroy(e);
         for (size_t i = 0; i < r->allocs.size(); ++i) {
@@ -1184,15 +1248,16 @@ int spdz_run_share_inputs(spdz_run* r) {
     });
 }
 
-int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
+int spdz_run_online_begin(spdz_run* r, int reuse) {
     return guard([&] {
         need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        need(!r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "online phase already begun (call spdz_run_mac_check)");
         if (r->consumed && !reuse)
             throw Error(SPDZ_ERR_TRIPLE_EXHAUSTED,
                         "TripleExhausted: preprocessing of this run was already consumed (deal again)");
-        const uint64_t launches0 = g_kernel_launches;
+        r->launches0 = g_kernel_launches;
         r->exchanged = 0;
-        auto t0 = std::chrono::steady_clock::now();
+        r->wall0 = std::chrono::steady_clock::now();
         for (auto& P : r->parties) {
             P.maclog.clear();
             device_guard(P.ctx);
@@ -1204,8 +1269,8 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
         ex.run_nodes();
         ex.open_root();
         r->consumed = true;
-        mac_check(r, rep, ex);  // also records t1 and synchronises
-        // outputs to host (party 0; all parties hold the same opened values)
+        r->in_flight = true;
+        // opened outputs to host on a copy stream, overlapping the MAC check
         const Val& rv = r->parties[0].ns[r->root].out;
         dev(r, 0);
         if (!r->host_out || r->host_out_cap < rv.lanes) {
@@ -1216,12 +1281,23 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
             r->host_out_owned = true;
         }
         r->host_out_len = rv.lanes;
-        lk(cudaMemcpyAsync(r->host_out, r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost, S(r, 0)),
+        lk(cudaEventRecord(r->ev_opened, S(r, 0)), "record opened");
+        lk(cudaStreamWaitEvent(r->copy_stream, r->ev_opened, 0), "wait opened");
+        lk(cudaMemcpyAsync(r->host_out, r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost, r->copy_stream),
            "D2H out");
-        lk(cudaStreamSynchronize(S(r, 0)), "sync out");
+    });
+}
+
+int spdz_run_mac_check(spdz_run* r, int use_coin, uint64_t coin, spdz_run_report_t* rep) {
+    return guard([&] {
+        need(r != nullptr && r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "no online phase in flight");
+        r->in_flight = false;
+        mac_check(r, rep, use_coin != 0, coin);  // records t1 and synchronises the party streams
+        dev(r, 0);
+        lk(cudaStreamSynchronize(r->copy_stream), "sync out");
         auto t1 = std::chrono::steady_clock::now();
         if (rep) {
-            rep->online_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+            rep->online_ms = std::chrono::duration<double, std::milli>(t1 - r->wall0).count();
             double dmax = 0;
             for (auto& P : r->parties) {
                 device_guard(P.ctx);
@@ -1233,8 +1309,8 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
             rep->scalar_triples_consumed = r->scalar_total;
             rep->matrix_triples_consumed = r->matrix_total;
             rep->bytes_exchanged = r->exchanged;
-            rep->output_digest = spdz_fnv1a64(r->host_out, r->host_out_len * 4, 1469598103934665603ull);
-            rep->kernel_launches = g_kernel_launches - launches0;
+            rep->output_digest = 0;  // spdz_run_output_digest (host byte loop, outside the online phase)
+            rep->kernel_launches = g_kernel_launches - r->launches0;
             for (int c = 0; c < SPDZ_KSTAT_N; ++c) rep->kstat[c] = spdz_kernel_stat_t{0, 0.0, 0};
             for (auto& rec : r->kt.recs) {
                 if (rec.cls < 0 || !rec.b) continue;
@@ -1250,12 +1326,25 @@ int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
     });
 }
 
+int spdz_run_online(spdz_run* r, int reuse, spdz_run_report_t* rep) {
+    int rc = spdz_run_online_begin(r, reuse);
+    if (rc) return rc;
+    return spdz_run_mac_check(r, 0, 0, rep);
+}
+
 int spdz_run_outputs(spdz_run* r, uint32_t* host_out, uint64_t cap, uint64_t* len) {
     return guard([&] {
         need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
         if (len) *len = r->host_out_len;
         if (host_out && host_out != r->host_out)
             std::memcpy(host_out, r->host_out, std::min<uint64_t>(cap, r->host_out_len) * 4);
+    });
+}
+
+int spdz_run_output_digest(spdz_run* r, uint64_t* digest) {
+    return guard([&] {  // runtime.cpp:573-574 (computed after the online phase, as the reference does)
+        need(r != nullptr && digest != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "bad digest args");
+        *digest = spdz_fnv1a64(r->host_out, r->host_out_len * 4, 1469598103934665603ull);
     });
 }
 

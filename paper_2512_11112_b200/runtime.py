@@ -158,6 +158,12 @@ class RunReport:
     coin: int
     kstat: dict = None  # kernel class -> {launches, ms, bytes} (profile_kernels)
 
+    def __post_init__(self):
+        if self.output_digest is None:  # runtime.cpp:573-574, host side, after the online phase
+            from ._lib import lib as _l
+            self.output_digest = _l().spdz_fnv1a64(self.outputs.ctypes.data, self.outputs.size * 4,
+                                                   1469598103934665603)
+
 
 class LocalRun:
     """All n parties of one online phase, device resident.
@@ -166,7 +172,7 @@ class LocalRun:
 
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
-                 stream_per_party: bool = False):
+                 stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -175,6 +181,9 @@ class LocalRun:
         o.coin = coin or 0
         o.profile_kernels = int(profile_kernels)
         o.stream_per_party = int(stream_per_party)
+        if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
+            o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
+        o.external_mac_verify = int(external_mac_verify)
         for p in range(_lib.MAX_PARTIES):
             o.devices[p] = (devices[p] if devices and p < len(devices) else 0)
         self._nodes = graph.to_c()
@@ -210,9 +219,15 @@ class LocalRun:
         self._out = out
         check(lib().spdz_run_bind_output(self.h, out.ctypes.data, out.size))
 
-    def online(self, reuse: bool = False) -> RunReport:
+    def online(self, reuse: bool = False, coin_fn=None) -> RunReport:
+        """One online phase.  `coin_fn()` (optional) is called after the
+        openings to agree on the MAC-check coin (e.g. parallel.joint_coin)."""
         rep = _lib.RunReport()
-        check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
+        if coin_fn is None:
+            check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
+        else:
+            check(lib().spdz_run_online_begin(self.h, int(reuse)))
+            check(lib().spdz_run_mac_check(self.h, 1, int(coin_fn()), C.byref(rep)))
         n = C.c_uint64()
         check(lib().spdz_run_outputs(self.h, None, 0, C.byref(n)))
         if getattr(self, "_out", None) is not None:
@@ -221,7 +236,7 @@ class LocalRun:
             out = np.empty(n.value, np.uint32)
             check(lib().spdz_run_outputs(self.h, out.ctypes.data, n.value, C.byref(n)))
         return RunReport(out, rep.online_ms, rep.online_device_ms, rep.scalar_triples_consumed,
-                         rep.matrix_triples_consumed, rep.bytes_exchanged, rep.output_digest, rep.kernel_launches,
+                         rep.matrix_triples_consumed, rep.bytes_exchanged, None, rep.kernel_launches,
                          list(rep.sigmas)[: self.n], rep.coin,
                          {name: dict(launches=rep.kstat[i].launches, ms=rep.kstat[i].ms, bytes=rep.kstat[i].bytes)
                           for i, name in enumerate(_lib.KSTAT_NAMES)})

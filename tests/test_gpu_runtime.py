@@ -141,7 +141,7 @@ def test_large_chain_vs_cleartext(gpu, kind, n):
 
 
 def test_linear_4096_secret_secret_property(gpu):
-    """C4 shape (4096x4096, slice 262140 -> 64 tiles): opened output equals W x + b."""
+    """C4 shape (4096x4096, slice 262140 -> 66 tiles of 63 rows): opened output equals W x + b."""
     from paper_2512_11112_b200 import linear_graph, run_local
     din = dout = 4096
     x, W, b = O.rand_field_vec(din, 1), O.rand_field_vec(din * dout, 2), O.rand_field_vec(dout, 3)
@@ -155,5 +155,40 @@ def test_linear_4096_secret_secret_property(gpu):
     acc_hi = ((Wt * hi) % P).sum(1) % P
     want = ((acc_lo + acc_hi * 65536 % P) % P + torch.from_numpy(b.astype(np.int64)).cuda()) % P
     np.testing.assert_array_equal(rep.outputs, want.cpu().numpy().astype(np.uint32))
-    assert rep.matrix_triples_consumed == 64
+    assert rep.matrix_triples_consumed == len(O.plan_tiles(din, dout, 262140)) == 66  # 63 rows per tile
     assert sum(rep.sigmas) % P == 0
+
+
+@pytest.mark.parametrize("kind,world", [("heavy", 2), ("mixed", 3)])
+def test_lane_sharding_equals_unsharded_run(gpu, kind, world):
+    """Each lane shard deals exactly its slice of the global preprocessing and
+    logs MAC records with global ranks: concatenated outputs, node shares and
+    the per-party sum of sigma partials equal the unsharded run (the invariant
+    the multi-GPU path rests on)."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    from paper_2512_11112_b200.parallel import shard_range
+    n, coin = 1000, 0x1234ABCD
+    x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+    full = LocalRun(chain_graph(kind, n), 2, coin=coin)
+    full.bind_inputs({"x": x, "y": y})
+    full.share_inputs()
+    rf = full.online()
+    outs, sig = [], [0, 0]
+    for r in range(world):
+        off, L = shard_range(n, world, r)
+        sh = LocalRun(chain_graph(kind, L), 2, coin=coin, shard=(off, n), external_mac_verify=True)
+        sh.bind_inputs({"x": x[off:off + L], "y": y[off:off + L]})
+        sh.share_inputs()
+        rs = sh.online()
+        outs.append(rs.outputs.copy())
+        sig = [(sig[p] + rs.sigmas[p]) % P for p in range(2)]
+        for nid in (6, 7, 8, 9):
+            for p in range(2):
+                v, m = sh.node_share_host(p, nid)
+                fv, fm = full.node_share_host(p, nid)
+                np.testing.assert_array_equal(v, fv[off:off + L])
+                np.testing.assert_array_equal(m, fm[off:off + L])
+        sh.close()
+    np.testing.assert_array_equal(np.concatenate(outs), rf.outputs)
+    assert sig == rf.sigmas
+    full.close()
