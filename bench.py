@@ -185,7 +185,17 @@ def run_ours(args, world, rank, local):
     n_mul = 4 if args.kind == "heavy" else (2 if args.kind == "mixed" else 0)
     mults_step = n_mul * lanes
     g = chain_graph(args.kind, lanes)
-    run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1 + rank)
+    coin_fn = None
+    if world > 1:
+        # weak scaling: rank r holds lanes [r*lanes, (r+1)*lanes) of one global circuit; its
+        # preprocessing is exactly that slice of the global dealer output, MAC ranks are global,
+        # the coin is agreed after the openings and sigma partials are verified across ranks.
+        from paper_2512_11112_b200 import parallel
+        run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1,
+                       shard=(rank * lanes, world * lanes), external_mac_verify=True)
+        coin_fn = parallel.joint_coin
+    else:
+        run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1)
     rng = np.random.default_rng(1234 + rank)
     x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
     y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
@@ -198,9 +208,17 @@ def run_ours(args, world, rank, local):
         run.bind_inputs(inputs)
         run.share_inputs()
 
+    def step():
+        rep = run.online(coin_fn=coin_fn)
+        if world > 1:
+            parallel.verify_sharded_sigmas(rep.sigmas)
+        elif sum(rep.sigmas) % P != 0:
+            raise RuntimeError("MAC check did not verify")
+        return rep
+
     for w in range(args.warmup):
         prepare(100 + w)
-        run.online()
+        step()
     # ---- device-timed steps (inputs resident, value) ----
     sampler = ClockSampler(dev)
     sampler.start()
@@ -211,11 +229,9 @@ def run_ours(args, world, rank, local):
         prepare(1000 + k)
         torch.cuda.synchronize()
         barrier(world)
-        rep = run.online()
+        rep = step()
         torch.cuda.synchronize()
         barrier(world)
-        if sum(rep.sigmas) % P != 0:
-            raise RuntimeError("MAC check did not verify")
         dev_ms.append(rep.online_device_ms)
         launches += rep.kernel_launches
         for name, st in rep.kstat.items():
@@ -239,7 +255,7 @@ def run_ours(args, world, rank, local):
         t1 = time.perf_counter()
         run.share_inputs()
         t2 = time.perf_counter()
-        rep = run.online()               # includes D2H of the opened outputs
+        rep = step()                     # includes D2H of the opened outputs
         t3 = time.perf_counter()
         e2e_ms += (t3 - t0) * 1e3
         parts += np.array([t1 - t0, t2 - t1, t3 - t2]) * 1e3
@@ -280,7 +296,8 @@ def run_ours(args, world, rank, local):
                 "vs_baseline": None, "dtype": "u32 (F_p, p=2^32-5)", "data": "synthetic",
                 "config": {"workload": f"{args.kind} mul-chain (4 Beaver multiplies + root open + MAC check), "
                                        f"2 parties on each GPU, {lanes} lanes per GPU",
-                           "lanes_per_gpu": lanes, "parties": 2, "parallelism": f"lane-sharded x{world}",
+                           "lanes_per_gpu": lanes, "parties": 2,
+                           "parallelism": f"lane-sharded x{world} (2 parties per GPU, global MAC check)",
                            "l2": "working set >> 126 MB L2 (inputs larger than L2, no flush needed)",
                            "timed": "online phase only (dealer + input sharing between steps, untimed)"},
                 "clocks": clocks, "gpu_launches": launches,

@@ -118,6 +118,9 @@ int spdz_ctx_party(const spdz_ctx* ctx);
 int spdz_ctx_sync(spdz_ctx* ctx);
 /* backend.hpp:35 */
 int spdz_capability(const spdz_ctx* ctx, spdz_capability_t* out);
+/* Measured CUDA-core integer pipe rate on ctx's device: IMAD.WIDE.U32 per second
+ * (the roofline denominator of the CUDA-core modular GEMM) and all integer ops/s. */
+int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_int_per_s);
 /* Number of kernels this library launched on any context since load (evidence counter). */
 uint64_t spdz_kernel_launches(void);
 

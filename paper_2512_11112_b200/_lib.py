@@ -79,6 +79,7 @@ _SIGS = {
     "spdz_ctx_sync": (C.c_int, [vp]),
     "spdz_capability": (C.c_int, [vp, C.POINTER(Capability)]),
     "spdz_kernel_launches": (C.c_uint64, []),
+    "spdz_diag_imad_wide_rate": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "spdz_add_batch": (C.c_int, [vp, C.POINTER(Share), C.POINTER(Share), C.POINTER(Share)]),
     "spdz_sub_batch": (C.c_int, [vp, C.POINTER(Share), C.POINTER(Share), C.POINTER(Share)]),
     "spdz_mul_mask": (C.c_int, [vp, C.POINTER(Share), C.POINTER(Share), C.POINTER(Triple), vp, vp]),

@@ -1,0 +1,61 @@
+// Diagnostics: measured integer-pipe peak of the CUDA cores on this device
+// (the denominator for the CUDA-core modular GEMM's roofline; MEASURED_PEAKS
+// only holds HBM and bf16 numbers).  Each thread runs 8 independent
+// IMAD.WIDE.U32 chains (u64 += u32*u32), so the fma pipe, not latency, bounds it.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_imad_wide_peak(uint32_t iters, uint32_t seed, unsigned long long* sink) {
+    uint32_t a[8];
+    unsigned long long acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        a[k] = seed * (threadIdx.x + 1) + k * 0x9e3779b9u;
+        acc[k] = k;
+    }
+    const uint32_t b = seed ^ blockIdx.x;
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += (unsigned long long)a[k] * b;  // IMAD.WIDE.U32
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] += (uint32_t)acc[k];                // keep the chains live
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= acc[k];
+    if (s == 0x123456789ull) sink[0] = s;
+}
+
+}  // namespace
+
+using namespace spdzb200;
+
+extern "C" int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_int_per_s) {
+    return guard([&] {
+        need(ctx && wide_per_s, SPDZ_ERR_INVALID_ARGUMENT, "bad diag args");
+        device_guard(ctx);
+        unsigned long long* sink = ctx->d_acc + 8;
+        const uint32_t iters = 4096;
+        const int grid = ctx->sms * 8;
+        cudaEvent_t e0, e1;
+        cuda_check(cudaEventCreate(&e0), "ev");
+        cuda_check(cudaEventCreate(&e1), "ev");
+        k_imad_wide_peak<<<grid, 256, 0, ctx->stream>>>(64, 7u, sink);  // warm
+        cuda_check(cudaEventRecord(e0, ctx->stream), "rec");
+        k_imad_wide_peak<<<grid, 256, 0, ctx->stream>>>(iters, 7u, sink);
+        cuda_check(cudaEventRecord(e1, ctx->stream), "rec");
+        cuda_check(cudaEventSynchronize(e1), "sync");
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double threads = double(grid) * 256;
+        *wide_per_s = threads * iters * 8 / (ms / 1e3);
+        if (total_int_per_s) *total_int_per_s = threads * iters * 16 / (ms / 1e3);  // + the IADD chain
+    });
+}

@@ -336,17 +336,31 @@ __global__ void __launch_bounds__(kThreads) k_pair_split(const uint32_t* __restr
 // sigma = S_m - alpha * S_x with S_m = sum r_j m_j and S_x = sum r_j x_j (two
 // lazily folded accumulators, one alpha-multiply per CTA instead of per record).
 // Four records per thread per step from 128-bit loads issued before the math.
-__device__ __forceinline__ void sigma_rec(uint64_t z, uint32_t x, uint32_t m, unsigned long long& sm,
-                                          unsigned long long& sx) {
+// 96-bit accumulator: lo (u64) + count of 2^64 carries (2^64 == 25 mod p).  The
+// carry-counting add runs on the ALU pipe, keeping the fma-heavy pipe for the
+// 64-bit multiplies of splitmix64 and the two products.
+struct Acc96 {
+    unsigned long long lo = 0;
+    uint32_t hi = 0;
+    __device__ __forceinline__ void add(unsigned long long v) {
+        lo += v;
+        hi += (lo < v) ? 1u : 0u;
+    }
+    __device__ __forceinline__ uint32_t mod() const {
+        return fp_reduce64((unsigned long long)fp_reduce64(lo) + (unsigned long long)hi * 25ull);
+    }
+};
+
+__device__ __forceinline__ void sigma_rec(uint64_t z, uint32_t x, uint32_t m, Acc96& sm, Acc96& sx) {
     const uint32_t r = fp_reduce64(mix64(z));
-    sm += fold1(mul_wide(r, m));
-    sx += fold1(mul_wide(r, x));
+    sm.add(mul_wide(r, m));
+    sx.add(mul_wide(r, x));
 }
 
 __global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restrict__ segs,
                                                         const MacChunk* __restrict__ chunks, uint32_t n_chunks,
                                                         uint64_t coin, uint32_t alpha, unsigned long long* acc) {
-    unsigned long long sm = 0ull, sx = 0ull;
+    Acc96 sm, sx;
     for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
         const MacChunk ch = chunks[c];
         const MacSegDev sg = segs[ch.seg];
@@ -382,11 +396,9 @@ __global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restr
             if (mb) m = fp_sub(m, __ldcs(mb + i));
             sigma_rec(z0 + (uint64_t)i * kGamma, __ldcs(xv + i), m, sm, sx);
         }
-        sm = fold1(sm);  // per chunk a thread adds <= 64 terms < 6*2^32
-        sx = fold1(sx);
     }
-    // sigma partial of this thread: S_m - alpha * S_x (mod p)
-    unsigned long long s[1] = {fp_sub(fp_reduce64(sm), fp_mul(alpha, fp_reduce64(sx)))};
+    // sigma partial of this thread: S_m - alpha * S_x (mod p); carries < 2^32 per thread
+    unsigned long long s[1] = {fp_sub(sm.mod(), fp_mul(alpha, sx.mod()))};
     block_sum<1>(s);
     if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
 }

@@ -152,17 +152,19 @@ class RunReport:
     scalar_triples_consumed: int
     matrix_triples_consumed: int
     bytes_exchanged: int
-    output_digest: int
+    output_digest_cached: int
     kernel_launches: int
     sigmas: list
     coin: int
     kstat: dict = None  # kernel class -> {launches, ms, bytes} (profile_kernels)
 
-    def __post_init__(self):
-        if self.output_digest is None:  # runtime.cpp:573-574, host side, after the online phase
-            from ._lib import lib as _l
-            self.output_digest = _l().spdz_fnv1a64(self.outputs.ctypes.data, self.outputs.size * 4,
-                                                   1469598103934665603)
+    @property
+    def output_digest(self) -> int:
+        """fnv1a64 of the opened outputs (runtime.cpp:573-574), computed on first access."""
+        if self.output_digest_cached is None:
+            self.output_digest_cached = lib().spdz_fnv1a64(self.outputs.ctypes.data, self.outputs.size * 4,
+                                                           1469598103934665603)
+        return self.output_digest_cached
 
 
 class LocalRun:
