@@ -126,20 +126,29 @@ def main():
     xs = DeviceShare(torch.from_numpy(rnd(din * batch, 2)).cuda(), torch.from_numpy(rnd(din * batch, 3)).cuda())
     ys = DeviceShare.empty(dout * batch)
     args_c = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
-    for _ in range(3):
-        check(lib().spdz_linear_secret_public(*args_c))
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = 20
-    e0.record()
-    for _ in range(iters):
-        check(lib().spdz_linear_secret_public(*args_c))
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / iters
     modmacs = 2 * din * dout * batch  # two planes
-    c3 = {"shape": [dout, din, batch], "kernel_ms": ms, "modmac_per_s": modmacs / (ms / 1e3),
-          "int_ops_per_s": 2 * modmacs / (ms / 1e3), "path": "CUDA-core k_modgemm (2 IMAD.WIDE per modMAC)"}
+    wide, tot = C.c_double(), C.c_double()
+    check(lib().spdz_diag_imad_wide_rate(ctx.h, C.byref(wide), C.byref(tot)))
+    c3 = {"shape": [dout, din, batch], "modmacs": modmacs, "imad_wide_peak_per_s": wide.value}
+    for path, name in ((1, "cuda_core"), (2, "tcgen05")):
+        check(lib().spdz_set_gemm_path(path))
+        for _ in range(3):
+            check(lib().spdz_linear_secret_public(*args_c))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters = 20
+        e0.record()
+        for _ in range(iters):
+            check(lib().spdz_linear_secret_public(*args_c))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        c3[name] = {"ms": ms, "modmac_per_s": modmacs / (ms / 1e3)}
+    check(lib().spdz_set_gemm_path(0))
+    c3["cuda_core"]["imad_wide_frac"] = 2 * c3["cuda_core"]["modmac_per_s"] / wide.value
+    # tensor pipe: 16 u8 x u8 MACs per modMAC; dense int8 peak 4.5 POPS = 2.25e15 MAC/s (nominal, B200)
+    c3["tcgen05"]["i8_mac_per_s"] = 16 * c3["tcgen05"]["modmac_per_s"]
+    c3["tcgen05"]["frac_of_nominal_i8"] = c3["tcgen05"]["i8_mac_per_s"] / 2.25e15
     if not args.no_ref:
         lin = {"x": rnd(din, 4), "W": rnd(din * dout, 5), "b": rnd(dout, 6)}
         one = ref_online(workloads.linear_ir(din, dout, w_private=False), lin, threads)

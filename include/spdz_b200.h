@@ -204,6 +204,9 @@ int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t*
  * on both planes.  w_public != 0: W public (w_vals), X secret (x->vals/x->macs,
  * row-major din x batch).  w_public == 0: W secret (w->vals/w->macs), X public
  * (x_pub).  Y row-major dout x batch.  Bias is a separate spdz_add_batch. */
+/* Contraction path of spdz_linear_secret_public: 0 auto (tcgen05 kind::i8 limb GEMM
+ * when din <= 8192, else CUDA cores), 1 CUDA-core IMAD.WIDE GEMM, 2 tcgen05 only. */
+int spdz_set_gemm_path(int path);
 int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32_t batch, int w_public,
                               const uint32_t* w_vals, const spdz_share_t* w_secret, const spdz_share_t* x_secret,
                               const uint32_t* x_pub, spdz_share_t* y);

@@ -104,6 +104,7 @@ _SIGS = {
     "spdz_matrix_open_combine": (C.c_int, [vp, C.POINTER(MTriple), vp, C.POINTER(vp), C.c_int, C.POINTER(Share),
                                            C.POINTER(Share), vp]),
     "spdz_matrix_combine": (C.c_int, [vp, C.POINTER(MTriple), vp, vp, C.POINTER(Share)]),
+    "spdz_set_gemm_path": (C.c_int, [C.c_int]),
     "spdz_linear_secret_public": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, vp, C.POINTER(Share),
                                             C.POINTER(Share), vp, C.POINTER(Share)]),
     "spdz_dealer_alpha": (C.c_int, [C.c_int, C.c_uint64, u32p, u32p]),

@@ -552,6 +552,28 @@ int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t*
     return guard([&] { matrix_combine_common(ctx, mt, D, nullptr, 0, nullptr, z, nullptr, E); });
 }
 
+static int g_gemm_path = 0;  // 0 auto (tcgen05 when K <= 8192), 1 CUDA-core, 2 tcgen05
+
+int spdz_set_gemm_path(int path) {
+    return guard([&] {
+        need(path >= 0 && path <= 2, SPDZ_ERR_INVALID_ARGUMENT, "gemm path must be 0, 1 or 2");
+        g_gemm_path = path;
+    });
+}
+
+static void modgemm_dispatch(spdz_ctx* ctx, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
+                             const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint32_t* y0, uint32_t* y1) {
+    const bool tc = g_gemm_path == 2 || (g_gemm_path == 0 && modgemm_tc_supported(din));
+    if (tc) {
+        need(modgemm_tc_supported(din), SPDZ_ERR_INVALID_ARGUMENT, "tcgen05 GEMM path needs 1 <= din <= 8192");
+        uint8_t* scratch = (uint8_t*)ctx->scratch.ensure(modgemm_tc_scratch_bytes(mode, dout, din, batch));
+        launch_ok(launch_modgemm_tc(ctx->stream, mode, dout, din, batch, w0, w1, x0, x1, y0, y1, scratch, ctx->sms),
+                  "k_modgemm_tc");
+    } else {
+        launch_ok(launch_modgemm(ctx->stream, mode, dout, din, batch, w0, w1, x0, x1, y0, y1), "k_modgemm");
+    }
+}
+
 int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32_t batch, int w_public,
                               const uint32_t* w_vals, const spdz_share_t* w_secret, const spdz_share_t* x_secret,
                               const uint32_t* x_pub, spdz_share_t* y) {
@@ -564,16 +586,14 @@ int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32
             need_share(x_secret, "x");
             check_lanes(x_secret->lanes, (uint64_t)din * batch);
             need(w_vals != nullptr || din == 0, SPDZ_ERR_INVALID_ARGUMENT, "null W");
-            launch_ok(launch_modgemm(ctx->stream, 0, dout, din, batch, w_vals, nullptr, x_secret->vals,
-                                     x_secret->macs, y->vals, y->macs),
-                      "k_modgemm");
+            modgemm_dispatch(ctx, 0, dout, din, batch, w_vals, nullptr, x_secret->vals, x_secret->macs, y->vals,
+                             y->macs);
         } else {
             need_share(w_secret, "w");
             check_lanes(w_secret->lanes, (uint64_t)din * dout);
             need(x_pub != nullptr || din == 0, SPDZ_ERR_INVALID_ARGUMENT, "null x");
-            launch_ok(launch_modgemm(ctx->stream, 1, dout, din, batch, w_secret->vals, w_secret->macs, x_pub, nullptr,
-                                     y->vals, y->macs),
-                      "k_modgemm");
+            modgemm_dispatch(ctx, 1, dout, din, batch, w_secret->vals, w_secret->macs, x_pub, nullptr, y->vals,
+                             y->macs);
         }
     });
 }

@@ -290,9 +290,27 @@ def test_matrix_mask_open_combine_two_party(gpu, golden):
         np.testing.assert_array_equal(H(z.macs), golden["mat_Zm"][i])
 
 
-@pytest.mark.parametrize("din,dout,batch", [(64, 32, 1), (96, 80, 5), (1024, 1024, 256), (40000, 3, 2)])
-def test_linear_secret_public_vs_oracle(gpu, din, dout, batch):
-    """runtime.cpp:303-334, batched over `batch` input columns; K=40000 crosses the accumulator fold."""
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("din,dout,batch", [(64, 32, 1), (96, 80, 5), (1024, 1024, 256), (200, 130, 70),
+                                            (8192, 40, 3), (40000, 3, 2)])
+def test_linear_secret_public_vs_oracle(gpu, din, dout, batch, path):
+    """runtime.cpp:303-334, batched over `batch` input columns, on both contraction
+    paths (1 = CUDA-core IMAD.WIDE, 2 = tcgen05 kind::i8 limb GEMM; K=8192 is the
+    tcgen05 exactness limit, K=40000 crosses the CUDA-core accumulator fold)."""
+    import ctypes as C
+    from paper_2512_11112_b200 import DeviceShare
+    from paper_2512_11112_b200._lib import check, lib
+    from paper_2512_11112_b200.backend import dshare
+    if path == 2 and din > 8192:
+        pytest.skip("tcgen05 path covers din <= 8192")
+    check(lib().spdz_set_gemm_path(path))
+    try:
+        _linear_secret_public_case(din, dout, batch)
+    finally:
+        check(lib().spdz_set_gemm_path(0))
+
+
+def _linear_secret_public_case(din, dout, batch):
     import ctypes as C
     from paper_2512_11112_b200 import DeviceShare
     from paper_2512_11112_b200._lib import check, lib
