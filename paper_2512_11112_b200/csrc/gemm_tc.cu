@@ -9,10 +9,11 @@
 //   2^0, 2^8, 2^16, 2^24, 2^32 = 5, 2^40 = 1280, 2^48 = 327680 (mod p).
 // Exactness: P_3 sums 4 limb products over K, 4 * 255^2 * K < 2^31 for K <= 8192.
 //
-// Operands are staged as u8 limb planes, K-major, padded to the tile (k_split_*),
-// copied to shared memory with cp.async in the canonical no-swizzle K-major
-// UMMA layout (8-row x 16-byte core matrices), double buffered against the MMAs;
-// one elected thread issues the MMAs and tcgen05.commit releases a stage.
+// Operands are re-laid out once per call (k_tile_rows / k_tile_cols) as u8 limb
+// tiles already in the canonical no-swizzle K-major UMMA image (8-row x 16-byte
+// core matrices), so each K stage is two 1-D TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx) into a 4-stage ring; warp 0 produces, one thread of
+// warp 1 issues the MMAs, tcgen05.commit frees a stage, all warps run the epilogue.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,15 +47,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         if (done) return;
     }
     __trap();
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
 // SMEM matrix descriptor, K-major, SWIZZLE_NONE (layout type 0), sm100 version 1.
@@ -99,43 +91,36 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // Shared-memory image of one limb tile (rows x TK bytes), canonical K-major
 // no-swizzle layout: byte (r, k) at (r/8)*SBO + (k/16)*LBO + (r%8)*16 + k%16.
+// The split kernels write the operands into global memory already in this image,
+// tile by tile, so one K stage is two contiguous 1-D TMA bulk copies.
 constexpr uint32_t kLBO = 128;                 // next 16-byte K chunk
 constexpr uint32_t kSBO = (TK / 16) * 128;     // next 8-row group
+constexpr int kStages = 4;
 
 template <int BN>
 struct TcSmem {
     static constexpr uint32_t A_LIMB = TM * TK;              // 8 KB
     static constexpr uint32_t B_LIMB = BN * TK;
-    static constexpr uint32_t STAGE = 4 * A_LIMB + 4 * B_LIMB;
-    static constexpr uint32_t BYTES = 2 * STAGE + 1024;      // + barriers / tmem slot
+    static constexpr uint32_t A_STAGE = 4 * A_LIMB;
+    static constexpr uint32_t B_STAGE = 4 * B_LIMB;
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    static constexpr uint32_t BYTES = kStages * STAGE + 2048; // + barriers / tmem slot + alignment
     static constexpr uint32_t TMEM_COLS = (7 * BN <= 256) ? 256 : 512;
 };
 
-// Copies one K stage of the A and B limb planes into shared memory.
-// A limb plane: [Mp][Kp] bytes; B limb plane: [Np][Kp] bytes (both K-major).
-template <int BN>
-__device__ __forceinline__ void load_stage(uint32_t sbase, const uint8_t* __restrict__ A, const uint8_t* __restrict__ B,
-                                           uint64_t Mp, uint64_t Np, uint32_t Kp, uint32_t m0, uint32_t n0,
-                                           uint32_t k0) {
-    using L = TcSmem<BN>;
-    // A: 4 limbs x 128 rows x 4 chunks of 16 B
-    for (uint32_t c = threadIdx.x; c < 4u * TM * (TK / 16); c += blockDim.x) {
-        const uint32_t limb = c / (TM * (TK / 16));
-        const uint32_t rem = c % (TM * (TK / 16));
-        const uint32_t r = rem / (TK / 16), kc = rem % (TK / 16);
-        const uint8_t* src = A + (uint64_t)limb * Mp * Kp + (uint64_t)(m0 + r) * Kp + k0 + kc * 16;
-        const uint32_t dst = sbase + limb * L::A_LIMB + (r >> 3) * kSBO + kc * kLBO + (r & 7) * 16;
-        cp_async16(dst, src);
-    }
-    const uint32_t bbase = sbase + 4 * L::A_LIMB;
-    for (uint32_t c = threadIdx.x; c < 4u * BN * (TK / 16); c += blockDim.x) {
-        const uint32_t limb = c / (BN * (TK / 16));
-        const uint32_t rem = c % (BN * (TK / 16));
-        const uint32_t r = rem / (TK / 16), kc = rem % (TK / 16);
-        const uint8_t* src = B + (uint64_t)limb * Np * Kp + (uint64_t)(n0 + r) * Kp + k0 + kc * 16;
-        const uint32_t dst = bbase + limb * L::B_LIMB + (r >> 3) * kSBO + kc * kLBO + (r & 7) * 16;
-        cp_async16(dst, src);
-    }
+__device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
+    return (r >> 3) * kSBO + (k >> 4) * kLBO + (r & 7) * 16 + (k & 15);
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // out plane mapping of C[row][col] (see launch_modgemm_tc)
@@ -146,23 +131,28 @@ struct TcOut {
     uint32_t* y1;
 };
 
+// Warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer, all 4 warps = epilogue.
+// A tiles: [Mp/128][KB] blocks of A_STAGE bytes; B tiles: [Np/BN][KB] blocks of B_STAGE bytes.
 template <int BN>
-__global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ A, const uint8_t* __restrict__ B,
-                                                               uint32_t M, uint32_t N, uint64_t Mp, uint64_t Np, uint32_t Kp,
-                                                               TcOut out) {
+__global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At, const uint8_t* __restrict__ Bt,
+                                                               uint32_t M, uint32_t N, uint32_t KB, TcOut out) {
     using L = TcSmem<BN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
     uint8_t* sgen = smem + (sbase - smem_u32(smem));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sgen + 2 * L::STAGE);  // [0..1] stage free, [2] final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + 2 * L::STAGE + 64);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sgen + kStages * L::STAGE);
+    uint64_t* empty = full + kStages;
+    uint64_t* done = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t m0 = blockIdx.y * TM, n0 = blockIdx.x * BN;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -175,28 +165,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    const uint32_t nkb = Kp / TK;
-    const uint32_t idesc = idesc_i8<BN>();
-    uint32_t uses[2] = {0, 0};
-    load_stage<BN>(sbase, A, B, Mp, Np, Kp, m0, n0, 0);
-    cp_async_commit();
-    uint32_t inited = 0;  // issuing thread: accumulators already written
-    for (uint32_t kb = 0; kb < nkb; ++kb) {
-        const uint32_t st = kb & 1;
-        if (kb + 1 < nkb) {
-            const uint32_t ns = st ^ 1;
-            if (uses[ns]) mbar_wait(&bars[ns], (uses[ns] - 1) & 1);  // MMAs of kb-1 released it
-            load_stage<BN>(sbase + ns * L::STAGE, A, B, Mp, Np, Kp, m0, n0, (kb + 1) * TK);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    if (warp == 0 && lane == 0) {  // ---- TMA producer ----
+        const uint8_t* a_src = At + (uint64_t)blockIdx.y * KB * L::A_STAGE;
+        const uint8_t* b_src = Bt + (uint64_t)blockIdx.x * KB * L::B_STAGE;
+        for (uint32_t kb = 0; kb < KB; ++kb) {
+            const uint32_t s = kb % kStages;
+            if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+            mbar_expect_tx(&full[s], L::STAGE);
+            const uint32_t dst = sbase + s * L::STAGE;
+            bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
+            bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async writes -> tensor core
-        __syncthreads();
-        if (threadIdx.x == 0) {
+    } else if (warp == 1 && lane == 0) {  // ---- MMA issuer ----
+        const uint32_t idesc = idesc_i8<BN>();
+        uint32_t inited = 0;
+        for (uint32_t kb = 0; kb < KB; ++kb) {
+            const uint32_t s = kb % kStages;
+            mbar_wait(&full[s], (kb / kStages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t sa = sbase + st * L::STAGE, sb = sa + 4 * L::A_LIMB;
+            const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
 #pragma unroll
             for (int ks = 0; ks < TK / 32; ++ks) {
 #pragma unroll
@@ -204,20 +191,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     const uint64_t ad = smem_desc(sa + i * L::A_LIMB + ks * 2 * kLBO, kLBO, kSBO);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int s = i + j;
+                        const int t = i + j;
                         const uint64_t bd = smem_desc(sb + j * L::B_LIMB + ks * 2 * kLBO, kLBO, kSBO);
-                        mma_i8(tmem + s * BN, ad, bd, idesc, (inited >> s) & 1u);
-                        inited |= 1u << s;
+                        mma_i8(tmem + t * BN, ad, bd, idesc, (inited >> t) & 1u);
+                        inited |= 1u << t;
                     }
                 }
             }
-            mma_commit(&bars[st]);  // stage st may be overwritten once these MMAs complete
+            mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        uses[st] += 1;
-        __syncwarp();
+        mma_commit(done);
     }
-    if (threadIdx.x == 0) mma_commit(&bars[2]);
-    mbar_wait(&bars[2], 0);
+    __syncwarp();
+    mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
 
     // epilogue: TMEM lane = row (warp w owns lanes 32w..32w+31), column = n
@@ -228,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     for (int cc = 0; cc < BN / 16; ++cc) {
         uint32_t v[7][16];
 #pragma unroll
-        for (int s = 0; s < 7; ++s) tmem_ld16(lane_base + s * BN + cc * 16, v[s]);
+        for (int t = 0; t < 7; ++t) tmem_ld16(lane_base + t * BN + cc * 16, v[t]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < M) {
 #pragma unroll
@@ -237,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                 if (col >= N) continue;
                 unsigned long long acc = 0;
 #pragma unroll
-                for (int s = 0; s < 7; ++s) acc += (unsigned long long)v[s][t] * kPow[s];
+                for (int q = 0; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
                 const uint32_t r = fp_reduce64(acc);
                 if (out.mode == 0) {
                     if (col < out.batch) out.y0[(uint64_t)row * out.batch + col] = r;
@@ -255,66 +241,100 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
 }
 
-// A limb planes (K-major): out[i][m][k] = byte i of A(m, k), zero padded to Mp x Kp.
-// A(m, k) = a0[m*K + k] for m < M0, a1[(m-M0)*K + k] for M0 <= m < M (row stacking).
-__global__ void k_split_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1, uint32_t M0, uint32_t M,
-                             uint32_t K, uint64_t Mp, uint32_t Kp, uint8_t* __restrict__ out) {
-    const uint64_t total = Mp * Kp / 4;  // 4 k per thread
-    const uint64_t plane = Mp * Kp;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t m = (t * 4) / Kp;
-        const uint32_t k = (uint32_t)((t * 4) % Kp);
-        uint32_t w[4];
+// A (rows, stacked a0 over a1) -> pre-tiled limb image: one thread per (row, 16-k chunk).
+// A(m, k) = a0[m*K + k] for m < M0, a1[(m-M0)*K + k] for M0 <= m < M; zero padded.
+__global__ void k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1, uint32_t M0, uint32_t M,
+                            uint32_t K, uint32_t Mp, uint32_t KB, uint8_t* __restrict__ out) {
+    const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < chunks; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t kc_all = (uint32_t)(t % ((uint64_t)KB * (TK / 16)));
+        const uint32_t m = (uint32_t)(t / ((uint64_t)KB * (TK / 16)));
+        const uint32_t k0 = kc_all * 16;
+        uint32_t w[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t kk = k + q;
-            w[q] = (m < M && kk < K) ? (m < M0 ? a0[m * K + kk] : a1[(m - M0) * K + kk]) : 0u;
+        for (int q = 0; q < 16; ++q) {
+            const uint32_t k = k0 + q;
+            w[q] = (m < M && k < K) ? (m < M0 ? a0[(uint64_t)m * K + k] : a1[(uint64_t)(m - M0) * K + k]) : 0u;
         }
+        const uint32_t mt = m / TM, r = m % TM, kb = k0 / TK, kk = k0 % TK;
+        uint8_t* blk = out + ((uint64_t)mt * KB + kb) * (4u * TM * TK);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint32_t packed = ((w[0] >> (8 * i)) & 0xFF) | (((w[1] >> (8 * i)) & 0xFF) << 8) |
-                                    (((w[2] >> (8 * i)) & 0xFF) << 16) | (((w[3] >> (8 * i)) & 0xFF) << 24);
-            reinterpret_cast<uint32_t*>(out + i * plane + m * Kp + k)[0] = packed;
+            uint32_t p[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                p[q] = ((w[4 * q] >> (8 * i)) & 0xFF) | (((w[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
+                       (((w[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((w[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
+            *reinterpret_cast<uint4*>(blk + i * (TM * TK) + core_off(r, kk)) = make_uint4(p[0], p[1], p[2], p[3]);
         }
     }
 }
 
-// B limb planes transposed to K-major: out[j][n][k] = byte j of B(k, n), zero padded.
-// B(k, n) = b0[k*NB + n] for n < NB, b1[k*NB + n - NB] for NB <= n < N (column stacking).
-__global__ void k_split_cols_t(const uint32_t* __restrict__ b0, const uint32_t* __restrict__ b1, uint32_t NB, uint32_t N,
-                               uint32_t K, uint64_t Np, uint32_t Kp, uint8_t* __restrict__ out) {
-    __shared__ uint32_t tile[32][33];
-    const uint64_t plane = Np * Kp;
-    const uint32_t kt = blockIdx.x * 32, nt = blockIdx.y * 32;
-    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {  // read rows k, coalesced over n
-        const uint32_t k = kt + yy, n = nt + threadIdx.x;
+// B (K x N, columns stacked b0 | b1) -> pre-tiled K-major limb image (transposed):
+// block = 64 k x 32 n through shared memory; one thread per (n, 16-k chunk) on the way out.
+template <int BN>
+__global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __restrict__ b1, uint32_t NB, uint32_t N,
+                            uint32_t K, uint32_t KB, uint8_t* __restrict__ out) {
+    __shared__ uint32_t tile[TK][33];
+    const uint32_t kb = blockIdx.x, nt32 = blockIdx.y * 32;
+    for (uint32_t e = threadIdx.x; e < TK * 32; e += blockDim.x) {
+        const uint32_t kk = e / 32, nn = e % 32;
+        const uint32_t k = kb * TK + kk, n = nt32 + nn;
         uint32_t v = 0;
         if (k < K && n < N) v = n < NB ? b0[(uint64_t)k * NB + n] : b1[(uint64_t)k * NB + (n - NB)];
-        tile[yy][threadIdx.x] = v;
+        tile[kk][nn] = v;
     }
     __syncthreads();
-    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {  // write rows n, coalesced over k
-        const uint32_t n = nt + yy, k = kt + threadIdx.x;
-        if (n < Np && k < Kp) {
-            const uint32_t v = tile[threadIdx.x][yy];
+    for (uint32_t c = threadIdx.x; c < 32 * (TK / 16); c += blockDim.x) {
+        const uint32_t nn = c / (TK / 16), kc = c % (TK / 16);
+        const uint32_t n = nt32 + nn;
+        const uint32_t nt = n / BN, r = n % BN;
+        uint8_t* blk = out + ((uint64_t)nt * KB + kb) * (4u * BN * TK);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) out[j * plane + (uint64_t)n * Kp + k] = (uint8_t)(v >> (8 * j));
+        for (int j = 0; j < 4; ++j) {
+            uint32_t p[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t base = kc * 16 + 4 * q;
+                p[q] = ((tile[base][nn] >> (8 * j)) & 0xFF) | (((tile[base + 1][nn] >> (8 * j)) & 0xFF) << 8) |
+                       (((tile[base + 2][nn] >> (8 * j)) & 0xFF) << 16) | (((tile[base + 3][nn] >> (8 * j)) & 0xFF) << 24);
+            }
+            *reinterpret_cast<uint4*>(blk + j * (BN * TK) + core_off(r, kc * 16)) = make_uint4(p[0], p[1], p[2], p[3]);
         }
     }
 }
 
 template <int BN>
-cudaError_t run_tc(cudaStream_t s, const uint8_t* Al, const uint8_t* Bl, uint32_t M, uint32_t N, uint64_t Mp,
-                   uint64_t Np, uint32_t Kp, const TcOut& out) {
+cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
+                   const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint8_t* scratch, const TcOut& out,
+                   int sms) {
     using L = TcSmem<BN>;
+    const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
+    const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
+    const uint32_t KB = (din + TK - 1) / TK;
+    uint8_t* At = scratch;
+    uint8_t* Bt = scratch + (uint64_t)4 * Mp * KB * TK;
+    {
+        const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+        const int grid = (int)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
+        if (mode == 0) k_tile_rows<<<grid, 256, 0, s>>>(w0, w0, M, M, din, Mp, KB, At);
+        else k_tile_rows<<<grid, 256, 0, s>>>(w0, w1, dout, M, din, Mp, KB, At);
+        ++g_kernel_launches;
+        dim3 g2(KB, (Np + 31) / 32);
+        if (mode == 0) k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x1, batch, N, din, KB, Bt);
+        else k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x0, batch, N, din, KB, Bt);
+        ++g_kernel_launches;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_modgemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)(Np / BN), (unsigned)(Mp / TM));
-    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(Al, Bl, M, N, Mp, Np, Kp, out);
+    dim3 grid(Np / BN, Mp / TM);
+    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, out);
     ++g_kernel_launches;
     return cudaGetLastError();
 }
@@ -336,29 +356,12 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
                               const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
                               uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms) {
     if (dout == 0 || batch == 0) return cudaSuccess;
-    const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
-    const uint64_t Mp = (M + TM - 1) / TM * TM, Np = (N + 63) / 64 * 64;
-    const uint32_t Kp = (din + TK - 1) / TK * TK;
-    uint8_t* Al = scratch;
-    uint8_t* Bl = scratch + 4 * Mp * Kp;
-    // limb planes
-    {
-        const uint64_t work = Mp * Kp / 4;
-        const int grid = (int)std::min<uint64_t>((work + 255) / 256, (uint64_t)sms * 16);
-        if (mode == 0) k_split_rows<<<grid, 256, 0, s>>>(w0, w0, M, M, din, Mp, Kp, Al);
-        else k_split_rows<<<grid, 256, 0, s>>>(w0, w1, dout, M, din, Mp, Kp, Al);
-        ++g_kernel_launches;
-        dim3 g2(Kp / 32, (unsigned)((Np + 31) / 32)), b2(32, 8);
-        if (mode == 0) k_split_cols_t<<<g2, b2, 0, s>>>(x0, x1, batch, N, din, Np, Kp, Bl);
-        else k_split_cols_t<<<g2, b2, 0, s>>>(x0, x0, batch, N, din, Np, Kp, Bl);
-        ++g_kernel_launches;
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
+    const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
     TcOut out{mode, dout, batch, y0, y1};
     // narrow N tiles when the 64-wide grid would leave SMs idle
-    if ((Mp / TM) * (Np / 64) < (uint64_t)sms) return run_tc<32>(s, Al, Bl, M, N, Mp, Np, Kp, out);
-    return run_tc<64>(s, Al, Bl, M, N, Mp, Np, Kp, out);
+    if (((M + TM - 1) / TM) * ((N + 63) / 64) < (uint64_t)sms)
+        return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
+    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
 }
 
 }  // namespace spdzb200
