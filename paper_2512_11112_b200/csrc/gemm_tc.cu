@@ -3,9 +3,11 @@
 //
 // u32 operands are split into four u8 limbs, A = sum_i 2^(8i) A_i, B = sum_j 2^(8j) B_j,
 // so A*B = sum_s 2^(8s) P_s with P_s = sum_{i+j=s} A_i B_j (s = 0..6).  Each P_s is an
-// exact u8 x u8 -> s32 tensor-core GEMM accumulated in TMEM (tcgen05.mma kind::i8,
-// M = 128, N = BN, K = 32 per instruction); 16 MMAs per K step.  The epilogue reads
-// the seven s32 accumulators (tcgen05.ld) and recombines them mod p:
+// exact u8 x u8 -> s32 tensor-core product (tcgen05.mma kind::i8, K = 32 per
+// instruction).  The four B limb tiles are stacked as one N = 4*BN operand, so a K
+// step is 4 MMAs (one per A limb, M = 128, N = 128) into D_i = A_i [B_0|B_1|B_2|B_3]
+// in TMEM; the epilogue reads D_i (tcgen05.ld), forms P_s = sum_{i+j=s} D_i[:, j] and
+// recombines mod p:
 //   2^0, 2^8, 2^16, 2^24, 2^32 = 5, 2^40 = 1280, 2^48 = 327680 (mod p).
 // Exactness: P_3 sums 4 limb products over K, 4 * 255^2 * K < 2^31 for K <= 8192.
 //
@@ -105,7 +107,8 @@ struct TcSmem {
     static constexpr uint32_t B_STAGE = 4 * B_LIMB;
     static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
     static constexpr uint32_t BYTES = kStages * STAGE + 2048; // + barriers / tmem slot + alignment
-    static constexpr uint32_t TMEM_COLS = (7 * BN <= 256) ? 256 : 512;
+    static constexpr uint32_t TMEM_COLS = (16 * BN <= 256) ? 256 : 512;  // D_i: 4 x (4 BN) columns
+    static_assert(16 * BN <= 512, "4 A limbs x (4 B limbs x BN) s32 columns must fit TMEM");
 };
 
 __device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
@@ -177,8 +180,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
         }
     } else if (warp == 1 && lane == 0) {  // ---- MMA issuer ----
-        const uint32_t idesc = idesc_i8<BN>();
-        uint32_t inited = 0;
+        // The 4 B limb tiles are stacked rows of one (4 BN) x TK K-major operand, so
+        // one MMA per A limb i computes D_i[:, j BN + n] = (A_i B_j)(m, n) for all j.
+        const uint32_t idesc = idesc_i8<4 * BN>();
         for (uint32_t kb = 0; kb < KB; ++kb) {
             const uint32_t s = kb % kStages;
             mbar_wait(&full[s], (kb / kStages) & 1);
@@ -186,16 +190,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
 #pragma unroll
             for (int ks = 0; ks < TK / 32; ++ks) {
+                const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const uint64_t ad = smem_desc(sa + i * L::A_LIMB + ks * 2 * kLBO, kLBO, kSBO);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int t = i + j;
-                        const uint64_t bd = smem_desc(sb + j * L::B_LIMB + ks * 2 * kLBO, kLBO, kSBO);
-                        mma_i8(tmem + t * BN, ad, bd, idesc, (inited >> t) & 1u);
-                        inited |= 1u << t;
-                    }
+                    mma_i8(tmem + i * 4 * BN, ad, bd, idesc, (kb | ks) ? 1u : 0u);
                 }
             }
             mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
@@ -212,10 +211,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
 #pragma unroll 1
     for (int cc = 0; cc < BN / 16; ++cc) {
+        // P_s = sum_{i+j=s} D_i[:, j BN + col]; each D_ij < 255^2 K <= 2^29, so P_s < 2^31
         uint32_t v[7][16];
 #pragma unroll
-        for (int t = 0; t < 7; ++t) tmem_ld16(lane_base + t * BN + cc * 16, v[t]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int t = 0; t < 7; ++t)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[t][q] = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t d[4][16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tmem_ld16(lane_base + (i * 4 + j) * BN + cc * 16, d[j]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[i + j][q] += d[j][q];
+        }
         if (row < M) {
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
@@ -358,10 +370,9 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
     if (dout == 0 || batch == 0) return cudaSuccess;
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
     TcOut out{mode, dout, batch, y0, y1};
-    // narrow N tiles when the 64-wide grid would leave SMs idle
-    if (((M + TM - 1) / TM) * ((N + 63) / 64) < (uint64_t)sms)
-        return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
-    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
+    (void)M;
+    (void)N;
+    return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
 }
 
 }  // namespace spdzb200
