@@ -121,6 +121,12 @@ int spdz_capability(const spdz_ctx* ctx, spdz_capability_t* out);
 /* Measured CUDA-core integer pipe rate on ctx's device: IMAD.WIDE.U32 per second
  * (the roofline denominator of the CUDA-core modular GEMM) and all integer ops/s. */
 int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_int_per_s);
+/* Diagnostic switches of the tcgen05 GEMM (bit 0: skip TMA loads, bit 1: skip MMAs); results
+ * are invalid while non-zero.  Attribution experiments only. */
+int spdz_diag_gemm_tc_flags(uint32_t flags);
+/* Per-CTA %globaltimer stamps of the last tcgen05 GEMM run with flag bit 4 (start, TMEM
+ * allocated, MMAs done, end); returns the number of u64 words written. */
+uint32_t spdz_diag_gemm_tc_timestamps(unsigned long long* host, uint32_t cap);
 /* Number of kernels this library launched on any context since load (evidence counter). */
 uint64_t spdz_kernel_launches(void);
 

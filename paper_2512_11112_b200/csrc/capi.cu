@@ -73,29 +73,22 @@ void assign_ranks(spdz_mac_segment_t* segs, uint64_t n) {
 }
 
 void mac_sigma_launch(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n, uint64_t coin, int slot) {
-    constexpr uint64_t kChunk = 1u << 14;
-    std::vector<MacSegDev> ds(n);
-    std::vector<MacChunk> ch;
-    for (uint64_t i = 0; i < n; ++i) {
-        need(segs[i].len == 0 || (segs[i].value && segs[i].mac_a), SPDZ_ERR_INVALID_ARGUMENT, "null MAC segment");
-        ds[i] = MacSegDev{segs[i].value, segs[i].mac_a, segs[i].mac_b, segs[i].len, segs[i].j0};
-        for (uint64_t s = 0; s < segs[i].len; s += kChunk)
-            ch.push_back(MacChunk{(uint32_t)i, (uint32_t)std::min<uint64_t>(kChunk, segs[i].len - s), s});
-    }
-    const size_t seg_bytes = ds.size() * sizeof(MacSegDev);
-    const size_t seg_al = (seg_bytes + 255) / 256 * 256;
-    const size_t total = seg_al + ch.size() * sizeof(MacChunk);
-    // Tables go through pinned staging so the copy is stream-ordered and async.
-    char* host = (char*)ctx->pinned.ensure(std::max<size_t>(total, 256));
-    cuda_check(cudaStreamSynchronize(ctx->stream), "sync(pinned staging reuse)");
-    std::memcpy(host, ds.data(), seg_bytes);
-    std::memcpy(host + seg_al, ch.data(), ch.size() * sizeof(MacChunk));
-    char* dev = (char*)ctx->seg_buf.ensure(std::max<size_t>(total, 256));
-    cuda_check(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, ctx->stream), "H2D mac tables");
+    // segment tables go by value as kernel parameters: no staging copy, no host sync
     cuda_check(cudaMemsetAsync(ctx->d_acc + slot, 0, 8, ctx->stream), "memset acc");
-    launch_ok(launch_mac_sigma(ctx->stream, (const MacSegDev*)dev, (const MacChunk*)(dev + seg_al),
-                               (uint32_t)ch.size(), coin, ctx->alpha, ctx->d_acc + slot, ctx->sms),
-              "k_mac_sigma");
+    for (uint64_t base = 0; base < n; base += kMacTableSegs) {
+        MacTable tab{};
+        tab.n = (uint32_t)std::min<uint64_t>(kMacTableSegs, n - base);
+        uint64_t chunks = 0;
+        for (uint32_t i = 0; i < tab.n; ++i) {
+            const auto& sg = segs[base + i];
+            need(sg.len == 0 || (sg.value && sg.mac_a), SPDZ_ERR_INVALID_ARGUMENT, "null MAC segment");
+            tab.seg[i] = MacSegDev{sg.value, sg.mac_a, sg.mac_b, sg.len, sg.j0};
+            tab.first[i] = chunks;
+            chunks += (sg.len + kSigmaChunk - 1) / kSigmaChunk;
+        }
+        tab.first[tab.n] = chunks;
+        launch_ok(launch_mac_sigma(ctx->stream, tab, coin, ctx->alpha, ctx->d_acc + slot, ctx->sms), "k_mac_sigma");
+    }
 }
 
 uint32_t mac_sigma_collect(spdz_ctx* ctx, int slot) {

@@ -59,3 +59,21 @@ extern "C" int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, doubl
         if (total_int_per_s) *total_int_per_s = threads * iters * 16 / (ms / 1e3);  // + the IADD chain
     });
 }
+
+namespace spdzb200 {
+void modgemm_tc_debug(uint32_t flags);
+uint32_t modgemm_tc_timestamps(unsigned long long* host, uint32_t cap);
+}
+
+// Per-CTA %globaltimer stamps (start, TMEM allocated, MMAs done, end) of the last
+// tcgen05 GEMM launched with diagnostic bit 4 set.  Returns the number of words.
+extern "C" uint32_t spdz_diag_gemm_tc_timestamps(unsigned long long* host, uint32_t cap) {
+    return spdzb200::modgemm_tc_timestamps(host, cap);
+}
+
+// Diagnostic switches of the tcgen05 GEMM (bit 0: skip TMA loads, bit 1: skip MMAs) — results are
+// garbage while set; used only to attribute time between the load and MMA halves of the pipeline.
+extern "C" int spdz_diag_gemm_tc_flags(uint32_t flags) {
+    spdzb200::modgemm_tc_debug(flags);
+    return 0;
+}

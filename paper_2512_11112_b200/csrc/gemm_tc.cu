@@ -138,7 +138,10 @@ struct TcOut {
 // A tiles: [Mp/128][KB] blocks of A_STAGE bytes; B tiles: [Np/BN][KB] blocks of B_STAGE bytes.
 template <int BN>
 __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At, const uint8_t* __restrict__ Bt,
-                                                               uint32_t M, uint32_t N, uint32_t KB, TcOut out) {
+                                                               uint32_t M, uint32_t N, uint32_t KB, TcOut out,
+                                                               uint32_t dbg, unsigned long long* tstamp) {
+    unsigned long long t_start = 0;
+    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     using L = TcSmem<BN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
@@ -167,6 +170,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    unsigned long long t_alloc = 0;
+    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_alloc));
 
     if (warp == 0 && lane == 0) {  // ---- TMA producer ----
         const uint8_t* a_src = At + (uint64_t)blockIdx.y * KB * L::A_STAGE;
@@ -174,8 +179,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
         for (uint32_t kb = 0; kb < KB; ++kb) {
             const uint32_t s = kb % kStages;
             if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-            mbar_expect_tx(&full[s], L::STAGE);
             const uint32_t dst = sbase + s * L::STAGE;
+            if (dbg & 1) {  // diagnostic: no loads
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+                continue;
+            }
+            mbar_expect_tx(&full[s], L::STAGE);
             bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
             bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
         }
@@ -188,6 +197,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             mbar_wait(&full[s], (kb / kStages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
+            if (dbg & 2) {  // diagnostic: no MMAs
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+                continue;
+            }
 #pragma unroll
             for (int ks = 0; ks < TK / 32; ++ks) {
                 const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
@@ -199,11 +212,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             }
             mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        mma_commit(done);
+        if (dbg & 2) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(done)) : "memory");
+        else mma_commit(done);
     }
     __syncwarp();
     mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    unsigned long long t_done = 0;
+    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
 
     // epilogue: TMEM lane = row (warp w owns lanes 32w..32w+31), column = n
     const uint32_t row = m0 + warp * 32 + lane;
@@ -251,22 +267,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
+    if (tstamp && threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
+        tstamp[4 * cta + 0] = t_start;
+        tstamp[4 * cta + 1] = t_alloc;
+        tstamp[4 * cta + 2] = t_done;
+        tstamp[4 * cta + 3] = t_end;
+    }
 }
 
-// A (rows, stacked a0 over a1) -> pre-tiled limb image: one thread per (row, 16-k chunk).
+// A (rows, stacked a0 over a1) -> pre-tiled limb image: one thread per (row, 16-k chunk),
+// 128-bit loads when the rows are 16-byte aligned (K % 4 == 0).
 // A(m, k) = a0[m*K + k] for m < M0, a1[(m-M0)*K + k] for M0 <= m < M; zero padded.
-__global__ void k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1, uint32_t M0, uint32_t M,
-                            uint32_t K, uint32_t Mp, uint32_t KB, uint8_t* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1,
+                                                   uint32_t M0, uint32_t M, uint32_t K, uint32_t Mp, uint32_t KB,
+                                                   uint8_t* __restrict__ out) {
     const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+    const bool v4 = (K % 4) == 0 && ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 15u) == 0;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < chunks; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t kc_all = (uint32_t)(t % ((uint64_t)KB * (TK / 16)));
         const uint32_t m = (uint32_t)(t / ((uint64_t)KB * (TK / 16)));
         const uint32_t k0 = kc_all * 16;
         uint32_t w[16];
+        const uint32_t* row = m < M0 ? a0 + (uint64_t)m * K : a1 + (uint64_t)(m - M0) * K;
+        if (v4 && m < M && k0 + 16 <= K) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const uint32_t k = k0 + q;
-            w[q] = (m < M && k < K) ? (m < M0 ? a0[(uint64_t)m * K + k] : a1[(uint64_t)(m - M0) * K + k]) : 0u;
+            for (int q = 0; q < 4; ++q) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + k0) + q);
+                w[4 * q] = u.x;
+                w[4 * q + 1] = u.y;
+                w[4 * q + 2] = u.z;
+                w[4 * q + 3] = u.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) w[q] = (m < M && k0 + q < K) ? row[k0 + q] : 0u;
         }
         const uint32_t mt = m / TM, r = m % TM, kb = k0 / TK, kk = k0 % TK;
         uint8_t* blk = out + ((uint64_t)mt * KB + kb) * (4u * TM * TK);
@@ -275,8 +312,8 @@ __global__ void k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __r
             uint32_t p[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                p[q] = ((w[4 * q] >> (8 * i)) & 0xFF) | (((w[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
-                       (((w[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((w[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
+                p[q] = __byte_perm(__byte_perm(w[4 * q] >> (8 * i), w[4 * q + 1] >> (8 * i), 0x0040),
+                                   __byte_perm(w[4 * q + 2] >> (8 * i), w[4 * q + 3] >> (8 * i), 0x0040), 0x5410);
             *reinterpret_cast<uint4*>(blk + i * (TM * TK) + core_off(r, kk)) = make_uint4(p[0], p[1], p[2], p[3]);
         }
     }
@@ -316,6 +353,10 @@ __global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __r
     }
 }
 
+uint32_t g_tc_dbg = 0;
+unsigned long long* g_tc_tstamp = nullptr;  // diagnostic per-CTA timestamps (bit 4)
+uint32_t g_tc_ctas = 0;
+
 template <int BN>
 cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
                    const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint8_t* scratch, const TcOut& out,
@@ -326,7 +367,7 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
     const uint32_t KB = (din + TK - 1) / TK;
     uint8_t* At = scratch;
     uint8_t* Bt = scratch + (uint64_t)4 * Mp * KB * TK;
-    {
+    if (!(g_tc_dbg & 8)) {  // (diagnostic bit 3 skips the re-layout kernels)
         const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
         const int grid = (int)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
         if (mode == 0) k_tile_rows<<<grid, 256, 0, s>>>(w0, w0, M, M, din, Mp, KB, At);
@@ -345,13 +386,29 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    if (g_tc_dbg & 4) return cudaSuccess;  // (diagnostic bit 2 skips the GEMM kernel)
     dim3 grid(Np / BN, Mp / TM);
-    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, out);
+    unsigned long long* ts = nullptr;
+    if (g_tc_dbg & 16) {
+        g_tc_ctas = grid.x * grid.y;
+        if (!g_tc_tstamp) cudaMalloc(&g_tc_tstamp, 4 * 8 * 65536);
+        if (g_tc_ctas <= 65536) ts = g_tc_tstamp;
+    }
+    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, out, g_tc_dbg, ts);
     ++g_kernel_launches;
     return cudaGetLastError();
 }
 
 }  // namespace
+
+void modgemm_tc_debug(uint32_t flags) { g_tc_dbg = flags; }
+uint32_t modgemm_tc_timestamps(unsigned long long* host, uint32_t cap) {
+    if (!g_tc_tstamp) return 0;
+    const uint32_t n = std::min(cap, 4 * g_tc_ctas);
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, g_tc_tstamp, n * 8ull, cudaMemcpyDeviceToHost);
+    return n;
+}
 
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch) {
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;

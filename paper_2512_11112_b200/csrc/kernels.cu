@@ -58,31 +58,57 @@ struct IO {
 };
 
 template <int NI, int NO, class Op>
+__device__ __forceinline__ void map_group(const IO<NI, NO>& io, uint64_t g, const Op& op, uint32_t (&a)[NI > 0 ? NI : 1][4]) {
+    uint32_t o[NO][4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        uint32_t ai[NI > 0 ? NI : 1], oi[NO];
+#pragma unroll
+        for (int k = 0; k < NI; ++k) ai[k] = a[k][l];
+        op(ai, oi);
+#pragma unroll
+        for (int k = 0; k < NO; ++k) o[k][l] = oi[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NO; ++k) st4(io.out[k], g, o[k]);
+}
+
+template <int NI, int NO, class Op>
+__device__ __forceinline__ void map_load(const IO<NI, NO>& io, uint64_t g, uint32_t (&a)[NI > 0 ? NI : 1][4]) {
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        uint4 v = Op::is_peer(k) ? ld4_peer(io.in[k], g) : ld4(io.in[k], g);
+        a[k][0] = v.x;
+        a[k][1] = v.y;
+        a[k][2] = v.z;
+        a[k][3] = v.w;
+    }
+}
+
+// Ops with few planes (mask, add) keep two 4-lane groups in flight per thread.
+template <class Op>
+struct MapUnroll {
+    static constexpr int value = 1;
+};
+
+template <int NI, int NO, class Op>
 __global__ void __launch_bounds__(kThreads) k_map(IO<NI, NO> io, uint64_t n, uint64_t n4, Op op) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint64_t g = t; g < n4; g += stride) {
+    uint64_t g = t;
+    if (MapUnroll<Op>::value == 2) {
+        for (; g + stride < n4; g += 2 * stride) {
+            uint32_t a[NI > 0 ? NI : 1][4], b[NI > 0 ? NI : 1][4];
+            map_load<NI, NO, Op>(io, g, a);
+            map_load<NI, NO, Op>(io, g + stride, b);
+            map_group<NI, NO, Op>(io, g, op, a);
+            map_group<NI, NO, Op>(io, g + stride, op, b);
+        }
+    }
+    for (; g < n4; g += stride) {
         uint32_t a[NI > 0 ? NI : 1][4];
-#pragma unroll
-        for (int k = 0; k < NI; ++k) {
-            uint4 v = Op::is_peer(k) ? ld4_peer(io.in[k], g) : ld4(io.in[k], g);
-            a[k][0] = v.x;
-            a[k][1] = v.y;
-            a[k][2] = v.z;
-            a[k][3] = v.w;
-        }
-        uint32_t o[NO][4];
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            uint32_t ai[NI > 0 ? NI : 1], oi[NO];
-#pragma unroll
-            for (int k = 0; k < NI; ++k) ai[k] = a[k][l];
-            op(ai, oi);
-#pragma unroll
-            for (int k = 0; k < NO; ++k) o[k][l] = oi[k];
-        }
-#pragma unroll
-        for (int k = 0; k < NO; ++k) st4(io.out[k], g, o[k]);
+        map_load<NI, NO, Op>(io, g, a);
+        map_group<NI, NO, Op>(io, g, op, a);
     }
     for (uint64_t i = n4 * 4 + t; i < n; i += stride) {
         uint32_t ai[NI > 0 ? NI : 1], oi[NO];
@@ -199,6 +225,19 @@ struct OpCombine {
             o[3] = e;
         }
     }
+};
+
+template <>
+struct MapUnroll<OpMask> {
+    static constexpr int value = 2;
+};
+template <>
+struct MapUnroll<OpAdd> {
+    static constexpr int value = 2;
+};
+template <>
+struct MapUnroll<OpSub> {
+    static constexpr int value = 2;
 };
 
 struct OpDiff : NoPeer {
@@ -357,31 +396,58 @@ __device__ __forceinline__ void sigma_rec(uint64_t z, uint32_t x, uint32_t m, Ac
     sx.add(mul_wide(r, x));
 }
 
-__global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restrict__ segs,
-                                                        const MacChunk* __restrict__ chunks, uint32_t n_chunks,
-                                                        uint64_t coin, uint32_t alpha, unsigned long long* acc) {
+// Segment table passed by value (no host->device copy, no host sync before the
+// launch): chunk c of the flattened record space belongs to segment i with
+// first[i] <= c < first[i+1]; chunks are kSigmaChunk records.
+__global__ void __launch_bounds__(kThreads) k_mac_sigma(MacTable tab, uint64_t coin, uint32_t alpha,
+                                                        unsigned long long* acc) {
     Acc96 sm, sx;
-    for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        const MacChunk ch = chunks[c];
-        const MacSegDev sg = segs[ch.seg];
-        const uint32_t* xv = sg.value + ch.start;
-        const uint32_t* ma = sg.mac_a + ch.start;
-        const uint32_t* mb = sg.mac_b ? sg.mac_b + ch.start : nullptr;
-        const uint64_t z0 = coin + (sg.j0 + ch.start + 1) * kGamma;  // z of record 0 of the chunk
+    const uint64_t n_chunks = tab.first[tab.n];
+    uint32_t seg = 0;
+    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        while (c >= tab.first[seg + 1]) ++seg;  // chunks visited in increasing order
+        const MacSegDev sg = tab.seg[seg];
+        const uint64_t start = (c - tab.first[seg]) * kSigmaChunk;
+        const uint32_t count = (uint32_t)((sg.len - start) < kSigmaChunk ? (sg.len - start) : kSigmaChunk);
+        const uint32_t* xv = sg.value + start;
+        const uint32_t* ma = sg.mac_a + start;
+        const uint32_t* mb = sg.mac_b ? sg.mac_b + start : nullptr;
+        const uint64_t z0 = coin + (sg.j0 + start + 1) * kGamma;  // z of record 0 of the chunk
         const bool v4 = ((reinterpret_cast<uintptr_t>(xv) | reinterpret_cast<uintptr_t>(ma) |
                           reinterpret_cast<uintptr_t>(mb)) & 15u) == 0;
         uint32_t done = 0;
         if (v4) {
-            const uint32_t n4 = ch.count / 4;
-            for (uint32_t g = threadIdx.x; g < n4; g += blockDim.x) {
+            const uint32_t n4 = count / 4;
+            uint32_t g = threadIdx.x;
+            for (; g + blockDim.x < n4; g += 2 * blockDim.x) {  // 8 records in flight per thread
+                const uint32_t g2 = g + blockDim.x;
+                const uint4 x1 = __ldcs(reinterpret_cast<const uint4*>(xv) + g);
+                const uint4 x2 = __ldcs(reinterpret_cast<const uint4*>(xv) + g2);
+                uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ma) + g);
+                uint4 m2 = __ldcs(reinterpret_cast<const uint4*>(ma) + g2);
+                if (mb) {
+                    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(mb) + g);
+                    const uint4 b2 = __ldcs(reinterpret_cast<const uint4*>(mb) + g2);
+                    m1 = make_uint4(fp_sub(m1.x, b1.x), fp_sub(m1.y, b1.y), fp_sub(m1.z, b1.z), fp_sub(m1.w, b1.w));
+                    m2 = make_uint4(fp_sub(m2.x, b2.x), fp_sub(m2.y, b2.y), fp_sub(m2.z, b2.z), fp_sub(m2.w, b2.w));
+                }
+                uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
+                sigma_rec(z, x1.x, m1.x, sm, sx);
+                sigma_rec(z + kGamma, x1.y, m1.y, sm, sx);
+                sigma_rec(z + 2 * kGamma, x1.z, m1.z, sm, sx);
+                sigma_rec(z + 3 * kGamma, x1.w, m1.w, sm, sx);
+                z = z0 + (uint64_t)(4 * g2) * kGamma;
+                sigma_rec(z, x2.x, m2.x, sm, sx);
+                sigma_rec(z + kGamma, x2.y, m2.y, sm, sx);
+                sigma_rec(z + 2 * kGamma, x2.z, m2.z, sm, sx);
+                sigma_rec(z + 3 * kGamma, x2.w, m2.w, sm, sx);
+            }
+            for (; g < n4; g += blockDim.x) {
                 const uint4 x = __ldcs(reinterpret_cast<const uint4*>(xv) + g);
                 uint4 m = __ldcs(reinterpret_cast<const uint4*>(ma) + g);
                 if (mb) {
                     const uint4 b = __ldcs(reinterpret_cast<const uint4*>(mb) + g);
-                    m.x = fp_sub(m.x, b.x);
-                    m.y = fp_sub(m.y, b.y);
-                    m.z = fp_sub(m.z, b.z);
-                    m.w = fp_sub(m.w, b.w);
+                    m = make_uint4(fp_sub(m.x, b.x), fp_sub(m.y, b.y), fp_sub(m.z, b.z), fp_sub(m.w, b.w));
                 }
                 const uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
                 sigma_rec(z, x.x, m.x, sm, sx);
@@ -391,7 +457,7 @@ __global__ void __launch_bounds__(kThreads) k_mac_sigma(const MacSegDev* __restr
             }
             done = n4 * 4;
         }
-        for (uint32_t i = done + threadIdx.x; i < ch.count; i += blockDim.x) {
+        for (uint32_t i = done + threadIdx.x; i < count; i += blockDim.x) {
             uint32_t m = __ldcs(ma + i);
             if (mb) m = fp_sub(m, __ldcs(mb + i));
             sigma_rec(z0 + (uint64_t)i * kGamma, __ldcs(xv + i), m, sm, sx);
@@ -816,11 +882,12 @@ cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t
     return launched();
 }
 
-cudaError_t launch_mac_sigma(cudaStream_t s, const MacSegDev* segs, const MacChunk* chunks, uint32_t n_chunks,
-                             uint64_t coin, uint32_t alpha, unsigned long long* acc, int sms) {
+cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
+                             unsigned long long* acc, int sms) {
+    const uint64_t n_chunks = tab.first[tab.n];
     if (n_chunks == 0) return cudaSuccess;
-    int grid = (int)(n_chunks < (uint32_t)(sms * 8) ? n_chunks : (uint32_t)(sms * 8));
-    k_mac_sigma<<<grid, kThreads, 0, s>>>(segs, chunks, n_chunks, coin, alpha, acc);
+    const int grid = (int)(n_chunks < (uint64_t)(sms * 8) ? n_chunks : (uint64_t)(sms * 8));
+    k_mac_sigma<<<grid, kThreads, 0, s>>>(tab, coin, alpha, acc);
     return launched();
 }
 

@@ -15,10 +15,12 @@ struct MacSegDev {            // device-side MAC segment descriptor
     uint64_t len;
     uint64_t j0;
 };
-struct MacChunk {             // work item: [start, start+count) of segment `seg`
-    uint32_t seg;
-    uint32_t count;
-    uint64_t start;
+constexpr uint32_t kSigmaChunk = 1u << 14;  // records per work item of the sigma kernel
+constexpr int kMacTableSegs = 48;          // segments per launch (kernel parameter table)
+struct MacTable {
+    uint32_t n;                            // segments in this table
+    MacSegDev seg[kMacTableSegs];
+    uint64_t first[kMacTableSegs + 1];     // first chunk of each segment (prefix sums), first[n] = total
 };
 
 struct LaunchInfo {
@@ -54,8 +56,8 @@ cudaError_t launch_finish_reduce(cudaStream_t s, const unsigned long long* acc, 
 cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t* cm, uint64_t pairs, uint32_t* xv,
                               uint32_t* xm, uint32_t* yv, uint32_t* ym, int sms);
 // MAC sigma partial over chunks; acc (u64) accumulates values < p per block.
-cudaError_t launch_mac_sigma(cudaStream_t s, const MacSegDev* segs, const MacChunk* chunks, uint32_t n_chunks,
-                             uint64_t coin, uint32_t alpha, unsigned long long* acc, int sms);
+cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
+                             unsigned long long* acc, int sms);
 // MAC sigma over explicit ranks (record form)
 cudaError_t launch_mac_sigma_ranked(cudaStream_t s, const uint32_t* value, const uint32_t* mac,
                                     const uint64_t* rank, uint64_t n, uint64_t coin, uint32_t alpha,

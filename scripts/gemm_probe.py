@@ -13,15 +13,71 @@ from paper_2512_11112_b200._lib import check, lib  # noqa: E402
 from paper_2512_11112_b200.backend import dshare  # noqa: E402
 
 P = 4294967291
-din = dout = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+pos = [a for a in sys.argv[1:] if not a.startswith("--")]
+din = dout = int(pos[0]) if pos else 1024
+batch = int(pos[1]) if len(pos) > 1 else 256
 rng = np.random.default_rng(0)
 rnd = lambda n: torch.from_numpy(rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)).cuda()
 ctx = Context(0, 0, 2, 1)
 W, xs = rnd(din * dout), DeviceShare(rnd(din * batch), rnd(din * batch))
 ys = DeviceShare.empty(dout * batch)
 args = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
+def graphed(reps=10):
+    """Device time per call from a CUDA graph of `reps` calls (host launch cost excluded)."""
+    for _ in range(3):
+        check(lib().spdz_linear_secret_public(*args))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.use_torch_stream()
+        for _ in range(reps):
+            check(lib().spdz_linear_secret_public(*args))
+    ctx.use_torch_stream()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1000
+
+
+def timed(reps=10):
+    for _ in range(3):
+        check(lib().spdz_linear_secret_public(*args))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        check(lib().spdz_linear_secret_public(*args))
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1000
+
+
+if "--diag" in sys.argv:
+    check(lib().spdz_set_gemm_path(2))
+    for flags, name in ((0, "full"), (1, "no loads"), (2, "no MMAs"), (3, "neither"), (4, "tiling only"),
+                        (8, "gemm only"), (11, "gemm only, no loads, no MMAs")):
+        lib().spdz_diag_gemm_tc_flags(flags)
+        print(f"tcgen05 {name}: {timed():.1f} us per call", flush=True)
+    lib().spdz_diag_gemm_tc_flags(16)
+    timed(1)
+    buf = (C.c_uint64 * 262144)()
+    n = lib().spdz_diag_gemm_tc_timestamps(buf, 262144)
+    ts = np.array(buf[:n], dtype=np.float64).reshape(-1, 4)
+    t0 = ts[:, 0].min()
+    print("per-CTA us: alloc %.2f  mainloop %.2f  epilogue %.2f | first start %.2f last start %.2f last end %.2f" % (
+        np.mean(ts[:, 1] - ts[:, 0]) / 1e3, np.mean(ts[:, 2] - ts[:, 1]) / 1e3, np.mean(ts[:, 3] - ts[:, 2]) / 1e3,
+        0.0, (ts[:, 0].max() - t0) / 1e3, (ts[:, 3].max() - t0) / 1e3), flush=True)
+    lib().spdz_diag_gemm_tc_flags(0)
 for path in (2, 1):
+    check(lib().spdz_set_gemm_path(path))
+    try:
+        print(f"path {path}: graphed {graphed():.1f} us per call (device)", flush=True)
+    except Exception as e:
+        print(f"path {path}: graph capture failed: {e}", flush=True)
     check(lib().spdz_set_gemm_path(path))
     for _ in range(3):
         check(lib().spdz_linear_secret_public(*args))
