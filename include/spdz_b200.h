@@ -300,6 +300,12 @@ typedef struct spdz_run_options {
     uint64_t shard_offset;
     uint64_t shard_total;
     int32_t external_mac_verify; /* 1: report per-party (partial) sigmas, caller verifies */
+    /* One party per process (multi-GPU / multi-process): 0 (default) = every party lives
+     * in this run; p + 1 = only party p is materialised here, the peers' opening payloads
+     * and completion flags are mapped with spdz_run_export / spdz_run_import (CUDA IPC,
+     * NVLink P2P loads) and ordered by stream memory operations.  Requires
+     * external_mac_verify = 1. */
+    int32_t single_party;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
@@ -332,6 +338,12 @@ typedef struct spdz_run spdz_run;
 int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
                     const spdz_run_options_t* opts, spdz_run** out);
 int spdz_run_destroy(spdz_run* run);
+/* IPC export of this process's party: opening payloads, input differences, root
+ * values and the opening-flag words.  *len receives the blob size (call with
+ * buf = NULL to query). */
+int spdz_run_export(spdz_run* run, void* buf, uint64_t cap, uint64_t* len);
+/* Maps other processes' export blobs (concatenated; own entries are skipped). */
+int spdz_run_import(spdz_run* run, const void* blob, uint64_t len);
 /* Re-runs the GPU dealer with `seed` (fresh preprocessing; inputs must be shared again). */
 int spdz_run_deal(spdz_run* run, uint64_t seed);
 /* Cleartext input for an INPUT node (host pointer).  Private inputs are shared

@@ -50,7 +50,7 @@ class RunOptions(C.Structure):  # spdz_run_options_t
     _fields_ = [("slice", C.c_uint64), ("dealer_seed", C.c_uint64), ("fixed_coin", C.c_int32), ("coin", C.c_uint64),
                 ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32),
                 ("stream_per_party", C.c_int32), ("shard_offset", C.c_uint64), ("shard_total", C.c_uint64),
-                ("external_mac_verify", C.c_int32)]
+                ("external_mac_verify", C.c_int32), ("single_party", C.c_int32)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t
@@ -138,6 +138,8 @@ _SIGS = {
     "spdz_run_mac_check": (C.c_int, [vp, C.c_int, C.c_uint64, C.POINTER(RunReport)]),
     "spdz_run_bind_output": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_node_share": (C.c_int, [vp, C.c_int, C.c_uint32, C.POINTER(Share)]),
+    "spdz_run_export": (C.c_int, [vp, vp, C.c_uint64, u64p]),
+    "spdz_run_import": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_inject_bitflip": (C.c_int, [vp, C.c_uint32, C.c_int, C.c_int, C.c_uint64, C.c_uint32]),
 }
 

@@ -5,6 +5,7 @@
 // kernels, ordered by per-party events (the batch-id matching of
 // net.cpp:61-95 becomes stream/event ordering).  Every share, triple pool,
 // opened-value log and MAC record lives in HBM as structure-of-arrays.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -80,6 +81,9 @@ struct LinTiles {
 };
 
 struct Party {
+    bool local = true;              // false: another process owns it (IPC-mapped peer)
+    uint32_t* flags = nullptr;      // opening-slot sequence words (local: allocated, remote: mapped)
+    std::vector<void*> mapped;      // IPC mappings to close
     spdz_ctx* ctx = nullptr;
     std::vector<NodeState> ns;
     uint32_t* pool[6] = {};         // scalar triples (views)
@@ -153,10 +157,14 @@ struct spdz_run {
     cudaEvent_t ev_opened = nullptr;
     cudaStream_t copy_stream = nullptr;
     bool in_flight = false;
+    bool any_remote = false;
+    uint32_t seq = 0;               // phase sequence number written to / awaited on opening flags
+    uint64_t n_slots = 0;
     uint64_t launches0 = 0;
     std::chrono::steady_clock::time_point wall0;
 
     uint32_t* alloc(int party, uint64_t words) {
+        if (!parties[party].local) return nullptr;  // remote party: pointers come from spdz_run_import
         const int dev = devices[party];
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         void* p = nullptr;
@@ -174,14 +182,62 @@ struct spdz_run {
         return (uint32_t*)p;
     }
     const spdz_node_t& node(uint32_t id) const { return nodes.at(id); }
+    int ref_party() const {  // a party whose state is materialised here
+        for (int p = 0; p < n; ++p)
+            if (parties[p].local) return p;
+        return 0;
+    }
     bool priv(uint32_t id) const { return nodes.at(id).is_private != 0; }
 };
 
 namespace {
 
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver entry points
+typedef CUresult (*PFN_waitv32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writev32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_addrrange)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_waitv32 g_waitv32 = nullptr;
+PFN_writev32 g_writev32 = nullptr;
+PFN_addrrange g_addrrange = nullptr;
+
+void load_stream_memops() {
+    if (g_waitv32 && g_writev32) return;
+    cudaDriverEntryPointQueryResult q;
+    cuda_check(cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&g_waitv32, cudaEnableDefault, &q),
+               "entry point cuStreamWaitValue32");
+    need(q == cudaDriverEntryPointSuccess && g_waitv32, SPDZ_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    cuda_check(cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&g_writev32, cudaEnableDefault, &q),
+               "entry point cuStreamWriteValue32");
+    need(q == cudaDriverEntryPointSuccess && g_writev32, SPDZ_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    cuda_check(cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&g_addrrange, cudaEnableDefault, &q),
+               "entry point cuMemGetAddressRange");
+    need(q == cudaDriverEntryPointSuccess && g_addrrange, SPDZ_ERR_CUDA, "cuMemGetAddressRange unavailable");
+}
+
 cudaStream_t S(spdz_run* r, int p) { return r->parties[p].ctx->stream; }
 int SMS(spdz_run* r, int p) { return r->parties[p].ctx->sms; }
 void dev(spdz_run* r, int p) { device_guard(r->parties[p].ctx); }
+
+// opening slot of (node, sub): sub 0 = the node's opening (Beaver / linear / root),
+// 1..62 = reduce_mul level sub-1, 63 = input-sharing difference of an input node
+uint64_t slot_of(uint32_t node, uint32_t sub) { return (uint64_t)node * 64 + sub; }
+
+// After party p's payload for `slot` is complete on its stream, publish it to
+// remote peers (stream-ordered write, with the default system-wide fence).
+void signal_remote(spdz_run* r, int p, uint64_t slot) {
+    if (!r->any_remote) return;
+    dev(r, p);
+    need(g_writev32(S(r, p), (CUdeviceptr)(r->parties[p].flags + slot), r->seq, 0) == CUDA_SUCCESS, SPDZ_ERR_CUDA,
+         "cuStreamWriteValue32");
+}
+
+// Party p's stream waits until remote party q has published `slot` for this phase.
+void wait_remote(spdz_run* r, int p, int q, uint64_t slot) {
+    dev(r, p);
+    need(g_waitv32(S(r, p), (CUdeviceptr)(r->parties[q].flags + slot), r->seq, CU_STREAM_WAIT_VALUE_GEQ) ==
+             CUDA_SUCCESS,
+         SPDZ_ERR_CUDA, "cuStreamWaitValue32");
+}
 
 cudaEvent_t new_event(spdz_run* r, int p) {
     dev(r, p);
@@ -397,17 +453,26 @@ void plan_buffers(spdz_run* r) {
         }
         const Val& rv = P.ns[r->root].out;
         P.outputs = r->alloc(p, std::max<uint64_t>(rv.lanes, 1));
+        if (!P.local) continue;
         cuda_check(cudaSetDevice(P.ctx->device), "dev");
         cuda_check(cudaEventCreate(&P.t0), "ev");
         cuda_check(cudaEventCreate(&P.t1), "ev");
+        // private input differences: party 0 publishes x - mask (preproc.cpp:146-151)
+        if (p == 0)
+            for (auto& [id, off] : r->input_mask_off) r->input_diff[id] = r->alloc(0, r->node(id).lanes);
+        // opening-slot flags (only read by remote peers)
+        r->n_slots = (uint64_t)r->nodes.size() * 64;
+        P.flags = r->alloc(p, r->n_slots);
+        cuda_check(cudaMemset(P.flags, 0, r->n_slots * 4), "memset flags");
     }
     // one open event per (party, node) plus reduce levels
     for (int p = 0; p < r->n; ++p) {
+        if (!r->parties[p].local) continue;
         size_t need_ev = r->nodes.size() + 1;
         for (auto& st : r->parties[p].ns) need_ev += st.levels.size();
         for (size_t k = 0; k < need_ev; ++k) new_event(r, p);
     }
-    dev(r, 0);
+    dev(r, r->ref_party());
     cuda_check(cudaEventCreateWithFlags(&r->ev_input, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&r->ev_opened, cudaEventDisableTiming), "event");
     cuda_check(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking), "copy stream");
@@ -418,12 +483,13 @@ void deal(spdz_run* r, uint64_t seed) {
     const int n = r->n;
     uint32_t alpha_sh[SPDZ_MAX_PARTIES], alpha;
     dealer_alpha(n, seed, alpha_sh, &alpha);
-    for (int p = 0; p < n; ++p) r->parties[p].ctx->alpha = alpha_sh[p];
+    for (int p = 0; p < n; ++p)
+        if (r->parties[p].local) r->parties[p].ctx->alpha = alpha_sh[p];
     const uint64_t S = r->scalar_total, M = r->mask_total;
     for (auto& [device, dd] : r->deals) {
         int p0 = -1;
         for (int p = 0; p < n; ++p)
-            if (r->devices[p] == device) { p0 = p; break; }
+            if (r->parties[p].local && r->devices[p] == device) { p0 = p; break; }
         spdz_ctx* ctx = r->parties[p0].ctx;
         device_guard(ctx);
         cuda_check(cudaMemsetAsync(ctx->d_flag, 0, 4, ctx->stream), "memset flag");
@@ -493,6 +559,7 @@ void alloc_deals(spdz_run* r) {
         for (auto c : r->tiles[id].counts) scratch = std::max<uint64_t>(scratch, (uint64_t)nd.din * c + nd.din + c);
     }
     for (int p = 0; p < n; ++p) {
+        if (!r->parties[p].local) continue;
         const int d = r->devices[p];
         if (r->deals.count(d)) continue;
         DeviceDeal dd;
@@ -517,6 +584,7 @@ void alloc_deals(spdz_run* r) {
     }
     for (int p = 0; p < n; ++p) {  // per-party views (party-major planes)
         auto& P = r->parties[p];
+        if (!P.local) continue;
         auto& dd = r->deals[r->devices[p]];
         for (int k = 0; k < 6; ++k) P.pool[k] = dd.pool[k] + p * S;
         P.mask_v = dd.mask_v + p * M;
@@ -565,6 +633,20 @@ struct Exec {
     void tend(int p, int idx, int cls, uint64_t bytes) { ktimer_end(r, p, idx, cls, bytes); }
 
     cudaEvent_t next_event(int p) { return r->parties[p].evs.at(ev_cursor[p]++); }
+
+    // party p's payload for `slot` is complete on its stream: tell local peers
+    // (event) and remote peers (flag word, spdz_run_import)
+    cudaEvent_t publish(int p, uint64_t slot) {
+        cudaEvent_t e = next_event(p);
+        lk(cudaEventRecord(e, S(r, p)), "record");
+        signal_remote(r, p, slot);
+        return e;
+    }
+    // party p's stream waits for party q's payload of `slot`
+    void await(int p, int q, cudaEvent_t ev, uint64_t slot) {
+        if (r->parties[q].local) lk(cudaStreamWaitEvent(S(r, p), ev, 0), "wait peer");
+        else wait_remote(r, p, q, slot);
+    }
 
     // bcast_share(s, lanes) into dst (runtime.cpp:41-47) when lanes differ
     void bcast_into(int p, const Val& s, const Val& dst) {
@@ -668,6 +750,7 @@ struct Exec {
         const uint64_t off = reg.base + exec * reg.stride;  // runtime.cpp:197
         std::vector<cudaEvent_t> sent(r->n);
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& st = P.ns[id];
             const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
@@ -679,11 +762,11 @@ struct Exec {
                                st.payload + L, L, SMS(r, p)),
                "k_mul_mask");
             tend(p, tk, SPDZ_KSTAT_MASK, 24 * L);
-            sent[p] = next_event(p);
-            lk(cudaEventRecord(sent[p], S(r, p)), "record");
+            sent[p] = publish(p, slot_of(id, 0));
         }
         const uint64_t batch = make_batch(id, exec, 0);
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& st = P.ns[id];
             dev(r, p);
@@ -692,7 +775,7 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                lk(cudaStreamWaitEvent(S(r, p), sent[q], 0), "wait peer");
+                await(p, q, sent[q], slot_of(id, 0));
                 const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, 2 * L, st.shadow);
                 pd[k] = src;
                 pe[k] = src + L;
@@ -717,9 +800,10 @@ struct Exec {
     // runtime.cpp:242-281
     void reduce_mul(uint32_t id, const Region& reg, uint64_t exec) {
         const auto& n = r->node(id);
-        const size_t nlev = r->parties[0].ns[id].levels.size();
+        const size_t nlev = r->parties[r->ref_party()].ns[id].levels.size();
         if (nlev == 0) {  // single lane: value passes through
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 auto& P = r->parties[p];
                 const Val& a = P.ns[n.operands[0]].out;
                 auto& o = P.ns[id].out;
@@ -733,8 +817,9 @@ struct Exec {
         for (size_t li = 0; li < nlev; ++li) {
             std::vector<cudaEvent_t> sent(r->n);
             const uint64_t off = reg.base + exec * reg.stride + used;
-            const uint64_t pairs = r->parties[0].ns[id].levels[li].pairs;
+            const uint64_t pairs = r->parties[r->ref_party()].ns[id].levels[li].pairs;
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 auto& P = r->parties[p];
                 auto& lv = P.ns[id].levels[li];
                 const uint32_t* cv = li == 0 ? P.ns[n.operands[0]].out.v : P.ns[id].levels[li - 1].zv;
@@ -748,11 +833,11 @@ struct Exec {
                 lk(launch_mul_mask(S(r, p), lv.xv, lv.yv, P.pool[0] + off, P.pool[2] + off, lv.payload,
                                    lv.payload + pairs, pairs, SMS(r, p)),
                    "mask");
-                sent[p] = next_event(p);
-                lk(cudaEventRecord(sent[p], S(r, p)), "record");
+                sent[p] = publish(p, slot_of(id, 1 + (uint32_t)li));
             }
             const uint64_t batch = make_batch(id, exec, sub++);
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 auto& P = r->parties[p];
                 auto& lv = P.ns[id].levels[li];
                 dev(r, p);
@@ -761,7 +846,7 @@ struct Exec {
                 int k = 0;
                 for (int q = 0; q < r->n; ++q) {
                     if (q == p) continue;
-                    lk(cudaStreamWaitEvent(S(r, p), sent[q], 0), "wait");
+                    await(p, q, sent[q], slot_of(id, 1 + (uint32_t)li));
                     pd[k] = r->parties[q].ns[id].levels[li].payload;
                     pe[k] = pd[k] + pairs;
                     ++k;
@@ -783,10 +868,11 @@ struct Exec {
     void linear(uint32_t id, uint64_t exec) {
         const auto& n = r->node(id);
         const uint32_t din = n.din, dout = n.dout;
-        const bool xp = !r->parties[0].ns[n.operands[0]].out.is_public;
-        const bool wp = !r->parties[0].ns[n.operands[1]].out.is_public;
+        const bool xp = !r->parties[r->ref_party()].ns[n.operands[0]].out.is_public;
+        const bool wp = !r->parties[r->ref_party()].ns[n.operands[1]].out.is_public;
         if (!xp || !wp) {
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 auto& P = r->parties[p];
                 auto& st = P.ns[id];
                 const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out, &b = P.ns[n.operands[2]].out;
@@ -831,6 +917,7 @@ struct Exec {
         const uint64_t batch0 = make_batch(id, exec, 0);
         std::vector<cudaEvent_t> sent(r->n);
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& st = P.ns[id];
             const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out, &b = P.ns[n.operands[2]].out;
@@ -851,10 +938,10 @@ struct Exec {
             lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
             lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
             tend(p, tk, SPDZ_KSTAT_MASK, 12 * cells + 12 * etot);
-            sent[p] = next_event(p);
-            lk(cudaEventRecord(sent[p], c->stream), "record");
+            sent[p] = publish(p, slot_of(id, 0));
         }
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& st = P.ns[id];
             const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out;
@@ -865,7 +952,7 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                lk(cudaStreamWaitEvent(c->stream, sent[q], 0), "wait");
+                await(p, q, sent[q], slot_of(id, 0));
                 const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, cells + etot, st.shadow);
                 peers[k] = src;
                 peersE[k] = src + cells;
@@ -936,16 +1023,18 @@ struct Exec {
                 case SPDZ_NODE_ADD:
                 case SPDZ_NODE_SUB:
                     for (int p = 0; p < r->n; ++p) {
+                        if (!r->parties[p].local) continue;
                         dev(r, p);
                         add(p, id, n.kind == SPDZ_NODE_SUB);
                     }
                     break;
                 case SPDZ_NODE_MUL: {
-                    const bool a = r->parties[0].ns[n.operands[0]].out.is_public;
-                    const bool b = r->parties[0].ns[n.operands[1]].out.is_public;
+                    const bool a = r->parties[r->ref_party()].ns[n.operands[0]].out.is_public;
+                    const bool b = r->parties[r->ref_party()].ns[n.operands[1]].out.is_public;
                     if (!a && !b) beaver(id, r->scalar.at(id), 0);
                     else
                         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                             dev(r, p);
                             mul_local(p, id);
                         }
@@ -953,13 +1042,15 @@ struct Exec {
                 }
                 case SPDZ_NODE_REDUCE_ADD:
                     for (int p = 0; p < r->n; ++p) {
+                        if (!r->parties[p].local) continue;
                         dev(r, p);
                         reduce_add(p, id);
                     }
                     break;
                 case SPDZ_NODE_REDUCE_MUL:
-                    if (r->parties[0].ns[n.operands[0]].out.is_public)
+                    if (r->parties[r->ref_party()].ns[n.operands[0]].out.is_public)
                         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                             dev(r, p);
                             reduce_mul_public(p, id);
                         }
@@ -977,10 +1068,11 @@ struct Exec {
 
     // runtime.cpp:551-560 open the root (batch make_batch(root, 1, 1))
     void open_root() {
-        const Val& rv0 = r->parties[0].ns[r->root].out;
+        const Val& rv0 = r->parties[r->ref_party()].ns[r->root].out;
         const uint64_t L = rv0.lanes;
         if (rv0.is_public) {
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 dev(r, p);
                 lk(cudaMemcpyAsync(r->parties[p].outputs, r->parties[p].ns[r->root].out.pub, L * 4,
                                    cudaMemcpyDeviceToDevice, S(r, p)),
@@ -990,12 +1082,13 @@ struct Exec {
         }
         std::vector<cudaEvent_t> ready(r->n);
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             dev(r, p);
-            ready[p] = next_event(p);
-            lk(cudaEventRecord(ready[p], S(r, p)), "record");
+            ready[p] = publish(p, slot_of(r->root, 0));
         }
         const uint64_t batch = make_batch(r->root, 1, 1);
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             const Val& rv = P.ns[r->root].out;
             dev(r, p);
@@ -1003,7 +1096,7 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                lk(cudaStreamWaitEvent(S(r, p), ready[q], 0), "wait");
+                await(p, q, ready[q], slot_of(r->root, 0));
                 peers[k++] = r->parties[q].ns[r->root].out.v;
                 r->exchanged += L * 4;
             }
@@ -1043,6 +1136,7 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
     }
     for (int p = 0; p < n; ++p) {
         auto& P = r->parties[p];
+        if (!P.local) continue;
         dev(r, p);
         assign_ranks(P.maclog.data(), P.maclog.size());
         uint64_t sbytes = 0;
@@ -1055,6 +1149,11 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
     std::vector<uint32_t> sig(n);
     std::vector<uint64_t> nonce2(n), commits(n);
     for (int p = 0; p < n; ++p) {
+        if (!r->parties[p].local) {  // another process reports this party's sigma
+            sig[p] = 0;
+            if (rep) rep->sigmas[p] = 0;
+            continue;
+        }
         dev(r, p);
         sig[p] = mac_sigma_collect(r->parties[p].ctx, 0);
         nonce2[p] = fresh_nonce();
@@ -1069,30 +1168,39 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
 
 void share_inputs(spdz_run* r) {
     // preproc.cpp:205-243: party 0 opens x - mask, everyone adds the public difference
+    ++r->seq;
     for (auto& [id, off] : r->input_mask_off) {
         const auto& n = r->node(id);
-        auto it = r->input_dev.find(id);
-        need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
-             "ShapeMismatch: no values bound for input node " + std::to_string(id));
-        uint32_t* x0 = it->second;  // reduced cleartext on party 0's device
-        uint32_t*& diff = r->input_diff[id];
-        if (!diff) diff = r->alloc(0, n.lanes);
-        auto& P0 = r->parties[0];
-        dev(r, 0);
-        lk(launch_pub_binop(P0.ctx->stream, 1, x0, false, P0.mask_c + off, false, diff, n.lanes, P0.ctx->sms),
-           "x - r");
-        cudaEvent_t ev = r->ev_input;
-        lk(cudaEventRecord(ev, P0.ctx->stream), "record");
+        uint32_t* diff = r->input_diff[id];  // party 0's buffer (IPC-mapped when party 0 is remote)
+        const uint64_t slot = slot_of(id, 63);
+        if (r->parties[0].local) {
+            auto it = r->input_dev.find(id);
+            need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
+                 "ShapeMismatch: no values bound for input node " + std::to_string(id));
+            uint32_t* x0 = it->second;  // reduced cleartext on party 0's device
+            auto& P0 = r->parties[0];
+            dev(r, 0);
+            lk(launch_pub_binop(P0.ctx->stream, 1, x0, false, P0.mask_c + off, false, diff, n.lanes, P0.ctx->sms),
+               "x - r");
+            lk(cudaEventRecord(r->ev_input, P0.ctx->stream), "record");
+            signal_remote(r, 0, slot);
+        }
+        need(diff != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "input difference of party 0 not imported");
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& o = P.ns[id].out;
             dev(r, p);
-            if (p) lk(cudaStreamWaitEvent(P.ctx->stream, ev, 0), "wait");
+            if (p) {
+                if (r->parties[0].local) lk(cudaStreamWaitEvent(P.ctx->stream, r->ev_input, 0), "wait");
+                else wait_remote(r, p, 0, slot);
+            }
             lk(launch_public(P.ctx->stream, 0, P.mask_v + off, P.mask_m + off, diff, false, 0u, false, p,
                              P.ctx->alpha, o.v, o.m, n.lanes, P.ctx->sms),
                "add_public(diff)");
         }
         for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
             dev(r, p);
             lk(cudaStreamSynchronize(S(r, p)), "sync");
         }
@@ -1106,6 +1214,7 @@ void share_inputs(spdz_run* r) {
             std::vector<uint32_t> red(it->second.size());
             for (size_t i = 0; i < red.size(); ++i) red[i] = it->second[i] % kP;
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 dev(r, p);
                 lk(cudaMemcpy(r->parties[p].ns[id].out.pub, red.data(), red.size() * 4, cudaMemcpyHostToDevice),
                    "H2D pub");
@@ -1114,6 +1223,7 @@ void share_inputs(spdz_run* r) {
         if (n.kind == SPDZ_NODE_CONST) {
             const uint32_t v = n.const_val % kP;
             for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
                 dev(r, p);
                 lk(cudaMemcpy(r->parties[p].ns[id].out.pub, &v, 4, cudaMemcpyHostToDevice), "H2D const");
             }
@@ -1121,6 +1231,35 @@ void share_inputs(spdz_run* r) {
     }
 }
 
+}  // namespace
+
+namespace {
+struct IpcEntry {
+    uint32_t kind;  // 0 flags, 1 node payload, 2 reduce-level payload, 3 root values, 4 input difference
+    uint32_t node, sub, pad;
+    uint64_t offset;
+    cudaIpcMemHandle_t handle;
+};
+struct IpcHeader {
+    uint32_t magic, version, party, n;
+};
+constexpr uint32_t kIpcMagic = 0x5350445au;  // "SPDZ"
+
+// every buffer a peer process reads, for local party p
+template <class F>
+void for_each_export(spdz_run* r, int p, F&& f) {
+    auto& P = r->parties[p];
+    f(0u, 0u, 0u, (void*)P.flags);
+    for (uint32_t id = 0; id < r->nodes.size(); ++id) {
+        auto& st = P.ns[id];
+        if (st.payload) f(1u, id, 0u, (void*)st.payload);
+        for (uint32_t li = 0; li < st.levels.size(); ++li) f(2u, id, li, (void*)st.levels[li].payload);
+    }
+    const Val& rv = P.ns[r->root].out;
+    if (!rv.is_public) f(3u, r->root, 0u, (void*)rv.v);
+    if (p == 0)
+        for (auto& [id, d] : r->input_diff) f(4u, id, 0u, (void*)d);
+}
 }  // namespace
 
 extern "C" {
@@ -1145,18 +1284,28 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
         r->devices.resize(n_parties);
         for (int p = 0; p < n_parties; ++p) r->devices[p] = (opts && opts->devices[p] >= 0) ? opts->devices[p] : 0;
         r->parties.resize(n_parties);
+        if (r->opts.single_party > 0) {  // one party per process; peers arrive via spdz_run_import
+            need(r->opts.single_party <= n_parties, SPDZ_ERR_INVALID_ARGUMENT, "single_party out of range");
+            for (int p = 0; p < n_parties; ++p) r->parties[p].local = p == r->opts.single_party - 1;
+            r->any_remote = n_parties > 1;
+            need(r->opts.external_mac_verify, SPDZ_ERR_INVALID_ARGUMENT,
+                 "single_party runs need external_mac_verify = 1 (sigmas are combined across processes)");
+            load_stream_memops();
+        }
         for (int p = 0; p < n_parties; ++p) {
+            if (!r->parties[p].local) continue;
             int rc = spdz_ctx_create(r->devices[p], p, n_parties, 0, &r->parties[p].ctx);
             if (rc) throw Error(rc, spdz_last_error());
             if (!r->opts.stream_per_party)  // parties sharing a device share its stream
                 for (int q = 0; q < p; ++q)
-                    if (r->devices[q] == r->devices[p]) {
+                    if (r->parties[q].local && r->devices[q] == r->devices[p]) {
                         r->parties[p].ctx->stream = r->parties[q].ctx->stream;
                         break;
                     }
         }
         for (int p = 0; p < n_parties; ++p)  // P2P between party devices (NVLink)
             for (int q = 0; q < n_parties; ++q) {
+                if (!r->parties[p].local || !r->parties[q].local) continue;
                 if (r->devices[p] == r->devices[q]) continue;
                 cudaSetDevice(r->devices[p]);
                 cudaError_t e = cudaDeviceEnablePeerAccess(r->devices[q], 0);
@@ -1182,6 +1331,7 @@ int spdz_run_destroy(spdz_run* r) {
     return guard([&] {
         if (!r) return;
         for (auto& P : r->parties) {
+            for (void* m : P.mapped) cudaIpcCloseMemHandle(m);
             if (!P.ctx) continue;
             cudaSetDevice(P.ctx->device);
             cudaStreamSynchronize(P.ctx->stream);
@@ -1190,7 +1340,7 @@ int spdz_run_destroy(spdz_run* r) {
             if (P.t1) cudaEventDestroy(P.t1);
         }
         if (r->ev_input) {
-            cudaSetDevice(r->devices[0]);
+            cudaSetDevice(r->devices[r->ref_party()]);
             cudaEventDestroy(r->ev_input);
             cudaEventDestroy(r->ev_opened);
             cudaStreamSynchronize(r->copy_stream);
@@ -1203,7 +1353,8 @@ int spdz_run_destroy(spdz_run* r) {
         }
         if (r->host_out && r->host_out_owned) cudaFreeHost(r->host_out);
         for (auto& P : r->parties) {
-            if (P.ctx && P.ctx->stream != P.ctx->own_stream) P.ctx->stream = P.ctx->own_stream;
+            if (!P.ctx) continue;
+            if (P.ctx->stream != P.ctx->own_stream) P.ctx->stream = P.ctx->own_stream;
             spdz_ctx_destroy(P.ctx);
         }
         delete r;
@@ -1255,11 +1406,15 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         if (r->consumed && !reuse)
             throw Error(SPDZ_ERR_TRIPLE_EXHAUSTED,
                         "TripleExhausted: preprocessing of this run was already consumed (deal again)");
+        need(!r->any_remote || r->opts.external_mac_verify, SPDZ_ERR_INVALID_ARGUMENT,
+             "runs with remote parties verify the MAC check externally (external_mac_verify = 1)");
         r->launches0 = g_kernel_launches;
         r->exchanged = 0;
+        ++r->seq;
         r->wall0 = std::chrono::steady_clock::now();
         for (auto& P : r->parties) {
             P.maclog.clear();
+            if (!P.local) continue;
             device_guard(P.ctx);
             lk(cudaEventRecord(P.t0, P.ctx->stream), "t0");
         }
@@ -1271,8 +1426,9 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         r->consumed = true;
         r->in_flight = true;
         // opened outputs to host on a copy stream, overlapping the MAC check
-        const Val& rv = r->parties[0].ns[r->root].out;
-        dev(r, 0);
+        const int op = r->ref_party();
+        const Val& rv = r->parties[op].ns[r->root].out;
+        dev(r, op);
         if (!r->host_out || r->host_out_cap < rv.lanes) {
             need(r->host_out_owned || !r->host_out, SPDZ_ERR_INVALID_ARGUMENT, "bound output buffer too small");
             if (r->host_out) cudaFreeHost(r->host_out);
@@ -1281,9 +1437,10 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
             r->host_out_owned = true;
         }
         r->host_out_len = rv.lanes;
-        lk(cudaEventRecord(r->ev_opened, S(r, 0)), "record opened");
+        lk(cudaEventRecord(r->ev_opened, S(r, op)), "record opened");
         lk(cudaStreamWaitEvent(r->copy_stream, r->ev_opened, 0), "wait opened");
-        lk(cudaMemcpyAsync(r->host_out, r->parties[0].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost, r->copy_stream),
+        lk(cudaMemcpyAsync(r->host_out, r->parties[op].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost,
+                           r->copy_stream),
            "D2H out");
     });
 }
@@ -1293,13 +1450,14 @@ int spdz_run_mac_check(spdz_run* r, int use_coin, uint64_t coin, spdz_run_report
         need(r != nullptr && r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "no online phase in flight");
         r->in_flight = false;
         mac_check(r, rep, use_coin != 0, coin);  // records t1 and synchronises the party streams
-        dev(r, 0);
+        dev(r, r->ref_party());
         lk(cudaStreamSynchronize(r->copy_stream), "sync out");
         auto t1 = std::chrono::steady_clock::now();
         if (rep) {
             rep->online_ms = std::chrono::duration<double, std::milli>(t1 - r->wall0).count();
             double dmax = 0;
             for (auto& P : r->parties) {
+                if (!P.local) continue;
                 device_guard(P.ctx);
                 float ms = 0;
                 lk(cudaEventElapsedTime(&ms, P.t0, P.t1), "elapsed");
@@ -1366,6 +1524,90 @@ int spdz_run_node_share(spdz_run* r, int party, uint32_t node, spdz_share_t* out
         out->vals = v.is_public ? v.pub : v.v;
         out->macs = v.is_public ? nullptr : v.m;
         out->lanes = v.lanes;
+    });
+}
+
+
+int spdz_run_export(spdz_run* r, void* buf, uint64_t cap, uint64_t* len) {
+    return guard([&] {
+        need(r != nullptr && len != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "bad export args");
+        load_stream_memops();
+        std::vector<uint8_t> out;
+        for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
+            dev(r, p);
+            std::vector<IpcEntry> es;
+            for_each_export(r, p, [&](uint32_t kind, uint32_t node, uint32_t sub, void* ptr) {
+                IpcEntry e{};
+                e.kind = kind;
+                e.node = node;
+                e.sub = sub;
+                CUdeviceptr base = 0;
+                size_t size = 0;
+                need(g_addrrange(&base, &size, (CUdeviceptr)ptr) == CUDA_SUCCESS, SPDZ_ERR_CUDA, "cuMemGetAddressRange");
+                e.offset = (uint64_t)((CUdeviceptr)ptr - base);
+                cuda_check(cudaIpcGetMemHandle(&e.handle, (void*)base), "cudaIpcGetMemHandle");
+                es.push_back(e);
+            });
+            IpcHeader h{kIpcMagic, 1u, (uint32_t)p, (uint32_t)es.size()};
+            const uint8_t* hb = reinterpret_cast<const uint8_t*>(&h);
+            out.insert(out.end(), hb, hb + sizeof h);
+            const uint8_t* eb = reinterpret_cast<const uint8_t*>(es.data());
+            out.insert(out.end(), eb, eb + es.size() * sizeof(IpcEntry));
+        }
+        *len = out.size();
+        if (buf) {
+            need(cap >= out.size(), SPDZ_ERR_INVALID_ARGUMENT, "export buffer too small");
+            std::memcpy(buf, out.data(), out.size());
+        }
+    });
+}
+
+int spdz_run_import(spdz_run* r, const void* blob, uint64_t len) {
+    return guard([&] {
+        need(r != nullptr && blob != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "bad import args");
+        const uint8_t* b = static_cast<const uint8_t*>(blob);
+        uint64_t at = 0;
+        const int lp = r->ref_party();
+        dev(r, lp);
+        while (at + sizeof(IpcHeader) <= len) {
+            IpcHeader h;
+            std::memcpy(&h, b + at, sizeof h);
+            at += sizeof h;
+            need(h.magic == kIpcMagic && h.version == 1, SPDZ_ERR_MALFORMED_SHARE_MESSAGE,
+                 "MalformedShareMessage: not a spdz_run export");
+            need(h.party < (uint32_t)r->n, SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: party");
+            need(at + (uint64_t)h.n * sizeof(IpcEntry) <= len, SPDZ_ERR_MALFORMED_SHARE_MESSAGE,
+                 "MalformedShareMessage: truncated export");
+            auto& Q = r->parties[h.party];
+            const bool skip = Q.local;  // our own export (all-gathered blobs)
+            for (uint32_t i = 0; i < h.n; ++i, at += sizeof(IpcEntry)) {
+                if (skip) continue;
+                IpcEntry e;
+                std::memcpy(&e, b + at, sizeof e);
+                void* base = nullptr;
+                cuda_check(cudaIpcOpenMemHandle(&base, e.handle, cudaIpcMemLazyEnablePeerAccess),
+                           "cudaIpcOpenMemHandle");
+                Q.mapped.push_back(base);
+                uint32_t* ptr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(base) + e.offset);
+                need(e.node < r->nodes.size(), SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: node");
+                auto& st = Q.ns[e.node];
+                switch (e.kind) {
+                    case 0: Q.flags = ptr; break;
+                    case 1: st.payload = ptr; break;
+                    case 2:
+                        need(e.sub < st.levels.size(), SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage");
+                        st.levels[e.sub].payload = ptr;
+                        break;
+                    case 3: st.out.v = ptr; break;
+                    case 4:
+                        need(h.party == 0, SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: diff");
+                        r->input_diff[e.node] = ptr;
+                        break;
+                    default: throw Error(SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: entry kind");
+                }
+            }
+        }
     });
 }
 

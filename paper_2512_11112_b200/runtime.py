@@ -174,7 +174,8 @@ class LocalRun:
 
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
-                 stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False):
+                 stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
+                 single_party: int | None = None):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -185,7 +186,9 @@ class LocalRun:
         o.stream_per_party = int(stream_per_party)
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
-        o.external_mac_verify = int(external_mac_verify)
+        o.external_mac_verify = int(external_mac_verify or single_party is not None)
+        if single_party is not None:  # this process owns only party `single_party` (peers via export/import)
+            o.single_party = int(single_party) + 1
         for p in range(_lib.MAX_PARTIES):
             o.devices[p] = (devices[p] if devices and p < len(devices) else 0)
         self._nodes = graph.to_c()
@@ -203,6 +206,19 @@ class LocalRun:
             self.close()
         except Exception:
             pass
+
+    def export_ipc(self) -> bytes:
+        """CUDA IPC handles of this process's party buffers (send to the peer processes)."""
+        n = C.c_uint64()
+        check(lib().spdz_run_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().spdz_run_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def import_ipc(self, blobs):
+        """Maps the peers' export blobs (own blob is skipped)."""
+        data = b"".join(blobs)
+        check(lib().spdz_run_import(self.h, data, len(data)))
 
     def deal(self, seed: int):
         check(lib().spdz_run_deal(self.h, seed))

@@ -1,0 +1,75 @@
+"""One party per process (the multi-GPU layout: party p on its own GPU set),
+here two processes sharing one B200: opening payloads, input differences and
+completion flags travel by CUDA IPC, ordering by stream memory operations.
+The opened outputs and each party's MAC sigma equal the single-process run
+(and the oracle's share-level simulation of the reference protocol)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+P = O.P
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _party(rank, world, port, kind, n, coin, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_11112_b200 import LocalRun, chain_graph
+        x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+        r = LocalRun(chain_graph(kind, n), 2, coin=coin, single_party=rank)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, r.export_ipc())
+        r.import_ipc(blobs)
+        if rank == 0:  # party 0 owns the private inputs (preproc.cpp:146-150)
+            r.bind_inputs({"x": x, "y": y})
+        r.share_inputs()
+        rep = r.online()
+        q.put((rank, rep.outputs.copy(), rep.sigmas[rank]))
+        dist.barrier()  # keep our buffers mapped until the peer is done
+        r.close()
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["heavy", "mixed"])
+def test_two_party_processes_over_ipc(gpu, kind):
+    n, coin = 4099, 0xC0FFEE
+    want = O.sim_chain(kind, 2, O.rand_field_vec(n, 1), O.rand_field_vec(n, 2), 1, coin)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_party, args=(r, 2, port, kind, n, coin, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        m = q.get(timeout=300)
+        assert not (isinstance(m[1], str) and m[1] == "error"), m
+        res[m[0]] = m
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        np.testing.assert_array_equal(res[rank][1], want["outputs"])
+        assert res[rank][2] == want["sigmas"][rank]
+    assert (res[0][2] + res[1][2]) % P == 0
