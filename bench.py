@@ -97,8 +97,13 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dev = int(os.environ.get("SPDZ_BENCH_DEVICE", local))
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("SPDZ_BENCH_BACKEND", "nccl")  # gloo: several ranks on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -113,7 +118,7 @@ def allmax(world, v: float) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -179,33 +184,52 @@ def run_ours(args, world, rank, local):
     from paper_2512_11112_b200 import LocalRun, chain_graph
     from paper_2512_11112_b200._lib import lib
 
-    dev = local
+    dev = int(os.environ.get("SPDZ_BENCH_DEVICE", local))  # override only for single-GPU tests
     torch.cuda.set_device(dev)
-    lanes = args.lanes
     n_mul = 4 if args.kind == "heavy" else (2 if args.kind == "mixed" else 0)
-    mults_step = n_mul * lanes
-    g = chain_graph(args.kind, lanes)
     coin_fn = None
-    if world > 1:
-        # weak scaling: rank r holds lanes [r*lanes, (r+1)*lanes) of one global circuit; its
-        # preprocessing is exactly that slice of the global dealer output, MAC ranks are global,
-        # the coin is agreed after the openings and sigma partials are verified across ranks.
-        from paper_2512_11112_b200 import parallel
-        run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1,
-                       shard=(rank * lanes, world * lanes), external_mac_verify=True)
-        coin_fn = parallel.joint_coin
-    else:
+    party = None
+    if world == 1:
+        # both parties on this GPU (each party's kernels get the whole HBM in turn)
+        lanes = args.lanes
+        total = lanes
+        g = chain_graph(args.kind, lanes)
         run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1)
+        parallelism = "2 parties on 1 GPU"
+    else:
+        # party p owns GPUs [p*G, (p+1)*G) (G = world/2); GPU k of party 0 and GPU k of party 1
+        # hold the same lane shard and open to each other over NVLink (CUDA IPC peer loads,
+        # stream-memory-op ordering).  Each GPU holds one party of 2*lanes lanes, i.e. the same
+        # per-GPU work as the 1-GPU run (two parties of `lanes`): weak scaling.
+        from paper_2512_11112_b200 import parallel
+        assert world % 2 == 0, "multi-GPU runs need an even number of GPUs (two parties)"
+        G = world // 2
+        party, k = rank // G, rank % G
+        lanes = 2 * args.lanes
+        total = G * lanes
+        g = chain_graph(args.kind, lanes)
+        run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1,
+                       shard=(k * lanes, total), single_party=party)
+        import torch.distributed as dist
+        blobs = [None] * world
+        dist.all_gather_object(blobs, run.export_ipc())
+        peer = (1 - party) * G + k
+        run.import_ipc([blobs[peer]])
+        coin_fn = parallel.joint_coin
+        parallelism = f"2 parties x {G} GPUs, lane-sharded, NVLink P2P opens"
+    mults_step = n_mul * total  # whole job, per step
     rng = np.random.default_rng(1234 + rank)
     x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
     y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
     x_pin = torch.from_numpy(x).pin_memory().numpy()
     y_pin = torch.from_numpy(y).pin_memory().numpy()
     inputs = {"x": x_pin, "y": y_pin}
+    owns_inputs = party in (None, 0)  # party 0 owns the private inputs (preproc.cpp:146-150)
 
     def prepare(seed):
         run.deal(seed)
-        run.bind_inputs(inputs)
+        if owns_inputs:
+            run.bind_inputs(inputs)
         run.share_inputs()
 
     def step():
@@ -240,7 +264,7 @@ def run_ours(args, world, rank, local):
                 a[f] += st[f]
     clocks = sampler.stop()
     total_ms = allmax(world, float(np.sum(dev_ms)))
-    value = mults_step * world * args.steps / (total_ms / 1e3)
+    value = mults_step * args.steps / (total_ms / 1e3)
     # ---- end to end: host buffers in, opened outputs out (public API) ----
     out_pin = torch.empty(lanes, dtype=torch.uint32).pin_memory().numpy()
     run.bind_output(out_pin)
@@ -251,7 +275,8 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
-        run.bind_inputs(inputs)          # H2D of the step's inputs
+        if owns_inputs:
+            run.bind_inputs(inputs)      # H2D of the step's inputs
         t1 = time.perf_counter()
         run.share_inputs()
         t2 = time.perf_counter()
@@ -263,7 +288,7 @@ def run_ours(args, world, rank, local):
     log(f"e2e per step: bind {parts[0] / args.steps:.3f} ms, share {parts[1] / args.steps:.3f} ms, "
         f"online+D2H {parts[2] / args.steps:.3f} ms")
     e2e_ms = allmax(world, e2e_ms)
-    e2e = mults_step * world * args.steps / (e2e_ms / 1e3)
+    e2e = mults_step * args.steps / (e2e_ms / 1e3)
     # ---- roofline of the dominant kernel class ----
     peak, peak_kind = load_peaks()
     dom = max(("mask", "combine", "sigma", "open"), key=lambda n: kstat[n]["ms"])
@@ -295,16 +320,17 @@ def run_ours(args, world, rank, local):
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u32 (F_p, p=2^32-5)", "data": "synthetic",
                 "config": {"workload": f"{args.kind} mul-chain (4 Beaver multiplies + root open + MAC check), "
-                                       f"2 parties on each GPU, {lanes} lanes per GPU",
-                           "lanes_per_gpu": lanes, "parties": 2,
-                           "parallelism": f"lane-sharded x{world} (2 parties per GPU, global MAC check)",
+                                       f"2 parties, {total} lanes",
+                           "lanes_total": total, "parties": 2, "parallelism": parallelism,
                            "l2": "working set >> 126 MB L2 (inputs larger than L2, no flush needed)",
                            "timed": "online phase only (dealer + input sharing between steps, untimed)"},
                 "clocks": clocks, "gpu_launches": launches,
-                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * lanes * 4,
-                        "d2h_bytes_per_step": lanes * 4, "ms_per_step": e2e_ms / args.steps},
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * total * 4,
+                        "d2h_bytes_per_step": total * 4 * (1 if world == 1 else 2),
+                        "ms_per_step": e2e_ms / args.steps},
                 "roofline": roofline, "cpu_baseline": cpu_baseline}
         print(json.dumps(line), flush=True)
+    barrier(world)  # peers may still hold IPC mappings of our buffers
     run.close()
 
 
