@@ -10,7 +10,10 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "libspdz_b200.so"
+import os as _os
+
+# SPDZ_B200_LIB: alternate build of the same library (reduction-variant experiments only)
+LIB_PATH = Path(_os.environ.get("SPDZ_B200_LIB", str(Path(__file__).resolve().parent / "libspdz_b200.so")))
 MAX_PARTIES = 8
 
 u32p = C.POINTER(C.c_uint32)

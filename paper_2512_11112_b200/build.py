@@ -31,12 +31,13 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra_flags=()) -> Path:
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out: Path | None = None) -> Path:
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [
         ROOT / "include" / "spdz_b200.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = ROOT / "build" / "obj"
+    lib = Path(out) if out else LIB
+    if not force and not _stale(lib, deps):
+        return lib
+    objdir = ROOT / "build" / ("obj" if out is None else "obj_" + lib.parent.name)
     objdir.mkdir(parents=True, exist_ok=True)
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
              *ARCH, *extra_flags]
@@ -53,14 +54,18 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> Path:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{out}")
         if verbose and out:
             sys.stdout.write(out)
-    tmp = LIB.with_suffix(".so.tmp")
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--barrett" in sys.argv:  # reduction-variant build for the ncu comparison (build/barrett/)
+        print(build(force=True, extra_flags=["-DSPDZ_REDUCE_BARRETT"], out=ROOT / "build" / "barrett" / "libspdz_b200.so"))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
