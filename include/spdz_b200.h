@@ -349,7 +349,9 @@ int spdz_run_deal(spdz_run* run, uint64_t seed);
 /* Cleartext input for an INPUT node (host pointer).  Private inputs are shared
  * with the dealer's input masks (preproc.cpp:205-243) during spdz_run_share_inputs. */
 int spdz_run_bind_input(spdz_run* run, uint32_t node, const uint32_t* host_vals, uint64_t len);
-/* Input sharing (setup, excluded from online time as in runtime.cpp:511-534). */
+/* Input sharing (setup, excluded from online time as in runtime.cpp:511-534).
+ * Asynchronous: it is stream-ordered before the next online phase; bound host
+ * inputs must stay untouched until that phase has begun. */
 int spdz_run_share_inputs(spdz_run* run);
 /* Online phase: node execution, root open, deferred MAC check.  Re-runnable
  * (triple consumption is reset per call only when `reuse_preprocessing` = 1 —

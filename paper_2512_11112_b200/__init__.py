@@ -9,9 +9,10 @@ layer).  The compute path is hand-written sm_100a CUDA behind a C ABI
 from . import errors  # noqa: F401
 from .backend import (BackendCapability, BackendRegistry, Context, DeviceShare, DeviceTriple,  # noqa: F401
                       GpuBackend, ShareVec, TripleShares)
-from .runtime import Graph, LocalRun, NodeSpec, RunReport, chain_graph, linear_graph, reduce_graph, run_local  # noqa
+from .runtime import (Graph, LocalRun, NodeSpec, RunReport, StreamedRun, chain_graph, linear_graph,  # noqa
+                      reduce_graph, run_local)
 
 P = 4294967291
 __all__ = ["errors", "GpuBackend", "BackendRegistry", "Context", "ShareVec", "TripleShares", "DeviceShare",
            "DeviceTriple", "Graph", "NodeSpec", "LocalRun", "run_local", "chain_graph", "linear_graph",
-           "reduce_graph", "RunReport", "P"]
+           "reduce_graph", "RunReport", "StreamedRun", "P"]

@@ -1199,11 +1199,6 @@ void share_inputs(spdz_run* r) {
                              P.ctx->alpha, o.v, o.m, n.lanes, P.ctx->sms),
                "add_public(diff)");
         }
-        for (int p = 0; p < r->n; ++p) {
-            if (!r->parties[p].local) continue;
-            dev(r, p);
-            lk(cudaStreamSynchronize(S(r, p)), "sync");
-        }
     }
     for (uint32_t id = 0; id < r->nodes.size(); ++id) {  // public inputs and constants
         const auto& n = r->nodes[id];

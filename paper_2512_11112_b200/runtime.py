@@ -12,6 +12,7 @@ the deferred MAC check (runtime.cpp:467-506).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -237,15 +238,18 @@ class LocalRun:
         self._out = out
         check(lib().spdz_run_bind_output(self.h, out.ctypes.data, out.size))
 
-    def online(self, reuse: bool = False, coin_fn=None) -> RunReport:
-        """One online phase.  `coin_fn()` (optional) is called after the
-        openings to agree on the MAC-check coin (e.g. parallel.joint_coin)."""
+    def online_begin(self, reuse: bool = False):
+        """Node execution + root open, enqueued (asynchronous); finish with mac_check()."""
+        check(lib().spdz_run_online_begin(self.h, int(reuse)))
+
+    def mac_check(self, coin: int | None = None) -> RunReport:
+        """Deferred MAC check of the phase begun by online_begin(); `coin` = agreed coin
+        (None: the run's own commit/reveal or fixed coin)."""
         rep = _lib.RunReport()
-        if coin_fn is None:
-            check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
-        else:
-            check(lib().spdz_run_online_begin(self.h, int(reuse)))
-            check(lib().spdz_run_mac_check(self.h, 1, int(coin_fn()), C.byref(rep)))
+        check(lib().spdz_run_mac_check(self.h, 0 if coin is None else 1, int(coin or 0), C.byref(rep)))
+        return self._report(rep)
+
+    def _report(self, rep) -> RunReport:
         n = C.c_uint64()
         check(lib().spdz_run_outputs(self.h, None, 0, C.byref(n)))
         if getattr(self, "_out", None) is not None:
@@ -258,6 +262,17 @@ class LocalRun:
                          list(rep.sigmas)[: self.n], rep.coin,
                          {name: dict(launches=rep.kstat[i].launches, ms=rep.kstat[i].ms, bytes=rep.kstat[i].bytes)
                           for i, name in enumerate(_lib.KSTAT_NAMES)})
+
+    def online(self, reuse: bool = False, coin_fn=None) -> RunReport:
+        """One online phase.  `coin_fn()` (optional) is called after the
+        openings to agree on the MAC-check coin (e.g. parallel.joint_coin)."""
+        rep = _lib.RunReport()
+        if coin_fn is None:
+            check(lib().spdz_run_online(self.h, int(reuse), C.byref(rep)))
+        else:
+            check(lib().spdz_run_online_begin(self.h, int(reuse)))
+            check(lib().spdz_run_mac_check(self.h, 1, int(coin_fn()), C.byref(rep)))
+        return self._report(rep)
 
     def node_share(self, party: int, node: int):
         s = _lib.Share()
@@ -282,6 +297,64 @@ def device_to_host(ptr: int, n: int) -> np.ndarray:
 
     torch.cuda.synchronize()
     return torch.as_tensor(_CAI(), device="cuda").cpu().numpy().copy()
+
+
+class StreamedRun:
+    """Host-streamed online phase of a lane-parallel circuit: the `total` lanes are
+    split into `chunks` exact lane shards (each a LocalRun with shard=(offset, total),
+    i.e. exactly its slice of the global preprocessing and global MAC ranks), each on
+    its own CUDA streams, so the H2D of chunk c+1 and the D2H of chunk c-1 overlap
+    the kernels of chunk c.  One MAC check covers all chunks: the coin is agreed
+    after every opening and the per-party sigma partials are summed (runtime.cpp:467-506)."""
+
+    def __init__(self, graph_fn, n_parties: int, total: int, chunks: int = 4, dealer_seed: int = 1,
+                 coin: int | None = None, devices=None):
+        self.n, self.total, self.coin = n_parties, total, coin
+        base, extra = divmod(total, chunks)
+        self.ranges = []
+        off = 0
+        for c in range(chunks):
+            L = base + (1 if c < extra else 0)
+            self.ranges.append((off, L))
+            off += L
+        self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
+                              shard=(o, total), external_mac_verify=True) for o, L in self.ranges]
+
+    def close(self):
+        for r in self.runs:
+            r.close()
+
+    def deal(self, seed: int):
+        for r in self.runs:
+            r.deal(seed)
+
+    def bind_output(self, out: np.ndarray):
+        for r, (o, L) in zip(self.runs, self.ranges):
+            r.bind_output(out[o:o + L])
+
+    def run(self, inputs: dict) -> RunReport:
+        """inputs: full-length host arrays (pin them for overlap).  Returns the combined report."""
+        for r, (o, L) in zip(self.runs, self.ranges):
+            r.bind_inputs({k: v[o:o + L] for k, v in inputs.items()})
+            r.share_inputs()
+            r.online_begin()
+        coin = self.coin
+        if coin is None:  # parties' nonces, revealed after all openings, chained (runtime.cpp:474-489)
+            coin = 0
+            for nz in (int.from_bytes(os.urandom(8), "little") for _ in range(self.n)):
+                coin = lib().spdz_fnv1a64((C.c_uint64 * 1)(nz), 8, coin)
+        reps = [r.mac_check(coin) for r in self.runs]
+        sig = [sum(rep.sigmas[p] for rep in reps) % 4294967291 for p in range(self.n)]
+        nonces = [int.from_bytes(os.urandom(8), "little") for _ in range(self.n)]
+        commits = [lib().spdz_commit_sigma(s, nz) for s, nz in zip(sig, nonces)]
+        rc = lib().spdz_verify_sigmas((C.c_uint32 * self.n)(*sig), (C.c_uint64 * self.n)(*nonces),
+                                      (C.c_uint64 * self.n)(*commits), self.n)
+        check(rc)
+        outs = np.concatenate([rep.outputs for rep in reps])
+        return RunReport(outs, max(rep.online_ms for rep in reps), max(rep.online_device_ms for rep in reps),
+                         sum(rep.scalar_triples_consumed for rep in reps), 0,
+                         sum(rep.bytes_exchanged for rep in reps), None,
+                         sum(rep.kernel_launches for rep in reps), sig, coin, None)
 
 
 def run_local(graph: Graph, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,

@@ -192,3 +192,28 @@ def test_lane_sharding_equals_unsharded_run(gpu, kind, world):
     np.testing.assert_array_equal(np.concatenate(outs), rf.outputs)
     assert sig == rf.sigmas
     full.close()
+
+
+@pytest.mark.parametrize("kind,chunks", [("heavy", 3), ("mixed", 4)])
+def test_streamed_run_equals_unsharded(gpu, kind, chunks):
+    """Host-streamed execution (lane chunks as exact shards on their own streams, one
+    joint MAC check) returns the unsharded outputs and per-party sigmas."""
+    from paper_2512_11112_b200 import LocalRun, StreamedRun, chain_graph
+    n, coin = 5003, 0xABC123
+    x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+    full = LocalRun(chain_graph(kind, n), 2, coin=coin)
+    full.bind_inputs({"x": x, "y": y})
+    full.share_inputs()
+    rf = full.online()
+    full.close()
+    sr = StreamedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks, coin=coin)
+    out = np.zeros(n, np.uint32)
+    sr.bind_output(out)
+    rep = sr.run({"x": x, "y": y})
+    np.testing.assert_array_equal(rep.outputs, rf.outputs)
+    np.testing.assert_array_equal(out, rf.outputs)
+    assert rep.sigmas == rf.sigmas
+    sr.deal(7)  # fresh preprocessing, same answer, MAC check verifies internally
+    rep2 = sr.run({"x": x, "y": y})
+    np.testing.assert_array_equal(rep2.outputs, rf.outputs)
+    sr.close()
