@@ -149,6 +149,48 @@ def main():
     # tensor pipe: 16 u8 x u8 MACs per modMAC; dense int8 peak 4.5 POPS = 2.25e15 MAC/s (nominal, B200)
     c3["tcgen05"]["i8_mac_per_s"] = 16 * c3["tcgen05"]["modmac_per_s"]
     c3["tcgen05"]["frac_of_nominal_i8"] = c3["tcgen05"]["i8_mac_per_s"] / 2.25e15
+    # batched large shapes (the integer-pipe target needs a batch dimension) + int8 peak
+    big = []
+    for bd, bb in ((4096, 1024), (8192, 1024)):
+        Wb = torch.from_numpy(rnd(bd * bd, 7)).cuda()
+        xb = DeviceShare(torch.from_numpy(rnd(bd * bb, 8)).cuda(), torch.from_numpy(rnd(bd * bb, 9)).cuda())
+        yb = DeviceShare.empty(bd * bb)
+        ab = (ctx.h, bd, bd, bb, 1, Wb.data_ptr(), None, C.byref(dshare(xb)), None, C.byref(dshare(yb)))
+        check(lib().spdz_set_gemm_path(2))
+        for _ in range(2):
+            check(lib().spdz_linear_secret_public(*ab))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            check(lib().spdz_linear_secret_public(*ab))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        mm = 2 * bd * bd * bb
+        big.append({"shape": [bd, bd, bb], "tcgen05_ms": ms, "modmac_per_s": mm / (ms / 1e3),
+                    "i8_mac_per_s": 16 * mm / (ms / 1e3)})
+        del Wb, xb, yb
+    check(lib().spdz_set_gemm_path(0))
+    a8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+    b8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+    for _ in range(3):
+        torch._int_mm(a8, b8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        torch._int_mm(a8, b8)
+    e1.record()
+    torch.cuda.synchronize()
+    i8_peak_mac = 8192 ** 3 / (e0.elapsed_time(e1) / 10 / 1e3)
+    for e in big:
+        e["frac_of_measured_i8"] = e["i8_mac_per_s"] / i8_peak_mac
+        e["frac_of_nominal_i8"] = e["i8_mac_per_s"] / 2.25e15
+    c3["tcgen05"]["frac_of_measured_i8"] = c3["tcgen05"]["i8_mac_per_s"] / i8_peak_mac
+    c3["batched_large"] = big
+    c3["measured_i8_peak_mac_per_s"] = i8_peak_mac
+    c3["i8_peak_source"] = "cuBLASLt int8 GEMM via torch._int_mm, 8192^3, this device"
     if not args.no_ref:
         lin = {"x": rnd(din, 4), "W": rnd(din * dout, 5), "b": rnd(dout, 6)}
         one = ref_online(workloads.linear_ir(din, dout, w_private=False), lin, threads)

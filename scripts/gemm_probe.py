@@ -89,3 +89,20 @@ for path in (2, 1):
     e1.record()
     torch.cuda.synchronize()
     print(f"path {path}: {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call", flush=True)
+
+if "--int8-peak" in sys.argv:
+    # measured dense int8 tensor peak on this device: cuBLASLt IMMA through torch._int_mm
+    for nn in (8192, 16384):
+        a = torch.randint(-128, 127, (nn, nn), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (nn, nn), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        print(f"int8 peak probe {nn}^3: {ms:.3f} ms = {2 * nn ** 3 / ms / 1e9:.1f} TOPS", flush=True)
