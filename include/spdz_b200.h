@@ -121,6 +121,10 @@ int spdz_capability(const spdz_ctx* ctx, spdz_capability_t* out);
 /* Measured CUDA-core integer pipe rate on ctx's device: IMAD.WIDE.U32 per second
  * (the roofline denominator of the CUDA-core modular GEMM) and all integer ops/s. */
 int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_int_per_s);
+/* Diagnostic: out[2i] = a representative < 2^32 of in[i] mod p, out[2i+1] = one of
+ * splitmix64-finaliser(in[i]) mod p (the MAC-check coefficient arithmetic of k_mac_sigma);
+ * device pointers, synchronous. */
+int spdz_diag_rep_check(spdz_ctx* ctx, const uint64_t* d_in, uint64_t n, uint32_t* d_out);
 /* Diagnostic switches of the tcgen05 GEMM (bit 0: skip TMA loads, bit 1: skip MMAs); results
  * are invalid while non-zero.  Attribution experiments only. */
 int spdz_diag_gemm_tc_flags(uint32_t flags);

@@ -78,15 +78,15 @@ void mac_sigma_launch(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n,
     for (uint64_t base = 0; base < n; base += kMacTableSegs) {
         MacTable tab{};
         tab.n = (uint32_t)std::min<uint64_t>(kMacTableSegs, n - base);
-        uint64_t chunks = 0;
+        uint64_t recs = 0;
         for (uint32_t i = 0; i < tab.n; ++i) {
             const auto& sg = segs[base + i];
             need(sg.len == 0 || (sg.value && sg.mac_a), SPDZ_ERR_INVALID_ARGUMENT, "null MAC segment");
             tab.seg[i] = MacSegDev{sg.value, sg.mac_a, sg.mac_b, sg.len, sg.j0};
-            tab.first[i] = chunks;
-            chunks += (sg.len + kSigmaChunk - 1) / kSigmaChunk;
+            tab.rec0[i] = recs;
+            recs += sg.len;
         }
-        tab.first[tab.n] = chunks;
+        tab.rec0[tab.n] = recs;
         launch_ok(launch_mac_sigma(ctx->stream, tab, coin, ctx->alpha, ctx->d_acc + slot, ctx->sms), "k_mac_sigma");
     }
 }

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 
+#include "field.cuh"
 #include "internal.hpp"
 
 namespace {
@@ -31,9 +32,31 @@ __global__ void __launch_bounds__(256) k_imad_wide_peak(uint32_t iters, uint32_t
     if (s == 0x123456789ull) sink[0] = s;
 }
 
+// out[2i] = rep_mod_p(v_i), out[2i+1] = mac_coeff_rep(v_i) for u64 v_i (edge-case checks of
+// the MAC-check record arithmetic against v mod p / reduce(mix64(v)) on the host).
+__global__ void k_rep_check(const unsigned long long* in, uint64_t n, uint32_t* out, spdzb200::SigConsts kc) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t l = (uint32_t)in[i], h = (uint32_t)(in[i] >> 32);
+        out[2 * i] = spdzb200::rep_mod_p(l, h, kc.five);
+        out[2 * i + 1] = spdzb200::mac_coeff_rep(l, h, kc);
+    }
+}
+
 }  // namespace
 
 using namespace spdzb200;
+
+extern "C" int spdz_diag_rep_check(spdz_ctx* ctx, const uint64_t* d_in, uint64_t n, uint32_t* d_out) {
+    return guard([&] {
+        need(ctx && (n == 0 || (d_in && d_out)), SPDZ_ERR_INVALID_ARGUMENT, "bad diag args");
+        device_guard(ctx);
+        if (n == 0) return;
+        k_rep_check<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, ctx->stream>>>(
+            reinterpret_cast<const unsigned long long*>(d_in), n, d_out, spdzb200::SigConsts{});
+        cuda_check(cudaGetLastError(), "k_rep_check");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
 
 extern "C" int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_int_per_s) {
     return guard([&] {

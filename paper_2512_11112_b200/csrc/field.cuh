@@ -94,4 +94,57 @@ __host__ __device__ __forceinline__ uint32_t mac_coeff(uint64_t coin, uint64_t j
     return fp_reduce64(mix64(coin + (j + 1) * kGamma));
 }
 
+#ifdef __CUDACC__
+// ---- MAC-check record arithmetic on 32-bit halves (kernels.cu k_mac_sigma) ----
+// ~45 instructions per record, split between the ALU pipe (xor/funnel shifts,
+// carry chains) and the fma-heavy pipe (multiplies, the h >> s halves of the
+// xorshifts, the fold by 5); ncu source-level sampling showed the ALU pipe as
+// the throttle when every shift and carry sat there.
+struct Acc96 {
+    uint32_t w0 = 0, w1 = 0, w2 = 0;
+    __device__ __forceinline__ void add(uint64_t v) {
+        asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, 0;"
+            : "+r"(w0), "+r"(w1), "+r"(w2)
+            : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+    }
+    __device__ __forceinline__ uint32_t mod() const {  // (w2 2^64 + w1 2^32 + w0) mod p, < 2^38 before the fold
+        return fp_reduce64((uint64_t)w0 + 5ull * w1 + 25ull * w2);
+    }
+};
+
+// Small constants passed as kernel parameters so that ptxas cannot fold
+// "h * 2^k" / "h * 5" into ALU shifts/LEAs: the multiplies then run on the
+// fma-heavy pipe, which the ALU-bound MAC-check record math leaves idle.
+struct SigConsts {
+    uint32_t sh30 = 1u << 2, sh27 = 1u << 5, sh31 = 1u << 1, five = 5u;
+};
+
+// z ^= z >> s (s < 32); hm = 2^(32-s): h >> s = umulhi(h, hm) on the fma pipe
+__device__ __forceinline__ void xorshift_r(uint32_t& l, uint32_t& h, int s, uint32_t hm) {
+    l ^= __funnelshift_r(l, h, s);
+    h ^= __umulhi(h, hm);
+}
+__device__ __forceinline__ void mul_const(uint32_t& l, uint32_t& h, uint32_t cl, uint32_t ch) {  // z *= c (mod 2^64)
+    const uint32_t t1 = h * cl, t2 = l * ch, hw = __umulhi(l, cl);
+    l = l * cl;
+    h = hw + t1 + t2;
+}
+// r' < 2^32 with r' == (h 2^32 + l) (mod p); not necessarily canonical.
+// s = l + 5h < 6 2^32; t = s_lo + 5 s_hi < 2^32 + 25; r' = t_lo + 5 t_hi (t_lo < 25 if t_hi).
+__device__ __forceinline__ uint32_t rep_mod_p(uint32_t l, uint32_t h, uint32_t five) {
+    const uint64_t s = (uint64_t)h * five + l;
+    const uint64_t t = (uint64_t)(uint32_t)(s >> 32) * five + (uint32_t)s;
+    return (uint32_t)(t >> 32) * five + (uint32_t)t;
+}
+// r' < 2^32 with r' == mix64(h:l) (mod p)  (hash.hpp:21-26, reduce: field.hpp:14)
+__device__ __forceinline__ uint32_t mac_coeff_rep(uint32_t l, uint32_t h, const SigConsts& kc) {
+    xorshift_r(l, h, 30, kc.sh30);
+    mul_const(l, h, 0x1ce4e5b9u, 0xbf58476du);
+    xorshift_r(l, h, 27, kc.sh27);
+    mul_const(l, h, 0x133111ebu, 0x94d049bbu);
+    xorshift_r(l, h, 31, kc.sh31);
+    return rep_mod_p(l, h, kc.five);
+}
+#endif  // __CUDACC__
+
 }  // namespace spdzb200

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "async.cuh"
 #include "field.cuh"
 #include "internal.hpp"
 
@@ -31,25 +32,6 @@ namespace {
 constexpr int TM = 128;   // rows per CTA tile (UMMA M)
 constexpr int TK = 64;    // K bytes (= elements) per stage
 constexpr int kThreadsTc = 128;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    uint32_t done = 0;
-    for (uint32_t it = 0; it < (1u << 26); ++it) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase));
-        if (done) return;
-    }
-    __trap();
-}
 
 // SMEM matrix descriptor, K-major, SWIZZLE_NONE (layout type 0), sm100 version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -115,17 +97,6 @@ __device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
     return (r >> 3) * kSBO + (k >> 4) * kLBO + (r & 7) * 16 + (k & 15);
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
 // out plane mapping of C[row][col] (see launch_modgemm_tc)
 struct TcOut {
     int mode;          // 0: cols [0,batch) -> y0, [batch, 2 batch) -> y1;  1: rows [0,dout) -> y0, rest -> y1
@@ -159,7 +130,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             mbar_init(&empty[s], 1);
         }
         mbar_init(done, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_fence_init();
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -181,7 +152,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
             const uint32_t dst = sbase + s * L::STAGE;
             if (dbg & 1) {  // diagnostic: no loads
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+                mbar_arrive(&full[s]);
                 continue;
             }
             mbar_expect_tx(&full[s], L::STAGE);
@@ -198,7 +169,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
             if (dbg & 2) {  // diagnostic: no MMAs
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+                mbar_arrive(&empty[s]);
                 continue;
             }
 #pragma unroll
@@ -212,7 +183,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             }
             mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        if (dbg & 2) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(done)) : "memory");
+        if (dbg & 2) mbar_arrive(done);
         else mma_commit(done);
     }
     __syncwarp();

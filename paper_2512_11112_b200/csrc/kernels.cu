@@ -372,98 +372,112 @@ __global__ void __launch_bounds__(kThreads) k_pair_split(const uint32_t* __restr
 
 // MAC sigma (spdz.cpp:126-138) in closed form: record of rank j contributes
 // r_j * (m_j - alpha x_j), r_j = reduce(mix(coin + (j+1) gamma)).  Order-free, so
-// sigma = S_m - alpha * S_x with S_m = sum r_j m_j and S_x = sum r_j x_j (two
-// lazily folded accumulators, one alpha-multiply per CTA instead of per record).
-// Four records per thread per step from 128-bit loads issued before the math.
-// 96-bit accumulator: lo (u64) + count of 2^64 carries (2^64 == 25 mod p).  The
-// carry-counting add runs on the ALU pipe, keeping the fma-heavy pipe for the
-// 64-bit multiplies of splitmix64 and the two products.
-struct Acc96 {
-    unsigned long long lo = 0;
-    uint32_t hi = 0;
-    __device__ __forceinline__ void add(unsigned long long v) {
-        lo += v;
-        hi += (lo < v) ? 1u : 0u;
-    }
-    __device__ __forceinline__ uint32_t mod() const {
-        return fp_reduce64((unsigned long long)fp_reduce64(lo) + (unsigned long long)hi * 25ull);
-    }
-};
-
-__device__ __forceinline__ void sigma_rec(uint64_t z, uint32_t x, uint32_t m, Acc96& sm, Acc96& sx) {
-    const uint32_t r = fp_reduce64(mix64(z));
+// sigma = S_m - alpha * S_x with S_m = sum r_j m_j and S_x = sum r_j x_j (one
+// alpha-multiply per thread instead of per record).
+//
+// The kernel is issue-bound on the fma-heavy pipe (every IMAD variant runs there;
+// ncu r01c: fmaheavy 76%, alu 63%, dram 59%), so the per-record arithmetic is
+// written on 32-bit halves to keep the IMAD count at the floor (two 64x64-bit
+// multiplies by constants = 2 IMAD.WIDE + 4 IMAD, two r*m products = 2 IMAD.WIDE)
+// and every add, carry and shift on the ALU pipe:
+//  * r' = any representative of mix mod p below 2^32 (not the canonical one):
+//    s = lo + 5 hi (< 6 2^32, 2^32 == 5) by shift/add-with-carry, then
+//    t = s_lo + 5 s_hi, plus 5 on the (rare) carry out of 32 bits;
+//  * S_m, S_x are exact 96-bit sums (add.cc chains); reduced once per thread
+//    (2^64 == 25, 2^32 == 5 mod p).
+__device__ __forceinline__ void z_step(uint32_t& zl, uint32_t& zh) {  // z += gamma
+    asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(zl), "+r"(zh));
+}
+__device__ __forceinline__ void sigma_rec(uint32_t zl, uint32_t zh, uint32_t x, uint32_t m, Acc96& sm, Acc96& sx,
+                                          const SigConsts& kc) {
+    const uint32_t r = mac_coeff_rep(zl, zh, kc);
     sm.add(mul_wide(r, m));
     sx.add(mul_wide(r, x));
 }
+// four consecutive records starting at state z
+__device__ __forceinline__ void sigma_rec4(uint64_t z, const uint4& x, const uint4& m, Acc96& sm, Acc96& sx,
+                                           const SigConsts& kc) {
+    uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
+    sigma_rec(zl, zh, x.x, m.x, sm, sx, kc);
+    z_step(zl, zh);
+    sigma_rec(zl, zh, x.y, m.y, sm, sx, kc);
+    z_step(zl, zh);
+    sigma_rec(zl, zh, x.z, m.z, sm, sx, kc);
+    z_step(zl, zh);
+    sigma_rec(zl, zh, x.w, m.w, sm, sx, kc);
+}
+__device__ __forceinline__ uint4 sub4(const uint4& a, const uint4& b) {
+    return make_uint4(fp_sub(a.x, b.x), fp_sub(a.y, b.y), fp_sub(a.z, b.z), fp_sub(a.w, b.w));
+}
 
 // Segment table passed by value (no host->device copy, no host sync before the
-// launch): chunk c of the flattened record space belongs to segment i with
-// first[i] <= c < first[i+1]; chunks are kSigmaChunk records.
-__global__ void __launch_bounds__(kThreads) k_mac_sigma(MacTable tab, uint64_t coin, uint32_t alpha,
-                                                        unsigned long long* acc) {
+// launch).  The concatenated record space [0, rec0[n]) is split into one
+// contiguous range per CTA (boundaries at multiples of kSigmaAlign records), so
+// every CTA does the same work (no tail wave) and walks at most a few segment
+// pieces.
+//
+// Compute-bound, not memory-bound (ncu r01d: the same kernel on L2-resident
+// records runs no faster than on HBM; a TMA-staged variant was slower), so the
+// block count is the occupancy limit (one wave) and loads are plain 128-bit.
+#ifndef SPDZ_SIGMA_MINB
+#define SPDZ_SIGMA_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, SPDZ_SIGMA_MINB) k_mac_sigma(MacTable tab, uint64_t coin, uint32_t alpha,
+                                                                         SigConsts kc, unsigned long long* acc) {
     Acc96 sm, sx;
-    const uint64_t n_chunks = tab.first[tab.n];
+    const uint64_t total = tab.rec0[tab.n];
+    const uint64_t units = (total + kSigmaAlign - 1) / kSigmaAlign;
+    const uint64_t lo_u = units * blockIdx.x / gridDim.x, hi_u = units * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t lo = lo_u * kSigmaAlign, hi = hi_u * kSigmaAlign < total ? hi_u * kSigmaAlign : total;
     uint32_t seg = 0;
-    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        while (c >= tab.first[seg + 1]) ++seg;  // chunks visited in increasing order
+    while (seg < tab.n && tab.rec0[seg + 1] <= lo) ++seg;
+    for (uint64_t pos = lo; pos < hi && seg < tab.n; ++seg) {
         const MacSegDev sg = tab.seg[seg];
-        const uint64_t start = (c - tab.first[seg]) * kSigmaChunk;
-        const uint32_t count = (uint32_t)((sg.len - start) < kSigmaChunk ? (sg.len - start) : kSigmaChunk);
+        const uint64_t s0 = tab.rec0[seg], s1 = tab.rec0[seg + 1] < hi ? tab.rec0[seg + 1] : hi;
+        if (s1 <= pos) continue;
+        const uint64_t start = pos - s0;
+        const uint32_t count = (uint32_t)(s1 - pos);  // < 2^31 (launcher)
+        pos = s1;
         const uint32_t* xv = sg.value + start;
         const uint32_t* ma = sg.mac_a + start;
         const uint32_t* mb = sg.mac_b ? sg.mac_b + start : nullptr;
-        const uint64_t z0 = coin + (sg.j0 + start + 1) * kGamma;  // z of record 0 of the chunk
+        const uint64_t z0 = coin + (sg.j0 + start + 1) * kGamma;  // z of record 0 of the piece
         const bool v4 = ((reinterpret_cast<uintptr_t>(xv) | reinterpret_cast<uintptr_t>(ma) |
                           reinterpret_cast<uintptr_t>(mb)) & 15u) == 0;
         uint32_t done = 0;
         if (v4) {
+            const uint4* x4 = reinterpret_cast<const uint4*>(xv);
+            const uint4* a4 = reinterpret_cast<const uint4*>(ma);
+            const uint4* b4 = reinterpret_cast<const uint4*>(mb);
             const uint32_t n4 = count / 4;
             uint32_t g = threadIdx.x;
             for (; g + blockDim.x < n4; g += 2 * blockDim.x) {  // 8 records in flight per thread
                 const uint32_t g2 = g + blockDim.x;
-                const uint4 x1 = __ldcs(reinterpret_cast<const uint4*>(xv) + g);
-                const uint4 x2 = __ldcs(reinterpret_cast<const uint4*>(xv) + g2);
-                uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ma) + g);
-                uint4 m2 = __ldcs(reinterpret_cast<const uint4*>(ma) + g2);
+                const uint4 x1 = __ldcs(x4 + g), x2 = __ldcs(x4 + g2);
+                uint4 m1 = __ldcs(a4 + g), m2 = __ldcs(a4 + g2);
                 if (mb) {
-                    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(mb) + g);
-                    const uint4 b2 = __ldcs(reinterpret_cast<const uint4*>(mb) + g2);
-                    m1 = make_uint4(fp_sub(m1.x, b1.x), fp_sub(m1.y, b1.y), fp_sub(m1.z, b1.z), fp_sub(m1.w, b1.w));
-                    m2 = make_uint4(fp_sub(m2.x, b2.x), fp_sub(m2.y, b2.y), fp_sub(m2.z, b2.z), fp_sub(m2.w, b2.w));
+                    m1 = sub4(m1, __ldcs(b4 + g));
+                    m2 = sub4(m2, __ldcs(b4 + g2));
                 }
-                uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
-                sigma_rec(z, x1.x, m1.x, sm, sx);
-                sigma_rec(z + kGamma, x1.y, m1.y, sm, sx);
-                sigma_rec(z + 2 * kGamma, x1.z, m1.z, sm, sx);
-                sigma_rec(z + 3 * kGamma, x1.w, m1.w, sm, sx);
-                z = z0 + (uint64_t)(4 * g2) * kGamma;
-                sigma_rec(z, x2.x, m2.x, sm, sx);
-                sigma_rec(z + kGamma, x2.y, m2.y, sm, sx);
-                sigma_rec(z + 2 * kGamma, x2.z, m2.z, sm, sx);
-                sigma_rec(z + 3 * kGamma, x2.w, m2.w, sm, sx);
+                sigma_rec4(z0 + (uint64_t)(4 * g) * kGamma, x1, m1, sm, sx, kc);
+                sigma_rec4(z0 + (uint64_t)(4 * g2) * kGamma, x2, m2, sm, sx, kc);
             }
             for (; g < n4; g += blockDim.x) {
-                const uint4 x = __ldcs(reinterpret_cast<const uint4*>(xv) + g);
-                uint4 m = __ldcs(reinterpret_cast<const uint4*>(ma) + g);
-                if (mb) {
-                    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(mb) + g);
-                    m = make_uint4(fp_sub(m.x, b.x), fp_sub(m.y, b.y), fp_sub(m.z, b.z), fp_sub(m.w, b.w));
-                }
-                const uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
-                sigma_rec(z, x.x, m.x, sm, sx);
-                sigma_rec(z + kGamma, x.y, m.y, sm, sx);
-                sigma_rec(z + 2 * kGamma, x.z, m.z, sm, sx);
-                sigma_rec(z + 3 * kGamma, x.w, m.w, sm, sx);
+                const uint4 x = __ldcs(x4 + g);
+                uint4 m = __ldcs(a4 + g);
+                if (mb) m = sub4(m, __ldcs(b4 + g));
+                sigma_rec4(z0 + (uint64_t)(4 * g) * kGamma, x, m, sm, sx, kc);
             }
             done = n4 * 4;
         }
         for (uint32_t i = done + threadIdx.x; i < count; i += blockDim.x) {
             uint32_t m = __ldcs(ma + i);
             if (mb) m = fp_sub(m, __ldcs(mb + i));
-            sigma_rec(z0 + (uint64_t)i * kGamma, __ldcs(xv + i), m, sm, sx);
+            const uint64_t z = z0 + (uint64_t)i * kGamma;
+            sigma_rec((uint32_t)z, (uint32_t)(z >> 32), __ldcs(xv + i), m, sm, sx, kc);
         }
     }
-    // sigma partial of this thread: S_m - alpha * S_x (mod p); carries < 2^32 per thread
+    // sigma partial of this thread: S_m - alpha * S_x (mod p)
     unsigned long long s[1] = {fp_sub(sm.mod(), fp_mul(alpha, sx.mod()))};
     block_sum<1>(s);
     if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
@@ -884,10 +898,18 @@ cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t
 
 cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
                              unsigned long long* acc, int sms) {
-    const uint64_t n_chunks = tab.first[tab.n];
-    if (n_chunks == 0) return cudaSuccess;
-    const int grid = (int)(n_chunks < (uint64_t)(sms * 8) ? n_chunks : (uint64_t)(sms * 8));
-    k_mac_sigma<<<grid, kThreads, 0, s>>>(tab, coin, alpha, acc);
+    const uint64_t units = (tab.rec0[tab.n] + kSigmaAlign - 1) / kSigmaAlign;
+    if (units == 0) return cudaSuccess;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mac_sigma, kThreads, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+    }
+    const uint64_t cap = (uint64_t)sms * per_sm;
+    const int grid = (int)(units < cap ? units : cap);
+    if ((units / grid + 1) * kSigmaAlign >= (1ull << 31)) return cudaErrorInvalidValue;  // per-CTA range < 2^31
+    k_mac_sigma<<<grid, kThreads, 0, s>>>(tab, coin, alpha, SigConsts{}, acc);
     return launched();
 }
 

@@ -15,12 +15,12 @@ struct MacSegDev {            // device-side MAC segment descriptor
     uint64_t len;
     uint64_t j0;
 };
-constexpr uint32_t kSigmaChunk = 1u << 14;  // records per work item of the sigma kernel
+constexpr uint32_t kSigmaAlign = 1024;     // CTA record ranges start at multiples of this
 constexpr int kMacTableSegs = 48;          // segments per launch (kernel parameter table)
 struct MacTable {
     uint32_t n;                            // segments in this table
     MacSegDev seg[kMacTableSegs];
-    uint64_t first[kMacTableSegs + 1];     // first chunk of each segment (prefix sums), first[n] = total
+    uint64_t rec0[kMacTableSegs + 1];      // first record of each segment (prefix sums), rec0[n] = total
 };
 
 struct LaunchInfo {

@@ -212,7 +212,7 @@ def test_mac_sigma_segments_large_vs_oracle(gpu):
     from paper_2512_11112_b200 import _lib
     from paper_2512_11112_b200._lib import check, lib
     c = ctx(0, 2, 31337)
-    sizes = [(5, 70001), (2, 3), (9, 1 << 18)]
+    sizes = [(5, 70001), (2, 3), (9, 1 << 18), (7, 100003)]  # (7): second half misaligned -> direct loads
     dev, segs_np = [], []
     segs = (_lib.MacSegment * (2 * len(sizes)))()
     k = 0
@@ -413,3 +413,32 @@ def test_host_backend_mirror_protocol_tests_280(gpu, golden):
                            ShareVec(Tt[4, 0][:10], Tt[5, 0][:10]))
     with pytest.raises(errors.TripleShortage):
         be.mul_mask(X0, Y0, t_short)
+
+
+def test_mac_coefficient_representatives_edge_cases(gpu):
+    """k_mac_sigma multiplies by a non-canonical representative r' < 2^32 of
+    mix64(z) mod p (field.cuh rep_mod_p); check it on the carry edge cases
+    (values whose lo + 5 hi wraps 2^32) and on random states."""
+    import torch
+    from paper_2512_11112_b200._lib import check, lib
+    M64 = (1 << 64) - 1
+    edge = [0, 1, P - 1, P, P + 1, (1 << 32) - 1, 1 << 32, M64, M64 - 24, M64 - 25, M64 - 26,
+            ((1 << 32) - 1) << 32, (((1 << 32) - 1) << 32) | 5, (0xCCCCCCCC << 32) | 0xFFFFFFFF,
+            (0x33333333 << 32) | 0xFFFFFFFC, (0x33333334 << 32) | 0xFFFFFFFB, (5 << 32) | 0xFFFFFFE6]
+    # hi such that 5 hi mod 2^32 + lo is just past 2^32 (the second-fold carry)
+    for hi in (0x33333333, 0x66666666, 0x99999999, 0xCCCCCCCC, 0xFFFFFFFF):
+        for lo in range(0xFFFFFFE0, 1 << 32, 3):
+            edge.append((hi << 32) | lo)
+    rng = np.random.default_rng(5)
+    vals = edge + [int(v) for v in rng.integers(0, 1 << 63, 4096, dtype=np.int64)] + \
+        [int(v) | (1 << 63) for v in rng.integers(0, 1 << 63, 4096, dtype=np.int64)]
+    arr = np.array(vals, dtype=np.uint64)
+    din = torch.from_numpy(arr.view(np.int64)).cuda()
+    dout = torch.empty(2 * len(arr), dtype=torch.int32, device="cuda")
+    c = ctx()
+    check(lib().spdz_diag_rep_check(c.h, din.data_ptr(), len(arr), dout.data_ptr()))
+    got = dout.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    for v, (rep, coeff) in zip(vals, got):
+        assert int(rep) % P == v % P, hex(v)
+        mixed = O.splitmix64((v - 0x9E3779B97F4A7C15) % (1 << 64))[0]  # splitmix64(s) = mix64(s + gamma)
+        assert int(coeff) % P == mixed % P, hex(v)
