@@ -125,12 +125,10 @@ int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, double* total_in
  * splitmix64-finaliser(in[i]) mod p (the MAC-check coefficient arithmetic of k_mac_sigma);
  * device pointers, synchronous. */
 int spdz_diag_rep_check(spdz_ctx* ctx, const uint64_t* d_in, uint64_t n, uint32_t* d_out);
-/* Diagnostic switches of the tcgen05 GEMM (bit 0: skip TMA loads, bit 1: skip MMAs); results
- * are invalid while non-zero.  Attribution experiments only. */
+/* Diagnostic switches of the tcgen05 GEMM: bit 2 skips the GEMM kernel, bit 3 the operand
+ * re-layout (results invalid while either is set); bit 6 / bit 7 force the 32- / 64-column
+ * output tile (results valid).  Attribution experiments and tests only. */
 int spdz_diag_gemm_tc_flags(uint32_t flags);
-/* Per-CTA %globaltimer stamps of the last tcgen05 GEMM run with flag bit 4 (start, TMEM
- * allocated, MMAs done, end); returns the number of u64 words written. */
-uint32_t spdz_diag_gemm_tc_timestamps(unsigned long long* host, uint32_t cap);
 /* Number of kernels this library launched on any context since load (evidence counter). */
 uint64_t spdz_kernel_launches(void);
 

@@ -85,17 +85,10 @@ extern "C" int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, doubl
 
 namespace spdzb200 {
 void modgemm_tc_debug(uint32_t flags);
-uint32_t modgemm_tc_timestamps(unsigned long long* host, uint32_t cap);
 }
 
-// Per-CTA %globaltimer stamps (start, TMEM allocated, MMAs done, end) of the last
-// tcgen05 GEMM launched with diagnostic bit 4 set.  Returns the number of words.
-extern "C" uint32_t spdz_diag_gemm_tc_timestamps(unsigned long long* host, uint32_t cap) {
-    return spdzb200::modgemm_tc_timestamps(host, cap);
-}
-
-// Diagnostic switches of the tcgen05 GEMM (bit 0: skip TMA loads, bit 1: skip MMAs) — results are
-// garbage while set; used only to attribute time between the load and MMA halves of the pipeline.
+// Diagnostic switches of the tcgen05 GEMM (gemm_tc.cu g_tc_dbg): bit 2 skips the GEMM kernel,
+// bit 3 the re-layout kernels (results invalid while set); bits 6/7 force the 32/64-column tile.
 extern "C" int spdz_diag_gemm_tc_flags(uint32_t flags) {
     spdzb200::modgemm_tc_debug(flags);
     return 0;

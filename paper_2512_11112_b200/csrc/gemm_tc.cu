@@ -2,20 +2,28 @@
 // layer (runtime.cpp:303-334, batched): C = A * B mod p, p = 2^32 - 5.
 //
 // u32 operands are split into four u8 limbs, A = sum_i 2^(8i) A_i, B = sum_j 2^(8j) B_j,
-// so A*B = sum_s 2^(8s) P_s with P_s = sum_{i+j=s} A_i B_j (s = 0..6).  Each P_s is an
-// exact u8 x u8 -> s32 tensor-core product (tcgen05.mma kind::i8, K = 32 per
-// instruction).  The four B limb tiles are stacked as one N = 4*BN operand, so a K
-// step is 4 MMAs (one per A limb, M = 128, N = 128) into D_i = A_i [B_0|B_1|B_2|B_3]
-// in TMEM; the epilogue reads D_i (tcgen05.ld), forms P_s = sum_{i+j=s} D_i[:, j] and
-// recombines mod p:
+// so A*B = sum_s 2^(8s) P_s with P_s = sum_{i+j=s} A_i B_j (s = 0..6).  Each limb
+// product is an exact u8 x u8 -> s32 tensor-core product (tcgen05.mma kind::i8, K = 32
+// per instruction); the epilogue recombines mod p with
 //   2^0, 2^8, 2^16, 2^24, 2^32 = 5, 2^40 = 1280, 2^48 = 327680 (mod p).
 // Exactness: P_3 sums 4 limb products over K, 4 * 255^2 * K < 2^31 for K <= 8192.
+//
+// Main kernel (k_modgemm_tc): a 128 x 64 output tile keeps the seven P_s
+// accumulators side by side in TMEM (P_s at columns [64 s, 64 s + 64), 448 of the 512
+// columns).  The four B limb tiles are stacked as one N = 256 operand [B_0|B_1|B_2|B_3],
+// so one MMA with A_i and destination column 64 i adds A_i B_j into P_{i+j} for all j:
+// four N = 256 MMAs per 32-deep K step cover all 16 limb products (the first K step
+// initialises the overlapping ranges with an N = 192 / 256 / 64 sequence).  N = 256 per
+// instruction keeps the shared-memory operand traffic at 96 B/clk; the 128 x 64 tile
+// needs 48 B/clk of L2->SMEM fill at the MMA rate.
 //
 // Operands are re-laid out once per call (k_tile_rows / k_tile_cols) as u8 limb
 // tiles already in the canonical no-swizzle K-major UMMA image (8-row x 16-byte
 // core matrices), so each K stage is two 1-D TMA bulk copies (cp.async.bulk +
-// mbarrier complete_tx) into a 4-stage ring; warp 0 produces, one thread of
-// warp 1 issues the MMAs, tcgen05.commit frees a stage, all warps run the epilogue.
+// mbarrier complete_tx) into a 4-stage ring.  The kernel is persistent (one CTA per
+// SM, tiles N-fastest so the B image stays L2-resident): warp 0 produces, one thread
+// of warp 1 issues the MMAs, warps 2-5 drain TMEM (tcgen05.ld) and store; the
+// producer keeps prefetching the next tile while the epilogue runs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,7 +39,6 @@ namespace {
 
 constexpr int TM = 128;   // rows per CTA tile (UMMA M)
 constexpr int TK = 64;    // K bytes (= elements) per stage
-constexpr int kThreadsTc = 128;
 
 // SMEM matrix descriptor, K-major, SWIZZLE_NONE (layout type 0), sm100 version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -45,7 +52,7 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 
 // Instruction descriptor: kind::i8, D = s32, A = B = u8, both K-major, M = 128, N = BN.
 template <int BN>
-__device__ __forceinline__ uint32_t idesc_i8() {
+__host__ __device__ constexpr uint32_t idesc_i8() {
     return (2u << 4)                      // c_format = S32
            | (0u << 7) | (0u << 10)       // a/b format = unsigned 8 bit
            | ((uint32_t)(BN >> 3) << 17)  // N >> 3
@@ -79,19 +86,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // tile by tile, so one K stage is two contiguous 1-D TMA bulk copies.
 constexpr uint32_t kLBO = 128;                 // next 16-byte K chunk
 constexpr uint32_t kSBO = (TK / 16) * 128;     // next 8-row group
-constexpr int kStages = 4;
-
-template <int BN>
-struct TcSmem {
-    static constexpr uint32_t A_LIMB = TM * TK;              // 8 KB
-    static constexpr uint32_t B_LIMB = BN * TK;
-    static constexpr uint32_t A_STAGE = 4 * A_LIMB;
-    static constexpr uint32_t B_STAGE = 4 * B_LIMB;
-    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
-    static constexpr uint32_t BYTES = kStages * STAGE + 2048; // + barriers / tmem slot + alignment
-    static constexpr uint32_t TMEM_COLS = (16 * BN <= 256) ? 256 : 512;  // D_i: 4 x (4 BN) columns
-    static_assert(16 * BN <= 512, "4 A limbs x (4 B limbs x BN) s32 columns must fit TMEM");
-};
 
 __device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
     return (r >> 3) * kSBO + (k >> 4) * kLBO + (r & 7) * 16 + (k & 15);
@@ -105,31 +99,53 @@ struct TcOut {
     uint32_t* y1;
 };
 
-// Warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer, all 4 warps = epilogue.
-// A tiles: [Mp/128][KB] blocks of A_STAGE bytes; B tiles: [Np/BN][KB] blocks of B_STAGE bytes.
-template <int BN>
-__global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At, const uint8_t* __restrict__ Bt,
-                                                               uint32_t M, uint32_t N, uint32_t KB, TcOut out,
-                                                               uint32_t dbg, unsigned long long* tstamp) {
-    unsigned long long t_start = 0;
-    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    using L = TcSmem<BN>;
+// ---------------------------------------------------------------------------
+// 128 x TN tiles, P_s accumulators, N = 4 TN MMAs, persistent, warp-specialised.
+// ---------------------------------------------------------------------------
+// TN = 64 for large problems (N = 256 MMAs); TN = 32 (N = 128 MMAs, twice the tiles)
+// when the TN = 64 tiling would leave SMs idle.
+constexpr int kStages = 4;
+constexpr int kThreadsTc = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+template <int TN>
+struct TcSmem {
+    static constexpr uint32_t A_LIMB = TM * TK;        // 8 KB
+    static constexpr uint32_t B_LIMB = TN * TK;        // 4 KB at TN = 64
+    static constexpr uint32_t A_STAGE = 4 * A_LIMB;    // 32 KB
+    static constexpr uint32_t B_STAGE = 4 * B_LIMB;    // 16 KB at TN = 64
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    static constexpr uint32_t BYTES = kStages * STAGE + 1024 + 256;
+    static constexpr uint32_t TMEM_COLS = 7 * TN <= 256 ? 256 : 512;
+};
+
+template <int TN>
+__device__ __forceinline__ void tmem_ld16_x7(uint32_t taddr, uint32_t (&v)[7][16]) {
+#pragma unroll
+    for (int t = 0; t < 7; ++t) tmem_ld16(taddr + t * TN, v[t]);
+}
+
+template <int TN>
+__global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At,
+                                                               const uint8_t* __restrict__ Bt, uint32_t M, uint32_t N,
+                                                               uint32_t KB, uint32_t tiles_n, uint32_t n_tiles,
+                                                               TcOut out) {
+    using L = TcSmem<TN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
     uint8_t* sgen = smem + (sbase - smem_u32(smem));
     uint64_t* full = reinterpret_cast<uint64_t*>(sgen + kStages * L::STAGE);
     uint64_t* empty = full + kStages;
-    uint64_t* done = empty + kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + kStages;  // MMAs of a tile done (tcgen05.commit)
+    uint64_t* tempty = tfull + 1;        // epilogue drained TMEM (4 warp arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t m0 = blockIdx.y * TM, n0 = blockIdx.x * BN;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 4);
         mbar_fence_init();
     }
     if (warp == 0) {
@@ -141,95 +157,120 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
-    unsigned long long t_alloc = 0;
-    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_alloc));
 
-    if (warp == 0 && lane == 0) {  // ---- TMA producer ----
-        const uint8_t* a_src = At + (uint64_t)blockIdx.y * KB * L::A_STAGE;
-        const uint8_t* b_src = Bt + (uint64_t)blockIdx.x * KB * L::B_STAGE;
-        for (uint32_t kb = 0; kb < KB; ++kb) {
-            const uint32_t s = kb % kStages;
-            if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-            const uint32_t dst = sbase + s * L::STAGE;
-            if (dbg & 1) {  // diagnostic: no loads
-                mbar_arrive(&full[s]);
-                continue;
-            }
-            mbar_expect_tx(&full[s], L::STAGE);
-            bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
-            bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
-        }
-    } else if (warp == 1 && lane == 0) {  // ---- MMA issuer ----
-        // The 4 B limb tiles are stacked rows of one (4 BN) x TK K-major operand, so
-        // one MMA per A limb i computes D_i[:, j BN + n] = (A_i B_j)(m, n) for all j.
-        const uint32_t idesc = idesc_i8<4 * BN>();
-        for (uint32_t kb = 0; kb < KB; ++kb) {
-            const uint32_t s = kb % kStages;
-            mbar_wait(&full[s], (kb / kStages) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
-            if (dbg & 2) {  // diagnostic: no MMAs
-                mbar_arrive(&empty[s]);
-                continue;
-            }
-#pragma unroll
-            for (int ks = 0; ks < TK / 32; ++ks) {
-                const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint64_t ad = smem_desc(sa + i * L::A_LIMB + ks * 2 * kLBO, kLBO, kSBO);
-                    mma_i8(tmem + i * 4 * BN, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer ----
+            uint32_t g = 0;
+            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const uint32_t mt = tile / tiles_n, nt = tile % tiles_n;
+                const uint8_t* a_src = At + (uint64_t)mt * KB * L::A_STAGE;
+                const uint8_t* b_src = Bt + (uint64_t)nt * KB * L::B_STAGE;
+                for (uint32_t kb = 0; kb < KB; ++kb, ++g) {
+                    const uint32_t s = g % kStages;
+                    if (g >= (uint32_t)kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
+                    const uint32_t dst = sbase + s * L::STAGE;
+                    mbar_expect_tx(&full[s], L::STAGE);
+                    bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
+                    bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
                 }
             }
-            mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        if (dbg & 2) mbar_arrive(done);
-        else mma_commit(done);
-    }
-    __syncwarp();
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    unsigned long long t_done = 0;
-    if (tstamp && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_done));
-
-    // epilogue: TMEM lane = row (warp w owns lanes 32w..32w+31), column = n
-    const uint32_t row = m0 + warp * 32 + lane;
-    const uint32_t lane_base = tmem + ((warp * 32u) << 16);
-    constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer ----
+            constexpr uint32_t id4 = idesc_i8<4 * TN>(), id3 = idesc_i8<3 * TN>(), id1 = idesc_i8<TN>();
+            uint32_t g = 0, it = 0;
+            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+                if (it > 0) mbar_wait(tempty, (it - 1) & 1);  // epilogue of the previous tile drained TMEM
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                for (uint32_t kb = 0; kb < KB; ++kb, ++g) {
+                    const uint32_t s = g % kStages;
+                    mbar_wait(&full[s], (g / kStages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
+#pragma unroll
+                    for (int ks = 0; ks < TK / 32; ++ks) {
+                        const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
+                        uint64_t ad[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) ad[i] = smem_desc(sa + i * L::A_LIMB + ks * 2 * kLBO, kLBO, kSBO);
+                        if (kb == 0 && ks == 0) {  // initialise P_0..P_6 (overlapping destination ranges)
+                            const uint64_t bd3 = smem_desc(sb + 3 * L::B_LIMB + ks * 2 * kLBO, kLBO, kSBO);
+                            mma_i8(tmem, ad[0], bd, id3, 0u);             // P0..P2  = A0 [B0|B1|B2]
+                            mma_i8(tmem + 3 * TN, ad[3], bd, id4, 0u);    // P3..P6  = A3 [B0..B3]
+                            mma_i8(tmem + 3 * TN, ad[0], bd3, id1, 1u);   // P3     += A0 B3
+                            mma_i8(tmem + 1 * TN, ad[1], bd, id4, 1u);    // P1..P4 += A1 [B0..B3]
+                            mma_i8(tmem + 2 * TN, ad[2], bd, id4, 1u);    // P2..P5 += A2 [B0..B3]
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) mma_i8(tmem + i * TN, ad[i], bd, id4, 1u);
+                        }
+                    }
+                    mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                }
+                mma_commit(tfull);  // accumulators of this tile complete
+            }
+        }
+    } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
+        const uint32_t quarter = warp & 3;
+        const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
+        constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
+        uint32_t it = 0;
+        for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+            const uint32_t mt = tile / tiles_n, nt = tile % tiles_n;
+            const uint32_t row = mt * TM + quarter * 32 + lane;
+            mbar_wait(tfull, it & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 16; ++cc) {
-        // P_s = sum_{i+j=s} D_i[:, j BN + col]; each D_ij < 255^2 K <= 2^29, so P_s < 2^31
-        uint32_t v[7][16];
+            for (int cc = 0; cc < TN / 16; ++cc) {
+                uint32_t v[7][16];
+                tmem_ld16_x7<TN>(lane_base + cc * 16, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (cc == TN / 16 - 1) {  // every column of this tile is in registers: release TMEM
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty);
+                }
+                const uint32_t col0 = nt * TN + cc * 16;
+                if (row >= M) continue;
+                uint32_t r[16];
 #pragma unroll
-        for (int t = 0; t < 7; ++t)
+                for (int t = 0; t < 16; ++t) {
+                    unsigned long long acc = 0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[t][q] = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            uint32_t d[4][16];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) tmem_ld16(lane_base + (i * 4 + j) * BN + cc * 16, d[j]);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int q = 0; q < 16; ++q) v[i + j][q] += d[j][q];
-        }
-        if (row < M) {
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const uint32_t col = n0 + cc * 16 + t;
-                if (col >= N) continue;
-                unsigned long long acc = 0;
-#pragma unroll
-                for (int q = 0; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
-                const uint32_t r = fp_reduce64(acc);
+                    for (int q = 0; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
+                    r[t] = fp_reduce64(acc);
+                }
+                // output plane + position of columns col0 .. col0+15
+                uint32_t* dst;
+                uint32_t lim;  // valid columns in this group
                 if (out.mode == 0) {
-                    if (col < out.batch) out.y0[(uint64_t)row * out.batch + col] = r;
-                    else out.y1[(uint64_t)row * out.batch + (col - out.batch)] = r;
+                    const bool hi = col0 >= out.batch;
+                    dst = hi ? out.y1 + (uint64_t)row * out.batch + (col0 - out.batch)
+                             : out.y0 + (uint64_t)row * out.batch + col0;
+                    lim = hi ? (col0 < N ? N - col0 : 0) : out.batch - col0;
                 } else {
-                    if (row < out.dout) out.y0[(uint64_t)row * out.batch + col] = r;
-                    else out.y1[(uint64_t)(row - out.dout) * out.batch + col] = r;
+                    const bool hi = row >= out.dout;
+                    dst = hi ? out.y1 + (uint64_t)(row - out.dout) * out.batch + col0
+                             : out.y0 + (uint64_t)row * out.batch + col0;
+                    lim = col0 < N ? N - col0 : 0;
+                }
+                if (lim >= 16 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        reinterpret_cast<uint4*>(dst)[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+                } else {
+                    // group straddles the plane boundary (mode 0, batch % 16 != 0) or the edge
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) {
+                        const uint32_t col = col0 + t;
+                        if (col >= N) break;
+                        if (out.mode == 0) {
+                            if (col < out.batch) out.y0[(uint64_t)row * out.batch + col] = r[t];
+                            else out.y1[(uint64_t)row * out.batch + (col - out.batch)] = r[t];
+                        } else {
+                            dst[t] = r[t];
+                        }
+                    }
                 }
             }
         }
@@ -238,54 +279,49 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
-    if (tstamp && threadIdx.x == 0) {
-        unsigned long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
-        tstamp[4 * cta + 0] = t_start;
-        tstamp[4 * cta + 1] = t_alloc;
-        tstamp[4 * cta + 2] = t_done;
-        tstamp[4 * cta + 3] = t_end;
-    }
 }
 
-// A (rows, stacked a0 over a1) -> pre-tiled limb image: one thread per (row, 16-k chunk),
-// 128-bit loads when the rows are 16-byte aligned (K % 4 == 0).
+// A (rows, stacked a0 over a1) -> pre-tiled limb image, one thread per 16-byte piece
+// of the (128-row x 64-k) block: piece q = (r / 8) * 32 + (k / 16) * 8 + r % 8 sits at
+// byte 16 q of each limb image (= core_off), so a warp's four limb stores are 4 x 512
+// contiguous bytes; its loads are 64-byte row segments.
 // A(m, k) = a0[m*K + k] for m < M0, a1[(m-M0)*K + k] for M0 <= m < M; zero padded.
 __global__ void __launch_bounds__(256) k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1,
                                                    uint32_t M0, uint32_t M, uint32_t K, uint32_t Mp, uint32_t KB,
                                                    uint8_t* __restrict__ out) {
-    const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+    constexpr uint32_t kPieces = TM * TK / 16;  // 512 per block
+    const uint64_t pieces = (uint64_t)(Mp / TM) * KB * kPieces;
     const bool v4 = (K % 4) == 0 && ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 15u) == 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < chunks; t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t kc_all = (uint32_t)(t % ((uint64_t)KB * (TK / 16)));
-        const uint32_t m = (uint32_t)(t / ((uint64_t)KB * (TK / 16)));
-        const uint32_t k0 = kc_all * 16;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < pieces; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t blk = t / kPieces;
+        const uint32_t q = (uint32_t)(t % kPieces);
+        const uint32_t r = (q / 32) * 8 + (q % 8), kk = ((q / 8) % 4) * 16;
+        const uint32_t mt = (uint32_t)(blk / KB), kb = (uint32_t)(blk % KB);
+        const uint32_t m = mt * TM + r, k0 = kb * TK + kk;
         uint32_t w[16];
         const uint32_t* row = m < M0 ? a0 + (uint64_t)m * K : a1 + (uint64_t)(m - M0) * K;
         if (v4 && m < M && k0 + 16 <= K) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + k0) + q);
-                w[4 * q] = u.x;
-                w[4 * q + 1] = u.y;
-                w[4 * q + 2] = u.z;
-                w[4 * q + 3] = u.w;
+            for (int c = 0; c < 4; ++c) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + k0) + c);
+                w[4 * c] = u.x;
+                w[4 * c + 1] = u.y;
+                w[4 * c + 2] = u.z;
+                w[4 * c + 3] = u.w;
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) w[q] = (m < M && k0 + q < K) ? row[k0 + q] : 0u;
+            for (int c = 0; c < 16; ++c) w[c] = (m < M && k0 + c < K) ? row[k0 + c] : 0u;
         }
-        const uint32_t mt = m / TM, r = m % TM, kb = k0 / TK, kk = k0 % TK;
-        uint8_t* blk = out + ((uint64_t)mt * KB + kb) * (4u * TM * TK);
+        uint8_t* dst = out + blk * (4u * TM * TK) + 16u * q;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             uint32_t p[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                p[q] = __byte_perm(__byte_perm(w[4 * q] >> (8 * i), w[4 * q + 1] >> (8 * i), 0x0040),
-                                   __byte_perm(w[4 * q + 2] >> (8 * i), w[4 * q + 3] >> (8 * i), 0x0040), 0x5410);
-            *reinterpret_cast<uint4*>(blk + i * (TM * TK) + core_off(r, kk)) = make_uint4(p[0], p[1], p[2], p[3]);
+            for (int c = 0; c < 4; ++c)
+                p[c] = __byte_perm(__byte_perm(w[4 * c] >> (8 * i), w[4 * c + 1] >> (8 * i), 0x0040),
+                                   __byte_perm(w[4 * c + 2] >> (8 * i), w[4 * c + 3] >> (8 * i), 0x0040), 0x5410);
+            *reinterpret_cast<uint4*>(dst + i * (TM * TK)) = make_uint4(p[0], p[1], p[2], p[3]);
         }
     }
 }
@@ -324,15 +360,17 @@ __global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __r
     }
 }
 
+// Diagnostic switches (attribution experiments, scripts/gemm_probe.py): bit 2 skips the GEMM
+// kernel, bit 3 the re-layout kernels (results invalid while set); bit 6 / bit 7 force the
+// 32- / 64-column tile width (results valid).
 uint32_t g_tc_dbg = 0;
-unsigned long long* g_tc_tstamp = nullptr;  // diagnostic per-CTA timestamps (bit 4)
-uint32_t g_tc_ctas = 0;
 
+// Re-layout both operands into limb images (B tiles BN columns wide), then run
+// the GEMM kernel with TN = BN.
 template <int BN>
 cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
                    const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint8_t* scratch, const TcOut& out,
                    int sms) {
-    using L = TcSmem<BN>;
     const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
     const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
     const uint32_t KB = (din + TK - 1) / TK;
@@ -351,21 +389,17 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (g_tc_dbg & 4) return cudaSuccess;  // (diagnostic bit 2 skips the GEMM kernel)
+    using L = TcSmem<BN>;
+    static bool attr2 = false;
+    if (!attr2) {
         cudaError_t e = cudaFuncSetAttribute(k_modgemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr2 = true;
     }
-    if (g_tc_dbg & 4) return cudaSuccess;  // (diagnostic bit 2 skips the GEMM kernel)
-    dim3 grid(Np / BN, Mp / TM);
-    unsigned long long* ts = nullptr;
-    if (g_tc_dbg & 16) {
-        g_tc_ctas = grid.x * grid.y;
-        if (!g_tc_tstamp) cudaMalloc(&g_tc_tstamp, 4 * 8 * 65536);
-        if (g_tc_ctas <= 65536) ts = g_tc_tstamp;
-    }
-    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, out, g_tc_dbg, ts);
+    const uint32_t tiles_n = Np / BN, n_tiles = tiles_n * (Mp / TM);
+    const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)sms);
+    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, tiles_n, n_tiles, out);
     ++g_kernel_launches;
     return cudaGetLastError();
 }
@@ -373,14 +407,6 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
 }  // namespace
 
 void modgemm_tc_debug(uint32_t flags) { g_tc_dbg = flags; }
-uint32_t modgemm_tc_timestamps(unsigned long long* host, uint32_t cap) {
-    if (!g_tc_tstamp) return 0;
-    const uint32_t n = std::min(cap, 4 * g_tc_ctas);
-    cudaDeviceSynchronize();
-    cudaMemcpy(host, g_tc_tstamp, n * 8ull, cudaMemcpyDeviceToHost);
-    return n;
-}
-
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch) {
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
     const uint64_t Mp = (M + TM - 1) / TM * TM, Np = (N + 63) / 64 * 64, Kp = (din + TK - 1) / TK * TK;
@@ -398,9 +424,11 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
     if (dout == 0 || batch == 0) return cudaSuccess;
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
     TcOut out{mode, dout, batch, y0, y1};
-    (void)M;
-    (void)N;
-    return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
+    // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
+    const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
+    const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
+    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
+    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
 }
 
 }  // namespace spdzb200

@@ -22,6 +22,10 @@ ctx = Context(0, 0, 2, 1)
 W, xs = rnd(din * dout), DeviceShare(rnd(din * batch), rnd(din * batch))
 ys = DeviceShare.empty(dout * batch)
 args = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
+BASE = (64 if "--tn32" in sys.argv else 0) | (128 if "--tn64" in sys.argv else 0)
+lib().spdz_diag_gemm_tc_flags(BASE)  # 64/128: force the 32/64-column tile width
+
+
 def graphed(reps=10):
     """Device time per call from a CUDA graph of `reps` calls (host launch cost excluded)."""
     for _ in range(3):
@@ -56,23 +60,14 @@ def timed(reps=10):
     return e0.elapsed_time(e1) / reps * 1000
 
 
-if "--diag" in sys.argv:
+if "--diag" in sys.argv:  # time split: re-layout kernels vs the GEMM kernel (results garbage while set)
     check(lib().spdz_set_gemm_path(2))
-    for flags, name in ((0, "full"), (1, "no loads"), (2, "no MMAs"), (3, "neither"), (4, "tiling only"),
-                        (8, "gemm only"), (11, "gemm only, no loads, no MMAs")):
-        lib().spdz_diag_gemm_tc_flags(flags)
-        print(f"tcgen05 {name}: {timed():.1f} us per call", flush=True)
-    lib().spdz_diag_gemm_tc_flags(16)
-    timed(1)
-    buf = (C.c_uint64 * 262144)()
-    n = lib().spdz_diag_gemm_tc_timestamps(buf, 262144)
-    ts = np.array(buf[:n], dtype=np.float64).reshape(-1, 4)
-    t0 = ts[:, 0].min()
-    print("per-CTA us: alloc %.2f  mainloop %.2f  epilogue %.2f | first start %.2f last start %.2f last end %.2f" % (
-        np.mean(ts[:, 1] - ts[:, 0]) / 1e3, np.mean(ts[:, 2] - ts[:, 1]) / 1e3, np.mean(ts[:, 3] - ts[:, 2]) / 1e3,
-        0.0, (ts[:, 0].max() - t0) / 1e3, (ts[:, 3].max() - t0) / 1e3), flush=True)
-    lib().spdz_diag_gemm_tc_flags(0)
-for path in (2, 1):
+    base = BASE
+    for flags, name in ((0, "full"), (4, "re-layout only"), (8, "gemm kernel only")):
+        lib().spdz_diag_gemm_tc_flags(base | flags)
+        print(f"tcgen05 {name}: graphed {graphed():.1f} us per call", flush=True)
+    lib().spdz_diag_gemm_tc_flags(base)
+for path in ((2,) if "--tc-only" in sys.argv else (2, 1)):
     check(lib().spdz_set_gemm_path(path))
     try:
         print(f"path {path}: graphed {graphed():.1f} us per call (device)", flush=True)

@@ -442,3 +442,57 @@ def test_mac_coefficient_representatives_edge_cases(gpu):
         assert int(rep) % P == v % P, hex(v)
         mixed = O.splitmix64((v - 0x9E3779B97F4A7C15) % (1 << 64))[0]  # splitmix64(s) = mix64(s + gamma)
         assert int(coeff) % P == mixed % P, hex(v)
+
+
+def _np_modmatmul(A, B):
+    """Exact (A @ B) mod p for u32 matrices: A split into 16-bit halves so every int64
+    partial dot product stays below 2^63 for K <= 2^15."""
+    A = A.astype(np.int64)
+    B = B.astype(np.int64)
+    lo = (A & 0xFFFF) @ B % P
+    hi = (A >> 16) @ B % P
+    return ((hi * 65536 + lo) % P).astype(np.uint32)
+
+
+@pytest.mark.parametrize("tiles", [0, 64, 128])
+@pytest.mark.parametrize("din,dout,batch,fill", [(512, 2048, 300, "rand"), (8192, 256, 64, "max"),
+                                                 (300, 130, 70, "rand"), (64, 1200, 520, "rand")])
+def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
+    """Every output of the tcgen05 GEMM (both planes, both modes) against an exact
+    numpy mod-p matmul: persistent tiles (more tiles than SMs), edge tiles, and
+    all-(p-1) operands at K = 8192 (the s32 limb-accumulator bound); tile width
+    chosen automatically (0), forced to 32 (64) or to 64 columns (128)."""
+    import ctypes as C
+    from paper_2512_11112_b200 import DeviceShare
+    from paper_2512_11112_b200._lib import check, lib
+    from paper_2512_11112_b200.backend import dshare
+    if fill == "max":
+        W = np.full(din * dout, P - 1, np.uint32)
+        Xv = np.full(din * batch, P - 1, np.uint32)
+        Xm = np.full(din * batch, P - 2, np.uint32)
+    else:
+        W, Xv, Xm = O.rand_field_vec(din * dout, 11), O.rand_field_vec(din * batch, 12), O.rand_field_vec(din * batch, 13)
+    c = ctx()
+    check(lib().spdz_set_gemm_path(2))
+    lib().spdz_diag_gemm_tc_flags(tiles)
+    try:
+        y = DeviceShare.empty(dout * batch)
+        x = share(Xv, Xm)
+        Wd = T(W)
+        check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 1, Wd.data_ptr(), None, C.byref(dshare(x)),
+                                              None, C.byref(dshare(y))))
+        Wmat = W.reshape(dout, din)
+        np.testing.assert_array_equal(H(y.vals).reshape(dout, batch), _np_modmatmul(Wmat, Xv.reshape(din, batch)))
+        np.testing.assert_array_equal(H(y.macs).reshape(dout, batch), _np_modmatmul(Wmat, Xm.reshape(din, batch)))
+        # mode 1: W secret (two planes), x public
+        Wm = O.rand_field_vec(din * dout, 14) if fill == "rand" else np.full(din * dout, P - 3, np.uint32)
+        w = share(W, Wm)
+        Xd = T(Xv)
+        check(lib().spdz_linear_secret_public(c.h, din, dout, batch, 0, None, C.byref(dshare(w)), None,
+                                              Xd.data_ptr(), C.byref(dshare(y))))
+        np.testing.assert_array_equal(H(y.vals).reshape(dout, batch), _np_modmatmul(Wmat, Xv.reshape(din, batch)))
+        np.testing.assert_array_equal(H(y.macs).reshape(dout, batch),
+                                      _np_modmatmul(Wm.reshape(dout, din), Xv.reshape(din, batch)))
+    finally:
+        lib().spdz_diag_gemm_tc_flags(0)
+        check(lib().spdz_set_gemm_path(0))
