@@ -9,6 +9,8 @@ C2  light / mixed / heavy chains, 2^16, 2^20, 2^24
 C3  linear secret x public 1024x1024, batch 256 (modular GEMM, both planes)
 C4  linear secret x secret 4096x4096 (+ MAC check), slice 262140 (64 tiles) and 1 tile
     + the paper's 8192x8192 layer (slice 262140, 265 tiles)
+    + the batched variant: X 4096 x 4096 secret, one batched matrix triple,
+      2 parties, mask + open + tcgen05 combine + MAC sigma of the opened [D|E]
 """
 from __future__ import annotations
 
@@ -63,6 +65,66 @@ def ref_online(ir, inputs, threads, slice_=262140, reps=1):
         _, rep = ref.run_local(ir, 2, inputs, threads=threads, slice_=slice_, io_timeout_ms=600000)
         best = rep["online_ms"] if best is None else min(best, rep["online_ms"])
     return best
+
+
+def bmatrix_bench(din, dout, batch, reps=3):
+    """Batched secret x secret layer, 2 parties on this GPU: both parties' mask, fused
+    open + combine (two tcgen05 limb GEMMs each) and MAC sigma of the opened [D|E]."""
+    import ctypes as C
+    import torch
+    from paper_2512_11112_b200 import Context, DeviceBMTriple, DeviceShare, _lib
+    from paper_2512_11112_b200._lib import check, lib
+    g = torch.Generator(device="cuda").manual_seed(din + batch)
+    rd = lambda n: torch.randint(0, P, (n,), dtype=torch.int64, device="cuda", generator=g).to(torch.uint32)
+    sh = lambda n: DeviceShare(rd(n), rd(n))
+    ctxs, parts = [], []
+    for p in range(2):
+        c = Context(0, p, 2, 1000 + p)
+        c.use_torch_stream()
+        t = DeviceBMTriple(din, dout, batch, sh(dout * din), sh(din * batch), sh(dout * batch))
+        w, x = sh(dout * din), sh(din * batch)
+        pay = torch.empty(dout * din + din * batch, dtype=torch.uint32, device="cuda")
+        op = torch.empty_like(pay)
+        z = DeviceShare.empty(dout * batch)
+        ctxs.append(c)
+        parts.append((t, w, x, pay, op, z))
+
+    def step():
+        for p in range(2):
+            t, w, x, pay, _, _ = parts[p]
+            ctxs[p].bmatrix_mask(w, x, t, pay)
+        for p in range(2):
+            t, w, x, pay, op, z = parts[p]
+            ctxs[p].bmatrix_open_combine(t, pay, [parts[1 - p][3]], z, op)
+        for p in range(2):
+            t, w, x, pay, op, z = parts[p]
+            segs = (_lib.MacSegment * 2)()
+            cells = dout * din
+            for k, (val, ma, mb, n, b) in enumerate(((op.data_ptr(), w.macs.data_ptr(), t.a.macs.data_ptr(), cells, 0),
+                                                     (op[cells:].data_ptr(), x.macs.data_ptr(), t.b.macs.data_ptr(),
+                                                      din * batch, 1))):
+                segs[k].value, segs[k].mac_a, segs[k].mac_b, segs[k].len, segs[k].batch_id = val, ma, mb, n, b
+            check(lib().spdz_mac_assign_ranks(segs, 2))
+            out = C.c_uint32()
+            check(lib().spdz_mac_sigma(ctxs[p].h, segs, 2, 0xDEADBEEF12345678, C.byref(out)))
+
+    step()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    modmacs = 2 * 4 * dout * din * batch  # 2 parties x (D [B'v|B'm] + [Av;Am] E)
+    for c in ctxs:
+        c.close()
+    return {"shape": [dout, din, batch], "parties": 2, "ms": ms, "modmacs": modmacs,
+            "i8_mac_per_s": 16 * modmacs / (ms / 1e3), "frac_of_nominal_i8": 16 * modmacs / (ms / 1e3) / 2.25e15,
+            "timed": "both parties: mask, open+combine (tcgen05), MAC sigma of [D|E] (host-synchronous)"}
 
 
 def main():
@@ -213,6 +275,11 @@ def main():
         c4.append(gr)
         print("C4", din, sl, gr["online_device_ms"], gr.get("reference_online_ms"), flush=True)
     res["C4_linear_secret_secret"] = c4
+    bm = bmatrix_bench(4096, 4096, 1024 if args.quick else 4096)
+    if not args.no_ref and c4 and c4[0].get("reference_online_ms"):
+        bm["reference_batch1_online_ms"] = c4[0]["reference_online_ms"]
+    res["C4_batched_secret_secret"] = bm
+    print("C4 batched", bm, flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(out, indent=1))
     print(json.dumps(out)[:2000])

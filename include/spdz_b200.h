@@ -74,6 +74,15 @@ typedef struct spdz_mtriple {
     spdz_share_t a, b, c;
 } spdz_mtriple_t;
 
+/* Batched matrix triple: the batch-N generalisation of one tile's triple
+ * (spdz.hpp:35-43) for W (dout x din) times a secret X (din x batch): A dout x din,
+ * B din x batch, C = A B dout x batch, all row-major.  Column j of (B, C) with A is an
+ * ordinary matrix triple {A, B[:,j], C[:,j]}. */
+typedef struct spdz_bmtriple {
+    uint32_t din, dout, batch;
+    spdz_share_t a, b, c;
+} spdz_bmtriple_t;
+
 /* Backend capability record (backend.hpp:21-27). */
 typedef struct spdz_capability {
     char name[32];
@@ -208,6 +217,19 @@ int spdz_matrix_open_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint
 /* spdz.cpp:98-124 with already-opened D (rows*din) and E (din). */
 int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t* D, const uint32_t* E,
                         spdz_share_t* z);
+/* Batched secret x secret linear layer (linear.cpp:30-61 and spdz.cpp:98-124 for `batch`
+ * input columns sharing one W and one A):
+ *   mask:  payload = [D = W.v - A.v (dout*din) | E = X.v - B.v (din*batch)]
+ *   open + combine: opened [D|E] = own + sum reduce(peer) -> opened_out (the MAC-log
+ *   values; required), then per column j exactly spdz::matrix_combine({A, B[:,j], C[:,j]},
+ *   D, E[:,j]):  Z.v = C.v + D B.v + A.v E (+ D E on party 0),
+ *                Z.m = C.m + D B.m + A.m E + alpha_i D E,
+ *   as two tcgen05 limb GEMMs: D [B.v + [p0] E | B.m + alpha_i E] and [A.v ; A.m] E.
+ *   Needs din <= 8192 (the s32 limb-accumulator bound). */
+int spdz_bmatrix_mask(spdz_ctx* ctx, const spdz_share_t* w, const spdz_share_t* x, const spdz_bmtriple_t* t,
+                      uint32_t* payload);
+int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uint32_t* own_payload,
+                              const uint32_t* const* peer_payload, int n_peers, spdz_share_t* z, uint32_t* opened_out);
 /* runtime.cpp:303-334, batched: Y[dout x batch] = W[dout x din] * X[din x batch]
  * on both planes.  w_public != 0: W public (w_vals), X secret (x->vals/x->macs,
  * row-major din x batch).  w_public == 0: W secret (w->vals/w->macs), X public

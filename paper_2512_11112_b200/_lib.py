@@ -38,6 +38,11 @@ class Capability(C.Structure):  # spdz_capability_t
                 ("executable", C.c_int32), ("sm_count", C.c_int32), ("device", C.c_int32)]
 
 
+class BMTriple(C.Structure):  # spdz_bmtriple_t
+    _fields_ = [("din", C.c_uint32), ("dout", C.c_uint32), ("batch", C.c_uint32), ("a", Share), ("b", Share),
+                ("c", Share)]
+
+
 class MacSegment(C.Structure):  # spdz_mac_segment_t
     _fields_ = [("value", vp), ("mac_a", vp), ("mac_b", vp), ("len", C.c_uint64), ("j0", C.c_uint64),
                 ("batch_id", C.c_uint64), ("lane0", C.c_uint64), ("batch_len", C.c_uint64)]
@@ -109,6 +114,9 @@ _SIGS = {
     "spdz_matrix_open_combine": (C.c_int, [vp, C.POINTER(MTriple), vp, C.POINTER(vp), C.c_int, C.POINTER(Share),
                                            C.POINTER(Share), vp]),
     "spdz_matrix_combine": (C.c_int, [vp, C.POINTER(MTriple), vp, vp, C.POINTER(Share)]),
+    "spdz_bmatrix_mask": (C.c_int, [vp, C.POINTER(Share), C.POINTER(Share), C.POINTER(BMTriple), vp]),
+    "spdz_bmatrix_open_combine": (C.c_int, [vp, C.POINTER(BMTriple), vp, C.POINTER(vp), C.c_int, C.POINTER(Share),
+                                            vp]),
     "spdz_set_gemm_path": (C.c_int, [C.c_int]),
     "spdz_linear_secret_public": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, vp, C.POINTER(Share),
                                             C.POINTER(Share), vp, C.POINTER(Share)]),

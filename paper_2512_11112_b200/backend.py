@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib, errors
-from ._lib import Share, Triple, check, lib
+from ._lib import BMTriple, Share, Triple, check, lib
 
 P = 4294967291  # field.hpp:10
 
@@ -159,6 +159,16 @@ class Context:
         arr = (C.c_void_p * max(1, len(peers)))(*[p.data_ptr() for p in peers])
         check(lib().spdz_open_sum(self.h, own.data_ptr(), arr, len(peers), own.numel(), out.data_ptr()))
 
+    # batched secret x secret linear layer (linear.cpp:30-61 / spdz.cpp:98-124 over `batch` columns)
+    def bmatrix_mask(self, w, x, t, payload):
+        check(lib().spdz_bmatrix_mask(self.h, C.byref(dshare(w)), C.byref(dshare(x)), C.byref(dbmtriple(t)),
+                                      payload.data_ptr()))
+
+    def bmatrix_open_combine(self, t, own_payload, peer_payloads, z, opened_out):
+        peers = (C.c_void_p * max(1, len(peer_payloads)))(*[p.data_ptr() for p in peer_payloads])
+        check(lib().spdz_bmatrix_open_combine(self.h, C.byref(dbmtriple(t)), own_payload.data_ptr(), peers,
+                                              len(peer_payloads), C.byref(dshare(z)), opened_out.data_ptr()))
+
 
 # ---------------------------------------------------------------- device tensors
 @dataclass
@@ -202,6 +212,21 @@ def dshare(s) -> Share:
 
 def dtriple(t) -> Triple:
     return Triple(dshare(t.a), dshare(t.b), dshare(t.c))
+
+
+@dataclass
+class DeviceBMTriple:
+    """Batched matrix triple: A dout x din, B din x batch, C = A B (dout x batch)."""
+    din: int
+    dout: int
+    batch: int
+    a: DeviceShare
+    b: DeviceShare
+    c: DeviceShare
+
+
+def dbmtriple(t) -> BMTriple:
+    return BMTriple(t.din, t.dout, t.batch, dshare(t.a), dshare(t.b), dshare(t.c))
 
 
 # ---------------------------------------------------------------- Backend mirror

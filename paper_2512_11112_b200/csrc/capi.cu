@@ -545,6 +545,80 @@ int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t*
     return guard([&] { matrix_combine_common(ctx, mt, D, nullptr, 0, nullptr, z, nullptr, E); });
 }
 
+static void check_bmtriple(const spdz_bmtriple_t* t) {
+    need(t != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null batched matrix triple");
+    need_share(&t->a, "A");
+    need_share(&t->b, "B");
+    need_share(&t->c, "C");
+    if (t->a.lanes != (uint64_t)t->dout * t->din || t->b.lanes != (uint64_t)t->din * t->batch ||
+        t->c.lanes != (uint64_t)t->dout * t->batch)
+        throw Error(SPDZ_ERR_TRIPLE_SHAPE_MISMATCH, "TripleShapeMismatch: batched matrix triple planes do not match " +
+                                                        std::to_string(t->dout) + "x" + std::to_string(t->din) + "x" +
+                                                        std::to_string(t->batch));
+}
+
+int spdz_bmatrix_mask(spdz_ctx* ctx, const spdz_share_t* w, const spdz_share_t* x, const spdz_bmtriple_t* t,
+                      uint32_t* payload) {
+    return guard([&] {  // linear.cpp:30-49, every column of X at once
+        need_ctx(ctx);
+        need_share(w, "w");
+        need_share(x, "x");
+        check_bmtriple(t);
+        check_lanes(w->lanes, (uint64_t)t->dout * t->din);
+        check_lanes(x->lanes, (uint64_t)t->din * t->batch);
+        need(payload != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null payload");
+        device_guard(ctx);
+        const uint64_t cells = (uint64_t)t->dout * t->din, ecount = (uint64_t)t->din * t->batch;
+        need(ecount <= 0xFFFFFFFFull, SPDZ_ERR_INVALID_ARGUMENT, "din * batch too large");
+        launch_ok(launch_matrix_mask(ctx->stream, w->vals, t->a.vals, cells, x->vals, t->b.vals, (uint32_t)ecount,
+                                     payload, ctx->sms),
+                  "k_matrix_mask");
+    });
+}
+
+int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uint32_t* own_payload,
+                              const uint32_t* const* peer_payload, int n_peers, spdz_share_t* z, uint32_t* opened_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        check_bmtriple(t);
+        need_share(z, "z");
+        check_lanes(z->lanes, (uint64_t)t->dout * t->batch);
+        need(own_payload && opened_out, SPDZ_ERR_INVALID_ARGUMENT, "null payload / opened_out");
+        need(n_peers >= 0 && n_peers <= kMaxPeers && (n_peers == 0 || peer_payload), SPDZ_ERR_INVALID_ARGUMENT,
+             "n_peers out of range");
+        need(modgemm_tc_supported(t->din), SPDZ_ERR_INVALID_ARGUMENT, "batched secret x secret layer needs din <= 8192");
+        device_guard(ctx);
+        const uint64_t cells = (uint64_t)t->dout * t->din, ecount = (uint64_t)t->din * t->batch;
+        // open [D|E] (net.cpp:170-215): one pass over both halves
+        launch_ok(launch_open_sum(ctx->stream, own_payload, peer_payload, n_peers, opened_out, cells + ecount,
+                                  ctx->sms),
+                  "open [D|E]");
+        if (t->dout == 0 || t->batch == 0) return;
+        const uint32_t* D = opened_out;
+        const uint32_t* E = opened_out + cells;
+        const uint64_t scratch = std::max(modgemm_tc_scratch_bytes(0, t->dout, t->din, t->batch),
+                                          modgemm_tc_scratch_bytes(1, t->dout, t->din, t->batch));
+        uint8_t* sc = (uint8_t*)ctx->scratch.ensure(scratch);
+        // Z = C + D [B.v + [p0] E | B.m + alpha_i E]   (spdz.cpp:117-123 regrouped, exact mod p)
+        TcAux g1;
+        g1.e = E;
+        g1.coef0 = ctx->party == 0 ? 1u : 0u;
+        g1.coef1 = ctx->alpha;
+        g1.add0 = t->c.vals;
+        g1.add1 = t->c.macs;
+        launch_ok(launch_modgemm_tc(ctx->stream, 0, t->dout, t->din, t->batch, D, nullptr, t->b.vals, t->b.macs,
+                                    z->vals, z->macs, sc, ctx->sms, &g1),
+                  "k_modgemm_tc (D B')");
+        // Z += [A.v ; A.m] E
+        TcAux g2;
+        g2.add0 = z->vals;
+        g2.add1 = z->macs;
+        launch_ok(launch_modgemm_tc(ctx->stream, 1, t->dout, t->din, t->batch, t->a.vals, t->a.macs, E, nullptr,
+                                    z->vals, z->macs, sc, ctx->sms, &g2),
+                  "k_modgemm_tc (A E)");
+    });
+}
+
 static int g_gemm_path = 0;  // 0 auto (tcgen05 when K <= 8192), 1 CUDA-core, 2 tcgen05
 
 int spdz_set_gemm_path(int path) {

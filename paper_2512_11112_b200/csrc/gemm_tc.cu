@@ -91,12 +91,20 @@ __device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
     return (r >> 3) * kSBO + (k >> 4) * kLBO + (r & 7) * 16 + (k & 15);
 }
 
+// B-operand transform of the re-layout (k_tile_cols)
+struct TcBx {
+    const uint32_t* e;
+    uint32_t coef0, coef1;
+};
+
 // out plane mapping of C[row][col] (see launch_modgemm_tc)
 struct TcOut {
     int mode;          // 0: cols [0,batch) -> y0, [batch, 2 batch) -> y1;  1: rows [0,dout) -> y0, rest -> y1
     uint32_t dout, batch;
     uint32_t* y0;
     uint32_t* y1;
+    const uint32_t* add0;  // optional addend planes (same layout as y0/y1, may alias them): y = add + C
+    const uint32_t* add1;
 };
 
 // ---------------------------------------------------------------------------
@@ -255,6 +263,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     lim = col0 < N ? N - col0 : 0;
                 }
                 if (lim >= 16 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+                    if (out.add0) {  // same offset in the addend plane as in the output plane
+                        const bool hi = out.mode == 0 ? col0 >= out.batch : row >= out.dout;
+                        const uint32_t* src = (hi ? out.add1 : out.add0) + (dst - (hi ? out.y1 : out.y0));
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 a = reinterpret_cast<const uint4*>(src)[c];
+                            r[4 * c] = fp_add(r[4 * c], a.x);
+                            r[4 * c + 1] = fp_add(r[4 * c + 1], a.y);
+                            r[4 * c + 2] = fp_add(r[4 * c + 2], a.z);
+                            r[4 * c + 3] = fp_add(r[4 * c + 3], a.w);
+                        }
+                    }
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
                         reinterpret_cast<uint4*>(dst)[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
@@ -264,12 +284,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     for (int t = 0; t < 16; ++t) {
                         const uint32_t col = col0 + t;
                         if (col >= N) break;
+                        uint64_t off;
+                        bool hi;
                         if (out.mode == 0) {
-                            if (col < out.batch) out.y0[(uint64_t)row * out.batch + col] = r[t];
-                            else out.y1[(uint64_t)row * out.batch + (col - out.batch)] = r[t];
+                            hi = col >= out.batch;
+                            off = (uint64_t)row * out.batch + (hi ? col - out.batch : col);
                         } else {
-                            dst[t] = r[t];
+                            hi = row >= out.dout;
+                            off = (uint64_t)(hi ? row - out.dout : row) * out.batch + col;
                         }
+                        uint32_t v = r[t];
+                        if (out.add0) v = fp_add(v, (hi ? out.add1 : out.add0)[off]);
+                        (hi ? out.y1 : out.y0)[off] = v;
                     }
                 }
             }
@@ -328,16 +354,24 @@ __global__ void __launch_bounds__(256) k_tile_rows(const uint32_t* __restrict__ 
 
 // B (K x N, columns stacked b0 | b1) -> pre-tiled K-major limb image (transposed):
 // block = 64 k x 32 n through shared memory; one thread per (n, 16-k chunk) on the way out.
+// With bx.e set, the operand is B + coef * E (E: K x NB, the same plane under both
+// halves; coef0 for columns < NB, coef1 after) — the matrix-triple combine's
+// B.v + [party 0] E and B.m + alpha_i E, formed on the way into the limb image.
 template <int BN>
 __global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __restrict__ b1, uint32_t NB, uint32_t N,
-                            uint32_t K, uint32_t KB, uint8_t* __restrict__ out) {
+                            uint32_t K, uint32_t KB, TcBx bx, uint8_t* __restrict__ out) {
     __shared__ uint32_t tile[TK][33];
     const uint32_t kb = blockIdx.x, nt32 = blockIdx.y * 32;
     for (uint32_t e = threadIdx.x; e < TK * 32; e += blockDim.x) {
         const uint32_t kk = e / 32, nn = e % 32;
         const uint32_t k = kb * TK + kk, n = nt32 + nn;
         uint32_t v = 0;
-        if (k < K && n < N) v = n < NB ? b0[(uint64_t)k * NB + n] : b1[(uint64_t)k * NB + (n - NB)];
+        if (k < K && n < N) {
+            const bool hi = n >= NB;
+            const uint64_t off = (uint64_t)k * NB + (hi ? n - NB : n);
+            v = (hi ? b1 : b0)[off];
+            if (bx.e) v = fp_add(v, fp_mul(hi ? bx.coef1 : bx.coef0, bx.e[off]));
+        }
         tile[kk][nn] = v;
     }
     __syncthreads();
@@ -369,8 +403,8 @@ uint32_t g_tc_dbg = 0;
 // the GEMM kernel with TN = BN.
 template <int BN>
 cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
-                   const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint8_t* scratch, const TcOut& out,
-                   int sms) {
+                   const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx, uint8_t* scratch,
+                   const TcOut& out, int sms) {
     const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
     const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
     const uint32_t KB = (din + TK - 1) / TK;
@@ -383,8 +417,8 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         else k_tile_rows<<<grid, 256, 0, s>>>(w0, w1, dout, M, din, Mp, KB, At);
         ++g_kernel_launches;
         dim3 g2(KB, (Np + 31) / 32);
-        if (mode == 0) k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x1, batch, N, din, KB, Bt);
-        else k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x0, batch, N, din, KB, Bt);
+        if (mode == 0) k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x1, batch, N, din, KB, bx, Bt);
+        else k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x0, batch, N, din, KB, TcBx{}, Bt);
         ++g_kernel_launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -418,17 +452,19 @@ bool modgemm_tc_supported(uint32_t din) { return din >= 1 && din <= 8192; }
 // Y (dout x batch, two planes) for the secret x public linear layer on tcgen05.
 //   mode 0: W public (w0), X secret planes (x0 vals, x1 macs): C = W * [Xv | Xm]
 //   mode 1: W secret planes (w0, w1), X public (x0):           C = [Wv ; Wm] * X
+// Optional (aux): mode 0 right operand X_h + coef_h * E; Y = addend + C.
 cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,
                               const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
-                              uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms) {
+                              uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms, const TcAux* aux) {
     if (dout == 0 || batch == 0) return cudaSuccess;
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
-    TcOut out{mode, dout, batch, y0, y1};
+    TcOut out{mode, dout, batch, y0, y1, aux ? aux->add0 : nullptr, aux ? aux->add1 : nullptr};
+    const TcBx bx{aux ? aux->e : nullptr, aux ? aux->coef0 : 0u, aux ? aux->coef1 : 0u};
     // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
     const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
     const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
-    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
-    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, scratch, out, sms);
+    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, out, sms);
+    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, out, sms);
 }
 
 }  // namespace spdzb200

@@ -86,9 +86,17 @@ cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din
 // tcgen05 kind::i8 limb GEMM (gemm_tc.cu); scratch >= modgemm_tc_scratch_bytes()
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch);
 bool modgemm_tc_supported(uint32_t din);
+// Optional extras of the tcgen05 GEMM: mode-0 right operand X_h + coef_h * e (e: din x batch),
+// and an addend (planes laid out like y, may alias y): y = add + W X.
+struct TcAux {
+    const uint32_t* e = nullptr;
+    uint32_t coef0 = 0, coef1 = 0;
+    const uint32_t* add0 = nullptr;
+    const uint32_t* add1 = nullptr;
+};
 cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,
                               const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
-                              uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms);
+                              uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms, const TcAux* aux = nullptr);
 
 // GPU dealer (spdz.cpp:162-249), closed-form splitmix64 stream.
 // lanes [j_first, j_first+count) of Dealer::triples(S_total); party p's share of

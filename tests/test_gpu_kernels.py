@@ -496,3 +496,58 @@ def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
     finally:
         lib().spdz_diag_gemm_tc_flags(0)
         check(lib().spdz_set_gemm_path(0))
+
+
+@pytest.mark.parametrize("din,dout,batch", [(96, 200, 40), (512, 384, 300), (1024, 256, 130)])
+def test_batched_secret_secret_linear(gpu, din, dout, batch):
+    """Batched secret x secret layer (spdz_bmatrix_mask / spdz_bmatrix_open_combine),
+    2 parties: (1) every party's opened [D|E] and, per column j, Z shares equal to the
+    reference's matrix_combine({A, B[:,j], C[:,j]}, D, E[:,j]) (oracle, spdz.cpp:98-124);
+    (2) Z reconstructs to W X and its MACs to alpha W X (exact numpy mod-p matmul)."""
+    import torch
+    from paper_2512_11112_b200 import DeviceBMTriple
+    d = O.Dealer(2, 77)
+    alpha = d.alpha
+    rng = np.random.default_rng(din + dout + batch)
+    rnd = lambda n: rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+    Wc, Xc, Ac, Bc = rnd(dout * din), rnd(din * batch), rnd(dout * din), rnd(din * batch)
+    Cc = _np_modmatmul(Ac.reshape(dout, din), Bc.reshape(din, batch)).reshape(-1)
+    sh = {k: d.share(v) for k, v in (("W", Wc), ("X", Xc), ("A", Ac), ("B", Bc), ("C", Cc))}
+    ctxs, trip, pay = [], [], []
+    for p in range(2):
+        c = ctx(p, 2, d.alpha_share(p))
+        t = DeviceBMTriple(din, dout, batch, share(sh["A"][0][p], sh["A"][1][p]), share(sh["B"][0][p], sh["B"][1][p]),
+                           share(sh["C"][0][p], sh["C"][1][p]))
+        w, x = share(sh["W"][0][p], sh["W"][1][p]), share(sh["X"][0][p], sh["X"][1][p])
+        pl = torch.empty(dout * din + din * batch, dtype=torch.uint32, device="cuda")
+        c.bmatrix_mask(w, x, t, pl)
+        ctxs.append(c)
+        trip.append(t)
+        pay.append(pl)
+    from paper_2512_11112_b200 import DeviceShare
+    zs, opened = [], []
+    for p in range(2):
+        z = DeviceShare.empty(dout * batch)
+        op = torch.empty_like(pay[p])
+        ctxs[p].bmatrix_open_combine(trip[p], pay[p], [pay[1 - p]], z, op)
+        zs.append((H(z.vals), H(z.macs)))
+        opened.append(H(op))
+    D = O.np_sub(Wc, Ac)
+    E = O.np_sub(Xc, Bc)
+    for p in range(2):
+        np.testing.assert_array_equal(opened[p], np.concatenate([D, E]))
+    Zv = O.reconstruct(np.stack([zs[0][0], zs[1][0]])).reshape(dout, batch)
+    Zm = O.reconstruct(np.stack([zs[0][1], zs[1][1]])).reshape(dout, batch)
+    want = _np_modmatmul(Wc.reshape(dout, din), Xc.reshape(din, batch))
+    np.testing.assert_array_equal(Zv, want)
+    np.testing.assert_array_equal(Zm, ((want.astype(np.uint64) * alpha) % P).astype(np.uint32))
+    Em = E.reshape(din, batch)
+    for j in (0, batch // 2, batch - 1):
+        for p in range(2):
+            mt = {"Av": sh["A"][0][p], "Am": sh["A"][1][p], "Bv": sh["B"][0][p].reshape(din, batch)[:, j].copy(),
+                  "Bm": sh["B"][1][p].reshape(din, batch)[:, j].copy(),
+                  "Cv": sh["C"][0][p].reshape(dout, batch)[:, j].copy(),
+                  "Cm": sh["C"][1][p].reshape(dout, batch)[:, j].copy()}
+            zv, zm = O.matrix_combine(din, dout, mt, D, Em[:, j].copy(), p, d.alpha_share(p))
+            np.testing.assert_array_equal(zs[p][0].reshape(dout, batch)[:, j], zv)
+            np.testing.assert_array_equal(zs[p][1].reshape(dout, batch)[:, j], zm)
