@@ -359,7 +359,7 @@ def main():
     ap.add_argument("--lanes", type=int, default=1 << 24)
     ap.add_argument("--cpu-sample-lanes", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run (1 = serial)")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="lane chunks of the host-streamed e2e run (1 = serial)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

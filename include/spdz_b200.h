@@ -392,6 +392,14 @@ int spdz_run_bind_output(spdz_run* run, uint32_t* host_out, uint64_t cap);
  * coin, then verification (unless external_mac_verify) and the report.
  * spdz_run_online = begin + mac_check(use_coin = 0). */
 int spdz_run_online_begin(spdz_run* run, int reuse_preprocessing);
+/* Optional caller-owned streams (device of party 0 / of the output party) for the input
+ * H2D copies and the output D2H copy, shared by several runs so that their copies queue
+ * in issue order (host-streamed execution).  NULL restores the run's own streams. */
+int spdz_run_set_copy_streams(spdz_run* run, void* h2d_stream, void* d2h_stream);
+/* First half of spdz_run_mac_check: agree on the coin and launch the sigma kernels
+ * asynchronously; the next spdz_run_mac_check collects and verifies (its coin
+ * arguments are then ignored). */
+int spdz_run_mac_check_launch(spdz_run* run, int use_coin, uint64_t coin);
 int spdz_run_mac_check(spdz_run* run, int use_coin, uint64_t coin, spdz_run_report_t* report);
 /* fnv1a64 digest of the last opened outputs (RunReport.output_digest, runtime.cpp:573). */
 int spdz_run_output_digest(spdz_run* run, uint64_t* digest);

@@ -156,6 +156,12 @@ struct spdz_run {
     cudaEvent_t ev_input = nullptr;
     cudaEvent_t ev_opened = nullptr;
     cudaStream_t copy_stream = nullptr;
+    // optional caller-owned copy streams shared by several runs (StreamedRun): H2D of the
+    // inputs in issue order on one stream, so chunk c's inputs land before chunk c+1's
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_h2d = nullptr, ev_out = nullptr;
+    bool mac_launched = false;      // spdz_run_mac_check_launch issued the sigma kernels
+    uint64_t mac_coin = 0;
     bool in_flight = false;
     bool any_remote = false;
     uint32_t seq = 0;               // phase sequence number written to / awaited on opening flags
@@ -475,6 +481,8 @@ void plan_buffers(spdz_run* r) {
     dev(r, r->ref_party());
     cuda_check(cudaEventCreateWithFlags(&r->ev_input, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&r->ev_opened, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&r->ev_h2d, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&r->ev_out, cudaEventDisableTiming), "event");
     cuda_check(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking), "copy stream");
 }
 
@@ -1115,7 +1123,7 @@ uint64_t fresh_nonce() {
 }
 
 // runtime.cpp:467-506
-void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t given_coin) {
+uint64_t agree_coin(spdz_run* r, bool have_coin, uint64_t given_coin) {
     const int n = r->n;
     uint64_t coin = 0;
     if (have_coin) {
@@ -1134,7 +1142,12 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
             coin = spdz_fnv1a64(&nonce[p], 8, coin);
         }
     }
-    for (int p = 0; p < n; ++p) {
+    return coin;
+}
+
+// sigma kernels of every local party (asynchronous)
+void mac_launch(spdz_run* r, uint64_t coin) {
+    for (int p = 0; p < r->n; ++p) {
         auto& P = r->parties[p];
         if (!P.local) continue;
         dev(r, p);
@@ -1146,6 +1159,11 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
         ktimer_end(r, p, tk, SPDZ_KSTAT_SIGMA, sbytes);
         lk(cudaEventRecord(P.t1, P.ctx->stream), "t1");
     }
+}
+
+// collect sigmas, commit/verify (spdz.cpp:140-158)
+void mac_finish(spdz_run* r, spdz_run_report_t* rep, uint64_t coin) {
+    const int n = r->n;
     std::vector<uint32_t> sig(n);
     std::vector<uint64_t> nonce2(n), commits(n);
     for (int p = 0; p < n; ++p) {
@@ -1164,6 +1182,12 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
     if (r->opts.external_mac_verify) return;  // partial sigmas: the caller sums shards and verifies
     int rc = spdz_verify_sigmas(sig.data(), nonce2.data(), commits.data(), n);
     if (rc) throw Error(rc, spdz_last_error());
+}
+
+void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t given_coin) {
+    const uint64_t coin = agree_coin(r, have_coin, given_coin);
+    mac_launch(r, coin);
+    mac_finish(r, rep, coin);
 }
 
 void share_inputs(spdz_run* r) {
@@ -1338,6 +1362,8 @@ int spdz_run_destroy(spdz_run* r) {
             cudaSetDevice(r->devices[r->ref_party()]);
             cudaEventDestroy(r->ev_input);
             cudaEventDestroy(r->ev_opened);
+            cudaEventDestroy(r->ev_h2d);
+            cudaEventDestroy(r->ev_out);
             cudaStreamSynchronize(r->copy_stream);
             cudaStreamDestroy(r->copy_stream);
         }
@@ -1380,7 +1406,13 @@ int spdz_run_bind_input(spdz_run* r, uint32_t node, const uint32_t* host_vals, u
         uint32_t* d = it == r->input_dev.end() ? (r->input_dev[node] = r->alloc(0, len)) : it->second;
         dev(r, 0);
         auto& P0 = r->parties[0];
-        lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, P0.ctx->stream), "H2D input");
+        if (r->h2d_stream) {
+            lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, r->h2d_stream), "H2D input");
+            lk(cudaEventRecord(r->ev_h2d, r->h2d_stream), "record h2d");
+            lk(cudaStreamWaitEvent(P0.ctx->stream, r->ev_h2d, 0), "wait h2d");
+        } else {
+            lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, P0.ctx->stream), "H2D input");
+        }
         // reduce mod p (preproc.cpp:149 fp::reduce): x * 1 mod p
         lk(launch_public(P0.ctx->stream, 3, d, d, nullptr, false, 1u, true, 0, 0, d, d, len, P0.ctx->sms),
            "reduce input");
@@ -1432,11 +1464,31 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
             r->host_out_owned = true;
         }
         r->host_out_len = rv.lanes;
+        cudaStream_t out_stream = r->d2h_stream ? r->d2h_stream : r->copy_stream;
         lk(cudaEventRecord(r->ev_opened, S(r, op)), "record opened");
-        lk(cudaStreamWaitEvent(r->copy_stream, r->ev_opened, 0), "wait opened");
-        lk(cudaMemcpyAsync(r->host_out, r->parties[op].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost,
-                           r->copy_stream),
+        lk(cudaStreamWaitEvent(out_stream, r->ev_opened, 0), "wait opened");
+        lk(cudaMemcpyAsync(r->host_out, r->parties[op].outputs, rv.lanes * 4, cudaMemcpyDeviceToHost, out_stream),
            "D2H out");
+        lk(cudaEventRecord(r->ev_out, out_stream), "record out");
+    });
+}
+
+int spdz_run_set_copy_streams(spdz_run* r, void* h2d_stream, void* d2h_stream) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        need(!r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "online phase in flight");
+        r->h2d_stream = static_cast<cudaStream_t>(h2d_stream);
+        r->d2h_stream = static_cast<cudaStream_t>(d2h_stream);
+    });
+}
+
+int spdz_run_mac_check_launch(spdz_run* r, int use_coin, uint64_t coin) {
+    return guard([&] {
+        need(r != nullptr && r->in_flight && !r->mac_launched, SPDZ_ERR_INVALID_ARGUMENT,
+             "no online phase in flight (or its MAC check was already launched)");
+        r->mac_coin = agree_coin(r, use_coin != 0, coin);
+        mac_launch(r, r->mac_coin);
+        r->mac_launched = true;
     });
 }
 
@@ -1444,9 +1496,14 @@ int spdz_run_mac_check(spdz_run* r, int use_coin, uint64_t coin, spdz_run_report
     return guard([&] {
         need(r != nullptr && r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "no online phase in flight");
         r->in_flight = false;
-        mac_check(r, rep, use_coin != 0, coin);  // records t1 and synchronises the party streams
+        if (r->mac_launched) {  // sigma kernels already in flight (spdz_run_mac_check_launch)
+            r->mac_launched = false;
+            mac_finish(r, rep, r->mac_coin);
+        } else {
+            mac_check(r, rep, use_coin != 0, coin);  // records t1 and synchronises the party streams
+        }
         dev(r, r->ref_party());
-        lk(cudaStreamSynchronize(r->copy_stream), "sync out");
+        lk(cudaEventSynchronize(r->ev_out), "sync out");
         auto t1 = std::chrono::steady_clock::now();
         if (rep) {
             rep->online_ms = std::chrono::duration<double, std::milli>(t1 - r->wall0).count();

@@ -242,6 +242,16 @@ class LocalRun:
         """Node execution + root open, enqueued (asynchronous); finish with mac_check()."""
         check(lib().spdz_run_online_begin(self.h, int(reuse)))
 
+    def set_copy_streams(self, h2d=None, d2h=None):
+        """Caller-owned streams (torch.cuda.Stream or raw handles) for the input H2D and
+        output D2H copies, shared by several runs so their copies queue in issue order."""
+        h = lambda s: None if s is None else int(getattr(s, "cuda_stream", s))
+        check(lib().spdz_run_set_copy_streams(self.h, h(h2d), h(d2h)))
+
+    def mac_check_launch(self, coin: int | None = None):
+        """Agree on the coin and enqueue the sigma kernels; mac_check() then collects."""
+        check(lib().spdz_run_mac_check_launch(self.h, 0 if coin is None else 1, int(coin or 0)))
+
     def mac_check(self, coin: int | None = None) -> RunReport:
         """Deferred MAC check of the phase begun by online_begin(); `coin` = agreed coin
         (None: the run's own commit/reveal or fixed coin)."""
@@ -319,6 +329,14 @@ class StreamedRun:
             off += L
         self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
                               shard=(o, total), external_mac_verify=True) for o, L in self.ranges]
+        # one H2D and one D2H stream shared by all chunks: copies complete in chunk order, so
+        # chunk c computes while chunk c+1's inputs cross PCIe (separate per-chunk copy
+        # streams would interleave the transfers and delay every chunk to the end of all H2D)
+        import torch
+        dev = (devices or [0])[0]
+        self._copy_streams = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+        for r in self.runs:
+            r.set_copy_streams(*self._copy_streams)
 
     def close(self):
         for r in self.runs:
@@ -348,7 +366,9 @@ class StreamedRun:
             coin = 0
             for nz in (int.from_bytes(os.urandom(8), "little") for _ in range(self.n)):
                 coin = lib().spdz_fnv1a64((C.c_uint64 * 1)(nz), 8, coin)
-        reps = [r.mac_check(coin) for r in self.runs]
+        for r in self.runs:  # every chunk's sigma kernels in flight before the first collect
+            r.mac_check_launch(coin)
+        reps = [r.mac_check() for r in self.runs]
         sig = [sum(rep.sigmas[p] for rep in reps) % 4294967291 for p in range(self.n)]
         nonces = [int.from_bytes(os.urandom(8), "little") for _ in range(self.n)]
         commits = [lib().spdz_commit_sigma(s, nz) for s, nz in zip(sig, nonces)]

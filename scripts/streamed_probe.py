@@ -29,10 +29,28 @@ for chunks in [int(c) for c in (sys.argv[1:] or ["1", "2", "4", "8"])]:
             t.append(time.perf_counter())
             r.online_begin()
             t.append(time.perf_counter())
-        reps = [r.mac_check(12345) for r in sr.runs]
+        t.append(time.perf_counter())
+        for r in sr.runs:
+            r.mac_check_launch(12345)
+        reps = [r.mac_check() for r in sr.runs]
         t.append(time.perf_counter())
         d = np.diff(t) * 1e3
         if k:
             print(f"chunks={chunks}: total {1e3 * (t[-1] - t[0]):.2f} ms | per-chunk bind/share/begin "
-                  f"{np.round(d[:-1].reshape(-1, 3).mean(0), 3)} | mac_check all {d[-1]:.2f} ms", flush=True)
+                  f"{np.round(d[:-2].reshape(-1, 3).mean(0), 3)} | issue all {1e3 * (t[-2] - t[0]):.2f} ms"
+                  f" | mac_check all {d[-1]:.2f} ms", flush=True)
     sr.close()
+
+# PCIe copy bandwidth of this box (pinned host <-> device, 128 MiB)
+hb = torch.empty(1 << 25, dtype=torch.int32).pin_memory()
+db = torch.empty(1 << 25, dtype=torch.int32, device="cuda")
+for name, fn in (("H2D", lambda: db.copy_(hb, non_blocking=True)), ("D2H", lambda: hb.copy_(db, non_blocking=True))):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{name}: {5 * hb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9:.1f} GB/s", flush=True)
