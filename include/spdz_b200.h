@@ -50,6 +50,8 @@ typedef enum spdz_status {
     SPDZ_ERR_MALFORMED_SHARE_MESSAGE = 9,/* net::MalformedShareMessage   net.hpp:34 */
     SPDZ_ERR_MAC_CHECK_FAILED = 10,      /* spdz::MacCheckFailed         spdz.hpp:12 */
     SPDZ_ERR_SLICE_TOO_SMALL = 11,       /* linear::SliceTooSmall        linear.hpp:10 */
+    SPDZ_ERR_STORE_FORMAT = 12,          /* spdz::StoreFormatError       triple_store.hpp:23 */
+    SPDZ_ERR_INSUFFICIENT_TRIPLES = 13,  /* preproc::InsufficientTriples preproc.cpp:182-201 */
     SPDZ_ERR_INVALID_ARGUMENT = 20,
     SPDZ_ERR_CUDA = 21,
     SPDZ_ERR_DEALER_REJECTION = 22,      /* GPU dealer hit the 25/2^64 rejection branch */
@@ -199,6 +201,16 @@ uint64_t spdz_commit_sigma(uint32_t sigma, uint64_t nonce);
 int spdz_verify_sigmas(const uint32_t* sigmas, const uint64_t* nonces, const uint64_t* commitments, uint64_t n);
 /* hash.hpp:11-19 */
 uint64_t spdz_fnv1a64(const void* data, uint64_t len, uint64_t seed);
+
+/* ---------------- preprocessing files ---------------- */
+typedef struct spdz_store_info {
+    int32_t party, n_parties;
+    uint32_t alpha_share;
+    uint64_t loop_iters, scalar_triples, matrix_triples, input_masks;
+} spdz_store_info_t;
+/* Validate an MPCT triple-store file (host only, nothing copied): magic, version,
+ * prime, every section inside the file, no trailing bytes (triple_store.cpp:196-244). */
+int spdz_store_inspect(const char* path, spdz_store_info_t* info);
 
 /* ---------------- linear layer ---------------- */
 /* linear.cpp:7-21.  Fills starts/counts (capacity `cap`), returns the tile
@@ -359,6 +371,12 @@ typedef struct spdz_run spdz_run;
 /* Builds the run: computes the triple layout (preproc.cpp:124-163), runs the
  * GPU dealer for every party (make_dealer_stores order, triple_store.cpp:248-287)
  * and allocates every device buffer of the online phase. */
+/* Host only: the triple layout spdz_run_create plans for this graph
+ * (preproc.cpp:124-163 compute_triple_layout): per region 5 words
+ * {kind 0 scalar / 1 matrix, node, base, stride, max_execs}, scalar regions first,
+ * nodes ascending; *n_regions receives the count (out may be NULL to query). */
+int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t* out, uint64_t cap,
+                       uint64_t* n_regions);
 int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
                     const spdz_run_options_t* opts, spdz_run** out);
 int spdz_run_destroy(spdz_run* run);
@@ -369,6 +387,15 @@ int spdz_run_export(spdz_run* run, void* buf, uint64_t cap, uint64_t* len);
 /* Maps other processes' export blobs (concatenated; own entries are skipped). */
 int spdz_run_import(spdz_run* run, const void* blob, uint64_t len);
 /* Re-runs the GPU dealer with `seed` (fresh preprocessing; inputs must be shared again). */
+/* One party's MPCT triple-store file (the reference's preprocessing output,
+ * write_store_file / read_store_file triple_store.cpp:163-244) loaded into this run's
+ * device pools instead of spdz_run_deal: the scalar triples of every region of the
+ * run's triple layout (preproc.cpp:124-163), the matrix triples in demand order and the
+ * input masks, read through pinned staging buffers.  Call once per local party.
+ * Errors: SPDZ_ERR_STORE_FORMAT (VersionMismatch / CorruptPayload),
+ * SPDZ_ERR_INSUFFICIENT_TRIPLES (store smaller than the run's demand, preproc.cpp:182-201),
+ * SPDZ_ERR_TRIPLE_SHAPE_MISMATCH (matrix triple of the wrong shape). */
+int spdz_run_load_store(spdz_run* run, int party, const char* path);
 int spdz_run_deal(spdz_run* run, uint64_t seed);
 /* Cleartext input for an INPUT node (host pointer).  Private inputs are shared
  * with the dealer's input masks (preproc.cpp:205-243) during spdz_run_share_inputs. */

@@ -86,6 +86,9 @@ def lib():
         L.reft_plan_tiles.restype = C.c_int64
         L.reft_graph_dump.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64]
         L.reft_graph_dump.restype = C.c_uint64
+        L.reft_triple_layout.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_char_p, C.c_uint64]
+        L.reft_triple_layout.restype = C.c_uint64
+        L.reft_write_dealer_stores.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_char_p]
         L.reft_interpret.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, U32P,
                                      C.c_uint64, C.POINTER(C.c_uint64)]
         L.reft_run_local.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
@@ -303,6 +306,25 @@ def graph_dump(ir_text: str) -> str:
     buf = C.create_string_buffer(n)
     lib().reft_graph_dump(ir_text.encode(), buf, n)
     return buf.value.decode()
+
+
+def triple_layout(ir_text: str, slice_: int = 262140, loop_iters: int = 1) -> dict:
+    """preproc::compute_triple_layout (preproc.cpp:124-163): {"scalar"|"matrix": {node: (base, stride, execs)}}."""
+    n = lib().reft_triple_layout(ir_text.encode(), slice_, loop_iters, None, 0)
+    buf = C.create_string_buffer(n)
+    lib().reft_triple_layout(ir_text.encode(), slice_, loop_iters, buf, n)
+    out = {"scalar": {}, "matrix": {}}
+    for line in buf.value.decode().splitlines():
+        k, node, base, stride, execs = line.split()
+        out["scalar" if k == "S" else "matrix"][int(node)] = (int(base), int(stride), int(execs))
+    return out
+
+
+def write_dealer_stores(ir_text: str, n_parties: int, out_dir: str, slice_: int = 262140, seed: int = 1,
+                        loop_iters: int = 1):
+    """The dealer tool's files for one circuit: <out_dir>/triples_<i>.bin (triple_store.cpp:288-303)."""
+    _check(lib().reft_write_dealer_stores(ir_text.encode(), n_parties, slice_, seed, loop_iters,
+                                          str(out_dir).encode()))
 
 
 def _inputs(inputs: dict):

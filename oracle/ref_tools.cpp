@@ -420,6 +420,38 @@ int reft_run_local(const char* ir_text, int n_parties, int threads, uint64_t sli
     });
 }
 
+// preproc.cpp:124-163: scalar/matrix regions of the compiled graph.  Writes
+// "S id base stride max_execs" / "M id base stride max_execs" lines; returns bytes needed.
+uint64_t reft_triple_layout(const char* ir_text, uint64_t slice, uint64_t loop_iters, char* buf, uint64_t cap) {
+    std::string out;
+    int rc = guard([&] {
+        auto g = compile_text(ir_text);
+        auto L = preproc::compute_triple_layout(g, slice, loop_iters);
+        for (auto& [id, r] : L.scalar)
+            out += "S " + std::to_string(id) + " " + std::to_string(r.base) + " " + std::to_string(r.stride) + " " +
+                   std::to_string(r.max_execs) + "\n";
+        for (auto& [id, r] : L.matrix)
+            out += "M " + std::to_string(id) + " " + std::to_string(r.base) + " " + std::to_string(r.stride) + " " +
+                   std::to_string(r.max_execs) + "\n";
+    });
+    if (rc) return 0;
+    if (buf && cap) std::strncpy(buf, out.c_str(), cap);
+    return out.size() + 1;
+}
+
+// The dealer tool's output for one circuit: compute_triple_demand (preproc.cpp) +
+// write_dealer_stores (triple_store.cpp:288-303) -> <out_dir>/triples_<i>.bin
+int reft_write_dealer_stores(const char* ir_text, int n_parties, uint64_t slice, uint64_t dealer_seed,
+                             uint64_t loop_iters, const char* out_dir) {
+    return guard([&] {
+        auto g = compile_text(ir_text);
+        auto demand = preproc::compute_triple_demand(g, slice, loop_iters);
+        spdz::Dealer dealer(n_parties, dealer_seed);
+        spdz::write_dealer_stores(dealer, demand.scalars, demand.matrix_shapes, demand.input_masks, out_dir,
+                                  loop_iters);
+    });
+}
+
 // Kernel-level CPU timing (pattern of benchmarks/kernel_bench.cpp:33-58):
 // best-of-`reps` wall time of CpuBackend::mul_mask + mul_combine on `lanes`.
 double reft_time_beaver_kernels(uint64_t lanes, int reps) {

@@ -43,6 +43,11 @@ class BMTriple(C.Structure):  # spdz_bmtriple_t
                 ("c", Share)]
 
 
+class StoreInfo(C.Structure):  # spdz_store_info_t
+    _fields_ = [("party", C.c_int32), ("n_parties", C.c_int32), ("alpha_share", C.c_uint32), ("loop_iters", C.c_uint64),
+                ("scalar_triples", C.c_uint64), ("matrix_triples", C.c_uint64), ("input_masks", C.c_uint64)]
+
+
 class MacSegment(C.Structure):  # spdz_mac_segment_t
     _fields_ = [("value", vp), ("mac_a", vp), ("mac_b", vp), ("len", C.c_uint64), ("j0", C.c_uint64),
                 ("batch_id", C.c_uint64), ("lane0", C.c_uint64), ("batch_len", C.c_uint64)]
@@ -140,6 +145,9 @@ _SIGS = {
                                   C.POINTER(vp)]),
     "spdz_run_destroy": (C.c_int, [vp]),
     "spdz_run_deal": (C.c_int, [vp, C.c_uint64]),
+    "spdz_triple_layout": (C.c_int, [C.POINTER(Node), C.c_uint32, C.c_uint64, u64p, C.c_uint64, u64p]),
+    "spdz_run_load_store": (C.c_int, [vp, C.c_int, C.c_char_p]),
+    "spdz_store_inspect": (C.c_int, [C.c_char_p, C.POINTER(StoreInfo)]),
     "spdz_run_bind_input": (C.c_int, [vp, C.c_uint32, vp, C.c_uint64]),
     "spdz_run_share_inputs": (C.c_int, [vp]),
     "spdz_run_online": (C.c_int, [vp, C.c_int, C.POINTER(RunReport)]),

@@ -20,6 +20,7 @@
 
 #include "field.cuh"
 #include "internal.hpp"
+#include "store.hpp"
 
 using namespace spdzb200;
 
@@ -556,6 +557,71 @@ void deal(spdz_run* r, uint64_t seed) {
     }
     r->consumed = false;
     r->dealer_seed = seed;
+}
+
+// ---- preprocessing from the reference's store files (instead of deal) ----
+// Party p's MPCT file: the slices of the global layout this run consumes, straight into
+// the pools deal() would have filled (same offsets, so the online phase is unchanged).
+void load_store(spdz_run* r, int p, const char* path) {
+    need(p >= 0 && p < r->n && r->parties[p].local, SPDZ_ERR_INVALID_ARGUMENT, "party is not local to this run");
+    const StoreLayout L = scan_store(path);
+    need(L.party == p && L.n_parties == r->n, SPDZ_ERR_STORE_FORMAT,
+         "VersionMismatch: store is party " + std::to_string(L.party) + " of " + std::to_string(L.n_parties) +
+             ", run needs party " + std::to_string(p) + " of " + std::to_string(r->n));
+    // demand check of load_run_bundle (preproc.cpp:182-201)
+    size_t mats_needed = 0;
+    for (auto& [id, reg] : r->matrix) mats_needed += r->tiles[id].starts.size();
+    if (L.n_scalar < r->scalar_total_global)
+        throw Error(SPDZ_ERR_INSUFFICIENT_TRIPLES, "InsufficientTriples: need " + std::to_string(r->scalar_total_global) +
+                                                       " scalar triples, store has " + std::to_string(L.n_scalar));
+    if (L.mats.size() < mats_needed)
+        throw Error(SPDZ_ERR_INSUFFICIENT_TRIPLES, "InsufficientTriples: need " + std::to_string(mats_needed) +
+                                                       " matrix triples, store has " + std::to_string(L.mats.size()));
+    if (L.n_masks < r->mask_total_global)
+        throw Error(SPDZ_ERR_INSUFFICIENT_TRIPLES, "InsufficientTriples: need " + std::to_string(r->mask_total_global) +
+                                                       " input masks, store has " + std::to_string(L.n_masks));
+    auto& P = r->parties[p];
+    dev(r, p);
+    StagedUpload up(path, r->copy_stream);
+    // scalar triples: region slices of the six planes (take_range offsets, triple_store.cpp:108-133)
+    for (auto& [id, reg] : r->scalar) {
+        const uint64_t cnt = reg.stride * reg.max_execs;
+        for (int q = 0; q < 6; ++q)
+            up.copy(L.scalar_off + 4 * ((uint64_t)q * L.n_scalar + reg.gbase), 4 * cnt, P.pool[q] + reg.base);
+    }
+    // matrix triples in demand order: linear nodes by id, tiles in order (take_matrix_at)
+    size_t k = 0;
+    for (auto& [id, reg] : r->matrix) {
+        const auto& nd = r->node(id);
+        const auto& lt = r->tiles[id];
+        auto& st = P.ns[id];
+        for (size_t t = 0; t < lt.starts.size(); ++t, ++k) {
+            const auto& m = L.mats[k];
+            const uint32_t rows = lt.counts[t];
+            if (m.rows != rows || m.din != nd.din)
+                throw Error(SPDZ_ERR_TRIPLE_SHAPE_MISMATCH,
+                            "TripleShapeMismatch: store has " + std::to_string(m.rows) + "x" + std::to_string(m.din) +
+                                ", tile needs " + std::to_string(rows) + "x" + std::to_string(nd.din));
+            const uint64_t cells = (uint64_t)rows * nd.din;
+            uint64_t at = m.off;
+            const uint64_t aoff = (uint64_t)lt.starts[t] * nd.din, boff = (uint64_t)t * nd.din;
+            uint32_t* dst[6] = {st.mA[0] + aoff, st.mA[1] + aoff, st.mB[0] + boff,
+                                st.mB[1] + boff, st.mC[0] + lt.starts[t], st.mC[1] + lt.starts[t]};
+            const uint64_t words[6] = {cells, cells, nd.din, nd.din, rows, rows};
+            for (int q = 0; q < 6; ++q) {
+                up.copy(at, 4 * words[q], dst[q]);
+                at += 4 * words[q];
+            }
+            (void)reg;
+        }
+    }
+    // input masks (take_masks, triple_store.cpp:156-161); party 0's file carries the clear values
+    for (auto& [id, moff] : r->input_mask_off)
+        up.copy_masks(L.masks_off, r->input_mask_gfirst[id], r->node(id).lanes, P.mask_v + moff, P.mask_m + moff,
+                      p == 0 ? P.mask_c + moff : nullptr);
+    up.finish();
+    P.ctx->alpha = L.alpha_share;
+    r->consumed = false;
 }
 
 void alloc_deals(spdz_run* r) {
@@ -1283,6 +1349,31 @@ void for_each_export(spdz_run* r, int p, F&& f) {
 
 extern "C" {
 
+int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t* out, uint64_t cap,
+                       uint64_t* n_regions) {
+    return guard([&] {  // host only: the planning step of spdz_run_create
+        need(nodes && n_nodes > 0 && n_regions, SPDZ_ERR_INVALID_ARGUMENT, "bad layout arguments");
+        spdz_run r;
+        r.nodes.assign(nodes, nodes + n_nodes);
+        r.opts.slice = slice ? slice : 262140;
+        plan_layout(&r);
+        uint64_t k = 0;
+        for (int kind = 0; kind < 2; ++kind)
+            for (auto& [id, reg] : kind == 0 ? r.scalar : r.matrix) {
+                if (out && k < cap) {
+                    uint64_t* o = out + 5 * k;
+                    o[0] = kind;
+                    o[1] = id;
+                    o[2] = kind == 0 ? reg.gbase : reg.base;
+                    o[3] = reg.stride;
+                    o[4] = reg.max_execs;
+                }
+                ++k;
+            }
+        *n_regions = k;
+    });
+}
+
 int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
                     const spdz_run_options_t* opts, spdz_run** out) {
     return guard([&] {
@@ -1379,6 +1470,14 @@ int spdz_run_destroy(spdz_run* r) {
             spdz_ctx_destroy(P.ctx);
         }
         delete r;
+    });
+}
+
+int spdz_run_load_store(spdz_run* r, int party, const char* path) {
+    return guard([&] {
+        need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
+        need(!r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "online phase in flight");
+        load_store(r, party, path);
     });
 }
 

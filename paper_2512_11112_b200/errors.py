@@ -56,6 +56,14 @@ class SliceTooSmall(SpdzError):
     code = 11
 
 
+class StoreFormatError(SpdzError):  # triple_store.hpp:23 (VersionMismatch / CorruptPayload)
+    code = 12
+
+
+class InsufficientTriples(SpdzError):  # preproc.cpp:182-201
+    code = 13
+
+
 class InvalidArgument(SpdzError, ValueError):
     code = 20
 
@@ -70,8 +78,8 @@ class DealerRejection(SpdzError):
 
 _BY_CODE = {c.code: c for c in (LaneMismatch, TripleShortage, BackendUnavailable, TripleExhausted,
                                 TripleShapeMismatch, MaskExhausted, PeerTimeout, LaneCountMismatch,
-                                MalformedShareMessage, MacCheckFailed, SliceTooSmall, InvalidArgument, CudaError,
-                                DealerRejection)}
+                                MalformedShareMessage, MacCheckFailed, SliceTooSmall, StoreFormatError,
+                                InsufficientTriples, InvalidArgument, CudaError, DealerRejection)}
 
 
 def from_code(code: int, msg: str) -> SpdzError:

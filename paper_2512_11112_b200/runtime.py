@@ -168,6 +168,28 @@ class RunReport:
         return self.output_digest_cached
 
 
+def triple_layout(graph: Graph, slice_: int = 262140) -> dict:
+    """The triple layout a run of `graph` uses (host only; preproc.cpp:124-163):
+    {"scalar"|"matrix": {node: (base, stride, max_execs)}}."""
+    nodes = graph.to_c()
+    n = C.c_uint64()
+    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, None, 0, C.byref(n)))
+    buf = (C.c_uint64 * (5 * max(n.value, 1)))()
+    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, buf, n.value, C.byref(n)))
+    out = {"scalar": {}, "matrix": {}}
+    for k in range(n.value):
+        kind, node, base, stride, execs = buf[5 * k:5 * k + 5]
+        out["scalar" if kind == 0 else "matrix"][int(node)] = (int(base), int(stride), int(execs))
+    return out
+
+
+def store_info(path) -> dict:
+    """Header and section counts of an MPCT triple-store file (validated; host only)."""
+    info = _lib.StoreInfo()
+    check(lib().spdz_store_inspect(str(path).encode(), C.byref(info)))
+    return {f: getattr(info, f) for f, _ in info._fields_}
+
+
 class LocalRun:
     """All n parties of one online phase, device resident.
 
@@ -223,6 +245,10 @@ class LocalRun:
 
     def deal(self, seed: int):
         check(lib().spdz_run_deal(self.h, seed))
+
+    def load_store(self, party: int, path):
+        """Party `party`'s preprocessing from the reference's MPCT store file (instead of deal)."""
+        check(lib().spdz_run_load_store(self.h, int(party), str(path).encode()))
 
     def bind_inputs(self, inputs: dict):
         for name, vals in inputs.items():

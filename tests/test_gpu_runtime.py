@@ -217,3 +217,63 @@ def test_streamed_run_equals_unsharded(gpu, kind, chunks):
     rep2 = sr.run({"x": x, "y": y})
     np.testing.assert_array_equal(rep2.outputs, rf.outputs)
     sr.close()
+
+
+def _store_case(case):
+    import json
+    from pathlib import Path
+    d = Path(__file__).resolve().parent / "golden" / "stores" / case
+    return d, json.loads((d / "layout.json").read_text())
+
+
+def _graph_and_inputs(spec):
+    from paper_2512_11112_b200 import chain_graph, linear_graph, reduce_graph
+    rng = np.random.default_rng(17)
+    rnd = lambda n: rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)
+    if spec[0] == "chain":
+        return chain_graph(spec[1], spec[2]), {"x": rnd(spec[2]), "y": rnd(spec[2])}
+    if spec[0] == "linear":
+        din, dout = spec[1], spec[2]
+        return linear_graph(din, dout), {"x": rnd(din), "W": rnd(din * dout), "b": rnd(dout)}
+    return reduce_graph(spec[1], spec[2]), {"x": rnd(spec[2])}
+
+
+@pytest.mark.parametrize("case", ["heavy_1000", "mixed_257_n3", "lin_96x80", "redmul_300_n3"])
+def test_reference_store_files_equal_gpu_dealer(gpu, case):
+    """Preprocessing loaded from the reference dealer tool's MPCT files
+    (spdz_run_load_store, one file per party) gives the same online phase as the GPU
+    dealer with the same seed: identical opened outputs and, for a fixed coin,
+    identical per-party MAC sigmas (so every triple and mask landed where deal() puts it)."""
+    from paper_2512_11112_b200 import LocalRun
+    d, m = _store_case(case)
+    g, inputs = _graph_and_inputs(m["graph"])
+    coin = 0x0123456789ABCDEF
+    res = []
+    for mode in ("store", "deal"):
+        r = LocalRun(g, m["parties"], slice_=m["slice"], dealer_seed=m["dealer_seed"], coin=coin)
+        if mode == "store":
+            for p, f in enumerate(m["files"]):
+                r.load_store(p, d / f)
+        else:
+            r.deal(m["dealer_seed"])
+        r.bind_inputs(inputs)
+        r.share_inputs()
+        rep = r.online()
+        res.append((rep.outputs.copy(), rep.sigmas))
+        r.close()
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
+    assert sum(res[0][1]) % P == 0
+
+
+def test_store_demand_and_party_checks(gpu):
+    from paper_2512_11112_b200 import LocalRun, chain_graph, errors
+    d, m = _store_case("heavy_1000")
+    r = LocalRun(chain_graph("heavy", 2000), 2)  # needs 8000 triples, the files hold 4000
+    with pytest.raises(errors.InsufficientTriples):
+        r.load_store(0, d / "triples_0.bin")
+    r.close()
+    r = LocalRun(chain_graph("heavy", 1000), 2)
+    with pytest.raises(errors.StoreFormatError, match="party 1"):
+        r.load_store(0, d / "triples_1.bin")
+    r.close()
