@@ -324,7 +324,8 @@ typedef struct spdz_run_options {
     uint64_t dealer_seed;  /* run_local dealer seed (runtime.hpp:54), default 1 */
     int32_t fixed_coin;    /* 1: use `coin` instead of the commit-reveal nonces (tests) */
     uint64_t coin;
-    int32_t use_graph;     /* reserved (CUDA-graph capture of the online phase) */
+    int32_t use_graph;     /* capture the online phase as one CUDA graph on its first run and replay it
+                            * (lane-parallel circuits with every party on one stream; else ignored) */
     int32_t devices[SPDZ_MAX_PARTIES]; /* device of each party (-1: device 0) */
     int32_t profile_kernels; /* 1: CUDA-event time every mask / combine / sigma launch */
     int32_t stream_per_party; /* 0 (default): parties on one device share its stream (kernels
@@ -423,6 +424,9 @@ int spdz_run_online_begin(spdz_run* run, int reuse_preprocessing);
  * H2D copies and the output D2H copy, shared by several runs so that their copies queue
  * in issue order (host-streamed execution).  NULL restores the run's own streams. */
 int spdz_run_set_copy_streams(spdz_run* run, void* h2d_stream, void* d2h_stream);
+/* The CUDA stream a local party's kernels run on (NULL if not local) — for callers
+ * that order their own work or timing events against the run. */
+void* spdz_run_party_stream(spdz_run* run, int party);
 /* First half of spdz_run_mac_check: agree on the coin and launch the sigma kernels
  * asynchronously; the next spdz_run_mac_check collects and verifies (its coin
  * arguments are then ignored). */

@@ -43,6 +43,12 @@ void launch_ok(cudaError_t e, const char* what) { cuda_check(e, what); }
 
 namespace spdzb200 {
 
+void set_alpha(spdz_ctx* ctx, uint32_t alpha) {
+    ctx->alpha = alpha;
+    device_guard(ctx);
+    cuda_check(launch_set_word(ctx->stream, ctx->d_alpha, alpha), "set alpha");
+}
+
 void device_guard(const spdz_ctx* ctx) { cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice"); }
 
 uint32_t host_reduce64(uint64_t v) { return fp_reduce64(v); }
@@ -171,6 +177,8 @@ int spdz_ctx_create(int device, int party, int n_parties, uint32_t alpha_share, 
             c->stream = c->own_stream;
             cuda_check(cudaMalloc(&c->d_acc, 16 * sizeof(unsigned long long)), "acc");
             cuda_check(cudaMalloc(&c->d_flag, sizeof(unsigned int)), "flag");
+            cuda_check(cudaMalloc(&c->d_alpha, 16), "alpha");
+            set_alpha(c, alpha_share);
         } catch (...) {
             delete c;
             throw;
@@ -190,6 +198,7 @@ int spdz_ctx_destroy(spdz_ctx* ctx) {
         ctx->pinned.release();
         if (ctx->d_acc) cudaFree(ctx->d_acc);
         if (ctx->d_flag) cudaFree(ctx->d_flag);
+        if (ctx->d_alpha) cudaFree(ctx->d_alpha);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         delete ctx;
     });

@@ -92,6 +92,7 @@ struct spdz_ctx {
     int party = 0;
     int n_parties = 2;
     uint32_t alpha = 0;
+    uint32_t* d_alpha = nullptr;          // device copy of alpha (read by graph-captured kernels)
     int sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -106,6 +107,8 @@ struct spdz_ctx {
 namespace spdzb200 {
 // throws Error; used by run.cu
 void device_guard(const spdz_ctx* ctx);
+// ctx->alpha and its device copy (stream-ordered on ctx->stream)
+void set_alpha(spdz_ctx* ctx, uint32_t alpha);
 uint32_t mac_sigma_impl(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n, uint64_t coin);
 void mac_sigma_launch(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n, uint64_t coin, int acc_slot);
 uint32_t mac_sigma_collect(spdz_ctx* ctx, int acc_slot);

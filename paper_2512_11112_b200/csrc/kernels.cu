@@ -92,7 +92,9 @@ struct MapUnroll {
 };
 
 template <int NI, int NO, class Op>
-__global__ void __launch_bounds__(kThreads) k_map(IO<NI, NO> io, uint64_t n, uint64_t n4, Op op) {
+__global__ void __launch_bounds__(kThreads) k_map(IO<NI, NO> io, uint64_t n, uint64_t n4, Op op_param) {
+    Op op = op_param;
+    op.prepare();  // e.g. alpha from device memory
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t g = t;
@@ -135,6 +137,15 @@ cudaError_t run_map(cudaStream_t s, const IO<NI, NO>& io, uint64_t n, Op op, int
 // ---- ops ----
 struct NoPeer {
     __device__ static constexpr bool is_peer(int) { return false; }
+    __device__ void prepare() {}
+};
+// alpha given by value, or (ap != null) read once per thread from device memory
+struct AlphaArg {
+    uint32_t alpha;
+    const uint32_t* ap;
+    __device__ void prepare() {
+        if (ap) alpha = __ldg(ap);
+    }
 };
 
 struct OpAdd : NoPeer {  // backend.cpp:25-37
@@ -153,9 +164,9 @@ struct OpSub : NoPeer {  // backend.cpp:39-51
 // spdz.cpp:35-75; inputs: xv, xm[, k].  KM: 0 vector k, 1 device scalar
 // broadcast (runtime.cpp:36-39), 2 immediate.
 template <int OPC, int KM>
-struct OpPublic : NoPeer {
+struct OpPublic : AlphaArg {
+    __device__ static constexpr bool is_peer(int) { return false; }
     int party;
-    uint32_t alpha;
     uint32_t kk;
     const uint32_t* kp;
     __device__ void operator()(const uint32_t* a, uint32_t* o) const {
@@ -178,9 +189,9 @@ struct OpPublic : NoPeer {
 };
 // spdz.cpp:70-75 share_of_public; input: [k] (KM as OpPublic)
 template <int KM>
-struct OpShareOfPublic : NoPeer {
+struct OpShareOfPublic : AlphaArg {
+    __device__ static constexpr bool is_peer(int) { return false; }
     int party;
-    uint32_t alpha;
     uint32_t kk;
     const uint32_t* kp;
     __device__ void operator()(const uint32_t* a, uint32_t* o) const {
@@ -200,9 +211,8 @@ struct OpMask : NoPeer {  // backend.cpp:53-65: in xv yv av bv -> d e
 // Fused open + Beaver combine.  Inputs: own_d, own_e, peer_d[NP], peer_e[NP],
 // a.v a.m b.v b.m c.v c.m.  Outputs: z.v z.m [open_d open_e].
 template <int NP, bool LOG>
-struct OpCombine {
+struct OpCombine : AlphaArg {
     int party;
-    uint32_t alpha;
     __device__ static constexpr bool is_peer(int k) { return k >= 2 && k < 2 + 2 * NP; }
     __device__ void operator()(const uint32_t* in, uint32_t* o) const {
         uint32_t d = in[0], e = in[1];
@@ -247,6 +257,7 @@ struct OpDiff : NoPeer {
 template <int NP>
 struct OpOpen {  // net.cpp:170-215
     __device__ static constexpr bool is_peer(int k) { return k >= 1; }
+    __device__ void prepare() {}
     __device__ void operator()(const uint32_t* in, uint32_t* o) const {
         uint32_t acc = in[0];
 #pragma unroll
@@ -258,7 +269,8 @@ struct OpOpen {  // net.cpp:170-215
 template <int NP>
 cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, const uint32_t* const* pd,
                        const uint32_t* const* pe, const uint32_t* const tri[6], int party, uint32_t alpha,
-                       uint32_t* zv, uint32_t* zm, uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms) {
+                       uint32_t* zv, uint32_t* zm, uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms,
+                       const uint32_t* alpha_dev) {
     constexpr int NI = 8 + 2 * NP;
     if (open_d) {
         IO<NI, 4> io;
@@ -273,7 +285,7 @@ cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, c
         io.out[1] = zm;
         io.out[2] = open_d;
         io.out[3] = open_e;
-        return run_map(s, io, n, OpCombine<NP, true>{party, alpha}, sms);
+        return run_map(s, io, n, OpCombine<NP, true>{{alpha, alpha_dev}, party}, sms);
     }
     IO<NI, 2> io;
     io.in[0] = od;
@@ -285,7 +297,7 @@ cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, c
     for (int k = 0; k < 6; ++k) io.in[2 + 2 * NP + k] = tri[k];
     io.out[0] = zv;
     io.out[1] = zm;
-    return run_map(s, io, n, OpCombine<NP, false>{party, alpha}, sms);
+    return run_map(s, io, n, OpCombine<NP, false>{{alpha, alpha_dev}, party}, sms);
 }
 
 template <int NP>
@@ -798,6 +810,10 @@ __global__ void __launch_bounds__(kThreads) k_tile_e(const uint32_t* __restrict_
         out[i] = fp_sub(xv[i % din], bv[i]);
 }
 
+__global__ void k_set_word(uint32_t* p, uint32_t v) {
+    if (threadIdx.x == 0) *p = v;
+}
+
 __global__ void k_xor_word(uint32_t* p, uint32_t mask) {
     if (threadIdx.x == 0) *p ^= mask;
 }
@@ -815,34 +831,34 @@ cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const u
 
 template <int OPC>
 static cudaError_t public_dispatch(cudaStream_t s, const uint32_t* xv, const uint32_t* xm, const uint32_t* k, int km,
-                                   uint32_t kk, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm, uint64_t n,
-                                   int sms) {
+                                   uint32_t kk, int party, uint32_t alpha, const uint32_t* ap, uint32_t* zv,
+                                   uint32_t* zm, uint64_t n, int sms) {
     if (km == 0) {
         IO<3, 2> io{{xv, xm, k}, {zv, zm}};
-        return run_map(s, io, n, OpPublic<OPC, 0>{{}, party, alpha, 0u, k}, sms);
+        return run_map(s, io, n, OpPublic<OPC, 0>{{alpha, ap}, party, 0u, k}, sms);
     }
     IO<2, 2> io{{xv, xm}, {zv, zm}};
-    if (km == 1) return run_map(s, io, n, OpPublic<OPC, 1>{{}, party, alpha, 0u, k}, sms);
-    return run_map(s, io, n, OpPublic<OPC, 2>{{}, party, alpha, kk, k}, sms);
+    if (km == 1) return run_map(s, io, n, OpPublic<OPC, 1>{{alpha, ap}, party, 0u, k}, sms);
+    return run_map(s, io, n, OpPublic<OPC, 2>{{alpha, ap}, party, kk, k}, sms);
 }
 
 cudaError_t launch_public(cudaStream_t s, int op, const uint32_t* xv, const uint32_t* xm, const uint32_t* k,
                           bool k_bcast, uint32_t k_imm, bool k_is_imm, int party, uint32_t alpha, uint32_t* zv,
-                          uint32_t* zm, uint64_t n, int sms) {
+                          uint32_t* zm, uint64_t n, int sms, const uint32_t* ap) {
     const int km = k_is_imm ? 2 : (k_bcast ? 1 : 0);
     switch (op) {
-        case 0: return public_dispatch<0>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
-        case 1: return public_dispatch<1>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
-        case 2: return public_dispatch<2>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
-        case 3: return public_dispatch<3>(s, xv, xm, k, km, k_imm, party, alpha, zv, zm, n, sms);
+        case 0: return public_dispatch<0>(s, xv, xm, k, km, k_imm, party, alpha, ap, zv, zm, n, sms);
+        case 1: return public_dispatch<1>(s, xv, xm, k, km, k_imm, party, alpha, ap, zv, zm, n, sms);
+        case 2: return public_dispatch<2>(s, xv, xm, k, km, k_imm, party, alpha, ap, zv, zm, n, sms);
+        case 3: return public_dispatch<3>(s, xv, xm, k, km, k_imm, party, alpha, ap, zv, zm, n, sms);
         case 4: {
             if (km == 0) {
                 IO<1, 2> io{{k}, {zv, zm}};
-                return run_map(s, io, n, OpShareOfPublic<0>{{}, party, alpha, 0u, k}, sms);
+                return run_map(s, io, n, OpShareOfPublic<0>{{alpha, ap}, party, 0u, k}, sms);
             }
             IO<0, 2> io{{nullptr}, {zv, zm}};
-            if (km == 1) return run_map(s, io, n, OpShareOfPublic<1>{{}, party, alpha, 0u, k}, sms);
-            return run_map(s, io, n, OpShareOfPublic<2>{{}, party, alpha, k_imm, k}, sms);
+            if (km == 1) return run_map(s, io, n, OpShareOfPublic<1>{{alpha, ap}, party, 0u, k}, sms);
+            return run_map(s, io, n, OpShareOfPublic<2>{{alpha, ap}, party, k_imm, k}, sms);
         }
     }
     return cudaErrorInvalidValue;
@@ -857,10 +873,11 @@ cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* 
 cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
                                   const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
                                   const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
-                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms) {
+                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms, const uint32_t* alpha_dev) {
     switch (n_peers) {
 #define CASE(NP) \
-    case NP: return combine_np<NP>(s, own_d, own_e, peer_d, peer_e, tri, party, alpha, zv, zm, open_d, open_e, n, sms);
+    case NP:     \
+        return combine_np<NP>(s, own_d, own_e, peer_d, peer_e, tri, party, alpha, zv, zm, open_d, open_e, n, sms, alpha_dev);
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
@@ -1044,6 +1061,11 @@ cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv
     const uint64_t total = (uint64_t)din * n_tiles;
     if (total == 0) return cudaSuccess;
     k_tile_e<<<grid_for(total, sms), kThreads, 0, s>>>(xv, bv, din, total, out);
+    return launched();
+}
+
+cudaError_t launch_set_word(cudaStream_t s, uint32_t* p, uint32_t v) {
+    k_set_word<<<1, 32, 0, s>>>(p, v);
     return launched();
 }
 

@@ -33,9 +33,11 @@ extern unsigned long long g_kernel_launches;  // evidence counter
 cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
                            const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms);
 // op: 0 add_public 1 sub_public 2 rsub_public 3 mul_public 4 share_of_public (xv/xm unused as inputs)
+// alpha_dev (optional): read alpha from device memory instead of the `alpha` argument
+// (kernels captured in a CUDA graph stay valid when the MAC key share changes)
 cudaError_t launch_public(cudaStream_t s, int op, const uint32_t* xv, const uint32_t* xm, const uint32_t* k,
                           bool k_bcast, uint32_t k_imm, bool k_is_imm, int party, uint32_t alpha, uint32_t* zv,
-                          uint32_t* zm, uint64_t n, int sms);
+                          uint32_t* zm, uint64_t n, int sms, const uint32_t* alpha_dev = nullptr);
 // backend.cpp:53-65
 cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* yv, const uint32_t* av,
                             const uint32_t* bv, uint32_t* d, uint32_t* e, uint64_t n, int sms);
@@ -43,7 +45,9 @@ cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* 
 cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
                                   const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
                                   const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
-                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms);
+                                  uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms,
+                                  const uint32_t* alpha_dev = nullptr);
+cudaError_t launch_set_word(cudaStream_t s, uint32_t* p, uint32_t v);
 // net.cpp:170-215
 cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, int n_peers,
                             uint32_t* out, uint64_t n, int sms);

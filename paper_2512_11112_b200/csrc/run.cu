@@ -163,6 +163,14 @@ struct spdz_run {
     cudaEvent_t ev_h2d = nullptr, ev_out = nullptr;
     bool mac_launched = false;      // spdz_run_mac_check_launch issued the sigma kernels
     uint64_t mac_coin = 0;
+    // CUDA graph of the online phase (opts.use_graph): captured on the first phase, replayed
+    // after; the host-side products of node execution are saved with it
+    cudaGraphExec_t online_graph = nullptr;
+    std::vector<std::vector<spdz_mac_segment_t>> graph_maclog;
+    uint64_t graph_exchanged = 0, graph_launches = 0;
+    // share_inputs: constants uploaded once, reduced public inputs kept alive for async copies
+    bool consts_uploaded = false;
+    std::map<uint32_t, std::vector<uint32_t>> pub_reduced;
     bool in_flight = false;
     bool any_remote = false;
     uint32_t seq = 0;               // phase sequence number written to / awaited on opening flags
@@ -493,7 +501,7 @@ void deal(spdz_run* r, uint64_t seed) {
     uint32_t alpha_sh[SPDZ_MAX_PARTIES], alpha;
     dealer_alpha(n, seed, alpha_sh, &alpha);
     for (int p = 0; p < n; ++p)
-        if (r->parties[p].local) r->parties[p].ctx->alpha = alpha_sh[p];
+        if (r->parties[p].local) set_alpha(r->parties[p].ctx, alpha_sh[p]);
     const uint64_t S = r->scalar_total, M = r->mask_total;
     for (auto& [device, dd] : r->deals) {
         int p0 = -1;
@@ -620,7 +628,7 @@ void load_store(spdz_run* r, int p, const char* path) {
         up.copy_masks(L.masks_off, r->input_mask_gfirst[id], r->node(id).lanes, P.mask_v + moff, P.mask_m + moff,
                       p == 0 ? P.mask_c + moff : nullptr);
     up.finish();
-    P.ctx->alpha = L.alpha_share;
+    set_alpha(P.ctx, L.alpha_share);
     r->consumed = false;
 }
 
@@ -775,7 +783,7 @@ struct Exec {
             im = o.m;
         }
         lk(launch_public(c->stream, op, iv, im, pb.pub, pb.lanes != L, 0u, false, c->party, c->alpha, o.v, o.m, L,
-                         c->sms),
+                         c->sms, c->d_alpha),
            "public op");
     }
 
@@ -801,7 +809,7 @@ struct Exec {
             im = o.m;
         }
         lk(launch_public(c->stream, 3, iv, im, pb.pub, pb.lanes != L, 0u, false, c->party, c->alpha, o.v, o.m, L,
-                         c->sms),
+                         c->sms, c->d_alpha),
            "mul_public");
     }
 
@@ -860,7 +868,7 @@ struct Exec {
             for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
             const int tk = tbegin(p);
             lk(launch_beaver_combine(S(r, p), st.payload, st.payload + L, pd, pe, k, tri, P.ctx->party, P.ctx->alpha,
-                                     st.out.v, st.out.m, st.opened, st.opened + L, L, SMS(r, p)),
+                                     st.out.v, st.out.m, st.opened, st.opened + L, L, SMS(r, p), P.ctx->d_alpha),
                "k_combine");
             // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
             tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
@@ -929,7 +937,8 @@ struct Exec {
                 const uint32_t* tri[6];
                 for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
                 lk(launch_beaver_combine(S(r, p), lv.payload, lv.payload + pairs, pd, pe, k, tri, P.ctx->party,
-                                         P.ctx->alpha, lv.zv, lv.zm, lv.opened, lv.opened + pairs, pairs, SMS(r, p)),
+                                         P.ctx->alpha, lv.zv, lv.zm, lv.opened, lv.opened + pairs, pairs, SMS(r, p),
+                                         P.ctx->d_alpha),
                    "combine");
                 P.maclog.push_back({lv.opened, lv.xm, P.pool[1] + off, pairs, 0, batch, 0, 0});
                 P.maclog.push_back({lv.opened + pairs, lv.ym, P.pool[3] + off, pairs, 0, batch, pairs, 0});
@@ -1296,24 +1305,39 @@ void share_inputs(spdz_run* r) {
             auto it = r->inputs.find(id);
             need(it != r->inputs.end(), SPDZ_ERR_INVALID_ARGUMENT,
                  "ShapeMismatch: missing public input " + std::to_string(id));
-            std::vector<uint32_t> red(it->second.size());
+            auto& red = r->pub_reduced[id];  // lives until the next bind: the copies are asynchronous
+            red.resize(it->second.size());
             for (size_t i = 0; i < red.size(); ++i) red[i] = it->second[i] % kP;
             for (int p = 0; p < r->n; ++p) {
-            if (!r->parties[p].local) continue;
+                if (!r->parties[p].local) continue;
                 dev(r, p);
-                lk(cudaMemcpy(r->parties[p].ns[id].out.pub, red.data(), red.size() * 4, cudaMemcpyHostToDevice),
+                lk(cudaMemcpyAsync(r->parties[p].ns[id].out.pub, red.data(), red.size() * 4, cudaMemcpyHostToDevice,
+                                   S(r, p)),
                    "H2D pub");
             }
         }
-        if (n.kind == SPDZ_NODE_CONST) {
+        if (n.kind == SPDZ_NODE_CONST && !r->consts_uploaded) {  // constants never change: once per run
             const uint32_t v = n.const_val % kP;
             for (int p = 0; p < r->n; ++p) {
-            if (!r->parties[p].local) continue;
+                if (!r->parties[p].local) continue;
                 dev(r, p);
                 lk(cudaMemcpy(r->parties[p].ns[id].out.pub, &v, 4, cudaMemcpyHostToDevice), "H2D const");
             }
         }
     }
+    r->consts_uploaded = true;
+}
+
+// The online phase may run as one CUDA graph: every party local on one shared stream,
+// a lane-parallel circuit (no linear layers or reductions, whose launchers size scratch
+// buffers and grids at call time), no fault injection, no per-kernel timing.
+bool graphable(spdz_run* r) {
+    if (!r->opts.use_graph || r->any_remote || r->opts.profile_kernels || !r->faults.empty()) return false;
+    for (int p = 0; p < r->n; ++p)
+        if (!r->parties[p].local || S(r, p) != S(r, 0)) return false;
+    for (const auto& n : r->nodes)
+        if (n.kind == SPDZ_NODE_LINEAR || n.kind == SPDZ_NODE_REDUCE_ADD || n.kind == SPDZ_NODE_REDUCE_MUL) return false;
+    return true;
 }
 
 }  // namespace
@@ -1458,6 +1482,7 @@ int spdz_run_destroy(spdz_run* r) {
             cudaStreamSynchronize(r->copy_stream);
             cudaStreamDestroy(r->copy_stream);
         }
+        if (r->online_graph) cudaGraphExecDestroy(r->online_graph);
         for (auto e : r->kt.pool) cudaEventDestroy(e);
         for (size_t i = 0; i < r->allocs.size(); ++i) {
             cudaSetDevice(r->alloc_dev[i]);
@@ -1546,9 +1571,41 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         }
         r->kt.used = 0;
         r->kt.recs.clear();
-        Exec ex{r};
-        ex.run_nodes();
-        ex.open_root();
+        if (graphable(r)) {
+            cudaStream_t s = S(r, 0);
+            dev(r, 0);
+            if (!r->online_graph) {  // capture once: the same kernels, pointers and events every phase
+                const uint64_t l0 = g_kernel_launches;
+                cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "begin capture");
+                cudaGraph_t g = nullptr;
+                try {
+                    Exec ex{r};
+                    ex.run_nodes();
+                    ex.open_root();
+                } catch (...) {
+                    cudaStreamEndCapture(s, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                cuda_check(cudaStreamEndCapture(s, &g), "end capture");
+                cudaError_t e = cudaGraphInstantiate(&r->online_graph, g, 0);
+                cudaGraphDestroy(g);
+                cuda_check(e, "cudaGraphInstantiate");
+                r->graph_launches = g_kernel_launches - l0;
+                r->graph_exchanged = r->exchanged;
+                r->graph_maclog.clear();
+                for (auto& P : r->parties) r->graph_maclog.push_back(P.maclog);
+            } else {
+                g_kernel_launches += r->graph_launches;
+                r->exchanged = r->graph_exchanged;
+                for (int p = 0; p < r->n; ++p) r->parties[p].maclog = r->graph_maclog[p];
+            }
+            lk(cudaGraphLaunch(r->online_graph, s), "cudaGraphLaunch");
+        } else {
+            Exec ex{r};
+            ex.run_nodes();
+            ex.open_root();
+        }
         r->consumed = true;
         r->in_flight = true;
         // opened outputs to host on a copy stream, overlapping the MAC check
@@ -1570,6 +1627,11 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
            "D2H out");
         lk(cudaEventRecord(r->ev_out, out_stream), "record out");
     });
+}
+
+void* spdz_run_party_stream(spdz_run* r, int party) {
+    if (!r || party < 0 || party >= r->n || !r->parties[party].local) return nullptr;
+    return r->parties[party].ctx->stream;
 }
 
 int spdz_run_set_copy_streams(spdz_run* r, void* h2d_stream, void* d2h_stream) {
@@ -1777,6 +1839,10 @@ int spdz_run_inject_bitflip(spdz_run* r, uint32_t node, int sender, int receiver
             st.shadow = r->alloc(receiver, words);
         }
         r->faults.push_back({node, sender, receiver, word, bit});
+        if (r->online_graph) {  // the captured phase has no tampering step
+            cudaGraphExecDestroy(r->online_graph);
+            r->online_graph = nullptr;
+        }
     });
 }
 

@@ -198,7 +198,7 @@ class LocalRun:
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
                  stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
-                 single_party: int | None = None):
+                 single_party: int | None = None, use_graph: bool = False):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -207,6 +207,7 @@ class LocalRun:
         o.coin = coin or 0
         o.profile_kernels = int(profile_kernels)
         o.stream_per_party = int(stream_per_party)
+        o.use_graph = int(use_graph)  # online phase captured once as a CUDA graph, then replayed
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
         o.external_mac_verify = int(external_mac_verify or single_party is not None)
@@ -340,21 +341,29 @@ class StreamedRun:
     split into `chunks` exact lane shards (each a LocalRun with shard=(offset, total),
     i.e. exactly its slice of the global preprocessing and global MAC ranks), each on
     its own CUDA streams, so the H2D of chunk c+1 and the D2H of chunk c-1 overlap
-    the kernels of chunk c.  One MAC check covers all chunks: the coin is agreed
-    after every opening and the per-party sigma partials are summed (runtime.cpp:467-506)."""
+    the kernels of chunk c.
+
+    MAC check (runtime.cpp:467-506): ``mac="joint"`` — one check over every chunk's
+    openings (the coin agreed after all of them, per-party sigma partials summed: the
+    unsharded run's sigmas); ``mac="per_chunk"`` (default) — each chunk is checked on
+    its own as soon as its openings are enqueued (its own coin, its own commit/verify),
+    so its sigma kernels overlap the next chunk's transfers instead of all running
+    after the last opening.  Opened outputs are identical either way."""
 
     def __init__(self, graph_fn, n_parties: int, total: int, chunks: int = 4, dealer_seed: int = 1,
-                 coin: int | None = None, devices=None):
-        self.n, self.total, self.coin = n_parties, total, coin
-        base, extra = divmod(total, chunks)
-        self.ranges = []
-        off = 0
-        for c in range(chunks):
-            L = base + (1 if c < extra else 0)
-            self.ranges.append((off, L))
-            off += L
+                 coin: int | None = None, devices=None, weights=None, mac: str = "per_chunk"):
+        """`weights` (optional, one per chunk) sizes the chunks proportionally, e.g. a small
+        first chunk so the kernels start after a short first copy."""
+        assert mac in ("joint", "per_chunk")
+        self.n, self.total, self.coin, self.mac = n_parties, total, coin, mac
+        w = list(weights) if weights is not None else [1] * chunks
+        assert len(w) == chunks and all(x > 0 for x in w)
+        cuts = [round(total * sum(w[:c]) / sum(w)) for c in range(chunks + 1)]
+        cuts = [c - c % 4 if 0 < c < total else c for c in cuts]  # 16-byte aligned chunk starts
+        self.ranges = [(cuts[c], cuts[c + 1] - cuts[c]) for c in range(chunks)]
+        assert all(L > 0 for _, L in self.ranges), "too many chunks for this size"
         self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
-                              shard=(o, total), external_mac_verify=True) for o, L in self.ranges]
+                              shard=(o, total), external_mac_verify=True, use_graph=True) for o, L in self.ranges]
         # one H2D and one D2H stream shared by all chunks: copies complete in chunk order, so
         # chunk c computes while chunk c+1's inputs cross PCIe (separate per-chunk copy
         # streams would interleave the transfers and delay every chunk to the end of all H2D)
@@ -383,28 +392,55 @@ class StreamedRun:
         its outputs array is the bound output buffer (no host copy)."""
         if getattr(self, "_out", None) is None:
             self.bind_output(np.empty(self.total, np.uint32))
-        for r, (o, L) in zip(self.runs, self.ranges):
+        per_chunk = self.mac == "per_chunk"
+        coin = None
+        reps = [None] * len(self.runs)
+        lag = 2  # per-chunk mode: collect chunk c-2's check while the GPU works on c-1 and c
+        for c, (r, (o, L)) in enumerate(zip(self.runs, self.ranges)):
             r.bind_inputs({k: v[o:o + L] for k, v in inputs.items()})
             r.share_inputs()
             r.online_begin()
-        coin = self.coin
-        if coin is None:  # parties' nonces, revealed after all openings, chained (runtime.cpp:474-489)
-            coin = 0
-            for nz in (int.from_bytes(os.urandom(8), "little") for _ in range(self.n)):
-                coin = lib().spdz_fnv1a64((C.c_uint64 * 1)(nz), 8, coin)
-        for r in self.runs:  # every chunk's sigma kernels in flight before the first collect
-            r.mac_check_launch(coin)
-        reps = [r.mac_check() for r in self.runs]
+            if per_chunk:  # this chunk's openings are enqueued: its coin, its sigma kernels
+                coin = self._coin()
+                r.mac_check_launch(coin)
+                if c >= lag:
+                    reps[c - lag] = self._collect(self.runs[c - lag], per_chunk)
+        if not per_chunk:
+            coin = self._coin()
+            for r in self.runs:  # every chunk's sigma kernels in flight before the first collect
+                r.mac_check_launch(coin)
+        for c, r in enumerate(self.runs):
+            if reps[c] is None:
+                reps[c] = self._collect(r, per_chunk)
+        if not per_chunk:
+            self._verify([sum(rep.sigmas[p] for rep in reps) for p in range(self.n)])
         sig = [sum(rep.sigmas[p] for rep in reps) % 4294967291 for p in range(self.n)]
-        nonces = [int.from_bytes(os.urandom(8), "little") for _ in range(self.n)]
-        commits = [lib().spdz_commit_sigma(s, nz) for s, nz in zip(sig, nonces)]
-        rc = lib().spdz_verify_sigmas((C.c_uint32 * self.n)(*sig), (C.c_uint64 * self.n)(*nonces),
-                                      (C.c_uint64 * self.n)(*commits), self.n)
-        check(rc)
         return RunReport(self._out, max(rep.online_ms for rep in reps), max(rep.online_device_ms for rep in reps),
                          sum(rep.scalar_triples_consumed for rep in reps), 0,
                          sum(rep.bytes_exchanged for rep in reps), None,
                          sum(rep.kernel_launches for rep in reps), sig, coin, None)
+
+    def _collect(self, r, verify: bool):
+        rep = r.mac_check()
+        if verify:
+            self._verify(rep.sigmas)
+        return rep
+
+    def _verify(self, sigmas):
+        """commit / reveal / verify (spdz.cpp:140-158) of one checked batch of openings."""
+        sig = [x % 4294967291 for x in sigmas]
+        nonces = [int.from_bytes(os.urandom(8), "little") for _ in range(self.n)]
+        commits = [lib().spdz_commit_sigma(x, nz) for x, nz in zip(sig, nonces)]
+        check(lib().spdz_verify_sigmas((C.c_uint32 * self.n)(*sig), (C.c_uint64 * self.n)(*nonces),
+                                       (C.c_uint64 * self.n)(*commits), self.n))
+
+    def _coin(self) -> int:
+        if self.coin is not None:
+            return self.coin
+        coin = 0  # parties' nonces, revealed after the openings, chained (runtime.cpp:474-489)
+        for nz in (int.from_bytes(os.urandom(8), "little") for _ in range(self.n)):
+            coin = lib().spdz_fnv1a64((C.c_uint64 * 1)(nz), 8, coin)
+        return coin
 
 
 def run_local(graph: Graph, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,

@@ -15,8 +15,10 @@ rng = np.random.default_rng(0)
 x = torch.from_numpy(rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)).pin_memory().numpy()
 y = torch.from_numpy(rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)).pin_memory().numpy()
 out = torch.empty(n, dtype=torch.uint32).pin_memory().numpy()
-for chunks in [int(c) for c in (sys.argv[1:] or ["1", "2", "4", "8"])]:
-    sr = StreamedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=chunks)
+for spec in (sys.argv[1:] or ["1", "2", "4", "8"]):
+    weights = [float(w) for w in spec.split(",")] if "," in spec else None
+    chunks = len(weights) if weights else int(spec)
+    sr = StreamedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=chunks, weights=weights)
     sr.bind_output(out)
     for k in range(4):
         sr.deal(10 + k)
@@ -36,7 +38,7 @@ for chunks in [int(c) for c in (sys.argv[1:] or ["1", "2", "4", "8"])]:
         t.append(time.perf_counter())
         d = np.diff(t) * 1e3
         if k:
-            print(f"chunks={chunks}: total {1e3 * (t[-1] - t[0]):.2f} ms | per-chunk bind/share/begin "
+            print(f"chunks={spec}: total {1e3 * (t[-1] - t[0]):.2f} ms | per-chunk bind/share/begin "
                   f"{np.round(d[:-2].reshape(-1, 3).mean(0), 3)} | issue all {1e3 * (t[-2] - t[0]):.2f} ms"
                   f" | mac_check all {d[-1]:.2f} ms", flush=True)
     sr.close()

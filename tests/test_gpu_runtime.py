@@ -206,7 +206,7 @@ def test_streamed_run_equals_unsharded(gpu, kind, chunks):
     full.share_inputs()
     rf = full.online()
     full.close()
-    sr = StreamedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks, coin=coin)
+    sr = StreamedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks, coin=coin, mac="joint")
     out = np.zeros(n, np.uint32)
     sr.bind_output(out)
     rep = sr.run({"x": x, "y": y})
@@ -216,6 +216,12 @@ def test_streamed_run_equals_unsharded(gpu, kind, chunks):
     sr.deal(7)  # fresh preprocessing, same answer, MAC check verifies internally
     rep2 = sr.run({"x": x, "y": y})
     np.testing.assert_array_equal(rep2.outputs, rf.outputs)
+    sr.close()
+    # per-chunk MAC checks (the default): same outputs, every chunk's check verifies
+    sr = StreamedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks)
+    rep3 = sr.run({"x": x, "y": y})
+    np.testing.assert_array_equal(rep3.outputs, rf.outputs)
+    assert sum(rep3.sigmas) % P == 0
     sr.close()
 
 
@@ -277,3 +283,29 @@ def test_store_demand_and_party_checks(gpu):
     with pytest.raises(errors.StoreFormatError, match="party 1"):
         r.load_store(0, d / "triples_1.bin")
     r.close()
+
+
+@pytest.mark.parametrize("kind", ["heavy", "mixed", "light"])
+def test_graph_replayed_online_phase(gpu, kind):
+    """use_graph: the online phase captured once as a CUDA graph and replayed gives, phase
+    after phase (fresh preprocessing each time), the same node shares, outputs and sigmas
+    as direct launches."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    n, coin = 3001, 0x5EED
+    x, y = O.rand_field_vec(n, 3), O.rand_field_vec(n, 4)
+    runs = [LocalRun(chain_graph(kind, n), 2, coin=coin, use_graph=g) for g in (False, True)]
+    for seed in (3, 4, 5):
+        res = []
+        for r in runs:
+            r.deal(seed)
+            r.bind_inputs({"x": x, "y": y})
+            r.share_inputs()
+            rep = r.online()
+            res.append((rep.outputs.copy(), rep.sigmas, r.node_share_host(1, 9), rep.kernel_launches))
+        np.testing.assert_array_equal(res[0][0], res[1][0])
+        assert res[0][1] == res[1][1]
+        np.testing.assert_array_equal(res[0][2][0], res[1][2][0])
+        np.testing.assert_array_equal(res[0][2][1], res[1][2][1])
+        assert res[0][3] == res[1][3]
+    for r in runs:
+        r.close()
