@@ -88,7 +88,7 @@ void mac_sigma_launch(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n,
         for (uint32_t i = 0; i < tab.n; ++i) {
             const auto& sg = segs[base + i];
             need(sg.len == 0 || (sg.value && sg.mac_a), SPDZ_ERR_INVALID_ARGUMENT, "null MAC segment");
-            tab.seg[i] = MacSegDev{sg.value, sg.mac_a, sg.mac_b, sg.len, sg.j0};
+            tab.seg[i] = MacSegDev{{sg.value}, {sg.mac_a}, {sg.mac_b}, sg.len, sg.j0};
             tab.rec0[i] = recs;
             recs += sg.len;
         }

@@ -418,6 +418,12 @@ __device__ __forceinline__ void sigma_rec4(uint64_t z, const uint4& x, const uin
     z_step(zl, zh);
     sigma_rec(zl, zh, x.w, m.w, sm, sx, kc);
 }
+template <int NP>
+struct SigmaOut {
+    uint32_t alpha[NP];
+    unsigned long long* acc[NP];
+};
+
 __device__ __forceinline__ uint4 sub4(const uint4& a, const uint4& b) {
     return make_uint4(fp_sub(a.x, b.x), fp_sub(a.y, b.y), fp_sub(a.z, b.z), fp_sub(a.w, b.w));
 }
@@ -434,9 +440,18 @@ __device__ __forceinline__ uint4 sub4(const uint4& a, const uint4& b) {
 #ifndef SPDZ_SIGMA_MINB
 #define SPDZ_SIGMA_MINB 4
 #endif
-__global__ void __launch_bounds__(kThreads, SPDZ_SIGMA_MINB) k_mac_sigma(MacTable tab, uint64_t coin, uint32_t alpha,
-                                                                         SigConsts kc, unsigned long long* acc) {
-    Acc96 sm, sx;
+template <int NP>
+struct SigmaMinBlocks {
+    static constexpr int value = NP == 1 ? SPDZ_SIGMA_MINB : 3;
+};
+
+// NP parties (NP = 1: one party's log; NP = 2: both local parties of a 2-party run,
+// whose logs have the same record ranks) — r_j is computed once per record and
+// applied to every party's (x_j, m_j), so the 2-party pass costs ~60% of two passes.
+template <int NP>
+__global__ void __launch_bounds__(kThreads, SigmaMinBlocks<NP>::value)
+    k_mac_sigma(MacTableT<NP> tab, uint64_t coin, SigmaOut<NP> so, SigConsts kc) {
+    Acc96 sm[NP], sx[NP];
     const uint64_t total = tab.rec0[tab.n];
     const uint64_t units = (total + kSigmaAlign - 1) / kSigmaAlign;
     const uint64_t lo_u = units * blockIdx.x / gridDim.x, hi_u = units * (blockIdx.x + 1) / gridDim.x;
@@ -444,55 +459,88 @@ __global__ void __launch_bounds__(kThreads, SPDZ_SIGMA_MINB) k_mac_sigma(MacTabl
     uint32_t seg = 0;
     while (seg < tab.n && tab.rec0[seg + 1] <= lo) ++seg;
     for (uint64_t pos = lo; pos < hi && seg < tab.n; ++seg) {
-        const MacSegDev sg = tab.seg[seg];
+        const MacSegT<NP>& sg = tab.seg[seg];
         const uint64_t s0 = tab.rec0[seg], s1 = tab.rec0[seg + 1] < hi ? tab.rec0[seg + 1] : hi;
         if (s1 <= pos) continue;
         const uint64_t start = pos - s0;
         const uint32_t count = (uint32_t)(s1 - pos);  // < 2^31 (launcher)
         pos = s1;
-        const uint32_t* xv = sg.value + start;
-        const uint32_t* ma = sg.mac_a + start;
-        const uint32_t* mb = sg.mac_b ? sg.mac_b + start : nullptr;
+        const uint32_t *xv[NP], *ma[NP], *mb[NP];
+        uintptr_t al = 0;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            xv[p] = sg.value[p] + start;
+            ma[p] = sg.mac_a[p] + start;
+            mb[p] = sg.mac_b[p] ? sg.mac_b[p] + start : nullptr;
+            al |= reinterpret_cast<uintptr_t>(xv[p]) | reinterpret_cast<uintptr_t>(ma[p]) |
+                  reinterpret_cast<uintptr_t>(mb[p]);
+        }
+        const bool has_b = mb[0] != nullptr;
         const uint64_t z0 = coin + (sg.j0 + start + 1) * kGamma;  // z of record 0 of the piece
-        const bool v4 = ((reinterpret_cast<uintptr_t>(xv) | reinterpret_cast<uintptr_t>(ma) |
-                          reinterpret_cast<uintptr_t>(mb)) & 15u) == 0;
         uint32_t done = 0;
-        if (v4) {
-            const uint4* x4 = reinterpret_cast<const uint4*>(xv);
-            const uint4* a4 = reinterpret_cast<const uint4*>(ma);
-            const uint4* b4 = reinterpret_cast<const uint4*>(mb);
+        if ((al & 15u) == 0) {
             const uint32_t n4 = count / 4;
             uint32_t g = threadIdx.x;
-            for (; g + blockDim.x < n4; g += 2 * blockDim.x) {  // 8 records in flight per thread
-                const uint32_t g2 = g + blockDim.x;
-                const uint4 x1 = __ldcs(x4 + g), x2 = __ldcs(x4 + g2);
-                uint4 m1 = __ldcs(a4 + g), m2 = __ldcs(a4 + g2);
-                if (mb) {
-                    m1 = sub4(m1, __ldcs(b4 + g));
-                    m2 = sub4(m2, __ldcs(b4 + g2));
+            if (NP == 1) {
+                const uint4* x4 = reinterpret_cast<const uint4*>(xv[0]);
+                const uint4* a4 = reinterpret_cast<const uint4*>(ma[0]);
+                const uint4* b4 = reinterpret_cast<const uint4*>(mb[0]);
+                for (; g + blockDim.x < n4; g += 2 * blockDim.x) {  // 8 records in flight per thread
+                    const uint32_t g2 = g + blockDim.x;
+                    const uint4 x1 = __ldcs(x4 + g), x2 = __ldcs(x4 + g2);
+                    uint4 m1 = __ldcs(a4 + g), m2 = __ldcs(a4 + g2);
+                    if (has_b) {
+                        m1 = sub4(m1, __ldcs(b4 + g));
+                        m2 = sub4(m2, __ldcs(b4 + g2));
+                    }
+                    sigma_rec4(z0 + (uint64_t)(4 * g) * kGamma, x1, m1, sm[0], sx[0], kc);
+                    sigma_rec4(z0 + (uint64_t)(4 * g2) * kGamma, x2, m2, sm[0], sx[0], kc);
                 }
-                sigma_rec4(z0 + (uint64_t)(4 * g) * kGamma, x1, m1, sm, sx, kc);
-                sigma_rec4(z0 + (uint64_t)(4 * g2) * kGamma, x2, m2, sm, sx, kc);
             }
             for (; g < n4; g += blockDim.x) {
-                const uint4 x = __ldcs(x4 + g);
-                uint4 m = __ldcs(a4 + g);
-                if (mb) m = sub4(m, __ldcs(b4 + g));
-                sigma_rec4(z0 + (uint64_t)(4 * g) * kGamma, x, m, sm, sx, kc);
+                uint4 x[NP], m[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    x[p] = __ldcs(reinterpret_cast<const uint4*>(xv[p]) + g);
+                    m[p] = __ldcs(reinterpret_cast<const uint4*>(ma[p]) + g);
+                    if (has_b) m[p] = sub4(m[p], __ldcs(reinterpret_cast<const uint4*>(mb[p]) + g));
+                }
+                const uint64_t z = z0 + (uint64_t)(4 * g) * kGamma;
+                uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    const uint32_t r = mac_coeff_rep(zl, zh, kc);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        const uint32_t xl = l == 0 ? x[p].x : l == 1 ? x[p].y : l == 2 ? x[p].z : x[p].w;
+                        const uint32_t ml = l == 0 ? m[p].x : l == 1 ? m[p].y : l == 2 ? m[p].z : m[p].w;
+                        sm[p].add(mul_wide(r, ml));
+                        sx[p].add(mul_wide(r, xl));
+                    }
+                    z_step(zl, zh);
+                }
             }
             done = n4 * 4;
         }
         for (uint32_t i = done + threadIdx.x; i < count; i += blockDim.x) {
-            uint32_t m = __ldcs(ma + i);
-            if (mb) m = fp_sub(m, __ldcs(mb + i));
             const uint64_t z = z0 + (uint64_t)i * kGamma;
-            sigma_rec((uint32_t)z, (uint32_t)(z >> 32), __ldcs(xv + i), m, sm, sx, kc);
+            const uint32_t r = mac_coeff_rep((uint32_t)z, (uint32_t)(z >> 32), kc);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                uint32_t mm = __ldcs(ma[p] + i);
+                if (has_b) mm = fp_sub(mm, __ldcs(mb[p] + i));
+                sm[p].add(mul_wide(r, mm));
+                sx[p].add(mul_wide(r, __ldcs(xv[p] + i)));
+            }
         }
     }
-    // sigma partial of this thread: S_m - alpha * S_x (mod p)
-    unsigned long long s[1] = {fp_sub(sm.mod(), fp_mul(alpha, sx.mod()))};
-    block_sum<1>(s);
-    if (threadIdx.x == 0) atomicAdd(acc, (unsigned long long)fp_reduce64(s[0]));
+    // sigma partial of this thread per party: S_m - alpha_p * S_x (mod p)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        unsigned long long s[1] = {fp_sub(sm[p].mod(), fp_mul(so.alpha[p], sx[p].mod()))};
+        block_sum<1>(s);
+        if (threadIdx.x == 0) atomicAdd(so.acc[p], (unsigned long long)fp_reduce64(s[0]));
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_mac_sigma_ranked(const uint32_t* __restrict__ value,
@@ -913,21 +961,32 @@ cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t
     return launched();
 }
 
-cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
-                             unsigned long long* acc, int sms) {
+template <int NP>
+static cudaError_t mac_sigma_np(cudaStream_t s, const MacTableT<NP>& tab, uint64_t coin, const SigmaOut<NP>& so,
+                                int sms) {
     const uint64_t units = (tab.rec0[tab.n] + kSigmaAlign - 1) / kSigmaAlign;
     if (units == 0) return cudaSuccess;
     static int per_sm = 0;
     if (per_sm == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mac_sigma, kThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mac_sigma<NP>, kThreads, 0) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
     }
     const uint64_t cap = (uint64_t)sms * per_sm;
     const int grid = (int)(units < cap ? units : cap);
     if ((units / grid + 1) * kSigmaAlign >= (1ull << 31)) return cudaErrorInvalidValue;  // per-CTA range < 2^31
-    k_mac_sigma<<<grid, kThreads, 0, s>>>(tab, coin, alpha, SigConsts{}, acc);
+    k_mac_sigma<NP><<<grid, kThreads, 0, s>>>(tab, coin, so, SigConsts{});
     return launched();
+}
+
+cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
+                             unsigned long long* acc, int sms) {
+    return mac_sigma_np<1>(s, tab, coin, SigmaOut<1>{{alpha}, {acc}}, sms);
+}
+
+cudaError_t launch_mac_sigma2(cudaStream_t s, const MacTableT<2>& tab, uint64_t coin, const uint32_t alpha[2],
+                              unsigned long long* const acc[2], int sms) {
+    return mac_sigma_np<2>(s, tab, coin, SigmaOut<2>{{alpha[0], alpha[1]}, {acc[0], acc[1]}}, sms);
 }
 
 cudaError_t launch_mac_sigma_ranked(cudaStream_t s, const uint32_t* value, const uint32_t* mac,

@@ -8,20 +8,26 @@ namespace spdzb200 {
 
 constexpr int kMaxPeers = 7;
 
-struct MacSegDev {            // device-side MAC segment descriptor
-    const uint32_t* value;
-    const uint32_t* mac_a;
-    const uint32_t* mac_b;    // may be null
+// Device-side MAC segment descriptor for NP parties whose logs share every record's
+// rank (same lengths, same j0): the coefficient stream is computed once for all of them.
+template <int NP>
+struct MacSegT {
+    const uint32_t* value[NP];
+    const uint32_t* mac_a[NP];
+    const uint32_t* mac_b[NP];  // may be null (then for every party)
     uint64_t len;
     uint64_t j0;
 };
 constexpr uint32_t kSigmaAlign = 1024;     // CTA record ranges start at multiples of this
 constexpr int kMacTableSegs = 48;          // segments per launch (kernel parameter table)
-struct MacTable {
+template <int NP>
+struct MacTableT {
     uint32_t n;                            // segments in this table
-    MacSegDev seg[kMacTableSegs];
+    MacSegT<NP> seg[kMacTableSegs];
     uint64_t rec0[kMacTableSegs + 1];      // first record of each segment (prefix sums), rec0[n] = total
 };
+using MacSegDev = MacSegT<1>;
+using MacTable = MacTableT<1>;
 
 struct LaunchInfo {
     int sm_count = 148;
@@ -62,6 +68,9 @@ cudaError_t launch_pair_split(cudaStream_t s, const uint32_t* cv, const uint32_t
 // MAC sigma partial over chunks; acc (u64) accumulates values < p per block.
 cudaError_t launch_mac_sigma(cudaStream_t s, const MacTable& tab, uint64_t coin, uint32_t alpha,
                              unsigned long long* acc, int sms);
+// Two parties' sigma partials in one pass (shared coefficients): acc[p] += party p's partial.
+cudaError_t launch_mac_sigma2(cudaStream_t s, const MacTableT<2>& tab, uint64_t coin, const uint32_t alpha[2],
+                              unsigned long long* const acc[2], int sms);
 // MAC sigma over explicit ranks (record form)
 cudaError_t launch_mac_sigma_ranked(cudaStream_t s, const uint32_t* value, const uint32_t* mac,
                                     const uint64_t* rank, uint64_t n, uint64_t coin, uint32_t alpha,

@@ -1221,12 +1221,57 @@ uint64_t agree_coin(spdz_run* r, bool have_coin, uint64_t given_coin) {
 }
 
 // sigma kernels of every local party (asynchronous)
+// Both parties of a 2-party run local on one stream with rank-identical logs: one pass
+// (the coefficient stream r_j is the same for both, spdz.cpp:131-135).
+bool mac_fusable(spdz_run* r) {
+    if (r->n != 2 || !r->parties[0].local || !r->parties[1].local || S(r, 0) != S(r, 1)) return false;
+    const auto &a = r->parties[0].maclog, &b = r->parties[1].maclog;
+    if (a.size() != b.size()) return false;
+    for (size_t i = 0; i < a.size(); ++i)
+        if (a[i].len != b[i].len || a[i].j0 != b[i].j0 || (a[i].mac_b == nullptr) != (b[i].mac_b == nullptr) ||
+            !a[i].value || !a[i].mac_a || !b[i].value || !b[i].mac_a)
+            return false;
+    return true;
+}
+
 void mac_launch(spdz_run* r, uint64_t coin) {
+    for (int p = 0; p < r->n; ++p)
+        if (r->parties[p].local) assign_ranks(r->parties[p].maclog.data(), r->parties[p].maclog.size());
+    if (mac_fusable(r)) {
+        auto &P0 = r->parties[0], &P1 = r->parties[1];
+        dev(r, 0);
+        cudaStream_t s = S(r, 0);
+        uint64_t sbytes = 0;
+        for (int p = 0; p < 2; ++p)
+            for (auto& sg : r->parties[p].maclog) sbytes += sg.len * (sg.mac_b ? 12 : 8);
+        const int tk = ktimer_begin(r, 0);
+        lk(cudaMemsetAsync(P0.ctx->d_acc, 0, 8, s), "memset acc");
+        lk(cudaMemsetAsync(P1.ctx->d_acc, 0, 8, s), "memset acc");
+        const auto &L0 = P0.maclog, &L1 = P1.maclog;
+        for (size_t base = 0; base < L0.size(); base += kMacTableSegs) {
+            MacTableT<2> tab{};
+            tab.n = (uint32_t)std::min<size_t>(kMacTableSegs, L0.size() - base);
+            uint64_t recs = 0;
+            for (uint32_t i = 0; i < tab.n; ++i) {
+                const auto &a = L0[base + i], &b = L1[base + i];
+                tab.seg[i] = MacSegT<2>{{a.value, b.value}, {a.mac_a, b.mac_a}, {a.mac_b, b.mac_b}, a.len, a.j0};
+                tab.rec0[i] = recs;
+                recs += a.len;
+            }
+            tab.rec0[tab.n] = recs;
+            const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
+            unsigned long long* const acc[2] = {P0.ctx->d_acc, P1.ctx->d_acc};
+            lk(launch_mac_sigma2(s, tab, coin, alpha, acc, P0.ctx->sms), "k_mac_sigma<2>");
+        }
+        ktimer_end(r, 0, tk, SPDZ_KSTAT_SIGMA, sbytes);
+        lk(cudaEventRecord(P0.t1, s), "t1");
+        lk(cudaEventRecord(P1.t1, s), "t1");
+        return;
+    }
     for (int p = 0; p < r->n; ++p) {
         auto& P = r->parties[p];
         if (!P.local) continue;
         dev(r, p);
-        assign_ranks(P.maclog.data(), P.maclog.size());
         uint64_t sbytes = 0;
         for (auto& sg : P.maclog) sbytes += sg.len * (sg.mac_b ? 12 : 8);
         const int tk = ktimer_begin(r, p);
