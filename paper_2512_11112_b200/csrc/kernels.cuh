@@ -54,6 +54,12 @@ cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const u
                                   uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms,
                                   const uint32_t* alpha_dev = nullptr);
 cudaError_t launch_set_word(cudaStream_t s, uint32_t* p, uint32_t v);
+// Both parties of a 2-party run on one GPU: de = {d0, e0, d1, e1} payload halves, z = {z0.v,
+// z0.m, z1.v, z1.m}; the opened d, e (one copy, identical for both parties) -> open_d/open_e.
+cudaError_t launch_beaver_combine2(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],
+                                   const uint32_t* const tri1[6], const uint32_t alpha[2],
+                                   const uint32_t* const alpha_dev[2], uint32_t* const z[4], uint32_t* open_d,
+                                   uint32_t* open_e, uint64_t n, int sms);
 // net.cpp:170-215
 cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, int n_peers,
                             uint32_t* out, uint64_t n, int sms);

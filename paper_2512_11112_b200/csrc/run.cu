@@ -847,6 +847,37 @@ struct Exec {
             sent[p] = publish(p, slot_of(id, 0));
         }
         const uint64_t batch = make_batch(id, exec, 0);
+        const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
+        bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+        for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
+        if (fuse2) {  // both parties in one pass: payloads read once, opened values logged once
+            auto &P0 = r->parties[0], &P1 = r->parties[1];
+            auto &s0 = P0.ns[id], &s1 = P1.ns[id];
+            dev(r, 0);
+            const uint32_t* de[4] = {s0.payload, s0.payload + L, s1.payload, s1.payload + L};
+            const uint32_t *t0[6], *t1[6];
+            for (int t = 0; t < 6; ++t) {
+                t0[t] = P0.pool[t] + off;
+                t1[t] = P1.pool[t] + off;
+            }
+            const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
+            const uint32_t* alpha_dev[2] = {P0.ctx->d_alpha, P1.ctx->d_alpha};
+            uint32_t* z[4] = {s0.out.v, s0.out.m, s1.out.v, s1.out.m};
+            const int tk = tbegin(0);
+            lk(launch_beaver_combine2(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, L,
+                                      SMS(r, 0)),
+               "k_combine2");
+            // [d|e] of both parties 16 + two parties' triple planes 48 + two z 16 + one opened log 8
+            tend(0, tk, SPDZ_KSTAT_COMBINE, 88 * L);
+            r->exchanged += 2 * (2 * L * 4);
+            for (int p = 0; p < 2; ++p) {  // log_open (runtime.cpp:224); the opened values are public
+                auto& P = r->parties[p];
+                auto& st = P.ns[id];
+                P.maclog.push_back({s0.opened, st.xa.m, P.pool[1] + off, L, 0, batch, so, 2 * G});
+                P.maclog.push_back({s0.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
+            }
+            return;
+        }
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -873,7 +904,6 @@ struct Exec {
             // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
             tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
             // log_open (runtime.cpp:224): records [d | e] with mac shares [x.m - a.m | y.m - b.m]
-            const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
             P.maclog.push_back({st.opened, st.xa.m, P.pool[1] + off, L, 0, batch, so, 2 * G});
             P.maclog.push_back({st.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
         }
@@ -1241,9 +1271,11 @@ void mac_launch(spdz_run* r, uint64_t coin) {
         auto &P0 = r->parties[0], &P1 = r->parties[1];
         dev(r, 0);
         cudaStream_t s = S(r, 0);
-        uint64_t sbytes = 0;
-        for (int p = 0; p < 2; ++p)
-            for (auto& sg : r->parties[p].maclog) sbytes += sg.len * (sg.mac_b ? 12 : 8);
+        uint64_t sbytes = 0;  // per record: each party's mac_a (+ mac_b), the opened value once if shared
+        for (size_t i = 0; i < P0.maclog.size(); ++i) {
+            const auto &a = P0.maclog[i], &b = P1.maclog[i];
+            sbytes += a.len * ((a.mac_b ? 16 : 8) + (a.value == b.value ? 4 : 8));
+        }
         const int tk = ktimer_begin(r, 0);
         lk(cudaMemsetAsync(P0.ctx->d_acc, 0, 8, s), "memset acc");
         lk(cudaMemsetAsync(P1.ctx->d_acc, 0, 8, s), "memset acc");
