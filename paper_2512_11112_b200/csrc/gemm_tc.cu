@@ -17,7 +17,7 @@
 // instruction keeps the shared-memory operand traffic at 96 B/clk; the 128 x 64 tile
 // needs 48 B/clk of L2->SMEM fill at the MMA rate.
 //
-// Operands are re-laid out once per call (k_tile_rows / k_tile_cols) as u8 limb
+// Operands are re-laid out once per call (k_tile_both: tile_rows / tile_cols) as u8 limb
 // tiles already in the canonical no-swizzle K-major UMMA image (8-row x 16-byte
 // core matrices), so each K stage is two 1-D TMA bulk copies (cp.async.bulk +
 // mbarrier complete_tx) into a 4-stage ring.  The kernel is persistent (one CTA per
@@ -91,7 +91,7 @@ __device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t k) {
     return (r >> 3) * kSBO + (k >> 4) * kLBO + (r & 7) * 16 + (k & 15);
 }
 
-// B-operand transform of the re-layout (k_tile_cols)
+// B-operand transform of the re-layout (tile_cols)
 struct TcBx {
     const uint32_t* e;
     uint32_t coef0, coef1;
@@ -135,7 +135,7 @@ template <int TN>
 __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At,
                                                                const uint8_t* __restrict__ Bt, uint32_t M, uint32_t N,
                                                                uint32_t KB, uint32_t tiles_n, uint32_t n_tiles,
-                                                               TcOut out) {
+                                                               TcOut out, uint32_t dbg) {
     using L = TcSmem<TN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: everything above overlapped the re-layout kernel;
+    // its limb images (and any earlier writes) are visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer ----
@@ -177,6 +180,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     const uint32_t s = g % kStages;
                     if (g >= (uint32_t)kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
                     const uint32_t dst = sbase + s * L::STAGE;
+                    if (dbg & 1) {  // diagnostic: no loads (attribution only, results invalid)
+                        mbar_arrive(&full[s]);
+                        continue;
+                    }
                     mbar_expect_tx(&full[s], L::STAGE);
                     bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
                     bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * L::B_STAGE, L::B_STAGE, &full[s]);
@@ -195,6 +202,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     mbar_wait(&full[s], (g / kStages) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
+                    if (dbg & 2) {  // diagnostic: no MMAs (attribution only, results invalid)
+                        mbar_arrive(&empty[s]);
+                        continue;
+                    }
 #pragma unroll
                     for (int ks = 0; ks < TK / 32; ++ks) {
                         const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
@@ -215,7 +226,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     }
                     mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
-                mma_commit(tfull);  // accumulators of this tile complete
+                if (dbg & 2) mbar_arrive(tfull);
+                else mma_commit(tfull);  // accumulators of this tile complete
             }
         }
     } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
@@ -312,13 +324,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
 // byte 16 q of each limb image (= core_off), so a warp's four limb stores are 4 x 512
 // contiguous bytes; its loads are 64-byte row segments.
 // A(m, k) = a0[m*K + k] for m < M0, a1[(m-M0)*K + k] for M0 <= m < M; zero padded.
-__global__ void __launch_bounds__(256) k_tile_rows(const uint32_t* __restrict__ a0, const uint32_t* __restrict__ a1,
-                                                   uint32_t M0, uint32_t M, uint32_t K, uint32_t Mp, uint32_t KB,
-                                                   uint8_t* __restrict__ out) {
+struct RowsArgs {
+    const uint32_t* a0;
+    const uint32_t* a1;
+    uint32_t M0, M, K, Mp, KB;
+    uint8_t* out;
+};
+__device__ __forceinline__ void tile_rows(const RowsArgs& ra, uint64_t t0, uint64_t stride) {
+    const uint32_t *a0 = ra.a0, *a1 = ra.a1;
+    const uint32_t M0 = ra.M0, M = ra.M, K = ra.K, Mp = ra.Mp, KB = ra.KB;
+    uint8_t* out = ra.out;
     constexpr uint32_t kPieces = TM * TK / 16;  // 512 per block
     const uint64_t pieces = (uint64_t)(Mp / TM) * KB * kPieces;
     const bool v4 = (K % 4) == 0 && ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 15u) == 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < pieces; t += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t t = t0; t < pieces; t += stride) {
         const uint64_t blk = t / kPieces;
         const uint32_t q = (uint32_t)(t % kPieces);
         const uint32_t r = (q / 32) * 8 + (q % 8), kk = ((q / 8) % 4) * 16;
@@ -357,11 +376,19 @@ __global__ void __launch_bounds__(256) k_tile_rows(const uint32_t* __restrict__ 
 // With bx.e set, the operand is B + coef * E (E: K x NB, the same plane under both
 // halves; coef0 for columns < NB, coef1 after) — the matrix-triple combine's
 // B.v + [party 0] E and B.m + alpha_i E, formed on the way into the limb image.
+struct ColsArgs {
+    const uint32_t* b0;
+    const uint32_t* b1;
+    uint32_t NB, N, K, KB;
+    TcBx bx;
+    uint8_t* out;
+};
 template <int BN>
-__global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __restrict__ b1, uint32_t NB, uint32_t N,
-                            uint32_t K, uint32_t KB, TcBx bx, uint8_t* __restrict__ out) {
-    __shared__ uint32_t tile[TK][33];
-    const uint32_t kb = blockIdx.x, nt32 = blockIdx.y * 32;
+__device__ __forceinline__ void tile_cols(const ColsArgs& ca, uint32_t kb, uint32_t nt32, uint32_t (&tile)[TK][33]) {
+    const uint32_t *b0 = ca.b0, *b1 = ca.b1;
+    const uint32_t NB = ca.NB, N = ca.N, K = ca.K, KB = ca.KB;
+    const TcBx& bx = ca.bx;
+    uint8_t* out = ca.out;
     for (uint32_t e = threadIdx.x; e < TK * 32; e += blockDim.x) {
         const uint32_t kk = e / 32, nn = e % 32;
         const uint32_t k = kb * TK + kk, n = nt32 + nn;
@@ -394,9 +421,25 @@ __global__ void k_tile_cols(const uint32_t* __restrict__ b0, const uint32_t* __r
     }
 }
 
-// Diagnostic switches (attribution experiments, scripts/gemm_probe.py): bit 2 skips the GEMM
-// kernel, bit 3 the re-layout kernels (results invalid while set); bit 6 / bit 7 force the
-// 32- / 64-column tile width (results valid).
+// Both re-layouts in one launch: blocks [0, row_blocks) split A (grid-strided pieces),
+// the rest transpose-split one 64 k x 32 n block of B each.  The first instruction
+// lets the dependent GEMM grid launch (programmatic dependent launch): its prologue
+// (barrier init, TMEM allocation) overlaps this kernel; it waits before reading.
+template <int BN>
+__global__ void __launch_bounds__(256) k_tile_both(RowsArgs ra, ColsArgs ca, uint32_t row_blocks, uint32_t col_kb) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ uint32_t tile[TK][33];
+    if (blockIdx.x < row_blocks) {
+        tile_rows(ra, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, (uint64_t)row_blocks * blockDim.x);
+    } else {
+        const uint32_t c = blockIdx.x - row_blocks;
+        tile_cols<BN>(ca, c % col_kb, (c / col_kb) * 32, tile);
+    }
+}
+
+// Diagnostic switches (attribution experiments, scripts/gemm_probe.py): bit 0 skips the TMA
+// loads, bit 1 the MMAs, bit 2 the GEMM kernel, bit 3 the re-layout kernels (results invalid
+// while any is set); bit 6 / bit 7 force the 32- / 64-column tile width (results valid).
 uint32_t g_tc_dbg = 0;
 
 // Re-layout both operands into limb images (B tiles BN columns wide), then run
@@ -410,18 +453,18 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
     const uint32_t KB = (din + TK - 1) / TK;
     uint8_t* At = scratch;
     uint8_t* Bt = scratch + (uint64_t)4 * Mp * KB * TK;
+    bool pdl = false;
     if (!(g_tc_dbg & 8)) {  // (diagnostic bit 3 skips the re-layout kernels)
         const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
-        const int grid = (int)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
-        if (mode == 0) k_tile_rows<<<grid, 256, 0, s>>>(w0, w0, M, M, din, Mp, KB, At);
-        else k_tile_rows<<<grid, 256, 0, s>>>(w0, w1, dout, M, din, Mp, KB, At);
-        ++g_kernel_launches;
-        dim3 g2(KB, (Np + 31) / 32);
-        if (mode == 0) k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x1, batch, N, din, KB, bx, Bt);
-        else k_tile_cols<BN><<<g2, 256, 0, s>>>(x0, x0, batch, N, din, KB, TcBx{}, Bt);
+        const uint32_t row_blocks = (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
+        const uint32_t col_blocks = KB * ((Np + 31) / 32);
+        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, At};
+        const ColsArgs ca{x0, mode == 0 ? x1 : x0, batch, N, din, KB, mode == 0 ? bx : TcBx{}, Bt};
+        k_tile_both<BN><<<row_blocks + col_blocks, 256, 0, s>>>(ra, ca, row_blocks, KB);
         ++g_kernel_launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        pdl = true;
     }
     if (g_tc_dbg & 4) return cudaSuccess;  // (diagnostic bit 2 skips the GEMM kernel)
     using L = TcSmem<BN>;
@@ -433,8 +476,20 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
     }
     const uint32_t tiles_n = Np / BN, n_tiles = tiles_n * (Mp / TM);
     const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)sms);
-    k_modgemm_tc<BN><<<grid, kThreadsTc, L::BYTES, s>>>(At, Bt, M, N, KB, tiles_n, n_tiles, out);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreadsTc);
+    cfg.dynamicSmemBytes = L::BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;  // overlap our prologue with the re-layout kernel's tail
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_modgemm_tc<BN>, (const uint8_t*)At, (const uint8_t*)Bt, M, N, KB,
+                                       tiles_n, n_tiles, out, g_tc_dbg & 3u);
     ++g_kernel_launches;
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -63,7 +63,8 @@ def timed(reps=10):
 if "--diag" in sys.argv:  # time split: re-layout kernels vs the GEMM kernel (results garbage while set)
     check(lib().spdz_set_gemm_path(2))
     base = BASE
-    for flags, name in ((0, "full"), (4, "re-layout only"), (8, "gemm kernel only")):
+    for flags, name in ((0, "full"), (4, "re-layout only"), (8, "gemm kernel only"), (9, "gemm, no loads"),
+                        (10, "gemm, no MMAs"), (11, "gemm, no loads no MMAs")):
         lib().spdz_diag_gemm_tc_flags(base | flags)
         print(f"tcgen05 {name}: graphed {graphed():.1f} us per call", flush=True)
     lib().spdz_diag_gemm_tc_flags(base)
