@@ -4,9 +4,12 @@
 // Every GPU result is compared bit-for-bit with the reference CpuBackend.
 // Exit 0 = all checks passed.  Built by integration/Makefile (needs the
 // reference headers and oracle/_ref/libllspdz_ref.so); runs on the GPU box.
+#include <atomic>
 #include <cstdio>
 #include <random>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "mpc/backend.hpp"
 #include "mpc/spdz.hpp"
@@ -17,7 +20,7 @@ std::shared_ptr<Backend> make_gpu_b200_backend(int device);
 
 using namespace mpc;
 
-static int failures = 0;
+static std::atomic<int> failures{0};
 #define CHECK(c)                                                    \
     do {                                                            \
         if (!(c)) {                                                 \
@@ -72,6 +75,32 @@ int main() {
             CHECK(z.vals == z_ref.vals && z.macs == z_ref.macs);
         }
     }
+    // concurrent callers (the runtime's worker threads, runtime.cpp:452-465): each thread's
+    // Beaver mask/combine through the shared backend equals the CpuBackend's
+    {
+        std::vector<std::thread> th;
+        for (int w = 0; w < 8; ++w)
+            th.emplace_back([&, w] {
+                const size_t lanes = 4096 + 97 * w;
+                spdz::Dealer d(2, 100 + w);
+                auto X = d.share(rand_field_vec(lanes, 200 + w)), Y = d.share(rand_field_vec(lanes, 300 + w));
+                auto T = d.triples(lanes);
+                for (int rep = 0; rep < 4; ++rep)
+                    for (int i = 0; i < 2; ++i) {
+                        std::vector<uint32_t> d0, e0, d1, e1;
+                        gpu->mul_mask(X[i], Y[i], T[i], d0, e0);
+                        cpu->mul_mask(X[i], Y[i], T[i], d1, e1);
+                        CHECK(d0 == d1 && e0 == e1);
+                        auto z = gpu->mul_combine(T[i], d0, e0, i, d.alpha_share(i));
+                        auto z_ref = spdz::beaver_combine(T[i], d0, e0, i, d.alpha_share(i));
+                        CHECK(z.vals == z_ref.vals && z.macs == z_ref.macs);
+                        auto s = gpu->add_batch(X[i], Y[i]);
+                        auto s_ref = cpu->add_batch(X[i], Y[i]);
+                        CHECK(s.vals == s_ref.vals && s.macs == s_ref.macs);
+                    }
+            });
+        for (auto& t : th) t.join();
+    }
     bool threw = false;
     try {
         spdz::ShareVec a, b;
@@ -93,6 +122,6 @@ int main() {
         threw = true;
     }
     CHECK(threw);
-    std::printf("%s: %d failures\n", failures ? "FAIL" : "PASS", failures);
+    std::printf("%s: %d failures\n", failures ? "FAIL" : "PASS", failures.load());
     return failures ? 1 : 0;
 }

@@ -13,6 +13,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "mpc/backend.hpp"
 #include "spdz_b200.h"
@@ -35,27 +36,69 @@ void ok(int rc) {
     if (rc != SPDZ_OK) raise(rc);
 }
 
+// The runtime calls the backend concurrently from its worker threads and open
+// continuations (runtime.cpp:221-238, 452-465; kernels must be pure, SPDZ_SPEC 473-474).
+// A context owns one CUDA stream and its staging buffers, so each call borrows a
+// context from a pool for its duration: concurrent calls run on separate streams
+// instead of queueing behind one lock.
+class CtxPool {
+public:
+    explicit CtxPool(int device) : device_(device) {}
+    ~CtxPool() {
+        for (auto* c : free_) spdz_ctx_destroy(c);
+    }
+    spdz_ctx* acquire() {
+        {
+            std::lock_guard lk(mu_);
+            if (!free_.empty()) {
+                spdz_ctx* c = free_.back();
+                free_.pop_back();
+                return c;
+            }
+        }
+        spdz_ctx* c = nullptr;  // party/alpha are per call (mul_combine carries them)
+        ok(spdz_ctx_create(device_, 0, 2, 0, &c));
+        return c;
+    }
+    void release(spdz_ctx* c) {
+        std::lock_guard lk(mu_);
+        free_.push_back(c);
+    }
+
+private:
+    int device_;
+    std::mutex mu_;
+    std::vector<spdz_ctx*> free_;
+};
+
+struct Lease {
+    CtxPool& pool;
+    spdz_ctx* ctx;
+    explicit Lease(CtxPool& p) : pool(p), ctx(p.acquire()) {}
+    ~Lease() { pool.release(ctx); }
+    Lease(const Lease&) = delete;
+    Lease& operator=(const Lease&) = delete;
+};
+
 class GpuB200Backend : public Backend {
 public:
-    explicit GpuB200Backend(int device) {
-        // party/alpha are per call (mul_combine carries them), so one context
-        ok(spdz_ctx_create(device, 0, 2, 0, &ctx_));
+    explicit GpuB200Backend(int device) : pool_(device) {
+        Lease l(pool_);
         spdz_capability_t c;
-        ok(spdz_capability(ctx_, &c));
+        ok(spdz_capability(l.ctx, &c));
         cap_.name = c.name;
         cap_.min_kernel_size = c.min_kernel_size;  // 1: no CPU fallback
         cap_.threads_per_block = c.threads_per_block;
         cap_.executable = c.executable != 0;
     }
-    ~GpuB200Backend() override { spdz_ctx_destroy(ctx_); }
 
     const BackendCapability& capability() const override { return cap_; }
 
     spdz::ShareVec add_batch(const spdz::ShareVec& x, const spdz::ShareVec& y) override {
         spdz::ShareVec z;
         z.resize(x.lanes());
-        std::lock_guard lk(mu_);  // one stream per context; kernels stay pure
-        ok(spdz_host_add_batch(ctx_, x.vals.data(), x.macs.data(), x.lanes(), y.vals.data(), y.macs.data(),
+        Lease l(pool_);
+        ok(spdz_host_add_batch(l.ctx, x.vals.data(), x.macs.data(), x.lanes(), y.vals.data(), y.macs.data(),
                                y.lanes(), z.vals.data(), z.macs.data()));
         return z;
     }
@@ -63,8 +106,8 @@ public:
     spdz::ShareVec sub_batch(const spdz::ShareVec& x, const spdz::ShareVec& y) override {
         spdz::ShareVec z;
         z.resize(x.lanes());
-        std::lock_guard lk(mu_);
-        ok(spdz_host_sub_batch(ctx_, x.vals.data(), x.macs.data(), x.lanes(), y.vals.data(), y.macs.data(),
+        Lease l(pool_);
+        ok(spdz_host_sub_batch(l.ctx, x.vals.data(), x.macs.data(), x.lanes(), y.vals.data(), y.macs.data(),
                                y.lanes(), z.vals.data(), z.macs.data()));
         return z;
     }
@@ -77,8 +120,8 @@ public:
         e_out.resize(x.lanes());
         const uint32_t* tri[6] = {t.a.vals.data(), t.a.macs.data(), t.b.vals.data(),
                                   t.b.macs.data(), t.c.vals.data(), t.c.macs.data()};
-        std::lock_guard lk(mu_);
-        ok(spdz_host_mul_mask(ctx_, x.vals.data(), y.vals.data(), x.lanes(), tri, t.a.lanes(), d_out.data(),
+        Lease l(pool_);
+        ok(spdz_host_mul_mask(l.ctx, x.vals.data(), y.vals.data(), x.lanes(), tri, t.a.lanes(), d_out.data(),
                               e_out.data()));
     }
 
@@ -90,8 +133,8 @@ public:
         z.resize(d.size());
         const uint32_t* tri[6] = {t.a.vals.data(), t.a.macs.data(), t.b.vals.data(),
                                   t.b.macs.data(), t.c.vals.data(), t.c.macs.data()};
-        std::lock_guard lk(mu_);
-        ok(spdz_host_mul_combine(ctx_, tri, t.a.lanes(), d.data(), e.data(), d.size(), party, alpha_share,
+        Lease l(pool_);
+        ok(spdz_host_mul_combine(l.ctx, tri, t.a.lanes(), d.data(), e.data(), d.size(), party, alpha_share,
                                  z.vals.data(), z.macs.data()));
         return z;
     }
@@ -99,15 +142,14 @@ public:
     spdz::ShareVec reduce_add(const spdz::ShareVec& x) override {
         spdz::ShareVec z;
         z.resize(1);
-        std::lock_guard lk(mu_);
-        ok(spdz_host_reduce_add(ctx_, x.vals.data(), x.macs.data(), x.lanes(), z.vals.data(), z.macs.data()));
+        Lease l(pool_);
+        ok(spdz_host_reduce_add(l.ctx, x.vals.data(), x.macs.data(), x.lanes(), z.vals.data(), z.macs.data()));
         return z;
     }
 
 private:
-    spdz_ctx* ctx_ = nullptr;
+    CtxPool pool_;
     BackendCapability cap_;
-    std::mutex mu_;
 };
 
 }  // namespace
