@@ -15,7 +15,7 @@
 
 namespace spdzb200 {
 
-unsigned long long g_kernel_launches = 0;
+std::atomic<unsigned long long> g_kernel_launches{0};
 
 namespace {
 
@@ -267,6 +267,28 @@ struct OpCombine2 {
         }
         o[4] = d;
         o[5] = e;
+    }
+};
+
+// Input sharing of one private input for both parties of a 2-party run on one GPU
+// (preproc.cpp:205-243 with spdz::add_public, spdz.cpp:35-45): x = reduce(raw input),
+// diff = x - r (opened by party 0), party 0: (mask.v + diff, mask.m + alpha_0 diff),
+// party 1: (mask.v, mask.m + alpha_1 diff).  Inputs: raw x, r (clear mask), party 0's
+// mask.v mask.m, party 1's.  Outputs: v0 m0 v1 m1.
+struct OpShareInput2 {
+    uint32_t alpha0, alpha1;
+    const uint32_t *ap0, *ap1;
+    __device__ static constexpr bool is_peer(int) { return false; }
+    __device__ void prepare() {
+        if (ap0) alpha0 = __ldg(ap0);
+        if (ap1) alpha1 = __ldg(ap1);
+    }
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        const uint32_t diff = fp_sub(fp_reduce32(in[0]), in[1]);
+        o[0] = fp_add(in[2], diff);
+        o[1] = fp_add(in[3], fp_mul(alpha0, diff));
+        o[2] = in[4];
+        o[3] = fp_add(in[5], fp_mul(alpha1, diff));
     }
 };
 
@@ -981,6 +1003,13 @@ cudaError_t launch_beaver_combine2(cudaStream_t s, const uint32_t* const de[4], 
     io.out[4] = open_d;
     io.out[5] = open_e;
     return run_map(s, io, n, OpCombine2{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]}, sms);
+}
+
+cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uint32_t* r_clear,
+                                const uint32_t* const mask[4], const uint32_t alpha[2],
+                                const uint32_t* const alpha_dev[2], uint32_t* const out[4], uint64_t n, int sms) {
+    IO<6, 4> io{{x_raw, r_clear, mask[0], mask[1], mask[2], mask[3]}, {out[0], out[1], out[2], out[3]}};
+    return run_map(s, io, n, OpShareInput2{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]}, sms);
 }
 
 cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, int n_peers,

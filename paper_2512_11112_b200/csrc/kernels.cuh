@@ -2,6 +2,8 @@
 // asynchronous on `stream` and returns cudaGetLastError() of its launch.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 
 namespace spdzb200 {
@@ -33,7 +35,7 @@ struct LaunchInfo {
     int sm_count = 148;
 };
 
-extern unsigned long long g_kernel_launches;  // evidence counter
+extern std::atomic<unsigned long long> g_kernel_launches;  // evidence counter (calls may be concurrent)
 
 // elementwise (backend.cpp:25-51, spdz.cpp:35-75)
 cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
@@ -54,6 +56,11 @@ cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const u
                                   uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms,
                                   const uint32_t* alpha_dev = nullptr);
 cudaError_t launch_set_word(cudaStream_t s, uint32_t* p, uint32_t v);
+// Input sharing for both parties of a 2-party run on one GPU: mask = {v0, m0, v1, m1}
+// input-mask shares, out = {v0, m0, v1, m1} input shares (preproc.cpp:205-243).
+cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uint32_t* r_clear,
+                                const uint32_t* const mask[4], const uint32_t alpha[2],
+                                const uint32_t* const alpha_dev[2], uint32_t* const out[4], uint64_t n, int sms);
 // Both parties of a 2-party run on one GPU: de = {d0, e0, d1, e1} payload halves, z = {z0.v,
 // z0.m, z1.v, z1.m}; the opened d, e (one copy, identical for both parties) -> open_d/open_e.
 cudaError_t launch_beaver_combine2(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],

@@ -1342,11 +1342,32 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
     mac_finish(r, rep, coin);
 }
 
+// Input sharing of a 2-party run with both parties on one stream runs as one kernel per
+// input (the bound input stays raw until then).
+bool share_fused(spdz_run* r) {
+    return r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+}
+
 void share_inputs(spdz_run* r) {
     // preproc.cpp:205-243: party 0 opens x - mask, everyone adds the public difference
     ++r->seq;
     for (auto& [id, off] : r->input_mask_off) {
         const auto& n = r->node(id);
+        if (share_fused(r)) {  // both parties in one pass from the raw input (reduced inline)
+            auto it = r->input_dev.find(id);
+            need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
+                 "ShapeMismatch: no values bound for input node " + std::to_string(id));
+            auto &P0 = r->parties[0], &P1 = r->parties[1];
+            dev(r, 0);
+            const uint32_t* mask[4] = {P0.mask_v + off, P0.mask_m + off, P1.mask_v + off, P1.mask_m + off};
+            const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
+            const uint32_t* alpha_dev[2] = {P0.ctx->d_alpha, P1.ctx->d_alpha};
+            uint32_t* out[4] = {P0.ns[id].out.v, P0.ns[id].out.m, P1.ns[id].out.v, P1.ns[id].out.m};
+            lk(launch_share_input2(S(r, 0), it->second, P0.mask_c + off, mask, alpha, alpha_dev, out, n.lanes,
+                                   P0.ctx->sms),
+               "share input (2 parties)");
+            continue;
+        }
         uint32_t* diff = r->input_diff[id];  // party 0's buffer (IPC-mapped when party 0 is remote)
         const uint64_t slot = slot_of(id, 63);
         if (r->parties[0].local) {
@@ -1614,9 +1635,10 @@ int spdz_run_bind_input(spdz_run* r, uint32_t node, const uint32_t* host_vals, u
         } else {
             lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, P0.ctx->stream), "H2D input");
         }
-        // reduce mod p (preproc.cpp:149 fp::reduce): x * 1 mod p
-        lk(launch_public(P0.ctx->stream, 3, d, d, nullptr, false, 1u, true, 0, 0, d, d, len, P0.ctx->sms),
-           "reduce input");
+        // reduce mod p (preproc.cpp:149 fp::reduce): x * 1 mod p, unless input sharing does it inline
+        if (!share_fused(r))
+            lk(launch_public(P0.ctx->stream, 3, d, d, nullptr, false, 1u, true, 0, 0, d, d, len, P0.ctx->sms),
+               "reduce input");
     });
 }
 

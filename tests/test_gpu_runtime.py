@@ -309,3 +309,26 @@ def test_graph_replayed_online_phase(gpu, kind):
         assert res[0][3] == res[1][3]
     for r in runs:
         r.close()
+
+
+@pytest.mark.parametrize("n_parties", [2, 3])
+def test_inputs_above_p_are_reduced(gpu, n_parties):
+    """preproc.cpp:149: bound inputs are reduced mod p before sharing (2 parties: inline in
+    the fused input-sharing kernel; 3 parties: the separate reduce pass)."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    n = 4099
+    rng = np.random.default_rng(9)
+    x = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    y = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    x[:64] = np.arange(P, P + 64, dtype=np.uint64).clip(max=(1 << 32) - 1).astype(np.uint32)
+    xr, yr = (x.astype(np.uint64) % P).astype(np.uint32), (y.astype(np.uint64) % P).astype(np.uint32)
+    t1 = O.np_mul(xr, yr)
+    t2 = O.np_mul(t1, xr)
+    t3 = O.np_mul(t2, yr)
+    want = O.np_mul(t3, t1)
+    r = LocalRun(chain_graph("heavy", n), n_parties)
+    r.bind_inputs({"x": x, "y": y})
+    r.share_inputs()
+    rep = r.online()
+    np.testing.assert_array_equal(rep.outputs, want)
+    r.close()
