@@ -18,7 +18,7 @@ rng = np.random.default_rng(0)
 x = torch.from_numpy(rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)).pin_memory().numpy()
 y = torch.from_numpy(rng.integers(0, P, n, dtype=np.uint64).astype(np.uint32)).pin_memory().numpy()
 out = torch.empty(n, dtype=torch.uint32).pin_memory().numpy()
-for spec in sys.argv[1:] or ["4", "8"]:
+for spec in [a for a in sys.argv[1:] if "," not in a] or ["4", "8"]:
     chunks, mac = (int(spec.split(":")[0]), spec.split(":")[1]) if ":" in spec else (int(spec), "per_chunk")
     sr = StreamedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=chunks, mac=mac)
     sr.bind_output(out)
@@ -63,8 +63,12 @@ for spec in sys.argv[1:] or ["4", "8"]:
 # wall time of the public call (what bench.py's e2e measures), with a cProfile of one call
 import cProfile  # noqa: E402
 import pstats  # noqa: E402
-for chunks in (4, 8):
-    sr = StreamedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=chunks)
+for spec in (sys.argv[1:] if len(sys.argv) > 1 else ["4", "8"]):
+    if ":" in spec:
+        continue
+    weights = [float(w) for w in spec.split(",")] if "," in spec else None
+    chunks = len(weights) if weights else int(spec)
+    sr = StreamedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=chunks, weights=weights)
     sr.bind_output(out)
     for k in range(4):
         sr.deal(100 + k)
@@ -76,6 +80,6 @@ for chunks in (4, 8):
         sr.run({"x": x, "y": y})
         if k == 3:
             pr.disable()
-        print(f"StreamedRun.run chunks={chunks}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+        print(f"StreamedRun.run chunks={spec}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
     pstats.Stats(pr).sort_stats("cumulative").print_stats(12)
     sr.close()
