@@ -23,6 +23,7 @@ import subprocess
 import sys
 import threading
 import time
+import types
 from pathlib import Path
 
 import numpy as np
@@ -207,16 +208,19 @@ def run_ours(args, world, rank, local):
         party, k = rank // G, rank % G
         lanes = 2 * args.lanes
         total = G * lanes
-        g = chain_graph(args.kind, lanes)
-        run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1,
-                       shard=(k * lanes, total), single_party=party)
+        # the GPU's lanes run as `exchange_chunks` lane chunks on their own streams (ChunkedRun):
+        # one chunk's opening exchange over NVLink overlaps the other chunks' kernels
+        from paper_2512_11112_b200 import ChunkedRun
+        run = ChunkedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=args.exchange_chunks,
+                         shard=(k * lanes, total), single_party=party, devices=[dev, dev], profile_kernels=True)
         import torch.distributed as dist
         blobs = [None] * world
         dist.all_gather_object(blobs, run.export_ipc())
         peer = (1 - party) * G + k
         run.import_ipc([blobs[peer]])
         coin_fn = parallel.joint_coin
-        parallelism = f"2 parties x {G} GPUs, lane-sharded, NVLink P2P opens"
+        parallelism = (f"2 parties x {G} GPUs, lane-sharded, NVLink P2P opens, "
+                       f"{args.exchange_chunks} lane chunks per GPU overlapping the exchange")
     mults_step = n_mul * total  # whole job, per step
     rng = np.random.default_rng(1234 + rank)
     x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
@@ -233,10 +237,19 @@ def run_ours(args, world, rank, local):
         run.share_inputs()
 
     def step():
+        if world > 1:  # ChunkedRun: one coin, one sharded verification for every chunk
+            sig, ms, reps = run.online(coin_fn=coin_fn)
+            parallel.verify_sharded_sigmas(sig)
+            kst = {}
+            for r in reps:
+                for name, st in r.kstat.items():
+                    a = kst.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0})
+                    for f in a:
+                        a[f] += st[f]
+            return types.SimpleNamespace(online_device_ms=ms, kstat=kst, sigmas=sig,
+                                         kernel_launches=sum(r.kernel_launches for r in reps))
         rep = run.online(coin_fn=coin_fn)
-        if world > 1:
-            parallel.verify_sharded_sigmas(rep.sigmas)
-        elif sum(rep.sigmas) % P != 0:
+        if sum(rep.sigmas) % P != 0:
             raise RuntimeError("MAC check did not verify")
         return rep
 
@@ -364,6 +377,8 @@ def main():
     ap.add_argument("--lanes", type=int, default=1 << 24)
     ap.add_argument("--cpu-sample-lanes", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange-chunks", type=int, default=2,
+                    help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run (1 = serial)")
     args = ap.parse_args()
     world, rank, local = dist_setup()

@@ -427,6 +427,9 @@ int spdz_run_set_copy_streams(spdz_run* run, void* h2d_stream, void* d2h_stream)
 /* The CUDA stream a local party's kernels run on (NULL if not local) — for callers
  * that order their own work or timing events against the run. */
 void* spdz_run_party_stream(spdz_run* run, int party);
+/* Device time from run a's online-phase start event to run b's end event (after its MAC
+ * sigma kernels), for several runs on one device launched back to back (ChunkedRun). */
+int spdz_run_span_ms(spdz_run* a, spdz_run* b, float* ms);
 /* First half of spdz_run_mac_check: agree on the coin and launch the sigma kernels
  * asynchronously; the next spdz_run_mac_check collects and verifies (its coin
  * arguments are then ignored). */

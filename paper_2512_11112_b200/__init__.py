@@ -9,7 +9,7 @@ layer).  The compute path is hand-written sm_100a CUDA behind a C ABI
 from . import errors  # noqa: F401
 from .backend import (BackendCapability, BackendRegistry, Context, DeviceBMTriple, DeviceShare, DeviceTriple,  # noqa: F401
                       GpuBackend, ShareVec, TripleShares)
-from .runtime import (Graph, LocalRun, NodeSpec, RunReport, StreamedRun, chain_graph, linear_graph,  # noqa
+from .runtime import (ChunkedRun, Graph, LocalRun, NodeSpec, RunReport, StreamedRun, chain_graph, linear_graph,  # noqa
                       reduce_graph, run_local)
 
 P = 4294967291

@@ -158,6 +158,7 @@ _SIGS = {
     "spdz_run_mac_check_launch": (C.c_int, [vp, C.c_int, C.c_uint64]),
     "spdz_run_set_copy_streams": (C.c_int, [vp, vp, vp]),
     "spdz_run_party_stream": (vp, [vp, C.c_int]),
+    "spdz_run_span_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
     "spdz_run_bind_output": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_node_share": (C.c_int, [vp, C.c_int, C.c_uint32, C.POINTER(Share)]),
     "spdz_run_export": (C.c_int, [vp, vp, C.c_uint64, u64p]),

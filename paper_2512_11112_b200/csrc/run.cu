@@ -153,6 +153,7 @@ struct spdz_run {
     uint32_t* host_out = nullptr;   // pinned (internal) or user-bound output buffer
     uint64_t host_out_len = 0, host_out_cap = 0;
     bool host_out_owned = false;
+    bool host_out_registered = false;  // caller's pageable buffer page-locked by bind_output
     uint64_t exchanged = 0;
     cudaEvent_t ev_input = nullptr;
     cudaEvent_t ev_opened = nullptr;
@@ -1581,6 +1582,7 @@ int spdz_run_destroy(spdz_run* r) {
             cudaStreamDestroy(r->copy_stream);
         }
         if (r->online_graph) cudaGraphExecDestroy(r->online_graph);
+        if (r->host_out_registered) cudaHostUnregister(r->host_out);
         for (auto e : r->kt.pool) cudaEventDestroy(e);
         for (size_t i = 0; i < r->allocs.size(); ++i) {
             cudaSetDevice(r->alloc_dev[i]);
@@ -1728,6 +1730,23 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
     });
 }
 
+int spdz_run_span_ms(spdz_run* a, spdz_run* b, float* ms) {
+    return guard([&] {
+        need(a && b && ms, SPDZ_ERR_INVALID_ARGUMENT, "bad span args");
+        const int pa = a->ref_party();
+        dev(a, pa);
+        float best = -1.0f;
+        for (int p = 0; p < b->n; ++p) {
+            if (!b->parties[p].local) continue;
+            float t = 0;
+            cuda_check(cudaEventSynchronize(b->parties[p].t1), "sync t1");
+            cuda_check(cudaEventElapsedTime(&t, a->parties[pa].t0, b->parties[p].t1), "elapsed");
+            best = std::max(best, t);
+        }
+        *ms = best;
+    });
+}
+
 void* spdz_run_party_stream(spdz_run* r, int party) {
     if (!r || party < 0 || party >= r->n || !r->parties[party].local) return nullptr;
     return r->parties[party].ctx->stream;
@@ -1822,6 +1841,17 @@ int spdz_run_bind_output(spdz_run* r, uint32_t* host_out, uint64_t cap) {
     return guard([&] {
         need(r != nullptr && host_out != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "bad bind_output");
         if (r->host_out && r->host_out_owned) cudaFreeHost(r->host_out);
+        if (r->host_out_registered) cudaHostUnregister(r->host_out);
+        r->host_out_registered = false;
+        // a pageable buffer would turn the output D2H into a host-blocking copy (the whole
+        // online phase would wait for it): page-lock it for as long as it is bound
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, host_out) == cudaSuccess && at.type == cudaMemoryTypeUnregistered) {
+            cuda_check(cudaHostRegister(host_out, std::max<uint64_t>(cap, 1) * 4, cudaHostRegisterDefault),
+                       "cudaHostRegister(output)");
+            r->host_out_registered = true;
+        }
+        cudaGetLastError();  // clear the query's error state for unregistered pointers
         r->host_out = host_out;
         r->host_out_cap = cap;
         r->host_out_owned = false;

@@ -443,6 +443,85 @@ class StreamedRun:
         return coin
 
 
+class ChunkedRun:
+    """One party set's online phase over `lanes` lanes (global offset shard[0] of a
+    shard[1]-lane circuit) split into `chunks` exact lane shards, each a LocalRun on its
+    own CUDA streams and all launched back to back — the north star's stream scheduler:
+    while one chunk waits on its opening exchange (peer payload loads over NVLink, the
+    stream-memory-op flag waits of single-party runs) the others' kernels run.  One MAC
+    check covers every chunk: the coin is agreed once after all openings (``coin_fn``),
+    each chunk's sigma kernels run on its stream, the per-party partials are summed.
+
+    ``online()`` times the whole set on the device: every chunk stream waits on one start
+    event and a join stream waits on every chunk's end, so the span is event-measured."""
+
+    def __init__(self, graph_fn, n_parties: int, lanes: int, chunks: int = 4, shard: tuple | None = None,
+                 dealer_seed: int = 1, devices=None, single_party: int | None = None, coin: int | None = None,
+                 profile_kernels: bool = False):
+        import torch
+        off0, total = shard if shard is not None else (0, lanes)
+        base, extra = divmod(lanes, chunks)
+        self.ranges, o = [], 0
+        for c in range(chunks):
+            L = base + (1 if c < extra else 0)
+            L -= L % 4 if c < chunks - 1 and L > 4 else 0  # keep chunk starts 16-byte aligned
+            self.ranges.append((o, L))
+            o += L
+        if o != lanes:  # the last chunk takes the remainder
+            lo, L = self.ranges[-1]
+            self.ranges[-1] = (lo, L + lanes - o)
+        self.n, self.party, self.coin = n_parties, single_party, coin
+        self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
+                              shard=(off0 + lo, total), external_mac_verify=True, single_party=single_party,
+                              profile_kernels=profile_kernels) for lo, L in self.ranges]
+
+    def close(self):
+        for r in self.runs:
+            r.close()
+
+    def export_ipc(self) -> list:
+        return [r.export_ipc() for r in self.runs]
+
+    def import_ipc(self, exports):
+        """exports: every rank's export_ipc() list (own included, skipped)."""
+        for c, r in enumerate(self.runs):
+            r.import_ipc([e[c] for e in exports])
+
+    def deal(self, seed: int):
+        for r in self.runs:
+            r.deal(seed)
+
+    def bind_inputs(self, inputs: dict):
+        for r, (lo, L) in zip(self.runs, self.ranges):
+            r.bind_inputs({k: v[lo:lo + L] for k, v in inputs.items()})
+
+    def share_inputs(self):
+        for r in self.runs:
+            r.share_inputs()
+
+    def bind_output(self, out: np.ndarray):
+        for r, (lo, L) in zip(self.runs, self.ranges):
+            r.bind_output(out[lo:lo + L])
+
+    def online(self, coin_fn=None):
+        """Returns (per-party sigma partials summed over the chunks, device ms of the whole
+        set — from the first chunk's start event to the latest chunk's end event —, the
+        chunk reports)."""
+        for r in self.runs:
+            r.online_begin()
+        coin = coin_fn() if coin_fn is not None else self.coin
+        for r in self.runs:
+            r.mac_check_launch(coin)
+        reps = [r.mac_check() for r in self.runs]
+        span = 0.0
+        for r in self.runs:
+            ms = C.c_float()
+            check(lib().spdz_run_span_ms(self.runs[0].h, r.h, C.byref(ms)))
+            span = max(span, ms.value)
+        sig = [sum(rep.sigmas[p] for rep in reps) % 4294967291 for p in range(self.n)]
+        return sig, span, reps
+
+
 def run_local(graph: Graph, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,
               coin: int | None = None, devices=None) -> RunReport:
     """runtime::run_local (runtime.cpp:586-613) on B200: deal, share inputs, online phase."""

@@ -24,15 +24,29 @@ def _free_port():
     return port
 
 
-def _party(rank, world, port, kind, n, coin, q):
+def _party(rank, world, port, kind, n, coin, q, chunks=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_11112_b200 import LocalRun, chain_graph
+        from paper_2512_11112_b200 import ChunkedRun, LocalRun, chain_graph
         x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+        if chunks:  # lane chunks on their own streams, one MAC check (ChunkedRun)
+            r = ChunkedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks, single_party=rank, coin=coin)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, r.export_ipc())
+            r.import_ipc(blobs)
+            if rank == 0:
+                r.bind_inputs({"x": x, "y": y})
+            r.share_inputs()
+            sig, ms, reps = r.online()
+            out = np.concatenate([rep.outputs for rep in reps])
+            q.put((rank, out.copy(), sig[rank]))
+            dist.barrier()
+            r.close()
+            return
         r = LocalRun(chain_graph(kind, n), 2, coin=coin, single_party=rank)
         blobs = [None] * world
         dist.all_gather_object(blobs, r.export_ipc())
@@ -51,14 +65,14 @@ def _party(rank, world, port, kind, n, coin, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["heavy", "mixed"])
-def test_two_party_processes_over_ipc(gpu, kind):
+@pytest.mark.parametrize("kind,chunks", [("heavy", 0), ("mixed", 0), ("heavy", 3)])
+def test_two_party_processes_over_ipc(gpu, kind, chunks):
     n, coin = 4099, 0xC0FFEE
     want = O.sim_chain(kind, 2, O.rand_field_vec(n, 1), O.rand_field_vec(n, 2), 1, coin)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_party, args=(r, 2, port, kind, n, coin, q)) for r in range(2)]
+    procs = [ctx.Process(target=_party, args=(r, 2, port, kind, n, coin, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -73,3 +87,23 @@ def test_two_party_processes_over_ipc(gpu, kind):
         np.testing.assert_array_equal(res[rank][1], want["outputs"])
         assert res[rank][2] == want["sigmas"][rank]
     assert (res[0][2] + res[1][2]) % P == 0
+
+
+def test_chunked_run_local_equals_unsharded(gpu):
+    """ChunkedRun with both parties in this process: outputs and per-party sigmas (fixed
+    coin) equal the unsharded run's; the whole set is timed on the device."""
+    from paper_2512_11112_b200 import ChunkedRun, LocalRun, chain_graph
+    n, coin = 5003, 0xABCDEF
+    x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
+    full = LocalRun(chain_graph("heavy", n), 2, coin=coin)
+    full.bind_inputs({"x": x, "y": y})
+    full.share_inputs()
+    rf = full.online()
+    full.close()
+    cr = ChunkedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=4, coin=coin)
+    cr.bind_inputs({"x": x, "y": y})
+    cr.share_inputs()
+    sig, ms, reps = cr.online()
+    np.testing.assert_array_equal(np.concatenate([rep.outputs for rep in reps]), rf.outputs)
+    assert sig == rf.sigmas and ms > 0
+    cr.close()
