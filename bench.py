@@ -381,11 +381,11 @@ def main():
                     help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run (1 = serial)")
     args = ap.parse_args()
+    if args.impl == "reference":  # CPU only: rank 0 runs it, no process group is needed
+        run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = dist_setup()
-    if args.impl == "reference":
-        run_reference_arm(args, world, rank)
-    else:
-        run_ours(args, world, rank, local)
+    run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
