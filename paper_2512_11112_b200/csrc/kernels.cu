@@ -712,6 +712,88 @@ __global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint3
     }
 }
 
+// Both parties of a 2-party linear layer on one GPU (spdz.cpp:98-124 for each party):
+// the opened D = D0 + reduce(D1) is computed and logged once, each party's A planes,
+// B_t, C and bias give its row result; sum D E (the same for both) is accumulated once.
+// G threads per row (G = 32: a warp per row, shuffle reduction, every row in flight at
+// once when rows are many; G = 256: a block per row for few long rows).
+
+template <int G, bool V4>
+__global__ void __launch_bounds__(kThreads) k_matrix_combine2(MC2Args a) {
+    constexpr int RPB = kThreads / G;  // rows per block
+    const uint32_t g = threadIdx.x % G, slot = threadIdx.x / G;
+    const uint64_t cells = (uint64_t)a.din * a.rows;
+    // r is warp-uniform for G = 32 (warp_sum only) and block-uniform for G = 256 (block_sum)
+    for (uint32_t r = blockIdx.x * RPB + slot; r < a.rows; r += gridDim.x * RPB) {
+        const uint64_t base = (uint64_t)r * a.din;
+        const uint64_t toff = (uint64_t)(r / a.rpt) * a.din;
+        const uint32_t* E = a.opened + cells + toff;
+        unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
+        if (V4) {
+            for (uint32_t c4 = g; c4 < a.din / 4; c4 += G) {
+                const uint64_t gg = base / 4 + c4;
+                const uint4 d0 = ld4(a.D0, gg), d1 = ld4(a.D1, gg);
+                const uint32_t d[4] = {fp_add(d0.x, fp_reduce32(d1.x)), fp_add(d0.y, fp_reduce32(d1.y)),
+                                       fp_add(d0.z, fp_reduce32(d1.z)), fp_add(d0.w, fp_reduce32(d1.w))};
+                st4(a.opened, gg, d);
+                const uint4 e4 = reinterpret_cast<const uint4*>(E)[c4];
+                const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+                for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const uint4 av = ld4(a.A[p][0], gg), am = ld4(a.A[p][1], gg);
+                    const uint4 bv = reinterpret_cast<const uint4*>(a.B[p][0] + toff)[c4];
+                    const uint4 bm = reinterpret_cast<const uint4*>(a.B[p][1] + toff)[c4];
+                    const uint32_t AV[4] = {av.x, av.y, av.z, av.w}, AM[4] = {am.x, am.y, am.z, am.w};
+                    const uint32_t BV[4] = {bv.x, bv.y, bv.z, bv.w}, BM[4] = {bm.x, bm.y, bm.z, bm.w};
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
+                        acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
+                    }
+                }
+            }
+        } else {
+            for (uint32_t c = g; c < a.din; c += G) {
+                const uint32_t d = fp_add(a.D0[base + c], fp_reduce32(a.D1[base + c]));
+                a.opened[base + c] = d;
+                const uint32_t e = E[c];
+                acc[4] += fold1(mul_wide(d, e));
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    acc[2 * p] += fold1(mul_wide(d, a.B[p][0][toff + c])) + fold1(mul_wide(a.A[p][0][base + c], e));
+                    acc[2 * p + 1] += fold1(mul_wide(d, a.B[p][1][toff + c])) + fold1(mul_wide(a.A[p][1][base + c], e));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[q] = fold1(acc[q]);  // < din/G * 12 * 2^32 before: safe below 2^64
+        if (G == 32) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[q] = warp_sum(acc[q]);
+        } else {
+            block_sum<5>(acc);
+        }
+        if (g == 0) {
+            const uint32_t de = fp_reduce64(acc[4]);
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {  // spdz.cpp:117-123, linear.cpp:59
+                uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(acc[2 * p]));
+                if (p == 0) vr = fp_add(vr, de);
+                uint32_t mr = fp_add(fp_reduce64((unsigned long long)a.Cc[p][1][r] + fp_reduce64(acc[2 * p + 1])),
+                                     fp_mul(a.alpha[p], de));
+                if (a.bias[p][0]) {
+                    vr = fp_add(vr, a.bias[p][0][r]);
+                    mr = fp_add(mr, a.bias[p][1][r]);
+                }
+                a.z[p][0][r] = vr;
+                a.z[p][1][r] = mr;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // CUDA-core modular GEMM: C (MxN) = A (MxK) * B (KxN) mod p, row-major.
 // A is split into 16-bit halves when staged to shared memory, so each MAC is
@@ -1125,6 +1207,26 @@ cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, u
 #undef CASE
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms) {
+    if (a.rows == 0) return cudaSuccess;
+    if (a.rpt == 0) return cudaErrorInvalidValue;
+    bool v4 = a.din % 4 == 0 && aligned16(a.D0) && aligned16(a.D1) && aligned16(a.opened);
+    for (int p = 0; p < 2; ++p)
+        v4 = v4 && aligned16(a.A[p][0]) && aligned16(a.A[p][1]) && aligned16(a.B[p][0]) && aligned16(a.B[p][1]);
+    const bool warp_rows = a.rows >= (uint32_t)sms * 8;  // enough rows to fill the GPU one warp each
+    if (warp_rows) {
+        const uint32_t blocks = (a.rows + kThreads / 32 - 1) / (kThreads / 32);
+        const int grid = (int)(blocks < (uint32_t)sms * 8 ? blocks : (uint32_t)sms * 8);
+        if (v4) k_matrix_combine2<32, true><<<grid, kThreads, 0, s>>>(a);
+        else k_matrix_combine2<32, false><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        const int grid = (int)(a.rows < (uint32_t)sms * 8 ? a.rows : (uint32_t)sms * 8);
+        if (v4) k_matrix_combine2<256, true><<<grid, kThreads, 0, s>>>(a);
+        else k_matrix_combine2<256, false><<<grid, kThreads, 0, s>>>(a);
+    }
+    return launched();
 }
 
 cudaError_t launch_modgemm(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,

@@ -56,6 +56,20 @@ cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const u
                                   uint32_t* open_d, uint32_t* open_e, uint64_t n, int sms,
                                   const uint32_t* alpha_dev = nullptr);
 cudaError_t launch_set_word(cudaStream_t s, uint32_t* p, uint32_t v);
+// Both parties' matrix combine (spdz.cpp:98-124) in one pass on one GPU (kernels.cu MC2Args).
+struct MC2Args {
+    uint32_t din, rows, rpt;
+    const uint32_t* D0;
+    const uint32_t* D1;
+    const uint32_t* A[2][2];
+    const uint32_t* B[2][2];
+    const uint32_t* Cc[2][2];
+    const uint32_t* bias[2][2];
+    uint32_t alpha[2];
+    uint32_t* z[2][2];
+    uint32_t* opened;
+};
+cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms);
 // Input sharing for both parties of a 2-party run on one GPU: mask = {v0, m0, v1, m1}
 // input-mask shares, out = {v0, m0, v1, m1} input shares (preproc.cpp:205-243).
 cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uint32_t* r_clear,

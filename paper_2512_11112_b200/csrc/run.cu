@@ -1054,6 +1054,52 @@ struct Exec {
             tend(p, tk, SPDZ_KSTAT_MASK, 12 * cells + 12 * etot);
             sent[p] = publish(p, slot_of(id, 0));
         }
+        bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+        for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
+        if (fuse2) {  // both parties in one pass: [D|E] opened and logged once, per-party rows
+            auto &P0 = r->parties[0], &P1 = r->parties[1];
+            auto &s0 = P0.ns[id], &s1 = P1.ns[id];
+            dev(r, 0);
+            const int tk = tbegin(0);
+            const uint32_t* peE[1] = {s1.payload + cells};
+            lk(launch_open_sum(S(r, 0), s0.payload + cells, peE, 1, s0.opened + cells, etot, SMS(r, 0)), "open E");
+            MC2Args a{};
+            a.din = din;
+            a.rows = dout;
+            a.rpt = lt.rpt;
+            a.D0 = s0.payload;
+            a.D1 = s1.payload;
+            for (int p = 0; p < 2; ++p) {
+                auto& st = r->parties[p].ns[id];
+                for (int q = 0; q < 2; ++q) {
+                    a.A[p][q] = st.mA[q];
+                    a.B[p][q] = st.mB[q];
+                    a.Cc[p][q] = st.mC[q];
+                }
+                a.bias[p][0] = st.bias_v;
+                a.bias[p][1] = st.bias_m;
+                a.alpha[p] = r->parties[p].ctx->alpha;
+                a.z[p][0] = st.out.v;
+                a.z[p][1] = st.out.m;
+            }
+            a.opened = s0.opened;
+            lk(launch_matrix_combine2(S(r, 0), a, SMS(r, 0)), "k_matrix_combine2");
+            // D0 4 + D1 4 + two parties' A.v A.m 16 + opened D 4 per cell (B, E from cache)
+            tend(0, tk, SPDZ_KSTAT_COMBINE, 28 * cells);
+            r->exchanged += 2 * (cells + etot) * 4;
+            for (int p = 0; p < 2; ++p) {
+                auto& P = r->parties[p];
+                const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out;
+                auto& st = P.ns[id];
+                for (uint32_t t = 0; t < ntiles; ++t) {  // linear.cpp:113 log per tile: [D_t | E_t]
+                    const uint64_t aoff = (uint64_t)lt.starts[t] * din, ct = (uint64_t)lt.counts[t] * din;
+                    P.maclog.push_back({s0.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
+                    P.maclog.push_back({s0.opened + cells + (uint64_t)t * din, x.m, st.mB[1] + (uint64_t)t * din,
+                                        din, 0, batch0 + t, ct, 0});
+                }
+            }
+            return;
+        }
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
