@@ -280,6 +280,17 @@ def main():
         bm["reference_batch1_online_ms"] = c4[0]["reference_online_ms"]
     res["C4_batched_secret_secret"] = bm
     print("C4 batched", bm, flush=True)
+
+    # C5 on one GPU: the 2^28-element mixed workload, both parties resident in HBM (the
+    # multi-GPU layouts of C5 are bench.py --gpus N)
+    if not args.quick:
+        n = 1 << 28
+        inp = {"x": rnd(n, 1), "y": rnd(n, 2)}
+        gr = gpu_online(chain_graph("mixed", n), inp, reps=2)
+        gr.update(kind="mixed", lanes=n, mults_per_s=2 * n / (gr["online_device_ms"] / 1e3),
+                  hbm_gb_allocated=torch.cuda.mem_get_info()[1] / 1e9 - torch.cuda.mem_get_info()[0] / 1e9)
+        res["C5_mixed_2e28_one_gpu"] = gr
+        print("C5 1gpu", gr["online_device_ms"], flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(out, indent=1))
     print(json.dumps(out)[:2000])
