@@ -295,6 +295,8 @@ def run_ours(args, world, rank, local):
             run.deal(4000 + w)
             run.run(inputs)
         torch.cuda.synchronize()
+    if world > 1:  # chunk by chunk through one in-order H2D stream (ChunkedRun.run_e2e)
+        run.stream_copies()
     e2e_ms = 0.0
     parts = np.zeros(3)
     for k in range(args.steps):
@@ -304,6 +306,10 @@ def run_ours(args, world, rank, local):
         t0 = time.perf_counter()
         if streamed:
             rep = run.run(inputs)        # H2D, input sharing, online phase, D2H, MAC check
+            t1 = t2 = t3 = time.perf_counter()
+        elif world > 1:
+            sig, _, _ = run.run_e2e(inputs if owns_inputs else None, coin_fn=coin_fn)
+            parallel.verify_sharded_sigmas(sig)
             t1 = t2 = t3 = time.perf_counter()
         else:
             if owns_inputs:
@@ -357,8 +363,9 @@ def run_ours(args, world, rank, local):
                            "l2": "working set >> 126 MB L2 (inputs larger than L2, no flush needed)",
                            "timed": "online phase only (dealer + input sharing between steps, untimed)"},
                 "clocks": clocks, "gpu_launches": launches,
-                "e2e": {"value": e2e, "unit": UNIT, "mode": f"host-streamed, {args.e2e_chunks} lane chunks"
-                        if streamed else "serial", "h2d_bytes_per_step": 2 * total * 4,
+                "e2e": {"value": e2e, "unit": UNIT,
+                        "mode": (f"host-streamed, {args.e2e_chunks} lane chunks" if streamed else
+                                 f"host-streamed per GPU, {args.exchange_chunks} lane chunks" if world > 1 else "serial"), "h2d_bytes_per_step": 2 * total * 4,
                         "d2h_bytes_per_step": total * 4 * (1 if world == 1 else 2),
                         "ms_per_step": e2e_ms / args.steps},
                 "roofline": roofline, "cpu_baseline": cpu_baseline}

@@ -503,12 +503,35 @@ class ChunkedRun:
         for r, (lo, L) in zip(self.runs, self.ranges):
             r.bind_output(out[lo:lo + L])
 
+    def stream_copies(self):
+        """Queue every chunk's input H2D (and output D2H) on one shared stream each, in chunk
+        order, so chunk c computes while chunk c+1's inputs cross PCIe (see StreamedRun)."""
+        import torch
+        if getattr(self, "_copy_streams", None) is None:
+            self._copy_streams = (torch.cuda.Stream(), torch.cuda.Stream())
+            for r in self.runs:
+                r.set_copy_streams(*self._copy_streams)
+
+    def run_e2e(self, inputs: dict | None, coin_fn=None):
+        """Host inputs to opened outputs (bound with bind_output) through the public calls,
+        chunk by chunk: bind (H2D), share, online phase; then one MAC check for all chunks.
+        `inputs` is None on ranks that own no private input."""
+        for r, (lo, L) in zip(self.runs, self.ranges):
+            if inputs is not None:
+                r.bind_inputs({k: v[lo:lo + L] for k, v in inputs.items()})
+            r.share_inputs()
+            r.online_begin()
+        return self._finish(coin_fn)
+
     def online(self, coin_fn=None):
         """Returns (per-party sigma partials summed over the chunks, device ms of the whole
         set — from the first chunk's start event to the latest chunk's end event —, the
         chunk reports)."""
         for r in self.runs:
             r.online_begin()
+        return self._finish(coin_fn)
+
+    def _finish(self, coin_fn):
         coin = coin_fn() if coin_fn is not None else self.coin
         for r in self.runs:
             r.mac_check_launch(coin)
