@@ -249,6 +249,15 @@ int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uin
 /* Contraction path of spdz_linear_secret_public: 0 auto (tcgen05 kind::i8 limb GEMM
  * when din <= 8192, else CUDA cores), 1 CUDA-core IMAD.WIDE GEMM, 2 tcgen05 only. */
 int spdz_set_gemm_path(int path);
+/* A public weight matrix prepared once for many secret x public calls (the layer's weights
+ * in an inference loop): its tcgen05 limb image is built at creation, so each call only
+ * re-lays out X.  W row-major dout x din (device), din <= 8192. */
+typedef struct spdz_linear_weights spdz_linear_weights;
+int spdz_linear_weights_create(spdz_ctx* ctx, uint32_t dout, uint32_t din, const uint32_t* w_public,
+                               spdz_linear_weights** out);
+int spdz_linear_weights_destroy(spdz_linear_weights* w);
+int spdz_linear_secret_public_prepared(spdz_ctx* ctx, const spdz_linear_weights* w, uint32_t batch,
+                                       const spdz_share_t* x_secret, spdz_share_t* y);
 int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32_t batch, int w_public,
                               const uint32_t* w_vals, const spdz_share_t* w_secret, const spdz_share_t* x_secret,
                               const uint32_t* x_pub, spdz_share_t* y);

@@ -123,6 +123,9 @@ _SIGS = {
     "spdz_bmatrix_open_combine": (C.c_int, [vp, C.POINTER(BMTriple), vp, C.POINTER(vp), C.c_int, C.POINTER(Share),
                                             vp]),
     "spdz_set_gemm_path": (C.c_int, [C.c_int]),
+    "spdz_linear_weights_create": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, C.POINTER(vp)]),
+    "spdz_linear_weights_destroy": (C.c_int, [vp]),
+    "spdz_linear_secret_public_prepared": (C.c_int, [vp, vp, C.c_uint32, C.POINTER(Share), C.POINTER(Share)]),
     "spdz_linear_secret_public": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, vp, C.POINTER(Share),
                                             C.POINTER(Share), vp, C.POINTER(Share)]),
     "spdz_dealer_alpha": (C.c_int, [C.c_int, C.c_uint64, u32p, u32p]),

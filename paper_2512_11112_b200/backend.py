@@ -159,6 +159,14 @@ class Context:
         arr = (C.c_void_p * max(1, len(peers)))(*[p.data_ptr() for p in peers])
         check(lib().spdz_open_sum(self.h, own.data_ptr(), arr, len(peers), own.numel(), out.data_ptr()))
 
+    # secret x public linear layer with the public W prepared once (runtime.cpp:303-334)
+    def prepare_weights(self, w, dout: int, din: int) -> "LinearWeights":
+        return LinearWeights(self, w, dout, din)
+
+    def linear_secret_public_prepared(self, weights: "LinearWeights", batch: int, x, y):
+        check(lib().spdz_linear_secret_public_prepared(self.h, weights.h, batch, C.byref(dshare(x)),
+                                                       C.byref(dshare(y))))
+
     # batched secret x secret linear layer (linear.cpp:30-61 / spdz.cpp:98-124 over `batch` columns)
     def bmatrix_mask(self, w, x, t, payload):
         check(lib().spdz_bmatrix_mask(self.h, C.byref(dshare(w)), C.byref(dshare(x)), C.byref(dbmtriple(t)),
@@ -212,6 +220,27 @@ def dshare(s) -> Share:
 
 def dtriple(t) -> Triple:
     return Triple(dshare(t.a), dshare(t.b), dshare(t.c))
+
+
+class LinearWeights:
+    """A public dout x din weight matrix (device uint32 tensor) laid out once as the tcgen05
+    GEMM's A-side limb image, for repeated secret x public calls."""
+
+    def __init__(self, ctx: "Context", w, dout: int, din: int):
+        h = C.c_void_p()
+        check(lib().spdz_linear_weights_create(ctx.h, dout, din, w.data_ptr(), C.byref(h)))
+        self.h, self.dout, self.din = h, dout, din
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().spdz_linear_weights_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass

@@ -650,6 +650,69 @@ static void modgemm_dispatch(spdz_ctx* ctx, int mode, uint32_t dout, uint32_t di
     }
 }
 
+struct spdz_linear_weights {
+    int device = 0;
+    uint32_t dout = 0, din = 0;
+    uint8_t* image = nullptr;  // tcgen05 A-side limb image of W
+};
+
+int spdz_linear_weights_create(spdz_ctx* ctx, uint32_t dout, uint32_t din, const uint32_t* w_public,
+                               spdz_linear_weights** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(out && (w_public || din == 0 || dout == 0), SPDZ_ERR_INVALID_ARGUMENT, "bad weights args");
+        need(modgemm_tc_supported(din), SPDZ_ERR_INVALID_ARGUMENT, "prepared weights need 1 <= din <= 8192");
+        device_guard(ctx);
+        auto* w = new spdz_linear_weights;
+        w->device = ctx->device;
+        w->dout = dout;
+        w->din = din;
+        try {
+            cuda_check(cudaMalloc(&w->image, std::max<uint64_t>(modgemm_tc_a_image_bytes(0, dout, din), 16)),
+                       "cudaMalloc(weights)");
+            if (dout)
+                launch_ok(launch_tile_a(ctx->stream, 0, dout, din, w_public, w_public, w->image, ctx->sms),
+                          "tile W");
+        } catch (...) {
+            if (w->image) cudaFree(w->image);
+            delete w;
+            throw;
+        }
+        *out = w;
+    });
+}
+
+int spdz_linear_weights_destroy(spdz_linear_weights* w) {
+    return guard([&] {
+        if (!w) return;
+        cudaSetDevice(w->device);
+        cudaDeviceSynchronize();  // the image may still be read by queued GEMMs
+        if (w->image) cudaFree(w->image);
+        delete w;
+    });
+}
+
+int spdz_linear_secret_public_prepared(spdz_ctx* ctx, const spdz_linear_weights* w, uint32_t batch,
+                                       const spdz_share_t* x_secret, spdz_share_t* y) {
+    return guard([&] {  // runtime.cpp:303-334 with W's re-layout done once (spdz_linear_weights_create)
+        need_ctx(ctx);
+        need(w != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null weights");
+        need(w->device == ctx->device, SPDZ_ERR_INVALID_ARGUMENT, "weights live on another device");
+        need_share(x_secret, "x");
+        need_share(y, "y");
+        check_lanes(x_secret->lanes, (uint64_t)w->din * batch);
+        check_lanes(y->lanes, (uint64_t)w->dout * batch);
+        device_guard(ctx);
+        if (w->dout == 0 || batch == 0) return;
+        uint8_t* scratch = (uint8_t*)ctx->scratch.ensure(modgemm_tc_scratch_bytes(0, w->dout, w->din, batch));
+        TcAux aux;
+        aux.a_image = w->image;
+        launch_ok(launch_modgemm_tc(ctx->stream, 0, w->dout, w->din, batch, nullptr, nullptr, x_secret->vals,
+                                    x_secret->macs, y->vals, y->macs, scratch, ctx->sms, &aux),
+                  "k_modgemm_tc (prepared W)");
+    });
+}
+
 int spdz_linear_secret_public(spdz_ctx* ctx, uint32_t din, uint32_t dout, uint32_t batch, int w_public,
                               const uint32_t* w_vals, const spdz_share_t* w_secret, const spdz_share_t* x_secret,
                               const uint32_t* x_pub, spdz_share_t* y) {

@@ -447,18 +447,20 @@ uint32_t g_tc_dbg = 0;
 template <int BN>
 cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
                    const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx, uint8_t* scratch,
-                   const TcOut& out, int sms) {
+                   const uint8_t* a_image, const TcOut& out, int sms) {
     const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
     const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
     const uint32_t KB = (din + TK - 1) / TK;
-    uint8_t* At = scratch;
-    uint8_t* Bt = scratch + (uint64_t)4 * Mp * KB * TK;
+    // a prepared A image (spdz_linear_weights) is used as is: only B is re-laid out
+    const uint8_t* At = a_image ? a_image : scratch;
+    uint8_t* Bt = a_image ? scratch : scratch + (uint64_t)4 * Mp * KB * TK;
     bool pdl = false;
     if (!(g_tc_dbg & 8)) {  // (diagnostic bit 3 skips the re-layout kernels)
         const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
-        const uint32_t row_blocks = (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
+        const uint32_t row_blocks =
+            a_image ? 0u : (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
         const uint32_t col_blocks = KB * ((Np + 31) / 32);
-        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, At};
+        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, scratch};
         const ColsArgs ca{x0, mode == 0 ? x1 : x0, batch, N, din, KB, mode == 0 ? bx : TcBx{}, Bt};
         k_tile_both<BN><<<row_blocks + col_blocks, 256, 0, s>>>(ra, ca, row_blocks, KB);
         ++g_kernel_launches;
@@ -518,8 +520,28 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
     // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
     const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
     const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
-    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, out, sms);
-    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, out, sms);
+    const uint8_t* ai = aux ? aux->a_image : nullptr;
+    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, ai, out, sms);
+    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, ai, out, sms);
+}
+
+// The A-side limb image alone (a public weight matrix prepared once for many calls).
+uint64_t modgemm_tc_a_image_bytes(int mode, uint32_t dout, uint32_t din) {
+    const uint64_t M = mode == 0 ? dout : 2ull * dout;
+    const uint64_t Mp = (M + TM - 1) / TM * TM, Kp = (din + TK - 1) / TK * TK;
+    return 4 * Mp * Kp;
+}
+
+cudaError_t launch_tile_a(cudaStream_t s, int mode, uint32_t dout, uint32_t din, const uint32_t* w0,
+                          const uint32_t* w1, uint8_t* image, int sms) {
+    const uint32_t M = mode == 0 ? dout : 2 * dout;
+    const uint32_t Mp = (M + TM - 1) / TM * TM, KB = (din + TK - 1) / TK;
+    const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+    const uint32_t row_blocks = (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
+    const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, image};
+    k_tile_both<64><<<row_blocks, 256, 0, s>>>(ra, ColsArgs{}, row_blocks, 1);
+    ++g_kernel_launches;
+    return cudaGetLastError();
 }
 
 }  // namespace spdzb200

@@ -133,7 +133,11 @@ struct TcAux {
     uint32_t coef0 = 0, coef1 = 0;
     const uint32_t* add0 = nullptr;
     const uint32_t* add1 = nullptr;
+    const uint8_t* a_image = nullptr;  // prepared A limb image (launch_tile_a): skip its re-layout
 };
+uint64_t modgemm_tc_a_image_bytes(int mode, uint32_t dout, uint32_t din);
+cudaError_t launch_tile_a(cudaStream_t s, int mode, uint32_t dout, uint32_t din, const uint32_t* w0,
+                          const uint32_t* w1, uint8_t* image, int sms);
 cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch,
                               const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1,
                               uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms, const TcAux* aux = nullptr);

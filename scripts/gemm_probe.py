@@ -86,6 +86,27 @@ for path in ((2,) if "--tc-only" in sys.argv else (2, 1)):
     torch.cuda.synchronize()
     print(f"path {path}: {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call", flush=True)
 
+if "--prepared" in sys.argv:  # W laid out once (spdz_linear_weights): per call only X's re-layout + GEMM
+    wts = ctx.prepare_weights(W, dout, din)
+    pargs = (ctx.h, wts.h, batch, C.byref(dshare(xs)), C.byref(dshare(ys)))
+    for _ in range(3):
+        check(lib().spdz_linear_secret_public_prepared(*pargs))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ctx.use_torch_stream()
+        for _ in range(10):
+            check(lib().spdz_linear_secret_public_prepared(*pargs))
+    ctx.use_torch_stream()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"prepared W: graphed {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call", flush=True)
+
 if "--int8-peak" in sys.argv:
     # measured dense int8 tensor peak on this device: cuBLASLt IMMA through torch._int_mm
     for nn in (8192, 16384):

@@ -551,3 +551,24 @@ def test_batched_secret_secret_linear(gpu, din, dout, batch):
             zv, zm = O.matrix_combine(din, dout, mt, D, Em[:, j].copy(), p, d.alpha_share(p))
             np.testing.assert_array_equal(zs[p][0].reshape(dout, batch)[:, j], zv)
             np.testing.assert_array_equal(zs[p][1].reshape(dout, batch)[:, j], zm)
+
+
+@pytest.mark.parametrize("din,dout,batch", [(1024, 1024, 256), (300, 130, 70), (512, 2048, 300)])
+def test_prepared_weights_equal_per_call(gpu, din, dout, batch):
+    """spdz_linear_secret_public_prepared (W laid out once) == the per-call path, twice in a row
+    (the prepared image is reused), both planes."""
+    from paper_2512_11112_b200 import DeviceShare
+    W = O.rand_field_vec(din * dout, 21)
+    Xv, Xm = O.rand_field_vec(din * batch, 22), O.rand_field_vec(din * batch, 23)
+    c = ctx()
+    Wd = T(W)
+    wts = c.prepare_weights(Wd, dout, din)
+    x = share(Xv, Xm)
+    want = (_np_modmatmul(W.reshape(dout, din), Xv.reshape(din, batch)),
+            _np_modmatmul(W.reshape(dout, din), Xm.reshape(din, batch)))
+    for _ in range(2):
+        y = DeviceShare.empty(dout * batch)
+        c.linear_secret_public_prepared(wts, batch, x, y)
+        np.testing.assert_array_equal(H(y.vals).reshape(dout, batch), want[0])
+        np.testing.assert_array_equal(H(y.macs).reshape(dout, batch), want[1])
+    wts.close()
