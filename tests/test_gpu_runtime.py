@@ -332,3 +332,39 @@ def test_inputs_above_p_are_reduced(gpu, n_parties):
     rep = r.online()
     np.testing.assert_array_equal(rep.outputs, want)
     r.close()
+
+
+@pytest.mark.parametrize("n_parties,slice_", [(3, 200), (3, 262140), (4, 1000)])
+def test_linear_secret_secret_multiparty(gpu, n_parties, slice_):
+    """The per-party linear path (n > 2: no co-located-pair fusion): y = W x + b mod p."""
+    from paper_2512_11112_b200 import linear_graph, run_local
+    din, dout = 96, 40
+    rng = np.random.default_rng(n_parties + slice_)
+    x = rng.integers(0, P, din, dtype=np.uint64).astype(np.uint32)
+    W = rng.integers(0, P, din * dout, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, P, dout, dtype=np.uint64).astype(np.uint32)
+    rep = run_local(linear_graph(din, dout), n_parties, {"x": x, "W": W, "b": b}, slice_=slice_)
+    want = (W.reshape(dout, din).astype(object) @ x.astype(object) + b.astype(object)) % P
+    np.testing.assert_array_equal(rep.outputs, want.astype(np.uint32))
+    assert sum(rep.sigmas) % P == 0
+
+
+def test_bitflip_on_linear_layer_aborts(gpu):
+    """A tampered [D|E] word on a 2-party linear layer (per-party path) fails the MAC check."""
+    from paper_2512_11112_b200 import LocalRun, errors, linear_graph
+    from paper_2512_11112_b200.runtime import LINEAR
+    din, dout = 64, 32
+    rng = np.random.default_rng(3)
+    inp = {"x": rng.integers(0, P, din, dtype=np.uint64).astype(np.uint32),
+           "W": rng.integers(0, P, din * dout, dtype=np.uint64).astype(np.uint32),
+           "b": rng.integers(0, P, dout, dtype=np.uint64).astype(np.uint32)}
+    g = linear_graph(din, dout)
+    lin = [i for i, nd in enumerate(g.nodes) if nd.kind == LINEAR][0]
+    for word in (5, din * dout + 3):
+        r = LocalRun(g, 2, slice_=500)
+        r.bind_inputs(inp)
+        r.share_inputs()
+        r.inject_bitflip(lin, 0, 1, word, 7)
+        with pytest.raises(errors.MacCheckFailed):
+            r.online()
+        r.close()
