@@ -236,8 +236,8 @@ int spdz_matrix_combine(spdz_ctx* ctx, const spdz_mtriple_t* mt, const uint32_t*
  *   values; required), then per column j exactly spdz::matrix_combine({A, B[:,j], C[:,j]},
  *   D, E[:,j]):  Z.v = C.v + D B.v + A.v E (+ D E on party 0),
  *                Z.m = C.m + D B.m + A.m E + alpha_i D E,
- *   as two tcgen05 limb GEMMs: D [B.v + [p0] E | B.m + alpha_i E] and [A.v ; A.m] E.
- *   Needs din <= 8192 (the s32 limb-accumulator bound). */
+ *   as two tcgen05 limb GEMMs: D [B.v + [p0] E | B.m + alpha_i E] and [A.v ; A.m] E
+ *   (K sliced by 8192, the s32 limb-accumulator bound). */
 int spdz_bmatrix_mask(spdz_ctx* ctx, const spdz_share_t* w, const spdz_share_t* x, const spdz_bmtriple_t* t,
                       uint32_t* payload);
 int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uint32_t* own_payload,
@@ -246,8 +246,9 @@ int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uin
  * on both planes.  w_public != 0: W public (w_vals), X secret (x->vals/x->macs,
  * row-major din x batch).  w_public == 0: W secret (w->vals/w->macs), X public
  * (x_pub).  Y row-major dout x batch.  Bias is a separate spdz_add_batch. */
-/* Contraction path of spdz_linear_secret_public: 0 auto (tcgen05 kind::i8 limb GEMM
- * when din <= 8192, else CUDA cores), 1 CUDA-core IMAD.WIDE GEMM, 2 tcgen05 only. */
+/* Contraction path of spdz_linear_secret_public: 0 auto (tcgen05 kind::i8 limb GEMM; din
+ * beyond 8192 runs as K slices of 8192 accumulated exactly mod p), 1 CUDA-core IMAD.WIDE
+ * GEMM, 2 tcgen05 only. */
 int spdz_set_gemm_path(int path);
 /* A public weight matrix prepared once for many secret x public calls (the layer's weights
  * in an inference loop): its tcgen05 limb image is built at creation, so each call only

@@ -595,7 +595,7 @@ int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uin
         need(own_payload && opened_out, SPDZ_ERR_INVALID_ARGUMENT, "null payload / opened_out");
         need(n_peers >= 0 && n_peers <= kMaxPeers && (n_peers == 0 || peer_payload), SPDZ_ERR_INVALID_ARGUMENT,
              "n_peers out of range");
-        need(modgemm_tc_supported(t->din), SPDZ_ERR_INVALID_ARGUMENT, "batched secret x secret layer needs din <= 8192");
+        need(modgemm_tc_supported(t->din), SPDZ_ERR_INVALID_ARGUMENT, "batched secret x secret layer needs din >= 1");
         device_guard(ctx);
         const uint64_t cells = (uint64_t)t->dout * t->din, ecount = (uint64_t)t->din * t->batch;
         // open [D|E] (net.cpp:170-215): one pass over both halves
@@ -628,7 +628,7 @@ int spdz_bmatrix_open_combine(spdz_ctx* ctx, const spdz_bmtriple_t* t, const uin
     });
 }
 
-static int g_gemm_path = 0;  // 0 auto (tcgen05 when K <= 8192), 1 CUDA-core, 2 tcgen05
+static int g_gemm_path = 0;  // 0 auto (tcgen05, K sliced by 8192), 1 CUDA-core, 2 tcgen05
 
 int spdz_set_gemm_path(int path) {
     return guard([&] {
@@ -641,7 +641,7 @@ static void modgemm_dispatch(spdz_ctx* ctx, int mode, uint32_t dout, uint32_t di
                              const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, uint32_t* y0, uint32_t* y1) {
     const bool tc = g_gemm_path == 2 || (g_gemm_path == 0 && modgemm_tc_supported(din));
     if (tc) {
-        need(modgemm_tc_supported(din), SPDZ_ERR_INVALID_ARGUMENT, "tcgen05 GEMM path needs 1 <= din <= 8192");
+        need(modgemm_tc_supported(din), SPDZ_ERR_INVALID_ARGUMENT, "tcgen05 GEMM path needs din >= 1");
         uint8_t* scratch = (uint8_t*)ctx->scratch.ensure(modgemm_tc_scratch_bytes(mode, dout, din, batch));
         launch_ok(launch_modgemm_tc(ctx->stream, mode, dout, din, batch, w0, w1, x0, x1, y0, y1, scratch, ctx->sms),
                   "k_modgemm_tc");
@@ -661,7 +661,7 @@ int spdz_linear_weights_create(spdz_ctx* ctx, uint32_t dout, uint32_t din, const
     return guard([&] {
         need_ctx(ctx);
         need(out && (w_public || din == 0 || dout == 0), SPDZ_ERR_INVALID_ARGUMENT, "bad weights args");
-        need(modgemm_tc_supported(din), SPDZ_ERR_INVALID_ARGUMENT, "prepared weights need 1 <= din <= 8192");
+        need(din >= 1 && din <= 8192, SPDZ_ERR_INVALID_ARGUMENT, "prepared weights need 1 <= din <= 8192");
         device_guard(ctx);
         auto* w = new spdz_linear_weights;
         w->device = ctx->device;

@@ -39,6 +39,7 @@ namespace {
 
 constexpr int TM = 128;   // rows per CTA tile (UMMA M)
 constexpr int TK = 64;    // K bytes (= elements) per stage
+constexpr uint32_t kMaxKSlice = 8192;  // 4 * 255^2 * K < 2^31: the s32 P_3 accumulator bound
 
 // SMEM matrix descriptor, K-major, SWIZZLE_NONE (layout type 0), sm100 version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -329,14 +330,16 @@ struct RowsArgs {
     const uint32_t* a1;
     uint32_t M0, M, K, Mp, KB;
     uint8_t* out;
+    uint32_t lda;  // row stride of a0/a1 (>= K; larger for a K slice of a wider matrix)
 };
 __device__ __forceinline__ void tile_rows(const RowsArgs& ra, uint64_t t0, uint64_t stride) {
     const uint32_t *a0 = ra.a0, *a1 = ra.a1;
-    const uint32_t M0 = ra.M0, M = ra.M, K = ra.K, Mp = ra.Mp, KB = ra.KB;
+    const uint32_t M0 = ra.M0, M = ra.M, K = ra.K, Mp = ra.Mp, KB = ra.KB, lda = ra.lda;
     uint8_t* out = ra.out;
     constexpr uint32_t kPieces = TM * TK / 16;  // 512 per block
     const uint64_t pieces = (uint64_t)(Mp / TM) * KB * kPieces;
-    const bool v4 = (K % 4) == 0 && ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 15u) == 0;
+    const bool v4 = (K % 4) == 0 && (lda % 4) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 15u) == 0;
     for (uint64_t t = t0; t < pieces; t += stride) {
         const uint64_t blk = t / kPieces;
         const uint32_t q = (uint32_t)(t % kPieces);
@@ -344,7 +347,7 @@ __device__ __forceinline__ void tile_rows(const RowsArgs& ra, uint64_t t0, uint6
         const uint32_t mt = (uint32_t)(blk / KB), kb = (uint32_t)(blk % KB);
         const uint32_t m = mt * TM + r, k0 = kb * TK + kk;
         uint32_t w[16];
-        const uint32_t* row = m < M0 ? a0 + (uint64_t)m * K : a1 + (uint64_t)(m - M0) * K;
+        const uint32_t* row = m < M0 ? a0 + (uint64_t)m * lda : a1 + (uint64_t)(m - M0) * lda;
         if (v4 && m < M && k0 + 16 <= K) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -445,9 +448,9 @@ uint32_t g_tc_dbg = 0;
 // Re-layout both operands into limb images (B tiles BN columns wide), then run
 // the GEMM kernel with TN = BN.
 template <int BN>
-cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t batch, const uint32_t* w0,
-                   const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx, uint8_t* scratch,
-                   const uint8_t* a_image, const TcOut& out, int sms) {
+cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t lda, uint32_t batch,
+                   const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx,
+                   uint8_t* scratch, const uint8_t* a_image, const TcOut& out, int sms) {
     const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
     const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
     const uint32_t KB = (din + TK - 1) / TK;
@@ -460,7 +463,7 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         const uint32_t row_blocks =
             a_image ? 0u : (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
         const uint32_t col_blocks = KB * ((Np + 31) / 32);
-        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, scratch};
+        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, scratch, lda};
         const ColsArgs ca{x0, mode == 0 ? x1 : x0, batch, N, din, KB, mode == 0 ? bx : TcBx{}, Bt};
         k_tile_both<BN><<<row_blocks + col_blocks, 256, 0, s>>>(ra, ca, row_blocks, KB);
         ++g_kernel_launches;
@@ -499,12 +502,13 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
 
 void modgemm_tc_debug(uint32_t flags) { g_tc_dbg = flags; }
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch) {
+    din = std::min<uint32_t>(din, kMaxKSlice);  // one K slice at a time
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
     const uint64_t Mp = (M + TM - 1) / TM * TM, Np = (N + 63) / 64 * 64, Kp = (din + TK - 1) / TK * TK;
     return 4 * (Mp + Np) * Kp + 256;
 }
 
-bool modgemm_tc_supported(uint32_t din) { return din >= 1 && din <= 8192; }
+bool modgemm_tc_supported(uint32_t din) { return din >= 1; }  // K > kMaxKSlice runs as K slices
 
 // Y (dout x batch, two planes) for the secret x public linear layer on tcgen05.
 //   mode 0: W public (w0), X secret planes (x0 vals, x1 macs): C = W * [Xv | Xm]
@@ -515,14 +519,31 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
                               uint32_t* y0, uint32_t* y1, uint8_t* scratch, int sms, const TcAux* aux) {
     if (dout == 0 || batch == 0) return cudaSuccess;
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
-    TcOut out{mode, dout, batch, y0, y1, aux ? aux->add0 : nullptr, aux ? aux->add1 : nullptr};
-    const TcBx bx{aux ? aux->e : nullptr, aux ? aux->coef0 : 0u, aux ? aux->coef1 : 0u};
-    // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
-    const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
-    const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
+    // K slices of at most kMaxKSlice (the s32 limb-accumulator bound); slice i > 0 adds into
+    // the running result through the epilogue addend, so the sum stays exact mod p
     const uint8_t* ai = aux ? aux->a_image : nullptr;
-    if (narrow) return run_tc<32>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, ai, out, sms);
-    return run_tc<64>(s, mode, dout, din, batch, w0, w1, x0, x1, bx, scratch, ai, out, sms);
+    if (ai && din > kMaxKSlice) return cudaErrorInvalidValue;  // prepared images are single-slice
+    for (uint32_t k0 = 0; k0 < din; k0 += kMaxKSlice) {
+        const uint32_t kc = std::min<uint32_t>(kMaxKSlice, din - k0);
+        TcOut out{mode, dout, batch, y0, y1, aux ? aux->add0 : nullptr, aux ? aux->add1 : nullptr};
+        if (k0 > 0) {
+            out.add0 = y0;
+            out.add1 = y1;
+        }
+        const uint64_t xo = (uint64_t)k0 * batch;  // X rows k0.. (row-major din x batch)
+        TcBx bx{aux && aux->e ? aux->e + xo : nullptr, aux ? aux->coef0 : 0u, aux ? aux->coef1 : 0u};
+        const uint32_t* a0 = w0 ? w0 + k0 : nullptr;
+        const uint32_t* a1 = w1 ? w1 + k0 : nullptr;
+        const uint32_t* b0 = x0 + xo;
+        const uint32_t* b1 = x1 ? x1 + xo : nullptr;
+        // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
+        const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
+        const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
+        cudaError_t e = narrow ? run_tc<32>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms)
+                               : run_tc<64>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // The A-side limb image alone (a public weight matrix prepared once for many calls).
@@ -538,7 +559,7 @@ cudaError_t launch_tile_a(cudaStream_t s, int mode, uint32_t dout, uint32_t din,
     const uint32_t Mp = (M + TM - 1) / TM * TM, KB = (din + TK - 1) / TK;
     const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
     const uint32_t row_blocks = (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
-    const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, image};
+    const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, image, din};
     k_tile_both<64><<<row_blocks, 256, 0, s>>>(ra, ColsArgs{}, row_blocks, 1);
     ++g_kernel_launches;
     return cudaGetLastError();

@@ -295,14 +295,12 @@ def test_matrix_mask_open_combine_two_party(gpu, golden):
                                             (8192, 40, 3), (40000, 3, 2)])
 def test_linear_secret_public_vs_oracle(gpu, din, dout, batch, path):
     """runtime.cpp:303-334, batched over `batch` input columns, on both contraction
-    paths (1 = CUDA-core IMAD.WIDE, 2 = tcgen05 kind::i8 limb GEMM; K=8192 is the
-    tcgen05 exactness limit, K=40000 crosses the CUDA-core accumulator fold)."""
+    paths (1 = CUDA-core IMAD.WIDE, 2 = tcgen05 kind::i8 limb GEMM; K=8192 is one
+    tcgen05 K slice, K=40000 runs as 5 slices and crosses the CUDA-core accumulator fold)."""
     import ctypes as C
     from paper_2512_11112_b200 import DeviceShare
     from paper_2512_11112_b200._lib import check, lib
     from paper_2512_11112_b200.backend import dshare
-    if path == 2 and din > 8192:
-        pytest.skip("tcgen05 path covers din <= 8192")
     check(lib().spdz_set_gemm_path(path))
     try:
         _linear_secret_public_case(din, dout, batch)
@@ -456,7 +454,8 @@ def _np_modmatmul(A, B):
 
 @pytest.mark.parametrize("tiles", [0, 64, 128])
 @pytest.mark.parametrize("din,dout,batch,fill", [(512, 2048, 300, "rand"), (8192, 256, 64, "max"),
-                                                 (300, 130, 70, "rand"), (64, 1200, 520, "rand")])
+                                                 (300, 130, 70, "rand"), (64, 1200, 520, "rand"),
+                                                 (20000, 192, 40, "max"), (8200, 130, 33, "rand")])
 def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
     """Every output of the tcgen05 GEMM (both planes, both modes) against an exact
     numpy mod-p matmul: persistent tiles (more tiles than SMs), edge tiles, and
@@ -498,7 +497,7 @@ def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
         check(lib().spdz_set_gemm_path(0))
 
 
-@pytest.mark.parametrize("din,dout,batch", [(96, 200, 40), (512, 384, 300), (1024, 256, 130)])
+@pytest.mark.parametrize("din,dout,batch", [(96, 200, 40), (512, 384, 300), (1024, 256, 130), (9000, 96, 20)])
 def test_batched_secret_secret_linear(gpu, din, dout, batch):
     """Batched secret x secret layer (spdz_bmatrix_mask / spdz_bmatrix_open_combine),
     2 parties: (1) every party's opened [D|E] and, per column j, Z shares equal to the
