@@ -14,4 +14,10 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mac_sigma -s 2 -c 1 -o gpurun_out/prof_sigma python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-chunks 1 > gpurun_out/ncu_sigma.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:OpMask -s 4 -c 1 -o gpurun_out/prof_mask python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-chunks 1 > gpurun_out/ncu_mask.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:k_modgemm_tc -s 1 -c 1 -o gpurun_out/prof_gemm_tc python scripts/gemm_probe.py 8192 1024 > gpurun_out/ncu_gemm.log 2>&1
+
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:k_matrix_combine2 -s 2 -c 1 -o gpurun_out/prof_matrix_combine2 python scripts/linear_probe.py > gpurun_out/ncu_mc2.log 2>&1
+timeout 300 python scripts/streamed_timeline.py 8 > gpurun_out/timeline.log 2>&1
+timeout 300 python scripts/linear_probe.py > gpurun_out/linear_probe.log 2>&1
+for s in "1024 256" "8192 1024"; do timeout 300 python scripts/gemm_probe.py $s --tc-only --diag --prepared; done > gpurun_out/gemm_diag.log 2>&1
+
 ls -la gpurun_out

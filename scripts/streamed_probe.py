@@ -56,3 +56,18 @@ for name, fn in (("H2D", lambda: db.copy_(hb, non_blocking=True)), ("D2H", lambd
     e1.record()
     torch.cuda.synchronize()
     print(f"{name}: {5 * hb.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9:.1f} GB/s", flush=True)
+
+# both directions at once (the streamed e2e overlaps input copies with output copies)
+hb2 = torch.empty(1 << 25, dtype=torch.int32).pin_memory()
+db2 = torch.empty(1 << 25, dtype=torch.int32, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5):
+    with torch.cuda.stream(s1):
+        db.copy_(hb, non_blocking=True)
+    with torch.cuda.stream(s2):
+        hb2.copy_(db2, non_blocking=True)
+torch.cuda.synchronize()
+dt = time.perf_counter() - t0
+print(f"H2D + D2H concurrently: {5 * hb.numel() * 4 / dt / 1e9:.1f} GB/s each way", flush=True)
