@@ -149,6 +149,7 @@ struct spdz_run {
     std::vector<int> alloc_dev;
     std::vector<Fault> faults;
     bool consumed = false;
+    bool masks_used = false;        // input masks consumed by share_inputs (take_masks cursor)
     uint64_t dealer_seed = 1;
     uint32_t* host_out = nullptr;   // pinned (internal) or user-bound output buffer
     uint64_t host_out_len = 0, host_out_cap = 0;
@@ -565,6 +566,7 @@ void deal(spdz_run* r, uint64_t seed) {
         check_dealer_flag(ctx);
     }
     r->consumed = false;
+    r->masks_used = false;
     r->dealer_seed = seed;
 }
 
@@ -631,6 +633,7 @@ void load_store(spdz_run* r, int p, const char* path) {
     up.finish();
     set_alpha(P.ctx, L.alpha_share);
     r->consumed = false;
+    r->masks_used = false;
 }
 
 void alloc_deals(spdz_run* r) {
@@ -1396,7 +1399,15 @@ bool share_fused(spdz_run* r) {
 }
 
 void share_inputs(spdz_run* r) {
-    // preproc.cpp:205-243: party 0 opens x - mask, everyone adds the public difference
+    // preproc.cpp:205-243: party 0 opens x - mask, everyone adds the public difference.
+    // A mask is used once (take_masks, triple_store.cpp:156-161): sharing again with the same
+    // preprocessing would open x' - r for the same r.
+    if (!r->input_mask_off.empty()) {
+        if (r->masks_used)
+            throw Error(SPDZ_ERR_MASK_EXHAUSTED,
+                        "MaskExhausted: the input masks of this preprocessing were already used (deal again)");
+        r->masks_used = true;
+    }
     ++r->seq;
     for (auto& [id, off] : r->input_mask_off) {
         const auto& n = r->node(id);

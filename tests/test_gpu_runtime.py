@@ -118,6 +118,8 @@ def test_triple_reuse_is_rejected_until_redeal(gpu, golden):
     r.online()
     with pytest.raises(errors.TripleExhausted):
         r.online()
+    with pytest.raises(errors.MaskExhausted):  # take_masks: a mask is opened once
+        r.share_inputs()
     r.deal(2)
     r.share_inputs()
     rep = r.online()
