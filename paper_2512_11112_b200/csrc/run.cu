@@ -833,7 +833,7 @@ struct Exec {
     // Beaver multiply (runtime.cpp:204-239): mask -> open [d|e] -> combine, all parties.
     // Both parties of a 2-party run on one stream: both masks, then one fused open+combine
     // (payloads read once, opened values logged once).  (Running it in L2-sized lane blocks so
-    // the payloads are re-read from L2 measured slower: the per-launch overhead dominates.)
+    // the payloads are re-read from L2 measured slower: the per-launch overhead dominated.)
     void beaver_pair(uint32_t id, uint64_t off) {
         const auto& n = r->node(id);
         const uint64_t L = n.lanes;
@@ -847,34 +847,29 @@ struct Exec {
             if (a.lanes != L) bcast_into(p, a, st.xa);
             if (b.lanes != L) bcast_into(p, b, st.xb);
         }
-        const uint64_t blk = L;
         const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
         const uint32_t* alpha_dev[2] = {P0.ctx->d_alpha, P1.ctx->d_alpha};
-        for (uint64_t b0 = 0; b0 < L; b0 += blk) {
-            const uint64_t nb = std::min<uint64_t>(blk, L - b0);
-            for (int p = 0; p < 2; ++p) {
-                auto& P = r->parties[p];
-                auto& st = P.ns[id];
-                const int tk = tbegin(p);
-                lk(launch_mul_mask(S(r, p), st.xa.v + b0, st.xb.v + b0, P.pool[0] + off + b0, P.pool[2] + off + b0,
-                                   st.payload + b0, st.payload + L + b0, nb, SMS(r, p)),
-                   "k_mul_mask");
-                tend(p, tk, SPDZ_KSTAT_MASK, 24 * nb);
-            }
-            const uint32_t* de[4] = {s0.payload + b0, s0.payload + L + b0, s1.payload + b0, s1.payload + L + b0};
-            const uint32_t *t0[6], *t1[6];
-            for (int t = 0; t < 6; ++t) {
-                t0[t] = P0.pool[t] + off + b0;
-                t1[t] = P1.pool[t] + off + b0;
-            }
-            uint32_t* z[4] = {s0.out.v + b0, s0.out.m + b0, s1.out.v + b0, s1.out.m + b0};
-            const int tk = tbegin(0);
-            lk(launch_beaver_combine2(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened + b0, s0.opened + L + b0, nb,
-                                      SMS(r, 0)),
-               "k_combine2");
-            // [d|e] of both parties 16 + two parties' triple planes 48 + two z 16 + one opened log 8
-            tend(0, tk, SPDZ_KSTAT_COMBINE, 88 * nb);
+        for (int p = 0; p < 2; ++p) {
+            auto& P = r->parties[p];
+            auto& st = P.ns[id];
+            const int tk = tbegin(p);
+            lk(launch_mul_mask(S(r, p), st.xa.v, st.xb.v, P.pool[0] + off, P.pool[2] + off, st.payload,
+                               st.payload + L, L, SMS(r, p)),
+               "k_mul_mask");
+            tend(p, tk, SPDZ_KSTAT_MASK, 24 * L);
         }
+        const uint32_t* de[4] = {s0.payload, s0.payload + L, s1.payload, s1.payload + L};
+        const uint32_t *t0[6], *t1[6];
+        for (int t = 0; t < 6; ++t) {
+            t0[t] = P0.pool[t] + off;
+            t1[t] = P1.pool[t] + off;
+        }
+        uint32_t* z[4] = {s0.out.v, s0.out.m, s1.out.v, s1.out.m};
+        const int tk = tbegin(0);
+        lk(launch_beaver_combine2(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, L, SMS(r, 0)),
+           "k_combine2");
+        // [d|e] of both parties 16 + two parties' triple planes 48 + two z 16 + one opened log 8
+        tend(0, tk, SPDZ_KSTAT_COMBINE, 88 * L);
         r->exchanged += 2 * (2 * L * 4);
     }
 
