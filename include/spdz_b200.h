@@ -317,6 +317,8 @@ typedef enum spdz_node_kind {
     SPDZ_NODE_ROOT = 8,    /* runtime.cpp:442-444 */
     SPDZ_NODE_LOAD = 9,    /* runtime.cpp:419-438: operands (base, start const) -> lane slice view */
     SPDZ_NODE_NOP = 10,    /* BlockLabel and other control nodes of a straight-line graph */
+    SPDZ_NODE_CMP_PUBLIC = 11, /* runtime.cpp:411-418: lane 0 of two public operands, const_val = ir::CmpPred
+                                  (Eq, Ne, Slt, Sgt, Sle, Sge; compared as u32 field elements) -> public 0/1 */
 } spdz_node_kind;
 
 typedef struct spdz_node {

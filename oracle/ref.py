@@ -95,6 +95,12 @@ def lib():
                                      C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, U32P, C.c_uint64,
                                      C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
                                      C.POINTER(C.c_uint64)]
+        L.reft_write_circuit_file.argtypes = [C.c_char_p, C.c_char_p]
+        L.reft_write_input_file.argtypes = [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, C.c_char_p]
+        L.reft_load_run_bundle.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64]
+        L.reft_run_bundle.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_char_p, C.c_uint64, C.c_int, U32P,
+                                      C.c_uint64, C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
+                                      C.POINTER(C.c_uint64)]
         L.reft_time_beaver_kernels.argtypes = [C.c_uint64, C.c_int]
         L.reft_time_beaver_kernels.restype = C.c_double
     return _lib
@@ -353,6 +359,38 @@ def run_local(ir_text: str, n_parties: int, inputs: dict, threads: int = 1, slic
     dig = C.c_uint64()
     _check(lib().reft_run_local(ir_text.encode(), n_parties, threads, slice_, dealer_seed, io_timeout_ms, k, cn, cv,
                                 cl, out, cap, C.byref(n), rep, C.byref(dig)))
+    report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
+                  matrix_triples=int(rep[4]), digest=dig.value)
+    return out[: n.value].copy(), report
+
+
+def write_circuit_file(ir_text: str, path):
+    """`llspdz compile`: the reference front end's MPCG file (circuit_io.cpp:188-194)."""
+    _check(lib().reft_write_circuit_file(ir_text.encode(), str(path).encode()))
+
+
+def write_input_file(inputs: dict, path):
+    """`llspdz pack-inputs`: an MPCI input file (preproc.cpp:15-43)."""
+    k, cn, cv, cl, keep = _inputs(inputs)
+    _check(lib().reft_write_input_file(k, cn, cv, cl, str(path).encode()))
+
+
+def load_run_bundle(circuit_path, triples_path, inputs_path, slice_: int = 262140):
+    """preproc::load_run_bundle (preproc.cpp:165-202); raises RefError on a failed cross-check."""
+    _check(lib().reft_load_run_bundle(str(circuit_path).encode(), str(triples_path).encode(),
+                                      str(inputs_path).encode(), slice_))
+
+
+def run_bundle(circuit_path, n_parties: int, triples_dir, inputs_path, slice_: int = 262140, threads: int = 1,
+               cap: int = 1 << 24):
+    """Every party's `llspdz run` (tools/main.cpp:111-130) over the simulated transport."""
+    out = np.empty(cap, np.uint32)
+    n = C.c_uint64()
+    rep = np.zeros(8, np.float64)
+    dig = C.c_uint64()
+    _check(lib().reft_run_bundle(str(circuit_path).encode(), n_parties, str(triples_dir).encode(),
+                                 str(inputs_path).encode(), slice_, threads, out, cap, C.byref(n), rep,
+                                 C.byref(dig)))
     report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
                   matrix_triples=int(rep[4]), digest=dig.value)
     return out[: n.value].copy(), report

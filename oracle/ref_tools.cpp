@@ -18,6 +18,7 @@
 
 #include "mpc/backend.hpp"
 #include "mpc/circuit.hpp"
+#include "mpc/circuit_io.hpp"
 #include "mpc/hash.hpp"
 #include "mpc/ir.hpp"
 #include "mpc/linear.hpp"
@@ -449,6 +450,67 @@ int reft_write_dealer_stores(const char* ir_text, int n_parties, uint64_t slice,
         spdz::Dealer dealer(n_parties, dealer_seed);
         spdz::write_dealer_stores(dealer, demand.scalars, demand.matrix_shapes, demand.input_masks, out_dir,
                                   loop_iters);
+    });
+}
+
+// ---- the CLI's artifacts (tools/main.cpp compile / pack-inputs / run) ----
+// circuit_io.cpp:188-194 — `llspdz compile`: IR text -> MPCG circuit file.
+int reft_write_circuit_file(const char* ir_text, const char* path) {
+    return guard([&] { circuit::write_circuit_file(compile_text(ir_text), path); });
+}
+
+// preproc.cpp:15-43 — `llspdz pack-inputs`: parameters -> MPCI input file.
+int reft_write_input_file(int n_inputs, const char* const* names, const uint32_t* const* vals, const uint64_t* lens,
+                          const char* path) {
+    return guard([&] { preproc::write_input_file(make_inputs(n_inputs, names, vals, lens), path); });
+}
+
+// preproc.cpp:165-202 load_run_bundle: the artifact cross-checks (error parity).
+int reft_load_run_bundle(const char* circuit_path, const char* triples_path, const char* inputs_path,
+                         uint64_t slice) {
+    return guard([&] { (void)preproc::load_run_bundle(circuit_path, triples_path, inputs_path, slice); });
+}
+
+// tools/main.cpp:111-130 run_one_party for every party at once: party i loads
+// <triples_dir>/triples_<i>.bin through load_run_bundle and runs PartyRuntime
+// over the simulated transport (runtime.cpp:586-613 with stores from files).
+int reft_run_bundle(const char* circuit_path, int n_parties, const char* triples_dir, const char* inputs_path,
+                    uint64_t slice, int threads, uint32_t* out, uint64_t cap, uint64_t* out_len, double* report,
+                    uint64_t* digest) {
+    return guard([&] {
+        runtime::RunOptions opts;
+        opts.threads = threads;
+        opts.slice = slice;
+        std::vector<preproc::RunBundle> bundles;
+        for (int i = 0; i < n_parties; ++i)
+            bundles.push_back(preproc::load_run_bundle(circuit_path,
+                                                       std::string(triples_dir) + "/triples_" + std::to_string(i) + ".bin",
+                                                       inputs_path, slice));
+        auto sessions = net::make_sim_sessions(n_parties);
+        std::vector<runtime::RunReport> reps(n_parties);
+        std::vector<std::exception_ptr> errors(n_parties);
+        std::vector<std::thread> th;
+        for (int i = 0; i < n_parties; ++i)
+            th.emplace_back([&, i] {
+                try {
+                    runtime::PartyRuntime rt(bundles[i].graph, bundles[i].store, sessions[i], opts);
+                    reps[i] = rt.run(bundles[i].inputs);
+                } catch (...) {
+                    errors[i] = std::current_exception();
+                }
+            });
+        for (auto& t : th) t.join();
+        for (auto& e : errors)
+            if (e) std::rethrow_exception(e);
+        auto& r0 = reps.at(0);
+        *out_len = r0.outputs.size();
+        std::memcpy(out, r0.outputs.data(), std::min<uint64_t>(cap, r0.outputs.size()) * 4);
+        report[0] = r0.setup_ms;
+        report[1] = r0.online_ms;
+        report[2] = double(r0.bytes_sent);
+        report[3] = double(r0.scalar_triples_consumed);
+        report[4] = double(r0.matrix_triples_consumed);
+        *digest = r0.output_digest;
     });
 }
 

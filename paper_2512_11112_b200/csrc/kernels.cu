@@ -974,7 +974,20 @@ __global__ void __launch_bounds__(kThreads) k_pub_binop(int op, const uint32_t* 
     const uint32_t a0 = a_b ? a[0] : 0u, b0 = b_b ? b[0] : 0u;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t x = a_b ? a0 : a[i], y = b_b ? b0 : b[i];
-        out[i] = op == 0 ? fp_add(x, y) : (op == 1 ? fp_sub(x, y) : fp_mul(x, y));
+        uint32_t z;
+        switch (op) {
+            case 0: z = fp_add(x, y); break;
+            case 1: z = fp_sub(x, y); break;
+            case 2: z = fp_mul(x, y); break;
+            // 3 + ir::CmpPred: cmp_eval (runtime.cpp:49-58) on the u32 representatives
+            case 3: z = x == y; break;
+            case 4: z = x != y; break;
+            case 5: z = x < y; break;
+            case 6: z = x > y; break;
+            case 7: z = x <= y; break;
+            default: z = x >= y; break;
+        }
+        out[i] = z;
     }
 }
 

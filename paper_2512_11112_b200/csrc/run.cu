@@ -368,6 +368,13 @@ void plan_buffers(spdz_run* r) {
                 case SPDZ_NODE_CONST:
                     pub_out(1);
                     break;
+                case SPDZ_NODE_CMP_PUBLIC:  // runtime.cpp:119-125 read_public: completed public scalars only
+                    for (int k = 0; k < 2; ++k)
+                        need(n.n_operands == 2 && opnd(k).is_public && opnd(k).lanes >= 1, SPDZ_ERR_INVALID_ARGUMENT,
+                             "runtime: node " + std::to_string(n.operands[k]) + " is not a completed public scalar");
+                    need(n.const_val <= 5, SPDZ_ERR_INVALID_ARGUMENT, "runtime: bad comparison predicate");
+                    pub_out(1);
+                    break;
                 case SPDZ_NODE_NOP:
                     break;
                 case SPDZ_NODE_LOAD: {  // runtime.cpp:419-438 (zero-copy slice)
@@ -1236,6 +1243,16 @@ struct Exec {
                         if (!r->parties[p].local) continue;
                         dev(r, p);
                         reduce_add(p, id);
+                    }
+                    break;
+                case SPDZ_NODE_CMP_PUBLIC:
+                    for (int p = 0; p < r->n; ++p) {
+                        if (!r->parties[p].local) continue;
+                        dev(r, p);
+                        auto& P = r->parties[p];
+                        lk(launch_pub_binop(S(r, p), 3 + (int)n.const_val, P.ns[n.operands[0]].out.pub, true,
+                                            P.ns[n.operands[1]].out.pub, true, P.ns[id].out.pub, 1, P.ctx->sms),
+                           "cmp public");
                     }
                     break;
                 case SPDZ_NODE_REDUCE_MUL:

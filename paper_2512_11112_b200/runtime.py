@@ -20,10 +20,10 @@ import numpy as np
 from . import _lib
 from ._lib import check, lib
 
-INPUT, CONST, ADD, SUB, MUL, REDUCE_ADD, REDUCE_MUL, LINEAR, ROOT, LOAD, NOP = range(11)
+INPUT, CONST, ADD, SUB, MUL, REDUCE_ADD, REDUCE_MUL, LINEAR, ROOT, LOAD, NOP, CMP_PUBLIC = range(12)
 KIND_NAMES = {"Input": INPUT, "Const": CONST, "Adder": ADD, "AddBatch": ADD, "Subtract": SUB, "SubBatch": SUB,
               "Multiplier": MUL, "MultBatch": MUL, "ReduceAdd": REDUCE_ADD, "ReduceMul": REDUCE_MUL,
-              "LinearLayer": LINEAR, "Root": ROOT, "Load": LOAD, "BlockLabel": NOP}
+              "LinearLayer": LINEAR, "Root": ROOT, "Load": LOAD, "BlockLabel": NOP, "CmpPublic": CMP_PUBLIC}
 
 
 @dataclass
@@ -43,6 +43,7 @@ class Graph:
     nodes: list = field(default_factory=list)
     root: int = -1
     inputs: dict = field(default_factory=dict)  # name -> node id (g.inputs order)
+    const_inputs: dict = field(default_factory=dict)  # name -> values of vector constants bound as public inputs
 
     def add(self, spec: NodeSpec) -> int:
         self.nodes.append(spec)
@@ -252,7 +253,7 @@ class LocalRun:
         check(lib().spdz_run_load_store(self.h, int(party), str(path).encode()))
 
     def bind_inputs(self, inputs: dict):
-        for name, vals in inputs.items():
+        for name, vals in (self.graph.const_inputs | inputs).items():
             v = np.ascontiguousarray(vals, dtype=np.uint32)
             check(lib().spdz_run_bind_input(self.h, self.graph.inputs[name], v.ctypes.data, v.size))
 

@@ -1,0 +1,101 @@
+"""Generates tests/golden/bundles/<case>/ — the three artifacts every party of a
+reference deployment is handed (tools/main.cpp:111-130, ``llspdz run``), all
+written by the UNMODIFIED reference (oracle/_ref):
+
+* circuit.mpcg   — ``llspdz compile`` of the IR (circuit_io.cpp:188-194); the IR is
+                   a fixture of the reference's own test suite (proj/tests/fixtures)
+                   or an oracle/workloads.py circuit,
+* inputs.mpci    — ``llspdz pack-inputs`` (preproc.cpp:15-43),
+* triples_<i>.bin — the dealer tool's MPCT stores (triple_store.cpp:288-303),
+* expected.json  — party 0's outputs, digest and triple counts from every party's
+                   ``run_one_party`` over the simulated transport (reft_run_bundle).
+
+    python tests/golden/make_bundles.py
+
+Run here (the reference exists only in this container); the files are committed
+and travel to the GPU box, where tests run them through artifacts.run_files.
+"""
+from __future__ import annotations
+
+import json
+import shutil
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from oracle import ref, workloads  # noqa: E402
+
+OUT = Path(__file__).resolve().parent / "bundles"
+FIXTURES = Path("/root/reference/proj/tests/fixtures")
+
+# a vector constant (a Const node with one value per lane) next to a public pointer input
+VECTOR_CONST_IR = workloads._HDR + """define i32 @main(ptr %x, ptr %y) {
+entry:
+""" + workloads._ann("x", True) + workloads._ann("y", False) + """  %a = load <16 x i32>, ptr %x
+  %b = load <16 x i32>, ptr %y
+  %s = add <16 x i32> %a, <i32 1, i32 2, i32 4294967295, i32 7, i32 0, i32 9, i32 4294967290, i32 3, i32 11, i32 5, i32 6, i32 8, i32 13, i32 4294967291, i32 17, i32 19>
+  %p = mul <16 x i32> %s, %b
+  %q = mul <16 x i32> %p, %a
+  %r = call i32 @llvm.vector.reduce.add.v16i32(<16 x i32> %q)
+  ret i32 %r
+}
+
+declare i32 @llvm.vector.reduce.add.v16i32(<16 x i32>)
+""" + workloads._DECL
+
+
+def rnd(n, seed):
+    return ref.rand_field_vec(n, seed)
+
+
+# name -> (ir, parties, slice, dealer seed, inputs)
+def cases():
+    fx = lambda f: (FIXTURES / f).read_text()
+    return {
+        "straight_line": (fx("straight_line.ll"), 2, 262140, 3, {"x": rnd(3, 1), "k": rnd(1, 2)}),
+        "vector_add_n3": (fx("vector_add.ll"), 3, 262140, 4, {"x": rnd(8, 3), "y": rnd(8, 4)}),
+        "linear_64x32": (fx("linear_64x32.ll"), 2, 256, 5, {"x": rnd(64, 5), "W": rnd(2048, 6), "b": rnd(32, 7)}),
+        "reduce_mul": (fx("reduce_mul.ll"), 2, 262140, 6, {"x": rnd(7, 8)}),
+        "select_shl_bits": (fx("select_shl_bits.ll"), 2, 262140, 7,
+                            {"x": rnd(1, 9), "k": np.array([5], np.uint32), "m": np.array([7], np.uint32)}),
+        "select_shl_bits_f": (fx("select_shl_bits.ll"), 2, 262140, 8,
+                              {"x": rnd(1, 10), "k": np.array([2], np.uint32), "m": np.array([9], np.uint32)}),
+        "vector_const": (VECTOR_CONST_IR, 2, 262140, 9, {"x": rnd(16, 11), "y": rnd(16, 12)}),
+        "mixed_1024_n3": (workloads.chain_ir("mixed", 1024), 3, 262140, 10, {"x": rnd(1024, 13), "y": rnd(1024, 14)}),
+        "linear_pub_w": (workloads.linear_ir(48, 40, w_private=False), 2, 262140, 11,
+                         {"x": rnd(48, 15), "W": rnd(48 * 40, 16), "b": rnd(40, 17)}),
+    }
+
+
+# circuits with control flow (Phi/Branch/loops): circuit files only (the executor rejects them)
+CONTROL_FLOW = ("diamond", "loop_sum", "nested_loop", "secret_branch")
+
+
+def main():
+    if OUT.exists():
+        shutil.rmtree(OUT)
+    (OUT / "control_flow").mkdir(parents=True)
+    for f in CONTROL_FLOW:
+        ref.write_circuit_file((FIXTURES / f"{f}.ll").read_text(), OUT / "control_flow" / f"{f}.mpcg")
+    for name, (ir, n, slice_, seed, inputs) in cases().items():
+        d = OUT / name
+        d.mkdir(parents=True)
+        ref.write_circuit_file(ir, d / "circuit.mpcg")
+        ref.write_input_file(inputs, d / "inputs.mpci")
+        ref.write_dealer_stores(ir, n, str(d), slice_=slice_, seed=seed, loop_iters=1)
+        out, rep = ref.run_bundle(d / "circuit.mpcg", n, d, d / "inputs.mpci", slice_)
+        clear = ref.interpret(ir, inputs)
+        assert np.array_equal(out, clear), name  # the online phase opens the cleartext result
+        meta = {"parties": n, "slice": slice_, "dealer_seed": seed, "outputs": out.tolist(),
+                "digest": rep["digest"], "scalar_triples": rep["scalar_triples"],
+                "matrix_triples": rep["matrix_triples"]}
+        (d / "expected.json").write_text(json.dumps(meta, indent=1))
+        print(name, n, "parties,", len(out), "outputs,", rep["scalar_triples"], "triples,",
+              sum(p.stat().st_size for p in d.iterdir()), "bytes")
+
+
+if __name__ == "__main__":
+    main()

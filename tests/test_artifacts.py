@@ -1,0 +1,222 @@
+"""The reference CLI's artifacts (tests/golden/bundles, written by the unmodified
+reference): MPCG circuit files, MPCI input files, MPCT stores.
+
+Host (no GPU):
+* every circuit parses and re-serialises to the identical bytes
+  (circuit_io.cpp:74-185); input files likewise (preproc.cpp:15-82);
+* the lowered graph's triple layout == the reference's (preproc.cpp:124-163);
+* load_run_bundle's cross-checks fail with the reference's exception kind and
+  message (ShapeMismatch, InsufficientTriples, VersionMismatch, CorruptPayload),
+  compared against the reference's own load_run_bundle where oracle/_ref exists;
+* control-flow circuits are refused (UnsupportedCircuit).
+
+GPU (-m gpu): run_files on every bundle == the reference's outputs, digest and
+triple consumption (party 0 of every party's ``llspdz run``).
+"""
+import json
+import shutil
+import struct
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_2512_11112_b200 import artifacts as A
+from paper_2512_11112_b200 import errors
+from paper_2512_11112_b200 import runtime as rt
+
+BUNDLES = Path(__file__).resolve().parent / "golden" / "bundles"
+CASES = sorted(p.name for p in BUNDLES.iterdir() if p.is_dir() and p.name != "control_flow")
+CF = sorted((BUNDLES / "control_flow").glob("*.mpcg"))
+HAS_REF = ref.available()
+
+
+def files(case):
+    d = BUNDLES / case
+    exp = json.loads((d / "expected.json").read_text())
+    stores = [d / f"triples_{i}.bin" for i in range(exp["parties"])]
+    return d / "circuit.mpcg", stores, d / "inputs.mpci", exp
+
+
+def test_cases_present():
+    assert {"straight_line", "vector_add_n3", "linear_64x32", "reduce_mul", "select_shl_bits", "vector_const",
+            "mixed_1024_n3"} <= set(CASES)
+    assert len(CF) >= 3
+
+
+@pytest.mark.parametrize("path", [BUNDLES / c / "circuit.mpcg" for c in CASES] + CF, ids=lambda p: p.parent.name +
+                         "/" + p.name)
+def test_circuit_roundtrip(path):
+    data = path.read_bytes()
+    cf = A.parse_circuit(data)
+    assert A.serialize_circuit(cf) == data
+    assert cf.nodes[cf.root].kind == "Root"
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_input_file_roundtrip(case, tmp_path):
+    _, _, inp, _ = files(case)
+    vals = A.read_input_file(inp)
+    A.write_input_file(vals, tmp_path / "x.mpci")
+    assert (tmp_path / "x.mpci").read_bytes() == inp.read_bytes()
+    sidecar = json.loads((tmp_path / "x.mpci.json").read_text())
+    assert [p["name"] for p in sidecar["params"]] == sorted(vals)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_bundle_checks_pass_and_layout(case):
+    circ, stores, inp, exp = files(case)
+    b = A.load_run_bundle(circ, stores, inp, exp["slice"])
+    assert b.demand["scalars"] == exp["scalar_triples"]
+    assert b.demand["matrices"] == exp["matrix_triples"]
+    for i, st in enumerate(b.stores):
+        assert st["party"] == i and st["n_parties"] == exp["parties"]
+    if HAS_REF:
+        for s in stores:
+            ref.load_run_bundle(circ, s, inp, exp["slice"])
+
+
+def test_vector_constant_becomes_public_values():
+    circ, stores, inp, _ = files("vector_const")
+    cf = A.read_circuit_file(circ)
+    g = cf.to_graph(A.read_input_file(inp))
+    (name, vals), = g.const_inputs.items()
+    node = g.nodes[g.inputs[name]]
+    assert node.kind == rt.INPUT and not node.is_private and node.lanes == 16
+    src = [n for n in cf.nodes if n.kind == "Const" and len(n.cvals) == 16][0]
+    assert vals.tolist() == [c % A.P for c in src.cvals]
+
+
+def test_cmp_public_lowered():
+    circ, _, inp, _ = files("select_shl_bits")
+    g = A.read_circuit_file(circ).to_graph(A.read_input_file(inp))
+    cmps = [n for n in g.nodes if n.kind == rt.CMP_PUBLIC]
+    assert len(cmps) == 2 and {n.const_val for n in cmps} <= set(range(6))
+
+
+@pytest.mark.parametrize("path", CF, ids=lambda p: p.stem)
+def test_control_flow_refused(path):
+    with pytest.raises(A.UnsupportedCircuit, match="UnsupportedCircuit: control flow"):
+        A.read_circuit_file(path).to_graph()
+
+
+# ---- error behaviour (preproc.cpp:165-202, circuit_io.cpp:117-185) ----
+def _ref_error(circ, store, inp, slice_):
+    if not HAS_REF:
+        return None
+    with pytest.raises(ref.RefError) as e:
+        ref.load_run_bundle(circ, store, inp, slice_)
+    return str(e.value).split("] ", 1)[1]
+
+
+def _expect(exc, circ, stores, inp, slice_, prefix):
+    with pytest.raises(exc) as e:
+        A.load_run_bundle(circ, stores, inp, slice_)
+    msg = str(e.value)
+    assert msg.startswith(prefix), msg
+    want = _ref_error(circ, stores[0], inp, slice_)
+    if want is not None:
+        assert msg == want
+
+
+def test_missing_parameter(tmp_path):
+    circ, stores, inp, exp = files("vector_add_n3")
+    vals = A.read_input_file(inp)
+    del vals["y"]
+    A.write_input_file(vals, tmp_path / "i.mpci")
+    _expect(A.ShapeMismatch, circ, stores, tmp_path / "i.mpci", exp["slice"],
+            "ShapeMismatch: input file lacks parameter 'y'")
+
+
+def test_wrong_parameter_size(tmp_path):
+    circ, stores, inp, exp = files("vector_add_n3")
+    vals = A.read_input_file(inp)
+    vals["x"] = vals["x"][:5]
+    A.write_input_file(vals, tmp_path / "i.mpci")
+    _expect(A.ShapeMismatch, circ, stores, tmp_path / "i.mpci", exp["slice"],
+            "ShapeMismatch: parameter 'x' has 5 elements, circuit expects 8")
+
+
+def test_insufficient_scalar_triples():
+    circ, _, inp, exp = files("vector_const")  # 16 triples needed
+    _, small, _, _ = files("straight_line")  # stores with 2
+    _expect(errors.InsufficientTriples, circ, small, inp, exp["slice"],
+            "InsufficientTriples: need 16 scalar triples, store has 2 (deficit 14)")
+
+
+def test_insufficient_matrix_triples():
+    circ, _, inp, exp = files("linear_64x32")
+    _, other, _, _ = files("straight_line")
+    _expect(errors.InsufficientTriples, circ, other, inp, exp["slice"], "InsufficientTriples: need 8 matrix")
+
+
+def test_insufficient_masks():
+    circ, _, inp, exp = files("linear_pub_w")  # no triples, 88 input masks (x and b private)
+    _, small, _, _ = files("straight_line")  # 3 masks
+    _expect(errors.InsufficientTriples, circ, small, inp, exp["slice"],
+            "InsufficientTriples: need 88 input masks, store has 3")
+
+
+@pytest.mark.parametrize("mutate,prefix", [
+    (lambda b: b"MPCX" + b[4:], "VersionMismatch: bad magic, not a circuit file"),
+    (lambda b: b[:4] + struct.pack("<I", 2) + b[8:], "VersionMismatch: circuit format version 2"),
+    (lambda b: b[:8] + struct.pack("<Q", 2**31 - 1) + b[16:], "VersionMismatch: circuit built for a different prime"),
+    (lambda b: b[:-3], "CorruptPayload: truncated circuit file"),
+    (lambda b: b + b"\0", "CorruptPayload: trailing bytes"),
+    (lambda b: b[:2], "CorruptPayload: truncated circuit file"),
+])
+def test_corrupt_circuit(tmp_path, mutate, prefix):
+    circ, stores, inp, exp = files("straight_line")
+    bad = tmp_path / "c.mpcg"
+    bad.write_bytes(mutate(circ.read_bytes()))
+    _expect(A.CircuitFormatError, bad, stores, inp, exp["slice"], prefix)
+
+
+@pytest.mark.parametrize("mutate,prefix", [
+    (lambda b: b"MPCJ" + b[4:], "VersionMismatch: not an input file"),
+    (lambda b: b[:4] + struct.pack("<I", 3) + b[8:], "VersionMismatch: input file version 3"),
+    (lambda b: b[:-1], "CorruptPayload: truncated input file"),
+])
+def test_corrupt_input_file(tmp_path, mutate, prefix):
+    circ, stores, inp, exp = files("straight_line")
+    bad = tmp_path / "i.mpci"
+    bad.write_bytes(mutate(inp.read_bytes()))
+    _expect(A.CircuitFormatError, circ, stores, bad, exp["slice"], prefix)
+
+
+def test_store_party_order(tmp_path):
+    circ, stores, inp, exp = files("straight_line")
+    b = A.load_run_bundle(circ, list(reversed(stores)), inp, exp["slice"])
+    with pytest.raises(errors.InvalidArgument, match="triple store belongs to party 1"):
+        A.run_bundle(b)
+
+
+# ---- GPU: the online phase from the reference's files ----
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_run_files_matches_reference(gpu, case):
+    circ, stores, inp, exp = files(case)
+    rep = A.run_files(circ, stores, inp, exp["slice"])
+    assert rep.outputs.tolist() == exp["outputs"]
+    assert rep.output_digest == exp["digest"]
+    assert rep.scalar_triples_consumed == exp["scalar_triples"]
+    assert rep.matrix_triples_consumed == exp["matrix_triples"]
+
+
+@pytest.mark.gpu
+def test_run_files_tampered_store_fails_mac(gpu, tmp_path):
+    """A flipped bit in party 1's c.m plane (a MAC share of c) must fail the MAC check."""
+    circ, stores, inp, exp = files("mixed_1024_n3")
+    info = rt.store_info(stores[1])
+    n = info["scalar_triples"]
+    data = bytearray(stores[1].read_bytes())
+    off = 4 + 4 + 8 + 4 + 4 + 4 + 8 + 8 + 4 * n * 5 + 4 * 17  # c.m plane, lane 17
+    data[off] ^= 1
+    d = tmp_path / "b"
+    d.mkdir()
+    shutil.copy(stores[0], d / "triples_0.bin")
+    (d / "triples_1.bin").write_bytes(bytes(data))
+    shutil.copy(stores[2], d / "triples_2.bin")
+    with pytest.raises(errors.MacCheckFailed):
+        A.run_files(circ, [d / f"triples_{i}.bin" for i in range(3)], inp, exp["slice"])
