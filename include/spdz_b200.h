@@ -319,7 +319,15 @@ typedef enum spdz_node_kind {
     SPDZ_NODE_NOP = 10,    /* BlockLabel and other control nodes of a straight-line graph */
     SPDZ_NODE_CMP_PUBLIC = 11, /* runtime.cpp:411-418: lane 0 of two public operands, const_val = ir::CmpPred
                                   (Eq, Ne, Slt, Sgt, Sle, Sge; compared as u32 field elements) -> public 0/1 */
+    /* Control flow (scheduler.cpp): a graph holding a PHI or BRANCH runs block by block
+     * from spdz_run_options_t.entry_label, every block a LABEL whose `next` chain lists
+     * its nodes in order.  In graphs without them LABEL is a NOP. */
+    SPDZ_NODE_PHI = 12,    /* operands[i] taken when the block is entered from phi_labels[i] */
+    SPDZ_NODE_BRANCH = 13, /* n_succ 1: jump to succ[0]; 2: operands[0] (public) != 0 ? succ[0] : succ[1] */
+    SPDZ_NODE_LABEL = 14,  /* BlockLabel: heads its block's `next` chain */
 } spdz_node_kind;
+
+#define SPDZ_NO_NODE 0xFFFFFFFFu
 
 typedef struct spdz_node {
     int32_t kind;
@@ -329,6 +337,13 @@ typedef struct spdz_node {
     uint32_t operands[3]; /* node ids (ids are the index in the node array) */
     uint32_t din, dout;   /* LINEAR only */
     uint32_t const_val;   /* CONST only (scalar broadcast) */
+    /* control flow (ignored by straight-line graphs) */
+    uint32_t next;        /* next node of the enclosing block (circuit::Node::next), SPDZ_NO_NODE ends it */
+    uint32_t loop_depth;  /* loops containing the node's block: triples provisioned loop_iters^depth times
+                             (preproc.cpp:124-163) */
+    uint32_t n_succ;      /* BRANCH */
+    uint32_t succ[2];
+    uint32_t phi_labels[3]; /* PHI: predecessor block of each operand */
 } spdz_node_t;
 
 typedef struct spdz_run_options {
@@ -355,6 +370,10 @@ typedef struct spdz_run_options {
      * NVLink P2P loads) and ordered by stream memory operations.  Requires
      * external_mac_verify = 1. */
     int32_t single_party;
+    /* Control-flow graphs: the entry block's LABEL and the loop provisioning factor
+     * (RunOptions / the store's loop_iters; 0 = 64, run_local's hint, runtime.cpp:597). */
+    uint32_t entry_label;
+    uint64_t loop_iters;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
@@ -388,8 +407,8 @@ typedef struct spdz_run spdz_run;
  * (preproc.cpp:124-163 compute_triple_layout): per region 5 words
  * {kind 0 scalar / 1 matrix, node, base, stride, max_execs}, scalar regions first,
  * nodes ascending; *n_regions receives the count (out may be NULL to query). */
-int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t* out, uint64_t cap,
-                       uint64_t* n_regions);
+int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t loop_iters,
+                       uint64_t* out, uint64_t cap, uint64_t* n_regions);
 int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, int n_parties,
                     const spdz_run_options_t* opts, spdz_run** out);
 int spdz_run_destroy(spdz_run* run);

@@ -56,14 +56,16 @@ class MacSegment(C.Structure):  # spdz_mac_segment_t
 class Node(C.Structure):  # spdz_node_t
     _fields_ = [("kind", C.c_int32), ("is_private", C.c_int32), ("lanes", C.c_uint32), ("n_operands", C.c_uint32),
                 ("operands", C.c_uint32 * 3), ("din", C.c_uint32), ("dout", C.c_uint32),
-                ("const_val", C.c_uint32)]
+                ("const_val", C.c_uint32), ("next", C.c_uint32), ("loop_depth", C.c_uint32), ("n_succ", C.c_uint32),
+                ("succ", C.c_uint32 * 2), ("phi_labels", C.c_uint32 * 3)]
 
 
 class RunOptions(C.Structure):  # spdz_run_options_t
     _fields_ = [("slice", C.c_uint64), ("dealer_seed", C.c_uint64), ("fixed_coin", C.c_int32), ("coin", C.c_uint64),
                 ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32),
                 ("stream_per_party", C.c_int32), ("shard_offset", C.c_uint64), ("shard_total", C.c_uint64),
-                ("external_mac_verify", C.c_int32), ("single_party", C.c_int32)]
+                ("external_mac_verify", C.c_int32), ("single_party", C.c_int32), ("entry_label", C.c_uint32),
+                ("loop_iters", C.c_uint64)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t
@@ -148,7 +150,7 @@ _SIGS = {
                                   C.POINTER(vp)]),
     "spdz_run_destroy": (C.c_int, [vp]),
     "spdz_run_deal": (C.c_int, [vp, C.c_uint64]),
-    "spdz_triple_layout": (C.c_int, [C.POINTER(Node), C.c_uint32, C.c_uint64, u64p, C.c_uint64, u64p]),
+    "spdz_triple_layout": (C.c_int, [C.POINTER(Node), C.c_uint32, C.c_uint64, C.c_uint64, u64p, C.c_uint64, u64p]),
     "spdz_run_load_store": (C.c_int, [vp, C.c_int, C.c_char_p]),
     "spdz_store_inspect": (C.c_int, [C.c_char_p, C.POINTER(StoreInfo)]),
     "spdz_run_bind_input": (C.c_int, [vp, C.c_uint32, vp, C.c_uint64]),

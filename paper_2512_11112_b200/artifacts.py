@@ -10,8 +10,8 @@ every party's online phase through ``LocalRun`` with its preprocessing
 streamed from the MPCT files (``spdz_run_load_store``).
 
 Parsing is host work on a few KB of metadata; nothing here computes on the
-shares.  The executor runs straight-line circuits: a circuit with
-control flow (Phi/Branch, loops) raises ``UnsupportedCircuit``.
+shares.  Circuits with control flow (Phi/Branch, loops) run block by block
+(``run_cfg`` in csrc/run.cu, the sequential reading of scheduler.cpp).
 """
 from __future__ import annotations
 
@@ -24,11 +24,10 @@ from pathlib import Path
 import numpy as np
 
 from .errors import InsufficientTriples, InvalidArgument, StoreFormatError
-from .runtime import (ADD, CMP_PUBLIC, CONST, INPUT, LINEAR, LOAD, MUL, NOP, REDUCE_ADD, REDUCE_MUL, ROOT, SUB,
-                      Graph, LocalRun, NodeSpec, RunReport, store_info, triple_layout)
+from .runtime import (ADD, BRANCH, CMP_PUBLIC, CONST, INPUT, LABEL, LINEAR, LOAD, MUL, NO_NODE, PHI, REDUCE_ADD,
+                      REDUCE_MUL, ROOT, SUB, Graph, LocalRun, NodeSpec, RunReport, store_info, triple_layout)
 
 P = 4294967291
-NO_NODE = 0xFFFFFFFF  # circuit::kNoNode
 
 # circuit.hpp:18-25, in enum order (the u8 written by serialize_circuit)
 REF_KINDS = ("Input", "Const", "Adder", "Multiplier", "Subtract", "AddBatch", "MultBatch", "SubBatch", "ReduceAdd",
@@ -38,7 +37,8 @@ CMP_PREDS = ("Eq", "Ne", "Slt", "Sgt", "Sle", "Sge")  # ir.hpp:53
 
 _TO_NODE = {"Input": INPUT, "Const": CONST, "Adder": ADD, "AddBatch": ADD, "Subtract": SUB, "SubBatch": SUB,
             "Multiplier": MUL, "MultBatch": MUL, "ReduceAdd": REDUCE_ADD, "ReduceMul": REDUCE_MUL, "Load": LOAD,
-            "LinearLayer": LINEAR, "BlockLabel": NOP, "Root": ROOT, "CmpPublic": CMP_PUBLIC}
+            "LinearLayer": LINEAR, "BlockLabel": LABEL, "Root": ROOT, "CmpPublic": CMP_PUBLIC, "Phi": PHI,
+            "Branch": BRANCH}
 
 
 class CircuitFormatError(StoreFormatError):
@@ -50,7 +50,8 @@ class ShapeMismatch(InvalidArgument):
 
 
 class UnsupportedCircuit(InvalidArgument):
-    """The circuit needs a part of the reference runtime this executor does not have (control flow)."""
+    """The circuit needs something this executor does not run (provisional Raw* nodes, a
+    triple-consuming reduce_mul or linear layer inside a loop, phis of more than 3 edges)."""
 
 
 # ---------------------------------------------------------------- MPCG circuit files
@@ -105,17 +106,26 @@ class CircuitFile:
         from the bound values (runtime.cpp:508-525).  Multi-value constants become
         public inputs bound from ``Graph.const_inputs`` (runtime.cpp:527-532)."""
         bad = sorted({n.kind for n in self.nodes if n.kind not in _TO_NODE})
-        if bad or self.loops:
-            what = ", ".join(bad) if bad else f"{len(self.loops)} loop(s)"
-            raise UnsupportedCircuit(f"UnsupportedCircuit: control flow ({what}); this executor runs "
-                                     "straight-line circuits")
+        if bad:
+            raise UnsupportedCircuit(f"UnsupportedCircuit: node kinds {', '.join(bad)}")
         by_node = {d.node: d for d in self.inputs}
+        depth = {}  # block -> loops containing it (circuit::loops_containing_block)
+        for members, _ in self.loops.values():
+            for b in members:
+                depth[b] = depth.get(b, 0) + 1
         g = Graph()
+        g.entry_label = self.entry_label
         for n in self.nodes:
-            if any(o >= n.id for o in n.operands):
-                raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} reads a later node")
             kind = _TO_NODE[n.kind]
-            spec = NodeSpec(kind, n.lanes, tuple(n.operands), n.is_private, din=n.din, dout=n.dout)
+            if kind != PHI and any(o >= n.id for o in n.operands):
+                raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} reads a later node")
+            if len(n.operands) > 3 or len(n.successors) > 2:
+                raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} has {len(n.operands)} operands")
+            loop_depth = depth.get(n.block, 0) if n.block != NO_NODE else 0
+            if loop_depth and kind in (LINEAR, REDUCE_MUL) and self.nodes[n.operands[0]].is_private:
+                raise UnsupportedCircuit(f"UnsupportedCircuit: {n.kind} {n.id} inside a loop")
+            spec = NodeSpec(kind, n.lanes, tuple(n.operands), n.is_private, din=n.din, dout=n.dout, next=n.next,
+                            loop_depth=loop_depth, succ=tuple(n.successors), phi_labels=tuple(n.phi_labels))
             if kind == INPUT:
                 d = by_node.get(n.id)
                 if d is None:
@@ -365,7 +375,7 @@ def load_run_bundle(circuit_path, triples_paths, inputs_path, slice_: int = 2621
             raise ShapeMismatch(f"ShapeMismatch: parameter '{d.name}' has {inputs[d.name].size} elements, "
                                 f"circuit expects {d.count}")
     g = cf.to_graph(inputs)
-    lay = triple_layout(g, slice_)
+    lay = triple_layout(g, slice_, stores[0]["loop_iters"] or 64)
     need_s = sum(stride * execs for _, stride, execs in lay["scalar"].values())
     need_m = sum(stride * execs for _, stride, execs in lay["matrix"].values())
     need_k = sum(int(inputs[d.name].size) for d in cf.inputs if d.is_private)
@@ -392,7 +402,8 @@ def run_bundle(bundle: RunBundle, devices=None, coin: int | None = None) -> RunR
             raise InvalidArgument(f"triple store belongs to party {st['party']}, run expects {i}")
         if st["n_parties"] != n:
             raise InvalidArgument(f"store expects {st['n_parties']} parties, bundle has {n} stores")
-    r = LocalRun(bundle.graph, n, bundle.slice, devices=devices, coin=coin)
+    r = LocalRun(bundle.graph, n, bundle.slice, devices=devices, coin=coin,
+                 loop_iters=bundle.stores[0]["loop_iters"] or 64)
     try:
         for i, path in enumerate(bundle.triples):
             r.load_store(i, path)

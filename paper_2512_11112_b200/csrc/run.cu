@@ -75,6 +75,11 @@ struct NodeState {                  // per party, per node
     uint32_t *bias_v = nullptr, *bias_m = nullptr;
     uint32_t *mA[2] = {nullptr, nullptr}, *mB[2] = {nullptr, nullptr}, *mC[2] = {nullptr, nullptr};
     uint32_t* lin_tmp = nullptr;    // public x public scratch
+    // control flow: a Beaver node's opened values and operand MAC shares, one slot per
+    // execution (the MAC check reads every execution's record after the last one)
+    uint32_t* opened_all = nullptr;
+    uint32_t* macsnap = nullptr;
+    bool dyn_load = false;          // LOAD whose start is computed at run time (own buffer)
 };
 
 struct LinTiles {
@@ -142,6 +147,9 @@ struct spdz_run {
     std::map<uint32_t, uint64_t> input_mask_off;          // private input node -> first mask (local)
     std::map<uint32_t, uint64_t> input_mask_gfirst;       // ... global index of that mask
     uint64_t scalar_total_global = 0, mask_total_global = 0;
+    bool cfg = false;               // graph with PHI/BRANCH: block-by-block execution (run_cfg)
+    uint64_t loop_iters = 64;       // triple provisioning of loop bodies (preproc.cpp:124-163)
+    uint64_t scalar_used = 0, matrix_used = 0;  // consumed by the last phase (control flow)
     uint64_t shard_off = 0, shard_total = 0, shard_L = 0;  // shard_total == 0: unsharded
     std::map<uint32_t, std::vector<uint32_t>> inputs;     // cleartext (host)
     std::map<uint32_t, uint32_t*> input_dev;              // cleartext staged on party 0's device
@@ -274,24 +282,31 @@ void plan_layout(spdz_run* r) {
     const uint64_t G = r->shard_total, off = r->shard_off;
     for (auto& n : r->nodes) {
         const uint32_t id = (uint32_t)(&n - r->nodes.data());
-        if (sh && n.lanes != 1 && n.lanes != r->shard_L && n.kind != SPDZ_NODE_NOP)
+        if (sh && n.lanes != 1 && n.lanes != r->shard_L && n.kind != SPDZ_NODE_NOP && n.kind != SPDZ_NODE_LABEL)
             throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: every vector node must have the shard's lanes");
+        // executions provisioned: loop_iters per enclosing loop (preproc.cpp:127-130)
+        uint64_t mult = 1;
+        for (uint32_t d = 0; d < n.loop_depth; ++d) {
+            need(mult <= (1ull << 40) / std::max<uint64_t>(r->loop_iters, 1), SPDZ_ERR_INVALID_ARGUMENT,
+                 "loop provisioning overflows");
+            mult *= r->loop_iters;
+        }
         switch (n.kind) {
             case SPDZ_NODE_MUL:
                 if (r->priv(n.operands[0]) && r->priv(n.operands[1])) {
-                    Region g{r->scalar_total, n.lanes, 1, sh ? r->scalar_total_global + off : r->scalar_total};
+                    Region g{r->scalar_total, n.lanes, mult, sh ? r->scalar_total_global + off : r->scalar_total};
                     r->scalar[id] = g;
-                    r->scalar_total += n.lanes;
-                    r->scalar_total_global += sh ? G : n.lanes;
+                    r->scalar_total += n.lanes * mult;
+                    r->scalar_total_global += (sh ? G : n.lanes) * mult;
                 }
                 break;
             case SPDZ_NODE_REDUCE_MUL: {
                 const auto& src = r->node(n.operands[0]);
                 if (sh) throw Error(SPDZ_ERR_INVALID_ARGUMENT, "sharded run: reduce_mul is not lane-parallel");
                 if (src.is_private && src.lanes >= 1) {
-                    r->scalar[id] = {r->scalar_total, src.lanes - 1ull, 1, r->scalar_total};
-                    r->scalar_total += src.lanes - 1ull;
-                    r->scalar_total_global += src.lanes - 1ull;
+                    r->scalar[id] = {r->scalar_total, src.lanes - 1ull, mult, r->scalar_total};
+                    r->scalar_total += (src.lanes - 1ull) * mult;
+                    r->scalar_total_global += (src.lanes - 1ull) * mult;
                 }
                 break;
             }
@@ -311,9 +326,10 @@ void plan_layout(spdz_run* r) {
                     lt.starts.resize(nt);
                     lt.counts.resize(nt);
                     lt.rpt = lt.counts[0];
-                    r->matrix[id] = {r->matrix_total, nt, 1};
-                    r->matrix_total += nt;
-                    for (auto c : lt.counts) r->mshapes.emplace_back(n.din, c);
+                    r->matrix[id] = {r->matrix_total, nt, mult};
+                    r->matrix_total += nt * mult;
+                    for (uint64_t k = 0; k < mult; ++k)  // preproc.cpp:104-112: per execution, per tile
+                        for (auto c : lt.counts) r->mshapes.emplace_back(n.din, c);
                     r->tiles[id] = lt;
                 }
                 break;
@@ -376,9 +392,21 @@ void plan_buffers(spdz_run* r) {
                     pub_out(1);
                     break;
                 case SPDZ_NODE_NOP:
+                case SPDZ_NODE_LABEL:
+                case SPDZ_NODE_BRANCH:
+                    break;
+                case SPDZ_NODE_PHI:  // its own buffer: the chosen value is copied in at block entry
+                    if (n.is_private) priv_out(L);
+                    else pub_out(L);
                     break;
                 case SPDZ_NODE_LOAD: {  // runtime.cpp:419-438 (zero-copy slice)
                     const Val& base = opnd(0);
+                    if (r->node(n.operands[1]).kind != SPDZ_NODE_CONST) {  // start known at run time: copied
+                        st.dyn_load = true;
+                        if (base.is_public) pub_out(L);
+                        else priv_out(L);
+                        break;
+                    }
                     const uint32_t start = const_of(r, n.operands[1]);
                     need((uint64_t)start + L <= base.lanes, SPDZ_ERR_INVALID_ARGUMENT, "runtime: load out of bounds");
                     st.out = base;
@@ -407,6 +435,11 @@ void plan_buffers(spdz_run* r) {
                         if (b.lanes != L) st.xb = Val{false, nullptr, r->alloc(p, L), r->alloc(p, L), L};
                         st.payload = r->alloc(p, 2 * L);
                         st.opened = r->alloc(p, 2 * L);
+                        if (r->cfg) {  // one MAC-log slot per provisioned execution
+                            const uint64_t execs = r->scalar.at(id).max_execs;
+                            st.opened_all = r->alloc(p, 2 * L * execs);
+                            st.macsnap = r->alloc(p, 2 * L * execs);
+                        }
                     } else {
                         priv_out(L);
                     }
@@ -418,6 +451,8 @@ void plan_buffers(spdz_run* r) {
                     break;
                 case SPDZ_NODE_REDUCE_MUL: {
                     const Val& a = opnd(0);
+                    need(!r->cfg || !r->scalar.count(id) || r->scalar.at(id).max_execs == 1, SPDZ_ERR_INVALID_ARGUMENT,
+                         "UnsupportedCircuit: reduce_mul inside a loop");
                     if (a.is_public) {
                         pub_out(1);
                         st.opened = r->alloc(p, std::max<uint64_t>(a.lanes, 1));  // scratch tree
@@ -449,6 +484,8 @@ void plan_buffers(spdz_run* r) {
                 }
                 case SPDZ_NODE_LINEAR: {
                     const Val &x = opnd(0), &w = opnd(1);
+                    need(!r->cfg || !r->matrix.count(id) || r->matrix.at(id).max_execs == 1, SPDZ_ERR_INVALID_ARGUMENT,
+                         "UnsupportedCircuit: linear layer inside a loop");
                     need(x.lanes == n.din && w.lanes == (uint64_t)n.din * n.dout, SPDZ_ERR_INVALID_ARGUMENT,
                          "ShapeMismatch: linear operands do not match din/dout");
                     if (x.is_public && w.is_public) {
@@ -587,9 +624,14 @@ void load_store(spdz_run* r, int p, const char* path) {
     need(L.party == p && L.n_parties == r->n, SPDZ_ERR_STORE_FORMAT,
          "VersionMismatch: store is party " + std::to_string(L.party) + " of " + std::to_string(L.n_parties) +
              ", run needs party " + std::to_string(p) + " of " + std::to_string(r->n));
+    // the layout of loop bodies scales with the store's loop_iters (PartyRuntime plans it from the store)
+    bool loops = false;
+    for (auto& nd : r->nodes) loops = loops || nd.loop_depth > 0;
+    need(!loops || L.loop_iters == r->loop_iters, SPDZ_ERR_STORE_FORMAT,
+         "VersionMismatch: store provisioned for loop_iters " + std::to_string(L.loop_iters) + ", run planned for " +
+             std::to_string(r->loop_iters));
     // demand check of load_run_bundle (preproc.cpp:182-201)
-    size_t mats_needed = 0;
-    for (auto& [id, reg] : r->matrix) mats_needed += r->tiles[id].starts.size();
+    const size_t mats_needed = r->matrix_total;
     if (L.n_scalar < r->scalar_total_global)
         throw Error(SPDZ_ERR_INSUFFICIENT_TRIPLES, "InsufficientTriples: need " + std::to_string(r->scalar_total_global) +
                                                        " scalar triples, store has " + std::to_string(L.n_scalar));
@@ -726,7 +768,11 @@ struct Exec {
     int tbegin(int p) { return ktimer_begin(r, p); }
     void tend(int p, int idx, int cls, uint64_t bytes) { ktimer_end(r, p, idx, cls, bytes); }
 
-    cudaEvent_t next_event(int p) { return r->parties[p].evs.at(ev_cursor[p]++); }
+    cudaEvent_t next_event(int p) {  // loops open a node once per execution: the pool grows on demand
+        auto& evs = r->parties[p].evs;
+        if (ev_cursor[p] >= (int)evs.size()) new_event(r, p);
+        return evs.at(ev_cursor[p]++);
+    }
 
     // party p's payload for `slot` is complete on its stream: tell local peers
     // (event) and remote peers (flag word, spdz_run_import)
@@ -837,6 +883,146 @@ struct Exec {
         return src;
     }
 
+    // The MAC shares a Beaver record is checked against: the operand planes themselves, or
+    // (control flow, where a later execution rewrites them) a per-execution snapshot.
+    const uint32_t* mac_slot(int p, uint32_t id, uint64_t exec, int which) {
+        auto& st = r->parties[p].ns[id];
+        const Val& x = which ? st.xb : st.xa;
+        if (!r->cfg) return x.m;
+        const uint64_t L = r->node(id).lanes;
+        uint32_t* dst = st.macsnap + 2 * L * exec + (which ? L : 0);
+        dev(r, p);
+        lk(cudaMemcpyAsync(dst, x.m, L * 4, cudaMemcpyDeviceToDevice, S(r, p)), "mac snapshot");
+        return dst;
+    }
+
+    // runtime.cpp:119-125 read_public: lane 0 of a completed public value (host read)
+    uint32_t read_public(uint32_t id) {
+        const int p = r->ref_party();
+        const Val& v = r->parties[p].ns[id].out;
+        need(v.is_public && v.lanes >= 1 && v.pub, SPDZ_ERR_INVALID_ARGUMENT,
+             "runtime: node " + std::to_string(id) + " is not a completed public scalar");
+        dev(r, p);
+        uint32_t x = 0;
+        lk(cudaMemcpyAsync(&x, v.pub, 4, cudaMemcpyDeviceToHost, S(r, p)), "read public");
+        lk(cudaStreamSynchronize(S(r, p)), "read public");
+        return x;
+    }
+
+    // runtime.cpp:419-438 with a start computed at run time: copy the slice
+    void load_dynamic(uint32_t id) {
+        const auto& n = r->node(id);
+        const uint32_t start = read_public(n.operands[1]);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            if (!P.local) continue;
+            const Val& base = P.ns[n.operands[0]].out;
+            const Val& o = P.ns[id].out;
+            need((uint64_t)start + n.lanes <= base.lanes, SPDZ_ERR_INVALID_ARGUMENT, "runtime: load out of bounds");
+            dev(r, p);
+            if (base.is_public) {
+                lk(cudaMemcpyAsync(o.pub, base.pub + start, n.lanes * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "load");
+            } else {
+                lk(cudaMemcpyAsync(o.v, base.v + start, n.lanes * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "load");
+                lk(cudaMemcpyAsync(o.m, base.m + start, n.lanes * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "load");
+            }
+        }
+    }
+
+    // vals[phi] = vals[chosen] (scheduler.cpp:242-262 via resolve_phi), into the phi's own
+    // buffer: broadcast a 1-lane value, and a public value reaching a private phi becomes
+    // the sharing of that public (share_of_public, spdz.cpp:66-75)
+    void phi_copy(uint32_t phi, uint32_t chosen) {
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            if (!P.local) continue;
+            const Val& s = P.ns[chosen].out;
+            const Val& o = P.ns[phi].out;
+            need(s.lanes == o.lanes || s.lanes == 1, SPDZ_ERR_LANE_MISMATCH,
+                 "LaneMismatch: phi " + std::to_string(phi) + " takes " + std::to_string(s.lanes) + " lanes into " +
+                     std::to_string(o.lanes));
+            dev(r, p);
+            spdz_ctx* c = P.ctx;
+            if (o.is_public) {
+                need(s.is_public, SPDZ_ERR_INVALID_ARGUMENT, "runtime: private value reaches public phi");
+                if (s.lanes == o.lanes)
+                    lk(cudaMemcpyAsync(o.pub, s.pub, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
+                else
+                    lk(launch_bcast(c->stream, s.pub, nullptr, o.pub, nullptr, o.lanes, c->sms), "phi bcast");
+                continue;
+            }
+            if (s.is_public) {  // party 0 holds k, MAC shares alpha_i * k
+                lk(launch_public(c->stream, 4, nullptr, nullptr, s.pub, s.lanes != o.lanes, 0u, false, c->party,
+                                 c->alpha, o.v, o.m, o.lanes, c->sms, c->d_alpha),
+                   "phi share_of_public");
+            } else if (s.lanes == o.lanes) {
+                lk(cudaMemcpyAsync(o.v, s.v, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
+                lk(cudaMemcpyAsync(o.m, s.m, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
+            } else {
+                lk(launch_bcast(c->stream, s.v, s.m, o.v, o.m, o.lanes, c->sms), "phi bcast");
+            }
+        }
+    }
+
+    // Block-by-block execution of a control-flow graph: the sequential reading of the
+    // reference's dataflow scheduler (scheduler.cpp).  Entering a block resolves its phis
+    // from the predecessor, then its nodes run in `next` order; a BRANCH reads its public
+    // condition (the one host synchronisation) and enters the successor; ROOT ends the phase.
+    void run_cfg() {
+        const uint32_t N = (uint32_t)r->nodes.size();
+        std::vector<uint64_t> execs(N, 0);
+        uint32_t label = r->opts.entry_label, pred = SPDZ_NO_NODE;
+        for (;;) {
+            need(label < N && r->nodes[label].kind == SPDZ_NODE_LABEL, SPDZ_ERR_INVALID_ARGUMENT,
+                 "runtime: block " + std::to_string(label) + " is not a block label");
+            // phi choices first, as enter_block_locked seeds them
+            std::vector<std::pair<uint32_t, uint32_t>> phis;
+            for (uint32_t u = r->nodes[label].next; u != SPDZ_NO_NODE; u = r->nodes.at(u).next) {
+                const auto& n = r->nodes.at(u);
+                if (n.kind != SPDZ_NODE_PHI) continue;
+                if (pred == SPDZ_NO_NODE)
+                    throw Error(SPDZ_ERR_INVALID_ARGUMENT, "UnknownPredecessor: phi " + std::to_string(u) +
+                                                               " entered with no recorded predecessor");
+                uint32_t chosen = SPDZ_NO_NODE;
+                for (uint32_t i = 0; i < n.n_operands; ++i)
+                    if (n.phi_labels[i] == pred) {
+                        chosen = n.operands[i];
+                        break;
+                    }
+                if (chosen == SPDZ_NO_NODE)
+                    throw Error(SPDZ_ERR_INVALID_ARGUMENT, "UnknownPredecessor: phi " + std::to_string(u) +
+                                                               " has no pair for block " + std::to_string(pred));
+                phis.emplace_back(u, chosen);
+            }
+            for (auto [phi, chosen] : phis) phi_copy(phi, chosen);
+            uint32_t dst = SPDZ_NO_NODE;
+            for (uint32_t u = r->nodes[label].next; u != SPDZ_NO_NODE; u = r->nodes.at(u).next) {
+                const auto& n = r->nodes.at(u);
+                if (n.kind == SPDZ_NODE_PHI) continue;
+                if (n.kind == SPDZ_NODE_ROOT) return;
+                if (n.kind == SPDZ_NODE_BRANCH) {  // scheduler.cpp:283-313
+                    if (n.n_succ == 1) {
+                        dst = n.succ[0];
+                    } else {
+                        need(n.n_succ == 2 && n.n_operands >= 1, SPDZ_ERR_INVALID_ARGUMENT, "runtime: malformed branch");
+                        const uint32_t cond = n.operands[0];
+                        if (r->priv(cond))
+                            throw Error(SPDZ_ERR_INVALID_ARGUMENT, "SecretControlFlow: branch " + std::to_string(u) +
+                                                                       " conditioned on private node " +
+                                                                       std::to_string(cond));
+                        dst = read_public(cond) ? n.succ[0] : n.succ[1];
+                    }
+                    break;
+                }
+                exec_node(u, execs[u]++);
+            }
+            need(dst != SPDZ_NO_NODE, SPDZ_ERR_INVALID_ARGUMENT,
+                 "runtime: block " + std::to_string(label) + " ends without a branch or the root");
+            pred = label;
+            label = dst;
+        }
+    }
+
     // Beaver multiply (runtime.cpp:204-239): mask -> open [d|e] -> combine, all parties.
     // Both parties of a 2-party run on one stream: both masks, then one fused open+combine
     // (payloads read once, opened values logged once).  (Running it in L2-sized lane blocks so
@@ -884,6 +1070,14 @@ struct Exec {
         const auto& n = r->node(id);
         const uint64_t L = n.lanes;
         const uint64_t off = reg.base + exec * reg.stride;  // runtime.cpp:197
+        if (r->cfg) {  // control flow: this execution's record gets its own slot (opened values + MAC shares)
+            for (int p = 0; p < r->n; ++p) {
+                auto& P = r->parties[p];
+                if (!P.local) continue;
+                auto& st = P.ns[id];
+                st.opened = st.opened_all + 2 * L * exec;
+            }
+        }
         bool pair = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
         for (auto& f : r->faults) pair = pair && f.node != id;
         if (pair) {
@@ -894,8 +1088,10 @@ struct Exec {
             for (int p = 0; p < 2; ++p) {  // log_open (runtime.cpp:224); the opened values are public
                 auto& P = r->parties[p];
                 auto& st = P.ns[id];
-                P.maclog.push_back({s0.opened, st.xa.m, P.pool[1] + off, L, 0, batch, so, 2 * G});
-                P.maclog.push_back({s0.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
+                const uint32_t* mx = mac_slot(p, id, exec, 0);
+                const uint32_t* my = mac_slot(p, id, exec, 1);
+                P.maclog.push_back({s0.opened, mx, P.pool[1] + off, L, 0, batch, so, 2 * G});
+                P.maclog.push_back({s0.opened + L, my, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
             }
             return;
         }
@@ -943,8 +1139,8 @@ struct Exec {
             // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
             tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
             // log_open (runtime.cpp:224): records [d | e] with mac shares [x.m - a.m | y.m - b.m]
-            P.maclog.push_back({st.opened, st.xa.m, P.pool[1] + off, L, 0, batch, so, 2 * G});
-            P.maclog.push_back({st.opened + L, st.xb.m, P.pool[3] + off, L, 0, batch, G + so, 2 * G});
+            P.maclog.push_back({st.opened, mac_slot(p, id, exec, 0), P.pool[1] + off, L, 0, batch, so, 2 * G});
+            P.maclog.push_back({st.opened + L, mac_slot(p, id, exec, 1), P.pool[3] + off, L, 0, batch, G + so, 2 * G});
         }
     }
 
@@ -1209,14 +1405,35 @@ struct Exec {
     }
 
     void run_nodes() {
-        for (uint32_t id = 0; id < r->nodes.size(); ++id) {
+        for (uint32_t id = 0; id < r->nodes.size(); ++id) exec_node(id, 0);
+    }
+
+    // runtime.cpp:185-200: execution `exec` of a triple-consuming node must be provisioned
+    const Region& provisioned(const std::map<uint32_t, Region>& regs, uint32_t id, uint64_t exec) {
+        const Region& g = regs.at(id);
+        if (exec >= g.max_execs)
+            throw Error(SPDZ_ERR_TRIPLE_EXHAUSTED, "TripleExhausted: node " + std::to_string(id) + " executed " +
+                                                       std::to_string(exec + 1) + " times, provisioned for " +
+                                                       std::to_string(g.max_execs) +
+                                                       " (raise --loop-iters at preprocessing)");
+        return g;
+    }
+
+    // runtime.cpp:360-450, one execution of node `id`
+    void exec_node(uint32_t id, uint64_t exec) {
+        {
             const auto& n = r->nodes[id];
             switch (n.kind) {
                 case SPDZ_NODE_INPUT:
                 case SPDZ_NODE_CONST:
                 case SPDZ_NODE_NOP:
-                case SPDZ_NODE_LOAD:
+                case SPDZ_NODE_LABEL:
+                case SPDZ_NODE_PHI:     // resolved at block entry (run_cfg)
+                case SPDZ_NODE_BRANCH:  // taken by run_cfg
                 case SPDZ_NODE_ROOT:
+                    break;
+                case SPDZ_NODE_LOAD:
+                    if (r->parties[r->ref_party()].ns[id].dyn_load) load_dynamic(id);
                     break;
                 case SPDZ_NODE_ADD:
                 case SPDZ_NODE_SUB:
@@ -1229,7 +1446,10 @@ struct Exec {
                 case SPDZ_NODE_MUL: {
                     const bool a = r->parties[r->ref_party()].ns[n.operands[0]].out.is_public;
                     const bool b = r->parties[r->ref_party()].ns[n.operands[1]].out.is_public;
-                    if (!a && !b) beaver(id, r->scalar.at(id), 0);
+                    if (!a && !b) {
+                        beaver(id, provisioned(r->scalar, id, exec), exec);
+                        r->scalar_used += n.lanes;
+                    }
                     else
                         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
@@ -1262,11 +1482,15 @@ struct Exec {
                             dev(r, p);
                             reduce_mul_public(p, id);
                         }
-                    else
-                        reduce_mul(id, r->scalar.at(id), 0);
+                    else {
+                        const Region& g = provisioned(r->scalar, id, exec);
+                        reduce_mul(id, g, exec);
+                        r->scalar_used += g.stride;
+                    }
                     break;
                 case SPDZ_NODE_LINEAR:
-                    linear(id, 0);
+                    if (r->matrix.count(id)) r->matrix_used += provisioned(r->matrix, id, exec).stride;
+                    linear(id, exec);
                     break;
                 default:
                     throw Error(SPDZ_ERR_INVALID_ARGUMENT, "runtime: unexpected node kind");
@@ -1533,7 +1757,7 @@ void share_inputs(spdz_run* r) {
 // a lane-parallel circuit (no linear layers or reductions, whose launchers size scratch
 // buffers and grids at call time), no fault injection, no per-kernel timing.
 bool graphable(spdz_run* r) {
-    if (!r->opts.use_graph || r->any_remote || r->opts.profile_kernels || !r->faults.empty()) return false;
+    if (!r->opts.use_graph || r->cfg || r->any_remote || r->opts.profile_kernels || !r->faults.empty()) return false;
     for (int p = 0; p < r->n; ++p)
         if (!r->parties[p].local || S(r, p) != S(r, 0)) return false;
     for (const auto& n : r->nodes)
@@ -1574,13 +1798,14 @@ void for_each_export(spdz_run* r, int p, F&& f) {
 
 extern "C" {
 
-int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t* out, uint64_t cap,
-                       uint64_t* n_regions) {
+int spdz_triple_layout(const spdz_node_t* nodes, uint32_t n_nodes, uint64_t slice, uint64_t loop_iters,
+                       uint64_t* out, uint64_t cap, uint64_t* n_regions) {
     return guard([&] {  // host only: the planning step of spdz_run_create
         need(nodes && n_nodes > 0 && n_regions, SPDZ_ERR_INVALID_ARGUMENT, "bad layout arguments");
         spdz_run r;
         r.nodes.assign(nodes, nodes + n_nodes);
         r.opts.slice = slice ? slice : 262140;
+        r.loop_iters = loop_iters ? loop_iters : 64;
         plan_layout(&r);
         uint64_t k = 0;
         for (int kind = 0; kind < 2; ++kind)
@@ -1612,10 +1837,27 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
         if (opts) r->opts = *opts;
         if (r->opts.slice == 0) r->opts.slice = 262140;
         if (r->opts.dealer_seed == 0 && !opts) r->opts.dealer_seed = 1;
+        r->loop_iters = r->opts.loop_iters ? r->opts.loop_iters : 64;
         for (uint32_t id = 0; id < n_nodes; ++id)
-            for (uint32_t k = 0; k < nodes[id].n_operands; ++k)
-                need(nodes[id].operands[k] < id, SPDZ_ERR_INVALID_ARGUMENT,
-                     "graph must be topologically ordered (operand id < node id)");
+            if (nodes[id].kind == SPDZ_NODE_PHI || nodes[id].kind == SPDZ_NODE_BRANCH) r->cfg = true;
+        for (uint32_t id = 0; id < n_nodes; ++id) {
+            const auto& nd = nodes[id];
+            need(nd.n_operands <= 3, SPDZ_ERR_INVALID_ARGUMENT, "at most 3 operands per node");
+            for (uint32_t k = 0; k < nd.n_operands; ++k)  // a phi may read a later node (loop back edge)
+                need(nd.kind == SPDZ_NODE_PHI ? nd.operands[k] < n_nodes : nd.operands[k] < id,
+                     SPDZ_ERR_INVALID_ARGUMENT, "graph must be topologically ordered (operand id < node id)");
+            if (r->cfg && nd.next != SPDZ_NO_NODE)
+                need(nd.next < n_nodes, SPDZ_ERR_INVALID_ARGUMENT, "block chain leaves the graph");
+            if (nd.kind == SPDZ_NODE_BRANCH)
+                for (uint32_t k = 0; k < nd.n_succ && k < 2; ++k)
+                    need(nd.succ[k] < n_nodes, SPDZ_ERR_INVALID_ARGUMENT, "branch target out of range");
+        }
+        if (r->cfg) {
+            need(r->opts.entry_label < n_nodes && nodes[r->opts.entry_label].kind == SPDZ_NODE_LABEL,
+                 SPDZ_ERR_INVALID_ARGUMENT, "control-flow graph needs entry_label = its entry block's LABEL");
+            need(!r->opts.shard_total && !r->opts.single_party, SPDZ_ERR_INVALID_ARGUMENT,
+                 "control-flow graphs run with every party local and unsharded");
+        }
         r->devices.resize(n_parties);
         for (int p = 0; p < n_parties; ++p) r->devices[p] = (opts && opts->devices[p] >= 0) ? opts->devices[p] : 0;
         r->parties.resize(n_parties);
@@ -1648,6 +1890,7 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
                 else cuda_check(e, "cudaDeviceEnablePeerAccess");
             }
         if (r->opts.shard_total) {
+            need(!r->cfg, SPDZ_ERR_INVALID_ARGUMENT, "sharded runs are straight-line");
             r->shard_off = r->opts.shard_offset;
             r->shard_total = r->opts.shard_total;
             for (auto& nd : r->nodes)
@@ -1806,7 +2049,9 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
             lk(cudaGraphLaunch(r->online_graph, s), "cudaGraphLaunch");
         } else {
             Exec ex{r};
-            ex.run_nodes();
+            r->scalar_used = r->matrix_used = 0;
+            if (r->cfg) ex.run_cfg();
+            else ex.run_nodes();
             ex.open_root();
         }
         r->consumed = true;
@@ -1897,8 +2142,9 @@ int spdz_run_mac_check(spdz_run* r, int use_coin, uint64_t coin, spdz_run_report
                 dmax = std::max(dmax, (double)ms);
             }
             rep->online_device_ms = dmax;
-            rep->scalar_triples_consumed = r->scalar_total;
-            rep->matrix_triples_consumed = r->matrix_total;
+            // straight-line: every provisioned triple; control flow: what the taken path used
+            rep->scalar_triples_consumed = r->cfg ? r->scalar_used : r->scalar_total;
+            rep->matrix_triples_consumed = r->cfg ? r->matrix_used : r->matrix_total;
             rep->bytes_exchanged = r->exchanged;
             rep->output_digest = 0;  // spdz_run_output_digest (host byte loop, outside the online phase)
             rep->kernel_launches = g_kernel_launches - r->launches0;

@@ -20,7 +20,8 @@ import numpy as np
 from . import _lib
 from ._lib import check, lib
 
-INPUT, CONST, ADD, SUB, MUL, REDUCE_ADD, REDUCE_MUL, LINEAR, ROOT, LOAD, NOP, CMP_PUBLIC = range(12)
+INPUT, CONST, ADD, SUB, MUL, REDUCE_ADD, REDUCE_MUL, LINEAR, ROOT, LOAD, NOP, CMP_PUBLIC, PHI, BRANCH, LABEL = range(15)
+NO_NODE = 0xFFFFFFFF
 KIND_NAMES = {"Input": INPUT, "Const": CONST, "Adder": ADD, "AddBatch": ADD, "Subtract": SUB, "SubBatch": SUB,
               "Multiplier": MUL, "MultBatch": MUL, "ReduceAdd": REDUCE_ADD, "ReduceMul": REDUCE_MUL,
               "LinearLayer": LINEAR, "Root": ROOT, "Load": LOAD, "BlockLabel": NOP, "CmpPublic": CMP_PUBLIC}
@@ -36,6 +37,11 @@ class NodeSpec:
     dout: int = 0
     const_val: int = 0
     name: str = ""
+    # control flow (PHI / BRANCH / LABEL graphs; include/spdz_b200.h spdz_node_t)
+    next: int = NO_NODE
+    loop_depth: int = 0
+    succ: tuple = ()
+    phi_labels: tuple = ()
 
 
 @dataclass
@@ -44,6 +50,7 @@ class Graph:
     root: int = -1
     inputs: dict = field(default_factory=dict)  # name -> node id (g.inputs order)
     const_inputs: dict = field(default_factory=dict)  # name -> values of vector constants bound as public inputs
+    entry_label: int = 0  # control-flow graphs: the entry block's LABEL
 
     def add(self, spec: NodeSpec) -> int:
         self.nodes.append(spec)
@@ -65,6 +72,11 @@ class Graph:
             for k, o in enumerate(n.operands):
                 c.operands[k] = o
             c.din, c.dout, c.const_val = n.din, n.dout, n.const_val
+            c.next, c.loop_depth, c.n_succ = n.next, n.loop_depth, len(n.succ)
+            for k, t in enumerate(n.succ):
+                c.succ[k] = t
+            for k, t in enumerate(n.phi_labels):
+                c.phi_labels[k] = t
         return arr
 
 
@@ -169,14 +181,15 @@ class RunReport:
         return self.output_digest_cached
 
 
-def triple_layout(graph: Graph, slice_: int = 262140) -> dict:
+def triple_layout(graph: Graph, slice_: int = 262140, loop_iters: int = 64) -> dict:
     """The triple layout a run of `graph` uses (host only; preproc.cpp:124-163):
-    {"scalar"|"matrix": {node: (base, stride, max_execs)}}."""
+    {"scalar"|"matrix": {node: (base, stride, max_execs)}}; loop bodies provisioned
+    loop_iters times per enclosing loop."""
     nodes = graph.to_c()
     n = C.c_uint64()
-    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, None, 0, C.byref(n)))
+    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, loop_iters, None, 0, C.byref(n)))
     buf = (C.c_uint64 * (5 * max(n.value, 1)))()
-    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, buf, n.value, C.byref(n)))
+    check(lib().spdz_triple_layout(nodes, len(graph.nodes), slice_, loop_iters, buf, n.value, C.byref(n)))
     out = {"scalar": {}, "matrix": {}}
     for k in range(n.value):
         kind, node, base, stride, execs = buf[5 * k:5 * k + 5]
@@ -199,7 +212,7 @@ class LocalRun:
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
                  stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
-                 single_party: int | None = None, use_graph: bool = False):
+                 single_party: int | None = None, use_graph: bool = False, loop_iters: int = 64):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -209,6 +222,8 @@ class LocalRun:
         o.profile_kernels = int(profile_kernels)
         o.stream_per_party = int(stream_per_party)
         o.use_graph = int(use_graph)  # online phase captured once as a CUDA graph, then replayed
+        o.entry_label = graph.entry_label
+        o.loop_iters = loop_iters  # control flow: loop bodies' triple provisioning (the store's loop_iters)
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
         o.external_mac_verify = int(external_mac_verify or single_party is not None)

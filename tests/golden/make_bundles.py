@@ -47,11 +47,32 @@ declare i32 @llvm.vector.reduce.add.v16i32(<16 x i32>)
 """ + workloads._DECL
 
 
+# a vector loop: acc <- acc * y + x, n times (public trip count); Beaver inside the loop body
+VECTOR_LOOP_IR = workloads._HDR + """define <512 x i32> @main(ptr %x, ptr %y, i32 %n) {
+entry:
+""" + workloads._ann("x", True) + workloads._ann("y", True) + """  %a = load <512 x i32>, ptr %x
+  %b = load <512 x i32>, ptr %y
+  br label %loop
+loop:
+  %i = phi i32 [ 1, %entry ], [ %inext, %loop ]
+  %acc = phi <512 x i32> [ %a, %entry ], [ %acc2, %loop ]
+  %t = mul <512 x i32> %acc, %b
+  %acc2 = add <512 x i32> %t, %a
+  %inext = add i32 %i, 1
+  %c = icmp sle i32 %inext, %n
+  br i1 %c, label %loop, label %exit
+exit:
+  ret <512 x i32> %acc2
+}
+
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
 
-# name -> (ir, parties, slice, dealer seed, inputs)
+# name -> (ir, parties, slice, dealer seed, inputs[, loop_iters])
 def cases():
     fx = lambda f: (FIXTURES / f).read_text()
     return {
@@ -67,11 +88,21 @@ def cases():
         "mixed_1024_n3": (workloads.chain_ir("mixed", 1024), 3, 262140, 10, {"x": rnd(1024, 13), "y": rnd(1024, 14)}),
         "linear_pub_w": (workloads.linear_ir(48, 40, w_private=False), 2, 262140, 11,
                          {"x": rnd(48, 15), "W": rnd(48 * 40, 16), "b": rnd(40, 17)}),
+        # control flow (Phi / Branch / loops), run block by block
+        "diamond_big": (fx("diamond.ll"), 2, 262140, 12, {"x": rnd(2, 18), "k": np.array([9], np.uint32)}),
+        "diamond_small": (fx("diamond.ll"), 3, 262140, 13, {"x": rnd(2, 19), "k": np.array([3], np.uint32)}),
+        "loop_sum": (fx("loop_sum.ll"), 2, 262140, 14, {"n": np.array([10], np.uint32)}, 16),
+        "nested_loop": (fx("nested_loop.ll"), 2, 262140, 15,
+                        {"x": rnd(2, 20), "a": np.array([3], np.uint32), "b": np.array([4], np.uint32)}, 5),
+        "loop_after_loop": (fx("loop_after_loop.ll"), 3, 262140, 16, {"x": rnd(2, 21), "n": np.array([6], np.uint32)},
+                            8),
+        "vector_loop": (VECTOR_LOOP_IR, 2, 262140, 17, {"x": rnd(512, 22), "y": rnd(512, 23),
+                                                        "n": np.array([5], np.uint32)}, 6),
     }
 
 
-# circuits with control flow (Phi/Branch/loops): circuit files only (the executor rejects them)
-CONTROL_FLOW = ("diamond", "loop_sum", "nested_loop", "secret_branch")
+# circuit files only: parse / lowering tests (secret_branch: SecretControlFlow at run time)
+CONTROL_FLOW = ("diamond", "loop_sum", "nested_loop", "loop_after_loop", "secret_branch")
 
 
 def main():
@@ -80,16 +111,19 @@ def main():
     (OUT / "control_flow").mkdir(parents=True)
     for f in CONTROL_FLOW:
         ref.write_circuit_file((FIXTURES / f"{f}.ll").read_text(), OUT / "control_flow" / f"{f}.mpcg")
-    for name, (ir, n, slice_, seed, inputs) in cases().items():
+    for name, (ir, n, slice_, seed, inputs, *rest) in cases().items():
+        loop_iters = rest[0] if rest else 1
         d = OUT / name
         d.mkdir(parents=True)
         ref.write_circuit_file(ir, d / "circuit.mpcg")
         ref.write_input_file(inputs, d / "inputs.mpci")
-        ref.write_dealer_stores(ir, n, str(d), slice_=slice_, seed=seed, loop_iters=1)
+        ref.write_dealer_stores(ir, n, str(d), slice_=slice_, seed=seed, loop_iters=loop_iters)
         out, rep = ref.run_bundle(d / "circuit.mpcg", n, d, d / "inputs.mpci", slice_)
         clear = ref.interpret(ir, inputs)
         assert np.array_equal(out, clear), name  # the online phase opens the cleartext result
-        meta = {"parties": n, "slice": slice_, "dealer_seed": seed, "outputs": out.tolist(),
+        lay = ref.triple_layout(ir, slice_, loop_iters)
+        meta = {"parties": n, "slice": slice_, "dealer_seed": seed, "loop_iters": loop_iters,
+                "layout": {k: {str(i): v for i, v in m.items()} for k, m in lay.items()}, "outputs": out.tolist(),
                 "digest": rep["digest"], "scalar_triples": rep["scalar_triples"],
                 "matrix_triples": rep["matrix_triples"]}
         (d / "expected.json").write_text(json.dumps(meta, indent=1))

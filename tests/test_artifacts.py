@@ -8,10 +8,12 @@ Host (no GPU):
 * load_run_bundle's cross-checks fail with the reference's exception kind and
   message (ShapeMismatch, InsufficientTriples, VersionMismatch, CorruptPayload),
   compared against the reference's own load_run_bundle where oracle/_ref exists;
-* control-flow circuits are refused (UnsupportedCircuit).
+* control-flow circuits (the reference's loop/branch fixtures) lower to PHI /
+  BRANCH / LABEL graphs whose loop-provisioned layout == the reference's.
 
 GPU (-m gpu): run_files on every bundle == the reference's outputs, digest and
-triple consumption (party 0 of every party's ``llspdz run``).
+triple consumption (party 0 of every party's ``llspdz run``), control flow
+included; a branch on a private value fails with SecretControlFlow.
 """
 import json
 import shutil
@@ -68,10 +70,13 @@ def test_input_file_roundtrip(case, tmp_path):
 def test_bundle_checks_pass_and_layout(case):
     circ, stores, inp, exp = files(case)
     b = A.load_run_bundle(circ, stores, inp, exp["slice"])
-    assert b.demand["scalars"] == exp["scalar_triples"]
-    assert b.demand["matrices"] == exp["matrix_triples"]
-    for i, st in enumerate(b.stores):
+    for i, st in enumerate(b.stores):  # the dealer tool writes exactly the demand
         assert st["party"] == i and st["n_parties"] == exp["parties"]
+        assert (b.demand["scalars"], b.demand["matrices"], b.demand["masks"]) == (
+            st["scalar_triples"], st["matrix_triples"], st["input_masks"])
+    lay = rt.triple_layout(b.graph, exp["slice"], exp["loop_iters"])
+    want = {k: {int(i): tuple(v) for i, v in m.items()} for k, m in exp["layout"].items()}
+    assert lay == want
     if HAS_REF:
         for s in stores:
             ref.load_run_bundle(circ, s, inp, exp["slice"])
@@ -96,9 +101,24 @@ def test_cmp_public_lowered():
 
 
 @pytest.mark.parametrize("path", CF, ids=lambda p: p.stem)
-def test_control_flow_refused(path):
-    with pytest.raises(A.UnsupportedCircuit, match="UnsupportedCircuit: control flow"):
-        A.read_circuit_file(path).to_graph()
+def test_control_flow_lowered(path):
+    cf = A.read_circuit_file(path)
+    g = cf.to_graph()
+    kinds = [n.kind for n in g.nodes]
+    assert rt.BRANCH in kinds and g.nodes[g.entry_label].kind == rt.LABEL
+    for n, src in zip(g.nodes, cf.nodes):
+        assert n.next == src.next
+        if n.kind == rt.PHI:
+            assert len(n.phi_labels) == len(n.operands) and all(g.nodes[b].kind == rt.LABEL for b in n.phi_labels)
+    in_loops = {b for members, _ in cf.loops.values() for b in members}
+    assert all((n.loop_depth > 0) == (src.block in in_loops) for n, src in zip(g.nodes, cf.nodes))
+
+
+def test_loop_provisioning_nested():
+    circ, _, inp, exp = files("nested_loop")
+    g = A.read_circuit_file(circ).to_graph(A.read_input_file(inp))
+    (node, (base, stride, execs)), = rt.triple_layout(g, exp["slice"], 7)["scalar"].items()
+    assert g.nodes[node].loop_depth == 2 and execs == 49 and stride == 1
 
 
 # ---- error behaviour (preproc.cpp:165-202, circuit_io.cpp:117-185) ----
@@ -202,6 +222,45 @@ def test_run_files_matches_reference(gpu, case):
     assert rep.output_digest == exp["digest"]
     assert rep.scalar_triples_consumed == exp["scalar_triples"]
     assert rep.matrix_triples_consumed == exp["matrix_triples"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in CASES if json.loads((BUNDLES / c / "expected.json").read_text())
+                                  ["loop_iters"] > 1 or c.startswith("diamond")])
+def test_control_flow_dealer_path(gpu, case):
+    """The same control-flow circuits with the GPU dealer (run_local's loop_iters 64)."""
+    circ, _, inp, exp = files(case)
+    vals = A.read_input_file(inp)
+    g = A.read_circuit_file(circ).to_graph(vals)
+    rep = rt.run_local(g, exp["parties"], vals, exp["slice"], dealer_seed=5)
+    assert rep.outputs.tolist() == exp["outputs"]
+    assert rep.scalar_triples_consumed == exp["scalar_triples"]
+
+
+@pytest.mark.gpu
+def test_secret_branch_refused(gpu):
+    g = A.read_circuit_file(BUNDLES / "control_flow" / "secret_branch.mpcg").to_graph()
+    with pytest.raises(errors.InvalidArgument, match="SecretControlFlow: branch 6 conditioned on private node 5"):
+        rt.run_local(g, 2, {"p": np.array([1], np.uint32)})
+
+
+@pytest.mark.gpu
+def test_loop_beyond_provisioning(gpu):
+    """More iterations than the store provisions: TripleExhausted (runtime.cpp:185-200)."""
+    circ, stores, inp, exp = files("vector_loop")  # loop_iters 6
+    vals = A.read_input_file(inp)
+    vals["n"] = np.array([9], np.uint32)
+    g = A.read_circuit_file(circ).to_graph(vals)
+    r = rt.LocalRun(g, 2, exp["slice"], loop_iters=exp["loop_iters"])
+    try:
+        for i, s in enumerate(stores):
+            r.load_store(i, s)
+        r.bind_inputs(vals)
+        r.share_inputs()
+        with pytest.raises(errors.TripleExhausted, match="executed 7 times, provisioned for 6"):
+            r.online()
+    finally:
+        r.close()
 
 
 @pytest.mark.gpu
