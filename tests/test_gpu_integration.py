@@ -19,3 +19,18 @@ def test_reference_backend_interface_drop_in(gpu):
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+RT = ROOT / "integration" / "_build" / "check_runtime"
+
+
+@pytest.mark.gpu
+def test_reference_runtime_drop_in(gpu):
+    """The reference's CircuitGraph / Inputs / store files through integration/b200_runtime.cpp
+    (run_files_b200, run_local_b200) == the unmodified PartyRuntime / run_local."""
+    if not RT.exists():
+        pytest.skip("integration/_build/check_runtime not built (needs /root/reference at build time)")
+    r = subprocess.run([str(RT), str(ROOT / "tests" / "golden" / "bundles")], capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("PASS")
