@@ -52,6 +52,8 @@ typedef enum spdz_status {
     SPDZ_ERR_SLICE_TOO_SMALL = 11,       /* linear::SliceTooSmall        linear.hpp:10 */
     SPDZ_ERR_STORE_FORMAT = 12,          /* spdz::StoreFormatError       triple_store.hpp:23 */
     SPDZ_ERR_INSUFFICIENT_TRIPLES = 13,  /* preproc::InsufficientTriples preproc.cpp:182-201 */
+    SPDZ_ERR_NET = 14,                   /* net::NetError / ConnectTimeout / IndexCollision net.hpp:19-30
+                                            (the message starts with the type's name) */
     SPDZ_ERR_INVALID_ARGUMENT = 20,
     SPDZ_ERR_CUDA = 21,
     SPDZ_ERR_DEALER_REJECTION = 22,      /* GPU dealer hit the 25/2^64 rejection branch */
@@ -374,6 +376,10 @@ typedef struct spdz_run_options {
      * (RunOptions / the store's loop_iters; 0 = 64, run_local's hint, runtime.cpp:597). */
     uint32_t entry_label;
     uint64_t loop_iters;
+    /* 1: the non-local parties of a single_party run are across a spdz_net mesh
+     * (spdz_run_attach_net before the online phase); their opening buffers are
+     * mirrored in local HBM and filled from the peers' frames. */
+    int32_t network;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes
@@ -474,6 +480,27 @@ int spdz_run_outputs(spdz_run* run, uint32_t* host_out, uint64_t cap, uint64_t* 
 int spdz_run_node_share(spdz_run* run, int party, uint32_t node, spdz_share_t* out);
 /* Test hook: flip `bit` of the payload word `word` that party `receiver`
  * reads from `sender` for node `node` (SimHub BitFlip, net.cpp:241-278). */
+/* ---------------- cross-host parties: the reference's wire format + TCP mesh ----------------
+ * Frames of net.hpp:40-49 (16-byte header {msg-type u8, pad[3], lane-count u32, batch-id u64}
+ * + u32 words, little-endian) over the mesh of net_tcp.cpp:152-235 (party i listens on
+ * endpoints[i] for higher indices and dials lower ones, announcing its index as a u32).  A
+ * B200 party and reference parties (or other B200 hosts) interoperate frame for frame. */
+typedef struct spdz_net spdz_net;
+int spdz_net_connect(int party, int n_parties, const char* const* endpoints, uint64_t connect_timeout_ms,
+                     uint64_t io_timeout_ms, spdz_net** out);
+int spdz_net_destroy(spdz_net* net);
+/* raw frames (tests / tooling): msg-type 0 OpenShares 1 Commit 2 Reveal 3 Nonce 4 Control */
+int spdz_net_send(spdz_net* net, int peer, int type, uint64_t batch, const uint32_t* words, uint32_t lanes);
+int spdz_net_recv(spdz_net* net, int peer, int type, uint64_t batch, uint32_t* out, uint64_t cap, uint64_t* lanes);
+int spdz_net_stats(spdz_net* net, uint64_t* bytes_sent, uint64_t* bytes_received);
+/* A single-party run (options.single_party = p + 1) whose peers are across the mesh:
+ * every opening is sent / received as the reference's frames with its batch ids
+ * (make_batch(node, exec, sub), runtime.cpp:22-24; linear tiles batch + tile; inputs
+ * kInputBatchBase + k; the MAC check's four exchanges at kMacBatchBase + 0..3,
+ * runtime.cpp:467-506), and the MAC check runs the reference's commit/reveal protocol.
+ * The mesh must outlive the run. */
+int spdz_run_attach_net(spdz_run* run, spdz_net* net);
+
 int spdz_run_inject_bitflip(spdz_run* run, uint32_t node, int sender, int receiver, uint64_t word, uint32_t bit);
 
 #ifdef __cplusplus

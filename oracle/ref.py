@@ -101,6 +101,11 @@ def lib():
         L.reft_run_bundle.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_char_p, C.c_uint64, C.c_int, U32P,
                                       C.c_uint64, C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
                                       C.POINTER(C.c_uint64)]
+        L.reft_run_party_tcp.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                         C.POINTER(C.c_char_p), C.c_uint64, C.c_int, C.c_uint64, U32P, C.c_uint64,
+                                         C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
+                                         C.POINTER(C.c_uint64)]
+        L.reft_mesh_probe.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_char_p), C.c_uint64, U32P, U32P, U32P]
         L.reft_time_beaver_kernels.argtypes = [C.c_uint64, C.c_int]
         L.reft_time_beaver_kernels.restype = C.c_double
     return _lib
@@ -394,6 +399,34 @@ def run_bundle(circuit_path, n_parties: int, triples_dir, inputs_path, slice_: i
     report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
                   matrix_triples=int(rep[4]), digest=dig.value)
     return out[: n.value].copy(), report
+
+
+def _eps(endpoints):
+    return (C.c_char_p * len(endpoints))(*[e.encode() for e in endpoints])
+
+
+def run_party_tcp(circuit_path, triples_path, inputs_path, party: int, endpoints, slice_: int = 262140,
+                  threads: int = 1, io_timeout_ms: int = 60000, cap: int = 1 << 24):
+    """One reference party over its TCP mesh (tools/main.cpp:111-130 run_one_party)."""
+    out = np.empty(cap, np.uint32)
+    n = C.c_uint64()
+    rep = np.zeros(8, np.float64)
+    dig = C.c_uint64()
+    _check(lib().reft_run_party_tcp(str(circuit_path).encode(), str(triples_path).encode(),
+                                    str(inputs_path).encode(), party, len(endpoints), _eps(endpoints), slice_,
+                                    threads, io_timeout_ms, out, cap, C.byref(n), rep, C.byref(dig)))
+    report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
+                  matrix_triples=int(rep[4]), bytes_received=int(rep[5]), digest=dig.value)
+    return out[: n.value].copy(), report
+
+
+def mesh_probe(party: int, endpoints, own):
+    """connect_mesh + exchange(Control, 5, {party, 100+party}) + open(77, own)."""
+    own = u32(own)
+    exch = np.zeros(2 * len(endpoints), np.uint32)
+    opened = np.zeros(own.size, np.uint32)
+    _check(lib().reft_mesh_probe(party, len(endpoints), _eps(endpoints), own.size, own, exch, opened))
+    return exch.reshape(-1, 2), opened
 
 
 def time_beaver_kernels(lanes: int, reps: int = 3) -> float:

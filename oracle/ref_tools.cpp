@@ -22,6 +22,7 @@
 #include "mpc/hash.hpp"
 #include "mpc/ir.hpp"
 #include "mpc/linear.hpp"
+#include "mpc/net.hpp"
 #include "mpc/oracle.hpp"
 #include "mpc/preproc.hpp"
 #include "mpc/runtime.hpp"
@@ -511,6 +512,53 @@ int reft_run_bundle(const char* circuit_path, int n_parties, const char* triples
         report[3] = double(r0.scalar_triples_consumed);
         report[4] = double(r0.matrix_triples_consumed);
         *digest = r0.output_digest;
+    });
+}
+
+// ---- one party across the reference's TCP mesh (cross-host interop checks) ----
+net::MeshConfig mesh_config(int party, int n, const char* const* endpoints, uint64_t io_timeout_ms) {
+    net::MeshConfig mc;
+    mc.party = party;
+    for (int i = 0; i < n; ++i) mc.endpoints.emplace_back(endpoints[i]);
+    if (io_timeout_ms) mc.io_timeout = std::chrono::milliseconds(io_timeout_ms);
+    return mc;
+}
+
+// tools/main.cpp:111-130 run_one_party: load_run_bundle, connect_mesh, PartyRuntime::run.
+int reft_run_party_tcp(const char* circuit_path, const char* triples_path, const char* inputs_path, int party, int n,
+                       const char* const* endpoints, uint64_t slice, int threads, uint64_t io_timeout_ms, uint32_t* out,
+                       uint64_t cap, uint64_t* out_len, double* report, uint64_t* digest) {
+    return guard([&] {
+        auto b = preproc::load_run_bundle(circuit_path, triples_path, inputs_path, slice);
+        auto session = net::connect_mesh(mesh_config(party, n, endpoints, io_timeout_ms));
+        runtime::RunOptions opts;
+        opts.threads = threads;
+        opts.slice = slice;
+        runtime::PartyRuntime rt(b.graph, b.store, session, opts);
+        auto r = rt.run(b.inputs);
+        *out_len = r.outputs.size();
+        std::memcpy(out, r.outputs.data(), std::min<uint64_t>(cap, r.outputs.size()) * 4);
+        report[0] = r.setup_ms;
+        report[1] = r.online_ms;
+        report[2] = double(r.bytes_sent);
+        report[3] = double(r.scalar_triples_consumed);
+        report[4] = double(r.matrix_triples_consumed);
+        report[5] = double(r.bytes_received);
+        *digest = r.output_digest;
+    });
+}
+
+// Transport probe (net.cpp:112-178): connect_mesh, then exchange(Control, 5, {party, 100 + party})
+// -> exch[n][2], then open(77, own[lanes]) -> opened[lanes].
+int reft_mesh_probe(int party, int n, const char* const* endpoints, uint64_t lanes, const uint32_t* own,
+                    uint32_t* exch, uint32_t* opened) {
+    return guard([&] {
+        auto s = net::connect_mesh(mesh_config(party, n, endpoints, 0));
+        auto fr = s->exchange(net::MsgType::Control, 5, {uint32_t(party), uint32_t(100 + party)});
+        for (int i = 0; i < n; ++i)
+            for (int k = 0; k < 2; ++k) exch[2 * i + k] = fr[i].size() > (size_t)k ? fr[i][k] : 0xFFFFFFFFu;
+        auto o = s->open(77, std::vector<uint32_t>(own, own + lanes));
+        std::memcpy(opened, o.data(), o.size() * 4);
     });
 }
 

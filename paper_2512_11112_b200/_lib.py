@@ -65,7 +65,7 @@ class RunOptions(C.Structure):  # spdz_run_options_t
                 ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32),
                 ("stream_per_party", C.c_int32), ("shard_offset", C.c_uint64), ("shard_total", C.c_uint64),
                 ("external_mac_verify", C.c_int32), ("single_party", C.c_int32), ("entry_label", C.c_uint32),
-                ("loop_iters", C.c_uint64)]
+                ("loop_iters", C.c_uint64), ("network", C.c_int32)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t
@@ -169,6 +169,12 @@ _SIGS = {
     "spdz_run_export": (C.c_int, [vp, vp, C.c_uint64, u64p]),
     "spdz_run_import": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_inject_bitflip": (C.c_int, [vp, C.c_uint32, C.c_int, C.c_int, C.c_uint64, C.c_uint32]),
+    "spdz_net_connect": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_char_p), C.c_uint64, C.c_uint64, C.POINTER(vp)]),
+    "spdz_net_destroy": (C.c_int, [vp]),
+    "spdz_net_send": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint64, vp, C.c_uint32]),
+    "spdz_net_recv": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint64, vp, C.c_uint64, u64p]),
+    "spdz_net_stats": (C.c_int, [vp, u64p, u64p]),
+    "spdz_run_attach_net": (C.c_int, [vp, vp]),
 }
 
 _lib = None

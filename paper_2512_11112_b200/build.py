@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libspdz_b200.so"
-SOURCES = ["kernels.cu", "capi.cu", "run.cu", "diag.cu", "gemm_tc.cu", "store.cu"]
+SOURCES = ["kernels.cu", "capi.cu", "run.cu", "diag.cu", "gemm_tc.cu", "store.cu", "net.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: Path 
             sys.stdout.write(out)
     lib.parent.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -1,0 +1,334 @@
+// The reference's wire format and TCP mesh (see net.hpp for the citations).
+#include "net.hpp"
+
+#include <arpa/inet.h>
+#include <netdb.h>
+#include <netinet/in.h>
+#include <netinet/tcp.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <cstring>
+#include <memory>
+
+#include "internal.hpp"
+
+namespace spdzb200 {
+
+namespace {
+
+bool write_all(int fd, const void* data, size_t len) {
+    const char* p = static_cast<const char*>(data);
+    while (len) {
+        const ssize_t k = ::send(fd, p, len, MSG_NOSIGNAL);
+        if (k <= 0) {
+            if (k < 0 && errno == EINTR) continue;
+            return false;
+        }
+        p += k;
+        len -= (size_t)k;
+    }
+    return true;
+}
+
+bool read_all(int fd, void* data, size_t len) {
+    char* p = static_cast<char*>(data);
+    while (len) {
+        const ssize_t k = ::recv(fd, p, len, 0);
+        if (k <= 0) {
+            if (k < 0 && errno == EINTR) continue;
+            return false;
+        }
+        p += k;
+        len -= (size_t)k;
+    }
+    return true;
+}
+
+uint32_t le32(const uint8_t* b) { return (uint32_t)b[0] | (uint32_t)b[1] << 8 | (uint32_t)b[2] << 16 | (uint32_t)b[3] << 24; }
+
+void split_endpoint(const std::string& ep, std::string& host, std::string& port) {
+    const auto colon = ep.rfind(':');
+    if (colon == std::string::npos)
+        throw Error(SPDZ_ERR_NET, "NetError: bad endpoint '" + ep + "', expected host:port");
+    host = ep.substr(0, colon);
+    port = ep.substr(colon + 1);
+}
+
+int dial(const std::string& host, const std::string& port, std::chrono::milliseconds timeout, int peer) {
+    addrinfo hints{};
+    hints.ai_family = AF_UNSPEC;
+    hints.ai_socktype = SOCK_STREAM;
+    const auto deadline = std::chrono::steady_clock::now() + timeout;
+    while (std::chrono::steady_clock::now() < deadline) {
+        addrinfo* res = nullptr;
+        if (getaddrinfo(host.c_str(), port.c_str(), &hints, &res) == 0) {
+            for (addrinfo* ai = res; ai; ai = ai->ai_next) {
+                const int fd = ::socket(ai->ai_family, ai->ai_socktype, ai->ai_protocol);
+                if (fd < 0) continue;
+                if (::connect(fd, ai->ai_addr, ai->ai_addrlen) == 0) {
+                    freeaddrinfo(res);
+                    return fd;
+                }
+                ::close(fd);
+            }
+            freeaddrinfo(res);
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(50));
+    }
+    throw Error(SPDZ_ERR_NET, "ConnectTimeout: peer " + std::to_string(peer) + " at " + host + ":" + port);
+}
+
+}  // namespace
+
+void encode_header(uint8_t* hdr, uint8_t type, uint32_t lanes, uint64_t batch) {
+    std::memset(hdr, 0, kFrameHeader);
+    hdr[0] = type;
+    for (int i = 0; i < 4; ++i) hdr[4 + i] = uint8_t(lanes >> (8 * i));
+    for (int i = 0; i < 8; ++i) hdr[8 + i] = uint8_t(batch >> (8 * i));
+}
+
+NetLink::~NetLink() {
+    stopping = true;
+    for (int fd : fds)
+        if (fd >= 0) ::shutdown(fd, SHUT_RDWR);
+    for (auto& t : readers)
+        if (t.joinable()) t.join();
+    for (int fd : fds)
+        if (fd >= 0) ::close(fd);
+}
+
+void NetLink::send(int peer, uint8_t type, uint64_t batch, const uint32_t* words, uint32_t lanes) {
+    need(peer >= 0 && peer < n && peer != party && fds[peer] >= 0, SPDZ_ERR_INVALID_ARGUMENT, "bad peer");
+    std::vector<uint8_t> buf(kFrameHeader + 4ull * lanes);  // little-endian host (x86-64 / aarch64)
+    encode_header(buf.data(), type, lanes, batch);
+    if (lanes) std::memcpy(buf.data() + kFrameHeader, words, 4ull * lanes);
+    std::lock_guard lk(send_mu[peer]);
+    if (!write_all(fds[peer], buf.data(), buf.size()))
+        throw Error(SPDZ_ERR_PEER_TIMEOUT, "PeerTimeout: send to peer " + std::to_string(peer) + " failed");
+    bytes_sent += buf.size();
+}
+
+void NetLink::broadcast(uint8_t type, uint64_t batch, const uint32_t* words, uint32_t lanes) {
+    for (int p = 0; p < n; ++p)
+        if (p != party) send(p, type, batch, words, lanes);
+}
+
+std::vector<uint32_t> NetLink::recv(int peer, uint8_t type, uint64_t batch) {
+    const auto key = std::make_tuple(type, batch, peer);
+    std::unique_lock lk(mu);
+    const bool got = cv.wait_for(lk, io_timeout, [&] { return inbox.count(key) || !peer_error[peer].empty(); });
+    auto it = inbox.find(key);
+    if (it == inbox.end()) {
+        if (!peer_error[peer].empty()) {
+            const std::string why = peer_error[peer];
+            throw Error(why.rfind("MalformedShareMessage", 0) == 0 ? SPDZ_ERR_MALFORMED_SHARE_MESSAGE
+                                                                   : SPDZ_ERR_PEER_TIMEOUT,
+                        why);
+        }
+        (void)got;
+        throw Error(SPDZ_ERR_PEER_TIMEOUT,
+                    "PeerTimeout: " + std::string(type == kMsgOpenShares ? "open" : "exchange") + " batch " +
+                        std::to_string(batch) + " from peer " + std::to_string(peer));
+    }
+    std::vector<uint32_t> out = std::move(it->second);
+    inbox.erase(it);
+    return out;
+}
+
+std::vector<std::vector<uint32_t>> NetLink::exchange(uint8_t type, uint64_t batch, const std::vector<uint32_t>& own) {
+    broadcast(type, batch, own.data(), (uint32_t)own.size());
+    std::vector<std::vector<uint32_t>> out(n);
+    out[party] = own;
+    for (int p = 0; p < n; ++p)
+        if (p != party) out[p] = recv(p, type, batch);
+    return out;
+}
+
+void NetLink::reader_loop(int peer) {
+    const int fd = fds[peer];
+    auto stop = [&](const std::string& why) {
+        std::lock_guard lk(mu);
+        peer_error[peer] = why;
+        cv.notify_all();
+    };
+    for (;;) {
+        uint8_t hdr[kFrameHeader];
+        if (!read_all(fd, hdr, sizeof hdr)) return stop("PeerTimeout: connection to peer " + std::to_string(peer) +
+                                                        " closed");
+        if (hdr[0] > kMsgControl)  // decode_header (net.cpp:21-29)
+            return stop("MalformedShareMessage: unknown msg-type " + std::to_string(hdr[0]));
+        const uint32_t lanes = le32(hdr + 4);
+        uint64_t batch = 0;
+        for (int i = 0; i < 8; ++i) batch |= uint64_t(hdr[8 + i]) << (8 * i);
+        std::vector<uint32_t> payload(lanes);
+        if (lanes && !read_all(fd, payload.data(), 4ull * lanes))
+            return stop("PeerTimeout: connection to peer " + std::to_string(peer) + " closed mid-frame");
+        if (stopping) return;
+        bytes_received += kFrameHeader + 4ull * lanes;
+        std::lock_guard lk(mu);
+        auto key = std::make_tuple(hdr[0], batch, peer);
+        if (inbox.count(key)) {  // net.cpp:196-198, 214-216
+            peer_error[peer] = "MalformedShareMessage: duplicate frame from peer " + std::to_string(peer);
+            cv.notify_all();
+            return;
+        }
+        inbox.emplace(key, std::move(payload));
+        cv.notify_all();
+    }
+}
+
+void NetLink::start_readers() {
+    for (int p = 0; p < n; ++p)
+        if (p != party) readers.emplace_back([this, p] { reader_loop(p); });
+}
+
+NetLink* connect_mesh(int party, const std::vector<std::string>& endpoints, std::chrono::milliseconds connect_timeout,
+                      std::chrono::milliseconds io_timeout) {
+    const int n = (int)endpoints.size();
+    need(party >= 0 && party < n, SPDZ_ERR_NET, "NetError: party index out of range");
+    auto link = std::make_unique<NetLink>(party, n);
+    link->io_timeout = io_timeout;
+    if (n == 1) return link.release();
+    int listen_fd = -1;
+    if (party < n - 1) {  // listen for higher indices
+        std::string host, port;
+        split_endpoint(endpoints[party], host, port);
+        listen_fd = ::socket(AF_INET, SOCK_STREAM, 0);
+        need(listen_fd >= 0, SPDZ_ERR_NET, "NetError: socket() failed");
+        int one = 1;
+        ::setsockopt(listen_fd, SOL_SOCKET, SO_REUSEADDR, &one, sizeof one);
+        sockaddr_in addr{};
+        addr.sin_family = AF_INET;
+        addr.sin_addr.s_addr = htonl(INADDR_ANY);
+        addr.sin_port = htons((uint16_t)std::stoi(port));
+        if (::bind(listen_fd, reinterpret_cast<sockaddr*>(&addr), sizeof addr) != 0) {
+            ::close(listen_fd);
+            throw Error(SPDZ_ERR_NET, "NetError: bind failed on port " + port);
+        }
+        ::listen(listen_fd, n);
+    }
+    auto attach = [&](int peer, int fd) {
+        int one = 1;
+        ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof one);
+        link->fds[peer] = fd;
+    };
+    try {
+        for (int p = 0; p < party; ++p) {  // dial lower indices, announcing our own
+            std::string host, port;
+            split_endpoint(endpoints[p], host, port);
+            const int fd = dial(host, port, connect_timeout, p);
+            uint8_t idx[4];
+            for (int i = 0; i < 4; ++i) idx[i] = uint8_t((uint32_t)party >> (8 * i));
+            if (!write_all(fd, idx, 4)) {
+                ::close(fd);
+                throw Error(SPDZ_ERR_NET, "ConnectTimeout: handshake with peer " + std::to_string(p));
+            }
+            attach(p, fd);
+        }
+        const int expected = n - 1 - party;
+        const auto deadline = std::chrono::steady_clock::now() + connect_timeout;
+        std::vector<bool> have(n, false);
+        for (int got = 0; got < expected;) {
+            pollfd pfd{listen_fd, POLLIN, 0};
+            const auto left =
+                std::chrono::duration_cast<std::chrono::milliseconds>(deadline - std::chrono::steady_clock::now());
+            if (left.count() <= 0 || ::poll(&pfd, 1, (int)left.count()) <= 0)
+                throw Error(SPDZ_ERR_NET, "ConnectTimeout: waiting for " + std::to_string(expected - got) + " peer(s)");
+            const int fd = ::accept(listen_fd, nullptr, nullptr);
+            if (fd < 0) continue;
+            uint8_t b[4];
+            if (!read_all(fd, b, 4)) {
+                ::close(fd);
+                continue;
+            }
+            const uint32_t idx = le32(b);
+            if (idx >= (uint32_t)n || (int)idx <= party || have[idx]) {
+                ::close(fd);
+                throw Error(SPDZ_ERR_NET, "IndexCollision: peer announced invalid index " + std::to_string(idx));
+            }
+            have[idx] = true;
+            attach((int)idx, fd);
+            ++got;
+        }
+    } catch (...) {
+        if (listen_fd >= 0) ::close(listen_fd);
+        throw;
+    }
+    if (listen_fd >= 0) ::close(listen_fd);
+    link->start_readers();
+    return link.release();
+}
+
+}  // namespace spdzb200
+
+using namespace spdzb200;
+
+struct spdz_net {
+    std::unique_ptr<NetLink> link;
+};
+
+extern "C" {
+
+int spdz_net_connect(int party, int n_parties, const char* const* endpoints, uint64_t connect_timeout_ms,
+                     uint64_t io_timeout_ms, spdz_net** out) {
+    return guard([&] {
+        need(out && endpoints && n_parties >= 1 && n_parties <= SPDZ_MAX_PARTIES, SPDZ_ERR_INVALID_ARGUMENT,
+             "bad mesh arguments");
+        std::vector<std::string> eps;
+        for (int i = 0; i < n_parties; ++i) {
+            need(endpoints[i] != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null endpoint");
+            eps.emplace_back(endpoints[i]);
+        }
+        auto* h = new spdz_net;
+        try {
+            h->link.reset(connect_mesh(party, eps, std::chrono::milliseconds(connect_timeout_ms ? connect_timeout_ms : 10000),
+                                       std::chrono::milliseconds(io_timeout_ms ? io_timeout_ms : 10000)));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int spdz_net_destroy(spdz_net* net) {
+    delete net;
+    return SPDZ_OK;
+}
+
+int spdz_net_send(spdz_net* net, int peer, int type, uint64_t batch, const uint32_t* words, uint32_t lanes) {
+    return guard([&] {
+        need(net != nullptr && type >= 0 && type <= kMsgControl, SPDZ_ERR_INVALID_ARGUMENT, "bad send");
+        net->link->send(peer, (uint8_t)type, batch, words, lanes);
+    });
+}
+
+int spdz_net_recv(spdz_net* net, int peer, int type, uint64_t batch, uint32_t* out, uint64_t cap, uint64_t* lanes) {
+    return guard([&] {
+        need(net != nullptr && lanes != nullptr && peer >= 0 && peer < net->link->n && peer != net->link->party,
+             SPDZ_ERR_INVALID_ARGUMENT, "bad recv");
+        auto v = net->link->recv(peer, (uint8_t)type, batch);
+        *lanes = v.size();
+        need(v.size() <= cap || out == nullptr, SPDZ_ERR_LANE_COUNT_MISMATCH,
+             "LaneCountMismatch: peer " + std::to_string(peer) + " sent " + std::to_string(v.size()) +
+                 " lanes, expected at most " + std::to_string(cap));
+        if (out && !v.empty()) std::memcpy(out, v.data(), v.size() * 4);
+    });
+}
+
+int spdz_net_stats(spdz_net* net, uint64_t* bytes_sent, uint64_t* bytes_received) {
+    return guard([&] {
+        need(net != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null mesh");
+        if (bytes_sent) *bytes_sent = net->link->bytes_sent;
+        if (bytes_received) *bytes_received = net->link->bytes_received;
+    });
+}
+
+}  // extern "C"
+
+namespace spdzb200 {
+NetLink* net_link(spdz_net* net) { return net ? net->link.get() : nullptr; }
+}  // namespace spdzb200

@@ -21,9 +21,14 @@
 
 #include "field.cuh"
 #include "internal.hpp"
+#include "net.hpp"
 #include "store.hpp"
 
 using namespace spdzb200;
+
+namespace spdzb200 {
+NetLink* net_link(spdz_net* net);  // net.cpp
+}
 
 namespace {
 
@@ -148,6 +153,9 @@ struct spdz_run {
     std::map<uint32_t, uint64_t> input_mask_gfirst;       // ... global index of that mask
     uint64_t scalar_total_global = 0, mask_total_global = 0;
     bool cfg = false;               // graph with PHI/BRANCH: block-by-block execution (run_cfg)
+    NetLink* net = nullptr;         // peers across the reference's TCP mesh (spdz_run_attach_net)
+    HostPinned net_stage;           // frame staging (D2H of own payloads, H2D of the peers')
+    std::vector<uint32_t> net_host; // per-tile frame assembly
     uint64_t loop_iters = 64;       // triple provisioning of loop bodies (preproc.cpp:124-163)
     uint64_t scalar_used = 0, matrix_used = 0;  // consumed by the last phase (control flow)
     uint64_t shard_off = 0, shard_total = 0, shard_L = 0;  // shard_total == 0: unsharded
@@ -190,7 +198,8 @@ struct spdz_run {
     std::chrono::steady_clock::time_point wall0;
 
     uint32_t* alloc(int party, uint64_t words) {
-        if (!parties[party].local) return nullptr;  // remote party: pointers come from spdz_run_import
+        // remote party: pointers come from spdz_run_import, or (network peers) local mirrors
+        if (!parties[party].local && !opts.network) return nullptr;
         const int dev = devices[party];
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         void* p = nullptr;
@@ -251,7 +260,7 @@ uint64_t slot_of(uint32_t node, uint32_t sub) { return (uint64_t)node * 64 + sub
 // After party p's payload for `slot` is complete on its stream, publish it to
 // remote peers (stream-ordered write, with the default system-wide fence).
 void signal_remote(spdz_run* r, int p, uint64_t slot) {
-    if (!r->any_remote) return;
+    if (!r->any_remote || r->opts.network) return;
     dev(r, p);
     need(g_writev32(S(r, p), (CUdeviceptr)(r->parties[p].flags + slot), r->seq, 0) == CUDA_SUCCESS, SPDZ_ERR_CUDA,
          "cuStreamWriteValue32");
@@ -527,6 +536,9 @@ void plan_buffers(spdz_run* r) {
         P.flags = r->alloc(p, r->n_slots);
         cuda_check(cudaMemset(P.flags, 0, r->n_slots * 4), "memset flags");
     }
+    // network peers: party 0's input differences arrive as frames into a local mirror
+    if (r->opts.network && !r->parties[0].local)
+        for (auto& [id, off] : r->input_mask_off) r->input_diff[id] = r->alloc(0, r->node(id).lanes);
     // one open event per (party, node) plus reduce levels
     for (int p = 0; p < r->n; ++p) {
         if (!r->parties[p].local) continue;
@@ -883,6 +895,69 @@ struct Exec {
         return src;
     }
 
+    // ---- network peers (the reference's frames, net.cpp) ----
+    bool netpeer(int q) const { return r->net && !r->parties[q].local; }
+
+    // party p's payload words to every peer as one frame (async_open / exchange send side)
+    void net_send(int p, uint8_t type, uint64_t batch, const uint32_t* dsrc, uint64_t words) {
+        need(r->net != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "network run without an attached mesh");
+        uint32_t* h = (uint32_t*)r->net_stage.ensure(std::max<uint64_t>(words, 1) * 4);
+        dev(r, p);
+        if (words) lk(cudaMemcpyAsync(h, dsrc, words * 4, cudaMemcpyDeviceToHost, S(r, p)), "D2H frame");
+        lk(cudaStreamSynchronize(S(r, p)), "frame");
+        r->net->broadcast(type, batch, h, (uint32_t)words);
+    }
+
+    // peer q's frame (type, batch) into device memory on party p's stream (net.cpp:186-208)
+    void net_recv(int p, int q, uint8_t type, uint64_t batch, uint32_t* ddst, uint64_t words) {
+        std::vector<uint32_t> v = r->net->recv(q, type, batch);
+        need(v.size() == words, SPDZ_ERR_LANE_COUNT_MISMATCH,
+             "LaneCountMismatch: peer " + std::to_string(q) + " sent " + std::to_string(v.size()) +
+                 " lanes, expected " + std::to_string(words));
+        if (!words) return;
+        uint32_t* h = (uint32_t*)r->net_stage.ensure(words * 4);
+        std::memcpy(h, v.data(), words * 4);
+        dev(r, p);
+        lk(cudaMemcpyAsync(ddst, h, words * 4, cudaMemcpyHostToDevice, S(r, p)), "H2D frame");
+        lk(cudaStreamSynchronize(S(r, p)), "frame");
+    }
+
+    // linear layer: one frame per tile, [D_t | E_t] (linear.cpp:94-113), batch batch0 + t;
+    // our payload holds [D (all rows) | E_t for every tile]
+    void net_send_tiles(int p, uint64_t batch0, const uint32_t* dsrc, uint32_t din, const LinTiles& lt) {
+        const uint64_t nt = lt.starts.size(), cells = (uint64_t)din * (lt.starts.empty() ? 0 : lt.starts.back() +
+                                                                                                    lt.counts.back());
+        const uint64_t words = cells + din * nt;
+        uint32_t* h = (uint32_t*)r->net_stage.ensure(words * 4);
+        dev(r, p);
+        lk(cudaMemcpyAsync(h, dsrc, words * 4, cudaMemcpyDeviceToHost, S(r, p)), "D2H tiles");
+        lk(cudaStreamSynchronize(S(r, p)), "tiles");
+        for (uint64_t t = 0; t < nt; ++t) {
+            const uint64_t ct = (uint64_t)lt.counts[t] * din;
+            r->net_host.resize(ct + din);
+            std::memcpy(r->net_host.data(), h + (uint64_t)lt.starts[t] * din, ct * 4);
+            std::memcpy(r->net_host.data() + ct, h + cells + t * din, din * 4ull);
+            r->net->broadcast(kMsgOpenShares, batch0 + t, r->net_host.data(), (uint32_t)(ct + din));
+        }
+    }
+    void net_recv_tiles(int p, int q, uint64_t batch0, uint32_t* ddst, uint32_t din, const LinTiles& lt) {
+        const uint64_t nt = lt.starts.size(), cells = (uint64_t)din * (lt.starts.back() + lt.counts.back());
+        const uint64_t words = cells + din * nt;
+        uint32_t* h = (uint32_t*)r->net_stage.ensure(words * 4);
+        for (uint64_t t = 0; t < nt; ++t) {
+            const uint64_t ct = (uint64_t)lt.counts[t] * din;
+            std::vector<uint32_t> v = r->net->recv(q, kMsgOpenShares, batch0 + t);
+            need(v.size() == ct + din, SPDZ_ERR_LANE_COUNT_MISMATCH,
+                 "LaneCountMismatch: peer " + std::to_string(q) + " sent " + std::to_string(v.size()) +
+                     " lanes, expected " + std::to_string(ct + din));
+            std::memcpy(h + (uint64_t)lt.starts[t] * din, v.data(), ct * 4);
+            std::memcpy(h + cells + t * din, v.data() + ct, din * 4ull);
+        }
+        dev(r, p);
+        lk(cudaMemcpyAsync(ddst, h, words * 4, cudaMemcpyHostToDevice, S(r, p)), "H2D tiles");
+        lk(cudaStreamSynchronize(S(r, p)), "tiles");
+    }
+
     // The MAC shares a Beaver record is checked against: the operand planes themselves, or
     // (control flow, where a later execution rewrites them) a per-execution snapshot.
     const uint32_t* mac_slot(int p, uint32_t id, uint64_t exec, int which) {
@@ -1110,6 +1185,7 @@ struct Exec {
                "k_mul_mask");
             tend(p, tk, SPDZ_KSTAT_MASK, 24 * L);
             sent[p] = publish(p, slot_of(id, 0));
+            if (r->net) net_send(p, kMsgOpenShares, make_batch(id, exec, 0), st.payload, 2 * L);
         }
         const uint64_t batch = make_batch(id, exec, 0);
         const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
@@ -1123,7 +1199,8 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                await(p, q, sent[q], slot_of(id, 0));
+                if (netpeer(q)) net_recv(p, q, kMsgOpenShares, batch, r->parties[q].ns[id].payload, 2 * L);
+                else await(p, q, sent[q], slot_of(id, 0));
                 const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, 2 * L, st.shadow);
                 pd[k] = src;
                 pe[k] = src + L;
@@ -1181,6 +1258,7 @@ struct Exec {
                                    lv.payload + pairs, pairs, SMS(r, p)),
                    "mask");
                 sent[p] = publish(p, slot_of(id, 1 + (uint32_t)li));
+                if (r->net) net_send(p, kMsgOpenShares, make_batch(id, exec, sub), lv.payload, 2 * pairs);
             }
             const uint64_t batch = make_batch(id, exec, sub++);
             for (int p = 0; p < r->n; ++p) {
@@ -1193,7 +1271,10 @@ struct Exec {
                 int k = 0;
                 for (int q = 0; q < r->n; ++q) {
                     if (q == p) continue;
-                    await(p, q, sent[q], slot_of(id, 1 + (uint32_t)li));
+                    if (netpeer(q))
+                        net_recv(p, q, kMsgOpenShares, batch, r->parties[q].ns[id].levels[li].payload, 2 * pairs);
+                    else
+                        await(p, q, sent[q], slot_of(id, 1 + (uint32_t)li));
                     pd[k] = r->parties[q].ns[id].levels[li].payload;
                     pe[k] = pd[k] + pairs;
                     ++k;
@@ -1287,6 +1368,7 @@ struct Exec {
             lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
             tend(p, tk, SPDZ_KSTAT_MASK, 12 * cells + 12 * etot);
             sent[p] = publish(p, slot_of(id, 0));
+            if (r->net) net_send_tiles(p, batch0, st.payload, din, lt);
         }
         bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
         for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
@@ -1346,7 +1428,8 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                await(p, q, sent[q], slot_of(id, 0));
+                if (netpeer(q)) net_recv_tiles(p, q, batch0, r->parties[q].ns[id].payload, din, lt);
+                else await(p, q, sent[q], slot_of(id, 0));
                 const uint32_t* src = peer_payload(p, q, id, r->parties[q].ns[id].payload, cells + etot, st.shadow);
                 peers[k] = src;
                 peersE[k] = src + cells;
@@ -1513,12 +1596,13 @@ struct Exec {
             return;
         }
         std::vector<cudaEvent_t> ready(r->n);
+        const uint64_t batch = make_batch(r->root, 1, 1);
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             dev(r, p);
             ready[p] = publish(p, slot_of(r->root, 0));
+            if (r->net) net_send(p, kMsgOpenShares, batch, r->parties[p].ns[r->root].out.v, L);
         }
-        const uint64_t batch = make_batch(r->root, 1, 1);
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -1528,7 +1612,8 @@ struct Exec {
             int k = 0;
             for (int q = 0; q < r->n; ++q) {
                 if (q == p) continue;
-                await(p, q, ready[q], slot_of(r->root, 0));
+                if (netpeer(q)) net_recv(p, q, kMsgOpenShares, batch, r->parties[q].ns[r->root].out.v, L);
+                else await(p, q, ready[q], slot_of(r->root, 0));
                 peers[k++] = r->parties[q].ns[r->root].out.v;
                 r->exchanged += L * 4;
             }
@@ -1655,7 +1740,55 @@ void mac_finish(spdz_run* r, spdz_run_report_t* rep, uint64_t coin) {
     if (rc) throw Error(rc, spdz_last_error());
 }
 
+// runtime.cpp:467-506 across the mesh: coin from committed nonces, sigma commit/reveal,
+// verify_sigmas over every party's reveal
+void mac_check_net(spdz_run* r, spdz_run_report_t* rep) {
+    NetLink& net = *r->net;
+    const int n = r->n, me = r->ref_party();
+    auto u64_of = [](const std::vector<uint32_t>& v, size_t at) {
+        need(v.size() >= at + 2, SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: short MAC-check frame");
+        return (uint64_t)v[at] | (uint64_t)v[at + 1] << 32;
+    };
+    const uint64_t nonce = fresh_nonce();
+    const uint64_t commit = spdz_fnv1a64(&nonce, 8, 1469598103934665603ull);
+    auto commits = net.exchange(kMsgCommit, kMacBatchBase, {(uint32_t)commit, (uint32_t)(commit >> 32)});
+    auto nonces = net.exchange(kMsgReveal, kMacBatchBase + 1, {(uint32_t)nonce, (uint32_t)(nonce >> 32)});
+    uint64_t coin = 0;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t ni = u64_of(nonces[i], 0);
+        if (spdz_fnv1a64(&ni, 8, 1469598103934665603ull) != u64_of(commits[i], 0))
+            throw Error(SPDZ_ERR_MAC_CHECK_FAILED, "MacCheckFailed: coin commitment mismatch from party " +
+                                                       std::to_string(i));
+        coin = spdz_fnv1a64(&ni, 8, coin);
+    }
+    mac_launch(r, coin);
+    dev(r, me);
+    const uint32_t sigma = mac_sigma_collect(r->parties[me].ctx, 0);
+    const uint64_t nonce2 = fresh_nonce();
+    const uint64_t sc = spdz_commit_sigma(sigma, nonce2);
+    auto scommits = net.exchange(kMsgCommit, kMacBatchBase + 2, {(uint32_t)sc, (uint32_t)(sc >> 32)});
+    auto reveals = net.exchange(kMsgReveal, kMacBatchBase + 3, {sigma, (uint32_t)nonce2, (uint32_t)(nonce2 >> 32)});
+    std::vector<uint32_t> sig(n);
+    std::vector<uint64_t> n2(n), cm(n);
+    for (int i = 0; i < n; ++i) {
+        need(!reveals[i].empty(), SPDZ_ERR_MALFORMED_SHARE_MESSAGE, "MalformedShareMessage: empty reveal");
+        sig[i] = reveals[i][0];
+        n2[i] = u64_of(reveals[i], 1);
+        cm[i] = u64_of(scommits[i], 0);
+    }
+    if (rep) {
+        for (int i = 0; i < n; ++i) rep->sigmas[i] = sig[i];
+        rep->coin = coin;
+    }
+    const int rc = spdz_verify_sigmas(sig.data(), n2.data(), cm.data(), n);
+    if (rc) throw Error(rc, spdz_last_error());
+}
+
 void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t given_coin) {
+    if (r->net) {
+        mac_check_net(r, rep);
+        return;
+    }
     const uint64_t coin = agree_coin(r, have_coin, given_coin);
     mac_launch(r, coin);
     mac_finish(r, rep, coin);
@@ -1678,8 +1811,46 @@ void share_inputs(spdz_run* r) {
         r->masks_used = true;
     }
     ++r->seq;
+    uint64_t input_batch = kInputBatchBase;  // preproc.cpp:207-231: one Control exchange per private input
     for (auto& [id, off] : r->input_mask_off) {
         const auto& n = r->node(id);
+        if (r->net) {  // peers across the mesh: exchange(Control, batch, diff), party 0's diff opens
+            need(r->net != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "network run without an attached mesh");
+            const uint64_t batch = input_batch++;
+            const int me = r->ref_party();
+            auto& P = r->parties[me];
+            uint32_t* diff = r->input_diff.at(id);
+            Exec ex{r};
+            if (me == 0) {
+                auto it = r->input_dev.find(id);
+                need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
+                     "ShapeMismatch: no values bound for input node " + std::to_string(id));
+                dev(r, 0);
+                lk(launch_pub_binop(P.ctx->stream, 1, it->second, false, P.mask_c + off, false, diff, n.lanes,
+                                    P.ctx->sms),
+                   "x - r");
+                ex.net_send(0, kMsgControl, batch, diff, n.lanes);
+            } else {
+                ex.net_send(me, kMsgControl, batch, nullptr, 0);
+            }
+            for (int q = 0; q < r->n; ++q) {
+                if (q == me) continue;
+                std::vector<uint32_t> v = r->net->recv(q, kMsgControl, batch);
+                if (q != 0) continue;  // only party 0 owns inputs (preproc.cpp:231)
+                need(v.size() == n.lanes, SPDZ_ERR_INVALID_ARGUMENT,
+                     "ShapeMismatch: opened input difference has wrong length");
+                uint32_t* h = (uint32_t*)r->net_stage.ensure(v.size() * 4);
+                std::memcpy(h, v.data(), v.size() * 4);
+                dev(r, me);
+                lk(cudaMemcpyAsync(diff, h, v.size() * 4, cudaMemcpyHostToDevice, P.ctx->stream), "H2D diff");
+                lk(cudaStreamSynchronize(P.ctx->stream), "diff");
+            }
+            dev(r, me);
+            lk(launch_public(P.ctx->stream, 0, P.mask_v + off, P.mask_m + off, diff, false, 0u, false, me,
+                             P.ctx->alpha, P.ns[id].out.v, P.ns[id].out.m, n.lanes, P.ctx->sms),
+               "add_public(diff)");
+            continue;
+        }
         if (share_fused(r)) {  // both parties in one pass from the raw input (reduced inline)
             auto it = r->input_dev.find(id);
             need(it != r->input_dev.end(), SPDZ_ERR_INVALID_ARGUMENT,
@@ -1855,8 +2026,8 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
         if (r->cfg) {
             need(r->opts.entry_label < n_nodes && nodes[r->opts.entry_label].kind == SPDZ_NODE_LABEL,
                  SPDZ_ERR_INVALID_ARGUMENT, "control-flow graph needs entry_label = its entry block's LABEL");
-            need(!r->opts.shard_total && !r->opts.single_party, SPDZ_ERR_INVALID_ARGUMENT,
-                 "control-flow graphs run with every party local and unsharded");
+            need(!r->opts.shard_total && (!r->opts.single_party || r->opts.network), SPDZ_ERR_INVALID_ARGUMENT,
+                 "control-flow graphs run unsharded, with every party local or across a network mesh");
         }
         r->devices.resize(n_parties);
         for (int p = 0; p < n_parties; ++p) r->devices[p] = (opts && opts->devices[p] >= 0) ? opts->devices[p] : 0;
@@ -1865,9 +2036,9 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
             need(r->opts.single_party <= n_parties, SPDZ_ERR_INVALID_ARGUMENT, "single_party out of range");
             for (int p = 0; p < n_parties; ++p) r->parties[p].local = p == r->opts.single_party - 1;
             r->any_remote = n_parties > 1;
-            need(r->opts.external_mac_verify, SPDZ_ERR_INVALID_ARGUMENT,
+            need(r->opts.external_mac_verify || r->opts.network, SPDZ_ERR_INVALID_ARGUMENT,
                  "single_party runs need external_mac_verify = 1 (sigmas are combined across processes)");
-            load_stream_memops();
+            if (!r->opts.network) load_stream_memops();
         }
         for (int p = 0; p < n_parties; ++p) {
             if (!r->parties[p].local) continue;
@@ -2298,6 +2469,19 @@ int spdz_run_import(spdz_run* r, const void* blob, uint64_t len) {
                 }
             }
         }
+    });
+}
+
+int spdz_run_attach_net(spdz_run* r, spdz_net* net) {
+    return guard([&] {
+        need(r != nullptr && net != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run or mesh");
+        need(r->opts.network && r->opts.single_party > 0, SPDZ_ERR_INVALID_ARGUMENT,
+             "attach a mesh to a single_party run created with network = 1");
+        NetLink* link = net_link(net);
+        need(link->n == r->n && link->party == r->opts.single_party - 1, SPDZ_ERR_INVALID_ARGUMENT,
+             "mesh is party " + std::to_string(link->party) + " of " + std::to_string(link->n) + ", run is party " +
+                 std::to_string(r->opts.single_party - 1) + " of " + std::to_string(r->n));
+        r->net = link;
     });
 }
 

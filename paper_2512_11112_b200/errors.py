@@ -64,6 +64,10 @@ class InsufficientTriples(SpdzError):  # preproc.cpp:182-201
     code = 13
 
 
+class NetError(SpdzError):  # net.hpp:19-30 (NetError, ConnectTimeout, IndexCollision)
+    code = 14
+
+
 class InvalidArgument(SpdzError, ValueError):
     code = 20
 
@@ -76,7 +80,7 @@ class DealerRejection(SpdzError):
     code = 22
 
 
-_BY_CODE = {c.code: c for c in (LaneMismatch, TripleShortage, BackendUnavailable, TripleExhausted,
+_BY_CODE = {c.code: c for c in (NetError, LaneMismatch, TripleShortage, BackendUnavailable, TripleExhausted,
                                 TripleShapeMismatch, MaskExhausted, PeerTimeout, LaneCountMismatch,
                                 MalformedShareMessage, MacCheckFailed, SliceTooSmall, StoreFormatError,
                                 InsufficientTriples, InvalidArgument, CudaError, DealerRejection)}

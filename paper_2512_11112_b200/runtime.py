@@ -212,7 +212,8 @@ class LocalRun:
     def __init__(self, graph: Graph, n_parties: int = 2, slice_: int = 262140, dealer_seed: int = 1,
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
                  stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
-                 single_party: int | None = None, use_graph: bool = False, loop_iters: int = 64):
+                 single_party: int | None = None, use_graph: bool = False, loop_iters: int = 64,
+                 network: bool = False):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -224,6 +225,8 @@ class LocalRun:
         o.use_graph = int(use_graph)  # online phase captured once as a CUDA graph, then replayed
         o.entry_label = graph.entry_label
         o.loop_iters = loop_iters  # control flow: loop bodies' triple provisioning (the store's loop_iters)
+        # peers across a TCP mesh (net.Mesh, attach_net): the reference's frames and MAC-check protocol
+        o.network = int(network)
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
         o.external_mac_verify = int(external_mac_verify or single_party is not None)
@@ -262,6 +265,11 @@ class LocalRun:
 
     def deal(self, seed: int):
         check(lib().spdz_run_deal(self.h, seed))
+
+    def attach_net(self, mesh):
+        """Peers across `mesh` (net.Mesh; single_party run created with network=True)."""
+        self._mesh = mesh  # the mesh must outlive the run
+        check(lib().spdz_run_attach_net(self.h, mesh.h))
 
     def load_store(self, party: int, path):
         """Party `party`'s preprocessing from the reference's MPCT store file (instead of deal)."""
