@@ -2141,7 +2141,9 @@ int spdz_run_bind_input(spdz_run* r, uint32_t node, const uint32_t* host_vals, u
             r->inputs[node] = std::vector<uint32_t>(host_vals, host_vals + len);
             return;
         }
-        // party 0 owns every private input (preproc.cpp:146-150): stage on its device
+        // party 0 owns every private input (preproc.cpp:146-150): stage on its device; other
+        // parties' copies of the values are not used (they receive x - r)
+        if (!r->parties[0].local) return;
         auto it = r->input_dev.find(node);
         uint32_t* d = it == r->input_dev.end() ? (r->input_dev[node] = r->alloc(0, len)) : it->second;
         dev(r, 0);
