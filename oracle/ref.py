@@ -106,6 +106,12 @@ def lib():
                                          C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
                                          C.POINTER(C.c_uint64)]
         L.reft_mesh_probe.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_char_p), C.c_uint64, U32P, U32P, U32P]
+        L.reft_interpret_circuit.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P,
+                                             U32P, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.reft_run_local_circuit.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                             C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, U32P, C.c_uint64,
+                                             C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
+                                             C.POINTER(C.c_uint64)]
         L.reft_time_beaver_kernels.argtypes = [C.c_uint64, C.c_int]
         L.reft_time_beaver_kernels.restype = C.c_double
     return _lib
@@ -399,6 +405,28 @@ def run_bundle(circuit_path, n_parties: int, triples_dir, inputs_path, slice_: i
     report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
                   matrix_triples=int(rep[4]), digest=dig.value)
     return out[: n.value].copy(), report
+
+
+def interpret_circuit(circuit_path, inputs: dict, cap: int = 1 << 24) -> np.ndarray:
+    """oracle::interpret on a circuit file."""
+    k, cn, cv, cl, keep = _inputs(inputs)
+    out = np.empty(cap, np.uint32)
+    n = C.c_uint64()
+    _check(lib().reft_interpret_circuit(str(circuit_path).encode(), k, cn, cv, cl, out, cap, C.byref(n)))
+    return out[: n.value].copy()
+
+
+def run_local_circuit(circuit_path, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,
+                      loop_iters: int = 64, cap: int = 1 << 24):
+    """runtime::run_local on a circuit file (loop_iters hint as given)."""
+    k, cn, cv, cl, keep = _inputs(inputs)
+    out = np.empty(cap, np.uint32)
+    n = C.c_uint64()
+    rep = np.zeros(8, np.float64)
+    dig = C.c_uint64()
+    _check(lib().reft_run_local_circuit(str(circuit_path).encode(), n_parties, slice_, dealer_seed, loop_iters, k, cn,
+                                        cv, cl, out, cap, C.byref(n), rep, C.byref(dig)))
+    return out[: n.value].copy(), dict(scalar_triples=int(rep[3]), matrix_triples=int(rep[4]), digest=dig.value)
 
 
 def _eps(endpoints):

@@ -562,6 +562,41 @@ int reft_mesh_probe(int party, int n, const char* const* endpoints, uint64_t lan
     });
 }
 
+// ---- circuit files through the reference's own interpreter / runtime ----
+// oracle.cpp:25 interpret on a circuit file.
+int reft_interpret_circuit(const char* circuit_path, int n_inputs, const char* const* names, const uint32_t* const* vals,
+                           const uint64_t* lens, uint32_t* out, uint64_t cap, uint64_t* out_len) {
+    return guard([&] {
+        auto g = circuit::read_circuit_file(circuit_path);
+        auto r = oracle::interpret(g, make_inputs(n_inputs, names, vals, lens));
+        *out_len = r.size();
+        std::memcpy(out, r.data(), std::min<uint64_t>(cap, r.size()) * 4);
+    });
+}
+
+// runtime.cpp:586-613 run_local on a circuit file, with its loop_iters hint.
+int reft_run_local_circuit(const char* circuit_path, int n_parties, uint64_t slice, uint64_t dealer_seed,
+                           uint64_t loop_iters, int n_inputs, const char* const* names, const uint32_t* const* vals,
+                           const uint64_t* lens, uint32_t* out, uint64_t cap, uint64_t* out_len, double* report,
+                           uint64_t* digest) {
+    return guard([&] {
+        auto g = circuit::read_circuit_file(circuit_path);
+        runtime::RunOptions opts;
+        opts.slice = slice;
+        auto reps = runtime::run_local(g, n_parties, make_inputs(n_inputs, names, vals, lens), opts, dealer_seed, {},
+                                       loop_iters);
+        auto& r0 = reps.at(0);
+        *out_len = r0.outputs.size();
+        std::memcpy(out, r0.outputs.data(), std::min<uint64_t>(cap, r0.outputs.size()) * 4);
+        report[0] = r0.setup_ms;
+        report[1] = r0.online_ms;
+        report[2] = double(r0.bytes_sent);
+        report[3] = double(r0.scalar_triples_consumed);
+        report[4] = double(r0.matrix_triples_consumed);
+        *digest = r0.output_digest;
+    });
+}
+
 // Kernel-level CPU timing (pattern of benchmarks/kernel_bench.cpp:33-58):
 // best-of-`reps` wall time of CpuBackend::mul_mask + mul_combine on `lanes`.
 double reft_time_beaver_kernels(uint64_t lanes, int reps) {

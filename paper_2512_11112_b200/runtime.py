@@ -570,9 +570,10 @@ class ChunkedRun:
 
 
 def run_local(graph: Graph, n_parties: int, inputs: dict, slice_: int = 262140, dealer_seed: int = 1,
-              coin: int | None = None, devices=None) -> RunReport:
-    """runtime::run_local (runtime.cpp:586-613) on B200: deal, share inputs, online phase."""
-    r = LocalRun(graph, n_parties, slice_, dealer_seed, devices, coin)
+              coin: int | None = None, devices=None, loop_iters: int = 64) -> RunReport:
+    """runtime::run_local (runtime.cpp:586-613) on B200: deal (loop bodies provisioned
+    loop_iters times, the reference's loop_iters_hint), share inputs, online phase."""
+    r = LocalRun(graph, n_parties, slice_, dealer_seed, devices, coin, loop_iters=loop_iters)
     try:
         r.bind_inputs(inputs)
         r.share_inputs()

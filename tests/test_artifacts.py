@@ -279,3 +279,90 @@ def test_run_files_tampered_store_fails_mac(gpu, tmp_path):
     shutil.copy(stores[2], d / "triples_2.bin")
     with pytest.raises(errors.MacCheckFailed):
         A.run_files(circ, [d / f"triples_{i}.bin" for i in range(3)], inp, exp["slice"])
+
+
+# ---- the reference's random branchy programs (tests/golden/generated) ----
+GEN = Path(__file__).resolve().parent / "golden" / "generated"
+GEN_META = json.loads((GEN / "expected.json").read_text())
+
+
+def test_generated_programs_present():
+    assert len(GEN_META) >= 150 and sum(k.endswith("_priv") for k in GEN_META) >= 50
+    kinds = set()
+    for name in GEN_META:
+        g = A.read_circuit_file(GEN / f"{name}.mpcg").to_graph({k: np.array(v, np.uint32) for k, v in
+                                                                GEN_META[name]["inputs"].items()})
+        kinds |= {n.kind for n in g.nodes}
+    assert {rt.PHI, rt.BRANCH, rt.CMP_PUBLIC, rt.MUL} <= kinds
+
+
+@pytest.mark.gpu
+def test_generated_programs_run(gpu):
+    """scheduler_tests.cpp:124-147 on B200: every generated program (public and with a private
+    parameter) == the reference interpreter; triple counts and digest == the reference's
+    run_local wherever that run completes (s108_priv: see make_generated.py)."""
+    bad = []
+    for name, m in GEN_META.items():
+        vals = {k: np.array(v, np.uint32) for k, v in m["inputs"].items()}
+        g = A.read_circuit_file(GEN / f"{name}.mpcg").to_graph(vals)
+        rep = rt.run_local(g, 2, vals, loop_iters=8)
+        ok = rep.outputs.tolist() == m["outputs"]
+        if m["reference"] == "ok":
+            ok = ok and rep.output_digest == m["digest"] and rep.scalar_triples_consumed == m["scalar_triples"]
+        if not ok:
+            bad.append(name)
+    assert not bad, bad
+
+
+# ---- runtime_tests.cpp mirrors on B200 (expected values: the reference interpreter) ----
+def _run(path, vals, n=2, **kw):
+    vals = {k: np.array(v, np.uint32) for k, v in vals.items()}
+    g = A.read_circuit_file(path).to_graph(vals)
+    return rt.run_local(g, n, vals, **kw)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAS_REF, reason="oracle/_ref not built")
+def test_party_counts_2_to_6(gpu):
+    """runtime_tests.cpp:54-62."""
+    path = BUNDLES / "straight_line" / "circuit.mpcg"
+    vals = {"x": [1000, 2000, 3000], "k": [9]}
+    want = ref.interpret_circuit(path, {k: np.array(v, np.uint32) for k, v in vals.items()}).tolist()
+    for n in range(2, 7):
+        assert _run(path, vals, n).outputs.tolist() == want, n
+
+
+@pytest.mark.gpu
+def test_loop_trip_counts(gpu):
+    """runtime_tests.cpp:133-137 (public-only loop under MPC) and scheduler_tests.cpp:98-103
+    (trip count 1 and the do-while shape with n = 0)."""
+    path = BUNDLES / "control_flow" / "loop_sum.mpcg"
+    assert _run(path, {"n": [25]}).outputs.tolist() == [325]
+    assert _run(path, {"n": [1]}).outputs.tolist() == [1]
+    assert _run(path, {"n": [0]}).outputs.tolist() == [1]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAS_REF, reason="oracle/_ref not built")
+def test_under_provisioned_loops(gpu):
+    """runtime_tests.cpp:107-114: 16 inner executions with loop_iters 2 -> TripleExhausted;
+    loop_iters 4 runs."""
+    path = BUNDLES / "control_flow" / "nested_loop.mpcg"
+    vals = {"x": [2, 3], "a": [4], "b": [4]}
+    with pytest.raises(errors.TripleExhausted, match="TripleExhausted"):
+        _run(path, vals, loop_iters=2)
+    want = ref.interpret_circuit(path, {k: np.array(v, np.uint32) for k, v in vals.items()}).tolist()
+    rep = _run(path, vals, loop_iters=4)
+    assert rep.outputs.tolist() == want and rep.scalar_triples_consumed == 16
+
+
+@pytest.mark.gpu
+def test_same_seed_same_transcript(gpu):
+    """runtime_tests.cpp:121-131: 3 parties, dealer seed 77 twice."""
+    circ, _, inp, exp = files("linear_64x32")
+    vals = A.read_input_file(inp)
+    g = A.read_circuit_file(circ).to_graph(vals)
+    a = rt.run_local(g, 3, vals, dealer_seed=77)
+    b = rt.run_local(g, 3, vals, dealer_seed=77)
+    assert a.output_digest == b.output_digest and a.outputs.tolist() == exp["outputs"]
+    assert a.matrix_triples_consumed == b.matrix_triples_consumed == 1
