@@ -85,6 +85,7 @@ struct NodeState {                  // per party, per node
     uint32_t* opened_all = nullptr;
     uint32_t* macsnap = nullptr;
     bool dyn_load = false;          // LOAD whose start is computed at run time (own buffer)
+    uint32_t* shadow_pub = nullptr; // control flow: the public value of a private-typed node holding one
 };
 
 struct LinTiles {
@@ -158,6 +159,10 @@ struct spdz_run {
     std::vector<uint32_t> net_host; // per-tile frame assembly
     uint64_t loop_iters = 64;       // triple provisioning of loop bodies (preproc.cpp:124-163)
     uint64_t scalar_used = 0, matrix_used = 0;  // consumed by the last phase (control flow)
+    // control flow: a private-typed node whose current value is public (a private phi that took
+    // a public incoming value, and the add/sub/mul results of such values), as the reference's
+    // RtValue::is_public is decided at run time (runtime.cpp:28-34)
+    std::vector<char> rt_pub;
     uint64_t shard_off = 0, shard_total = 0, shard_L = 0;  // shard_total == 0: unsharded
     std::map<uint32_t, std::vector<uint32_t>> inputs;     // cleartext (host)
     std::map<uint32_t, uint32_t*> input_dev;              // cleartext staged on party 0's device
@@ -405,8 +410,12 @@ void plan_buffers(spdz_run* r) {
                 case SPDZ_NODE_BRANCH:
                     break;
                 case SPDZ_NODE_PHI:  // its own buffer: the chosen value is copied in at block entry
-                    if (n.is_private) priv_out(L);
-                    else pub_out(L);
+                    if (n.is_private) {
+                        priv_out(L);
+                        st.shadow_pub = r->alloc(p, L);
+                    } else {
+                        pub_out(L);
+                    }
                     break;
                 case SPDZ_NODE_LOAD: {  // runtime.cpp:419-438 (zero-copy slice)
                     const Val& base = opnd(0);
@@ -449,6 +458,7 @@ void plan_buffers(spdz_run* r) {
                             st.opened_all = r->alloc(p, 2 * L * execs);
                             st.macsnap = r->alloc(p, 2 * L * execs);
                         }
+
                     } else {
                         priv_out(L);
                     }
@@ -521,6 +531,10 @@ void plan_buffers(spdz_run* r) {
                 default:
                     throw Error(SPDZ_ERR_INVALID_ARGUMENT, "runtime: unexpected node kind " + std::to_string(n.kind));
             }
+            // control flow: private-typed add/sub/mul/phi may hold a public value at run time
+            if (r->cfg && !st.out.is_public && !st.shadow_pub &&
+                (n.kind == SPDZ_NODE_ADD || n.kind == SPDZ_NODE_SUB || n.kind == SPDZ_NODE_MUL || n.kind == SPDZ_NODE_PHI))
+                st.shadow_pub = r->alloc(p, L);
         }
         const Val& rv = P.ns[r->root].out;
         P.outputs = r->alloc(p, std::max<uint64_t>(rv.lanes, 1));
@@ -1008,6 +1022,7 @@ struct Exec {
     // buffer: broadcast a 1-lane value, and a public value reaching a private phi becomes
     // the sharing of that public (share_of_public, spdz.cpp:66-75)
     void phi_copy(uint32_t phi, uint32_t chosen) {
+        const bool dyn = r->nodes[phi].is_private && eff_pub(chosen);
         for (int p = 0; p < r->n; ++p) {
             auto& P = r->parties[p];
             if (!P.local) continue;
@@ -1026,10 +1041,16 @@ struct Exec {
                     lk(launch_bcast(c->stream, s.pub, nullptr, o.pub, nullptr, o.lanes, c->sms), "phi bcast");
                 continue;
             }
-            if (s.is_public) {  // party 0 holds k, MAC shares alpha_i * k
-                lk(launch_public(c->stream, 4, nullptr, nullptr, s.pub, s.lanes != o.lanes, 0u, false, c->party,
+            if (eff_pub(chosen)) {  // party 0 holds k, MAC shares alpha_i * k; k kept as the public value
+                const uint32_t* k = pub_of(p, chosen);
+                lk(launch_public(c->stream, 4, nullptr, nullptr, k, s.lanes != o.lanes, 0u, false, c->party,
                                  c->alpha, o.v, o.m, o.lanes, c->sms, c->d_alpha),
                    "phi share_of_public");
+                uint32_t* sp = P.ns[phi].shadow_pub;
+                if (s.lanes == o.lanes)
+                    lk(cudaMemcpyAsync(sp, k, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
+                else
+                    lk(launch_bcast(c->stream, k, nullptr, sp, nullptr, o.lanes, c->sms), "phi bcast");
             } else if (s.lanes == o.lanes) {
                 lk(cudaMemcpyAsync(o.v, s.v, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
                 lk(cudaMemcpyAsync(o.m, s.m, o.lanes * 4, cudaMemcpyDeviceToDevice, c->stream), "phi");
@@ -1037,6 +1058,65 @@ struct Exec {
                 lk(launch_bcast(c->stream, s.v, s.m, o.v, o.m, o.lanes, c->sms), "phi bcast");
             }
         }
+        r->rt_pub[phi] = dyn;
+    }
+
+    // is the node's current value public (statically, or a private-typed node holding a public)?
+    bool eff_pub(uint32_t id) const {
+        return r->parties[r->ref_party()].ns[id].out.is_public || (r->cfg && r->rt_pub[id]);
+    }
+    const uint32_t* pub_of(int p, uint32_t id) const {
+        const auto& st = r->parties[p].ns[id];
+        return st.out.is_public ? st.out.pub : st.shadow_pub;
+    }
+
+    // Control flow: add/sub/mul of a private-typed node whose operands are public at run time
+    // compute publicly (the public value kept beside its sharing), and a multiply by such a value
+    // is a local mul_public — no Beaver triple, as the reference's exec_add / exec_mul_local see
+    // public RtValues (runtime.cpp:129-183).  Returns true when it handled the node.
+    bool exec_dynamic_public(uint32_t id) {
+        const auto& n = r->nodes[id];
+        if (n.kind != SPDZ_NODE_ADD && n.kind != SPDZ_NODE_SUB && n.kind != SPDZ_NODE_MUL) return false;
+        if (r->parties[r->ref_party()].ns[id].out.is_public) return false;
+        r->rt_pub[id] = 0;
+        const bool pa = eff_pub(n.operands[0]), pb = eff_pub(n.operands[1]);
+        const bool dyn_a = pa && !r->parties[r->ref_party()].ns[n.operands[0]].out.is_public;
+        const bool dyn_b = pb && !r->parties[r->ref_party()].ns[n.operands[1]].out.is_public;
+        if (!dyn_a && !dyn_b) return false;  // static typing already decides this node
+        const uint64_t L = n.lanes;
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            if (!P.local) continue;
+            auto& st = P.ns[id];
+            const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
+            spdz_ctx* c = P.ctx;
+            dev(r, p);
+            if (pa && pb) {  // public op, then its sharing for private-typed consumers
+                const int op = n.kind == SPDZ_NODE_ADD ? 0 : (n.kind == SPDZ_NODE_SUB ? 1 : 2);
+                lk(launch_pub_binop(c->stream, op, pub_of(p, n.operands[0]), a.lanes != L, pub_of(p, n.operands[1]),
+                                    b.lanes != L, st.shadow_pub, L, c->sms),
+                   "dyn pub op");
+                lk(launch_public(c->stream, 4, nullptr, nullptr, st.shadow_pub, false, 0u, false, c->party, c->alpha,
+                                 st.out.v, st.out.m, L, c->sms, c->d_alpha),
+                   "dyn share_of_public");
+                continue;
+            }
+            if (n.kind != SPDZ_NODE_MUL) return false;  // share +- sharing-of-public == add_public
+            const Val& sh = pa ? b : a;
+            const uint32_t* k = pub_of(p, pa ? n.operands[0] : n.operands[1]);
+            const uint64_t kl = (pa ? a : b).lanes;
+            const uint32_t *iv = sh.v, *im = sh.m;
+            if (sh.lanes != L) {
+                bcast_into(p, sh, st.out);
+                iv = st.out.v;
+                im = st.out.m;
+            }
+            lk(launch_public(c->stream, 3, iv, im, k, kl != L, 0u, false, c->party, c->alpha, st.out.v, st.out.m, L,
+                             c->sms, c->d_alpha),
+               "dyn mul_public");
+        }
+        r->rt_pub[id] = pa && pb;
+        return true;
     }
 
     // Block-by-block execution of a control-flow graph: the sequential reading of the
@@ -1504,6 +1584,7 @@ struct Exec {
 
     // runtime.cpp:360-450, one execution of node `id`
     void exec_node(uint32_t id, uint64_t exec) {
+        if (r->cfg && exec_dynamic_public(id)) return;
         {
             const auto& n = r->nodes[id];
             switch (n.kind) {
@@ -2223,7 +2304,10 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         } else {
             Exec ex{r};
             r->scalar_used = r->matrix_used = 0;
-            if (r->cfg) ex.run_cfg();
+            if (r->cfg) {
+                r->rt_pub.assign(r->nodes.size(), 0);
+                ex.run_cfg();
+            }
             else ex.run_nodes();
             ex.open_root();
         }
