@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <exception>
 #include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <string>
 #include <thread>
 #include <vector>
@@ -29,6 +31,14 @@ using namespace mpc;
 namespace fs = std::filesystem;
 
 static int failures = 0;
+
+// `"key": <integer>` from a bundle's expected.json (flat numbers only)
+static uint64_t json_number(const fs::path& path, const std::string& key, uint64_t fallback) {
+    std::ifstream is(path);
+    const std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    const auto at = text.find("\"" + key + "\":");
+    return at == std::string::npos ? fallback : std::stoull(text.substr(at + key.size() + 3));
+}
 
 static runtime::RunReport reference_files(const circuit::CircuitGraph& g, const std::vector<std::string>& triples,
                                           const preproc::Inputs& in, runtime::RunOptions opts) {
@@ -83,7 +93,7 @@ int main(int argc, char** argv) {
         for (int i = 0; fs::exists(d / ("triples_" + std::to_string(i) + ".bin")); ++i)
             triples.push_back((d / ("triples_" + std::to_string(i) + ".bin")).string());
         runtime::RunOptions opts;
-        opts.slice = name == "linear_64x32" ? 256 : 262140;  // the slice the bundle's stores were dealt for
+        opts.slice = json_number(d / "expected.json", "slice", 262140);  // the slice the stores were dealt for
         try {
             compare(name + " (store files)", reference_files(g, triples, in, opts),
                     runtime::run_files_b200(g, triples, in, opts, 0)[0]);

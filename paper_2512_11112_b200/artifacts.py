@@ -50,8 +50,8 @@ class ShapeMismatch(InvalidArgument):
 
 
 class UnsupportedCircuit(InvalidArgument):
-    """The circuit needs something this executor does not run (provisional Raw* nodes, a
-    triple-consuming reduce_mul or linear layer inside a loop, phis of more than 3 edges)."""
+    """The circuit needs something this executor does not run (provisional Raw* nodes, phis
+    of more than 3 edges, operands later than the node)."""
 
 
 # ---------------------------------------------------------------- MPCG circuit files
@@ -122,8 +122,6 @@ class CircuitFile:
             if len(n.operands) > 3 or len(n.successors) > 2:
                 raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} has {len(n.operands)} operands")
             loop_depth = depth.get(n.block, 0) if n.block != NO_NODE else 0
-            if loop_depth and kind in (LINEAR, REDUCE_MUL) and self.nodes[n.operands[0]].is_private:
-                raise UnsupportedCircuit(f"UnsupportedCircuit: {n.kind} {n.id} inside a loop")
             spec = NodeSpec(kind, n.lanes, tuple(n.operands), n.is_private, din=n.din, dout=n.dout, next=n.next,
                             loop_depth=loop_depth, succ=tuple(n.successors), phi_labels=tuple(n.phi_labels))
             if kind == INPUT:

@@ -65,6 +65,8 @@ struct RedLevel {
     uint32_t *payload = nullptr, *opened = nullptr, *shadow = nullptr;
     uint32_t *zv = nullptr, *zm = nullptr;  // pairs (+1 odd passthrough)
     uint64_t out_lanes = 0;
+    // control flow: xm / ym / opened of every provisioned execution (the MAC log reads them all)
+    uint32_t *xm_all = nullptr, *ym_all = nullptr, *opened_all = nullptr;
 };
 
 struct NodeState {                  // per party, per node
@@ -79,6 +81,7 @@ struct NodeState {                  // per party, per node
     // linear
     uint32_t *bias_v = nullptr, *bias_m = nullptr;
     uint32_t *mA[2] = {nullptr, nullptr}, *mB[2] = {nullptr, nullptr}, *mC[2] = {nullptr, nullptr};
+    uint32_t *mA0[2] = {nullptr, nullptr}, *mB0[2] = {nullptr, nullptr}, *mC0[2] = {nullptr, nullptr};  // exec 0
     uint32_t* lin_tmp = nullptr;    // public x public scratch
     // control flow: a Beaver node's opened values and operand MAC shares, one slot per
     // execution (the MAC check reads every execution's record after the last one)
@@ -470,8 +473,6 @@ void plan_buffers(spdz_run* r) {
                     break;
                 case SPDZ_NODE_REDUCE_MUL: {
                     const Val& a = opnd(0);
-                    need(!r->cfg || !r->scalar.count(id) || r->scalar.at(id).max_execs == 1, SPDZ_ERR_INVALID_ARGUMENT,
-                         "UnsupportedCircuit: reduce_mul inside a loop");
                     if (a.is_public) {
                         pub_out(1);
                         st.opened = r->alloc(p, std::max<uint64_t>(a.lanes, 1));  // scratch tree
@@ -488,6 +489,12 @@ void plan_buffers(spdz_run* r) {
                         lv.ym = r->alloc(p, lv.pairs);
                         lv.payload = r->alloc(p, 2 * lv.pairs);
                         lv.opened = r->alloc(p, 2 * lv.pairs);
+                        if (r->cfg) {  // every execution keeps its MAC-log records
+                            const uint64_t E = r->scalar.count(id) ? r->scalar.at(id).max_execs : 1;
+                            lv.xm_all = r->alloc(p, lv.pairs * E);
+                            lv.ym_all = r->alloc(p, lv.pairs * E);
+                            lv.opened_all = r->alloc(p, 2 * lv.pairs * E);
+                        }
                         lv.out_lanes = lv.pairs + (cur & 1);
                         lv.zv = r->alloc(p, lv.out_lanes);
                         lv.zm = r->alloc(p, lv.out_lanes);
@@ -503,8 +510,6 @@ void plan_buffers(spdz_run* r) {
                 }
                 case SPDZ_NODE_LINEAR: {
                     const Val &x = opnd(0), &w = opnd(1);
-                    need(!r->cfg || !r->matrix.count(id) || r->matrix.at(id).max_execs == 1, SPDZ_ERR_INVALID_ARGUMENT,
-                         "UnsupportedCircuit: linear layer inside a loop");
                     need(x.lanes == n.din && w.lanes == (uint64_t)n.din * n.dout, SPDZ_ERR_INVALID_ARGUMENT,
                          "ShapeMismatch: linear operands do not match din/dout");
                     if (x.is_public && w.is_public) {
@@ -519,6 +524,11 @@ void plan_buffers(spdz_run* r) {
                         const uint64_t cells = (uint64_t)n.din * n.dout, etot = (uint64_t)n.din * lt.starts.size();
                         st.payload = r->alloc(p, cells + etot);
                         st.opened = r->alloc(p, cells + etot);
+                        if (r->cfg) {  // every execution: opened [D|E] and the W.m / x.m it is checked against
+                            const uint64_t E = r->matrix.at(id).max_execs;
+                            st.opened_all = r->alloc(p, (cells + etot) * E);
+                            st.macsnap = r->alloc(p, (cells + n.din) * E);
+                        }
                         st.bias_v = r->alloc(p, n.dout);
                         st.bias_m = r->alloc(p, n.dout);
                         st.lin_tmp = r->alloc(p, 2ull * n.dout);
@@ -599,7 +609,10 @@ void deal(spdz_run* r, uint64_t seed) {
             const auto& nd = r->node(id);
             const auto& lt = r->tiles[id];
             auto& pl = dd.layer[id];
-            const uint64_t cells_all = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * lt.starts.size();
+            const uint64_t cells_one = (uint64_t)nd.din * nd.dout, etot_one = (uint64_t)nd.din * lt.starts.size();
+            const uint64_t E = reg.max_execs;  // per party: E executions, party stride E * plane
+            const uint64_t cells_all = E * cells_one, etot = E * etot_one;
+            for (uint64_t ex = 0; ex < E; ++ex)  // preproc.cpp:104-112: per execution, per tile
             for (size_t t = 0; t < lt.starts.size(); ++t) {
                 const uint32_t rows = lt.counts[t];
                 const uint64_t cells = (uint64_t)nd.din * rows;
@@ -611,18 +624,18 @@ void deal(spdz_run* r, uint64_t seed) {
                 lk(launch_dealer_uniform(ctx->stream, seed, k, nd.din, 1, B, ctx->d_flag, ctx->sms), "deal B");
                 k += nd.din;
                 lk(launch_dealer_matvec(ctx->stream, A, B, nd.din, rows, Cc), "deal C");
-                const uint64_t aoff = (uint64_t)lt.starts[t] * nd.din;
+                const uint64_t aoff = ex * cells_one + (uint64_t)lt.starts[t] * nd.din;
                 lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, A, cells, pl[0] + aoff, pl[1] + aoff, cells_all,
                                        ctx->d_flag, ctx->sms),
                    "share A");
                 k += dealer_draws_share(n, cells);
-                const uint64_t boff = (uint64_t)t * nd.din;
+                const uint64_t boff = ex * etot_one + (uint64_t)t * nd.din;
                 lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, B, nd.din, pl[2] + boff, pl[3] + boff, etot,
                                        ctx->d_flag, ctx->sms),
                    "share B");
                 k += dealer_draws_share(n, nd.din);
-                lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, Cc, rows, pl[4] + lt.starts[t],
-                                       pl[5] + lt.starts[t], nd.dout, ctx->d_flag, ctx->sms),
+                lk(launch_dealer_share(ctx->stream, n, seed, k, alpha, Cc, rows, pl[4] + ex * nd.dout + lt.starts[t],
+                                       pl[5] + ex * nd.dout + lt.starts[t], E * nd.dout, ctx->d_flag, ctx->sms),
                    "share C");
                 k += dealer_draws_share(n, rows);
                 (void)reg;
@@ -682,6 +695,8 @@ void load_store(spdz_run* r, int p, const char* path) {
         const auto& nd = r->node(id);
         const auto& lt = r->tiles[id];
         auto& st = P.ns[id];
+        const uint64_t cells1 = (uint64_t)nd.din * nd.dout, etot1 = (uint64_t)nd.din * lt.starts.size();
+        for (uint64_t ex = 0; ex < reg.max_execs; ++ex)
         for (size_t t = 0; t < lt.starts.size(); ++t, ++k) {
             const auto& m = L.mats[k];
             const uint32_t rows = lt.counts[t];
@@ -691,9 +706,10 @@ void load_store(spdz_run* r, int p, const char* path) {
                                 ", tile needs " + std::to_string(rows) + "x" + std::to_string(nd.din));
             const uint64_t cells = (uint64_t)rows * nd.din;
             uint64_t at = m.off;
-            const uint64_t aoff = (uint64_t)lt.starts[t] * nd.din, boff = (uint64_t)t * nd.din;
-            uint32_t* dst[6] = {st.mA[0] + aoff, st.mA[1] + aoff, st.mB[0] + boff,
-                                st.mB[1] + boff, st.mC[0] + lt.starts[t], st.mC[1] + lt.starts[t]};
+            const uint64_t aoff = ex * cells1 + (uint64_t)lt.starts[t] * nd.din, boff = ex * etot1 + (uint64_t)t * nd.din;
+            const uint64_t coff = ex * nd.dout + lt.starts[t];
+            uint32_t* dst[6] = {st.mA0[0] + aoff, st.mA0[1] + aoff, st.mB0[0] + boff,
+                                st.mB0[1] + boff, st.mC0[0] + coff, st.mC0[1] + coff};
             const uint64_t words[6] = {cells, cells, nd.din, nd.din, rows, rows};
             for (int q = 0; q < 6; ++q) {
                 up.copy(at, 4 * words[q], dst[q]);
@@ -729,16 +745,17 @@ void alloc_deals(spdz_run* r) {
         dd.mask_v = r->alloc_dev_words(d, n * M);
         dd.mask_m = r->alloc_dev_words(d, n * M);
         dd.mask_c = r->alloc_dev_words(d, M);
-        for (auto& [id, reg] : r->matrix) {
+        for (auto& [id, reg] : r->matrix) {  // per party: max_execs executions of every plane
             const auto& nd = r->node(id);
+            const uint64_t E = reg.max_execs;
             const uint64_t cells = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * r->tiles[id].starts.size();
             std::array<uint32_t*, 6> pl;
-            pl[0] = r->alloc_dev_words(d, n * cells);
-            pl[1] = r->alloc_dev_words(d, n * cells);
-            pl[2] = r->alloc_dev_words(d, n * etot);
-            pl[3] = r->alloc_dev_words(d, n * etot);
-            pl[4] = r->alloc_dev_words(d, n * (uint64_t)nd.dout);
-            pl[5] = r->alloc_dev_words(d, n * (uint64_t)nd.dout);
+            pl[0] = r->alloc_dev_words(d, n * E * cells);
+            pl[1] = r->alloc_dev_words(d, n * E * cells);
+            pl[2] = r->alloc_dev_words(d, n * E * etot);
+            pl[3] = r->alloc_dev_words(d, n * E * etot);
+            pl[4] = r->alloc_dev_words(d, n * E * (uint64_t)nd.dout);
+            pl[5] = r->alloc_dev_words(d, n * E * (uint64_t)nd.dout);
             dd.layer[id] = pl;
         }
         dd.scratch = r->alloc_dev_words(d, scratch);
@@ -757,12 +774,13 @@ void alloc_deals(spdz_run* r) {
             const uint64_t cells = (uint64_t)nd.din * nd.dout, etot = (uint64_t)nd.din * r->tiles[id].starts.size();
             auto& pl = dd.layer[id];
             auto& st = P.ns[id];
-            st.mA[0] = pl[0] + p * cells;
-            st.mA[1] = pl[1] + p * cells;
-            st.mB[0] = pl[2] + p * etot;
-            st.mB[1] = pl[3] + p * etot;
-            st.mC[0] = pl[4] + p * (uint64_t)nd.dout;
-            st.mC[1] = pl[5] + p * (uint64_t)nd.dout;
+            const uint64_t E = r->matrix.at(id).max_execs;
+            st.mA[0] = st.mA0[0] = pl[0] + p * E * cells;
+            st.mA[1] = st.mA0[1] = pl[1] + p * E * cells;
+            st.mB[0] = st.mB0[0] = pl[2] + p * E * etot;
+            st.mB[1] = st.mB0[1] = pl[3] + p * E * etot;
+            st.mC[0] = st.mC0[0] = pl[4] + p * E * (uint64_t)nd.dout;
+            st.mC[1] = st.mC0[1] = pl[5] + p * E * (uint64_t)nd.dout;
         }
     }
 }
@@ -1318,6 +1336,15 @@ struct Exec {
             return;
         }
         uint64_t used = 0, sub = 1;
+        if (r->cfg)  // this execution's MAC-log slots
+            for (int p = 0; p < r->n; ++p) {
+                if (!r->parties[p].local) continue;
+                for (auto& lv : r->parties[p].ns[id].levels) {
+                    lv.xm = lv.xm_all + lv.pairs * exec;
+                    lv.ym = lv.ym_all + lv.pairs * exec;
+                    lv.opened = lv.opened_all + 2 * lv.pairs * exec;
+                }
+            }
         for (size_t li = 0; li < nlev; ++li) {
             std::vector<cudaEvent_t> sent(r->n);
             const uint64_t off = reg.base + exec * reg.stride + used;
@@ -1425,6 +1452,27 @@ struct Exec {
         const uint64_t etot = (uint64_t)din * ntiles;
         const uint64_t batch0 = make_batch(id, exec, 0);
         std::vector<cudaEvent_t> sent(r->n);
+        for (int p = 0; p < r->n; ++p) {  // execution `exec`'s matrix triples (take_matrix_at, runtime.cpp:346-350)
+            if (!r->parties[p].local) continue;
+            auto& st = r->parties[p].ns[id];
+            for (int q = 0; q < 2; ++q) {
+                st.mA[q] = st.mA0[q] + exec * cells;
+                st.mB[q] = st.mB0[q] + exec * etot;
+                st.mC[q] = st.mC0[q] + exec * dout;
+            }
+            if (r->cfg) st.opened = st.opened_all + exec * (cells + etot);
+        }
+        // the W.m / x.m the records are checked against: the operands, or (control flow) a snapshot
+        auto mac_planes = [&](int p) -> std::pair<const uint32_t*, const uint32_t*> {
+            auto& P = r->parties[p];
+            const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out;
+            if (!r->cfg) return {w.m, x.m};
+            uint32_t* snap = P.ns[id].macsnap + exec * (cells + din);
+            dev(r, p);
+            lk(cudaMemcpyAsync(snap, w.m, cells * 4, cudaMemcpyDeviceToDevice, S(r, p)), "snapshot W.m");
+            lk(cudaMemcpyAsync(snap + cells, x.m, din * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "snapshot x.m");
+            return {snap, snap + cells};
+        };
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -1485,12 +1533,12 @@ struct Exec {
             r->exchanged += 2 * (cells + etot) * 4;
             for (int p = 0; p < 2; ++p) {
                 auto& P = r->parties[p];
-                const Val &x = P.ns[n.operands[0]].out, &w = P.ns[n.operands[1]].out;
+                const auto [wm, xm] = mac_planes(p);
                 auto& st = P.ns[id];
                 for (uint32_t t = 0; t < ntiles; ++t) {  // linear.cpp:113 log per tile: [D_t | E_t]
                     const uint64_t aoff = (uint64_t)lt.starts[t] * din, ct = (uint64_t)lt.counts[t] * din;
-                    P.maclog.push_back({s0.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
-                    P.maclog.push_back({s0.opened + cells + (uint64_t)t * din, x.m, st.mB[1] + (uint64_t)t * din,
+                    P.maclog.push_back({s0.opened + aoff, wm + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
+                    P.maclog.push_back({s0.opened + cells + (uint64_t)t * din, xm, st.mB[1] + (uint64_t)t * din,
                                         din, 0, batch0 + t, ct, 0});
                 }
             }
@@ -1524,10 +1572,11 @@ struct Exec {
                "k_matrix_combine");
             // own D 4 + peer D 4k + A.v A.m 8 + opened D 4 per cell (B, E from cache)
             tend(p, tk, SPDZ_KSTAT_COMBINE, (16 + 4ull * k) * cells);
+            const auto [wm, xm] = mac_planes(p);
             for (uint32_t t = 0; t < ntiles; ++t) {  // linear.cpp:113 log per tile: [D_t | E_t]
                 const uint64_t aoff = (uint64_t)lt.starts[t] * din, ct = (uint64_t)lt.counts[t] * din;
-                P.maclog.push_back({st.opened + aoff, w.m + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
-                P.maclog.push_back({st.opened + cells + (uint64_t)t * din, x.m, st.mB[1] + (uint64_t)t * din, din, 0,
+                P.maclog.push_back({st.opened + aoff, wm + aoff, st.mA[1] + aoff, ct, 0, batch0 + t, 0, 0});
+                P.maclog.push_back({st.opened + cells + (uint64_t)t * din, xm, st.mB[1] + (uint64_t)t * din, din, 0,
                                     batch0 + t, ct, 0});
             }
         }
@@ -2369,6 +2418,8 @@ int spdz_run_mac_check_launch(spdz_run* r, int use_coin, uint64_t coin) {
     return guard([&] {
         need(r != nullptr && r->in_flight && !r->mac_launched, SPDZ_ERR_INVALID_ARGUMENT,
              "no online phase in flight (or its MAC check was already launched)");
+        need(!r->net, SPDZ_ERR_INVALID_ARGUMENT,
+             "network runs agree on the coin with their peers: use spdz_run_mac_check");
         r->mac_coin = agree_coin(r, use_coin != 0, coin);
         mac_launch(r, r->mac_coin);
         r->mac_launched = true;

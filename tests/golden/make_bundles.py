@@ -68,6 +68,46 @@ exit:
 """ + workloads._DECL
 
 
+# a secret x secret linear layer inside a loop (matrix triples per execution, loop_iters x tiles)
+LINEAR_LOOP_IR = workloads._HDR + """define ptr @main(ptr %x, ptr %W, ptr %b, i32 %n) {
+entry:
+""" + workloads._ann("x", True) + workloads._ann("W", True) + workloads._ann("b", True) + """  br label %loop
+loop:
+  %i = phi i32 [ 1, %entry ], [ %inext, %loop ]
+  %y = call ptr @mark_linear_layer(ptr %x, ptr %W, ptr %b, i32 16, i32 12)
+  %inext = add i32 %i, 1
+  %c = icmp sle i32 %inext, %n
+  br i1 %c, label %loop, label %exit
+exit:
+  ret ptr %y
+}
+
+declare ptr @mark_linear_layer(ptr, ptr, ptr, i32, i32)
+""" + workloads._DECL
+
+# reduce_mul of a loop-carried vector (a Beaver product tree per execution)
+REDUCE_LOOP_IR = workloads._HDR + """define i32 @main(ptr %x, i32 %n) {
+entry:
+""" + workloads._ann("x", True) + """  %a = load <9 x i32>, ptr %x
+  br label %loop
+loop:
+  %i = phi i32 [ 1, %entry ], [ %inext, %loop ]
+  %v = phi <9 x i32> [ %a, %entry ], [ %v2, %loop ]
+  %p = call i32 @llvm.vector.reduce.mul.v9i32(<9 x i32> %v)
+  %v2 = add <9 x i32> %v, %a
+  %acc = phi i32 [ 0, %entry ], [ %acc2, %loop ]
+  %acc2 = add i32 %acc, %p
+  %inext = add i32 %i, 1
+  %c = icmp sle i32 %inext, %n
+  br i1 %c, label %loop, label %exit
+exit:
+  ret i32 %acc2
+}
+
+declare i32 @llvm.vector.reduce.mul.v9i32(<9 x i32>)
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
@@ -98,6 +138,9 @@ def cases():
                             8),
         "vector_loop": (VECTOR_LOOP_IR, 2, 262140, 17, {"x": rnd(512, 22), "y": rnd(512, 23),
                                                         "n": np.array([5], np.uint32)}, 6),
+        "linear_loop": (LINEAR_LOOP_IR, 2, 64, 18, {"x": rnd(16, 24), "W": rnd(192, 25), "b": rnd(12, 26),
+                                                    "n": np.array([3], np.uint32)}, 4),
+        "reduce_mul_loop": (REDUCE_LOOP_IR, 3, 262140, 19, {"x": rnd(9, 27), "n": np.array([4], np.uint32)}, 5),
     }
 
 
