@@ -112,6 +112,8 @@ def lib():
                                              C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, U32P, C.c_uint64,
                                              C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
                                              C.POINTER(C.c_uint64)]
+        L.reft_kernel_bench.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]
+        L.reft_kernel_bench.restype = C.c_double
         L.reft_time_beaver_kernels.argtypes = [C.c_uint64, C.c_int]
         L.reft_time_beaver_kernels.restype = C.c_double
     return _lib
@@ -455,6 +457,11 @@ def mesh_probe(party: int, endpoints, own):
     opened = np.zeros(own.size, np.uint32)
     _check(lib().reft_mesh_probe(party, len(endpoints), _eps(endpoints), own.size, own, exch, opened))
     return exch.reshape(-1, 2), opened
+
+
+def kernel_bench(kind: int, a: int = 0, b: int = 0, iters: int = 10) -> float:
+    """benchmarks/kernel_bench.cpp cases on the reference CpuBackend: mean ns per iteration."""
+    return lib().reft_kernel_bench(kind, a, b, iters)
 
 
 def time_beaver_kernels(lanes: int, reps: int = 3) -> float:

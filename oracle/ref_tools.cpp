@@ -597,6 +597,58 @@ int reft_run_local_circuit(const char* circuit_path, int n_parties, uint64_t sli
     });
 }
 
+// benchmarks/kernel_bench.cpp:24-88 cases, timed here: mean ns per iteration over `iters`
+// iterations (kind 0 FieldMul, 1 AddBatch(a lanes), 2 MulMaskCombine(a lanes),
+// 3 MatrixCombine(din a, rows b), 4 PlanTiles(8192, 8192, 262140)).
+double reft_kernel_bench(int kind, uint64_t a, uint64_t b, uint64_t iters) {
+    auto rs = [](size_t lanes, uint64_t seed) {  // kernel_bench.cpp:12-22
+        std::mt19937_64 rng(seed);
+        ShareVec s;
+        for (size_t i = 0; i < lanes; ++i) {
+            s.vals.push_back(uint32_t(rng() % kPrime));
+            s.macs.push_back(uint32_t(rng() % kPrime));
+        }
+        return s;
+    };
+    auto be = backend::make_cpu_backend();
+    volatile uint64_t sink = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    if (kind == 0) {
+        uint32_t x = 123456789, y = 987654321;
+        for (uint64_t i = 0; i < iters; ++i) x = fp::mul(x, y);
+        sink = x;
+        t0 = t0;  // timed below with the same clock
+    } else if (kind == 1) {
+        auto x = rs(a, 1), y = rs(a, 2);
+        t0 = std::chrono::steady_clock::now();
+        for (uint64_t i = 0; i < iters; ++i) sink += be->add_batch(x, y).vals[0];
+    } else if (kind == 2) {
+        auto x = rs(a, 1), y = rs(a, 2);
+        spdz::TripleShares t{rs(a, 3), rs(a, 4), rs(a, 5)};
+        std::vector<uint32_t> d, e;
+        t0 = std::chrono::steady_clock::now();
+        for (uint64_t i = 0; i < iters; ++i) {
+            be->mul_mask(x, y, t, d, e);
+            sink += be->mul_combine(t, d, e, 0, 7).vals[0];
+        }
+    } else if (kind == 3) {
+        spdz::MatrixTripleShares mt;
+        mt.din = uint32_t(a);
+        mt.rows = uint32_t(b);
+        mt.a = rs(a * b, 1);
+        mt.b = rs(a, 2);
+        mt.c = rs(b, 3);
+        auto D = rs(a * b, 4).vals;
+        auto E = rs(a, 5).vals;
+        t0 = std::chrono::steady_clock::now();
+        for (uint64_t i = 0; i < iters; ++i) sink += spdz::matrix_combine(mt, D, E, 0, 7).vals[0];
+    } else {
+        for (uint64_t i = 0; i < iters; ++i) sink += linear::plan_tiles(8192, 8192, 262140).tiles.size();
+    }
+    (void)sink;
+    return std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count() / double(iters);
+}
+
 // Kernel-level CPU timing (pattern of benchmarks/kernel_bench.cpp:33-58):
 // best-of-`reps` wall time of CpuBackend::mul_mask + mul_combine on `lanes`.
 double reft_time_beaver_kernels(uint64_t lanes, int reps) {

@@ -17,6 +17,7 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
 
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:k_matrix_combine2 -s 2 -c 1 -o gpurun_out/prof_matrix_combine2 python scripts/linear_probe.py > gpurun_out/ncu_mc2.log 2>&1
 timeout 300 python scripts/streamed_timeline.py 8 > gpurun_out/timeline.log 2>&1
+timeout 600 python scripts/kernel_bench.py > gpurun_out/kernel_bench.json 2> gpurun_out/kernel_bench.err
 timeout 300 python scripts/linear_probe.py > gpurun_out/linear_probe.log 2>&1
 for s in "1024 256" "8192 1024"; do timeout 300 python scripts/gemm_probe.py $s --tc-only --diag --prepared; done > gpurun_out/gemm_diag.log 2>&1
 
