@@ -145,6 +145,23 @@ int spdz_diag_gemm_tc_flags(uint32_t flags);
 /* Number of kernels this library launched on any context since load (evidence counter). */
 uint64_t spdz_kernel_launches(void);
 
+/* ---------------- device buffers and completion events ----------------
+ * SoA share buffers in HBM and stream-ordered copies (host buffers must stay valid, and
+ * unchanged, until an event recorded after the copy has completed); events let a
+ * caller's pump loop poll completion without blocking (runtime.cpp:452-465). */
+int spdz_share_alloc(spdz_ctx* ctx, uint64_t lanes, spdz_share_t* out);
+int spdz_share_free(spdz_ctx* ctx, spdz_share_t* s);
+int spdz_share_upload(spdz_ctx* ctx, spdz_share_t* dst, const uint32_t* host_vals, const uint32_t* host_macs,
+                      uint64_t lanes);
+int spdz_share_download(spdz_ctx* ctx, const spdz_share_t* src, uint32_t* host_vals, uint32_t* host_macs,
+                        uint64_t lanes);
+typedef struct spdz_event spdz_event;
+int spdz_event_record(spdz_ctx* ctx, spdz_event** out);   /* records on ctx's stream */
+int spdz_event_query(spdz_event* ev, int* done);          /* non-blocking: *done = 1 when complete */
+int spdz_event_sync(spdz_event* ev);
+int spdz_event_wait(spdz_ctx* ctx, spdz_event* ev);       /* ctx's stream waits for ev (other party / device) */
+int spdz_event_destroy(spdz_event* ev);
+
 /* ---------------- Backend: batched share ops (device) ---------------- */
 /* backend.hpp:37 / backend.cpp:25-37: z = x + y on both planes */
 int spdz_add_batch(spdz_ctx* ctx, const spdz_share_t* x, const spdz_share_t* y, spdz_share_t* z);
@@ -197,6 +214,18 @@ int spdz_mac_sigma(spdz_ctx* ctx, const spdz_mac_segment_t* segs, uint64_t n_seg
 int spdz_mac_sigma_records(spdz_ctx* ctx, const uint64_t* host_batch, const uint32_t* host_lane,
                            const uint32_t* dev_value, const uint32_t* dev_mac, uint64_t n, uint64_t coin,
                            uint32_t* sigma_out);
+/* The log itself, kept in the context for a caller-driven runtime (log_open,
+ * runtime.cpp:112-117, and mac_check, runtime.cpp:467-506): append each opening's
+ * device arrays as it completes (from any thread; a batch may arrive in pieces, lanes
+ * continue), then one sigma over every record with ranks in (batch_id, lane) order.
+ * mac = dev_mac - dev_mac_sub when dev_mac_sub is not NULL (de_macs = x.m - a.m without
+ * materialising it).  The arrays must stay valid until spdz_mac_log_sigma returns. */
+int spdz_mac_log_append(spdz_ctx* ctx, uint64_t batch_id, const uint32_t* dev_opened, const uint32_t* dev_mac,
+                        const uint32_t* dev_mac_sub, uint64_t len);
+int spdz_mac_log_size(spdz_ctx* ctx, uint64_t* n_records);
+int spdz_mac_log_sigma(spdz_ctx* ctx, uint64_t coin, uint32_t* sigma_out);
+int spdz_mac_log_clear(spdz_ctx* ctx);
+
 /* spdz.cpp:140-145 */
 uint64_t spdz_commit_sigma(uint32_t sigma, uint64_t nonce);
 /* spdz.cpp:147-158: SPDZ_OK or SPDZ_ERR_MAC_CHECK_FAILED */

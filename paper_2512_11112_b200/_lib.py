@@ -169,6 +169,19 @@ _SIGS = {
     "spdz_run_export": (C.c_int, [vp, vp, C.c_uint64, u64p]),
     "spdz_run_import": (C.c_int, [vp, vp, C.c_uint64]),
     "spdz_run_inject_bitflip": (C.c_int, [vp, C.c_uint32, C.c_int, C.c_int, C.c_uint64, C.c_uint32]),
+    "spdz_share_alloc": (C.c_int, [vp, C.c_uint64, C.POINTER(Share)]),
+    "spdz_share_free": (C.c_int, [vp, C.POINTER(Share)]),
+    "spdz_share_upload": (C.c_int, [vp, C.POINTER(Share), vp, vp, C.c_uint64]),
+    "spdz_share_download": (C.c_int, [vp, C.POINTER(Share), vp, vp, C.c_uint64]),
+    "spdz_event_record": (C.c_int, [vp, C.POINTER(vp)]),
+    "spdz_event_query": (C.c_int, [vp, C.POINTER(C.c_int)]),
+    "spdz_event_sync": (C.c_int, [vp]),
+    "spdz_event_wait": (C.c_int, [vp, vp]),
+    "spdz_event_destroy": (C.c_int, [vp]),
+    "spdz_mac_log_append": (C.c_int, [vp, C.c_uint64, vp, vp, vp, C.c_uint64]),
+    "spdz_mac_log_size": (C.c_int, [vp, u64p]),
+    "spdz_mac_log_sigma": (C.c_int, [vp, C.c_uint64, C.POINTER(C.c_uint32)]),
+    "spdz_mac_log_clear": (C.c_int, [vp]),
     "spdz_net_connect": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_char_p), C.c_uint64, C.c_uint64, C.POINTER(vp)]),
     "spdz_net_destroy": (C.c_int, [vp]),
     "spdz_net_send": (C.c_int, [vp, C.c_int, C.c_int, C.c_uint64, vp, C.c_uint32]),

@@ -160,6 +160,33 @@ class Context:
         check(lib().spdz_open_sum(self.h, own.data_ptr(), arr, len(peers), own.numel(), out.data_ptr()))
 
     # secret x public linear layer with the public W prepared once (runtime.cpp:303-334)
+    # ---- completion events and the caller-driven MAC log ----
+    def record_event(self) -> "DeviceEvent":
+        h = C.c_void_p()
+        check(lib().spdz_event_record(self.h, C.byref(h)))
+        return DeviceEvent(h)
+
+    def wait_event(self, ev: "DeviceEvent"):
+        check(lib().spdz_event_wait(self.h, ev.h))
+
+    def mac_log_append(self, batch_id: int, opened, mac, mac_sub=None):
+        """log_open (runtime.cpp:112-117) of one opening's device arrays (tensors kept alive by the caller)."""
+        check(lib().spdz_mac_log_append(self.h, batch_id, opened.data_ptr(), mac.data_ptr(),
+                                        mac_sub.data_ptr() if mac_sub is not None else None, opened.numel()))
+
+    def mac_log_size(self) -> int:
+        n = C.c_uint64()
+        check(lib().spdz_mac_log_size(self.h, C.byref(n)))
+        return n.value
+
+    def mac_log_sigma(self, coin: int) -> int:
+        s = C.c_uint32()
+        check(lib().spdz_mac_log_sigma(self.h, coin, C.byref(s)))
+        return s.value
+
+    def mac_log_clear(self):
+        check(lib().spdz_mac_log_clear(self.h))
+
     def prepare_weights(self, w, dout: int, din: int) -> "LinearWeights":
         return LinearWeights(self, w, dout, din)
 
@@ -176,6 +203,32 @@ class Context:
         peers = (C.c_void_p * max(1, len(peer_payloads)))(*[p.data_ptr() for p in peer_payloads])
         check(lib().spdz_bmatrix_open_combine(self.h, C.byref(dbmtriple(t)), own_payload.data_ptr(), peers,
                                               len(peer_payloads), C.byref(dshare(z)), opened_out.data_ptr()))
+
+
+class DeviceEvent:
+    """A completion event on a context's stream (spdz_event_*): poll from a pump loop."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def done(self) -> bool:
+        d = C.c_int()
+        check(lib().spdz_event_query(self.h, C.byref(d)))
+        return bool(d.value)
+
+    def sync(self):
+        check(lib().spdz_event_sync(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().spdz_event_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- device tensors

@@ -933,4 +933,170 @@ int spdz_host_reduce_add(spdz_ctx* ctx, const uint32_t* xv, const uint32_t* xm, 
     });
 }
 
+// ---------------- device buffers and completion events ----------------
+int spdz_share_alloc(spdz_ctx* ctx, uint64_t lanes, spdz_share_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(out != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null share");
+        device_guard(ctx);
+        void *v = nullptr, *m = nullptr;
+        cuda_check(cudaMalloc(&v, std::max<uint64_t>(lanes, 1) * 4), "cudaMalloc(share)");
+        if (cudaMalloc(&m, std::max<uint64_t>(lanes, 1) * 4) != cudaSuccess) {
+            cudaFree(v);
+            throw Error(SPDZ_ERR_CUDA, "cudaMalloc(share): out of device memory");
+        }
+        *out = spdz_share_t{(uint32_t*)v, (uint32_t*)m, lanes};
+    });
+}
+
+int spdz_share_free(spdz_ctx* ctx, spdz_share_t* s) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!s) return;
+        device_guard(ctx);
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync before free");
+        if (s->vals) cudaFree(s->vals);
+        if (s->macs) cudaFree(s->macs);
+        *s = spdz_share_t{nullptr, nullptr, 0};
+    });
+}
+
+int spdz_share_upload(spdz_ctx* ctx, spdz_share_t* dst, const uint32_t* hv, const uint32_t* hm, uint64_t lanes) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_share(dst, "dst");
+        need(lanes <= dst->lanes && (lanes == 0 || (hv && hm)), SPDZ_ERR_INVALID_ARGUMENT, "bad upload");
+        device_guard(ctx);
+        cuda_check(cudaMemcpyAsync(dst->vals, hv, lanes * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D vals");
+        cuda_check(cudaMemcpyAsync(dst->macs, hm, lanes * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D macs");
+    });
+}
+
+int spdz_share_download(spdz_ctx* ctx, const spdz_share_t* src, uint32_t* hv, uint32_t* hm, uint64_t lanes) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_share(src, "src");
+        need(lanes <= src->lanes && (lanes == 0 || (hv && hm)), SPDZ_ERR_INVALID_ARGUMENT, "bad download");
+        device_guard(ctx);
+        cuda_check(cudaMemcpyAsync(hv, src->vals, lanes * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H vals");
+        cuda_check(cudaMemcpyAsync(hm, src->macs, lanes * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H macs");
+    });
+}
+
+}  // extern "C"
+
+struct spdz_event {
+    cudaEvent_t ev = nullptr;
+    int device = 0;
+};
+
+extern "C" {
+
+int spdz_event_record(spdz_ctx* ctx, spdz_event** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(out != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null event");
+        device_guard(ctx);
+        auto* e = new spdz_event;
+        e->device = ctx->device;
+        if (cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventRecord(e->ev, ctx->stream) != cudaSuccess) {
+            if (e->ev) cudaEventDestroy(e->ev);
+            delete e;
+            throw Error(SPDZ_ERR_CUDA, "event record failed");
+        }
+        *out = e;
+    });
+}
+
+int spdz_event_query(spdz_event* e, int* done) {
+    return guard([&] {
+        need(e != nullptr && done != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null event");
+        cudaSetDevice(e->device);
+        const cudaError_t r = cudaEventQuery(e->ev);
+        if (r == cudaErrorNotReady) {
+            cudaGetLastError();  // not an error: clear it
+            *done = 0;
+            return;
+        }
+        cuda_check(r, "cudaEventQuery");
+        *done = 1;
+    });
+}
+
+int spdz_event_sync(spdz_event* e) {
+    return guard([&] {
+        need(e != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null event");
+        cudaSetDevice(e->device);
+        cuda_check(cudaEventSynchronize(e->ev), "cudaEventSynchronize");
+    });
+}
+
+int spdz_event_wait(spdz_ctx* ctx, spdz_event* e) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(e != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null event");
+        device_guard(ctx);
+        cuda_check(cudaStreamWaitEvent(ctx->stream, e->ev, 0), "cudaStreamWaitEvent");
+    });
+}
+
+int spdz_event_destroy(spdz_event* e) {
+    if (!e) return SPDZ_OK;
+    cudaSetDevice(e->device);
+    cudaEventDestroy(e->ev);
+    delete e;
+    return SPDZ_OK;
+}
+
+// ---------------- caller-driven MAC log (runtime.cpp:112-117, 467-506) ----------------
+int spdz_mac_log_append(spdz_ctx* ctx, uint64_t batch_id, const uint32_t* dev_opened, const uint32_t* dev_mac,
+                        const uint32_t* dev_mac_sub, uint64_t len) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(len == 0 || (dev_opened && dev_mac), SPDZ_ERR_INVALID_ARGUMENT, "null log arrays");
+        if (!len) return;
+        std::lock_guard lk(ctx->maclog_mu);
+        uint64_t& lane0 = ctx->maclog_lanes[batch_id];  // log_open lanes continue within a batch
+        ctx->maclog.push_back({dev_opened, dev_mac, dev_mac_sub, len, 0, batch_id, lane0, 0});
+        lane0 += len;
+    });
+}
+
+int spdz_mac_log_size(spdz_ctx* ctx, uint64_t* n) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(n != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null out");
+        std::lock_guard lk(ctx->maclog_mu);
+        uint64_t k = 0;
+        for (auto& sg : ctx->maclog) k += sg.len;
+        *n = k;
+    });
+}
+
+int spdz_mac_log_sigma(spdz_ctx* ctx, uint64_t coin, uint32_t* sigma_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        need(sigma_out != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null sigma_out");
+        std::vector<spdz_mac_segment_t> segs;
+        {
+            std::lock_guard lk(ctx->maclog_mu);
+            segs = ctx->maclog;
+            for (auto& sg : segs) sg.batch_len = ctx->maclog_lanes[sg.batch_id];
+        }
+        assign_ranks(segs.data(), segs.size());
+        device_guard(ctx);
+        *sigma_out = segs.empty() ? 0u : mac_sigma_impl(ctx, segs.data(), segs.size(), coin);
+    });
+}
+
+int spdz_mac_log_clear(spdz_ctx* ctx) {
+    return guard([&] {
+        need_ctx(ctx);
+        std::lock_guard lk(ctx->maclog_mu);
+        ctx->maclog.clear();
+        ctx->maclog_lanes.clear();
+    });
+}
+
 }  // extern "C"

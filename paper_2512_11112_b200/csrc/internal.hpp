@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,6 +104,11 @@ struct spdz_ctx {
     spdzb200::DevBuf seg_buf;             // MAC segment + chunk tables
     spdzb200::DevBuf rank_buf;
     spdzb200::HostPinned pinned;
+    // caller-driven MAC log (spdz_mac_log_*, runtime.cpp:112-117): device segments, appended
+    // from any thread; per batch id the records logged so far (next lane0)
+    std::mutex maclog_mu;
+    std::vector<spdz_mac_segment_t> maclog;
+    std::map<uint64_t, uint64_t> maclog_lanes;
 };
 
 namespace spdzb200 {
