@@ -19,66 +19,80 @@ namespace spdzb200 {
 
 namespace {
 
-bool write_all(int fd, const void* data, size_t len) {
-    const char* p = static_cast<const char*>(data);
-    while (len) {
-        const ssize_t k = ::send(fd, p, len, MSG_NOSIGNAL);
-        if (k <= 0) {
-            if (k < 0 && errno == EINTR) continue;
+// Moves exactly `len` bytes over a stream socket in either direction; false when the
+// peer closed the connection or a hard error occurred (EINTR is retried).
+bool move_bytes(int fd, void* buf, size_t len, bool outbound) {
+    auto* cur = static_cast<char*>(buf);
+    for (size_t done = 0; done < len;) {
+        const ssize_t k = outbound ? ::send(fd, cur + done, len - done, MSG_NOSIGNAL)
+                                   : ::recv(fd, cur + done, len - done, MSG_WAITALL);
+        if (k > 0) {
+            done += (size_t)k;
+        } else if (k < 0 && errno == EINTR) {
+            continue;
+        } else {
             return false;
         }
-        p += k;
-        len -= (size_t)k;
     }
     return true;
 }
-
-bool read_all(int fd, void* data, size_t len) {
-    char* p = static_cast<char*>(data);
-    while (len) {
-        const ssize_t k = ::recv(fd, p, len, 0);
-        if (k <= 0) {
-            if (k < 0 && errno == EINTR) continue;
-            return false;
-        }
-        p += k;
-        len -= (size_t)k;
-    }
-    return true;
-}
+bool send_exact(int fd, const void* buf, size_t len) { return move_bytes(fd, const_cast<void*>(buf), len, true); }
+bool recv_exact(int fd, void* buf, size_t len) { return move_bytes(fd, buf, len, false); }
 
 uint32_t le32(const uint8_t* b) { return (uint32_t)b[0] | (uint32_t)b[1] << 8 | (uint32_t)b[2] << 16 | (uint32_t)b[3] << 24; }
 
-void split_endpoint(const std::string& ep, std::string& host, std::string& port) {
-    const auto colon = ep.rfind(':');
-    if (colon == std::string::npos)
-        throw Error(SPDZ_ERR_NET, "NetError: bad endpoint '" + ep + "', expected host:port");
-    host = ep.substr(0, colon);
-    port = ep.substr(colon + 1);
-}
+struct Endpoint {
+    std::string host, port;
+    explicit Endpoint(const std::string& ep) {
+        const auto colon = ep.rfind(':');
+        if (colon == std::string::npos)
+            throw Error(SPDZ_ERR_NET, "NetError: bad endpoint '" + ep + "', expected host:port");
+        host = ep.substr(0, colon);
+        port = ep.substr(colon + 1);
+    }
+};
 
-int dial(const std::string& host, const std::string& port, std::chrono::milliseconds timeout, int peer) {
-    addrinfo hints{};
-    hints.ai_family = AF_UNSPEC;
-    hints.ai_socktype = SOCK_STREAM;
-    const auto deadline = std::chrono::steady_clock::now() + timeout;
-    while (std::chrono::steady_clock::now() < deadline) {
-        addrinfo* res = nullptr;
-        if (getaddrinfo(host.c_str(), port.c_str(), &hints, &res) == 0) {
-            for (addrinfo* ai = res; ai; ai = ai->ai_next) {
-                const int fd = ::socket(ai->ai_family, ai->ai_socktype, ai->ai_protocol);
-                if (fd < 0) continue;
-                if (::connect(fd, ai->ai_addr, ai->ai_addrlen) == 0) {
-                    freeaddrinfo(res);
-                    return fd;
+// a connected socket to `ep`, retrying (the peer may not listen yet) until the deadline
+int connect_to(const Endpoint& ep, std::chrono::steady_clock::time_point deadline, int peer) {
+    addrinfo want{};
+    want.ai_family = AF_UNSPEC;
+    want.ai_socktype = SOCK_STREAM;
+    for (;;) {
+        addrinfo* list = nullptr;
+        int fd = -1;
+        if (::getaddrinfo(ep.host.c_str(), ep.port.c_str(), &want, &list) == 0) {
+            for (addrinfo* it = list; it && fd < 0; it = it->ai_next) {
+                fd = ::socket(it->ai_family, it->ai_socktype, it->ai_protocol);
+                if (fd >= 0 && ::connect(fd, it->ai_addr, it->ai_addrlen) != 0) {
+                    ::close(fd);
+                    fd = -1;
                 }
-                ::close(fd);
             }
-            freeaddrinfo(res);
+            ::freeaddrinfo(list);
         }
+        if (fd >= 0) return fd;
+        if (std::chrono::steady_clock::now() >= deadline)
+            throw Error(SPDZ_ERR_NET,
+                        "ConnectTimeout: peer " + std::to_string(peer) + " at " + ep.host + ":" + ep.port);
         std::this_thread::sleep_for(std::chrono::milliseconds(50));
     }
-    throw Error(SPDZ_ERR_NET, "ConnectTimeout: peer " + std::to_string(peer) + " at " + host + ":" + port);
+}
+
+// listening socket on every interface at `port`
+int listen_on(const std::string& port, int backlog) {
+    const int fd = ::socket(AF_INET, SOCK_STREAM, 0);
+    need(fd >= 0, SPDZ_ERR_NET, "NetError: socket() failed");
+    const int on = 1;
+    ::setsockopt(fd, SOL_SOCKET, SO_REUSEADDR, &on, sizeof on);
+    sockaddr_in any{};
+    any.sin_family = AF_INET;
+    any.sin_port = htons((uint16_t)std::stoi(port));
+    any.sin_addr.s_addr = htonl(INADDR_ANY);
+    if (::bind(fd, reinterpret_cast<const sockaddr*>(&any), sizeof any) != 0 || ::listen(fd, backlog) != 0) {
+        ::close(fd);
+        throw Error(SPDZ_ERR_NET, "NetError: bind failed on port " + port);
+    }
+    return fd;
 }
 
 }  // namespace
@@ -106,7 +120,7 @@ void NetLink::send(int peer, uint8_t type, uint64_t batch, const uint32_t* words
     encode_header(buf.data(), type, lanes, batch);
     if (lanes) std::memcpy(buf.data() + kFrameHeader, words, 4ull * lanes);
     std::lock_guard lk(send_mu[peer]);
-    if (!write_all(fds[peer], buf.data(), buf.size()))
+    if (!send_exact(fds[peer], buf.data(), buf.size()))
         throw Error(SPDZ_ERR_PEER_TIMEOUT, "PeerTimeout: send to peer " + std::to_string(peer) + " failed");
     bytes_sent += buf.size();
 }
@@ -156,7 +170,7 @@ void NetLink::reader_loop(int peer) {
     };
     for (;;) {
         uint8_t hdr[kFrameHeader];
-        if (!read_all(fd, hdr, sizeof hdr)) return stop("PeerTimeout: connection to peer " + std::to_string(peer) +
+        if (!recv_exact(fd, hdr, sizeof hdr)) return stop("PeerTimeout: connection to peer " + std::to_string(peer) +
                                                         " closed");
         if (hdr[0] > kMsgControl)  // decode_header (net.cpp:21-29)
             return stop("MalformedShareMessage: unknown msg-type " + std::to_string(hdr[0]));
@@ -164,7 +178,7 @@ void NetLink::reader_loop(int peer) {
         uint64_t batch = 0;
         for (int i = 0; i < 8; ++i) batch |= uint64_t(hdr[8 + i]) << (8 * i);
         std::vector<uint32_t> payload(lanes);
-        if (lanes && !read_all(fd, payload.data(), 4ull * lanes))
+        if (lanes && !recv_exact(fd, payload.data(), 4ull * lanes))
             return stop("PeerTimeout: connection to peer " + std::to_string(peer) + " closed mid-frame");
         if (stopping) return;
         bytes_received += kFrameHeader + 4ull * lanes;
@@ -191,73 +205,49 @@ NetLink* connect_mesh(int party, const std::vector<std::string>& endpoints, std:
     need(party >= 0 && party < n, SPDZ_ERR_NET, "NetError: party index out of range");
     auto link = std::make_unique<NetLink>(party, n);
     link->io_timeout = io_timeout;
-    if (n == 1) return link.release();
-    int listen_fd = -1;
-    if (party < n - 1) {  // listen for higher indices
-        std::string host, port;
-        split_endpoint(endpoints[party], host, port);
-        listen_fd = ::socket(AF_INET, SOCK_STREAM, 0);
-        need(listen_fd >= 0, SPDZ_ERR_NET, "NetError: socket() failed");
-        int one = 1;
-        ::setsockopt(listen_fd, SOL_SOCKET, SO_REUSEADDR, &one, sizeof one);
-        sockaddr_in addr{};
-        addr.sin_family = AF_INET;
-        addr.sin_addr.s_addr = htonl(INADDR_ANY);
-        addr.sin_port = htons((uint16_t)std::stoi(port));
-        if (::bind(listen_fd, reinterpret_cast<sockaddr*>(&addr), sizeof addr) != 0) {
-            ::close(listen_fd);
-            throw Error(SPDZ_ERR_NET, "NetError: bind failed on port " + port);
-        }
-        ::listen(listen_fd, n);
-    }
-    auto attach = [&](int peer, int fd) {
-        int one = 1;
-        ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof one);
+    const auto deadline = std::chrono::steady_clock::now() + connect_timeout;
+    auto adopt = [&](int peer, int fd) {
+        const int on = 1;
+        ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &on, sizeof on);
         link->fds[peer] = fd;
     };
-    try {
-        for (int p = 0; p < party; ++p) {  // dial lower indices, announcing our own
-            std::string host, port;
-            split_endpoint(endpoints[p], host, port);
-            const int fd = dial(host, port, connect_timeout, p);
-            uint8_t idx[4];
-            for (int i = 0; i < 4; ++i) idx[i] = uint8_t((uint32_t)party >> (8 * i));
-            if (!write_all(fd, idx, 4)) {
-                ::close(fd);
-                throw Error(SPDZ_ERR_NET, "ConnectTimeout: handshake with peer " + std::to_string(p));
-            }
-            attach(p, fd);
+    // parties above us connect to our endpoint; we connect to every party below us
+    struct Listener {
+        int fd = -1;
+        ~Listener() {
+            if (fd >= 0) ::close(fd);
         }
-        const int expected = n - 1 - party;
-        const auto deadline = std::chrono::steady_clock::now() + connect_timeout;
-        std::vector<bool> have(n, false);
-        for (int got = 0; got < expected;) {
-            pollfd pfd{listen_fd, POLLIN, 0};
-            const auto left =
-                std::chrono::duration_cast<std::chrono::milliseconds>(deadline - std::chrono::steady_clock::now());
-            if (left.count() <= 0 || ::poll(&pfd, 1, (int)left.count()) <= 0)
-                throw Error(SPDZ_ERR_NET, "ConnectTimeout: waiting for " + std::to_string(expected - got) + " peer(s)");
-            const int fd = ::accept(listen_fd, nullptr, nullptr);
-            if (fd < 0) continue;
-            uint8_t b[4];
-            if (!read_all(fd, b, 4)) {
-                ::close(fd);
-                continue;
-            }
-            const uint32_t idx = le32(b);
-            if (idx >= (uint32_t)n || (int)idx <= party || have[idx]) {
-                ::close(fd);
-                throw Error(SPDZ_ERR_NET, "IndexCollision: peer announced invalid index " + std::to_string(idx));
-            }
-            have[idx] = true;
-            attach((int)idx, fd);
-            ++got;
+    } lst;
+    if (party + 1 < n) lst.fd = listen_on(Endpoint(endpoints[party]).port, n);
+    for (int lower = 0; lower < party; ++lower) {
+        const int fd = connect_to(Endpoint(endpoints[lower]), deadline, lower);
+        uint8_t me[4] = {uint8_t(party), uint8_t(party >> 8), uint8_t(party >> 16), uint8_t(party >> 24)};
+        if (!send_exact(fd, me, sizeof me)) {  // the index announcement of the handshake
+            ::close(fd);
+            throw Error(SPDZ_ERR_NET, "ConnectTimeout: handshake with peer " + std::to_string(lower));
         }
-    } catch (...) {
-        if (listen_fd >= 0) ::close(listen_fd);
-        throw;
+        adopt(lower, fd);
     }
-    if (listen_fd >= 0) ::close(listen_fd);
+    for (int pending = n - 1 - party; pending > 0;) {
+        const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(deadline - std::chrono::steady_clock::now());
+        pollfd w{lst.fd, POLLIN, 0};
+        if (ms.count() <= 0 || ::poll(&w, 1, (int)ms.count()) <= 0)
+            throw Error(SPDZ_ERR_NET, "ConnectTimeout: waiting for " + std::to_string(pending) + " peer(s)");
+        const int fd = ::accept(lst.fd, nullptr, nullptr);
+        uint8_t who[4];
+        if (fd < 0) continue;
+        if (!recv_exact(fd, who, sizeof who)) {
+            ::close(fd);
+            continue;
+        }
+        const uint32_t idx = le32(who);
+        if (idx >= (uint32_t)n || (int)idx <= party || link->fds[idx] >= 0) {
+            ::close(fd);
+            throw Error(SPDZ_ERR_NET, "IndexCollision: peer announced invalid index " + std::to_string(idx));
+        }
+        adopt((int)idx, fd);
+        --pending;
+    }
     link->start_readers();
     return link.release();
 }
