@@ -1150,7 +1150,10 @@ struct Exec {
                  "runtime: block " + std::to_string(label) + " is not a block label");
             // phi choices first, as enter_block_locked seeds them
             std::vector<std::pair<uint32_t, uint32_t>> phis;
+            uint32_t steps = 0;
             for (uint32_t u = r->nodes[label].next; u != SPDZ_NO_NODE; u = r->nodes.at(u).next) {
+                need(++steps <= N, SPDZ_ERR_INVALID_ARGUMENT, "runtime: block " + std::to_string(label) +
+                                                                  "'s node chain does not end");
                 const auto& n = r->nodes.at(u);
                 if (n.kind != SPDZ_NODE_PHI) continue;
                 if (pred == SPDZ_NO_NODE)
