@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "field.cuh"
 #include "kernels.cuh"
@@ -1228,7 +1229,11 @@ cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms) {
     bool v4 = a.din % 4 == 0 && aligned16(a.D0) && aligned16(a.D1) && aligned16(a.opened);
     for (int p = 0; p < 2; ++p)
         v4 = v4 && aligned16(a.A[p][0]) && aligned16(a.A[p][1]) && aligned16(a.B[p][0]) && aligned16(a.B[p][1]);
-    const bool warp_rows = a.rows >= (uint32_t)sms * 8;  // enough rows to fill the GPU one warp each
+    static const int force_g = [] {  // SPDZ_MC2_G=32|256: override the row-group choice (experiments)
+        const char* e = std::getenv("SPDZ_MC2_G");
+        return e ? std::atoi(e) : 0;
+    }();
+    const bool warp_rows = force_g ? force_g == 32 : a.rows >= (uint32_t)sms * 8;  // a warp per row fills the GPU
     if (warp_rows) {
         const uint32_t blocks = (a.rows + kThreads / 32 - 1) / (kThreads / 32);
         const int grid = (int)(blocks < (uint32_t)sms * 8 ? blocks : (uint32_t)sms * 8);
