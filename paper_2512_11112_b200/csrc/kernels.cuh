@@ -21,7 +21,7 @@ struct MacSegT {
     uint64_t j0;
 };
 constexpr uint32_t kSigmaAlign = 1024;     // CTA record ranges start at multiples of this
-constexpr int kMacTableSegs = 48;          // segments per launch (kernel parameter table)
+constexpr int kMacTableSegs = 384;         // segments per launch (kernel parameter table, < 32 KB for NP = 2)
 template <int NP>
 struct MacTableT {
     uint32_t n;                            // segments in this table
