@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -18,6 +19,8 @@
 #include <random>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "field.cuh"
 #include "internal.hpp"
@@ -29,6 +32,37 @@ using namespace spdzb200;
 namespace spdzb200 {
 NetLink* net_link(spdz_net* net);  // net.cpp
 }
+
+namespace {
+// NVTX ranges per executed node, root open and MAC check (SURVEY §5 tracing plan), on when
+// SPDZ_NVTX=1 so that an nsys / ncu timeline names the online phase's steps
+bool nvtx_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPDZ_NVTX");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct NvtxRange {
+    bool active;
+    NvtxRange(const char* what, long a = -1, long b = -1) : active(nvtx_on()) {
+        if (!active) return;
+        char msg[96];
+        if (a < 0) std::snprintf(msg, sizeof msg, "%s", what);
+        else if (b < 0) std::snprintf(msg, sizeof msg, "%s %ld", what, a);
+        else std::snprintf(msg, sizeof msg, "%s node %ld exec %ld", what, a, b);
+        nvtxRangePushA(msg);
+    }
+    ~NvtxRange() {
+        if (active) nvtxRangePop();
+    }
+};
+const char* kind_label(int k) {
+    static const char* names[] = {"input", "const", "add", "sub", "mul", "reduce_add", "reduce_mul", "linear",
+                                  "root", "load", "nop", "cmp_public", "phi", "branch", "label"};
+    return k >= 0 && k < (int)(sizeof names / sizeof names[0]) ? names[k] : "node";
+}
+}  // namespace
 
 namespace {
 
@@ -1636,6 +1670,7 @@ struct Exec {
 
     // runtime.cpp:360-450, one execution of node `id`
     void exec_node(uint32_t id, uint64_t exec) {
+        NvtxRange range(kind_label(r->nodes[id].kind), (long)id, (long)exec);
         if (r->cfg && exec_dynamic_public(id)) return;
         {
             const auto& n = r->nodes[id];
@@ -1716,6 +1751,7 @@ struct Exec {
 
     // runtime.cpp:551-560 open the root (batch make_batch(root, 1, 1))
     void open_root() {
+        NvtxRange range("open root");
         const Val& rv0 = r->parties[r->ref_party()].ns[r->root].out;
         const uint64_t L = rv0.lanes;
         if (rv0.is_public) {
@@ -1802,6 +1838,7 @@ bool mac_fusable(spdz_run* r) {
 }
 
 void mac_launch(spdz_run* r, uint64_t coin) {
+    NvtxRange range("mac check sigma");
     for (int p = 0; p < r->n; ++p)
         if (r->parties[p].local) assign_ranks(r->parties[p].maclog.data(), r->parties[p].maclog.size());
     if (mac_fusable(r)) {
