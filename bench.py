@@ -287,8 +287,9 @@ def run_ours(args, world, rank, local):
         # PCIe transfers of one chunk overlap the kernels of another (StreamedRun)
         from paper_2512_11112_b200 import StreamedRun
         run.close()
-        run = StreamedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=args.e2e_chunks,
-                          devices=[dev, dev])
+        wts = [float(x) for x in args.e2e_weights.split(",")] if args.e2e_weights else None
+        run = StreamedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=len(wts) if wts else args.e2e_chunks,
+                          devices=[dev, dev], weights=wts)
         run.bind_output(out_pin)
     if streamed:  # untimed warm-up (first call captures each chunk's CUDA graph)
         for w in range(max(args.warmup, 1)):
@@ -387,6 +388,8 @@ def main():
     ap.add_argument("--exchange-chunks", type=int, default=2,
                     help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run (1 = serial)")
+    ap.add_argument("--e2e-weights", default="", help="relative lane-chunk sizes of the host-streamed e2e run "
+                    "(comma-separated; overrides --e2e-chunks)")
     args = ap.parse_args()
     if args.impl == "reference":  # CPU only: rank 0 runs it, no process group is needed
         run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
