@@ -1783,7 +1783,7 @@ struct Exec {
                 if (q == p) continue;
                 if (netpeer(q)) net_recv(p, q, kMsgOpenShares, batch, r->parties[q].ns[r->root].out.v, L);
                 else await(p, q, ready[q], slot_of(r->root, 0));
-                peers[k++] = r->parties[q].ns[r->root].out.v;
+                peers[k++] = peer_payload(p, q, r->root, r->parties[q].ns[r->root].out.v, L, P.ns[r->root].shadow);
                 r->exchanged += L * 4;
             }
             const int tk = tbegin(p);
@@ -2668,10 +2668,11 @@ int spdz_run_inject_bitflip(spdz_run* r, uint32_t node, int sender, int receiver
         need(sender >= 0 && sender < r->n && receiver >= 0 && receiver < r->n && sender != receiver,
              SPDZ_ERR_INVALID_ARGUMENT, "bad sender/receiver");
         auto& st = r->parties[receiver].ns[node];
-        need(st.payload != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "node has no opening to tamper with");
+        const bool root = node == r->root && !st.out.is_public;  // the root open (runtime.cpp:555-558)
+        need(st.payload != nullptr || root, SPDZ_ERR_INVALID_ARGUMENT, "node has no opening to tamper with");
         if (!st.shadow) {
             const auto& n = r->node(node);
-            uint64_t words = 2ull * n.lanes;
+            uint64_t words = root ? st.out.lanes : 2ull * n.lanes;
             if (n.kind == SPDZ_NODE_LINEAR)
                 words = (uint64_t)n.din * n.dout + (uint64_t)n.din * r->tiles[node].starts.size();
             st.shadow = r->alloc(receiver, words);

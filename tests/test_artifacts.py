@@ -366,3 +366,34 @@ def test_same_seed_same_transcript(gpu):
     b = rt.run_local(g, 3, vals, dealer_seed=77)
     assert a.output_digest == b.output_digest and a.outputs.tolist() == exp["outputs"]
     assert a.matrix_triples_consumed == b.matrix_triples_consumed == 1
+
+
+@pytest.mark.gpu
+def test_acceptance_c3_tamper(gpu):
+    """acceptance.cpp:112-140 on B200: straight_line, 100 runs each with one bit flipped in the
+    (i % 3)-th opened frame (Beaver 1, Beaver 2, root open) as receiver i % 2 sees it ->
+    100/100 MacCheckFailed; 100 honest runs with fresh dealer seeds -> 0 aborts."""
+    circ = BUNDLES / "straight_line" / "circuit.mpcg"
+    vals = {"x": np.array([1234, 5678, 91011], np.uint32), "k": np.array([13], np.uint32)}
+    g = A.read_circuit_file(circ).to_graph(vals)
+    opened = [i for i, n in enumerate(g.nodes) if n.kind == rt.MUL] + [g.root]
+    assert len(opened) == 3
+    aborts = 0
+    for i in range(100):
+        r = rt.LocalRun(g, 2, dealer_seed=1000 + i)
+        try:
+            receiver = i % 2
+            r.inject_bitflip(opened[i % 3], 1 - receiver, receiver, 0, i % 32)
+            r.bind_inputs(vals)
+            r.share_inputs()
+            r.online()
+        except errors.MacCheckFailed:
+            aborts += 1
+        finally:
+            r.close()
+    assert aborts == 100
+    want = ref.interpret_circuit(circ, vals).tolist() if HAS_REF else None
+    for i in range(100):
+        rep = rt.run_local(g, 2, vals, dealer_seed=2000 + i)
+        if want is not None:
+            assert rep.outputs.tolist() == want
