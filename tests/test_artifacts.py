@@ -397,3 +397,18 @@ def test_acceptance_c3_tamper(gpu):
         rep = rt.run_local(g, 2, vals, dealer_seed=2000 + i)
         if want is not None:
             assert rep.outputs.tolist() == want
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAS_REF, reason="oracle/_ref not built")
+def test_acceptance_c8_c9_linear(gpu):
+    """acceptance.cpp:295-331 (slice 640 over 64x32: 4 tiles, 4 matrix triples) and :333-346
+    (2..6 parties agree with the interpreter)."""
+    circ, _, inp, exp = files("linear_64x32")
+    vals = A.read_input_file(inp)
+    g = A.read_circuit_file(circ).to_graph(vals)
+    want = ref.interpret_circuit(circ, vals).tolist()
+    rep = rt.run_local(g, 2, vals, slice_=640, dealer_seed=31)
+    assert rep.outputs.tolist() == want and rep.matrix_triples_consumed == 4
+    for n in range(2, 7):
+        assert rt.run_local(g, n, vals).outputs.tolist() == want, n

@@ -135,3 +135,32 @@ def test_connect_timeout():
     eps = free_ports(2)
     with pytest.raises(errors.NetError, match="ConnectTimeout"):
         Mesh(1, eps, connect_timeout_ms=300)
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_b200_mesh_frame_counts(n):
+    """acceptance.cpp:348-366 with every party a B200 mesh endpoint: a one-lane open moves
+    exactly one 20-byte frame to and from each of the n-1 peers."""
+    eps = free_ports(n)
+    got = [None] * n
+
+    def party(i):
+        m = Mesh(i, eps, connect_timeout_ms=20000, io_timeout_ms=20000)
+        for q in range(n):
+            if q != i:
+                m.send(q, OPEN_SHARES, 1, [i])
+        total = i
+        for q in range(n):
+            if q != i:
+                total += int(m.recv(q, OPEN_SHARES, 1)[0])
+        got[i] = (total, m.stats())
+        m.close()
+
+    th = [threading.Thread(target=party, args=(i,)) for i in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(60)
+    for total, (sent, received) in got:
+        assert total == n * (n - 1) // 2
+        assert sent == received == (n - 1) * 20
