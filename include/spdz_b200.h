@@ -360,12 +360,15 @@ typedef enum spdz_node_kind {
 
 #define SPDZ_NO_NODE 0xFFFFFFFFu
 
+#define SPDZ_MAX_OPERANDS 8
+
 typedef struct spdz_node {
     int32_t kind;
     int32_t is_private;   /* privacy tag (graph_builder.cpp:495) */
     uint32_t lanes;       /* lane count of the node's value */
     uint32_t n_operands;
-    uint32_t operands[3]; /* node ids (ids are the index in the node array) */
+    uint32_t operands[SPDZ_MAX_OPERANDS]; /* node ids (the index in the node array); a PHI has one per
+                                             incoming edge, other nodes at most 3 */
     uint32_t din, dout;   /* LINEAR only */
     uint32_t const_val;   /* CONST only (scalar broadcast) */
     /* control flow (ignored by straight-line graphs) */
@@ -374,7 +377,7 @@ typedef struct spdz_node {
                              (preproc.cpp:124-163) */
     uint32_t n_succ;      /* BRANCH */
     uint32_t succ[2];
-    uint32_t phi_labels[3]; /* PHI: predecessor block of each operand */
+    uint32_t phi_labels[SPDZ_MAX_OPERANDS]; /* PHI: predecessor block of each operand */
 } spdz_node_t;
 
 typedef struct spdz_run_options {

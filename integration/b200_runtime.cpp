@@ -98,11 +98,12 @@ Lowered lower(const circuit::CircuitGraph& g, const preproc::Inputs& inputs) {
         o.kind = kind_of(n.kind);
         o.is_private = n.is_private;
         o.lanes = n.lanes;
-        if (n.operands.size() > 3 || n.successors.size() > 2)
+        if (n.operands.size() > (n.kind == circuit::NodeKind::Phi ? size_t(SPDZ_MAX_OPERANDS) : size_t(3)) ||
+            n.successors.size() > 2)
             throw std::runtime_error("UnsupportedCircuit: node " + std::to_string(n.id) + " has too many edges");
         o.n_operands = (uint32_t)n.operands.size();
         for (size_t k = 0; k < n.operands.size(); ++k) o.operands[k] = n.operands[k];
-        for (size_t k = 0; k < n.phi_labels.size() && k < 3; ++k) o.phi_labels[k] = n.phi_labels[k];
+        for (size_t k = 0; k < n.phi_labels.size() && k < SPDZ_MAX_OPERANDS; ++k) o.phi_labels[k] = n.phi_labels[k];
         o.n_succ = (uint32_t)n.successors.size();
         for (size_t k = 0; k < n.successors.size(); ++k) o.succ[k] = n.successors[k];
         o.din = n.din;

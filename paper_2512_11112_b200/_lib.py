@@ -15,6 +15,7 @@ import os as _os
 # SPDZ_B200_LIB: alternate build of the same library (reduction-variant experiments only)
 LIB_PATH = Path(_os.environ.get("SPDZ_B200_LIB") or str(Path(__file__).resolve().parent / "libspdz_b200.so"))
 MAX_PARTIES = 8
+MAX_OPERANDS = 8  # SPDZ_MAX_OPERANDS
 
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
@@ -55,9 +56,9 @@ class MacSegment(C.Structure):  # spdz_mac_segment_t
 
 class Node(C.Structure):  # spdz_node_t
     _fields_ = [("kind", C.c_int32), ("is_private", C.c_int32), ("lanes", C.c_uint32), ("n_operands", C.c_uint32),
-                ("operands", C.c_uint32 * 3), ("din", C.c_uint32), ("dout", C.c_uint32),
+                ("operands", C.c_uint32 * MAX_OPERANDS), ("din", C.c_uint32), ("dout", C.c_uint32),
                 ("const_val", C.c_uint32), ("next", C.c_uint32), ("loop_depth", C.c_uint32), ("n_succ", C.c_uint32),
-                ("succ", C.c_uint32 * 2), ("phi_labels", C.c_uint32 * 3)]
+                ("succ", C.c_uint32 * 2), ("phi_labels", C.c_uint32 * MAX_OPERANDS)]
 
 
 class RunOptions(C.Structure):  # spdz_run_options_t

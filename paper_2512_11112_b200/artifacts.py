@@ -28,6 +28,7 @@ from .runtime import (ADD, BRANCH, CMP_PUBLIC, CONST, INPUT, LABEL, LINEAR, LOAD
                       REDUCE_MUL, ROOT, SUB, Graph, LocalRun, NodeSpec, RunReport, store_info, triple_layout)
 
 P = 4294967291
+MAX_OPERANDS = 8  # SPDZ_MAX_OPERANDS: incoming edges of a phi
 
 # circuit.hpp:18-25, in enum order (the u8 written by serialize_circuit)
 REF_KINDS = ("Input", "Const", "Adder", "Multiplier", "Subtract", "AddBatch", "MultBatch", "SubBatch", "ReduceAdd",
@@ -51,7 +52,7 @@ class ShapeMismatch(InvalidArgument):
 
 class UnsupportedCircuit(InvalidArgument):
     """The circuit needs something this executor does not run (provisional Raw* nodes, phis
-    of more than 3 edges, operands later than the node)."""
+    of more than 8 incoming edges, operands later than the node)."""
 
 
 # ---------------------------------------------------------------- MPCG circuit files
@@ -119,7 +120,7 @@ class CircuitFile:
             kind = _TO_NODE[n.kind]
             if kind != PHI and any(o >= n.id for o in n.operands):
                 raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} reads a later node")
-            if len(n.operands) > 3 or len(n.successors) > 2:
+            if len(n.operands) > (MAX_OPERANDS if kind == PHI else 3) or len(n.successors) > 2:
                 raise UnsupportedCircuit(f"UnsupportedCircuit: node {n.id} has {len(n.operands)} operands")
             loop_depth = depth.get(n.block, 0) if n.block != NO_NODE else 0
             spec = NodeSpec(kind, n.lanes, tuple(n.operands), n.is_private, din=n.din, dout=n.dout, next=n.next,

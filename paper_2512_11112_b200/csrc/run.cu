@@ -2183,7 +2183,8 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
             if (nodes[id].kind == SPDZ_NODE_PHI || nodes[id].kind == SPDZ_NODE_BRANCH) r->cfg = true;
         for (uint32_t id = 0; id < n_nodes; ++id) {
             const auto& nd = nodes[id];
-            need(nd.n_operands <= 3, SPDZ_ERR_INVALID_ARGUMENT, "at most 3 operands per node");
+            need(nd.n_operands <= (nd.kind == SPDZ_NODE_PHI ? SPDZ_MAX_OPERANDS : 3u), SPDZ_ERR_INVALID_ARGUMENT,
+                 "too many operands (phis take up to SPDZ_MAX_OPERANDS incoming edges, other nodes 3)");
             for (uint32_t k = 0; k < nd.n_operands; ++k)  // a phi may read a later node (loop back edge)
                 need(nd.kind == SPDZ_NODE_PHI ? nd.operands[k] < n_nodes : nd.operands[k] < id,
                      SPDZ_ERR_INVALID_ARGUMENT, "graph must be topologically ordered (operand id < node id)");

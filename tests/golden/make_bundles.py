@@ -108,6 +108,41 @@ declare i32 @llvm.vector.reduce.mul.v9i32(<9 x i32>)
 """ + workloads._DECL
 
 
+# a four-way join: one phi with four incoming edges (nested public branches)
+PHI4_IR = workloads._HDR + """define i32 @main(ptr %x, i32 %k) {
+entry:
+""" + workloads._ann("x", True) + """  %a = load i32, ptr %x
+  %p1 = getelementptr inbounds i32, ptr %x, i64 1
+  %b = load i32, ptr %p1
+  %c1 = icmp sgt i32 %k, 10
+  br i1 %c1, label %hi, label %lo
+hi:
+  %c2 = icmp sgt i32 %k, 20
+  br i1 %c2, label %vhi, label %mhi
+vhi:
+  %r1 = mul i32 %a, %b
+  br label %join
+mhi:
+  %r2 = add i32 %a, %b
+  br label %join
+lo:
+  %c3 = icmp sgt i32 %k, 5
+  br i1 %c3, label %mlo, label %vlo
+mlo:
+  %r3 = sub i32 %a, %b
+  br label %join
+vlo:
+  %t = mul i32 %a, %a
+  %r4 = mul i32 %t, %b
+  br label %join
+join:
+  %r = phi i32 [ %r1, %vhi ], [ %r2, %mhi ], [ %r3, %mlo ], [ %r4, %vlo ]
+  ret i32 %r
+}
+
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
@@ -141,6 +176,8 @@ def cases():
         "linear_loop": (LINEAR_LOOP_IR, 2, 64, 18, {"x": rnd(16, 24), "W": rnd(192, 25), "b": rnd(12, 26),
                                                     "n": np.array([3], np.uint32)}, 4),
         "reduce_mul_loop": (REDUCE_LOOP_IR, 3, 262140, 19, {"x": rnd(9, 27), "n": np.array([4], np.uint32)}, 5),
+        "phi4_vhi": (PHI4_IR, 2, 262140, 20, {"x": rnd(2, 28), "k": np.array([25], np.uint32)}),
+        "phi4_vlo": (PHI4_IR, 3, 262140, 21, {"x": rnd(2, 29), "k": np.array([1], np.uint32)}),
     }
 
 
