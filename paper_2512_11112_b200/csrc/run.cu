@@ -1754,6 +1754,18 @@ struct Exec {
         NvtxRange range("open root");
         const Val& rv0 = r->parties[r->ref_party()].ns[r->root].out;
         const uint64_t L = rv0.lanes;
+        // control flow: a private-typed root holding a public value is public at run time —
+        // the reference returns it without an opening or a MAC record (runtime.cpp:553-555)
+        const uint32_t src = r->nodes[r->root].n_operands ? r->nodes[r->root].operands[0] : r->root;
+        if (r->cfg && !rv0.is_public && r->rt_pub[src]) {
+            for (int p = 0; p < r->n; ++p) {
+                if (!r->parties[p].local) continue;
+                dev(r, p);
+                lk(cudaMemcpyAsync(r->parties[p].outputs, pub_of(p, src), L * 4, cudaMemcpyDeviceToDevice, S(r, p)),
+                   "copy out");
+            }
+            return;
+        }
         if (rv0.is_public) {
             for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;

@@ -143,6 +143,27 @@ join:
 """ + workloads._DECL
 
 
+# a private phi that takes a public incoming value: the root is public at run time (no opening)
+PHI_PUBLIC_ROOT_IR = workloads._HDR + """define i32 @main(ptr %x, i32 %k) {
+entry:
+""" + workloads._ann("x", True) + """  %a = load i32, ptr %x
+  %c = icmp sgt i32 %k, 10
+  br i1 %c, label %sec, label %pub
+sec:
+  %s = mul i32 %a, %a
+  br label %join
+pub:
+  %q = add i32 %k, 7
+  br label %join
+join:
+  %r = phi i32 [ %s, %sec ], [ %q, %pub ]
+  %t = mul i32 %r, %r
+  ret i32 %t
+}
+
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
@@ -178,6 +199,8 @@ def cases():
         "reduce_mul_loop": (REDUCE_LOOP_IR, 3, 262140, 19, {"x": rnd(9, 27), "n": np.array([4], np.uint32)}, 5),
         "phi4_vhi": (PHI4_IR, 2, 262140, 20, {"x": rnd(2, 28), "k": np.array([25], np.uint32)}),
         "phi4_vlo": (PHI4_IR, 3, 262140, 21, {"x": rnd(2, 29), "k": np.array([1], np.uint32)}),
+        "phi_public_root": (PHI_PUBLIC_ROOT_IR, 2, 262140, 22, {"x": rnd(1, 30), "k": np.array([3], np.uint32)}),
+        "phi_secret_root": (PHI_PUBLIC_ROOT_IR, 2, 262140, 23, {"x": rnd(1, 31), "k": np.array([30], np.uint32)}),
     }
 
 
