@@ -575,10 +575,18 @@ void plan_buffers(spdz_run* r) {
                 default:
                     throw Error(SPDZ_ERR_INVALID_ARGUMENT, "runtime: unexpected node kind " + std::to_string(n.kind));
             }
-            // control flow: private-typed add/sub/mul/phi may hold a public value at run time
-            if (r->cfg && !st.out.is_public && !st.shadow_pub &&
-                (n.kind == SPDZ_NODE_ADD || n.kind == SPDZ_NODE_SUB || n.kind == SPDZ_NODE_MUL || n.kind == SPDZ_NODE_PHI))
-                st.shadow_pub = r->alloc(p, L);
+            // control flow: private-typed add/sub/mul/phi/reductions may hold a public value at run
+            // time; a load's public value is a view of its base's (a copy for a run-time start)
+            if (r->cfg && !st.out.is_public && !st.shadow_pub) {
+                if (n.kind == SPDZ_NODE_ADD || n.kind == SPDZ_NODE_SUB || n.kind == SPDZ_NODE_MUL ||
+                    n.kind == SPDZ_NODE_PHI || n.kind == SPDZ_NODE_REDUCE_ADD)
+                    st.shadow_pub = r->alloc(p, L);
+                else if (n.kind == SPDZ_NODE_REDUCE_MUL)  // product-tree scratch over the operand's lanes
+                    st.shadow_pub = r->alloc(p, std::max<uint64_t>(opnd(0).lanes, 1));
+                else if (n.kind == SPDZ_NODE_LOAD && P.ns[n.operands[0]].shadow_pub)
+                    st.shadow_pub = st.dyn_load ? r->alloc(p, L)
+                                                : P.ns[n.operands[0]].shadow_pub + const_of(r, n.operands[1]);
+            }
         }
         const Val& rv = P.ns[r->root].out;
         P.outputs = r->alloc(p, std::max<uint64_t>(rv.lanes, 1));
@@ -1122,14 +1130,76 @@ struct Exec {
         return st.out.is_public ? st.out.pub : st.shadow_pub;
     }
 
+    // load / reduce_add / reduce_mul of a private-typed value that is public at run time:
+    // computed publicly (a reduce_mul needs no product tree), its sharing beside it
+    bool exec_dynamic_unary(uint32_t id) {
+        const auto& n = r->nodes[id];
+        const uint32_t src = n.operands[0];
+        r->rt_pub[id] = 0;
+        if (!r->rt_pub[src] || r->parties[r->ref_party()].ns[src].out.is_public) return false;
+        if (n.kind == SPDZ_NODE_LOAD) {  // the share view (or copy) plus the public value's
+            exec_node_static_load(id);
+            r->rt_pub[id] = 1;
+            return true;
+        }
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            if (!P.local) continue;
+            auto& st = P.ns[id];
+            const Val& a = P.ns[src].out;
+            spdz_ctx* c = P.ctx;
+            dev(r, p);
+            const uint32_t* k = pub_of(p, src);
+            if (n.kind == SPDZ_NODE_REDUCE_ADD) {
+                lk(cudaMemsetAsync(c->d_acc + 2, 0, 16, c->stream), "memset");
+                lk(launch_reduce_add(c->stream, k, k, a.lanes, c->d_acc + 2, c->sms), "dyn reduce");
+                lk(launch_finish_reduce(c->stream, c->d_acc + 2, st.shadow_pub, st.shadow_pub), "finish");
+            } else {  // product of the lanes, folded in halves (order-free)
+                uint64_t len = a.lanes;
+                lk(cudaMemcpyAsync(st.shadow_pub, k, len * 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
+                while (len > 1) {
+                    const uint64_t half = len / 2;
+                    lk(launch_pub_binop(c->stream, 2, st.shadow_pub, false, st.shadow_pub + (len - half), false,
+                                        st.shadow_pub, half, c->sms),
+                       "dyn product");
+                    len -= half;
+                }
+            }
+            lk(launch_public(c->stream, 4, nullptr, nullptr, st.shadow_pub, false, 0u, false, c->party, c->alpha,
+                             st.out.v, st.out.m, 1, c->sms, c->d_alpha),
+               "dyn share_of_public");
+        }
+        r->rt_pub[id] = 1;
+        return true;
+    }
+
+    // a load's usual execution (a view needs nothing; a run-time start copies), plus the public
+    // value's slice when its base is public at run time
+    void exec_node_static_load(uint32_t id) {
+        const auto& n = r->nodes[id];
+        if (!r->parties[r->ref_party()].ns[id].dyn_load) return;  // views: shadow_pub points into the base's
+        const uint32_t start = read_public(n.operands[1]);
+        load_dynamic(id);
+        for (int p = 0; p < r->n; ++p) {
+            auto& P = r->parties[p];
+            if (!P.local) continue;
+            dev(r, p);
+            lk(cudaMemcpyAsync(P.ns[id].shadow_pub, P.ns[n.operands[0]].shadow_pub + start, n.lanes * 4ull,
+                               cudaMemcpyDeviceToDevice, S(r, p)),
+               "dyn load");
+        }
+    }
+
     // Control flow: add/sub/mul of a private-typed node whose operands are public at run time
     // compute publicly (the public value kept beside its sharing), and a multiply by such a value
     // is a local mul_public — no Beaver triple, as the reference's exec_add / exec_mul_local see
     // public RtValues (runtime.cpp:129-183).  Returns true when it handled the node.
     bool exec_dynamic_public(uint32_t id) {
         const auto& n = r->nodes[id];
-        if (n.kind != SPDZ_NODE_ADD && n.kind != SPDZ_NODE_SUB && n.kind != SPDZ_NODE_MUL) return false;
         if (r->parties[r->ref_party()].ns[id].out.is_public) return false;
+        if (n.kind == SPDZ_NODE_LOAD || n.kind == SPDZ_NODE_REDUCE_ADD || n.kind == SPDZ_NODE_REDUCE_MUL)
+            return exec_dynamic_unary(id);
+        if (n.kind != SPDZ_NODE_ADD && n.kind != SPDZ_NODE_SUB && n.kind != SPDZ_NODE_MUL) return false;
         r->rt_pub[id] = 0;
         const bool pa = eff_pub(n.operands[0]), pb = eff_pub(n.operands[1]);
         const bool dyn_a = pa && !r->parties[r->ref_party()].ns[n.operands[0]].out.is_public;

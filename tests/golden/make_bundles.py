@@ -164,6 +164,32 @@ join:
 """ + workloads._DECL
 
 
+# a private vector phi taking a public incoming value, then loaded from, reduced and multiplied
+PHI_PUBLIC_REDUCE_IR = workloads._HDR + """define i32 @main(ptr %x, ptr %y, i32 %k) {
+entry:
+""" + workloads._ann("x", True) + workloads._ann("y", False) + """  %a = load <4 x i32>, ptr %x
+  %b = load <4 x i32>, ptr %y
+  %c = icmp sgt i32 %k, 10
+  br i1 %c, label %sec, label %pub
+sec:
+  %s = mul <4 x i32> %a, %a
+  br label %join
+pub:
+  %q = add <4 x i32> %b, %b
+  br label %join
+join:
+  %r = phi <4 x i32> [ %s, %sec ], [ %q, %pub ]
+  %m = call i32 @llvm.vector.reduce.mul.v4i32(<4 x i32> %r)
+  %n = call i32 @llvm.vector.reduce.add.v4i32(<4 x i32> %r)
+  %t = mul i32 %m, %n
+  ret i32 %t
+}
+
+declare i32 @llvm.vector.reduce.mul.v4i32(<4 x i32>)
+declare i32 @llvm.vector.reduce.add.v4i32(<4 x i32>)
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
@@ -201,6 +227,10 @@ def cases():
         "phi4_vlo": (PHI4_IR, 3, 262140, 21, {"x": rnd(2, 29), "k": np.array([1], np.uint32)}),
         "phi_public_root": (PHI_PUBLIC_ROOT_IR, 2, 262140, 22, {"x": rnd(1, 30), "k": np.array([3], np.uint32)}),
         "phi_secret_root": (PHI_PUBLIC_ROOT_IR, 2, 262140, 23, {"x": rnd(1, 31), "k": np.array([30], np.uint32)}),
+        "phi_public_reduce": (PHI_PUBLIC_REDUCE_IR, 2, 262140, 24, {"x": rnd(4, 32), "y": rnd(4, 33),
+                                                                   "k": np.array([3], np.uint32)}),
+        "phi_secret_reduce": (PHI_PUBLIC_REDUCE_IR, 2, 262140, 25, {"x": rnd(4, 34), "y": rnd(4, 35),
+                                                                   "k": np.array([30], np.uint32)}),
     }
 
 
