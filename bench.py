@@ -36,7 +36,8 @@ UNIT = "mult/s"
 
 
 def log(*a):
-    print(*a, file=sys.stderr, flush=True)
+    if os.environ.get("RANK", "0") == "0":  # one rank's progress lines (the others would interleave)
+        print(*a, file=sys.stderr, flush=True)
 
 
 # ------------------------------------------------------------------ clocks
