@@ -5,7 +5,9 @@
 //   run_local_b200  replaces runtime::run_local (runtime.cpp:586-613): GPU
 //                   dealer with the same seed and loop_iters hint;
 //   run_files_b200  replaces every party's `llspdz run` (tools/main.cpp:111-130):
-//                   party i's preprocessing from its MPCT store file.
+//                   party i's preprocessing from its MPCT store file;
+//   run_one_party_b200  replaces one party's `llspdz run --party i --config ...`: a
+//                   B200 party over the reference's TCP mesh among reference parties.
 //
 // A maintainer adds this file next to tools/main.cpp and routes `run --local`
 // / `bench` to it (a `--backend b200` flag).  Reports carry the fields
@@ -150,9 +152,17 @@ struct Run {
     }
 };
 
+struct Mesh {
+    spdz_net* h = nullptr;
+    ~Mesh() {
+        if (h) spdz_net_destroy(h);
+    }
+};
+
 std::vector<RunReport> execute(const circuit::CircuitGraph& g, int n_parties, const preproc::Inputs& inputs,
                                const RunOptions& opts, uint64_t dealer_seed, uint64_t loop_iters,
-                               const std::vector<std::string>* stores, int device) {
+                               const std::vector<std::string>* stores, int device, int single_party = -1,
+                               spdz_net* mesh = nullptr) {
     auto t0 = std::chrono::steady_clock::now();
     Lowered L = lower(g, inputs);
     spdz_run_options_t o;
@@ -162,10 +172,19 @@ std::vector<RunReport> execute(const circuit::CircuitGraph& g, int n_parties, co
     for (int p = 0; p < SPDZ_MAX_PARTIES; ++p) o.devices[p] = device;
     o.entry_label = g.entry_label == circuit::kNoNode ? 0 : g.entry_label;
     o.loop_iters = loop_iters;
+    if (mesh) {  // one party; the others across the reference's TCP mesh
+        o.single_party = single_party + 1;
+        o.network = 1;
+        o.external_mac_verify = 1;
+    }
     Run r;
     ok(spdz_run_create(L.nodes.data(), (uint32_t)L.nodes.size(), g.root, n_parties, &o, &r.h));
-    if (stores)
+    if (mesh) {
+        ok(spdz_run_attach_net(r.h, mesh));
+        ok(spdz_run_load_store(r.h, single_party, (*stores)[0].c_str()));
+    } else if (stores) {
         for (int p = 0; p < n_parties; ++p) ok(spdz_run_load_store(r.h, p, (*stores)[p].c_str()));
+    }
     for (auto& [node, vals] : L.bind) ok(spdz_run_bind_input(r.h, node, vals.data(), vals.size()));
     ok(spdz_run_share_inputs(r.h));
     auto t1 = std::chrono::steady_clock::now();
@@ -202,6 +221,29 @@ std::vector<RunReport> run_files_b200(const circuit::CircuitGraph& g, const std:
     ok(spdz_store_inspect(triples[0].c_str(), &info));
     return execute(g, (int)triples.size(), inputs, opts, 1, info.loop_iters ? info.loop_iters : 64, &triples,
                    device);
+}
+
+// tools/main.cpp:111-130 run_one_party with a B200 party: this party's MPCT store, the
+// reference's endpoints list (net::MeshConfig), the other parties reference processes or
+// other B200 hosts.
+RunReport run_one_party_b200(const circuit::CircuitGraph& g, const std::string& triples,
+                             const preproc::Inputs& inputs, int party, const std::vector<std::string>& endpoints,
+                             RunOptions opts, int device, uint64_t connect_timeout_ms, uint64_t io_timeout_ms) {
+    spdz_store_info_t info;
+    ok(spdz_store_inspect(triples.c_str(), &info));
+    if (info.party != party)
+        throw std::runtime_error("triple store belongs to party " + std::to_string(info.party) + ", --party says " +
+                                 std::to_string(party));
+    if (info.n_parties != endpoints.size())
+        throw std::runtime_error("endpoints file names " + std::to_string(endpoints.size()) +
+                                 " parties, store expects " + std::to_string(info.n_parties));
+    std::vector<const char*> eps;
+    for (auto& e : endpoints) eps.push_back(e.c_str());
+    Mesh m;
+    ok(spdz_net_connect(party, (int)eps.size(), eps.data(), connect_timeout_ms, io_timeout_ms, &m.h));
+    const std::vector<std::string> mine{triples};
+    return execute(g, (int)endpoints.size(), inputs, opts, 1, info.loop_iters ? info.loop_iters : 64, &mine, device,
+                   party, m.h)[0];
 }
 
 }  // namespace mpc::runtime

@@ -21,6 +21,9 @@
 #include "mpc/triple_store.hpp"
 
 namespace mpc::runtime {
+RunReport run_one_party_b200(const circuit::CircuitGraph& g, const std::string& triples,
+                             const preproc::Inputs& inputs, int party, const std::vector<std::string>& endpoints,
+                             RunOptions opts, int device, uint64_t connect_timeout_ms, uint64_t io_timeout_ms);
 std::vector<RunReport> run_local_b200(const circuit::CircuitGraph& g, int n_parties, const preproc::Inputs& inputs,
                                       RunOptions opts, uint64_t dealer_seed, uint64_t loop_iters_hint, int device);
 std::vector<RunReport> run_files_b200(const circuit::CircuitGraph& g, const std::vector<std::string>& triples,
@@ -101,6 +104,46 @@ int main(int argc, char** argv) {
                     runtime::run_local_b200(g, (int)triples.size(), in, opts, 3, 64, 0)[0]);
         } catch (const std::exception& e) {
             std::printf("%-40s FAIL  %s\n", name.c_str(), e.what());
+            ++failures;
+        }
+    }
+    // one B200 party among reference parties over the TCP mesh (`llspdz run --party`)
+    for (const char* name : {"mixed_1024_n3", "nested_loop", "linear_64x32"}) {
+        const fs::path d = fs::path(argv[1]) / name;
+        auto g = circuit::read_circuit_file((d / "circuit.mpcg").string());
+        auto in = preproc::read_input_file((d / "inputs.mpci").string());
+        runtime::RunOptions opts;
+        opts.slice = json_number(d / "expected.json", "slice", 262140);
+        const int n = (int)json_number(d / "expected.json", "parties", 2);
+        std::vector<std::string> eps;
+        for (int i = 0; i < n; ++i) eps.push_back("127.0.0.1:" + std::to_string(23400 + 10 * n + i));
+        std::vector<runtime::RunReport> reps(n);
+        std::vector<std::exception_ptr> errs(n);
+        std::vector<std::thread> th;
+        for (int q = 0; q < n; ++q)
+            th.emplace_back([&, q] {
+                try {
+                    const std::string tr = (d / ("triples_" + std::to_string(q) + ".bin")).string();
+                    if (q == 1) {
+                        reps[q] = runtime::run_one_party_b200(g, tr, in, q, eps, opts, 0, 20000, 30000);
+                    } else {
+                        net::MeshConfig mc;
+                        mc.party = q;
+                        mc.endpoints = eps;
+                        runtime::PartyRuntime rt(g, spdz::read_store_file(tr), net::connect_mesh(mc), opts);
+                        reps[q] = rt.run(in);
+                    }
+                } catch (...) {
+                    errs[q] = std::current_exception();
+                }
+            });
+        for (auto& t : th) t.join();
+        try {
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+            compare(std::string(name) + " (B200 party 1 over TCP)", reps[0], reps[1]);
+        } catch (const std::exception& e) {
+            std::printf("%-40s FAIL  %s\n", name, e.what());
             ++failures;
         }
     }
