@@ -719,8 +719,11 @@ __global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint3
 // G threads per row (G = 32: a warp per row, shuffle reduction, every row in flight at
 // once when rows are many; G = 256: a block per row for few long rows).
 
+#ifndef SPDZ_MC2_MINB
+#define SPDZ_MC2_MINB 1  // resident blocks per SM the register budget must allow (occupancy experiments)
+#endif
 template <int G, bool V4>
-__global__ void __launch_bounds__(kThreads) k_matrix_combine2(MC2Args a) {
+__global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2Args a) {
     constexpr int RPB = kThreads / G;  // rows per block
     const uint32_t g = threadIdx.x % G, slot = threadIdx.x / G;
     const uint64_t cells = (uint64_t)a.din * a.rows;
