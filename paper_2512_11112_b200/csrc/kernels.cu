@@ -656,7 +656,11 @@ __global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint3
             const uint32_t n4 = din / 4;
             for (uint32_t g = threadIdx.x; g < n4; g += blockDim.x) {
                 const uint64_t gg = base / 4 + g;
+                // all loads before the opened-D store (E lives in `opened`: a later load would wait)
                 uint4 d4 = ld4(own, gg);
+                const uint4 av = ld4(Av, gg), am = ld4(Am, gg);
+                const uint4 bv = reinterpret_cast<const uint4*>(Bv)[g], bm = reinterpret_cast<const uint4*>(Bm)[g];
+                const uint4 e4 = reinterpret_cast<const uint4*>(E)[g];
                 uint32_t d[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
@@ -667,9 +671,6 @@ __global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint3
                     d[3] = fp_add(d[3], fp_reduce32(q.w));
                 }
                 st4(opened, gg, d);
-                uint4 av = ld4(Av, gg), am = ld4(Am, gg);
-                uint4 bv = reinterpret_cast<const uint4*>(Bv)[g], bm = reinterpret_cast<const uint4*>(Bm)[g];
-                uint4 e4 = reinterpret_cast<const uint4*>(E)[g];
                 const uint32_t A0[4] = {av.x, av.y, av.z, av.w}, A1[4] = {am.x, am.y, am.z, am.w};
                 const uint32_t B0[4] = {bv.x, bv.y, bv.z, bv.w}, B1[4] = {bm.x, bm.y, bm.z, bm.w};
                 const uint32_t Ee[4] = {e4.x, e4.y, e4.z, e4.w};
@@ -736,27 +737,36 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
         if (V4) {
             for (uint32_t c4 = g; c4 < a.din / 4; c4 += G) {
                 const uint64_t gg = base / 4 + c4;
+                // every load of the iteration issued before the opened-D store: the pointers are
+                // not restrict, so a load after the store would wait for it (two round trips)
                 const uint4 d0 = ld4(a.D0, gg), d1 = ld4(a.D1, gg);
+                const uint4 e4 = reinterpret_cast<const uint4*>(E)[c4];
+                uint4 av[2], am[2], bv[2], bm[2];
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    av[p] = ld4(a.A[p][0], gg);
+                    am[p] = ld4(a.A[p][1], gg);
+                    bv[p] = reinterpret_cast<const uint4*>(a.B[p][0] + toff)[c4];
+                    bm[p] = reinterpret_cast<const uint4*>(a.B[p][1] + toff)[c4];
+                }
                 const uint32_t d[4] = {fp_add(d0.x, fp_reduce32(d1.x)), fp_add(d0.y, fp_reduce32(d1.y)),
                                        fp_add(d0.z, fp_reduce32(d1.z)), fp_add(d0.w, fp_reduce32(d1.w))};
-                st4(a.opened, gg, d);
-                const uint4 e4 = reinterpret_cast<const uint4*>(E)[c4];
                 const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
                 for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const uint4 av = ld4(a.A[p][0], gg), am = ld4(a.A[p][1], gg);
-                    const uint4 bv = reinterpret_cast<const uint4*>(a.B[p][0] + toff)[c4];
-                    const uint4 bm = reinterpret_cast<const uint4*>(a.B[p][1] + toff)[c4];
-                    const uint32_t AV[4] = {av.x, av.y, av.z, av.w}, AM[4] = {am.x, am.y, am.z, am.w};
-                    const uint32_t BV[4] = {bv.x, bv.y, bv.z, bv.w}, BM[4] = {bm.x, bm.y, bm.z, bm.w};
+                    const uint32_t AV[4] = {av[p].x, av[p].y, av[p].z, av[p].w};
+                    const uint32_t AM[4] = {am[p].x, am[p].y, am[p].z, am[p].w};
+                    const uint32_t BV[4] = {bv[p].x, bv[p].y, bv[p].z, bv[p].w};
+                    const uint32_t BM[4] = {bm[p].x, bm[p].y, bm[p].z, bm[p].w};
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
                         acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
                         acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
                     }
                 }
+                st4(a.opened, gg, d);
             }
         } else {
             for (uint32_t c = g; c < a.din; c += G) {
