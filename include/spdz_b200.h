@@ -22,7 +22,11 @@
  *    returns the thread-local message; codes map 1:1 onto the reference's
  *    exception types (listed per code).
  *  - A context is owned by one party; distinct contexts may be driven from
- *    distinct threads concurrently (kernels are pure).
+ *    distinct threads concurrently (kernels are pure).  One
+ *    context is driven by one thread at a time (its stream, staging buffers and
+ *    accumulators are not locked), except spdz_mac_log_append (locked).
+ *  - A run (spdz_run_*) is driven by one thread at a time; distinct runs, and
+ *    distinct meshes (spdz_net_*), may live on distinct threads.
  */
 #ifndef SPDZ_B200_H
 #define SPDZ_B200_H
