@@ -11,7 +11,7 @@ streamed from the MPCT files (``spdz_run_load_store``).
 
 Parsing is host work on a few KB of metadata; nothing here computes on the
 shares.  Circuits with control flow (Phi/Branch, loops) run block by block
-(``run_cfg`` in csrc/run.cu, the sequential reading of scheduler.cpp).
+(``run_cfg`` in csrc/run_exec.hpp, the sequential reading of scheduler.cpp).
 """
 from __future__ import annotations
 
