@@ -412,3 +412,29 @@ def test_acceptance_c8_c9_linear(gpu):
     assert rep.outputs.tolist() == want and rep.matrix_triples_consumed == 4
     for n in range(2, 7):
         assert rt.run_local(g, n, vals).outputs.tolist() == want, n
+
+
+# ---- random straight-line vector programs (tests/golden/fuzz, make_fuzz.py) ----
+FUZZ = Path(__file__).resolve().parent / "golden" / "fuzz"
+FUZZ_META = json.loads((FUZZ / "expected.json").read_text())
+
+
+def test_fuzz_programs_lower():
+    assert len(FUZZ_META) >= 40
+    for name, m in FUZZ_META.items():
+        vals = {k: np.array(v, np.uint32) for k, v in m["inputs"].items()}
+        A.read_circuit_file(FUZZ / f"{name}.mpcg").to_graph(vals)
+
+
+@pytest.mark.gpu
+def test_fuzz_programs_run(gpu):
+    """Outputs, digests and triple counts == the reference run_local on every program."""
+    bad = []
+    for name, m in FUZZ_META.items():
+        vals = {k: np.array(v, np.uint32) for k, v in m["inputs"].items()}
+        g = A.read_circuit_file(FUZZ / f"{name}.mpcg").to_graph(vals)
+        rep = rt.run_local(g, m["parties"], vals, dealer_seed=9)
+        if (rep.outputs.tolist() != m["outputs"] or rep.output_digest != m["digest"]
+                or rep.scalar_triples_consumed != m["scalar_triples"]):
+            bad.append(name)
+    assert not bad, bad
