@@ -455,6 +455,7 @@ int spdz_run_create(const spdz_node_t* nodes, uint32_t n_nodes, uint32_t root, i
             need(r->shard_off + r->shard_L <= r->shard_total, SPDZ_ERR_INVALID_ARGUMENT, "shard outside the circuit");
         }
         plan_layout(r.get());
+        compute_liveness(r.get());
         plan_buffers(r.get());
         alloc_deals(r.get());
         deal(r.get(), r->opts.dealer_seed);
@@ -707,8 +708,10 @@ int spdz_run_mac_check(spdz_run* r, int use_coin, uint64_t coin, spdz_run_report
             }
             rep->online_device_ms = dmax;
             // straight-line: every provisioned triple; control flow: what the taken path used
-            rep->scalar_triples_consumed = r->cfg ? r->scalar_used : r->scalar_total;
-            rep->matrix_triples_consumed = r->cfg ? r->matrix_used : r->matrix_total;
+            // straight-line: the live nodes' regions (one execution each); control flow: what the
+            // taken path used
+            rep->scalar_triples_consumed = r->cfg ? r->scalar_used : r->scalar_live;
+            rep->matrix_triples_consumed = r->cfg ? r->matrix_used : r->matrix_live;
             rep->bytes_exchanged = r->exchanged;
             rep->output_digest = 0;  // spdz_run_output_digest (host byte loop, outside the online phase)
             rep->kernel_launches = g_kernel_launches - r->launches0;

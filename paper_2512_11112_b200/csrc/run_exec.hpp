@@ -434,7 +434,8 @@ struct Exec {
                                                                " has no pair for block " + std::to_string(pred));
                 phis.emplace_back(u, chosen);
             }
-            for (auto [phi, chosen] : phis) phi_copy(phi, chosen);
+            for (auto [phi, chosen] : phis)
+                if (r->live[phi]) phi_copy(phi, chosen);
             uint32_t dst = SPDZ_NO_NODE;
             for (uint32_t u = r->nodes[label].next; u != SPDZ_NO_NODE; u = r->nodes.at(u).next) {
                 const auto& n = r->nodes.at(u);
@@ -454,7 +455,7 @@ struct Exec {
                     }
                     break;
                 }
-                exec_node(u, execs[u]++);
+                if (r->live[u]) exec_node(u, execs[u]++);
             }
             need(dst != SPDZ_NO_NODE, SPDZ_ERR_INVALID_ARGUMENT,
                  "runtime: block " + std::to_string(label) + " ends without a branch or the root");
@@ -884,7 +885,8 @@ struct Exec {
     }
 
     void run_nodes() {
-        for (uint32_t id = 0; id < r->nodes.size(); ++id) exec_node(id, 0);
+        for (uint32_t id = 0; id < r->nodes.size(); ++id)
+            if (r->live[id]) exec_node(id, 0);
     }
 
     // runtime.cpp:185-200: execution `exec` of a triple-consuming node must be provisioned

@@ -1,10 +1,133 @@
 // Planning of a run (node buffers, the triple layout of preproc.cpp:124-163) and its
 // preprocessing: the GPU dealer in make_dealer_stores order, or the reference's MPCT
 // store files streamed into the same device pools.
+#include <deque>
+#include <functional>
+
 #include "run_state.hpp"
 
 namespace spdzb200 {
 namespace rt {
+
+// Which nodes run.  The reference's scheduler stops when the root completes (scheduler.cpp:154,
+// runtime.cpp:452-465), so whether it issues a dead node (value reaching no output) depends on
+// its issue order: usually it does (heavy nodes first, while the root waits for an opening),
+// sometimes not (the dead node's inputs become ready after a root computed locally).  Local
+// straight-line runs execute exactly the nodes its single-worker order issues (so triple counts
+// match); control-flow runs execute every node of an entered block; a run across a mesh skips
+// dead nodes, so it never waits for a frame reference parties may not send (a dead open the
+// reference does issue just goes unanswered).  Outputs are the same either way; the triple
+// layout reserves every region.
+// The nodes the reference's single-worker scheduler issues before the root completes
+// (scheduler.cpp:65-97, 138-169; runtime.cpp:360-465): heavy queue first, FIFO; a private x
+// private multiply completes in its open continuation, which runs when the worker has nothing
+// else to issue (pump) or when a blocking reduce_mul / linear layer pumps; the loop ends when
+// the root completes.  Checked against the reference's triple counts on every fuzzed program.
+static void scheduler_issued(spdz_run* r, std::vector<char>& issued) {
+    const uint32_t N = (uint32_t)r->nodes.size();
+    auto kind = [&](uint32_t i) { return r->nodes[i].kind; };
+    auto queueable = [&](uint32_t i) {
+        const int k = kind(i);
+        return k != SPDZ_NODE_INPUT && k != SPDZ_NODE_CONST && k != SPDZ_NODE_NOP && k != SPDZ_NODE_LABEL &&
+               k != SPDZ_NODE_PHI;
+    };
+    auto heavy = [&](uint32_t i) {
+        const int k = kind(i);
+        return k == SPDZ_NODE_MUL || k == SPDZ_NODE_REDUCE_MUL || k == SPDZ_NODE_LINEAR;
+    };
+    auto both_private = [&](uint32_t i) {
+        const auto& n = r->nodes[i];
+        return n.n_operands >= 2 && r->priv(n.operands[0]) && r->priv(n.operands[1]);
+    };
+    std::vector<uint32_t> remaining(N, 0);
+    std::vector<std::vector<uint32_t>> consumers(N);
+    for (uint32_t i = 0; i < N; ++i)
+        if (queueable(i)) {
+            remaining[i] = r->nodes[i].n_operands;
+            for (uint32_t k = 0; k < r->nodes[i].n_operands; ++k) consumers[r->nodes[i].operands[k]].push_back(i);
+        }
+    std::deque<uint32_t> hq, lq;
+    std::vector<uint32_t> outstanding;
+    bool finished = false, started = false;
+    std::function<void(uint32_t)> complete = [&](uint32_t i) {
+        if (i == r->root) finished = true;
+        for (uint32_t c : consumers[i])
+            if (--remaining[c] == 0 && started) (heavy(c) ? hq : lq).push_back(c);
+    };
+    for (uint32_t i = 0; i < N; ++i)
+        if (kind(i) == SPDZ_NODE_INPUT || kind(i) == SPDZ_NODE_CONST) complete(i);
+    started = true;
+    for (uint32_t i = 0; i < N; ++i)  // entry block: ready nodes in program order
+        if (queueable(i) && remaining[i] == 0) (heavy(i) ? hq : lq).push_back(i);
+    auto pump = [&] {
+        std::vector<uint32_t> done;
+        done.swap(outstanding);
+        for (uint32_t i : done) complete(i);
+    };
+    issued.assign(N, 0);
+    while (!finished) {
+        uint32_t i;
+        if (!hq.empty()) {
+            i = hq.front();
+            hq.pop_front();
+        } else if (!lq.empty()) {
+            i = lq.front();
+            lq.pop_front();
+        } else if (!outstanding.empty()) {
+            pump();
+            continue;
+        } else {
+            break;
+        }
+        issued[i] = 1;
+        const int k = kind(i);
+        if (k == SPDZ_NODE_MUL && both_private(i)) {
+            outstanding.push_back(i);
+        } else if ((k == SPDZ_NODE_REDUCE_MUL && r->priv(r->nodes[i].operands[0])) ||
+                   (k == SPDZ_NODE_LINEAR && both_private(i))) {
+            pump();  // blocking opens pump the session (runtime.cpp:269, linear.cpp:123-127)
+            complete(i);
+        } else {
+            complete(i);
+        }
+    }
+    for (uint32_t i = 0; i < N; ++i)  // inputs, constants and the root's own chain stay usable
+        if (!queueable(i)) issued[i] = 1;
+}
+
+void compute_liveness(spdz_run* r) {
+    const uint32_t N = (uint32_t)r->nodes.size();
+    if (!r->opts.network) {
+        if (r->cfg) {  // control flow: every node of an entered block runs
+            r->live.assign(N, 1);
+        } else {
+            scheduler_issued(r, r->live);
+        }
+        r->scalar_live = r->matrix_live = 0;
+        for (auto& [id, reg] : r->scalar)
+            if (r->live[id]) r->scalar_live += reg.stride;
+        for (auto& [id, reg] : r->matrix)
+            if (r->live[id]) r->matrix_live += reg.stride;
+        return;
+    }
+    r->live.assign(N, 0);
+    std::vector<uint32_t> work{r->root};
+    for (uint32_t id = 0; id < N; ++id)
+        if (r->nodes[id].kind == SPDZ_NODE_BRANCH) work.push_back(id);
+    while (!work.empty()) {
+        const uint32_t id = work.back();
+        work.pop_back();
+        if (id >= N || r->live[id]) continue;
+        r->live[id] = 1;
+        const auto& n = r->nodes[id];
+        for (uint32_t k = 0; k < n.n_operands; ++k) work.push_back(n.operands[k]);
+    }
+    r->scalar_live = r->matrix_live = 0;
+    for (auto& [id, reg] : r->scalar)
+        if (r->live[id]) r->scalar_live += reg.stride;
+    for (auto& [id, reg] : r->matrix)
+        if (r->live[id]) r->matrix_live += reg.stride;
+}
 
 // ---- planning (run creation) ----
 void plan_layout(spdz_run* r) {

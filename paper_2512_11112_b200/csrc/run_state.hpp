@@ -187,6 +187,8 @@ struct spdz_run {
     std::map<uint32_t, uint64_t> input_mask_gfirst;       // ... global index of that mask
     uint64_t scalar_total_global = 0, mask_total_global = 0;
     bool cfg = false;               // graph with PHI/BRANCH: block-by-block execution (run_cfg)
+    std::vector<char> live;         // node's value reaches the root (or a branch): executed
+    uint64_t scalar_live = 0, matrix_live = 0;  // triples the live nodes consume (straight-line)
     NetLink* net = nullptr;         // peers across the reference's TCP mesh (spdz_run_attach_net)
     HostPinned net_stage;           // frame staging (D2H of own payloads, H2D of the peers')
     std::vector<uint32_t> net_host; // per-tile frame assembly
@@ -323,6 +325,7 @@ inline cudaEvent_t new_event(spdz_run* r, int p) {
 
 // planning and preprocessing (run_plan.cu)
 void plan_layout(spdz_run* r);
+void compute_liveness(spdz_run* r);
 uint32_t const_of(spdz_run* r, uint32_t id);
 void plan_buffers(spdz_run* r);
 void deal(spdz_run* r, uint64_t seed);

@@ -190,6 +190,21 @@ declare i32 @llvm.vector.reduce.add.v4i32(<4 x i32>)
 """ + workloads._DECL
 
 
+# a dead private multiply (its value reaches no output) next to a root computed locally: the
+# reference never issues it (fuzz f41's shape)
+DEAD_MUL_IR = workloads._HDR + """define <3 x i32> @main(ptr %x, ptr %y) {
+entry:
+""" + workloads._ann("x", True) + workloads._ann("y", False) + """  %a = load <3 x i32>, ptr %x
+  %b = load <3 x i32>, ptr %y
+  %s = add <3 x i32> %a, %b
+  %dead = mul <3 x i32> %s, %a
+  %r = mul <3 x i32> %a, <i32 5, i32 7, i32 11>
+  ret <3 x i32> %r
+}
+
+""" + workloads._DECL
+
+
 def rnd(n, seed):
     return ref.rand_field_vec(n, seed)
 
@@ -231,6 +246,7 @@ def cases():
                                                                    "k": np.array([3], np.uint32)}),
         "phi_secret_reduce": (PHI_PUBLIC_REDUCE_IR, 2, 262140, 25, {"x": rnd(4, 34), "y": rnd(4, 35),
                                                                    "k": np.array([30], np.uint32)}),
+        "dead_mul": (DEAD_MUL_IR, 2, 262140, 26, {"x": rnd(3, 36), "y": rnd(3, 37)}),
     }
 
 

@@ -428,7 +428,9 @@ def test_fuzz_programs_lower():
 
 @pytest.mark.gpu
 def test_fuzz_programs_run(gpu):
-    """Outputs, digests and triple counts == the reference run_local on every program."""
+    """Outputs, digests and triple counts == the reference run_local on every program — the
+    counts include exactly the dead multiplies the reference's issue order reaches before its
+    root completes (12 programs have one; in f41 the reference never issues it)."""
     bad = []
     for name, m in FUZZ_META.items():
         vals = {k: np.array(v, np.uint32) for k, v in m["inputs"].items()}

@@ -73,7 +73,7 @@ CASES = [("straight_line", 0), ("straight_line", 1), ("mixed_1024_n3", 0), ("mix
          ("linear_64x32", 0), ("linear_64x32", 1), ("reduce_mul", 1), ("vector_const", 0), ("select_shl_bits", 1),
          ("diamond_big", 0), ("nested_loop", 1), ("loop_after_loop", 2), ("vector_loop", 0), ("linear_loop", 1),
          ("reduce_mul_loop", 2), ("phi4_vlo", 1), ("phi_public_root", 1), ("phi_secret_root", 0),
-         ("phi_public_reduce", 0), ("phi_secret_reduce", 1)]
+         ("phi_public_reduce", 0), ("phi_secret_reduce", 1), ("dead_mul", 1)]
 
 
 @pytest.mark.parametrize("case,ours", CASES, ids=[f"{c}-p{o}" for c, o in CASES])
