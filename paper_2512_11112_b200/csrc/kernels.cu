@@ -497,12 +497,15 @@ __device__ __forceinline__ uint4 sub4(const uint4& a, const uint4& b) {
 // Compute-bound, not memory-bound (ncu r01d: the same kernel on L2-resident
 // records runs no faster than on HBM; a TMA-staged variant was slower), so the
 // block count is the occupancy limit (one wave) and loads are plain 128-bit.
+#ifndef SPDZ_SIGMA2_MINB
+#define SPDZ_SIGMA2_MINB 3
+#endif
 #ifndef SPDZ_SIGMA_MINB
 #define SPDZ_SIGMA_MINB 4
 #endif
 template <int NP>
 struct SigmaMinBlocks {
-    static constexpr int value = NP == 1 ? SPDZ_SIGMA_MINB : 3;
+    static constexpr int value = NP == 1 ? SPDZ_SIGMA_MINB : SPDZ_SIGMA2_MINB;
 };
 
 // NP parties (NP = 1: one party's log; NP = 2: both local parties of a 2-party run,
