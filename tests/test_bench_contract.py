@@ -40,3 +40,25 @@ def test_reference_arm_nonzero_ranks_are_silent():
     r = _run({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_json_line(gpu):
+    """The driver's N > 1 launch (torch.distributed.run, one process per party GPU set; here both
+    ranks on the one GPU with gloo for the host-side collectives): one JSON line from rank 0 with
+    n_gpus = 2, weak scaling, and a positive whole-job value."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, SPDZ_BENCH_DEVICE="0", SPDZ_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--lanes", str(1 << 20)],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["e2e"]["value"] > 0
