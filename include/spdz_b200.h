@@ -527,6 +527,10 @@ int spdz_net_connect(int party, int n_parties, const char* const* endpoints, uin
 int spdz_net_destroy(spdz_net* net);
 /* raw frames (tests / tooling): msg-type 0 OpenShares 1 Commit 2 Reveal 3 Nonce 4 Control */
 int spdz_net_send(spdz_net* net, int peer, int type, uint64_t batch, const uint32_t* words, uint32_t lanes);
+/* spdz_net_recv: a frame longer than cap lanes returns SPDZ_ERR_LANE_COUNT_MISMATCH with its
+ * length in *lanes and stays queued (retry with a larger buffer); out == NULL consumes the frame
+ * and returns only its length.  Frames announcing more than 2^30 lanes stop the peer's reader
+ * with MalformedShareMessage before anything is allocated. */
 int spdz_net_recv(spdz_net* net, int peer, int type, uint64_t batch, uint32_t* out, uint64_t cap, uint64_t* lanes);
 int spdz_net_stats(spdz_net* net, uint64_t* bytes_sent, uint64_t* bytes_received);
 /* A single-party run (options.single_party = p + 1) whose peers are across the mesh:

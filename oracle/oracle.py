@@ -64,6 +64,7 @@ def lib():
         L.or_dealer_rng_state.restype = C.c_uint64
         L.or_dealer_share.argtypes = [C.c_void_p, U32P, C.c_uint64, U32P, U32P]
         L.or_dealer_share_random.argtypes = [C.c_void_p, C.c_uint64, U32P, U32P, U32P]
+        L.or_dealer_masks.argtypes = [C.c_void_p, C.c_uint64, U32P, U32P, U32P]
         L.or_dealer_triples.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
         L.or_dealer_matrix_triples.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]
         L.or_add_batch.argtypes = [U32P, U32P, U32P, U32P, C.c_uint64, C.c_int, U32P, U32P]
@@ -180,11 +181,8 @@ def dealer_stores(n: int, seed: int, scalars: int, mshapes=(), masks: int = 0):
     mv = np.zeros((n, masks), np.uint32)
     mm = np.zeros((n, masks), np.uint32)
     mc = np.zeros(masks, np.uint32)
-    for j in range(masks):
-        c, v, m = d.share_random(1)
-        mv[:, j] = v[:, 0]
-        mm[:, j] = m[:, 0]
-        mc[j] = c[0]
+    if masks:  # one share_random(1) per mask, in C
+        lib().or_dealer_masks(d._buf, masks, mc, mv, mm)
     out["masks"] = (mv, mm, mc)
     out["dealer"] = d
     return out

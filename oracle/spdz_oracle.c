@@ -145,6 +145,19 @@ void or_dealer_share_random(or_dealer_t* d, uint64_t len, uint32_t* clear, uint3
     or_dealer_share(d, clear, len, out_v, out_m);
 }
 
+/* triple_store.cpp:248-287: make_dealer_stores draws each input mask as share_random(1);
+   mv/mm party-major (n * count), clear[count]. */
+void or_dealer_masks(or_dealer_t* d, uint64_t count, uint32_t* clear, uint32_t* mv, uint32_t* mm) {
+    uint32_t v[64], m[64];
+    for (uint64_t j = 0; j < count; ++j) {
+        or_dealer_share_random(d, 1, clear + j, v, m);
+        for (int i = 0; i < d->n; ++i) {
+            mv[(uint64_t)i * count + j] = v[i];
+            mm[(uint64_t)i * count + j] = m[i];
+        }
+    }
+}
+
 /* spdz.cpp:210-225; planes[6] each n*lanes (a.v a.m b.v b.m c.v c.m). */
 void or_dealer_triples(or_dealer_t* d, uint64_t lanes, uint32_t* const* planes) {
     uint32_t* a = (uint32_t*)malloc(lanes * 4);

@@ -432,9 +432,18 @@ __global__ void __launch_bounds__(kThreads) k_pair_split(const uint32_t* __restr
                                                          const uint32_t* __restrict__ cm, uint64_t pairs,
                                                          uint32_t* xv, uint32_t* xm, uint32_t* yv, uint32_t* ym) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // a load at a constant odd offset is a zero-copy view (run_plan.cu), so the
+    // pair view is 8-byte aligned only sometimes: the 64-bit path needs both planes aligned
+    const bool wide = ((reinterpret_cast<uintptr_t>(cv) | reinterpret_cast<uintptr_t>(cm)) & 7) == 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
-        uint2 v = reinterpret_cast<const uint2*>(cv)[i];
-        uint2 m = reinterpret_cast<const uint2*>(cm)[i];
+        uint2 v, m;
+        if (wide) {
+            v = reinterpret_cast<const uint2*>(cv)[i];
+            m = reinterpret_cast<const uint2*>(cm)[i];
+        } else {
+            v = make_uint2(cv[2 * i], cv[2 * i + 1]);
+            m = make_uint2(cm[2 * i], cm[2 * i + 1]);
+        }
         xv[i] = v.x;
         yv[i] = v.y;
         xm[i] = m.x;

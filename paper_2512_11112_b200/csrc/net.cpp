@@ -130,7 +130,7 @@ void NetLink::broadcast(uint8_t type, uint64_t batch, const uint32_t* words, uin
         if (p != party) send(p, type, batch, words, lanes);
 }
 
-std::vector<uint32_t> NetLink::recv(int peer, uint8_t type, uint64_t batch) {
+std::vector<uint32_t> NetLink::recv(int peer, uint8_t type, uint64_t batch, uint64_t* cap) {
     const auto key = std::make_tuple(type, batch, peer);
     std::unique_lock lk(mu);
     const bool got = cv.wait_for(lk, io_timeout, [&] { return inbox.count(key) || !peer_error[peer].empty(); });
@@ -146,6 +146,10 @@ std::vector<uint32_t> NetLink::recv(int peer, uint8_t type, uint64_t batch) {
         throw Error(SPDZ_ERR_PEER_TIMEOUT,
                     "PeerTimeout: " + std::string(type == kMsgOpenShares ? "open" : "exchange") + " batch " +
                         std::to_string(batch) + " from peer " + std::to_string(peer));
+    }
+    if (cap && it->second.size() > *cap) {  // too long for the caller's buffer: keep the frame
+        *cap = it->second.size();
+        return {};
     }
     std::vector<uint32_t> out = std::move(it->second);
     inbox.erase(it);
@@ -177,7 +181,16 @@ void NetLink::reader_loop(int peer) {
         const uint32_t lanes = le32(hdr + 4);
         uint64_t batch = 0;
         for (int i = 0; i < 8; ++i) batch |= uint64_t(hdr[8 + i]) << (8 * i);
-        std::vector<uint32_t> payload(lanes);
+        if (lanes > max_frame_lanes)
+            return stop("MalformedShareMessage: frame of " + std::to_string(lanes) + " lanes from peer " +
+                        std::to_string(peer) + " exceeds the " + std::to_string(max_frame_lanes) + "-lane limit");
+        std::vector<uint32_t> payload;
+        try {
+            payload.resize(lanes);
+        } catch (const std::bad_alloc&) {
+            return stop("MalformedShareMessage: cannot allocate a " + std::to_string(lanes) + "-lane frame from peer " +
+                        std::to_string(peer));
+        }
         if (lanes && !recv_exact(fd, payload.data(), 4ull * lanes))
             return stop("PeerTimeout: connection to peer " + std::to_string(peer) + " closed mid-frame");
         if (stopping) return;
@@ -300,10 +313,13 @@ int spdz_net_recv(spdz_net* net, int peer, int type, uint64_t batch, uint32_t* o
     return guard([&] {
         need(net != nullptr && lanes != nullptr && peer >= 0 && peer < net->link->n && peer != net->link->party,
              SPDZ_ERR_INVALID_ARGUMENT, "bad recv");
-        auto v = net->link->recv(peer, (uint8_t)type, batch);
-        *lanes = v.size();
-        need(v.size() <= cap || out == nullptr, SPDZ_ERR_LANE_COUNT_MISMATCH,
-             "LaneCountMismatch: peer " + std::to_string(peer) + " sent " + std::to_string(v.size()) +
+        // the frame stays queued when it does not fit, so a retry with a larger buffer gets it
+        const uint64_t room = out ? cap : ~0ull;
+        uint64_t fit = room;
+        auto v = net->link->recv(peer, (uint8_t)type, batch, &fit);
+        *lanes = fit > room ? fit : v.size();  // fit > room: the frame did not fit and is still queued
+        need(fit <= room, SPDZ_ERR_LANE_COUNT_MISMATCH,
+             "LaneCountMismatch: peer " + std::to_string(peer) + " sent " + std::to_string(*lanes) +
                  " lanes, expected at most " + std::to_string(cap));
         if (out && !v.empty()) std::memcpy(out, v.data(), v.size() * 4);
     });

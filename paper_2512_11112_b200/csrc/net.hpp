@@ -44,13 +44,18 @@ struct NetLink {
     std::vector<std::string> peer_error;  // reader of peer p stopped: why
     std::atomic<uint64_t> bytes_sent{0}, bytes_received{0};
     std::atomic<bool> stopping{false};
+    // frames announcing more lanes are rejected as MalformedShareMessage before any
+    // allocation (a corrupt header must not take the host process down); 2^30 lanes = 4 GiB
+    uint64_t max_frame_lanes = 1ull << 30;
 
     NetLink(int party_, int n_) : party(party_), n(n_), fds(n_, -1), send_mu(n_), peer_error(n_) {}
     ~NetLink();
     void send(int peer, uint8_t type, uint64_t batch, const uint32_t* words, uint32_t lanes);
     void broadcast(uint8_t type, uint64_t batch, const uint32_t* words, uint32_t lanes);
     // blocks until peer's frame (type, batch) is in the inbox; removes and returns its payload
-    std::vector<uint32_t> recv(int peer, uint8_t type, uint64_t batch);
+    // cap (optional): a frame longer than *cap lanes is left in the inbox and its length
+    // returned in *cap with an empty vector, so the caller can retry with a larger buffer
+    std::vector<uint32_t> recv(int peer, uint8_t type, uint64_t batch, uint64_t* cap = nullptr);
     // Session::exchange (net.cpp:140-178): send to all, one frame of (type, batch) from each
     std::vector<std::vector<uint32_t>> exchange(uint8_t type, uint64_t batch, const std::vector<uint32_t>& own);
     void start_readers();

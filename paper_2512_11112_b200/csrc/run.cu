@@ -563,7 +563,7 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         if (r->consumed && !reuse)
             throw Error(SPDZ_ERR_TRIPLE_EXHAUSTED,
                         "TripleExhausted: preprocessing of this run was already consumed (deal again)");
-        need(!r->any_remote || r->opts.external_mac_verify, SPDZ_ERR_INVALID_ARGUMENT,
+        need(!r->any_remote || r->opts.external_mac_verify || r->opts.network, SPDZ_ERR_INVALID_ARGUMENT,
              "runs with remote parties verify the MAC check externally (external_mac_verify = 1)");
         r->launches0 = g_kernel_launches;
         r->exchanged = 0;

@@ -686,9 +686,20 @@ struct Exec {
                     lk(launch_modgemm(c->stream, 1, dout, din, 1, w.pub, w.pub, x.pub, nullptr, st.lin_tmp,
                                       st.out.pub),
                        "modgemm");
-                    lk(launch_pub_binop(c->stream, 0, st.lin_tmp, false, b.pub, b.lanes != dout, st.out.pub, dout,
-                                        c->sms),
-                       "bias");
+                    if (b.is_public) {
+                        lk(launch_pub_binop(c->stream, 0, st.lin_tmp, false, b.pub, b.lanes != dout, st.out.pub, dout,
+                                            c->sms),
+                           "bias");
+                    } else if (b.lanes == dout) {  // exec_add(y public, b private) = add_public(b, y)
+                        lk(launch_public(c->stream, 0, b.v, b.m, st.lin_tmp, false, 0u, false, c->party, c->alpha,
+                                         st.out.v, st.out.m, dout, c->sms, c->d_alpha),
+                           "bias pub");
+                    } else {
+                        lk(launch_bcast(c->stream, b.v, b.m, st.out.v, st.out.m, dout, c->sms), "bcast");
+                        lk(launch_public(c->stream, 0, st.out.v, st.out.m, st.lin_tmp, false, 0u, false, c->party,
+                                         c->alpha, st.out.v, st.out.m, dout, c->sms, c->d_alpha),
+                           "bias pub");
+                    }
                     continue;
                 }
                 uint32_t* yv = st.lin_tmp;

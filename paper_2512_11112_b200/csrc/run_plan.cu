@@ -352,7 +352,10 @@ void plan_buffers(spdz_run* r) {
                     need(x.lanes == n.din && w.lanes == (uint64_t)n.din * n.dout, SPDZ_ERR_INVALID_ARGUMENT,
                          "ShapeMismatch: linear operands do not match din/dout");
                     if (x.is_public && w.is_public) {
-                        pub_out(n.dout);
+                        // any private operand makes the node private (graph_builder.cpp:123):
+                        // a private bias gives add_public(b, W x) (runtime.cpp:129-162)
+                        if (n.n_operands > 2 && !opnd(2).is_public) priv_out(n.dout);
+                        else pub_out(n.dout);
                         st.lin_tmp = r->alloc(p, n.dout);
                     } else if (x.is_public != w.is_public) {
                         priv_out(n.dout);

@@ -40,10 +40,16 @@ class Mesh:
         w = np.ascontiguousarray(words, dtype=np.uint32)
         check(lib().spdz_net_send(self.h, peer, msg_type, batch, w.ctypes.data if w.size else None, w.size))
 
-    def recv(self, peer: int, msg_type: int, batch: int, cap: int = 1 << 24) -> np.ndarray:
-        out = np.empty(cap, np.uint32)
+    def recv(self, peer: int, msg_type: int, batch: int, cap: int = 1 << 24, grow: bool = True) -> np.ndarray:
+        """The frame (msg_type, batch) from ``peer``.  A frame longer than ``cap`` stays
+        queued: with ``grow`` it is fetched again into a buffer of its size, else
+        LaneCountMismatch is raised."""
+        out = np.empty(max(cap, 1), np.uint32)
         n = C.c_uint64()
-        check(lib().spdz_net_recv(self.h, peer, msg_type, batch, out.ctypes.data, cap, C.byref(n)))
+        rc = lib().spdz_net_recv(self.h, peer, msg_type, batch, out.ctypes.data, cap, C.byref(n))
+        if rc == 8 and grow and n.value > cap:  # SPDZ_ERR_LANE_COUNT_MISMATCH, frame still queued
+            return self.recv(peer, msg_type, batch, cap=n.value, grow=False)
+        check(rc)
         return out[: n.value].copy()
 
     def stats(self) -> tuple:

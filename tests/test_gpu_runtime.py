@@ -85,6 +85,54 @@ def test_reduce_mul_sizes(gpu, n):
     assert int(rep.outputs[0]) == want
 
 
+@pytest.mark.parametrize("n,start", [(2, 1), (9, 1), (1000, 1), (4097, 3), (1000, 2)])
+def test_reduce_mul_over_offset_load(gpu, n, start):
+    """reduce.mul of a load at a constant offset (getelementptr %x, start): the load is a
+    zero-copy view, so the product tree's pair view may be 4-byte aligned only.
+    The reference's run_local gives the cleartext product for this IR (checked here in
+    the container with oracle/_ref)."""
+    from paper_2512_11112_b200 import run_local
+    from paper_2512_11112_b200.runtime import CONST, INPUT, LOAD, NOP, REDUCE_MUL, ROOT, Graph, NodeSpec
+    g = Graph()
+    x = g.input("x", n + start, True)
+    c = g.add(NodeSpec(CONST, 1, (), False, const_val=start))
+    g.add(NodeSpec(NOP))
+    a = g.add(NodeSpec(LOAD, n, (x, c), True))
+    r = g.add(NodeSpec(REDUCE_MUL, 1, (a,), True))
+    g.root = g.add(NodeSpec(ROOT, 1, (r,), True))
+    xs = O.rand_field_vec(n + start, 3)
+    rep = run_local(g, 2, {"x": xs})
+    want = 1
+    for v in xs[start:].tolist():
+        want = want * v % P
+    assert int(rep.outputs[0]) == want
+    assert sum(rep.sigmas) % P == 0
+
+
+@pytest.mark.parametrize("b_len", [8, 1])
+def test_linear_public_public_private_bias(gpu, b_len):
+    """x and W public, b private: the node is private (graph_builder.cpp:123) and
+    y = add_public(b, W x) (runtime.cpp:289-302 then exec_add, runtime.cpp:129-162).
+    Checked against cleartext, which the reference's run_local reproduces for this IR."""
+    from paper_2512_11112_b200 import run_local
+    from paper_2512_11112_b200.runtime import LINEAR, ROOT, Graph, NodeSpec, INPUT, CONST, NOP
+    din, dout = 16, 8
+    g = Graph()
+    x = g.input("x", din, False)
+    w = g.input("W", din * dout, False)
+    b = g.input("b", b_len, True)
+    g.add(NodeSpec(CONST, 1, (), False, const_val=0))
+    g.add(NodeSpec(NOP))
+    lin = g.add(NodeSpec(LINEAR, dout, (x, w, b), True, din=din, dout=dout))
+    g.root = g.add(NodeSpec(ROOT, dout, (lin,), True))
+    xs, W, bs = O.rand_field_vec(din, 4), O.rand_field_vec(din * dout, 5), O.rand_field_vec(b_len, 6)
+    rep = run_local(g, 2, {"x": xs, "W": W, "b": bs})
+    bb = np.resize(bs.astype(object), dout)
+    want = (W.astype(object).reshape(dout, din).dot(xs.astype(object)) + bb) % P
+    np.testing.assert_array_equal(rep.outputs.astype(np.uint64), want.astype(np.uint64))
+    assert sum(rep.sigmas) % P == 0
+
+
 def test_bitflip_aborts_with_mac_check_failed(gpu, golden):
     """acceptance.cpp:112-139: a flipped payload bit on any opening aborts the run."""
     from paper_2512_11112_b200 import LocalRun, chain_graph, errors
