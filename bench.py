@@ -6,13 +6,22 @@ t1 = x*y; t2 = t1*x; t3 = t2*y; t4 = t3*t1 over <2^24 x i32> private inputs,
 phase (4 Beaver multiplies of 2^24 lanes = 67.1 M mults, open, MAC check), as
 the reference's RunReport.online_ms (runtime.cpp:534-565).  Preprocessing
 (GPU dealer) and input sharing run between steps, outside the timed region,
-exactly as the reference's online_ms excludes them.
+exactly as the reference's online_ms excludes them.  After every timed step
+(outside the timed region) 4096 random opened lanes are checked against
+cleartext.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 --impl reference times the unmodified reference CPU implementation
-(oracle/_ref/libllspdz_ref.so, runtime::run_local with one worker thread per
-host core per party) on a bounded sample of the same workload.
+(oracle/_ref/libllspdz_ref.so: PartyRuntime of runtime.cpp over the simulated
+transport, one worker thread per host core per party) on the SAME workload
+(2^24 lanes at N=1; the dealer runs once, every step gets freshly loaded copies
+of the dealt stores, outside the reference's own online_ms).
+
+The line also carries a ``linear`` block (BASELINE's "linear-layer online ms"
+half, N=1 only): C3 secret x public 1024x1024 batch 256 on the tcgen05 limb
+GEMM, C4 secret x secret 4096x4096 + MAC check, the batched 4096^3 layer, and
+the reference's run_local online ms for C3/C4 beside them.
 """
 from __future__ import annotations
 
@@ -149,38 +158,101 @@ def allmax(world, v: float) -> float:
     return float(t.item())
 
 
+# ------------------------------------------------------------------ workload
+N_MUL = {"heavy": 4, "mixed": 2}
+
+
+def workload_config(kind: str, total: int) -> dict:
+    """`config` of BOTH arms (identical for the same N, so the driver's ratio is same-config)."""
+    return {"workload": f"{kind} mul-chain ({N_MUL[kind]} Beaver multiplies + root open + MAC check), "
+                        f"2 parties, {total} lanes",
+            "lanes_total": total, "parties": 2, "field": "F_p, p = 2^32 - 5",
+            "inputs": "x, y uniform in [0, p) (synthetic), dealer seeded",
+            "l2": "working set >> 126 MB L2 (inputs larger than L2, no flush needed)",
+            "timed": "online phase (input sharing and preprocessing outside, as RunReport.online_ms)"}
+
+
+def inputs_for(shard: int, lanes: int):
+    """x, y of one lane shard (both parties' ranks of a pair draw the same values)."""
+    rng = np.random.default_rng(1234 + shard)
+    return (rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32),
+            rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32))
+
+
+def clear_chain(kind: str, x, y):
+    """the chain in cleartext mod p (the spot check of the opened outputs)."""
+    ops = {"mixed": "*+*+", "heavy": "****"}[kind]
+    f = {"*": lambda a, b: a * b % P, "+": lambda a, b: (a + b) % P}
+    a, b = x.astype(np.uint64) % P, y.astype(np.uint64) % P
+    t1 = f[ops[0]](a, b)
+    t2 = f[ops[1]](t1, a)
+    t3 = f[ops[2]](t2, b)
+    return f[ops[3]](t3, t1).astype(np.uint32)
+
+
+class SpotCheck:
+    """4096 random opened lanes per step against cleartext (outside the timed region)."""
+
+    def __init__(self, kind, x, y, lanes=4096, seed=99):
+        self.kind, self.x, self.y = kind, x, y
+        self.rng = np.random.default_rng(seed)
+        self.k = min(lanes, len(x))
+        self.checked = 0
+
+    def __call__(self, outputs, what):
+        idx = self.rng.choice(len(self.x), self.k, replace=False)
+        want = clear_chain(self.kind, self.x[idx], self.y[idx])
+        got = np.asarray(outputs)[idx]
+        if not np.array_equal(got, want):
+            bad = idx[got != want]
+            raise RuntimeError(f"{what}: {bad.size} of {self.k} spot-checked output lanes differ from "
+                               f"cleartext (first lanes {bad[:4].tolist()})")
+        self.checked += self.k
+
+
 # ------------------------------------------------------------------ reference arm
-def reference_rate(lanes: int, steps: int, warmup: int, kind: str):
-    """Times runtime::run_local of the unmodified reference (oracle/_ref)."""
-    from oracle import ref, workloads
-    threads = os.cpu_count() or 1
-    ir = workloads.chain_ir(kind, lanes)
-    rng = np.random.default_rng(0)
-    x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
-    y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
-    for _ in range(warmup):
-        ref.run_local(ir, 2, {"x": x, "y": y}, threads=threads, io_timeout_ms=600000)
-    total = 0.0
-    for _ in range(steps):
-        _, rep = ref.run_local(ir, 2, {"x": x, "y": y}, threads=threads, io_timeout_ms=600000)
-        total += rep["online_ms"]
-    mults = 4 * lanes * steps if kind == "heavy" else 2 * lanes * steps
-    return mults / (total / 1e3), total / steps, threads
-
-
 def run_reference_arm(args, world, rank):
+    """The unmodified reference (oracle/_ref) on the host cores, same workload as our arm at N=1:
+    PartyRuntime of every party over the simulated transport, dealer once, fresh store copies
+    per step; value from the reference's own RunReport.online_ms."""
     if rank != 0:
         return
-    lanes = args.cpu_sample_lanes
-    rate, ms, threads = reference_rate(lanes, args.steps, args.warmup, args.kind)
+    from oracle import ref, workloads
+    threads = os.cpu_count() or 1
+    total = args.lanes  # N=1: our arm's 2 parties x `lanes` on one GPU
+    same = world == 1
+    if not same:
+        log(f"reference arm at N={world}: timing the {args.lanes}-lane single-GPU workload as the sample")
+    x, y = inputs_for(0, total)
+    t0 = time.perf_counter()
+    b = ref.BenchRun(workloads.chain_ir(args.kind, total), 2, dealer_seed=1)
+    deal_s = time.perf_counter() - t0
+    out = np.empty(total, np.uint32)
+    spot = SpotCheck(args.kind, x, y)
+    for _ in range(args.warmup):
+        b.run({"x": x, "y": y}, threads=threads, out=out)
+    online = []
+    extra = []
+    for _ in range(args.steps):
+        _, rep = b.run({"x": x, "y": y}, threads=threads, out=out)
+        online.append(rep["online_ms"])
+        extra.append((rep["setup_ms"], rep["copy_ms"]))
+        spot(out, "reference")
+    b.close()
+    ms = float(np.sum(online)) / args.steps
+    rate = N_MUL[args.kind] * total / (ms / 1e3)
+    cfg = workload_config(args.kind, total) if same else dict(workload_config(args.kind, total), sample_of_n_gpus=world)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32 (F_p, p=2^32-5)", "data": "synthetic",
-            "config": {"workload": f"{args.kind} mul-chain, 2 parties, reference runtime::run_local (CPU)",
-                       "lanes_per_step": lanes, "full_workload_lanes": args.lanes},
+            "config": cfg, "same_workload_as_ours": same,
+            "placement": f"2 parties as host threads, {threads} worker threads per party (runtime::run_local shape)",
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{args.kind} chain of {lanes} lanes per step (bounded sample of the "
-                                       f"{args.lanes}-lane workload), {threads} worker threads per party"},
+                             "sample": f"the full {total}-lane {args.kind} chain every step; dealer once "
+                                       f"({deal_s:.1f} s), per step a fresh copy of the dealt stores "
+                                       f"(median {np.median([c for _, c in extra]):.0f} ms) and input sharing "
+                                       f"(median {np.median([s for s, _ in extra]):.0f} ms) outside online_ms"},
+            "output_spot_check": {"lanes_per_step": spot.k, "checked": spot.checked},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -204,21 +276,94 @@ def load_traffic(kernel: str):
     return None
 
 
+def linear_block(with_reference: bool) -> dict:
+    """BASELINE's "linear-layer online ms" half on this GPU (C3, C4, batched C4), device-timed
+    with CUDA events on the launching stream; the reference's run_local beside (CPU leg)."""
+    import ctypes as C
+
+    import torch
+
+    import bench_configs as bc
+    from paper_2512_11112_b200 import Context, DeviceShare, linear_graph
+    from paper_2512_11112_b200._lib import check, lib
+    from paper_2512_11112_b200.backend import dshare
+    out = {}
+    # C3: W public 1024x1024, X secret 1024x256, both planes (one 1024x1024x512 modular GEMM)
+    din = dout = 1024
+    batch = 256
+    ctx = Context(0, 0, 2, 12345)
+    ctx.use_torch_stream()
+    W = torch.from_numpy(bc.rnd(din * dout, 1)).cuda()
+    xs = DeviceShare(torch.from_numpy(bc.rnd(din * batch, 2)).cuda(), torch.from_numpy(bc.rnd(din * batch, 3)).cuda())
+    ys = DeviceShare.empty(dout * batch)
+    a = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
+    check(lib().spdz_set_gemm_path(2))
+    for _ in range(5):
+        check(lib().spdz_linear_secret_public(*a))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 50
+    e0.record()
+    for _ in range(iters):
+        check(lib().spdz_linear_secret_public(*a))
+    e1.record()
+    torch.cuda.synchronize()
+    check(lib().spdz_set_gemm_path(0))
+    us = e0.elapsed_time(e1) / iters * 1e3
+    # spot check: 64 random output cells of the value plane against exact integer W x
+    rng = np.random.default_rng(7)
+    Wh, Xh, Yh = W.cpu().numpy(), xs.vals.cpu().numpy().reshape(din, batch), ys.vals.cpu().numpy().reshape(dout, batch)
+    for _ in range(64):
+        r, c = int(rng.integers(dout)), int(rng.integers(batch))
+        if int(Yh[r, c]) != sum(int(w) * int(v) for w, v in zip(Wh[r * din:(r + 1) * din], Xh[:, c])) % P:
+            raise RuntimeError("C3 output mismatch")
+    modmacs = 2 * din * dout * batch
+    out["C3_secret_public_1024x1024_b256"] = {
+        "us": us, "modmacs": modmacs, "path": "tcgen05 kind::i8 limb GEMM (16 u8 MACs per modMAC)",
+        "i8_mac_per_s": 16 * modmacs / (us / 1e6), "frac_of_nominal_i8": 16 * modmacs / (us / 1e6) / 2.25e15,
+        "i8_peak_source": "nominal dense int8 2.25e15 MAC/s (B200)"}
+    ctx.close()
+    del W, xs, ys
+    # C4: secret x secret 4096x4096 + MAC check, 2 parties on this GPU (slice 262140: 64 tiles)
+    din = dout = 4096
+    inp = {"x": bc.rnd(din, 1), "W": bc.rnd(din * dout, 2), "b": bc.rnd(dout, 3)}
+    g = bc.gpu_online(linear_graph(din, dout), inp, reps=5, slice_=262140)
+    out["C4_secret_secret_4096x4096"] = {
+        "online_device_ms": g["online_device_ms"], "online_wall_ms": g["online_wall_ms"], "tiles": 64,
+        "kernels": {k: {"ms": round(v["ms"] / 6, 4), "GBs": round(v["GBs"] or 0, 1)} for k, v in g["kernels"].items()},
+        "timed": "mask, open [D|E], combine, root open, MAC check (both parties)"}
+    bm = bc.bmatrix_bench(4096, 4096, 4096)
+    out["C4_batched_4096x4096x4096"] = {"ms": bm["ms"], "frac_of_nominal_i8": bm["frac_of_nominal_i8"],
+                                        "timed": bm["timed"]}
+    if with_reference:
+        from oracle import ref, workloads
+        if ref.available():
+            th = os.cpu_count() or 1
+            c3in = {"x": bc.rnd(1024, 4), "W": bc.rnd(1024 * 1024, 5), "b": bc.rnd(1024, 6)}
+            one = bc.ref_online(workloads.linear_ir(1024, 1024, w_private=False), c3in, th)
+            out["C3_secret_public_1024x1024_b256"]["reference_batch1_online_ms"] = one
+            out["C3_secret_public_1024x1024_b256"]["reference_b256_online_ms_est"] = one * 256
+            out["C4_secret_secret_4096x4096"]["reference_online_ms"] = bc.ref_online(
+                workloads.linear_ir(4096, 4096), inp, th, slice_=262140)
+            out["reference_threads_per_party"] = th
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
 
     from paper_2512_11112_b200 import LocalRun, chain_graph
-    from paper_2512_11112_b200._lib import lib
 
     dev = int(os.environ.get("SPDZ_BENCH_DEVICE", local))  # override only for single-GPU tests
     torch.cuda.set_device(dev)
-    n_mul = 4 if args.kind == "heavy" else (2 if args.kind == "mixed" else 0)
+    n_mul = N_MUL[args.kind]
     coin_fn = None
     party = None
     if world == 1:
         # both parties on this GPU (each party's kernels get the whole HBM in turn)
         lanes = args.lanes
         total = lanes
+        shard = 0
         g = chain_graph(args.kind, lanes)
         run = LocalRun(g, 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1)
         parallelism = "2 parties on 1 GPU"
@@ -228,28 +373,24 @@ def run_ours(args, world, rank, local):
         # stream-memory-op ordering).  Each GPU holds one party of 2*lanes lanes, i.e. the same
         # per-GPU work as the 1-GPU run (two parties of `lanes`): weak scaling.
         from paper_2512_11112_b200 import parallel
-        assert world % 2 == 0, "multi-GPU runs need an even number of GPUs (two parties)"
-        G = world // 2
-        party, k = rank // G, rank % G
+        party, shard, G, peer = parallel.party_layout(world, rank)
         lanes = 2 * args.lanes
         total = G * lanes
         # the GPU's lanes run as `exchange_chunks` lane chunks on their own streams (ChunkedRun):
         # one chunk's opening exchange over NVLink overlaps the other chunks' kernels
         from paper_2512_11112_b200 import ChunkedRun
         run = ChunkedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=args.exchange_chunks,
-                         shard=(k * lanes, total), single_party=party, devices=[dev, dev], profile_kernels=True)
+                         shard=(shard * lanes, total), single_party=party, devices=[dev, dev], profile_kernels=True)
         import torch.distributed as dist
         blobs = [None] * world
         dist.all_gather_object(blobs, run.export_ipc())
-        peer = (1 - party) * G + k
         run.import_ipc([blobs[peer]])
         coin_fn = parallel.joint_coin
         parallelism = (f"2 parties x {G} GPUs, lane-sharded, NVLink P2P opens, "
                        f"{args.exchange_chunks} lane chunks per GPU overlapping the exchange")
     mults_step = n_mul * total  # whole job, per step
-    rng = np.random.default_rng(1234 + rank)
-    x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
-    y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
+    x, y = inputs_for(shard, lanes)
+    spot = SpotCheck(args.kind, x, y, seed=99 + rank)
     x_pin = torch.from_numpy(x).pin_memory().numpy()
     y_pin = torch.from_numpy(y).pin_memory().numpy()
     inputs = {"x": x_pin, "y": y_pin}
@@ -272,6 +413,7 @@ def run_ours(args, world, rank, local):
                     for f in a:
                         a[f] += st[f]
             return types.SimpleNamespace(online_device_ms=ms, kstat=kst, sigmas=sig,
+                                         outputs=np.concatenate([r.outputs for r in reps]),
                                          kernel_launches=sum(r.kernel_launches for r in reps))
         rep = run.online(coin_fn=coin_fn)
         if sum(rep.sigmas) % P != 0:
@@ -280,7 +422,7 @@ def run_ours(args, world, rank, local):
 
     for w in range(args.warmup):
         prepare(100 + w)
-        step()
+        spot(step().outputs, "warm-up step")
     # ---- device-timed steps (inputs resident, value) ----
     sampler = ClockSampler(dev)
     sampler.start()
@@ -300,59 +442,63 @@ def run_ours(args, world, rank, local):
             a = kstat.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0})
             for f in a:
                 a[f] += st[f]
+        spot(rep.outputs, f"timed step {k}")  # outside the timed region
     clocks = sampler.stop()
     total_ms = allmax(world, float(np.sum(dev_ms)))
     value = mults_step * args.steps / (total_ms / 1e3)
     # ---- end to end: host buffers in, opened outputs out (public API) ----
     out_pin = torch.empty(lanes, dtype=torch.uint32).pin_memory().numpy()
-    run.bind_output(out_pin)
-    streamed = world == 1 and args.e2e_chunks > 1
-    if streamed:
-        # host-streamed execution: lane chunks as exact shards on their own streams, so the
-        # PCIe transfers of one chunk overlap the kernels of another (StreamedRun)
+    e2e = {}
+    if world == 1:
+        # host-streamed execution (StreamedRun): lane chunks as exact shards on their own streams, so
+        # the PCIe transfers of one chunk overlap the kernels of another.  Headline: ONE deferred MAC
+        # check over every chunk's openings (mac="joint", as the reference's single check,
+        # runtime.cpp:467-506), pinned host inputs.  Beside it: pageable host inputs, and a MAC check
+        # per chunk (each a full SPDZ check of its own openings, overlapping later chunks' copies).
         from paper_2512_11112_b200 import StreamedRun
         run.close()
-        wts = [float(x) for x in args.e2e_weights.split(",")] if args.e2e_weights else None
-        run = StreamedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=len(wts) if wts else args.e2e_chunks,
-                          devices=[dev, dev], weights=wts)
+        wts = [float(v) for v in args.e2e_weights.split(",")] if args.e2e_weights else None
+        chunks = len(wts) if wts else args.e2e_chunks
+        variants = [("joint", inputs, "pinned"), ("joint", {"x": x, "y": y}, "pageable"),
+                    ("per_chunk", inputs, "pinned")]
+        for mac, inp, mem in variants:
+            sr = StreamedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=chunks, devices=[dev, dev],
+                             weights=wts, mac=mac)
+            sr.bind_output(out_pin)
+            for w in range(max(args.warmup, 1)):  # untimed: the first call captures each chunk's graph
+                sr.deal(4000 + w)
+                sr.run(inp)
+            torch.cuda.synchronize()
+            e2e_ms = 0.0
+            for k in range(args.steps):
+                sr.deal(5000 + k)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                rep = sr.run(inp)  # H2D, input sharing, online phase, D2H, MAC check
+                e2e_ms += (time.perf_counter() - t0) * 1e3
+                spot(rep.outputs, f"e2e ({mac}, {mem}) step {k}")
+            sr.close()
+            e2e[(mac, mem)] = e2e_ms / args.steps
+            log(f"e2e {mac} MAC check, {mem} inputs: {e2e_ms / args.steps:.3f} ms/step")
+        e2e_mode = f"host-streamed, {chunks} lane chunks, one deferred MAC check, pinned host inputs"
+        e2e_ms_step = e2e[("joint", "pinned")]
+    else:
         run.bind_output(out_pin)
-    if streamed:  # untimed warm-up (first call captures each chunk's CUDA graph)
-        for w in range(max(args.warmup, 1)):
-            run.deal(4000 + w)
-            run.run(inputs)
-        torch.cuda.synchronize()
-    if world > 1:  # chunk by chunk through one in-order H2D stream (ChunkedRun.run_e2e)
-        run.stream_copies()
-    e2e_ms = 0.0
-    parts = np.zeros(3)
-    for k in range(args.steps):
-        run.deal(5000 + k)
-        torch.cuda.synchronize()
-        barrier(world)
-        t0 = time.perf_counter()
-        if streamed:
-            rep = run.run(inputs)        # H2D, input sharing, online phase, D2H, MAC check
-            t1 = t2 = t3 = time.perf_counter()
-        elif world > 1:
+        run.stream_copies()  # chunk by chunk through one in-order H2D stream (ChunkedRun.run_e2e)
+        e2e_ms = 0.0
+        for k in range(args.steps):
+            run.deal(5000 + k)
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
             sig, _, _ = run.run_e2e(inputs if owns_inputs else None, coin_fn=coin_fn)
             parallel.verify_sharded_sigmas(sig)
-            t1 = t2 = t3 = time.perf_counter()
-        else:
-            if owns_inputs:
-                run.bind_inputs(inputs)  # H2D of the step's inputs
-            t1 = time.perf_counter()
-            run.share_inputs()
-            t2 = time.perf_counter()
-            rep = step()                 # includes D2H of the opened outputs
-            t3 = time.perf_counter()
-        e2e_ms += (t3 - t0) * 1e3
-        parts += np.array([t1 - t0, t2 - t1, t3 - t2]) * 1e3
-        barrier(world)
-    log(f"e2e per step ({'streamed, %d chunks' % args.e2e_chunks if streamed else 'serial'}): "
-        f"{e2e_ms / args.steps:.3f} ms; bind {parts[0] / args.steps:.3f} ms, share {parts[1] / args.steps:.3f} ms, "
-        f"online+D2H {parts[2] / args.steps:.3f} ms")
-    e2e_ms = allmax(world, e2e_ms)
-    e2e = mults_step * args.steps / (e2e_ms / 1e3)
+            e2e_ms += (time.perf_counter() - t0) * 1e3
+            barrier(world)
+            spot(out_pin, f"e2e step {k}")
+        e2e_ms_step = allmax(world, e2e_ms) / args.steps
+        e2e_mode = f"host-streamed per GPU, {args.exchange_chunks} lane chunks, one sharded MAC check"
+    e2e_val = mults_step / (e2e_ms_step / 1e3)
     # ---- roofline of the dominant kernel class ----
     peak, peak_kind = load_peaks()
     dom = max(("mask", "combine", "sigma", "open"), key=lambda n: kstat[n]["ms"])
@@ -365,36 +511,46 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_kind, "bytes_per_launch": st["bytes"] // max(st["launches"], 1),
                 "launch_ms": round(st["ms"] / max(st["launches"], 1), 4), "step_share": shares,
                 "all_kernels_gbs": {n: round(kstat[n]["bytes"] / max(kstat[n]["ms"], 1e-9) / 1e6, 1) for n in kstat}}
+    linear = None
+    if world == 1 and not args.no_linear:
+        linear = linear_block(with_reference=rank == 0 and not args.no_cpu_baseline)
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import ref
+            from oracle import ref, workloads
             if ref.available():
-                rate, ms, threads = reference_rate(args.cpu_sample_lanes, 2, 0, args.kind)
-                cpu_baseline = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                                "sample": f"{args.kind} chain, {args.cpu_sample_lanes} lanes x 2 runs of the "
-                                          f"reference runtime::run_local, {threads} worker threads per party"}
+                sl = args.cpu_sample_lanes
+                th = os.cpu_count() or 1
+                b = ref.BenchRun(workloads.chain_ir(args.kind, sl), 2, dealer_seed=1)
+                xs, ys = inputs_for(0, sl)
+                oms = [b.run({"x": xs, "y": ys}, threads=th)[1]["online_ms"] for _ in range(2)]
+                b.close()
+                cpu_baseline = {"value": n_mul * sl / (np.mean(oms) / 1e3), "unit": UNIT, "cores": th,
+                                "kind": "reference",
+                                "sample": f"{args.kind} chain, {sl} lanes x 2 runs of the reference PartyRuntime "
+                                          f"(runtime::run_local shape), {th} worker threads per party; the "
+                                          f"full-size same-config timing is bench.py --impl reference"}
             else:
                 cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                 "sample": "oracle/_ref not built"}
         except Exception as e:  # the baseline is reported, never the measured arm
             cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0:
+        e2e_line = {"value": e2e_val, "unit": UNIT, "mode": e2e_mode, "h2d_bytes_per_step": 2 * total * 4,
+                    "d2h_bytes_per_step": total * 4 * (1 if world == 1 else 2), "ms_per_step": e2e_ms_step}
+        if world == 1:
+            e2e_line["pageable_inputs"] = {"value": mults_step / (e2e[("joint", "pageable")] / 1e3),
+                                           "ms_per_step": e2e[("joint", "pageable")]}
+            e2e_line["per_chunk_mac_check"] = {"value": mults_step / (e2e[("per_chunk", "pinned")] / 1e3),
+                                               "ms_per_step": e2e[("per_chunk", "pinned")]}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u32 (F_p, p=2^32-5)", "data": "synthetic",
-                "config": {"workload": f"{args.kind} mul-chain (4 Beaver multiplies + root open + MAC check), "
-                                       f"2 parties, {total} lanes",
-                           "lanes_total": total, "parties": 2, "parallelism": parallelism,
-                           "l2": "working set >> 126 MB L2 (inputs larger than L2, no flush needed)",
-                           "timed": "online phase only (dealer + input sharing between steps, untimed)"},
+                "config": workload_config(args.kind, total), "parallelism": parallelism,
                 "clocks": clocks, "gpu_launches": launches,
-                "e2e": {"value": e2e, "unit": UNIT,
-                        "mode": (f"host-streamed, {args.e2e_chunks} lane chunks" if streamed else
-                                 f"host-streamed per GPU, {args.exchange_chunks} lane chunks" if world > 1 else "serial"), "h2d_bytes_per_step": 2 * total * 4,
-                        "d2h_bytes_per_step": total * 4 * (1 if world == 1 else 2),
-                        "ms_per_step": e2e_ms / args.steps},
-                "roofline": roofline, "cpu_baseline": cpu_baseline}
+                "output_spot_check": {"lanes_per_step": spot.k, "checked": spot.checked,
+                                      "against": "cleartext chain of the step's inputs"},
+                "e2e": e2e_line, "roofline": roofline, "linear": linear, "cpu_baseline": cpu_baseline}
         print(json.dumps(line), flush=True)
     barrier(world)  # peers may still hold IPC mappings of our buffers
     run.close()
@@ -408,11 +564,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kind", default="heavy", choices=["heavy", "mixed"])
     ap.add_argument("--lanes", type=int, default=1 << 24)
-    ap.add_argument("--cpu-sample-lanes", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample-lanes", type=int, default=1 << 20,
+                    help="our arm's cpu_baseline leg (a bounded sample; --impl reference runs the full size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-linear", action="store_true", help="skip the linear-layer block")
     ap.add_argument("--exchange-chunks", type=int, default=2,
                     help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run (1 = serial)")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run")
     ap.add_argument("--e2e-weights", default="", help="relative lane-chunk sizes of the host-streamed e2e run "
                     "(comma-separated; overrides --e2e-chunks)")
     args = ap.parse_args()

@@ -112,6 +112,12 @@ def lib():
                                              C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), U64P, U32P, C.c_uint64,
                                              C.POINTER(C.c_uint64), np.ctypeslib.ndpointer(np.float64),
                                              C.POINTER(C.c_uint64)]
+        L.reft_bench_create.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_uint64]
+        L.reft_bench_create.restype = C.c_void_p
+        L.reft_bench_free.argtypes = [C.c_void_p]
+        L.reft_bench_run.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_char_p),
+                                     C.POINTER(C.c_void_p), U64P, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                     np.ctypeslib.ndpointer(np.float64)]
         L.reft_kernel_bench.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]
         L.reft_kernel_bench.restype = C.c_double
         L.reft_time_beaver_kernels.argtypes = [C.c_uint64, C.c_int]
@@ -375,6 +381,38 @@ def run_local(ir_text: str, n_parties: int, inputs: dict, threads: int = 1, slic
     report = dict(setup_ms=rep[0], online_ms=rep[1], bytes_sent=int(rep[2]), scalar_triples=int(rep[3]),
                   matrix_triples=int(rep[4]), digest=dig.value)
     return out[: n.value].copy(), report
+
+
+class BenchRun:
+    """runtime::run_local with the dealer run once (ref_tools.cpp reft_bench_*): every
+    ``run`` gives each party a freshly loaded copy of its dealt store and runs the
+    unmodified PartyRuntime; returns (outputs, report) with the reference's own
+    ``online_ms`` (input sharing and the store copy excluded, as in RunReport)."""
+
+    def __init__(self, ir_text: str, n_parties: int, slice_: int = 262140, dealer_seed: int = 1):
+        self.h = lib().reft_bench_create(ir_text.encode(), n_parties, slice_, dealer_seed)
+        if not self.h:
+            raise RefError(99, lib().reft_last_error().decode())
+
+    def run(self, inputs: dict, threads: int = 1, io_timeout_ms: int = 600000, out: np.ndarray | None = None):
+        k, cn, cv, cl, keep = _inputs(inputs)
+        n = C.c_uint64()
+        rep = np.zeros(4, np.float64)
+        cap = 0 if out is None else out.size
+        _check(lib().reft_bench_run(self.h, threads, io_timeout_ms, k, cn, cv, cl,
+                                    None if out is None else out.ctypes.data, cap, C.byref(n), rep))
+        return n.value, dict(setup_ms=rep[0], online_ms=rep[1], copy_ms=rep[2])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().reft_bench_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def write_circuit_file(ir_text: str, path):

@@ -672,4 +672,96 @@ double reft_time_beaver_kernels(uint64_t lanes, int reps) {
     return best;
 }
 
+// ---- same-config reference timing (bench.py --impl reference) ----
+// runtime::run_local (runtime.cpp:586-613) split so the dealer runs once: `reft_bench_create`
+// compiles the graph and deals every party's store (make_dealer_stores, triple_store.cpp:248);
+// each `reft_bench_run` gives every party a freshly loaded copy of its store (all cursors and
+// consumed bitmaps at zero, as read_store_file returns one) and runs the unmodified
+// PartyRuntime over the simulated transport.  report: [setup_ms, online_ms, copy_ms] (max
+// over parties; online_ms is the reference's own RunReport.online_ms).
+struct RefBench {
+    circuit::CircuitGraph g;
+    std::vector<std::shared_ptr<spdz::TripleStore>> stores;
+    int n = 2;
+    uint64_t slice = 262140;
+};
+
+void* reft_bench_create(const char* ir_text, int n_parties, uint64_t slice, uint64_t dealer_seed) {
+    void* h = nullptr;
+    int rc = guard([&] {
+        auto b = std::make_unique<RefBench>();
+        b->g = compile_text(ir_text);
+        b->n = n_parties;
+        b->slice = slice;
+        const uint64_t loop_iters_hint = 64;
+        auto demand = preproc::compute_triple_demand(b->g, slice, loop_iters_hint);
+        spdz::Dealer dealer(n_parties, dealer_seed);
+        b->stores = spdz::make_dealer_stores(dealer, demand.scalars, demand.matrix_shapes, demand.input_masks,
+                                             loop_iters_hint);
+        h = b.release();
+    });
+    return rc == RC_OK ? h : nullptr;
+}
+
+void reft_bench_free(void* h) { delete static_cast<RefBench*>(h); }
+
+int reft_bench_run(void* h, int threads, uint64_t io_timeout_ms, int n_inputs, const char* const* names,
+                   const uint32_t* const* vals, const uint64_t* lens, uint32_t* out, uint64_t cap,
+                   uint64_t* out_len, double* report) {
+    return guard([&] {
+        auto* b = static_cast<RefBench*>(h);
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::shared_ptr<spdz::TripleStore>> fresh;
+        for (auto& s : b->stores) {
+            auto c = std::make_shared<spdz::TripleStore>();
+            c->party = s->party;
+            c->n_parties = s->n_parties;
+            c->alpha_share = s->alpha_share;
+            c->loop_iters = s->loop_iters;
+            c->a_vals = s->a_vals;
+            c->a_macs = s->a_macs;
+            c->b_vals = s->b_vals;
+            c->b_macs = s->b_macs;
+            c->c_vals = s->c_vals;
+            c->c_macs = s->c_macs;
+            c->matrix = s->matrix;
+            c->masks = s->masks;
+            fresh.push_back(std::move(c));
+        }
+        auto inputs = make_inputs(n_inputs, names, vals, lens);
+        const double copy_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        runtime::RunOptions opts;
+        opts.threads = threads;
+        opts.slice = b->slice;
+        auto sessions = net::make_sim_sessions(b->n);
+        for (auto& s : sessions) s->io_timeout = std::chrono::milliseconds(io_timeout_ms ? io_timeout_ms : 600000);
+        std::vector<runtime::RunReport> reps(b->n);
+        std::vector<std::exception_ptr> errors(b->n);
+        std::vector<std::thread> th;
+        for (int i = 0; i < b->n; ++i)
+            th.emplace_back([&, i] {
+                try {
+                    runtime::PartyRuntime rt(b->g, fresh[i], sessions[i], opts);
+                    reps[i] = rt.run(inputs);
+                } catch (...) {
+                    errors[i] = std::current_exception();
+                }
+            });
+        for (auto& t : th) t.join();
+        for (auto& e : errors)
+            if (e) std::rethrow_exception(e);
+        double online = 0, setup = 0;
+        for (auto& r : reps) {
+            online = std::max(online, r.online_ms);
+            setup = std::max(setup, r.setup_ms);
+        }
+        auto& r0 = reps.at(0);
+        *out_len = r0.outputs.size();
+        if (out) std::memcpy(out, r0.outputs.data(), std::min<uint64_t>(cap, r0.outputs.size()) * 4);
+        report[0] = setup;
+        report[1] = online;
+        report[2] = copy_ms;
+    });
+}
+
 }  // extern "C"

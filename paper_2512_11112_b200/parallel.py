@@ -32,6 +32,17 @@ def shard_range(total: int, world: int, rank: int):
     return off, base + (1 if rank < extra else 0)
 
 
+def party_layout(world: int, rank: int):
+    """Rank -> (party, shard, G, peer_rank) of the 2-party multi-GPU layout:
+    party p owns ranks [p*G, (p+1)*G) with G = world/2; rank k of party 0 and rank k of
+    party 1 hold lane shard k and open to each other (peer_rank)."""
+    if world < 2 or world % 2:
+        raise ValueError("the two-party layout needs an even number of ranks")
+    G = world // 2
+    party, shard = divmod(rank, G)
+    return party, shard, G, (1 - party) * G + shard
+
+
 def _fnv_u64(v: int, seed: int = FNV_SEED) -> int:
     b = (C.c_uint64 * 1)(v)
     return lib().spdz_fnv1a64(b, 8, seed)

@@ -105,3 +105,20 @@ def test_two_rank_coin_and_sigma_verification_gloo():
     assert ranges == [(0, 500), (500, 500)]
     verdicts = [m[1] for m in msgs if len(m) == 2]
     assert verdicts == ["MacCheckFailed", "MacCheckFailed"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_party_layout(world):
+    """bench.py's N-GPU mapping: every rank has exactly one peer of the other party with the
+    same shard, each party owns world/2 ranks, and the pairing is an involution."""
+    from paper_2512_11112_b200 import parallel
+    seen = set()
+    for rank in range(world):
+        party, shard, G, peer = parallel.party_layout(world, rank)
+        assert G == world // 2 and 0 <= shard < G and party in (0, 1)
+        p2, s2, _, back = parallel.party_layout(world, peer)
+        assert p2 == 1 - party and s2 == shard and back == rank
+        seen.add((party, shard))
+    assert len(seen) == world
+    with pytest.raises(ValueError):
+        parallel.party_layout(3, 0)
