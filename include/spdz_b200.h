@@ -146,6 +146,11 @@ int spdz_diag_rep_check(spdz_ctx* ctx, const uint64_t* d_in, uint64_t n, uint32_
  * re-layout (results invalid while either is set); bit 6 / bit 7 force the 32- / 64-column
  * output tile (results valid).  Attribution experiments and tests only. */
 int spdz_diag_gemm_tc_flags(uint32_t flags);
+/* Diagnostic timeline of the tcgen05 GEMM kernel: when dev_buf (device memory, 8 u64 per
+ * CTA) is set, every CTA writes %globaltimer at entry, after setup, after the dependent-launch
+ * wait, at its first full stage, after its last MMA commit, when the epilogue gets the
+ * accumulators, after its stores and at exit.  NULL switches it off. */
+int spdz_diag_gemm_tc_timeline(void* dev_buf);
 /* Number of kernels this library launched on any context since load (evidence counter). */
 uint64_t spdz_kernel_launches(void);
 

@@ -96,6 +96,7 @@ _SIGS = {
     "spdz_capability": (C.c_int, [vp, C.POINTER(Capability)]),
     "spdz_kernel_launches": (C.c_uint64, []),
     "spdz_diag_gemm_tc_flags": (C.c_int, [C.c_uint32]),
+    "spdz_diag_gemm_tc_timeline": (C.c_int, [C.c_void_p]),
     "spdz_diag_imad_wide_rate": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "spdz_diag_rep_check": (C.c_int, [vp, vp, C.c_uint64, vp]),
     "spdz_add_batch": (C.c_int, [vp, C.POINTER(Share), C.POINTER(Share), C.POINTER(Share)]),

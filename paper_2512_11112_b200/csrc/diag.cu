@@ -85,10 +85,16 @@ extern "C" int spdz_diag_imad_wide_rate(spdz_ctx* ctx, double* wide_per_s, doubl
 
 namespace spdzb200 {
 void modgemm_tc_debug(uint32_t flags);
+void modgemm_tc_timeline(uint64_t* dev_buf);
 }
 
 // Diagnostic switches of the tcgen05 GEMM (gemm_tc.cu g_tc_dbg): bit 2 skips the GEMM kernel,
 // bit 3 the re-layout kernels (results invalid while set); bits 6/7 force the 32/64-column tile.
+extern "C" int spdz_diag_gemm_tc_timeline(void* dev_buf) {
+    spdzb200::modgemm_tc_timeline(static_cast<uint64_t*>(dev_buf));
+    return 0;
+}
+
 extern "C" int spdz_diag_gemm_tc_flags(uint32_t flags) {
     spdzb200::modgemm_tc_debug(flags);
     return 0;

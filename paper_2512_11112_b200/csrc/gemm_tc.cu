@@ -73,6 +73,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// diagnostic timeline (spdz_diag_gemm_tc_timeline): per CTA 8 %globaltimer stamps
+__device__ __forceinline__ void tl_mark(uint64_t* tl, uint32_t slot) {
+    if (tl) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tl[blockIdx.x * 8 + slot] = t;
+    }
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -136,7 +145,7 @@ template <int TN>
 __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __restrict__ At,
                                                                const uint8_t* __restrict__ Bt, uint32_t M, uint32_t N,
                                                                uint32_t KB, uint32_t tiles_n, uint32_t n_tiles,
-                                                               TcOut out, uint32_t dbg) {
+                                                               TcOut out, uint32_t dbg, uint64_t* tl) {
     using L = TcSmem<TN>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
@@ -147,6 +156,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     uint64_t* tempty = tfull + 1;        // epilogue drained TMEM (4 warp arrivals)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) tl_mark(tl, 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -166,9 +176,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) tl_mark(tl, 1);
     // programmatic dependent launch: everything above overlapped the re-layout kernel;
     // its limb images (and any earlier writes) are visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) tl_mark(tl, 2);
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer ----
@@ -202,6 +214,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     const uint32_t s = g % kStages;
                     mbar_wait(&full[s], (g / kStages) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (g == 0) tl_mark(tl, 3);
                     const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
                     if (dbg & 2) {  // diagnostic: no MMAs (attribution only, results invalid)
                         mbar_arrive(&empty[s]);
@@ -230,6 +243,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                 if (dbg & 2) mbar_arrive(tfull);
                 else mma_commit(tfull);  // accumulators of this tile complete
             }
+            tl_mark(tl, 4);
         }
     } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
         const uint32_t quarter = warp & 3;
@@ -241,6 +255,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             const uint32_t row = mt * TM + quarter * 32 + lane;
             mbar_wait(tfull, it & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
+            if (warp == 2 && lane == 0) tl_mark(tl, 5);
 #pragma unroll 1
             for (int cc = 0; cc < TN / 16; ++cc) {
                 uint32_t v[7][16];
@@ -312,10 +327,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                     }
                 }
             }
+            if (warp == 2 && lane == 0) tl_mark(tl, 6);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (threadIdx.x == 0) tl_mark(tl, 7);
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
 }
@@ -444,6 +461,7 @@ __global__ void __launch_bounds__(256) k_tile_both(RowsArgs ra, ColsArgs ca, uin
 // loads, bit 1 the MMAs, bit 2 the GEMM kernel, bit 3 the re-layout kernels (results invalid
 // while any is set); bit 6 / bit 7 force the 32- / 64-column tile width (results valid).
 uint32_t g_tc_dbg = 0;
+uint64_t* g_tc_tl = nullptr;  // diagnostic timeline buffer (8 stamps per CTA), or null
 
 // Re-layout both operands into limb images (B tiles BN columns wide), then run
 // the GEMM kernel with TN = BN.
@@ -492,7 +510,7 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;  // overlap our prologue with the re-layout kernel's tail
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_modgemm_tc<BN>, (const uint8_t*)At, (const uint8_t*)Bt, M, N, KB,
-                                       tiles_n, n_tiles, out, g_tc_dbg & 3u);
+                                       tiles_n, n_tiles, out, g_tc_dbg & 3u, g_tc_tl);
     ++g_kernel_launches;
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -501,6 +519,7 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
 }  // namespace
 
 void modgemm_tc_debug(uint32_t flags) { g_tc_dbg = flags; }
+void modgemm_tc_timeline(uint64_t* dev_buf) { g_tc_tl = dev_buf; }
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch) {
     din = std::min<uint32_t>(din, kMaxKSlice);  // one K slice at a time
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;

@@ -684,7 +684,7 @@ struct Exec {
                 dev(r, p);
                 if (!xp && !wp) {  // public x public: y = W x, then exec_add(y, b)
                     lk(launch_modgemm(c->stream, 1, dout, din, 1, w.pub, w.pub, x.pub, nullptr, st.lin_tmp,
-                                      st.out.pub),
+                                      st.lin_tmp + dout),
                        "modgemm");
                     if (b.is_public) {
                         lk(launch_pub_binop(c->stream, 0, st.lin_tmp, false, b.pub, b.lanes != dout, st.out.pub, dout,

@@ -356,7 +356,7 @@ void plan_buffers(spdz_run* r) {
                         // a private bias gives add_public(b, W x) (runtime.cpp:129-162)
                         if (n.n_operands > 2 && !opnd(2).is_public) priv_out(n.dout);
                         else pub_out(n.dout);
-                        st.lin_tmp = r->alloc(p, n.dout);
+                        st.lin_tmp = r->alloc(p, 2ull * n.dout);  // W x (the GEMM writes two planes)
                     } else if (x.is_public != w.is_public) {
                         priv_out(n.dout);
                         st.lin_tmp = r->alloc(p, 2ull * n.dout);

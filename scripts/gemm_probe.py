@@ -107,6 +107,36 @@ if "--prepared" in sys.argv:  # W laid out once (spdz_linear_weights): per call 
     torch.cuda.synchronize()
     print(f"prepared W: graphed {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call", flush=True)
 
+if "--timeline" in sys.argv:
+    # per-CTA %globaltimer stamps of the GEMM kernel (relative to the earliest CTA entry), for
+    # the full call and for the GEMM alone with the diagnostic switches
+    check(lib().spdz_set_gemm_path(2))
+    buf = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    names = ["entry", "setup", "pdl_wait", "first_full", "mma_done", "epi_start", "epi_done", "exit"]
+    for flags, name in ((0, "full call (re-layout + gemm, PDL)"), (8, "gemm kernel only"),
+                        (11, "gemm, no loads no MMAs"), (9, "gemm, no loads"), (10, "gemm, no MMAs")):
+        lib().spdz_diag_gemm_tc_flags(BASE | flags)
+        for _ in range(3):
+            check(lib().spdz_linear_secret_public(*args))
+        torch.cuda.synchronize()
+        buf.zero_()
+        lib().spdz_diag_gemm_tc_timeline(buf.data_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        check(lib().spdz_linear_secret_public(*args))
+        e1.record()
+        torch.cuda.synchronize()
+        lib().spdz_diag_gemm_tc_timeline(None)
+        t = buf.view(148, 8).cpu().numpy()
+        t = t[t[:, 0] > 0]
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1000.0
+        print(f"timeline [{name}] {len(t)} CTAs, event {e0.elapsed_time(e1) * 1000:.1f} us:", flush=True)
+        for k, nm in enumerate(names):
+            col = rel[:, k]
+            print(f"   {nm:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")
+    lib().spdz_diag_gemm_tc_flags(BASE)
+
 if "--int8-peak" in sys.argv:
     # measured dense int8 tensor peak on this device: cuBLASLt IMMA through torch._int_mm
     for nn in (8192, 16384):
