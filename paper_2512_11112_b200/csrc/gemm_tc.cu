@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                 }
             }
         }
+        __syncwarp();  // reconverge before the final (aligned) block barrier
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer ----
             constexpr uint32_t id4 = idesc_i8<4 * TN>(), id3 = idesc_i8<3 * TN>(), id1 = idesc_i8<TN>();
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             }
             tl_mark(tl, 4);
         }
+        __syncwarp();
     } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
         const uint32_t quarter = warp & 3;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);

@@ -824,6 +824,106 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
     }
 }
 
+// Balanced variant (16-byte path): the dout x din cell space is one flat range of uint4
+// groups split evenly over every resident warp of a one-wave grid, so no warp holds more than
+// its share (a warp per row leaves a 1.15-wave tail at 4096 rows: 4096 warps on 148 x 24 warp
+// slots).  A warp walks its range row segment by row segment; each segment's five lazy sums
+// are warp-reduced and added to the row's u64 accumulators (scratch, zero between launches),
+// and the warp that completes a row (its lane count reaches din/4) finalises it: C + sums,
+// party 0's de, alpha_i de, bias (spdz.cpp:117-123, linear.cpp:59) — then re-zeroes the
+// row's scratch.  Sums stay below 2^64: a segment adds < 2^40 and a row has at most din/4
+// segments.
+__global__ void __launch_bounds__(kThreads, 3) k_matrix_combine2_flat(MC2Args a, unsigned long long* acc_rows,
+                                                                      unsigned int* done_rows) {
+    const uint32_t din4 = a.din / 4;
+    const uint64_t cells = (uint64_t)a.din * a.rows;
+    const uint64_t U = (uint64_t)din4 * a.rows;
+    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t u0 = U * w / warps;
+    const uint64_t u1 = U * (w + 1) / warps;
+    while (u0 < u1) {
+        const uint32_t r = (uint32_t)(u0 / din4);
+        const uint64_t rbase = (uint64_t)r * din4;
+        const uint64_t rend = u1 < rbase + din4 ? u1 : rbase + din4;
+        const uint64_t toff = (uint64_t)(r / a.rpt) * a.din;
+        const uint4* E4 = reinterpret_cast<const uint4*>(a.opened + cells + toff);
+        const uint4* B4[2][2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            B4[p][0] = reinterpret_cast<const uint4*>(a.B[p][0] + toff);
+            B4[p][1] = reinterpret_cast<const uint4*>(a.B[p][1] + toff);
+        }
+        unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
+        for (uint64_t gg = u0 + lane; gg < rend; gg += 32) {
+            const uint32_t c4 = (uint32_t)(gg - rbase);
+            const uint4 d0 = ld4(a.D0, gg), d1 = ld4(a.D1, gg);
+            uint4 av[2], am[2], bv[2], bm[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                av[p] = ld4(a.A[p][0], gg);
+                am[p] = ld4(a.A[p][1], gg);
+            }
+            const uint4 e4 = E4[c4];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                bv[p] = B4[p][0][c4];
+                bm[p] = B4[p][1][c4];
+            }
+            const uint32_t d[4] = {fp_add(d0.x, fp_reduce32(d1.x)), fp_add(d0.y, fp_reduce32(d1.y)),
+                                   fp_add(d0.z, fp_reduce32(d1.z)), fp_add(d0.w, fp_reduce32(d1.w))};
+            const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const uint32_t AV[4] = {av[p].x, av[p].y, av[p].z, av[p].w};
+                const uint32_t AM[4] = {am[p].x, am[p].y, am[p].z, am[p].w};
+                const uint32_t BV[4] = {bv[p].x, bv[p].y, bv[p].z, bv[p].w};
+                const uint32_t BM[4] = {bm[p].x, bm[p].y, bm[p].z, bm[p].w};
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
+                    acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
+                }
+            }
+            st4(a.opened, gg, d);
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[q] = warp_sum(fold1(acc[q]));
+        if (lane == 0) {
+            unsigned long long* ar = acc_rows + (uint64_t)r * 5;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) atomicAdd(ar + q, acc[q]);
+            __threadfence();
+            const uint32_t seg = (uint32_t)(rend - u0);
+            if (atomicAdd(done_rows + r, seg) + seg == din4) {  // last segment of row r: finalise it
+                __threadfence();
+                unsigned long long sum[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) sum[q] = atomicExch(ar + q, 0ull);
+                done_rows[r] = 0;
+                const uint32_t de = fp_reduce64(sum[4]);
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(sum[2 * p]));
+                    if (p == 0) vr = fp_add(vr, de);
+                    uint32_t mr = fp_add(fp_reduce64((unsigned long long)a.Cc[p][1][r] + fp_reduce64(sum[2 * p + 1])),
+                                         fp_mul(a.alpha[p], de));
+                    if (a.bias[p][0]) {
+                        vr = fp_add(vr, a.bias[p][0][r]);
+                        mr = fp_add(mr, a.bias[p][1][r]);
+                    }
+                    a.z[p][0][r] = vr;
+                    a.z[p][1][r] = mr;
+                }
+            }
+        }
+        u0 = rend;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // CUDA-core modular GEMM: C (MxN) = A (MxK) * B (KxN) mod p, row-major.
 // A is split into 16-bit halves when staged to shared memory, so each MAC is
@@ -1252,12 +1352,28 @@ cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, u
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms) {
+cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms, unsigned long long* acc_rows,
+                                   unsigned int* done_rows) {
     if (a.rows == 0) return cudaSuccess;
     if (a.rpt == 0) return cudaErrorInvalidValue;
     bool v4 = a.din % 4 == 0 && aligned16(a.D0) && aligned16(a.D1) && aligned16(a.opened);
     for (int p = 0; p < 2; ++p)
         v4 = v4 && aligned16(a.A[p][0]) && aligned16(a.A[p][1]) && aligned16(a.B[p][0]) && aligned16(a.B[p][1]);
+    static const bool flat_off = std::getenv("SPDZ_MC2_ROWS") != nullptr;  // experiments: the row-per-warp kernel
+    if (v4 && acc_rows && done_rows && !flat_off) {
+        static int per_sm = 0;
+        if (!per_sm) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matrix_combine2_flat, kThreads, 0) !=
+                    cudaSuccess || per_sm < 1)
+                per_sm = 1;
+        }
+        const uint64_t units = (uint64_t)(a.din / 4) * a.rows;
+        uint64_t grid = (uint64_t)sms * per_sm;
+        const uint64_t need = (units + kThreads - 1) / kThreads;  // small layers: no idle warps
+        if (need < grid) grid = need ? need : 1;
+        k_matrix_combine2_flat<<<(int)grid, kThreads, 0, s>>>(a, acc_rows, done_rows);
+        return launched();
+    }
     static const int force_g = [] {  // SPDZ_MC2_G=32|256: override the row-group choice (experiments)
         const char* e = std::getenv("SPDZ_MC2_G");
         return e ? std::atoi(e) : 0;

@@ -69,7 +69,10 @@ struct MC2Args {
     uint32_t* z[2][2];
     uint32_t* opened;
 };
-cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms);
+// acc_rows (5 u64 per row) / done_rows (u32 per row): zeroed scratch for the balanced kernel
+// (left zeroed); null selects the warp-per-row kernel
+cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms, unsigned long long* acc_rows = nullptr,
+                                   unsigned int* done_rows = nullptr);
 // Input sharing for both parties of a 2-party run on one GPU: mask = {v0, m0, v1, m1}
 // input-mask shares, out = {v0, m0, v1, m1} input shares (preproc.cpp:205-243).
 cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uint32_t* r_clear,

@@ -752,6 +752,8 @@ struct Exec {
             lk(cudaMemcpyAsync(snap + cells, x.m, din * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "snapshot x.m");
             return {snap, snap + cells};
         };
+        bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+        for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -771,14 +773,20 @@ struct Exec {
                 lk(launch_bcast(c->stream, b.v, b.m, st.bias_v, st.bias_m, dout, c->sms), "bcast");
             // mask_tile for every tile: [D (all rows) | E_t for every tile]
             const int tk = tbegin(p);
-            lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
+            if (!fuse2) {
+                lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
+            } else if (p == 0) {  // both parties' D = W.v - A.v in one pass (d = x - a, e = y - b of mul_mask)
+                auto& P1 = r->parties[1];
+                const Val& w1 = P1.ns[n.operands[1]].out;
+                lk(launch_mul_mask(c->stream, w.v, w1.v, st.mA[0], P1.ns[id].mA[0], st.payload, P1.ns[id].payload,
+                                   cells, c->sms),
+                   "mask D (both parties)");
+            }
             lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
-            tend(p, tk, SPDZ_KSTAT_MASK, 12 * cells + 12 * etot);
+            tend(p, tk, SPDZ_KSTAT_MASK, (fuse2 ? (p == 0 ? 24 * cells : 0) : 12 * cells) + 12 * etot);
             sent[p] = publish(p, slot_of(id, 0));
             if (r->net) net_send_tiles(p, batch0, st.payload, din, lt);
         }
-        bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
-        for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
         if (fuse2) {  // both parties in one pass: [D|E] opened and logged once, per-party rows
             auto &P0 = r->parties[0], &P1 = r->parties[1];
             auto &s0 = P0.ns[id], &s1 = P1.ns[id];
@@ -806,7 +814,9 @@ struct Exec {
                 a.z[p][1] = st.out.m;
             }
             a.opened = s0.opened;
-            lk(launch_matrix_combine2(S(r, 0), a, SMS(r, 0)), "k_matrix_combine2");
+            auto* acc_rows = reinterpret_cast<unsigned long long*>(s0.mc2_scratch);
+            auto* done_rows = reinterpret_cast<unsigned int*>(s0.mc2_scratch + 10ull * dout);
+            lk(launch_matrix_combine2(S(r, 0), a, SMS(r, 0), acc_rows, done_rows), "k_matrix_combine2");
             // D0 4 + D1 4 + two parties' A.v A.m 16 + opened D 4 per cell (B, E from cache)
             tend(0, tk, SPDZ_KSTAT_COMBINE, 28 * cells);
             r->exchanged += 2 * (cells + etot) * 4;

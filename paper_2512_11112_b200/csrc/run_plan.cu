@@ -374,6 +374,10 @@ void plan_buffers(spdz_run* r) {
                         st.bias_v = r->alloc(p, n.dout);
                         st.bias_m = r->alloc(p, n.dout);
                         st.lin_tmp = r->alloc(p, 2ull * n.dout);
+                        if (r->n == 2 && p == 0 && r->parties[0].local && r->parties[1].local) {
+                            st.mc2_scratch = r->alloc(p, 11ull * n.dout);  // 5 x u64 + u32 per row
+                            cuda_check(cudaMemset(st.mc2_scratch, 0, 44ull * n.dout), "memset(mc2 scratch)");
+                        }
                     }
                     break;
                 }

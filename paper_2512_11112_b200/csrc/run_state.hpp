@@ -109,6 +109,7 @@ struct NodeState {                  // per party, per node
     uint32_t *mA[2] = {nullptr, nullptr}, *mB[2] = {nullptr, nullptr}, *mC[2] = {nullptr, nullptr};
     uint32_t *mA0[2] = {nullptr, nullptr}, *mB0[2] = {nullptr, nullptr}, *mC0[2] = {nullptr, nullptr};  // exec 0
     uint32_t* lin_tmp = nullptr;    // public x public scratch
+    uint32_t* mc2_scratch = nullptr; // co-located combine: 5 u64 sums + 1 u32 count per row (zeroed)
     // control flow: a Beaver node's opened values and operand MAC shares, one slot per
     // execution (the MAC check reads every execution's record after the last one)
     uint32_t* opened_all = nullptr;

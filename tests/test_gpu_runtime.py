@@ -418,3 +418,48 @@ def test_bitflip_on_linear_layer_aborts(gpu):
         with pytest.raises(errors.MacCheckFailed):
             r.online()
         r.close()
+
+
+def _clear_linear(W, x, b, din, dout):
+    """exact W x + b mod p (int64 on the GPU, x in 16-bit halves)."""
+    import torch
+    Wt = torch.from_numpy(W.astype(np.int64)).cuda().view(dout, din)
+    xt = torch.from_numpy(x.astype(np.int64)).cuda()
+    lo, hi = xt & 0xFFFF, xt >> 16
+    acc_lo = ((Wt * lo) % P).sum(1) % P
+    acc_hi = ((Wt * hi) % P).sum(1) % P
+    bt = torch.from_numpy(np.resize(b, dout).astype(np.int64)).cuda()
+    return ((acc_lo + acc_hi * 65536 % P) % P + bt).remainder(P).cpu().numpy().astype(np.uint32)
+
+
+@pytest.mark.parametrize("din,dout,slice_", [(1028, 300, 262140), (4096, 257, 8192), (36, 4100, 262140),
+                                             (4096, 4096, 262140), (1030, 33, 262140)])
+def test_colocated_linear_combine_equals_per_party(gpu, din, dout, slice_):
+    """The co-located secret x secret layer (both parties' D masked in one pass, the balanced
+    k_matrix_combine2 with per-row last-arriver finalisation; din % 4 != 0 takes the row
+    kernel) against the per-party path (one stream per party: mask + k_matrix_combine<1>):
+    every output share of both parties and both sigmas are bit-exact; the opened output is
+    W x + b.  Run twice on one LocalRun so the combine's row scratch is shown to re-zero."""
+    from paper_2512_11112_b200 import LocalRun, linear_graph
+    coin = 0x1234
+    x, W, b = O.rand_field_vec(din, 1), O.rand_field_vec(din * dout, 2), O.rand_field_vec(dout, 3)
+    inp = {"x": x, "W": W, "b": b}
+    g = linear_graph(din, dout)
+    lin = next(i for i, nd in enumerate(g.nodes) if nd.kind == 7)
+    want = _clear_linear(W, x, b, din, dout)
+    runs = {}
+    for per_party in (False, True):
+        r = LocalRun(g, 2, slice_=slice_, coin=coin, stream_per_party=per_party)
+        for rep_i in range(2):
+            r.deal(7 + rep_i)
+            r.bind_inputs(inp)
+            r.share_inputs()
+            rep = r.online()
+            np.testing.assert_array_equal(rep.outputs, want)
+            assert sum(rep.sigmas) % P == 0
+        runs[per_party] = (rep.sigmas, [r.node_share_host(p, lin) for p in range(2)])
+        r.close()
+    assert runs[False][0] == runs[True][0]
+    for p in range(2):
+        for k in range(2):
+            np.testing.assert_array_equal(runs[False][1][p][k], runs[True][1][p][k])
