@@ -421,6 +421,15 @@ typedef struct spdz_run_options {
      * (spdz_run_attach_net before the online phase); their opening buffers are
      * mirrored in local HBM and filled from the peers' frames. */
     int32_t network;
+    /* Node-level stream scheduling of straight-line graphs (the reference scheduler's
+     * concurrent issue of independent nodes, scheduler.cpp:66-95): 0 / 1 (default) = every
+     * node of a party on its stream, in id order; k > 1 = the nodes are spread over k
+     * streams per device by data dependence (a node continues its first operand's chain
+     * when it is that chain's latest node, else takes the next stream), cross-stream
+     * operands are awaited with events, and the streams are joined before the root open.
+     * A node waiting for a peer's opening then stalls only its own stream, so independent
+     * nodes run on.  Reductions and linear layers stay on stream 0 (shared scratch). */
+    int32_t node_streams;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes

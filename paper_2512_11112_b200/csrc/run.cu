@@ -484,6 +484,19 @@ int spdz_run_destroy(spdz_run* r) {
             cudaStreamSynchronize(r->copy_stream);
             cudaStreamDestroy(r->copy_stream);
         }
+        for (auto& [d, v] : r->lane_streams) {
+            cudaSetDevice(d);
+            for (auto st : v) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
+        }
+        for (int p = 0; p < (int)r->node_ev.size(); ++p) {
+            cudaSetDevice(r->devices[p]);
+            for (auto e : r->node_ev[p])
+                if (e) cudaEventDestroy(e);
+            if (r->lane_fork[p]) cudaEventDestroy(r->lane_fork[p]);
+        }
         if (r->online_graph) cudaGraphExecDestroy(r->online_graph);
         if (r->host_out_registered) cudaHostUnregister(r->host_out);
         for (auto e : r->kt.pool) cudaEventDestroy(e);

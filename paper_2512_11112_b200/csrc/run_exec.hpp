@@ -906,8 +906,117 @@ struct Exec {
     }
 
     void run_nodes() {
+        if (r->opts.node_streams > 1 && !r->net) return run_nodes_lanes();
         for (uint32_t id = 0; id < r->nodes.size(); ++id)
             if (r->live[id]) exec_node(id, 0);
+    }
+
+    // ---- node-level streams (opts.node_streams; scheduler.cpp:66-95 issues independent nodes
+    // concurrently and completes openings by continuation, net.cpp:61-95) ----
+    static bool launches_work(uint32_t kind) {
+        return kind == SPDZ_NODE_ADD || kind == SPDZ_NODE_SUB || kind == SPDZ_NODE_MUL ||
+               kind == SPDZ_NODE_REDUCE_ADD || kind == SPDZ_NODE_REDUCE_MUL || kind == SPDZ_NODE_LINEAR ||
+               kind == SPDZ_NODE_CMP_PUBLIC;
+    }
+    // a compute node a value depends on (a static LOAD is a view of its base operand)
+    int producer(uint32_t id) const {
+        while (r->nodes[id].kind == SPDZ_NODE_LOAD && r->nodes[id].n_operands) id = r->nodes[id].operands[0];
+        return launches_work(r->nodes[id].kind) ? (int)id : -1;
+    }
+    void plan_lanes() {
+        const int K = r->opts.node_streams;
+        const uint32_t N = (uint32_t)r->nodes.size();
+        r->node_lane.assign(N, -1);
+        std::vector<int> tail(K, -1);  // latest node of each stream
+        int rr = 1;
+        for (uint32_t id = 0; id < N; ++id) {
+            const auto& n = r->nodes[id];
+            if (!r->live[id] || !launches_work(n.kind)) continue;
+            int lane = -1;
+            if (n.kind == SPDZ_NODE_REDUCE_ADD || n.kind == SPDZ_NODE_REDUCE_MUL || n.kind == SPDZ_NODE_LINEAR) {
+                lane = 0;  // ctx scratch (reduction accumulators) is shared: one stream
+            } else {
+                for (uint32_t k = 0; k < n.n_operands && lane < 0; ++k) {
+                    const int o = producer(n.operands[k]);
+                    if (o >= 0 && r->node_lane[o] >= 0 && tail[r->node_lane[o]] == o) lane = r->node_lane[o];
+                }
+                if (lane < 0) {  // a new chain: the next stream (0 is kept for the serial kinds)
+                    lane = K > 1 ? rr : 0;
+                    rr = rr + 1 < K ? rr + 1 : 1;
+                }
+            }
+            r->node_lane[id] = lane;
+            tail[lane] = (int)id;
+        }
+        r->node_ev.assign(r->n, std::vector<cudaEvent_t>(N, nullptr));
+        for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
+            dev(r, p);
+            auto& v = r->lane_streams[r->devices[p]];
+            while ((int)v.size() < K) {
+                cudaStream_t st;
+                cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "lane stream");
+                v.push_back(st);
+            }
+            for (uint32_t id = 0; id < N; ++id)
+                if (r->node_lane[id] >= 0)
+                    cuda_check(cudaEventCreateWithFlags(&r->node_ev[p][id], cudaEventDisableTiming), "node event");
+            if (!r->lane_fork[p]) cuda_check(cudaEventCreateWithFlags(&r->lane_fork[p], cudaEventDisableTiming), "fork");
+        }
+    }
+    void run_nodes_lanes() {
+        const int K = r->opts.node_streams;
+        if (r->node_lane.size() != r->nodes.size()) plan_lanes();
+        std::vector<cudaStream_t> main(r->n, nullptr);
+        for (int p = 0; p < r->n; ++p) {  // fork: every stream starts after the main stream's work
+            if (!r->parties[p].local) continue;
+            dev(r, p);
+            main[p] = S(r, p);
+            lk(cudaEventRecord(r->lane_fork[p], main[p]), "fork");
+            for (auto st : r->lane_streams[r->devices[p]]) lk(cudaStreamWaitEvent(st, r->lane_fork[p], 0), "fork wait");
+        }
+        for (uint32_t id = 0; id < r->nodes.size(); ++id) {
+            if (!r->live[id]) continue;
+            const int lane = r->node_lane[id];
+            if (lane < 0) {
+                exec_node(id, 0);
+                continue;
+            }
+            const auto& n = r->nodes[id];
+            for (int p = 0; p < r->n; ++p) {
+                if (!r->parties[p].local) continue;
+                dev(r, p);
+                cudaStream_t st = r->lane_streams[r->devices[p]][lane];
+                r->parties[p].ctx->stream = st;
+                for (uint32_t k = 0; k < n.n_operands; ++k) {
+                    const int o = producer(n.operands[k]);
+                    if (o >= 0 && r->node_lane[o] != lane) lk(cudaStreamWaitEvent(st, r->node_ev[p][o], 0), "dep");
+                }
+            }
+            try {
+                exec_node(id, 0);
+            } catch (...) {
+                for (int p = 0; p < r->n; ++p)
+                    if (main[p]) r->parties[p].ctx->stream = main[p];
+                throw;
+            }
+            for (int p = 0; p < r->n; ++p) {
+                if (!r->parties[p].local) continue;
+                dev(r, p);
+                lk(cudaEventRecord(r->node_ev[p][id], S(r, p)), "node done");
+                r->parties[p].ctx->stream = main[p];
+            }
+        }
+        for (int p = 0; p < r->n; ++p) {  // join: the root open and the MAC check follow every stream
+            if (!r->parties[p].local) continue;
+            dev(r, p);
+            auto& v = r->lane_streams[r->devices[p]];
+            for (int k = 0; k < K; ++k) {
+                cudaEvent_t e = next_event(p);
+                lk(cudaEventRecord(e, v[k]), "join");
+                lk(cudaStreamWaitEvent(main[p], e, 0), "join wait");
+            }
+        }
     }
 
     // runtime.cpp:185-200: execution `exec` of a triple-consuming node must be provisioned

@@ -237,6 +237,12 @@ struct spdz_run {
     uint64_t n_slots = 0;
     uint64_t launches0 = 0;
     std::chrono::steady_clock::time_point wall0;
+    // node-level streams (opts.node_streams > 1): stream index of every node (-1: launches
+    // nothing), the streams per device, and per party one event per node (recorded after it)
+    std::vector<int> node_lane;
+    std::map<int, std::vector<cudaStream_t>> lane_streams;
+    std::vector<std::vector<cudaEvent_t>> node_ev;
+    cudaEvent_t lane_fork[SPDZ_MAX_PARTIES] = {};
 
     uint32_t* alloc(int party, uint64_t words) {
         // remote party: pointers come from spdz_run_import, or (network peers) local mirrors

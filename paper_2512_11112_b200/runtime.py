@@ -213,7 +213,7 @@ class LocalRun:
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
                  stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
                  single_party: int | None = None, use_graph: bool = False, loop_iters: int = 64,
-                 network: bool = False):
+                 network: bool = False, node_streams: int = 1):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -227,6 +227,8 @@ class LocalRun:
         o.loop_iters = loop_iters  # control flow: loop bodies' triple provisioning (the store's loop_iters)
         # peers across a TCP mesh (net.Mesh, attach_net): the reference's frames and MAC-check protocol
         o.network = int(network)
+        # > 1: independent nodes on their own streams (an opening wait stalls only its chain)
+        o.node_streams = int(node_streams)
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
         o.external_mac_verify = int(external_mac_verify or single_party is not None)
@@ -481,7 +483,7 @@ class ChunkedRun:
 
     def __init__(self, graph_fn, n_parties: int, lanes: int, chunks: int = 4, shard: tuple | None = None,
                  dealer_seed: int = 1, devices=None, single_party: int | None = None, coin: int | None = None,
-                 profile_kernels: bool = False):
+                 profile_kernels: bool = False, node_streams: int = 1):
         import torch
         off0, total = shard if shard is not None else (0, lanes)
         base, extra = divmod(lanes, chunks)
@@ -497,7 +499,7 @@ class ChunkedRun:
         self.n, self.party, self.coin = n_parties, single_party, coin
         self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
                               shard=(off0 + lo, total), external_mac_verify=True, single_party=single_party,
-                              profile_kernels=profile_kernels) for lo, L in self.ranges]
+                              profile_kernels=profile_kernels, node_streams=node_streams) for lo, L in self.ranges]
 
     def close(self):
         for r in self.runs:
