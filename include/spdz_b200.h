@@ -521,6 +521,10 @@ int spdz_run_span_ms(spdz_run* a, spdz_run* b, float* ms);
  * asynchronously; the next spdz_run_mac_check collects and verifies (its coin
  * arguments are then ignored). */
 int spdz_run_mac_check_launch(spdz_run* run, int use_coin, uint64_t coin);
+/* Blocks the host until every opening of the phase begun by spdz_run_online_begin is
+ * complete on this run's local parties (the opened values are final): the point after which
+ * a MAC-check coin may be agreed (runtime.cpp:467-506 draws it after the openings). */
+int spdz_run_wait_openings(spdz_run* run);
 int spdz_run_mac_check(spdz_run* run, int use_coin, uint64_t coin, spdz_run_report_t* report);
 /* fnv1a64 digest of the last opened outputs (RunReport.output_digest, runtime.cpp:573). */
 int spdz_run_output_digest(spdz_run* run, uint64_t* digest);

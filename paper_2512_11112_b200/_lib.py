@@ -162,6 +162,7 @@ _SIGS = {
     "spdz_run_online_begin": (C.c_int, [vp, C.c_int]),
     "spdz_run_output_digest": (C.c_int, [vp, u64p]),
     "spdz_run_mac_check": (C.c_int, [vp, C.c_int, C.c_uint64, C.POINTER(RunReport)]),
+    "spdz_run_wait_openings": (C.c_int, [vp]),
     "spdz_run_mac_check_launch": (C.c_int, [vp, C.c_int, C.c_uint64]),
     "spdz_run_set_copy_streams": (C.c_int, [vp, vp, vp]),
     "spdz_run_party_stream": (vp, [vp, C.c_int]),

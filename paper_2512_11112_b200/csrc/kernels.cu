@@ -834,108 +834,6 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
 // party 0's de, alpha_i de, bias (spdz.cpp:117-123, linear.cpp:59) — then re-zeroes the
 // row's scratch.  Sums stay below 2^64: a segment adds < 2^40 and a row has at most din/4
 // segments.
-__global__ void __launch_bounds__(kThreads, 3) k_matrix_combine2_flat(MC2Args a, unsigned long long* acc_rows,
-                                                                      unsigned int* done_rows) {
-    const uint32_t din4 = a.din / 4;
-    const uint64_t cells = (uint64_t)a.din * a.rows;
-    const uint64_t U = (uint64_t)din4 * a.rows;
-    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
-    const uint64_t w = (uint64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32;
-    const uint32_t lane = threadIdx.x & 31;
-    uint64_t u0 = U * w / warps;
-    const uint64_t u1 = U * (w + 1) / warps;
-    while (u0 < u1) {
-        const uint32_t r = (uint32_t)(u0 / din4);
-        const uint64_t rbase = (uint64_t)r * din4;
-        const uint64_t rend = u1 < rbase + din4 ? u1 : rbase + din4;
-        const uint64_t toff = (uint64_t)(r / a.rpt) * a.din;
-        const uint4* E4 = reinterpret_cast<const uint4*>(a.opened + cells + toff);
-        const uint4* B4[2][2];
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            B4[p][0] = reinterpret_cast<const uint4*>(a.B[p][0] + toff);
-            B4[p][1] = reinterpret_cast<const uint4*>(a.B[p][1] + toff);
-        }
-        unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
-        for (uint64_t gg = u0 + lane; gg < rend; gg += 32) {
-            const uint32_t c4 = (uint32_t)(gg - rbase);
-            const uint4 d0 = ld4(a.D0, gg), d1 = ld4(a.D1, gg);
-            uint4 av[2], am[2], bv[2], bm[2];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                av[p] = ld4(a.A[p][0], gg);
-                am[p] = ld4(a.A[p][1], gg);
-            }
-            const uint4 e4 = E4[c4];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                bv[p] = B4[p][0][c4];
-                bm[p] = B4[p][1][c4];
-            }
-            const uint32_t d[4] = {fp_add(d0.x, fp_reduce32(d1.x)), fp_add(d0.y, fp_reduce32(d1.y)),
-                                   fp_add(d0.z, fp_reduce32(d1.z)), fp_add(d0.w, fp_reduce32(d1.w))};
-            const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
-#pragma unroll
-            for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const uint32_t AV[4] = {av[p].x, av[p].y, av[p].z, av[p].w};
-                const uint32_t AM[4] = {am[p].x, am[p].y, am[p].z, am[p].w};
-                const uint32_t BV[4] = {bv[p].x, bv[p].y, bv[p].z, bv[p].w};
-                const uint32_t BM[4] = {bm[p].x, bm[p].y, bm[p].z, bm[p].w};
-#pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                    acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
-                    acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
-                }
-            }
-            st4(a.opened, gg, d);
-        }
-#pragma unroll
-        for (int q = 0; q < 5; ++q) acc[q] = warp_sum(fold1(acc[q]));
-        if (lane == 0) {
-            unsigned long long* ar = acc_rows + (uint64_t)r * 5;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) atomicAdd(ar + q, acc[q]);
-            __threadfence();
-            const uint32_t seg = (uint32_t)(rend - u0);
-            if (atomicAdd(done_rows + r, seg) + seg == din4) {  // last segment of row r: finalise it
-                __threadfence();
-                unsigned long long sum[5];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) sum[q] = atomicExch(ar + q, 0ull);
-                done_rows[r] = 0;
-                const uint32_t de = fp_reduce64(sum[4]);
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(sum[2 * p]));
-                    if (p == 0) vr = fp_add(vr, de);
-                    uint32_t mr = fp_add(fp_reduce64((unsigned long long)a.Cc[p][1][r] + fp_reduce64(sum[2 * p + 1])),
-                                         fp_mul(a.alpha[p], de));
-                    if (a.bias[p][0]) {
-                        vr = fp_add(vr, a.bias[p][0][r]);
-                        mr = fp_add(mr, a.bias[p][1][r]);
-                    }
-                    a.z[p][0][r] = vr;
-                    a.z[p][1][r] = mr;
-                }
-            }
-        }
-        u0 = rend;
-    }
-}
-
-// Pipelined variant for din % 128 == 0 (every 32-group of uint4 units lies in one row, so a
-// row change is warp-uniform): each lane streams its eleven 16-byte operands (D0, D1, both
-// parties' A.v A.m, E, both parties' B.v B.m) through a per-warp shared-memory ring with
-// cp.async, MC2_STAGES groups ahead of the arithmetic, so HBM sees several groups of every warp
-// in flight regardless of the register budget (ncu r02a: the register-fed kernel held 34% of
-// the warp slots and 65% of DRAM bandwidth).  A lane only reads back slots it copied itself.
-constexpr int MC2_STAGES = 4;
-constexpr int MC2_WARPS = 8;
-constexpr int MC2_STREAMS = 11;
-constexpr uint32_t MC2_SMEM = MC2_WARPS * MC2_STAGES * MC2_STREAMS * 32 * 16;  // 180 KB
-
 __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (&acc)[5], uint32_t r, uint32_t seg,
                                           uint32_t din4, unsigned long long* acc_rows, unsigned int* done_rows,
                                           uint32_t lane) {
@@ -972,81 +870,96 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
     for (int q = 0; q < 5; ++q) acc[q] = 0ull;
 }
 
-__global__ void __launch_bounds__(MC2_WARPS * 32, 1) k_matrix_combine2_pipe(MC2Args a, unsigned long long* acc_rows,
-                                                                            unsigned int* done_rows) {
-    extern __shared__ __align__(16) uint8_t mc2_smem[];
-    const uint32_t din4 = a.din / 4, gpr = din4 / 32;  // 32-unit groups per row
+struct MC2Ld {
+    uint4 d0, d1, e4, av[2], am[2], bv[2], bm[2];
+};
+__device__ __forceinline__ void mc2_load(const MC2Args& a, uint64_t gg, uint32_t c4, const uint4* E4,
+                                         const uint4* const (&B4)[2][2], MC2Ld& L) {
+    L.d0 = ld4(a.D0, gg);
+    L.d1 = ld4(a.D1, gg);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        L.av[p] = ld4(a.A[p][0], gg);
+        L.am[p] = ld4(a.A[p][1], gg);
+    }
+    L.e4 = E4[c4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        L.bv[p] = B4[p][0][c4];
+        L.bm[p] = B4[p][1][c4];
+    }
+}
+__device__ __forceinline__ void mc2_compute(const MC2Args& a, uint64_t gg, const MC2Ld& L,
+                                            unsigned long long (&acc)[5]) {
+    const uint32_t d[4] = {fp_add(L.d0.x, fp_reduce32(L.d1.x)), fp_add(L.d0.y, fp_reduce32(L.d1.y)),
+                           fp_add(L.d0.z, fp_reduce32(L.d1.z)), fp_add(L.d0.w, fp_reduce32(L.d1.w))};
+    const uint32_t e[4] = {L.e4.x, L.e4.y, L.e4.z, L.e4.w};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const uint32_t AV[4] = {L.av[p].x, L.av[p].y, L.av[p].z, L.av[p].w};
+        const uint32_t AM[4] = {L.am[p].x, L.am[p].y, L.am[p].z, L.am[p].w};
+        const uint32_t BV[4] = {L.bv[p].x, L.bv[p].y, L.bv[p].z, L.bv[p].w};
+        const uint32_t BM[4] = {L.bm[p].x, L.bm[p].y, L.bm[p].z, L.bm[p].w};
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
+            acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
+        }
+    }
+    st4(a.opened, gg, d);
+}
+
+// Balanced variant (16-byte path): the dout x din cell space is one flat range of uint4
+// groups split evenly over every resident warp of a one-wave grid, so no warp holds more than
+// its share (a warp per row leaves a 1.15-wave tail at 4096 rows: 4096 warps on 148 x 24 warp
+// slots).  A warp walks its range row segment by row segment; each segment's five lazy sums
+// are warp-reduced and added to the row's u64 accumulators (scratch, zero between launches),
+// and the warp that completes a row (its lane count reaches din/4) finalises it: C + sums,
+// party 0's de, alpha_i de, bias (spdz.cpp:117-123, linear.cpp:59) — then re-zeroes the
+// row's scratch.  Sums stay below 2^64: a segment adds < 2^40 and a row has at most din/4
+// segments.  UNROLL = 2 issues two groups' loads before either group's arithmetic (more
+// bytes in flight per warp at the cost of registers; MINB resident blocks per SM).
+template <int UNROLL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_matrix_combine2_flat(MC2Args a, unsigned long long* acc_rows,
+                                                                         unsigned int* done_rows) {
+    const uint32_t din4 = a.din / 4;
     const uint64_t cells = (uint64_t)a.din * a.rows;
-    const uint64_t NG = (uint64_t)gpr * a.rows;
-    const uint64_t warps = (uint64_t)gridDim.x * MC2_WARPS;
-    const uint32_t wib = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const uint64_t w = (uint64_t)blockIdx.x * MC2_WARPS + wib;
-    const uint64_t g0 = NG * w / warps, g1 = NG * (w + 1) / warps;
-    // ring slot (stage, stream) of this lane: 16 bytes at ((stage * 11 + stream) * 32 + lane) * 16
-    const uint32_t ring = smem_u32(mc2_smem) + wib * (MC2_STAGES * MC2_STREAMS * 32 * 16) + lane * 16;
-    const uint4* ringp = reinterpret_cast<const uint4*>(mc2_smem + wib * (MC2_STAGES * MC2_STREAMS * 32 * 16)) + lane;
-    auto issue = [&](uint64_t g, int stage) {
-        if (g < g1) {
-            const uint64_t u = g * 32 + lane;
-            const uint32_t r = (uint32_t)(g / gpr);
-            const uint64_t c4 = u - (uint64_t)r * din4;
-            const uint64_t t4 = (uint64_t)(r / a.rpt) * din4 + c4;  // tile vector index (uint4)
-            const uint32_t base = ring + stage * (MC2_STREAMS * 32 * 16);
-            cp_async16(base + 0 * 512, reinterpret_cast<const uint4*>(a.D0) + u);
-            cp_async16(base + 1 * 512, reinterpret_cast<const uint4*>(a.D1) + u);
-            cp_async16(base + 2 * 512, reinterpret_cast<const uint4*>(a.A[0][0]) + u);
-            cp_async16(base + 3 * 512, reinterpret_cast<const uint4*>(a.A[0][1]) + u);
-            cp_async16(base + 4 * 512, reinterpret_cast<const uint4*>(a.A[1][0]) + u);
-            cp_async16(base + 5 * 512, reinterpret_cast<const uint4*>(a.A[1][1]) + u);
-            cp_async16(base + 6 * 512, reinterpret_cast<const uint4*>(a.opened + cells) + t4);
-            cp_async16(base + 7 * 512, reinterpret_cast<const uint4*>(a.B[0][0]) + t4);
-            cp_async16(base + 8 * 512, reinterpret_cast<const uint4*>(a.B[0][1]) + t4);
-            cp_async16(base + 9 * 512, reinterpret_cast<const uint4*>(a.B[1][0]) + t4);
-            cp_async16(base + 10 * 512, reinterpret_cast<const uint4*>(a.B[1][1]) + t4);
-        }
-        cp_async_commit();  // (an empty group past the range keeps the wait counts uniform)
-    };
-#pragma unroll
-    for (int s = 0; s < MC2_STAGES - 1; ++s) issue(g0 + s, s);
-    unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
-    uint32_t cur = g0 < g1 ? (uint32_t)(g0 / gpr) : 0, seg = 0;
-    int stage = 0;
-    for (uint64_t g = g0; g < g1; ++g) {
-        issue(g + MC2_STAGES - 1, (stage + MC2_STAGES - 1) % MC2_STAGES);
-        cp_async_wait<MC2_STAGES - 1>();
-        const uint32_t r = (uint32_t)(g / gpr);
-        if (r != cur) {
-            mc2_flush(a, acc, cur, seg, din4, acc_rows, done_rows, lane);
-            cur = r;
-            seg = 0;
-        }
-        const uint4* sl = ringp + stage * (MC2_STREAMS * 32);
-        const uint4 d0 = sl[0 * 32], d1 = sl[1 * 32], e4 = sl[6 * 32];
-        const uint4 av[2] = {sl[2 * 32], sl[4 * 32]}, am[2] = {sl[3 * 32], sl[5 * 32]};
-        const uint4 bv[2] = {sl[7 * 32], sl[9 * 32]}, bm[2] = {sl[8 * 32], sl[10 * 32]};
-        const uint32_t d[4] = {fp_add(d0.x, fp_reduce32(d1.x)), fp_add(d0.y, fp_reduce32(d1.y)),
-                               fp_add(d0.z, fp_reduce32(d1.z)), fp_add(d0.w, fp_reduce32(d1.w))};
-        const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
-#pragma unroll
-        for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const uint32_t AV[4] = {av[p].x, av[p].y, av[p].z, av[p].w};
-            const uint32_t AM[4] = {am[p].x, am[p].y, am[p].z, am[p].w};
-            const uint32_t BV[4] = {bv[p].x, bv[p].y, bv[p].z, bv[p].w};
-            const uint32_t BM[4] = {bm[p].x, bm[p].y, bm[p].z, bm[p].w};
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
-                acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
+    const uint64_t U = (uint64_t)din4 * a.rows;
+    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t u0 = U * w / warps;
+    const uint64_t u1 = U * (w + 1) / warps;
+    while (u0 < u1) {
+        const uint32_t r = (uint32_t)(u0 / din4);
+        const uint64_t rbase = (uint64_t)r * din4;
+        const uint64_t rend = u1 < rbase + din4 ? u1 : rbase + din4;
+        const uint64_t toff = (uint64_t)(r / a.rpt) * a.din;
+        const uint4* E4 = reinterpret_cast<const uint4*>(a.opened + cells + toff);
+        const uint4* const B4[2][2] = {
+            {reinterpret_cast<const uint4*>(a.B[0][0] + toff), reinterpret_cast<const uint4*>(a.B[0][1] + toff)},
+            {reinterpret_cast<const uint4*>(a.B[1][0] + toff), reinterpret_cast<const uint4*>(a.B[1][1] + toff)}};
+        unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
+        uint64_t gg = u0 + lane;
+        if (UNROLL == 2) {
+            for (; gg + 32 < rend; gg += 64) {
+                MC2Ld L0, L1;
+                mc2_load(a, gg, (uint32_t)(gg - rbase), E4, B4, L0);
+                mc2_load(a, gg + 32, (uint32_t)(gg + 32 - rbase), E4, B4, L1);
+                mc2_compute(a, gg, L0, acc);
+                mc2_compute(a, gg + 32, L1, acc);
             }
         }
-        st4(a.opened, g * 32 + lane, d);
-        seg += 32;
-        stage = stage + 1 < MC2_STAGES ? stage + 1 : 0;
+        for (; gg < rend; gg += 32) {
+            MC2Ld L0;
+            mc2_load(a, gg, (uint32_t)(gg - rbase), E4, B4, L0);
+            mc2_compute(a, gg, L0, acc);
+        }
+        mc2_flush(a, acc, r, (uint32_t)(rend - u0), din4, acc_rows, done_rows, lane);
+        u0 = rend;
     }
-    cp_async_wait<0>();
-    if (g0 < g1) mc2_flush(a, acc, cur, seg, din4, acc_rows, done_rows, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1485,34 +1398,22 @@ cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms, un
     for (int p = 0; p < 2; ++p)
         v4 = v4 && aligned16(a.A[p][0]) && aligned16(a.A[p][1]) && aligned16(a.B[p][0]) && aligned16(a.B[p][1]);
     static const bool flat_off = std::getenv("SPDZ_MC2_ROWS") != nullptr;  // experiments: the row-per-warp kernel
+    static const int unroll = [] {  // SPDZ_MC2_UNROLL=1|2 (experiments; default 2)
+        const char* e = std::getenv("SPDZ_MC2_UNROLL");
+        return e && std::atoi(e) == 1 ? 1 : 2;
+    }();
     if (v4 && acc_rows && done_rows && !flat_off) {
-        static int per_sm = 0;
-        if (!per_sm) {
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matrix_combine2_flat, kThreads, 0) !=
-                    cudaSuccess || per_sm < 1)
-                per_sm = 1;
+        auto kern = unroll == 2 ? k_matrix_combine2_flat<2, 2> : k_matrix_combine2_flat<1, 3>;
+        static int per_sm[2] = {0, 0};
+        int& ps = per_sm[unroll - 1];
+        if (!ps) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kThreads, 0) != cudaSuccess || ps < 1) ps = 1;
         }
         const uint64_t units = (uint64_t)(a.din / 4) * a.rows;
-        uint64_t grid = (uint64_t)sms * per_sm;
+        uint64_t grid = (uint64_t)sms * ps;
         const uint64_t need = (units + kThreads - 1) / kThreads;  // small layers: no idle warps
         if (need < grid) grid = need ? need : 1;
-        static const bool pipe_off = std::getenv("SPDZ_MC2_FLAT") != nullptr;  // experiments
-        if (a.din % 128 == 0 && !pipe_off) {
-            static bool attr = false;
-            if (!attr) {
-                cudaError_t e = cudaFuncSetAttribute(k_matrix_combine2_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     MC2_SMEM);
-                if (e != cudaSuccess) return e;
-                attr = true;
-            }
-            const uint64_t groups = units / 32;
-            uint64_t pg = (uint64_t)sms;
-            const uint64_t pneed = (groups + MC2_WARPS - 1) / MC2_WARPS;
-            if (pneed < pg) pg = pneed ? pneed : 1;
-            k_matrix_combine2_pipe<<<(int)pg, MC2_WARPS * 32, MC2_SMEM, s>>>(a, acc_rows, done_rows);
-            return launched();
-        }
-        k_matrix_combine2_flat<<<(int)grid, kThreads, 0, s>>>(a, acc_rows, done_rows);
+        kern<<<(int)grid, kThreads, 0, s>>>(a, acc_rows, done_rows);
         return launched();
     }
     static const int force_g = [] {  // SPDZ_MC2_G=32|256: override the row-group choice (experiments)

@@ -316,8 +316,6 @@ bool graphable(spdz_run* r) {
     if (!r->opts.use_graph || r->cfg || r->any_remote || r->opts.profile_kernels || !r->faults.empty()) return false;
     for (int p = 0; p < r->n; ++p)
         if (!r->parties[p].local || S(r, p) != S(r, 0)) return false;
-    for (const auto& n : r->nodes)
-        if (n.kind == SPDZ_NODE_LINEAR || n.kind == SPDZ_NODE_REDUCE_ADD || n.kind == SPDZ_NODE_REDUCE_MUL) return false;
     return true;
 }
 
@@ -474,6 +472,7 @@ int spdz_run_destroy(spdz_run* r) {
             for (auto e : P.evs) cudaEventDestroy(e);
             if (P.t0) cudaEventDestroy(P.t0);
             if (P.t1) cudaEventDestroy(P.t1);
+            if (P.t_open) cudaEventDestroy(P.t_open);
         }
         if (r->ev_input) {
             cudaSetDevice(r->devices[r->ref_party()]);
@@ -630,6 +629,11 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
             else ex.run_nodes();
             ex.open_root();
         }
+        for (auto& P : r->parties) {  // the phase's openings are complete once these fire
+            if (!P.local) continue;
+            device_guard(P.ctx);
+            lk(cudaEventRecord(P.t_open, P.ctx->stream), "t_open");
+        }
         r->consumed = true;
         r->in_flight = true;
         // opened outputs to host on a copy stream, overlapping the MAC check
@@ -681,6 +685,17 @@ int spdz_run_set_copy_streams(spdz_run* r, void* h2d_stream, void* d2h_stream) {
         need(!r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "online phase in flight");
         r->h2d_stream = static_cast<cudaStream_t>(h2d_stream);
         r->d2h_stream = static_cast<cudaStream_t>(d2h_stream);
+    });
+}
+
+int spdz_run_wait_openings(spdz_run* r) {
+    return guard([&] {
+        need(r != nullptr && r->in_flight, SPDZ_ERR_INVALID_ARGUMENT, "no online phase in flight");
+        for (auto& P : r->parties) {
+            if (!P.local) continue;
+            device_guard(P.ctx);
+            lk(cudaEventSynchronize(P.t_open), "wait openings");
+        }
     });
 }
 

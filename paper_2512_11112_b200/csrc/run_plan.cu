@@ -405,6 +405,7 @@ void plan_buffers(spdz_run* r) {
         if (!P.local) continue;
         cuda_check(cudaSetDevice(P.ctx->device), "dev");
         cuda_check(cudaEventCreate(&P.t0), "ev");
+        cuda_check(cudaEventCreateWithFlags(&P.t_open, cudaEventDisableTiming), "ev");
         cuda_check(cudaEventCreate(&P.t1), "ev");
         // private input differences: party 0 publishes x - mask (preproc.cpp:146-151)
         if (p == 0)

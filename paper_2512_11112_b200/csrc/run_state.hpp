@@ -135,6 +135,7 @@ struct Party {
     std::vector<spdz_mac_segment_t> maclog;
     std::vector<cudaEvent_t> evs;   // open-slot events
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaEvent_t t_open = nullptr;   // every opening of the phase complete (spdz_run_wait_openings)
 };
 
 struct DeviceDeal {                 // one dealer output per device (all parties' shares)

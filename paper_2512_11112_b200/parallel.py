@@ -97,3 +97,25 @@ def verify_sharded_sigmas(partial_sigmas, group=None):
     if rc:
         raise errors.from_code(rc, lib().spdz_last_error().decode())
     return sig
+
+
+def verify_sharded_sigma_sets(partial_sets, group=None):
+    """Several independent MAC checks at once (ChunkedRun mac="per_chunk": one per lane chunk,
+    each with its own coin): partial_sets[c][p] = this rank's sigma partial of party p in
+    check c.  One all-gather; each check's partials summed over the ranks and verified
+    (commit / reveal / verify_sigmas, spdz.cpp:140-158).  Raises MacCheckFailed."""
+    checks = len(partial_sets)
+    n = len(partial_sets[0]) if checks else 0
+    flat = [int(s) for ps in partial_sets for s in ps]
+    gathered = _all_gather_ints(flat, group)
+    out = []
+    for c in range(checks):
+        sig = [sum(g[c * n + p] for g in gathered) % P for p in range(n)]
+        nonces = [int.from_bytes(os.urandom(8), "little") for _ in range(n)]
+        commits = [lib().spdz_commit_sigma(s, nz) for s, nz in zip(sig, nonces)]
+        rc = lib().spdz_verify_sigmas((C.c_uint32 * n)(*sig), (C.c_uint64 * n)(*nonces),
+                                      (C.c_uint64 * n)(*commits), n)
+        if rc:
+            raise errors.from_code(rc, lib().spdz_last_error().decode())
+        out.append(sig)
+    return out

@@ -301,6 +301,11 @@ class LocalRun:
         h = lambda s: None if s is None else int(getattr(s, "cuda_stream", s))
         check(lib().spdz_run_set_copy_streams(self.h, h(h2d), h(d2h)))
 
+    def wait_openings(self):
+        """Blocks until every opening of the phase begun by online_begin() is complete (the
+        opened values are final); a MAC-check coin is agreed only after this."""
+        check(lib().spdz_run_wait_openings(self.h))
+
     def mac_check_launch(self, coin: int | None = None):
         """Agree on the coin and enqueue the sigma kernels; mac_check() then collects."""
         check(lib().spdz_run_mac_check_launch(self.h, 0 if coin is None else 1, int(coin or 0)))
@@ -422,15 +427,23 @@ class StreamedRun:
         coin = None
         reps = [None] * len(self.runs)
         lag = 2  # per-chunk mode: collect chunk c-2's check while the GPU works on c-1 and c
+
+        def check_chunk(c):  # chunk c's openings are final: its coin, its sigma kernels
+            nonlocal coin
+            self.runs[c].wait_openings()
+            coin = self._coin()
+            self.runs[c].mac_check_launch(coin)
+
         for c, (r, (o, L)) in enumerate(zip(self.runs, self.ranges)):
             r.bind_inputs({k: v[o:o + L] for k, v in inputs.items()})
             r.share_inputs()
             r.online_begin()
-            if per_chunk:  # this chunk's openings are enqueued: its coin, its sigma kernels
-                coin = self._coin()
-                r.mac_check_launch(coin)
-                if c >= lag:
-                    reps[c - lag] = self._collect(self.runs[c - lag], per_chunk)
+            if per_chunk and c >= 1:  # chunk c is queued behind c-1: the GPU stays busy meanwhile
+                check_chunk(c - 1)
+                if c - 1 >= lag:
+                    reps[c - 1 - lag] = self._collect(self.runs[c - 1 - lag], per_chunk)
+        if per_chunk:
+            check_chunk(len(self.runs) - 1)
         if not per_chunk:
             coin = self._coin()
             for r in self.runs:  # every chunk's sigma kernels in flight before the first collect
@@ -483,8 +496,14 @@ class ChunkedRun:
 
     def __init__(self, graph_fn, n_parties: int, lanes: int, chunks: int = 4, shard: tuple | None = None,
                  dealer_seed: int = 1, devices=None, single_party: int | None = None, coin: int | None = None,
-                 profile_kernels: bool = False, node_streams: int = 1):
+                 profile_kernels: bool = False, node_streams: int = 1, mac: str = "joint"):
+        """mac="joint": one coin after every chunk's openings, per-party partials summed over the
+        chunks; mac="per_chunk": chunk c's coin is agreed as soon as its openings are final and its
+        sigma kernels launched while later chunks still run (each chunk a full SPDZ check of its
+        own openings), so the issue-bound sigma overlaps the next chunk's HBM-bound kernels."""
         import torch
+        assert mac in ("joint", "per_chunk")
+        self.mac = mac
         off0, total = shard if shard is not None else (0, lanes)
         base, extra = divmod(lanes, chunks)
         self.ranges, o = [], 0
@@ -558,15 +577,24 @@ class ChunkedRun:
         return self._finish(coin_fn)
 
     def _finish(self, coin_fn):
-        coin = coin_fn() if coin_fn is not None else self.coin
-        for r in self.runs:
-            r.mac_check_launch(coin)
+        """joint: returns the per-party sigma partials summed over the chunks; per_chunk: a list
+        of per-chunk partial vectors (each checked on its own, parallel.verify_sharded_sigma_sets)."""
+        if self.mac == "per_chunk":
+            for r in self.runs:  # chunk order = completion order of the openings
+                r.wait_openings()
+                r.mac_check_launch(coin_fn() if coin_fn is not None else self.coin)
+        else:
+            coin = coin_fn() if coin_fn is not None else self.coin
+            for r in self.runs:
+                r.mac_check_launch(coin)
         reps = [r.mac_check() for r in self.runs]
         span = 0.0
         for r in self.runs:
             ms = C.c_float()
             check(lib().spdz_run_span_ms(self.runs[0].h, r.h, C.byref(ms)))
             span = max(span, ms.value)
+        if self.mac == "per_chunk":
+            return [list(rep.sigmas[:self.n]) for rep in reps], span, reps
         sig = [sum(rep.sigmas[p] for rep in reps) % 4294967291 for p in range(self.n)]
         return sig, span, reps
 

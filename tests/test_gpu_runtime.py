@@ -463,3 +463,39 @@ def test_colocated_linear_combine_equals_per_party(gpu, din, dout, slice_):
     for p in range(2):
         for k in range(2):
             np.testing.assert_array_equal(runs[False][1][p][k], runs[True][1][p][k])
+
+
+@pytest.mark.parametrize("case", ["linear_ss", "linear_wpub", "reduce_add", "reduce_mul", "linear_8192"])
+def test_graph_replay_linear_and_reductions(gpu, case):
+    """use_graph captures the whole online phase (linear layers and reductions included) on
+    the first phase and replays it: outputs, node shares and sigmas (fixed coin) of the
+    replayed phases equal the eagerly executed ones, phase by phase with fresh dealing."""
+    from paper_2512_11112_b200 import LocalRun, linear_graph, reduce_graph
+    coin = 0xFEED
+    if case.startswith("linear"):
+        din, dout = (8192, 64) if case == "linear_8192" else (516, 130)
+        g = linear_graph(din, dout, w_private=case != "linear_wpub")
+        inp = {"x": O.rand_field_vec(din, 1), "W": O.rand_field_vec(din * dout, 2), "b": O.rand_field_vec(dout, 3)}
+    else:
+        g = reduce_graph(case.split("_")[1], 1001)
+        inp = {"x": O.rand_field_vec(1001, 4)}
+    node = g.nodes[g.root].operands[0]
+    got = {}
+    for use_graph in (False, True):
+        r = LocalRun(g, 2, slice_=65536, coin=coin, use_graph=use_graph)
+        out = []
+        for it in range(3):
+            r.deal(11 + it)
+            r.bind_inputs(inp)
+            r.share_inputs()
+            rep = r.online()
+            assert sum(rep.sigmas) % P == 0
+            out.append((rep.outputs.copy(), rep.sigmas, [r.node_share_host(p, node) for p in range(2)]))
+        got[use_graph] = out
+        r.close()
+    for (o0, s0, n0), (o1, s1, n1) in zip(got[False], got[True]):
+        np.testing.assert_array_equal(o0, o1)
+        assert s0 == s1
+        for p in range(2):
+            for k in range(2):
+                np.testing.assert_array_equal(n0[p][k], n1[p][k])
