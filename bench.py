@@ -327,9 +327,12 @@ def linear_block(with_reference: bool) -> dict:
     # C4: secret x secret 4096x4096 + MAC check, 2 parties on this GPU (slice 262140: 64 tiles)
     din = dout = 4096
     inp = {"x": bc.rnd(din, 1), "W": bc.rnd(din * dout, 2), "b": bc.rnd(dout, 3)}
-    g = bc.gpu_online(linear_graph(din, dout), inp, reps=5, slice_=262140)
+    g = bc.gpu_online(linear_graph(din, dout), inp, reps=5, slice_=262140)  # eager, per-kernel events
+    gg = bc.gpu_online(linear_graph(din, dout), inp, reps=10, slice_=262140, use_graph=True)
     out["C4_secret_secret_4096x4096"] = {
-        "online_device_ms": g["online_device_ms"], "online_wall_ms": g["online_wall_ms"], "tiles": 64,
+        "online_device_ms": gg["online_device_ms"], "online_wall_ms": gg["online_wall_ms"],
+        "eager_online_device_ms": g["online_device_ms"], "tiles": 64,
+        "mode": "online phase captured once as a CUDA graph and replayed after every re-deal",
         "kernels": {k: {"ms": round(v["ms"], 4), "GBs": round(v["GBs"] or 0, 1)} for k, v in g["kernels"].items()},
         "timed": "mask, open [D|E], combine, root open, MAC check (both parties)"}
     bm = bc.bmatrix_bench(4096, 4096, 4096)
@@ -347,6 +350,45 @@ def linear_block(with_reference: bool) -> dict:
                 workloads.linear_ir(4096, 4096), inp, th, slice_=262140)
             out["reference_threads_per_party"] = th
     return out
+
+
+def per_party_block(args, dev, inputs, spot, colocated_step_ms, colocated_kstat) -> dict:
+    """The N-GPU kernel mix on this GPU: each party on its own stream with its own kernels
+    (mask, OpCombine<1> reading the peer's payload from the other party's buffers, k_mac_sigma<1>)
+    instead of the co-located fusions (OpCombine2 / k_mac_sigma<2>, which read shared payloads and
+    coefficient streams once for both parties).  Per-kernel-class GB/s against each kernel's byte
+    contract, and the per-party step time beside the co-located step's."""
+    import torch
+
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    r = LocalRun(chain_graph(args.kind, args.lanes), 2, devices=[dev, dev], profile_kernels=True, dealer_seed=1,
+                 stream_per_party=True)
+    ms, kst = [], {}
+    for k in range(args.warmup + args.steps):
+        r.deal(7000 + k)
+        r.bind_inputs(inputs)
+        r.share_inputs()
+        torch.cuda.synchronize()
+        rep = r.online()
+        if sum(rep.sigmas) % P != 0:
+            raise RuntimeError("MAC check did not verify")
+        spot(rep.outputs, f"per-party step {k}")
+        if k >= args.warmup:
+            ms.append(rep.online_device_ms)
+            for name, st in rep.kstat.items():
+                a = kst.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0})
+                for f in a:
+                    a[f] += st[f]
+    r.close()
+    step = float(np.mean(ms))
+    gbs = lambda d: {n: round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1) for n, v in d.items() if v["launches"]}
+    return {"placement": "2 parties on 1 GPU, one stream and one set of kernels per party",
+            "ms_per_step": step, "mult_per_s": N_MUL[args.kind] * args.lanes / (step / 1e3),
+            "vs_colocated_step": step / colocated_step_ms, "kernels_gbs": gbs(kst),
+            "kernel_ms_per_step": {n: round(v["ms"] / args.steps, 4) for n, v in kst.items() if v["launches"]},
+            "colocated_kernels_gbs": gbs(colocated_kstat),
+            "contracts_bytes": {"mask": "24 per lane", "combine": "48 + 8 (peer d, e) per lane (OpCombine<1>)",
+                                "sigma": "12 per record (k_mac_sigma<1>)"}}
 
 
 def run_ours(args, world, rank, local):
@@ -380,14 +422,16 @@ def run_ours(args, world, rank, local):
         # one chunk's opening exchange over NVLink overlaps the other chunks' kernels
         from paper_2512_11112_b200 import ChunkedRun
         run = ChunkedRun(lambda L: chain_graph(args.kind, L), 2, lanes, chunks=args.exchange_chunks,
-                         shard=(shard * lanes, total), single_party=party, devices=[dev, dev], profile_kernels=True)
+                         shard=(shard * lanes, total), single_party=party, devices=[dev, dev], profile_kernels=True,
+                         mac="per_chunk")
         import torch.distributed as dist
         blobs = [None] * world
         dist.all_gather_object(blobs, run.export_ipc())
         run.import_ipc([blobs[peer]])
         coin_fn = parallel.joint_coin
         parallelism = (f"2 parties x {G} GPUs, lane-sharded, NVLink P2P opens, "
-                       f"{args.exchange_chunks} lane chunks per GPU overlapping the exchange")
+                       f"{args.exchange_chunks} lane chunks per GPU overlapping the exchange, "
+                       f"one MAC check per chunk (coin after the chunk's openings)")
     mults_step = n_mul * total  # whole job, per step
     x, y = inputs_for(shard, lanes)
     spot = SpotCheck(args.kind, x, y, seed=99 + rank)
@@ -403,9 +447,9 @@ def run_ours(args, world, rank, local):
         run.share_inputs()
 
     def step():
-        if world > 1:  # ChunkedRun: one coin, one sharded verification for every chunk
+        if world > 1:  # ChunkedRun: per chunk a coin after its openings, one gather verifies them all
             sig, ms, reps = run.online(coin_fn=coin_fn)
-            parallel.verify_sharded_sigmas(sig)
+            parallel.verify_sharded_sigma_sets(sig)
             kst = {}
             for r in reps:
                 for name, st in r.kstat.items():
@@ -492,7 +536,7 @@ def run_ours(args, world, rank, local):
             barrier(world)
             t0 = time.perf_counter()
             sig, _, _ = run.run_e2e(inputs if owns_inputs else None, coin_fn=coin_fn)
-            parallel.verify_sharded_sigmas(sig)
+            parallel.verify_sharded_sigma_sets(sig)
             e2e_ms += (time.perf_counter() - t0) * 1e3
             barrier(world)
             spot(out_pin, f"e2e step {k}")
@@ -511,6 +555,9 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_kind, "bytes_per_launch": st["bytes"] // max(st["launches"], 1),
                 "launch_ms": round(st["ms"] / max(st["launches"], 1), 4), "step_share": shares,
                 "all_kernels_gbs": {n: round(kstat[n]["bytes"] / max(kstat[n]["ms"], 1e-9) / 1e6, 1) for n in kstat}}
+    per_party = None
+    if world == 1 and not args.no_per_party:
+        per_party = per_party_block(args, dev, inputs, spot, step_ms, kstat)
     linear = None
     if world == 1 and not args.no_linear:
         linear = linear_block(with_reference=rank == 0 and not args.no_cpu_baseline)
@@ -550,7 +597,8 @@ def run_ours(args, world, rank, local):
                 "clocks": clocks, "gpu_launches": launches,
                 "output_spot_check": {"lanes_per_step": spot.k, "checked": spot.checked,
                                       "against": "cleartext chain of the step's inputs"},
-                "e2e": e2e_line, "roofline": roofline, "linear": linear, "cpu_baseline": cpu_baseline}
+                "e2e": e2e_line, "roofline": roofline, "per_party": per_party, "linear": linear,
+                "cpu_baseline": cpu_baseline}
         print(json.dumps(line), flush=True)
     barrier(world)  # peers may still hold IPC mappings of our buffers
     run.close()
@@ -568,6 +616,7 @@ def main():
                     help="our arm's cpu_baseline leg (a bounded sample; --impl reference runs the full size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-linear", action="store_true", help="skip the linear-layer block")
+    ap.add_argument("--no-per-party", action="store_true", help="skip the per-party-kernel block")
     ap.add_argument("--exchange-chunks", type=int, default=2,
                     help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run")

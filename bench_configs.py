@@ -33,9 +33,11 @@ def rnd(n, seed):
     return np.random.default_rng(seed).integers(0, P, n, dtype=np.uint64).astype(np.uint32)
 
 
-def gpu_online(graph, inputs, reps=5, slice_=262140, profile=True):
+def gpu_online(graph, inputs, reps=5, slice_=262140, profile=True, use_graph=False):
+    """profile: per-kernel-class CUDA-event times (eager launches); use_graph: the online phase
+    captured once as a CUDA graph and replayed (profile must be off)."""
     from paper_2512_11112_b200 import LocalRun
-    r = LocalRun(graph, 2, slice_=slice_, profile_kernels=profile)
+    r = LocalRun(graph, 2, slice_=slice_, profile_kernels=profile and not use_graph, use_graph=use_graph)
     dev, wall, reps_out = [], [], None
     for k in range(reps + 1):
         r.deal(10 + k)

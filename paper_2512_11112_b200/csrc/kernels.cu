@@ -657,7 +657,8 @@ __global__ void __launch_bounds__(kThreads) k_matrix_combine(uint32_t din, uint3
                                                              const uint32_t* __restrict__ biasv,
                                                              const uint32_t* __restrict__ biasm, int party,
                                                              uint32_t alpha, uint32_t* zv, uint32_t* zm,
-                                                             uint32_t* opened) {
+                                                             uint32_t* opened, const uint32_t* alpha_dev) {
+    if (alpha_dev) alpha = __ldg(alpha_dev);  // graph replays follow a re-deal
     const uint64_t cells = (uint64_t)din * rows;
     const uint32_t* peers[NP > 0 ? NP : 1];
 #pragma unroll
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
                 uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(acc[2 * p]));
                 if (p == 0) vr = fp_add(vr, de);
                 uint32_t mr = fp_add(fp_reduce64((unsigned long long)a.Cc[p][1][r] + fp_reduce64(acc[2 * p + 1])),
-                                     fp_mul(a.alpha[p], de));
+                                     fp_mul(a.alpha_dev[p] ? __ldg(a.alpha_dev[p]) : a.alpha[p], de));
                 if (a.bias[p][0]) {
                     vr = fp_add(vr, a.bias[p][0][r]);
                     mr = fp_add(mr, a.bias[p][1][r]);
@@ -843,9 +844,12 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
         unsigned long long* ar = acc_rows + (uint64_t)r * 5;
 #pragma unroll
         for (int q = 0; q < 5; ++q) atomicAdd(ar + q, acc[q]);
-        __threadfence();
-        if (atomicAdd(done_rows + r, seg) + seg == din4) {  // last segment of row r: finalise it
-            __threadfence();
+        // release: the sums above are visible before the count; acquire: the finaliser sees
+        // every other segment's sums (no full fences on the warp's path)
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(prev) : "l"(done_rows + r), "r"(seg)
+                     : "memory");
+        if (prev + seg == din4) {  // last segment of row r: finalise it
             unsigned long long sum[5];
 #pragma unroll
             for (int q = 0; q < 5; ++q) sum[q] = atomicExch(ar + q, 0ull);
@@ -856,7 +860,7 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
                 uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(sum[2 * p]));
                 if (p == 0) vr = fp_add(vr, de);
                 uint32_t mr = fp_add(fp_reduce64((unsigned long long)a.Cc[p][1][r] + fp_reduce64(sum[2 * p + 1])),
-                                     fp_mul(a.alpha[p], de));
+                                     fp_mul(a.alpha_dev[p] ? __ldg(a.alpha_dev[p]) : a.alpha[p], de));
                 if (a.bias[p][0]) {
                     vr = fp_add(vr, a.bias[p][0][r]);
                     mr = fp_add(mr, a.bias[p][1][r]);
@@ -1178,6 +1182,37 @@ __global__ void __launch_bounds__(kThreads) k_tile_e(const uint32_t* __restrict_
         out[i] = fp_sub(xv[i % din], bv[i]);
 }
 
+// Both parties' linear-layer mask in one launch (linear.cpp:40-47, value planes): D_p = W_p.v
+// - A_p.v over every cell, then E_p[t] = x_p.v - B_p.v[t] for every tile, as one grid-strided
+// range of uint4 groups (two in flight per thread), so the layer's mask is one kernel instead
+// of a D pass plus an E pass per party.
+__device__ __forceinline__ uint4 fp_sub4(const uint4 a, const uint4 b) {
+    return make_uint4(fp_sub(a.x, b.x), fp_sub(a.y, b.y), fp_sub(a.z, b.z), fp_sub(a.w, b.w));
+}
+__device__ __forceinline__ void linmask_group(const LinMask2Args& m, uint64_t ud, uint32_t din4, uint64_t g) {
+    if (g < ud) {
+        const uint4 w0 = ld4(m.w[0], g), a0 = ld4(m.a[0], g), w1 = ld4(m.w[1], g), a1 = ld4(m.a[1], g);
+        reinterpret_cast<uint4*>(m.pay[0])[g] = fp_sub4(w0, a0);
+        reinterpret_cast<uint4*>(m.pay[1])[g] = fp_sub4(w1, a1);
+    } else {
+        const uint64_t e = g - ud, c4 = e % din4;
+        const uint4 x0 = ld4(m.x[0], c4), b0 = ld4(m.b[0], e), x1 = ld4(m.x[1], c4), b1 = ld4(m.b[1], e);
+        reinterpret_cast<uint4*>(m.pay[0] + m.cells)[e] = fp_sub4(x0, b0);
+        reinterpret_cast<uint4*>(m.pay[1] + m.cells)[e] = fp_sub4(x1, b1);
+    }
+}
+__global__ void __launch_bounds__(kThreads) k_linear_mask2(LinMask2Args m) {
+    const uint64_t ud = m.cells / 4, total = ud + (uint64_t)m.din * m.ntiles / 4;
+    const uint32_t din4 = m.din / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; g + stride < total; g += 2 * stride) {  // both groups' loads issue before either's stores
+        linmask_group(m, ud, din4, g);
+        linmask_group(m, ud, din4, g + stride);
+    }
+    if (g < total) linmask_group(m, ud, din4, g);
+}
+
 __global__ void k_set_word(uint32_t* p, uint32_t v) {
     if (threadIdx.x == 0) *p = v;
 }
@@ -1354,16 +1389,17 @@ template <int NP>
 static cudaError_t mc_np(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
                          const PeerPtrs& peers_dev, const uint32_t* const mt[6], const uint32_t* biasv,
                          const uint32_t* biasm, int party, uint32_t alpha, uint32_t* zv, uint32_t* zm,
-                         uint32_t* opened, bool v4, int sms) {
+                         uint32_t* opened, bool v4, int sms, const uint32_t* alpha_dev) {
     const int grid = (int)(rows < (uint32_t)(sms * 8) ? rows : (uint32_t)(sms * 8));
     if (rows == 0) return cudaSuccess;
     if (v4)
         k_matrix_combine<NP, true><<<grid, kThreads, 0, s>>>(din, rows, rpt, own, peers_dev, mt[0], mt[1], mt[2], mt[3],
-                                                             mt[4], mt[5], biasv, biasm, party, alpha, zv, zm, opened);
+                                                             mt[4], mt[5], biasv, biasm, party, alpha, zv, zm, opened,
+                                                             alpha_dev);
     else
         k_matrix_combine<NP, false><<<grid, kThreads, 0, s>>>(din, rows, rpt, own, peers_dev, mt[0], mt[1], mt[2], mt[3],
                                                               mt[4], mt[5], biasv, biasm, party, alpha, zv, zm,
-                                                              opened);
+                                                              opened, alpha_dev);
     return launched();
 }
 
@@ -1371,7 +1407,7 @@ static cudaError_t mc_np(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t r
 cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
                                   const uint32_t* const* peers, int n_peers, const uint32_t* const mt[6],
                                   const uint32_t* biasv, const uint32_t* biasm, int party, uint32_t alpha,
-                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms) {
+                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms, const uint32_t* alpha_dev) {
     const uint64_t cells = (uint64_t)din * rows;
     bool v4 = (din % 4 == 0) && aligned16(own) && aligned16(opened) && aligned16(mt[0]) && aligned16(mt[1]) &&
               aligned16(mt[2]) && aligned16(mt[3]);
@@ -1383,7 +1419,9 @@ cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, u
     for (int p = 0; p < n_peers; ++p) peer_table.p[p] = peers[p];
     switch (n_peers) {
 #define CASE(NP) \
-    case NP: return mc_np<NP>(s, din, rows, rpt, own, peer_table, mt, biasv, biasm, party, alpha, zv, zm, opened, v4, sms);
+    case NP:                                                                                                         \
+        return mc_np<NP>(s, din, rows, rpt, own, peer_table, mt, biasv, biasm, party, alpha, zv, zm, opened, v4, sms, \
+                         alpha_dev);
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
@@ -1507,6 +1545,17 @@ cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv
     const uint64_t total = (uint64_t)din * n_tiles;
     if (total == 0) return cudaSuccess;
     k_tile_e<<<grid_for(total, sms), kThreads, 0, s>>>(xv, bv, din, total, out);
+    return launched();
+}
+
+cudaError_t launch_linear_mask2(cudaStream_t s, const LinMask2Args& m, int sms) {
+    bool ok = m.din % 4 == 0 && m.cells % 4 == 0;
+    for (int p = 0; p < 2; ++p)
+        ok = ok && aligned16(m.w[p]) && aligned16(m.a[p]) && aligned16(m.x[p]) && aligned16(m.b[p]) && aligned16(m.pay[p]);
+    if (!ok) return cudaErrorInvalidValue;  // caller falls back to the per-plane kernels
+    const uint64_t total = m.cells / 4 + (uint64_t)m.din * m.ntiles / 4;
+    if (total == 0) return cudaSuccess;
+    k_linear_mask2<<<grid_for(total, sms), kThreads, 0, s>>>(m);
     return launched();
 }
 

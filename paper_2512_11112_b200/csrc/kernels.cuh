@@ -66,6 +66,7 @@ struct MC2Args {
     const uint32_t* Cc[2][2];
     const uint32_t* bias[2][2];
     uint32_t alpha[2];
+    const uint32_t* alpha_dev[2];  // optional: alpha_i read from device memory (CUDA-graph safe)
     uint32_t* z[2][2];
     uint32_t* opened;
 };
@@ -115,7 +116,20 @@ cudaError_t launch_matrix_mask(cudaStream_t s, const uint32_t* wv, const uint32_
 cudaError_t launch_matrix_combine(cudaStream_t s, uint32_t din, uint32_t rows, uint32_t rpt, const uint32_t* own,
                                   const uint32_t* const* peers, int n_peers, const uint32_t* const mt[6],
                                   const uint32_t* biasv, const uint32_t* biasm, int party, uint32_t alpha,
-                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms);
+                                  uint32_t* zv, uint32_t* zm, uint32_t* opened, int sms,
+                                  const uint32_t* alpha_dev = nullptr);
+// Both co-located parties' linear mask: pay_p = [W_p.v - A_p.v (cells) | x_p.v - B_p.v[t] (t < ntiles)].
+// Needs din % 4 == 0 and 16-byte aligned planes (else cudaErrorInvalidValue: use the per-plane kernels).
+struct LinMask2Args {
+    const uint32_t* w[2];
+    const uint32_t* a[2];
+    const uint32_t* x[2];
+    const uint32_t* b[2];
+    uint32_t* pay[2];
+    uint64_t cells;
+    uint32_t din, ntiles;
+};
+cudaError_t launch_linear_mask2(cudaStream_t s, const LinMask2Args& m, int sms);
 // E_t = x - B_t for all tiles (B: n_tiles x din)
 cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t n_tiles,
                           uint32_t* out, int sms);

@@ -710,7 +710,7 @@ struct Exec {
                     lk(launch_modgemm(c->stream, 0, dout, din, 1, w.pub, nullptr, x.v, x.m, yv, ym), "modgemm");
                 if (b.is_public)
                     lk(launch_public(c->stream, 0, yv, ym, b.pub, b.lanes != dout, 0u, false, c->party, c->alpha,
-                                     st.out.v, st.out.m, dout, c->sms),
+                                     st.out.v, st.out.m, dout, c->sms, c->d_alpha),
                        "bias pub");
                 else if (b.lanes == dout)
                     lk(launch_add_sub(c->stream, false, yv, ym, b.v, b.m, st.out.v, st.out.m, dout, c->sms), "bias");
@@ -754,6 +754,7 @@ struct Exec {
         };
         bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
         for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
+        bool fuse2_masked = false;  // party 0's launch also wrote party 1's E
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -764,7 +765,7 @@ struct Exec {
             // bias shares bs (runtime.cpp:344-345)
             if (b.is_public)
                 lk(launch_public(c->stream, 4, nullptr, nullptr, b.pub, b.lanes != dout, 0u, false, c->party, c->alpha,
-                                 st.bias_v, st.bias_m, dout, c->sms),
+                                 st.bias_v, st.bias_m, dout, c->sms, c->d_alpha),
                    "share_of_public");
             else if (b.lanes == dout) {
                 lk(cudaMemcpyAsync(st.bias_v, b.v, dout * 4ull, cudaMemcpyDeviceToDevice, c->stream), "copy");
@@ -773,16 +774,29 @@ struct Exec {
                 lk(launch_bcast(c->stream, b.v, b.m, st.bias_v, st.bias_m, dout, c->sms), "bcast");
             // mask_tile for every tile: [D (all rows) | E_t for every tile]
             const int tk = tbegin(p);
+            bool e_done = false;
             if (!fuse2) {
                 lk(launch_matrix_mask(c->stream, w.v, st.mA[0], cells, x.v, st.mB[0], 0, st.payload, c->sms), "mask D");
-            } else if (p == 0) {  // both parties' D = W.v - A.v in one pass (d = x - a, e = y - b of mul_mask)
+            } else if (p == 0) {  // both parties' [D | E_t...] in one pass
                 auto& P1 = r->parties[1];
-                const Val& w1 = P1.ns[n.operands[1]].out;
-                lk(launch_mul_mask(c->stream, w.v, w1.v, st.mA[0], P1.ns[id].mA[0], st.payload, P1.ns[id].payload,
-                                   cells, c->sms),
-                   "mask D (both parties)");
+                const Val &w1 = P1.ns[n.operands[1]].out, &x1 = P1.ns[n.operands[0]].out;
+                const LinMask2Args m{{w.v, w1.v}, {st.mA[0], P1.ns[id].mA[0]}, {x.v, x1.v},
+                                     {st.mB[0], P1.ns[id].mB[0]}, {st.payload, P1.ns[id].payload}, cells, din, ntiles};
+                const cudaError_t e = launch_linear_mask2(c->stream, m, c->sms);
+                if (e == cudaSuccess) {
+                    e_done = fuse2_masked = true;
+                } else if (e == cudaErrorInvalidValue) {  // unaligned: D with mul_mask's d = x - a, e = y - b
+                    lk(launch_mul_mask(c->stream, w.v, w1.v, st.mA[0], P1.ns[id].mA[0], st.payload,
+                                       P1.ns[id].payload, cells, c->sms),
+                       "mask D (both parties)");
+                } else {
+                    lk(e, "linear mask (both parties)");
+                }
+            } else {
+                e_done = fuse2_masked;
             }
-            lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
+            if (!e_done)
+                lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
             tend(p, tk, SPDZ_KSTAT_MASK, (fuse2 ? (p == 0 ? 24 * cells : 0) : 12 * cells) + 12 * etot);
             sent[p] = publish(p, slot_of(id, 0));
             if (r->net) net_send_tiles(p, batch0, st.payload, din, lt);
@@ -810,6 +824,7 @@ struct Exec {
                 a.bias[p][0] = st.bias_v;
                 a.bias[p][1] = st.bias_m;
                 a.alpha[p] = r->parties[p].ctx->alpha;
+                a.alpha_dev[p] = r->parties[p].ctx->d_alpha;  // graph replays follow a re-deal
                 a.z[p][0] = st.out.v;
                 a.z[p][1] = st.out.m;
             }
@@ -857,7 +872,7 @@ struct Exec {
             lk(launch_open_sum(c->stream, st.payload + cells, peersE, k, st.opened + cells, etot, c->sms), "open E");
             const uint32_t* m6[6] = {st.mA[0], st.mA[1], st.mB[0], st.mB[1], st.mC[0], st.mC[1]};
             lk(launch_matrix_combine(c->stream, din, dout, lt.rpt, st.payload, peers, k, m6, st.bias_v, st.bias_m,
-                                     c->party, c->alpha, st.out.v, st.out.m, st.opened, c->sms),
+                                     c->party, c->alpha, st.out.v, st.out.m, st.opened, c->sms, c->d_alpha),
                "k_matrix_combine");
             // own D 4 + peer D 4k + A.v A.m 8 + opened D 4 per cell (B, E from cache)
             tend(p, tk, SPDZ_KSTAT_COMBINE, (16 + 4ull * k) * cells);
