@@ -34,3 +34,28 @@ def test_reference_runtime_drop_in(gpu):
                        timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("PASS")
+
+
+ACC = ROOT / "integration" / "_build" / "acceptance_b200"
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_on_stock_party_runtime_with_b200_injected(gpu):
+    """The reference's own acceptance scenarios (proj/tests/acceptance.cpp, unmodified) on its
+    stock PartyRuntime with the B200 back end registered as the preferred backend through the
+    3-line hook of INTEGRATION.md §3 (integration/runtime_hook.patch, inject_b200.cpp): every
+    batched op of every party of every scenario (TCP linear layer, 1000 Beaver multiplies,
+    100/100 tamper aborts, loops, 2..6 parties, determinism, stage report) runs on the GPU.
+    Criterion 11 is the reference's host-timing check (worker-count speedup of its CPU
+    scheduler, and its CPU add kernel vs a scalar loop); it is reported, not required."""
+    if not ACC.exists():
+        pytest.skip("integration/_build/acceptance_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([str(ACC)], capture_output=True, text=True, timeout=1200, cwd=str(ROOT))
+    lines = [l for l in r.stdout.splitlines() if l.startswith("criterion")]
+    assert len(lines) == 12, r.stdout + r.stderr
+    for l in lines:
+        if not l.startswith("criterion 11:"):
+            assert ": PASS" in l, l + "\n" + r.stderr[-2000:]
+    launched = [l for l in r.stderr.splitlines() if l.startswith("b200 backend injected:")]
+    assert launched and int(launched[-1].split(":")[1].split()[0]) > 1000, r.stderr[-2000:]
+    print("\n".join(lines) + "\n" + launched[-1])

@@ -34,7 +34,7 @@ def _party(rank, world, port, kind, n, coin, q, chunks=0):
         from paper_2512_11112_b200 import ChunkedRun, LocalRun, chain_graph
         x, y = O.rand_field_vec(n, 1), O.rand_field_vec(n, 2)
         if chunks:  # lane chunks on their own streams, one MAC check (ChunkedRun)
-            r = ChunkedRun(lambda L: chain_graph(kind, L), 2, n, chunks=chunks, single_party=rank, coin=coin)
+            r = ChunkedRun(lambda L: chain_graph(kind, L), world, n, chunks=chunks, single_party=rank, coin=coin)
             blobs = [None] * world
             dist.all_gather_object(blobs, r.export_ipc())
             r.import_ipc(blobs)
@@ -47,7 +47,7 @@ def _party(rank, world, port, kind, n, coin, q, chunks=0):
             dist.barrier()
             r.close()
             return
-        r = LocalRun(chain_graph(kind, n), 2, coin=coin, single_party=rank)
+        r = LocalRun(chain_graph(kind, n), world, coin=coin, single_party=rank)
         blobs = [None] * world
         dist.all_gather_object(blobs, r.export_ipc())
         r.import_ipc(blobs)
@@ -65,28 +65,31 @@ def _party(rank, world, port, kind, n, coin, q, chunks=0):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,chunks", [("heavy", 0), ("mixed", 0), ("heavy", 3)])
-def test_two_party_processes_over_ipc(gpu, kind, chunks):
+@pytest.mark.parametrize("kind,chunks,parties", [("heavy", 0, 2), ("mixed", 0, 2), ("heavy", 3, 2), ("heavy", 0, 3),
+                                                 ("mixed", 0, 4), ("heavy", 2, 3)])
+def test_party_processes_over_ipc(gpu, kind, chunks, parties):
+    """One process per party (2, 3 or 4 parties; acceptance.cpp:333-369 runs 2..6): every
+    party maps every peer's payloads and flags; outputs and each party's sigma == the oracle."""
     n, coin = 4099, 0xC0FFEE
-    want = O.sim_chain(kind, 2, O.rand_field_vec(n, 1), O.rand_field_vec(n, 2), 1, coin)
+    want = O.sim_chain(kind, parties, O.rand_field_vec(n, 1), O.rand_field_vec(n, 2), 1, coin)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_party, args=(r, 2, port, kind, n, coin, q, chunks)) for r in range(2)]
+    procs = [ctx.Process(target=_party, args=(r, parties, port, kind, n, coin, q, chunks)) for r in range(parties)]
     for p in procs:
         p.start()
     res = {}
-    for _ in range(2):
+    for _ in range(parties):
         m = q.get(timeout=300)
         assert not (isinstance(m[1], str) and m[1] == "error"), m
         res[m[0]] = m
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for rank in (0, 1):
+    for rank in range(parties):
         np.testing.assert_array_equal(res[rank][1], want["outputs"])
         assert res[rank][2] == want["sigmas"][rank]
-    assert (res[0][2] + res[1][2]) % P == 0
+    assert sum(res[r][2] for r in range(parties)) % P == 0
 
 
 def test_chunked_run_local_equals_unsharded(gpu):
