@@ -51,13 +51,14 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
     return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
 }
 
-// Instruction descriptor: kind::i8, D = s32, A = B = u8, both K-major, M = 128, N = BN.
-template <int BN>
+// Instruction descriptor: kind::i8, D = s32, A = B = u8, both K-major, M = BM (128, or 256 for a
+// CTA pair), N = BN.
+template <int BN, int BM = TM>
 __host__ __device__ constexpr uint32_t idesc_i8() {
     return (2u << 4)                      // c_format = S32
            | (0u << 7) | (0u << 10)       // a/b format = unsigned 8 bit
            | ((uint32_t)(BN >> 3) << 17)  // N >> 3
-           | ((uint32_t)(TM >> 4) << 24); // M >> 4
+           | ((uint32_t)(BM >> 4) << 24); // M >> 4
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -134,6 +135,70 @@ struct TcSmem {
     static constexpr uint32_t BYTES = kStages * STAGE + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 7 * TN <= 256 ? 256 : 512;
 };
+
+// sum_s 2^(8s) P_s mod p for 16 columns (2^32 = 5, 2^40 = 1280, 2^48 = 327680 mod p)
+__device__ __forceinline__ void tc_recombine16(const uint32_t (&v)[7][16], uint32_t (&r)[16]) {
+    constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        unsigned long long acc = 0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
+        r[t] = fp_reduce64(acc);
+    }
+}
+
+// 16 results of output row `row`, columns col0 .. col0+15 of C, into their plane (+ addend)
+__device__ __forceinline__ void tc_store16(const TcOut& out, uint32_t N, uint32_t row, uint32_t col0,
+                                           uint32_t (&r)[16]) {
+    uint32_t* dst;
+    uint32_t lim;  // valid columns in this group
+    if (out.mode == 0) {
+        const bool hi = col0 >= out.batch;
+        dst = hi ? out.y1 + (uint64_t)row * out.batch + (col0 - out.batch) : out.y0 + (uint64_t)row * out.batch + col0;
+        lim = hi ? (col0 < N ? N - col0 : 0) : out.batch - col0;
+    } else {
+        const bool hi = row >= out.dout;
+        dst = hi ? out.y1 + (uint64_t)(row - out.dout) * out.batch + col0 : out.y0 + (uint64_t)row * out.batch + col0;
+        lim = col0 < N ? N - col0 : 0;
+    }
+    if (lim >= 16 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        if (out.add0) {  // same offset in the addend plane as in the output plane
+            const bool hi = out.mode == 0 ? col0 >= out.batch : row >= out.dout;
+            const uint32_t* src = (hi ? out.add1 : out.add0) + (dst - (hi ? out.y1 : out.y0));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 a = reinterpret_cast<const uint4*>(src)[c];
+                r[4 * c] = fp_add(r[4 * c], a.x);
+                r[4 * c + 1] = fp_add(r[4 * c + 1], a.y);
+                r[4 * c + 2] = fp_add(r[4 * c + 2], a.z);
+                r[4 * c + 3] = fp_add(r[4 * c + 3], a.w);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            reinterpret_cast<uint4*>(dst)[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+    } else {
+        // group straddles the plane boundary (mode 0, batch % 16 != 0) or the edge
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const uint32_t col = col0 + t;
+            if (col >= N) break;
+            uint64_t off;
+            bool hi;
+            if (out.mode == 0) {
+                hi = col >= out.batch;
+                off = (uint64_t)row * out.batch + (hi ? col - out.batch : col);
+            } else {
+                hi = row >= out.dout;
+                off = (uint64_t)(hi ? row - out.dout : row) * out.batch + col;
+            }
+            uint32_t v = r[t];
+            if (out.add0) v = fp_add(v, (hi ? out.add1 : out.add0)[off]);
+            (hi ? out.y1 : out.y0)[off] = v;
+        }
+    }
+}
 
 template <int TN>
 __device__ __forceinline__ void tmem_ld16_x7(uint32_t taddr, uint32_t (&v)[7][16]) {
@@ -250,7 +315,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
         const uint32_t quarter = warp & 3;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
-        constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
         uint32_t it = 0;
         for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
             const uint32_t mt = tile / tiles_n, nt = tile % tiles_n;
@@ -271,63 +335,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
                 const uint32_t col0 = nt * TN + cc * 16;
                 if (row >= M) continue;
                 uint32_t r[16];
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    unsigned long long acc = 0;
-#pragma unroll
-                    for (int q = 0; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
-                    r[t] = fp_reduce64(acc);
-                }
-                // output plane + position of columns col0 .. col0+15
-                uint32_t* dst;
-                uint32_t lim;  // valid columns in this group
-                if (out.mode == 0) {
-                    const bool hi = col0 >= out.batch;
-                    dst = hi ? out.y1 + (uint64_t)row * out.batch + (col0 - out.batch)
-                             : out.y0 + (uint64_t)row * out.batch + col0;
-                    lim = hi ? (col0 < N ? N - col0 : 0) : out.batch - col0;
-                } else {
-                    const bool hi = row >= out.dout;
-                    dst = hi ? out.y1 + (uint64_t)(row - out.dout) * out.batch + col0
-                             : out.y0 + (uint64_t)row * out.batch + col0;
-                    lim = col0 < N ? N - col0 : 0;
-                }
-                if (lim >= 16 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-                    if (out.add0) {  // same offset in the addend plane as in the output plane
-                        const bool hi = out.mode == 0 ? col0 >= out.batch : row >= out.dout;
-                        const uint32_t* src = (hi ? out.add1 : out.add0) + (dst - (hi ? out.y1 : out.y0));
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const uint4 a = reinterpret_cast<const uint4*>(src)[c];
-                            r[4 * c] = fp_add(r[4 * c], a.x);
-                            r[4 * c + 1] = fp_add(r[4 * c + 1], a.y);
-                            r[4 * c + 2] = fp_add(r[4 * c + 2], a.z);
-                            r[4 * c + 3] = fp_add(r[4 * c + 3], a.w);
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        reinterpret_cast<uint4*>(dst)[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
-                } else {
-                    // group straddles the plane boundary (mode 0, batch % 16 != 0) or the edge
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        const uint32_t col = col0 + t;
-                        if (col >= N) break;
-                        uint64_t off;
-                        bool hi;
-                        if (out.mode == 0) {
-                            hi = col >= out.batch;
-                            off = (uint64_t)row * out.batch + (hi ? col - out.batch : col);
-                        } else {
-                            hi = row >= out.dout;
-                            off = (uint64_t)(hi ? row - out.dout : row) * out.batch + col;
-                        }
-                        uint32_t v = r[t];
-                        if (out.add0) v = fp_add(v, (hi ? out.add1 : out.add0)[off]);
-                        (hi ? out.y1 : out.y0)[off] = v;
-                    }
-                }
+                tc_recombine16(v, r);
+                tc_store16(out, N, row, col0, r);
             }
             if (warp == 2 && lane == 0) tl_mark(tl, 6);
         }
@@ -337,6 +346,227 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
     if (threadIdx.x == 0) tl_mark(tl, 7);
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2, M = 256) for problems whose 128 x 64 tiling
+// leaves SMs idle (C3: 1024 x 512 outputs = 64 such tiles).  A pair of CTAs on one TPC owns a
+// 256 x TN output tile (TN = 32): each CTA stages its own 128 rows of the four A limbs and two
+// of the four stacked B limbs ([B0|B1] in rank 0, [B2|B3] in rank 1), and the leader issues
+// N = 4 TN MMAs whose B operand spans both CTAs' shared memory.  Per CTA that is 6 KB of
+// operand reads per 64-clock MMA (96 B/clk) instead of the single-CTA N = 128 tile's 8 KB
+// (128 B/clk, shared-memory bound: the r02 timeline measured its MMA phase at 7.2 us against
+// 4.2 us of tensor work).  The P_s accumulators of each CTA's 128 rows live in its own TMEM;
+// every tile starts from TMEM zeroed by the epilogue (tcgen05.st), so all MMAs accumulate —
+// the single-CTA kernel's N = 192 / 64 initialisation sequence would split B across the pair
+// differently.  Stage hand-off: each CTA's TMA completes on its own full barrier; the peer's
+// warp 1 forwards its completion to the leader (remote mbarrier arrive, release.cluster); the
+// leader's commits are multicast to both CTAs' empty / accumulator barriers; both CTAs'
+// epilogue warps arrive (locally or remotely) on the leader's TMEM-empty barrier.
+constexpr int kStages2 = 6;
+constexpr int kThreadsTc2 = 320;  // warp 0 TMA, warp 1 MMA (leader) / forwarder (peer), warps 2-9 epilogue
+template <int TN>
+struct Tc2Smem {
+    static constexpr uint32_t A_LIMB = TM * TK;        // 8 KB: this CTA's 128 rows
+    static constexpr uint32_t A_STAGE = 4 * A_LIMB;    // 32 KB
+    static constexpr uint32_t B_LIMB = TN * TK;        // 2 KB at TN = 32
+    static constexpr uint32_t B_STAGE = 2 * B_LIMB;    // this CTA's two limbs of [B0|B1|B2|B3]
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    static constexpr uint32_t BYTES = kStages2 * STAGE + 1024 + 512;
+    static constexpr uint32_t TMEM_COLS = 7 * TN <= 256 ? 256 : 512;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// bounded wait with cluster-scope acquire (the arrivals came from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    for (uint32_t it = 0; it < (1u << 26); ++it) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+    }
+    __trap();
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+    asm volatile("tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(d_tmem), "l"(adesc), "l"(bdesc),
+                 "r"(idesc));
+}
+// arrive on `bar` (same shared offset) in both CTAs of the pair once the issued MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+}
+
+template <int TN>
+__global__ void __launch_bounds__(kThreadsTc2, 1) k_modgemm_tc2(const uint8_t* __restrict__ At,
+                                                                 const uint8_t* __restrict__ Bt, uint32_t M, uint32_t N,
+                                                                 uint32_t KB, uint32_t tiles_n, uint32_t n_tiles,
+                                                                 TcOut out, uint64_t* tl) {
+    static_assert(TN == 32, "epilogue assigns one 16-column chunk per warp of each lane quarter");
+    using L = Tc2Smem<TN>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
+    uint8_t* sgen = smem + (sbase - smem_u32(smem));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sgen + kStages2 * L::STAGE);
+    uint64_t* empty = full + kStages2;
+    uint64_t* pfull = empty + kStages2;  // leader: the peer's stage landed
+    uint64_t* tfull = pfull + kStages2;  // both CTAs: the tile's MMAs completed
+    uint64_t* tempty = tfull + 1;        // leader: 16 epilogue warps drained and re-zeroed TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    if (threadIdx.x == 0) {
+        tl_mark(tl, 0);
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&pfull[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 16);
+        mbar_fence_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(L::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs: barriers initialised, TMEM allocated
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) {
+        uint32_t lead;  // the pair's accumulators sit at the same TMEM address in both CTAs
+        asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(lead) : "r"(mapa_shared(smem_u32(tmem_slot), 0)));
+        if (lead != tmem) __trap();
+        tl_mark(tl, 1);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) tl_mark(tl, 2);
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs: own A rows, own two B limbs) ----
+            uint32_t g = 0;
+            for (uint32_t tile = pair; tile < n_tiles; tile += npairs) {
+                const uint32_t mt = tile / tiles_n, nt = tile % tiles_n;
+                const uint8_t* a_src = At + (uint64_t)(2 * mt + rank) * KB * L::A_STAGE;
+                const uint8_t* b_src = Bt + (uint64_t)nt * KB * (4 * L::B_LIMB) + rank * L::B_STAGE;
+                for (uint32_t kb = 0; kb < KB; ++kb, ++g) {
+                    const uint32_t s = g % kStages2;
+                    if (g >= (uint32_t)kStages2) mbar_wait(&empty[s], ((g / kStages2) - 1) & 1);
+                    const uint32_t dst = sbase + s * L::STAGE;
+                    mbar_expect_tx(&full[s], L::STAGE);
+                    bulk_g2s(dst, a_src + (uint64_t)kb * L::A_STAGE, L::A_STAGE, &full[s]);
+                    bulk_g2s(dst + L::A_STAGE, b_src + (uint64_t)kb * (4 * L::B_LIMB), L::B_STAGE, &full[s]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 1) {  // ---- peer: forward each landed stage to the leader ----
+            const uint32_t lead_pfull = mapa_shared(smem_u32(pfull), 0);
+            uint32_t g = 0;
+            for (uint32_t tile = pair; tile < n_tiles; tile += npairs)
+                for (uint32_t kb = 0; kb < KB; ++kb, ++g) {
+                    const uint32_t s = g % kStages2;
+                    mbar_wait(&full[s], (g / kStages2) & 1);
+                    mbar_arrive_cluster(lead_pfull + s * 8);
+                }
+        } else if (lane == 0) {  // ---- leader: MMA issuer for the pair ----
+            constexpr uint32_t id4 = idesc_i8<4 * TN, 2 * TM>();
+            uint32_t g = 0, it = 0;
+            for (uint32_t tile = pair; tile < n_tiles; tile += npairs, ++it) {
+                mbar_wait_cluster(tempty, it & 1);  // both CTAs' TMEM drained and zeroed
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                for (uint32_t kb = 0; kb < KB; ++kb, ++g) {
+                    const uint32_t s = g % kStages2;
+                    mbar_wait(&full[s], (g / kStages2) & 1);
+                    mbar_wait_cluster(&pfull[s], (g / kStages2) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (g == 0) tl_mark(tl, 3);
+                    const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
+#pragma unroll
+                    for (int ks = 0; ks < TK / 32; ++ks) {
+                        const uint64_t bd = smem_desc(sb + ks * 2 * kLBO, kLBO, kSBO);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            mma_i8_pair(tmem + i * TN, smem_desc(sa + i * L::A_LIMB + ks * 2 * kLBO, kLBO, kSBO), bd,
+                                        id4);
+                    }
+                    mma_commit_pair(&empty[s]);  // frees the stage in both CTAs
+                }
+                mma_commit_pair(tfull);  // both CTAs' accumulators complete
+            }
+            tl_mark(tl, 4);
+        }
+        __syncwarp();
+    } else {  // ---- epilogue: warps 2..9; TMEM lane quarter = warp % 4, 16-column chunk = (warp - 2) / 4 ----
+        const uint32_t quarter = warp & 3, chunk = (warp - 2) >> 2;
+        const uint32_t lane_base = tmem + ((quarter * 32u) << 16) + chunk * 16;
+        const uint32_t tempty_addr = rank == 0 ? smem_u32(tempty) : mapa_shared(smem_u32(tempty), 0);
+        auto zero_and_release = [&]() {  // the next tile's MMAs accumulate onto zeros
+#pragma unroll
+            for (int q = 0; q < 7; ++q) tmem_zero16(lane_base + q * TN);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_addr);
+        };
+        zero_and_release();
+        uint32_t it = 0;
+        for (uint32_t tile = pair; tile < n_tiles; tile += npairs, ++it) {
+            const uint32_t mt = tile / tiles_n, nt = tile % tiles_n;
+            const uint32_t row = (2 * mt + rank) * TM + quarter * 32 + lane;
+            mbar_wait(tfull, it & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (warp == 2 && lane == 0) tl_mark(tl, 5);
+            uint32_t v[7][16];
+            tmem_ld16_x7<TN>(lane_base, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            zero_and_release();
+            if (row < M) {
+                uint32_t r[16];
+                tc_recombine16(v, r);
+                tc_store16(out, N, row, nt * TN + chunk * 16, r);
+            }
+            if (warp == 2 && lane == 0) tl_mark(tl, 6);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // no CTA leaves while its peer may still signal it
+    if (threadIdx.x == 0) tl_mark(tl, 7);
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::TMEM_COLS));
 }
 
 // A (rows, stacked a0 over a1) -> pre-tiled limb image, one thread per 16-byte piece
@@ -470,9 +700,9 @@ uint64_t* g_tc_tl = nullptr;  // diagnostic timeline buffer (8 stamps per CTA), 
 template <int BN>
 cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t lda, uint32_t batch,
                    const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx,
-                   uint8_t* scratch, const uint8_t* a_image, const TcOut& out, int sms) {
+                   uint8_t* scratch, const uint8_t* a_image, const TcOut& out, int sms, bool pair = false) {
     const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
-    const uint32_t Mp = (M + TM - 1) / TM * TM, Np = (N + BN - 1) / BN * BN;
+    const uint32_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Np = (N + BN - 1) / BN * BN;  // pair tiles: 256 rows
     const uint32_t KB = (din + TK - 1) / TK;
     // a prepared A image (spdz_linear_weights) is used as is: only B is re-laid out
     const uint8_t* At = a_image ? a_image : scratch;
@@ -492,6 +722,37 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         pdl = true;
     }
     if (g_tc_dbg & 4) return cudaSuccess;  // (diagnostic bit 2 skips the GEMM kernel)
+    if (pair) {  // CTA pairs on 256 x 32 tiles (k_modgemm_tc2)
+        using L2 = Tc2Smem<32>;
+        static bool attr_pair = false;
+        if (!attr_pair) {
+            cudaError_t e = cudaFuncSetAttribute(k_modgemm_tc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 L2::BYTES);
+            if (e != cudaSuccess) return e;
+            attr_pair = true;
+        }
+        const uint32_t tiles_n = Np / 32, n_tiles = tiles_n * (Mp / (2 * TM));
+        const uint32_t pairs = std::min<uint32_t>(n_tiles, (uint32_t)sms / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(kThreadsTc2);
+        cfg.dynamicSmemBytes = L2::BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 2 : 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_modgemm_tc2<32>, (const uint8_t*)At, (const uint8_t*)Bt, M, N, KB,
+                                           tiles_n, n_tiles, out, g_tc_tl);
+        ++g_kernel_launches;
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
     using L = TcSmem<BN>;
     static bool attr2 = false;
     if (!attr2) {
@@ -499,7 +760,7 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
         if (e != cudaSuccess) return e;
         attr2 = true;
     }
-    const uint32_t tiles_n = Np / BN, n_tiles = tiles_n * (Mp / TM);
+    const uint32_t tiles_n = Np / BN, n_tiles = tiles_n * ((M + TM - 1) / TM);  // (the image pads M to 256)
     const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)sms);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -525,7 +786,7 @@ void modgemm_tc_timeline(uint64_t* dev_buf) { g_tc_tl = dev_buf; }
 uint64_t modgemm_tc_scratch_bytes(int mode, uint32_t dout, uint32_t din, uint32_t batch) {
     din = std::min<uint32_t>(din, kMaxKSlice);  // one K slice at a time
     const uint64_t M = mode == 0 ? dout : 2ull * dout, N = mode == 0 ? 2ull * batch : batch;
-    const uint64_t Mp = (M + TM - 1) / TM * TM, Np = (N + 63) / 64 * 64, Kp = (din + TK - 1) / TK * TK;
+    const uint64_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Np = (N + 63) / 64 * 64, Kp = (din + TK - 1) / TK * TK;
     return 4 * (Mp + Np) * Kp + 256;
 }
 
@@ -557,10 +818,12 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
         const uint32_t* a1 = w1 ? w1 + k0 : nullptr;
         const uint32_t* b0 = x0 + xo;
         const uint32_t* b1 = x1 ? x1 + xo : nullptr;
-        // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64)
+        // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64);
+        // narrow problems run as CTA pairs on 256 x 32 tiles (bit 8 keeps the single-CTA 128 x 32 kernel)
         const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
         const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
-        cudaError_t e = narrow ? run_tc<32>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms)
+        const bool pair = narrow && !(g_tc_dbg & 256);
+        cudaError_t e = narrow ? run_tc<32>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms, pair)
                                : run_tc<64>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms);
         if (e != cudaSuccess) return e;
     }
@@ -570,14 +833,14 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
 // The A-side limb image alone (a public weight matrix prepared once for many calls).
 uint64_t modgemm_tc_a_image_bytes(int mode, uint32_t dout, uint32_t din) {
     const uint64_t M = mode == 0 ? dout : 2ull * dout;
-    const uint64_t Mp = (M + TM - 1) / TM * TM, Kp = (din + TK - 1) / TK * TK;
+    const uint64_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Kp = (din + TK - 1) / TK * TK;
     return 4 * Mp * Kp;
 }
 
 cudaError_t launch_tile_a(cudaStream_t s, int mode, uint32_t dout, uint32_t din, const uint32_t* w0,
                           const uint32_t* w1, uint8_t* image, int sms) {
     const uint32_t M = mode == 0 ? dout : 2 * dout;
-    const uint32_t Mp = (M + TM - 1) / TM * TM, KB = (din + TK - 1) / TK;
+    const uint32_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), KB = (din + TK - 1) / TK;
     const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
     const uint32_t row_blocks = (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
     const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, image, din};
