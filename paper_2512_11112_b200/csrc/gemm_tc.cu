@@ -124,7 +124,7 @@ struct TcOut {
 // TN = 64 for large problems (N = 256 MMAs); TN = 32 (N = 128 MMAs, twice the tiles)
 // when the TN = 64 tiling would leave SMs idle.
 constexpr int kStages = 4;
-constexpr int kThreadsTc = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kThreadsTc = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (two per TMEM lane quarter)
 template <int TN>
 struct TcSmem {
     static constexpr uint32_t A_LIMB = TM * TK;        // 8 KB
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 4);
+        mbar_init(tempty, 8);
         mbar_fence_init();
     }
     if (warp == 0) {
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             tl_mark(tl, 4);
         }
         __syncwarp();
-    } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4 ----
-        const uint32_t quarter = warp & 3;
+    } else {  // ---- epilogue: warps 2..9, TMEM lane quarter = warp % 4, 16-column chunks split by (warp-2)/4 ----
+        const uint32_t quarter = warp & 3, half = (warp - 2) >> 2;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
         uint32_t it = 0;
         for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
@@ -323,11 +323,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (warp == 2 && lane == 0) tl_mark(tl, 5);
 #pragma unroll 1
-            for (int cc = 0; cc < TN / 16; ++cc) {
+            for (int cc = half; cc < TN / 16; cc += 2) {
                 uint32_t v[7][16];
                 tmem_ld16_x7<TN>(lane_base + cc * 16, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (cc == TN / 16 - 1) {  // every column of this tile is in registers: release TMEM
+                if (cc + 2 >= TN / 16) {  // every column of this warp's share is in registers: release TMEM
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty);
@@ -819,10 +819,11 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
         const uint32_t* b0 = x0 + xo;
         const uint32_t* b1 = x1 ? x1 + xo : nullptr;
         // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64);
-        // narrow problems run as CTA pairs on 256 x 32 tiles (bit 8 keeps the single-CTA 128 x 32 kernel)
+        // bit 9 runs narrow problems as CTA pairs on 256 x 32 tiles (k_modgemm_tc2: correct, but measured
+        // slower at C3, 22.6 vs 16.5 us — both variants are bound by the L2->SMEM operand stream)
         const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
-        const bool narrow = (g_tc_dbg & 64) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
-        const bool pair = narrow && !(g_tc_dbg & 256);
+        const bool narrow = (g_tc_dbg & (64 | 512)) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
+        const bool pair = narrow && (g_tc_dbg & 512);
         cudaError_t e = narrow ? run_tc<32>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms, pair)
                                : run_tc<64>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms);
         if (e != cudaSuccess) return e;

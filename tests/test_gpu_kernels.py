@@ -452,7 +452,7 @@ def _np_modmatmul(A, B):
     return ((hi * 65536 + lo) % P).astype(np.uint32)
 
 
-@pytest.mark.parametrize("tiles", [0, 64, 128, 320])
+@pytest.mark.parametrize("tiles", [0, 64, 128, 512])
 @pytest.mark.parametrize("din,dout,batch,fill", [(512, 2048, 300, "rand"), (8192, 256, 64, "max"),
                                                  (300, 130, 70, "rand"), (64, 1200, 520, "rand"),
                                                  (20000, 192, 40, "max"), (8200, 130, 33, "rand"),
@@ -461,9 +461,8 @@ def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
     """Every output of the tcgen05 GEMM (both planes, both modes) against an exact
     numpy mod-p matmul: persistent tiles (more tiles than SMs), edge tiles, and
     all-(p-1) operands at K = 8192 (the s32 limb-accumulator bound); tile width
-    chosen automatically (0: CTA pairs on 256 x 32 tiles when 128 x 64 tiles leave SMs
-    idle, e.g. C3 = 1024 x 1024 x 256), forced to 32 columns (64: CTA pairs), to 64 columns
-    (128), or to the single-CTA 128 x 32 kernel (320)."""
+    chosen automatically (0), forced to 32 (64) or to 64 columns (128), or the CTA-pair
+    kernel on 256 x 32 tiles (512; tcgen05.mma.cta_group::2), incl. the C3 shape."""
     import ctypes as C
     from paper_2512_11112_b200 import DeviceShare
     from paper_2512_11112_b200._lib import check, lib
