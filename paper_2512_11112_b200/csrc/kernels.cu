@@ -210,6 +210,15 @@ struct OpMask : NoPeer {  // backend.cpp:53-65: in xv yv av bv -> d e
     }
 };
 
+struct OpMask2 : NoPeer {  // both co-located parties: x0 y0 a0 b0 x1 y1 a1 b1 -> d0 e0 d1 e1
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        o[0] = fp_sub(a[0], a[2]);
+        o[1] = fp_sub(a[1], a[3]);
+        o[2] = fp_sub(a[4], a[6]);
+        o[3] = fp_sub(a[5], a[7]);
+    }
+};
+
 // Fused open + Beaver combine.  Inputs: own_d, own_e, peer_d[NP], peer_e[NP],
 // a.v a.m b.v b.m c.v c.m.  Outputs: z.v z.m [open_d open_e].
 template <int NP, bool LOG>
@@ -1271,6 +1280,12 @@ cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* 
                             const uint32_t* bv, uint32_t* d, uint32_t* e, uint64_t n, int sms) {
     IO<4, 2> io{{xv, yv, av, bv}, {d, e}};
     return run_map(s, io, n, OpMask{}, sms);
+}
+
+cudaError_t launch_mul_mask2(cudaStream_t s, const uint32_t* const xyab[8], uint32_t* const de[4], uint64_t n,
+                             int sms) {
+    IO<8, 4> io{{xyab[0], xyab[1], xyab[2], xyab[3], xyab[4], xyab[5], xyab[6], xyab[7]}, {de[0], de[1], de[2], de[3]}};
+    return run_map(s, io, n, OpMask2{}, sms);
 }
 
 cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,

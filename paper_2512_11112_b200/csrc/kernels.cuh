@@ -49,6 +49,10 @@ cudaError_t launch_public(cudaStream_t s, int op, const uint32_t* xv, const uint
 // backend.cpp:53-65
 cudaError_t launch_mul_mask(cudaStream_t s, const uint32_t* xv, const uint32_t* yv, const uint32_t* av,
                             const uint32_t* bv, uint32_t* d, uint32_t* e, uint64_t n, int sms);
+// both co-located parties' masks in one pass: xyab = {x0.v y0.v a0.v b0.v x1.v y1.v a1.v b1.v},
+// de = {d0 e0 d1 e1}
+cudaError_t launch_mul_mask2(cudaStream_t s, const uint32_t* const xyab[8], uint32_t* const de[4], uint64_t n,
+                             int sms);
 // spdz.cpp:77-96 fused with the open of net.cpp:170-215: d = own_d + sum reduce(peer_d) ...
 cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
                                   const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,

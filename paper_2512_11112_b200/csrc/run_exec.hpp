@@ -483,14 +483,13 @@ struct Exec {
         }
         const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
         const uint32_t* alpha_dev[2] = {P0.ctx->d_alpha, P1.ctx->d_alpha};
-        for (int p = 0; p < 2; ++p) {
-            auto& P = r->parties[p];
-            auto& st = P.ns[id];
-            const int tk = tbegin(p);
-            lk(launch_mul_mask(S(r, p), st.xa.v, st.xb.v, P.pool[0] + off, P.pool[2] + off, st.payload,
-                               st.payload + L, L, SMS(r, p)),
-               "k_mul_mask");
-            tend(p, tk, SPDZ_KSTAT_MASK, 24 * L);
+        {  // both parties' d = x - a, e = y - b in one pass (48 bytes per lane)
+            const int tk = tbegin(0);
+            const uint32_t* xyab[8] = {s0.xa.v, s0.xb.v, P0.pool[0] + off, P0.pool[2] + off,
+                                       s1.xa.v, s1.xb.v, P1.pool[0] + off, P1.pool[2] + off};
+            uint32_t* const dd[4] = {s0.payload, s0.payload + L, s1.payload, s1.payload + L};
+            lk(launch_mul_mask2(S(r, 0), xyab, dd, L, SMS(r, 0)), "k_mul_mask2");
+            tend(0, tk, SPDZ_KSTAT_MASK, 48 * L);
         }
         const uint32_t* de[4] = {s0.payload, s0.payload + L, s1.payload, s1.payload + L};
         const uint32_t *t0[6], *t1[6];
