@@ -430,6 +430,10 @@ typedef struct spdz_run_options {
      * A node waiting for a peer's opening then stalls only its own stream, so independent
      * nodes run on.  Reductions and linear layers stay on stream 0 (shared scratch). */
     int32_t node_streams;
+    /* 1: parties that share a device and stream still run their own kernels (mask, open +
+     * combine, MAC sigma, input sharing per party), as they would on separate GPUs; 0
+     * (default): two such parties' passes are fused (payloads and coefficients read once). */
+    int32_t separate_party_kernels;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes

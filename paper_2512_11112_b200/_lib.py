@@ -66,7 +66,8 @@ class RunOptions(C.Structure):  # spdz_run_options_t
                 ("use_graph", C.c_int32), ("devices", C.c_int32 * MAX_PARTIES), ("profile_kernels", C.c_int32),
                 ("stream_per_party", C.c_int32), ("shard_offset", C.c_uint64), ("shard_total", C.c_uint64),
                 ("external_mac_verify", C.c_int32), ("single_party", C.c_int32), ("entry_label", C.c_uint32),
-                ("loop_iters", C.c_uint64), ("network", C.c_int32), ("node_streams", C.c_int32)]
+                ("loop_iters", C.c_uint64), ("network", C.c_int32), ("node_streams", C.c_int32),
+                ("separate_party_kernels", C.c_int32)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t

@@ -42,7 +42,7 @@ uint64_t agree_coin(spdz_run* r, bool have_coin, uint64_t given_coin) {
 // Both parties of a 2-party run local on one stream with rank-identical logs: one pass
 // (the coefficient stream r_j is the same for both, spdz.cpp:131-135).
 bool mac_fusable(spdz_run* r) {
-    if (r->n != 2 || !r->parties[0].local || !r->parties[1].local || S(r, 0) != S(r, 1)) return false;
+    if (!colocated2(r)) return false;
     const auto &a = r->parties[0].maclog, &b = r->parties[1].maclog;
     if (a.size() != b.size()) return false;
     for (size_t i = 0; i < a.size(); ++i)
@@ -182,7 +182,7 @@ void mac_check(spdz_run* r, spdz_run_report_t* rep, bool have_coin, uint64_t giv
 // Input sharing of a 2-party run with both parties on one stream runs as one kernel per
 // input (the bound input stays raw until then).
 bool share_fused(spdz_run* r) {
-    return r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+    return colocated2(r);
 }
 
 void share_inputs(spdz_run* r) {

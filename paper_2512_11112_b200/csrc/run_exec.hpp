@@ -518,7 +518,7 @@ struct Exec {
                 st.opened = st.opened_all + 2 * L * exec;
             }
         }
-        bool pair = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+        bool pair = colocated2(r);
         for (auto& f : r->faults) pair = pair && f.node != id;
         if (pair) {
             beaver_pair(id, off);
@@ -751,7 +751,7 @@ struct Exec {
             lk(cudaMemcpyAsync(snap + cells, x.m, din * 4ull, cudaMemcpyDeviceToDevice, S(r, p)), "snapshot x.m");
             return {snap, snap + cells};
         };
-        bool fuse2 = r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1);
+        bool fuse2 = colocated2(r);
         for (auto& f : r->faults) fuse2 = fuse2 && f.node != id;
         bool fuse2_masked = false;  // party 0's launch also wrote party 1's E
         for (int p = 0; p < r->n; ++p) {

@@ -299,6 +299,11 @@ inline void load_stream_memops() {
 }
 
 inline cudaStream_t S(spdz_run* r, int p) { return r->parties[p].ctx->stream; }
+// both parties of a 2-party run on one stream: their passes may be fused (read shared data once)
+inline bool colocated2(spdz_run* r) {
+    return r->n == 2 && r->parties[0].local && r->parties[1].local && S(r, 0) == S(r, 1) &&
+           !r->opts.separate_party_kernels;
+}
 inline int SMS(spdz_run* r, int p) { return r->parties[p].ctx->sms; }
 inline void dev(spdz_run* r, int p) { device_guard(r->parties[p].ctx); }
 

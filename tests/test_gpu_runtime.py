@@ -499,3 +499,35 @@ def test_graph_replay_linear_and_reductions(gpu, case):
         for p in range(2):
             for k in range(2):
                 np.testing.assert_array_equal(n0[p][k], n1[p][k])
+
+
+@pytest.mark.parametrize("case", ["heavy", "mixed", "linear", "linear_v1"])
+def test_separate_party_kernels_equal_fused(gpu, case):
+    """separate_party_kernels: the two parties on one stream run their own mask, open +
+    combine, input-sharing and sigma kernels (the per-GPU kernel mix of the multi-GPU layout);
+    outputs, node shares and sigmas (fixed coin) are bit-exact with the co-located fused
+    passes."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph, linear_graph
+    coin = 0xA11CE
+    if case.startswith("linear"):
+        din, dout = (516, 130) if case == "linear" else (1030, 33)
+        g = linear_graph(din, dout)
+        inp = {"x": O.rand_field_vec(din, 1), "W": O.rand_field_vec(din * dout, 2), "b": O.rand_field_vec(dout, 3)}
+    else:
+        n = (1 << 20) + 3
+        g = chain_graph(case, n)
+        inp = {"x": O.rand_field_vec(n, 1), "y": O.rand_field_vec(n, 2)}
+    node = g.nodes[g.root].operands[0]
+    got = {}
+    for sep in (False, True):
+        r = LocalRun(g, 2, slice_=65536, coin=coin, separate_party_kernels=sep)
+        r.bind_inputs(inp)
+        r.share_inputs()
+        rep = r.online()
+        got[sep] = (rep.outputs.copy(), rep.sigmas, [r.node_share_host(p, node) for p in range(2)])
+        r.close()
+    np.testing.assert_array_equal(got[False][0], got[True][0])
+    assert got[False][1] == got[True][1]
+    for p in range(2):
+        for k in range(2):
+            np.testing.assert_array_equal(got[False][2][p][k], got[True][2][p][k])
