@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libspdz_b200.so"
-SOURCES = ["kernels.cu", "capi.cu", "run.cu", "run_plan.cu", "diag.cu", "gemm_tc.cu", "store.cu", "net.cpp"]
+SOURCES = ["kernels.cu", "capi.cu", "run.cu", "run_plan.cu", "diag.cu", "gemm_tc.cu", "store.cu", "net.cpp", "hostcopy.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "field.cuh"
+#include "hostcopy.hpp"
 #include "internal.hpp"
 
 using namespace spdzb200;
@@ -833,13 +834,21 @@ struct Staging {
         off += (words * 4 + 15) / 16 * 16;
         return p;
     }
+    // large pageable host vectors (the reference Backend's std::vector operands) go through the
+    // pinned staging ring at multi-threaded memcpy speed (hostcopy.cu)
     uint32_t* up(const uint32_t* h, uint64_t words) {
         uint32_t* d = take(words);
-        if (words) cuda_check(cudaMemcpyAsync(d, h, words * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        if (words * 4 >= (1u << 20) && is_pageable(h))
+            cuda_check(staged_h2d(ctx->device, d, h, words * 4, ctx->stream), "staged H2D");
+        else if (words)
+            cuda_check(cudaMemcpyAsync(d, h, words * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
         return d;
     }
     void down(uint32_t* h, const uint32_t* d, uint64_t words) {
-        if (words) cuda_check(cudaMemcpyAsync(h, d, words * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        if (words * 4 >= (1u << 20) && is_pageable(h))
+            cuda_check(staged_d2h(ctx->device, h, d, words * 4, ctx->stream), "staged D2H");
+        else if (words)
+            cuda_check(cudaMemcpyAsync(h, d, words * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     }
     void sync() { cuda_check(cudaStreamSynchronize(ctx->stream), "sync"); }
 };

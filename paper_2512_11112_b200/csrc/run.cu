@@ -5,6 +5,7 @@
 // kernels, ordered by per-party events (the batch-id matching of
 // net.cpp:61-95 becomes stream/event ordering).  Every share, triple pool,
 // opened-value log and MAC record lives in HBM as structure-of-arrays.
+#include "hostcopy.hpp"
 #include "run_exec.hpp"
 #include "run_state.hpp"
 
@@ -547,12 +548,15 @@ int spdz_run_bind_input(spdz_run* r, uint32_t node, const uint32_t* host_vals, u
         uint32_t* d = it == r->input_dev.end() ? (r->input_dev[node] = r->alloc(0, len)) : it->second;
         dev(r, 0);
         auto& P0 = r->parties[0];
+        // pageable sources (plain numpy / std::vector) go through the pinned staging ring at
+        // multi-threaded memcpy speed (hostcopy.cu); pinned ones are DMA'd directly
+        const bool staged = len * 4 >= (1u << 20) && is_pageable(host_vals);
+        cudaStream_t hs = r->h2d_stream ? r->h2d_stream : P0.ctx->stream;
+        if (staged) lk(staged_h2d(r->devices[0], d, host_vals, len * 4, hs), "staged H2D input");
+        else lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, hs), "H2D input");
         if (r->h2d_stream) {
-            lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, r->h2d_stream), "H2D input");
             lk(cudaEventRecord(r->ev_h2d, r->h2d_stream), "record h2d");
             lk(cudaStreamWaitEvent(P0.ctx->stream, r->ev_h2d, 0), "wait h2d");
-        } else {
-            lk(cudaMemcpyAsync(d, host_vals, len * 4, cudaMemcpyHostToDevice, P0.ctx->stream), "H2D input");
         }
         // reduce mod p (preproc.cpp:149 fp::reduce): x * 1 mod p, unless input sharing does it inline
         if (!share_fused(r))
@@ -769,7 +773,7 @@ int spdz_run_outputs(spdz_run* r, uint32_t* host_out, uint64_t cap, uint64_t* le
         need(r != nullptr, SPDZ_ERR_INVALID_ARGUMENT, "null run");
         if (len) *len = r->host_out_len;
         if (host_out && host_out != r->host_out)
-            std::memcpy(host_out, r->host_out, std::min<uint64_t>(cap, r->host_out_len) * 4);
+            parallel_copy(host_out, r->host_out, std::min<uint64_t>(cap, r->host_out_len) * 4);
     });
 }
 

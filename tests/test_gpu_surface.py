@@ -103,3 +103,28 @@ def test_share_buffers_roundtrip(gpu):
     assert np.array_equal(m2, (m.astype(np.uint64) * 3 % P).astype(np.uint32))
     check(lib().spdz_share_free(c.h, C.byref(s)))
     assert not s.vals and s.lanes == 0
+
+
+@pytest.mark.parametrize("n", [(1 << 21) + 5, 3 << 20])
+def test_host_backend_large_pageable_vs_oracle(gpu, n):
+    """The reference-shaped Backend over host vectors (backend.cpp:25-74) at sizes where the
+    operands go through the pinned staging ring (hostcopy.cu: pageable numpy in, pageable
+    numpy out, slices copied by the worker pool): add, sub, mask, combine == the oracle."""
+    from oracle import oracle as O
+    from paper_2512_11112_b200.backend import GpuBackend, ShareVec, TripleShares
+    be = GpuBackend(0)
+    xv, xm, yv, ym = (O.rand_field_vec(n, s) for s in (1, 2, 3, 4))
+    x, y = ShareVec(xv, xm), ShareVec(yv, ym)
+    for sub in (False, True):
+        z = (be.sub_batch if sub else be.add_batch)(x, y)
+        wv, wm = O.add_batch(xv, xm, yv, ym, sub=sub)
+        assert np.array_equal(z.vals, wv) and np.array_equal(z.macs, wm)
+    d = O.Dealer(2, 17)
+    tri = d.triples(n)
+    t0 = TripleShares(ShareVec(tri[0, 0], tri[1, 0]), ShareVec(tri[2, 0], tri[3, 0]), ShareVec(tri[4, 0], tri[5, 0]))
+    dd, ee = be.mul_mask(x, y, t0)
+    wd, we = O.mul_mask(xv, yv, tri[0, 0], tri[2, 0])
+    assert np.array_equal(dd, wd) and np.array_equal(ee, we)
+    z = be.mul_combine(t0, wd, we, 0, d.alpha_share(0))
+    zv, zm = O.beaver_combine(tri[:, 0], wd, we, 0, d.alpha_share(0))
+    assert np.array_equal(z.vals, zv) and np.array_equal(z.macs, zm)
