@@ -8,6 +8,7 @@
 //   * bench.py --impl reference / cpu_baseline — times the reference CPU path.
 //
 // Every function cites the reference entry point it forwards to.
+#include <malloc.h>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -675,8 +676,9 @@ double reft_time_beaver_kernels(uint64_t lanes, int reps) {
 // ---- same-config reference timing (bench.py --impl reference) ----
 // runtime::run_local (runtime.cpp:586-613) split so the dealer runs once: `reft_bench_create`
 // compiles the graph and deals every party's store (make_dealer_stores, triple_store.cpp:248);
-// each `reft_bench_run` gives every party a freshly loaded copy of its store (all cursors and
-// consumed bitmaps at zero, as read_store_file returns one) and runs the unmodified
+// each `reft_bench_run` gives every party a fresh store holding the dealt pools (all cursors and
+// consumed bitmaps at zero, as read_store_file returns one; the pools are moved in and back out,
+// never copied, so the full 2^24-lane workload fits the host's memory) and runs the unmodified
 // PartyRuntime over the simulated transport.  report: [setup_ms, online_ms, copy_ms] (max
 // over parties; online_ms is the reference's own RunReport.online_ms).
 struct RefBench {
@@ -685,6 +687,18 @@ struct RefBench {
     int n = 2;
     uint64_t slice = 262140;
 };
+
+// the pools of `src` into `dst` (moved: the stores can hold gigabytes at 2^24 lanes)
+static void move_pools(spdz::TripleStore& dst, spdz::TripleStore& src) {
+    dst.a_vals = std::move(src.a_vals);
+    dst.a_macs = std::move(src.a_macs);
+    dst.b_vals = std::move(src.b_vals);
+    dst.b_macs = std::move(src.b_macs);
+    dst.c_vals = std::move(src.c_vals);
+    dst.c_macs = std::move(src.c_macs);
+    dst.matrix = std::move(src.matrix);
+    dst.masks = std::move(src.masks);
+}
 
 void* reft_bench_create(const char* ir_text, int n_parties, uint64_t slice, uint64_t dealer_seed) {
     void* h = nullptr;
@@ -718,16 +732,16 @@ int reft_bench_run(void* h, int threads, uint64_t io_timeout_ms, int n_inputs, c
             c->n_parties = s->n_parties;
             c->alpha_share = s->alpha_share;
             c->loop_iters = s->loop_iters;
-            c->a_vals = s->a_vals;
-            c->a_macs = s->a_macs;
-            c->b_vals = s->b_vals;
-            c->b_macs = s->b_macs;
-            c->c_vals = s->c_vals;
-            c->c_macs = s->c_macs;
-            c->matrix = s->matrix;
-            c->masks = s->masks;
+            move_pools(*c, *s);  // the dealt pools, lent to the fresh store for this run (no copy)
             fresh.push_back(std::move(c));
         }
+        struct GiveBack {  // take_range copies out of the pools and never writes them: hand them back
+            RefBench* b;
+            std::vector<std::shared_ptr<spdz::TripleStore>>* fresh;
+            ~GiveBack() {
+                for (size_t i = 0; i < fresh->size(); ++i) move_pools(*b->stores[i], *(*fresh)[i]);
+            }
+        } give_back{b, &fresh};
         auto inputs = make_inputs(n_inputs, names, vals, lens);
         const double copy_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         runtime::RunOptions opts;
@@ -748,6 +762,7 @@ int reft_bench_run(void* h, int threads, uint64_t io_timeout_ms, int n_inputs, c
                 }
             });
         for (auto& t : th) t.join();
+        malloc_trim(0);  // the runtimes' freed buffers back to the OS (per-thread arenas grow across runs)
         for (auto& e : errors)
             if (e) std::rethrow_exception(e);
         double online = 0, setup = 0;
