@@ -333,31 +333,52 @@ def linear_block(with_reference: bool) -> dict:
     ys = DeviceShare.empty(dout * batch)
     a = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
     check(lib().spdz_set_gemm_path(2))
-    for _ in range(5):
-        check(lib().spdz_linear_secret_public(*a))
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = 50
-    e0.record()
-    for _ in range(iters):
-        check(lib().spdz_linear_secret_public(*a))
-    e1.record()
-    torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / iters * 1e3
-    # the inference case: public W laid out once (spdz_linear_weights_create), per call X's limb split + GEMM
+
+    def eager_us(fn):
+        """per call, back-to-back launches from the host (host launch cost included)"""
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters * 1e3
+
+    def graphed_us(fn):
+        """per call, `iters` calls captured once as a CUDA graph and replayed (device time: how the
+        executor runs a layer inside a graphed online phase)"""
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ctx.use_torch_stream()
+            for _ in range(iters):
+                fn()
+        ctx.use_torch_stream()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters * 1e3
+
+    per_call = lambda: check(lib().spdz_linear_secret_public(*a))  # noqa: E731
+    us_eager, us = eager_us(per_call), graphed_us(per_call)
+    # the inference case: public W laid out once (spdz_linear_weights_create), per call one launch
     wts = ctx.prepare_weights(W, dout, din)
     pargs = (ctx.h, wts.h, batch, C.byref(dshare(xs)), C.byref(dshare(ys)))
-    for _ in range(5):
-        check(lib().spdz_linear_secret_public_prepared(*pargs))
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(iters):
-        check(lib().spdz_linear_secret_public_prepared(*pargs))
-    e1.record()
-    torch.cuda.synchronize()
-    us_prep = e0.elapsed_time(e1) / iters * 1e3
+    prepared = lambda: check(lib().spdz_linear_secret_public_prepared(*pargs))  # noqa: E731
+    us_prep_eager, us_prep = eager_us(prepared), graphed_us(prepared)
     wts.close()
     check(lib().spdz_set_gemm_path(0))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # measured dense int8 tensor throughput of this device (cuBLASLt IMMA via torch._int_mm, 8192^3)
     a8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda")
     b8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
@@ -380,8 +401,12 @@ def linear_block(with_reference: bool) -> dict:
             raise RuntimeError("C3 output mismatch")
     modmacs = 2 * din * dout * batch
     out["C3_secret_public_1024x1024_b256"] = {
-        "us": us, "us_prepared_weights": us_prep, "modmacs": modmacs,
-        "path": "tcgen05 kind::i8 limb GEMM (16 u8 MACs per modMAC)",
+        "us": us, "us_prepared_weights": us_prep, "us_eager": us_eager, "us_prepared_weights_eager": us_prep_eager,
+        "timing": "us / us_prepared_weights: device time per call inside a replayed CUDA graph of 50 calls; "
+                  "*_eager: 50 back-to-back calls from Python (host launch cost included)",
+        "modmacs": modmacs,
+        "path": "tcgen05 kind::i8 limb GEMM (16 u8 MACs per modMAC), split-K CTA clusters on 128x64 tiles",
+        "frac_of_nominal_i8_prepared": 16 * modmacs / (us_prep / 1e6) / 2.25e15,
         "i8_mac_per_s": 16 * modmacs / (us / 1e6), "frac_of_nominal_i8": 16 * modmacs / (us / 1e6) / 2.25e15,
         "frac_of_measured_i8": 16 * modmacs / (us / 1e6) / i8_peak,
         "measured_i8_peak_mac_per_s": i8_peak,

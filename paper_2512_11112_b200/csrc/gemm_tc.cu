@@ -74,22 +74,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-// diagnostic timeline (spdz_diag_gemm_tc_timeline): per CTA 8 %globaltimer stamps
+// diagnostic timeline (spdz_diag_gemm_tc_timeline): per CTA 16 %globaltimer stamps
 __device__ __forceinline__ void tl_mark(uint64_t* tl, uint32_t slot) {
     if (tl) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        tl[blockIdx.x * 8 + slot] = t;
+        tl[blockIdx.x * 16 + slot] = t;
     }
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-}
 
 // Shared-memory image of one limb tile (rows x TK bytes), canonical K-major
 // no-swizzle layout: byte (r, k) at (r/8)*SBO + (k/16)*LBO + (r%8)*16 + k%16.
@@ -200,10 +193,37 @@ __device__ __forceinline__ void tc_store16(const TcOut& out, uint32_t N, uint32_
     }
 }
 
+// The seven P_s accumulators of 16 columns (TMEM columns taddr + s TN), issued as one block of
+// loads with a single wait: as separate statements ptxas may serialise them (one TMEM round trip
+// each) when registers are tight, which measured ~1 us per 16-column chunk in the split-K epilogue.
 template <int TN>
 __device__ __forceinline__ void tmem_ld16_x7(uint32_t taddr, uint32_t (&v)[7][16]) {
-#pragma unroll
-    for (int t = 0; t < 7; ++t) tmem_ld16(taddr + t * TN, v[t]);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%112];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%113];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%114];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%115];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%64,%65,%66,%67,%68,%69,%70,%71,%72,%73,%74,%75,%76,%77,%78,%79}, [%116];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%80,%81,%82,%83,%84,%85,%86,%87,%88,%89,%90,%91,%92,%93,%94,%95}, [%117];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%96,%97,%98,%99,%100,%101,%102,%103,%104,%105,%106,%107,%108,%109,%110,%111}, [%118];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]),
+          "=r"(v[0][8]), "=r"(v[0][9]), "=r"(v[0][10]), "=r"(v[0][11]), "=r"(v[0][12]), "=r"(v[0][13]), "=r"(v[0][14]), "=r"(v[0][15]),
+          "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]), "=r"(v[1][7]),
+          "=r"(v[1][8]), "=r"(v[1][9]), "=r"(v[1][10]), "=r"(v[1][11]), "=r"(v[1][12]), "=r"(v[1][13]), "=r"(v[1][14]), "=r"(v[1][15]),
+          "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]), "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]),
+          "=r"(v[2][8]), "=r"(v[2][9]), "=r"(v[2][10]), "=r"(v[2][11]), "=r"(v[2][12]), "=r"(v[2][13]), "=r"(v[2][14]), "=r"(v[2][15]),
+          "=r"(v[3][0]), "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]), "=r"(v[3][6]), "=r"(v[3][7]),
+          "=r"(v[3][8]), "=r"(v[3][9]), "=r"(v[3][10]), "=r"(v[3][11]), "=r"(v[3][12]), "=r"(v[3][13]), "=r"(v[3][14]), "=r"(v[3][15]),
+          "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]), "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
+          "=r"(v[4][8]), "=r"(v[4][9]), "=r"(v[4][10]), "=r"(v[4][11]), "=r"(v[4][12]), "=r"(v[4][13]), "=r"(v[4][14]), "=r"(v[4][15]),
+          "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]), "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]),
+          "=r"(v[5][8]), "=r"(v[5][9]), "=r"(v[5][10]), "=r"(v[5][11]), "=r"(v[5][12]), "=r"(v[5][13]), "=r"(v[5][14]), "=r"(v[5][15]),
+          "=r"(v[6][0]), "=r"(v[6][1]), "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]), "=r"(v[6][7]),
+          "=r"(v[6][8]), "=r"(v[6][9]), "=r"(v[6][10]), "=r"(v[6][11]), "=r"(v[6][12]), "=r"(v[6][13]), "=r"(v[6][14]), "=r"(v[6][15])
+        : "r"(taddr + 0 * TN), "r"(taddr + 1 * TN), "r"(taddr + 2 * TN), "r"(taddr + 3 * TN),
+          "r"(taddr + 4 * TN), "r"(taddr + 5 * TN), "r"(taddr + 6 * TN)
+        : "memory");
 }
 
 template <int TN>
@@ -326,7 +346,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) k_modgemm_tc(const uint8_t* __r
             for (int cc = half; cc < TN / 16; cc += 2) {
                 uint32_t v[7][16];
                 tmem_ld16_x7<TN>(lane_base + cc * 16, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (cc + 2 >= TN / 16) {  // every column of this warp's share is in registers: release TMEM
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
@@ -552,7 +571,6 @@ __global__ void __launch_bounds__(kThreadsTc2, 1) k_modgemm_tc2(const uint8_t* _
             if (warp == 2 && lane == 0) tl_mark(tl, 5);
             uint32_t v[7][16];
             tmem_ld16_x7<TN>(lane_base, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             zero_and_release();
             if (row < M) {
                 uint32_t r[16];
@@ -689,6 +707,275 @@ __global__ void __launch_bounds__(256) k_tile_both(RowsArgs ra, ColsArgs ca, uin
     }
 }
 
+// ---------------------------------------------------------------------------
+// Narrow problems (C3: 1024 x 512 outputs, K = 1024): split-K CTA clusters on 128 x 64 tiles
+// (k_modgemm_tcs).
+// ---------------------------------------------------------------------------
+// Per SM the limb GEMM is bound by shared-memory bandwidth (~128 B/clk: operand fills plus the
+// MMAs' operand reads) and, in the epilogue, by TMEM reads (~64 B/clk: seven s32 accumulators per
+// output).  The persistent kernel's 128 x 32 tiles (the only tiling that fills the SMs at C3) issue
+// N = 128 MMAs that read 8 KB per 64 clocks, 208 B/clk with the fills: ~1.6x the tensor time.  Here
+// a cluster of two CTAs shares one 128 x 64 output tile and splits K: N = 256 MMAs (96 B/clk) plus
+// fills (48 B/clk), 2 x 64 = 128 CTAs at C3, at the price of each CTA draining all 448 accumulator
+// columns of its K half (twice the epilogue's TMEM reads).  Each CTA recombines its 64 columns mod
+// p, pushes the 32 its peer finalises into the peer's shared memory (st.shared::cluster) and, after
+// one cluster barrier, adds the peer's half to its own 32 columns.  Operands: A (W) always from a
+// limb image by TMA (prepared once for a public W, or by the re-layout launch); X either from the
+// re-layout launch's image by TMA, or — with a prepared W, one launch per call — split into limbs
+// by the 16 worker warps (8 consecutive k of one column per thread, warp-coalesced loads).  The
+// worker warps then drain TMEM, one 16-column chunk each (4 per TMEM lane quarter).
+constexpr int kStagesS = 4;
+constexpr int kWorkWarps = 16;    // producers, then one 16-column epilogue chunk each (4 per TMEM lane quarter)
+constexpr int kThreadsTcs = 32 * (1 + kWorkWarps);  // warp 0: MMA issuer
+struct TcsSmem {
+    static constexpr uint32_t A_LIMB = TM * TK;      // 8 KB
+    static constexpr uint32_t A_STAGE = 4 * A_LIMB;  // 32 KB
+    static constexpr uint32_t B_LIMB = 64 * TK;      // 4 KB
+    static constexpr uint32_t B_STAGE = 4 * B_LIMB;  // 16 KB
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    static constexpr uint32_t XPITCH = 36;           // exchange row pitch (u32): conflict-free v4 stores
+    static constexpr uint32_t XBUF = TM * XPITCH * 4;  // 18 KB
+    static constexpr uint32_t BYTES = kStagesS * STAGE + XBUF + 1024 + 256;
+};
+
+// 4 u32 words -> their 4 byte-planes: limb[i] = [w0.b_i, w1.b_i, w2.b_i, w3.b_i]
+__device__ __forceinline__ void split4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&limb)[4]) {
+    const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+    const uint32_t t2 = __byte_perm(w2, w3, 0x5140), t3 = __byte_perm(w2, w3, 0x7362);
+    limb[0] = __byte_perm(t0, t2, 0x5410);
+    limb[1] = __byte_perm(t0, t2, 0x7632);
+    limb[2] = __byte_perm(t1, t3, 0x5410);
+    limb[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+struct TcsArgs {
+    const uint8_t* a_image;  // A limb image (mt-major blocks of 4 x 128 x 64, KB per row block)
+    const uint8_t* b_image;  // B limb image of the re-layout kernel (nt-major blocks of 4 x 64 x 64), or null
+    ColsArgs b;              // X (K x N, b0 | b1 columns, row stride NB) when b_image is null
+    uint32_t M, N, KB, tiles_n;
+    TcOut out;
+};
+
+// One stage's B words in registers (worker thread pt in [0, 512)): 8 consecutive k of one column of
+// X.  Every load of a stage is issued before any of its words is used (the limb split happens in
+// tcs_store_b), and the next stage's loads are in flight while this one is stored.
+struct TcsLd {
+    uint32_t b[8];
+};
+
+__device__ __forceinline__ void tcs_load_b(const ColsArgs& ca, uint32_t nt, uint32_t kb, uint32_t pt, TcsLd& x) {
+    const uint32_t n = nt * 64 + (pt & 63), k0 = kb * TK + (pt >> 6) * 8;
+    const uint32_t* col = (n >= ca.NB ? ca.b1 + (n - ca.NB) : ca.b0 + n) + (uint64_t)k0 * ca.NB;
+    if (n < ca.N && k0 + 8 <= ca.K) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x.b[i] = __ldg(col + (uint64_t)i * ca.NB);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x.b[i] = (n < ca.N && k0 + i < ca.K) ? __ldg(col + (uint64_t)i * ca.NB) : 0u;
+    }
+}
+
+// split the loaded words into the stage's four B limb tiles (canonical K-major no-swizzle image)
+__device__ __forceinline__ void tcs_store_b(uint8_t* sb, uint32_t pt, const TcsLd& x) {
+    const uint32_t n = pt & 63, kk = (pt >> 6) * 8;
+    uint32_t l0[4], l1[4];
+    split4(x.b[0], x.b[1], x.b[2], x.b[3], l0);
+    split4(x.b[4], x.b[5], x.b[6], x.b[7], l1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<uint2*>(sb + j * TcsSmem::B_LIMB + core_off(n, kk)) = make_uint2(l0[j], l1[j]);
+}
+
+// Eight output columns c0 .. c0+7 of this thread's TMEM lane: the seven P_s (7 x 8 words, one
+// wait), recombined mod p.
+template <int TN>
+__device__ __forceinline__ void tc_chunk8(uint32_t taddr, uint32_t* r) {
+    uint32_t v[7][8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%56];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%57];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%58];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%59];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%60];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%61];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%62];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]), "=r"(v[0][6]),
+          "=r"(v[0][7]), "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]),
+          "=r"(v[1][6]), "=r"(v[1][7]), "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]), "=r"(v[2][4]),
+          "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]), "=r"(v[3][0]), "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]),
+          "=r"(v[3][4]), "=r"(v[3][5]), "=r"(v[3][6]), "=r"(v[3][7]), "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]),
+          "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]), "=r"(v[5][0]), "=r"(v[5][1]),
+          "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]), "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]), "=r"(v[6][0]),
+          "=r"(v[6][1]), "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]), "=r"(v[6][7])
+        : "r"(taddr), "r"(taddr + TN), "r"(taddr + 2 * TN), "r"(taddr + 3 * TN), "r"(taddr + 4 * TN),
+          "r"(taddr + 5 * TN), "r"(taddr + 6 * TN)
+        : "memory");
+    constexpr uint32_t kPow[7] = {1u, 256u, 65536u, 16777216u, 5u, 1280u, 327680u};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        unsigned long long acc = v[0][t];
+#pragma unroll
+        for (int q = 1; q < 7; ++q) acc += (unsigned long long)v[q][t] * kPow[q];
+        r[t] = fp_reduce64(acc);
+    }
+}
+
+template <bool kBImg>
+__global__ void __launch_bounds__(kThreadsTcs, 1) k_modgemm_tcs(const TcsArgs p, uint64_t* tl) {
+    using L = TcsSmem;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = (smem_u32(smem) + 1023u) & ~1023u;
+    uint8_t* sgen = smem + (sbase - smem_u32(smem));
+    uint32_t* xbuf = reinterpret_cast<uint32_t*>(sgen + kStagesS * L::STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sgen + kStagesS * L::STAGE + L::XBUF);
+    uint64_t* empty = full + kStagesS;
+    uint64_t* tfull = empty + kStagesS;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t ks, kr;  // K split (cluster size) and this CTA's K half
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ks));
+    kr = ks > 1 ? cluster_rank() : 0u;
+    const uint32_t tile = blockIdx.x / ks, mt = tile / p.tiles_n, nt = tile % p.tiles_n;
+    const uint32_t kper = (p.KB + ks - 1) / ks, kb0 = kr * kper, kb1 = min(p.KB, kb0 + kper);
+    const uint32_t nkb = kb1 > kb0 ? kb1 - kb0 : 0;  // the launcher splits only when both halves are non-empty
+    if (threadIdx.x == 0) {
+        tl_mark(tl, 0);
+        for (int s = 0; s < kStagesS; ++s) {
+            mbar_init(&full[s], kWorkWarps + 1);  // + the TMA thread's expect_tx arrival
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_fence_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    if (ks > 1) cluster_sync_all();  // the peer is running (its shared memory is addressable) and initialised
+    else __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) tl_mark(tl, 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs written by the previous kernel are visible
+    if (threadIdx.x == 0) tl_mark(tl, 2);
+
+    // worker warps 1-16: TMEM lane quarter = warp % 4, 16-column chunk = (warp - 1) / 4
+    const uint32_t quarter = warp & 3, cidx = (warp - 1) >> 2;
+    const uint32_t lrow = quarter * 32 + lane, row = mt * TM + lrow;
+    uint32_t r[16];  // this warp's chunk, mod p
+    if (warp == 0) {
+        if (lane == 0) {  // ---- MMA issuer ----
+            constexpr uint32_t id4 = idesc_i8<256>(), id3 = idesc_i8<192>(), id1 = idesc_i8<64>();
+            for (uint32_t g = 0; g < nkb; ++g) {
+                const uint32_t s = g % kStagesS;
+                mbar_wait(&full[s], (g / kStagesS) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (g == 0) tl_mark(tl, 3);
+                const uint32_t sa = sbase + s * L::STAGE, sb = sa + L::A_STAGE;
+#pragma unroll
+                for (int kq = 0; kq < TK / 32; ++kq) {
+                    const uint64_t bd = smem_desc(sb + kq * 2 * kLBO, kLBO, kSBO);
+                    uint64_t ad[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) ad[i] = smem_desc(sa + i * L::A_LIMB + kq * 2 * kLBO, kLBO, kSBO);
+                    if (g == 0 && kq == 0) {  // initialise P_0..P_6 (overlapping destination ranges)
+                        const uint64_t bd3 = smem_desc(sb + 3 * L::B_LIMB + kq * 2 * kLBO, kLBO, kSBO);
+                        mma_i8(tmem, ad[0], bd, id3, 0u);
+                        mma_i8(tmem + 3 * 64, ad[3], bd, id4, 0u);
+                        mma_i8(tmem + 3 * 64, ad[0], bd3, id1, 1u);
+                        mma_i8(tmem + 1 * 64, ad[1], bd, id4, 1u);
+                        mma_i8(tmem + 2 * 64, ad[2], bd, id4, 1u);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) mma_i8(tmem + i * 64, ad[i], bd, id4, 1u);
+                    }
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(tfull);
+            tl_mark(tl, 4);
+        }
+        __syncwarp();
+    } else {  // ---- warps 1-16: producers, then epilogue ----
+        const uint32_t pt = threadIdx.x - 32;
+        auto put = [&](const TcsLd& x, uint32_t g) {
+            const uint32_t s = g % kStagesS;
+            if (lane == 0 && g >= (uint32_t)kStagesS) mbar_wait(&empty[s], ((g / kStagesS) - 1) & 1);
+            __syncwarp();
+            if (pt == 0) {
+                mbar_expect_tx(&full[s], L::A_STAGE + (kBImg ? L::B_STAGE : 0u));
+                bulk_g2s(sbase + s * L::STAGE, p.a_image + ((uint64_t)mt * p.KB + kb0 + g) * L::A_STAGE, L::A_STAGE,
+                         &full[s]);
+                if (kBImg)
+                    bulk_g2s(sbase + s * L::STAGE + L::A_STAGE,
+                             p.b_image + ((uint64_t)nt * p.KB + kb0 + g) * L::B_STAGE, L::B_STAGE, &full[s]);
+            }
+            if (!kBImg) {
+                tcs_store_b(sgen + s * L::STAGE + L::A_STAGE, pt, x);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor-core reads
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        };
+        TcsLd x0, x1;
+        if (!kBImg && nkb > 0) tcs_load_b(p.b, nt, kb0, pt, x0);
+        for (uint32_t g = 0; g < nkb; g += 2) {
+            if (!kBImg && g + 1 < nkb) tcs_load_b(p.b, nt, kb0 + g + 1, pt, x1);
+            put(x0, g);
+            if (g + 1 >= nkb) break;
+            if (!kBImg && g + 2 < nkb) tcs_load_b(p.b, nt, kb0 + g + 2, pt, x0);
+            put(x1, g + 1);
+        }
+        if (warp == 1 && lane == 0) tl_mark(tl, 8);  // this warp's last stage handed over
+        // ---- epilogue: one 16-column chunk per warp, as two 8-column halves ----
+        mbar_wait(tfull, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (warp == 1 && lane == 0) tl_mark(tl, 5);
+        const uint32_t taddr = tmem + ((quarter * 32u) << 16) + cidx * 16;
+        tc_chunk8<64>(taddr, r);
+        tc_chunk8<64>(taddr + 8, r + 8);
+        if (ks == 1) {
+            if (row < p.M) tc_store16(p.out, p.N, row, nt * 64 + cidx * 16, r);
+        } else if ((cidx >> 1) != kr) {  // the peer finalises these columns: push them
+            const uint32_t dst = mapa_shared(smem_u32(xbuf + lrow * L::XPITCH + 16 * (cidx & 1)), 1 - kr);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) st_cluster_v4(dst + 16 * c, r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+            if (warp == 1 && lane == 0) tl_mark(tl, 9);
+        }
+        if (warp == 1 && lane == 0) tl_mark(tl, 10);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    if (ks > 1) {
+        __syncwarp();
+        cluster_sync_all();  // every pushed half is in its owner's shared memory
+        if (threadIdx.x == 32) tl_mark(tl, 11);
+        if (warp > 0 && (cidx >> 1) == kr) {
+            const uint4* src = reinterpret_cast<const uint4*>(xbuf + lrow * L::XPITCH + 16 * (cidx & 1));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 u = src[c];
+                r[4 * c] = fp_add(r[4 * c], u.x);
+                r[4 * c + 1] = fp_add(r[4 * c + 1], u.y);
+                r[4 * c + 2] = fp_add(r[4 * c + 2], u.z);
+                r[4 * c + 3] = fp_add(r[4 * c + 3], u.w);
+            }
+            if (row < p.M) tc_store16(p.out, p.N, row, nt * 64 + cidx * 16, r);
+        }
+    }
+    if (warp == 1 && lane == 0) tl_mark(tl, 6);
+    __syncthreads();
+    if (threadIdx.x == 0) tl_mark(tl, 7);
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // Diagnostic switches (attribution experiments, scripts/gemm_probe.py): bit 0 skips the TMA
 // loads, bit 1 the MMAs, bit 2 the GEMM kernel, bit 3 the re-layout kernels (results invalid
 // while any is set); bit 6 / bit 7 force the 32- / 64-column tile width (results valid).
@@ -779,6 +1066,70 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
     return cudaGetLastError();
 }
 
+// Narrow problems: k_modgemm_tcs on 128 x 64 tiles, K split over a 2-CTA cluster when both halves
+// get at least one stage and the doubled grid still fits on the SMs (diagnostic bit 11 keeps one CTA).
+// A prepared W image: one launch, X split into limbs by the worker warps.  Otherwise both operands
+// are re-laid out first (k_tile_both, PDL-chained) and every stage is two TMA bulk copies.
+cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t lda, uint32_t batch,
+                    const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx,
+                    const uint8_t* a_image, uint8_t* scratch, const TcOut& out, int sms) {
+    const uint32_t M = mode == 0 ? dout : 2 * dout, N = mode == 0 ? 2 * batch : batch;
+    const uint32_t KB = (din + TK - 1) / TK, tiles_n = (N + 63) / 64, tiles = tiles_n * ((M + TM - 1) / TM);
+    const uint32_t ks = (KB >= 2 && 2 * tiles <= (uint32_t)sms && !(g_tc_dbg & 2048)) ? 2 : 1;
+    TcsArgs p{};
+    p.a_image = a_image;
+    p.b = ColsArgs{x0, mode == 0 ? x1 : x0, batch, N, din, KB, mode == 0 ? bx : TcBx{}, nullptr};
+    p.M = M;
+    p.N = N;
+    p.KB = KB;
+    p.tiles_n = tiles_n;
+    p.out = out;
+    const bool pdl = !a_image || bx.e;  // a re-layout kernel runs first
+    if (pdl) {  // re-layout kernel: A (unless prepared) and B limb images
+        const uint32_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Np = (N + 63) / 64 * 64;
+        uint8_t* At = a_image ? nullptr : scratch;
+        uint8_t* Bt = a_image ? scratch : scratch + (uint64_t)4 * Mp * KB * TK;
+        const uint64_t chunks = (uint64_t)Mp * KB * (TK / 16);
+        const uint32_t row_blocks = a_image ? 0u : (uint32_t)std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 16);
+        const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, At, lda};
+        ColsArgs ca = p.b;
+        ca.out = Bt;
+        k_tile_both<64><<<row_blocks + KB * (Np / 32), 256, 0, s>>>(ra, ca, row_blocks, KB);
+        ++g_kernel_launches;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        p.a_image = a_image ? a_image : At;
+        p.b_image = Bt;
+    }
+    static bool attr = false;
+    if (!attr) {
+        for (auto* f : {k_modgemm_tcs<false>, k_modgemm_tcs<true>}) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, TcsSmem::BYTES);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(tiles * ks);
+    cfg.blockDim = dim3(kThreadsTcs);
+    cfg.dynamicSmemBytes = TcsSmem::BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = ks;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the re-layout kernel
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = ks > 1 ? attrs : attrs + 1;
+    cfg.numAttrs = (ks > 1 ? 1 : 0) + (pdl ? 1 : 0);
+    cudaError_t e = p.b_image ? cudaLaunchKernelEx(&cfg, k_modgemm_tcs<true>, p, g_tc_tl)
+                              : cudaLaunchKernelEx(&cfg, k_modgemm_tcs<false>, p, g_tc_tl);
+    ++g_kernel_launches;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 void modgemm_tc_debug(uint32_t flags) { g_tc_dbg = flags; }
@@ -818,12 +1169,20 @@ cudaError_t launch_modgemm_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t 
         const uint32_t* a1 = w1 ? w1 + k0 : nullptr;
         const uint32_t* b0 = x0 + xo;
         const uint32_t* b1 = x1 ? x1 + xo : nullptr;
-        // TN = 64 unless that tiling leaves SMs idle (diagnostic bit 6 forces TN = 32, bit 7 TN = 64);
-        // bit 9 runs narrow problems as CTA pairs on 256 x 32 tiles (k_modgemm_tc2: correct, but measured
-        // slower at C3, 22.6 vs 16.5 us — both variants are bound by the L2->SMEM operand stream)
+        // Problems whose 128 x 64 tiling fills the SMs: the persistent k_modgemm_tc (TN = 64) after one
+        // re-layout launch.  Narrower ones (C3): the split-K cluster kernel k_modgemm_tcs, operands split
+        // in its producer warps (bit 12 forces it for any shape, bit 11 keeps it on one CTA per tile).
+        // Diagnostic comparisons: bit 6 the TN = 32 persistent kernel, bit 7 TN = 64, bit 9 the CTA-pair
+        // kernel on 256 x 32 tiles (k_modgemm_tc2; correct, measured slower at C3).
         const uint64_t tiles64 = (M + TM - 1) / TM * ((N + 63) / 64);
         const bool narrow = (g_tc_dbg & (64 | 512)) || (!(g_tc_dbg & 128) && tiles64 < (uint64_t)sms);
         const bool pair = narrow && (g_tc_dbg & 512);
+        const bool split = (g_tc_dbg & 4096) || (narrow && !(g_tc_dbg & (64 | 128 | 512)));
+        if (split && !(g_tc_dbg & 15)) {
+            cudaError_t e = run_tcs(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, ai, scratch, out, sms);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
         cudaError_t e = narrow ? run_tc<32>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms, pair)
                                : run_tc<64>(s, mode, dout, kc, din, batch, a0, a1, b0, b1, bx, scratch, ai, out, sms);
         if (e != cudaSuccess) return e;

@@ -23,6 +23,9 @@ W, xs = rnd(din * dout), DeviceShare(rnd(din * batch), rnd(din * batch))
 ys = DeviceShare.empty(dout * batch)
 args = (ctx.h, din, dout, batch, 1, W.data_ptr(), None, C.byref(dshare(xs)), None, C.byref(dshare(ys)))
 BASE = (64 if "--tn32" in sys.argv else 0) | (128 if "--tn64" in sys.argv else 0)
+for a in sys.argv:
+    if a.startswith("--flags="):  # any diagnostic flag set (e.g. 8192: operands re-laid out first)
+        BASE |= int(a.split("=", 1)[1])
 lib().spdz_diag_gemm_tc_flags(BASE)  # 64/128: force the 32/64-column tile width
 
 
@@ -108,33 +111,101 @@ if "--prepared" in sys.argv:  # W laid out once (spdz_linear_weights): per call 
     print(f"prepared W: graphed {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call", flush=True)
 
 if "--timeline" in sys.argv:
-    # per-CTA %globaltimer stamps of the GEMM kernel (relative to the earliest CTA entry), for
-    # the full call and for the GEMM alone with the diagnostic switches
+    # per-CTA %globaltimer stamps of the GEMM kernel (relative to the earliest CTA entry), for the
+    # given diagnostic flag sets (--tl-flags=a,b,...; default: the full call and the old switches)
     check(lib().spdz_set_gemm_path(2))
-    buf = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
-    names = ["entry", "setup", "pdl_wait", "first_full", "mma_done", "epi_start", "epi_done", "exit"]
-    for flags, name in ((0, "full call (re-layout + gemm, PDL)"), (8, "gemm kernel only"),
-                        (11, "gemm, no loads no MMAs"), (9, "gemm, no loads"), (10, "gemm, no MMAs")):
+    buf = torch.zeros(160 * 16, dtype=torch.int64, device="cuda")
+    names = ["entry", "setup", "pdl_wait", "first_full", "mma_done", "epi_start", "epi_done", "exit",
+             "prod_done", "pushed", "own_done", "cluster_sync"]
+    sel = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--tl-flags=")]
+    fl = [(int(f), f"flags {f}") for f in sel[0].split(",")] if sel else \
+        [(0, "full call"), (8, "gemm kernel only"), (11, "gemm, no loads no MMAs"), (9, "gemm, no loads"),
+         (10, "gemm, no MMAs")]
+    if "--tl-prepared" in sys.argv:  # the prepared-W call (one launch) instead of W per call
+        tl_w = ctx.prepare_weights(W, dout, din)
+        tl_args = (ctx.h, tl_w.h, batch, C.byref(dshare(xs)), C.byref(dshare(ys)))
+        tl_fn = lib().spdz_linear_secret_public_prepared
+    else:
+        tl_args, tl_fn = args, lib().spdz_linear_secret_public
+    for flags, name in fl:
         lib().spdz_diag_gemm_tc_flags(BASE | flags)
         for _ in range(3):
-            check(lib().spdz_linear_secret_public(*args))
+            check(tl_fn(*tl_args))
         torch.cuda.synchronize()
         buf.zero_()
         lib().spdz_diag_gemm_tc_timeline(buf.data_ptr())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        check(lib().spdz_linear_secret_public(*args))
+        check(tl_fn(*tl_args))
         e1.record()
         torch.cuda.synchronize()
         lib().spdz_diag_gemm_tc_timeline(None)
-        t = buf.view(148, 8).cpu().numpy()
+        t = buf.view(160, 16).cpu().numpy()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        rel = (t - t0) / 1000.0
         print(f"timeline [{name}] {len(t)} CTAs, event {e0.elapsed_time(e1) * 1000:.1f} us:", flush=True)
         for k, nm in enumerate(names):
-            col = rel[:, k]
-            print(f"   {nm:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")
+            col = t[:, k]
+            col = col[col > 0]
+            if col.size == 0:
+                continue
+            rel = (col - t0) / 1000.0
+            print(f"   {nm:12s} min {rel.min():7.2f}  med {np.median(rel):7.2f}  max {rel.max():7.2f} us")
+    lib().spdz_diag_gemm_tc_flags(BASE)
+
+if "--variants" in sys.argv:
+    # the narrow-problem kernels side by side: split-K cluster kernel (default), the same on one CTA
+    # per tile (2048), the persistent TN = 32 kernel (64), CTA pairs (512); per call through the
+    # public API, eager (host launch included) and CUDA-graph replayed (device time), W per call
+    # (re-layout launch + GEMM) and prepared once (spdz_linear_weights)
+    check(lib().spdz_set_gemm_path(2))
+    wts = ctx.prepare_weights(W, dout, din)
+    pargs = (ctx.h, wts.h, batch, C.byref(dshare(xs)), C.byref(dshare(ys)))
+
+    def prep_call():
+        check(lib().spdz_linear_secret_public_prepared(*pargs))
+
+    def plain_call():
+        check(lib().spdz_linear_secret_public(*args))
+
+    def time_eager(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1000
+
+    def time_graph(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ctx.use_torch_stream()
+            for _ in range(reps):
+                fn()
+        ctx.use_torch_stream()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1000
+
+    for flags, name in ((0, "split-K cluster (k_modgemm_tcs, ks=2)"), (2048, "k_modgemm_tcs, ks=1"),
+                        (64, "persistent TN=32 + re-layout"), (512, "CTA pair 256x32 + re-layout")):
+        lib().spdz_diag_gemm_tc_flags(flags)
+        r = [time_eager(plain_call), time_graph(plain_call), time_eager(prep_call), time_graph(prep_call)]
+        print(f"variant [{name}]: W per call: eager {r[0]:.1f} us, graphed {r[1]:.1f} us; "
+              f"prepared W: eager {r[2]:.1f} us, graphed {r[3]:.1f} us", flush=True)
+    wts.close()
     lib().spdz_diag_gemm_tc_flags(BASE)
 
 if "--int8-peak" in sys.argv:

@@ -452,7 +452,7 @@ def _np_modmatmul(A, B):
     return ((hi * 65536 + lo) % P).astype(np.uint32)
 
 
-@pytest.mark.parametrize("tiles", [0, 64, 128, 512])
+@pytest.mark.parametrize("tiles", [0, 64, 128, 512, 2048, 4096, 6144])
 @pytest.mark.parametrize("din,dout,batch,fill", [(512, 2048, 300, "rand"), (8192, 256, 64, "max"),
                                                  (300, 130, 70, "rand"), (64, 1200, 520, "rand"),
                                                  (20000, 192, 40, "max"), (8200, 130, 33, "rand"),
@@ -461,8 +461,10 @@ def test_linear_secret_public_full_matrix(gpu, din, dout, batch, fill, tiles):
     """Every output of the tcgen05 GEMM (both planes, both modes) against an exact
     numpy mod-p matmul: persistent tiles (more tiles than SMs), edge tiles, and
     all-(p-1) operands at K = 8192 (the s32 limb-accumulator bound); tile width
-    chosen automatically (0), forced to 32 (64) or to 64 columns (128), or the CTA-pair
-    kernel on 256 x 32 tiles (512; tcgen05.mma.cta_group::2), incl. the C3 shape."""
+    chosen automatically (0: narrow shapes take the split-K cluster kernel k_modgemm_tcs), forced
+    to 32 (64) or to 64 columns (128) on the persistent kernel, the CTA-pair kernel on 256 x 32
+    tiles (512; tcgen05.mma.cta_group::2), k_modgemm_tcs on one CTA per tile (2048), or
+    k_modgemm_tcs for every shape, split-K (4096) or not (6144), incl. the C3 shape."""
     import ctypes as C
     from paper_2512_11112_b200 import DeviceShare
     from paper_2512_11112_b200._lib import check, lib
@@ -554,10 +556,22 @@ def test_batched_secret_secret_linear(gpu, din, dout, batch):
             np.testing.assert_array_equal(zs[p][1].reshape(dout, batch)[:, j], zm)
 
 
+@pytest.mark.parametrize("flags", [0, 2048, 4096])
 @pytest.mark.parametrize("din,dout,batch", [(1024, 1024, 256), (300, 130, 70), (512, 2048, 300)])
-def test_prepared_weights_equal_per_call(gpu, din, dout, batch):
-    """spdz_linear_secret_public_prepared (W laid out once) == the per-call path, twice in a row
-    (the prepared image is reused), both planes."""
+def test_prepared_weights_equal_per_call(gpu, din, dout, batch, flags):
+    """spdz_linear_secret_public_prepared (W laid out once) == exact W X, twice in a row
+    (the prepared image is reused), both planes; kernel chosen automatically (0), the split-K
+    cluster kernel on one CTA per tile (2048) or forced for every shape (4096)."""
+    from paper_2512_11112_b200 import DeviceShare
+    from paper_2512_11112_b200._lib import lib
+    lib().spdz_diag_gemm_tc_flags(flags)
+    try:
+        _prepared_case(din, dout, batch)
+    finally:
+        lib().spdz_diag_gemm_tc_flags(0)
+
+
+def _prepared_case(din, dout, batch):
     from paper_2512_11112_b200 import DeviceShare
     W = O.rand_field_vec(din * dout, 21)
     Xv, Xm = O.rand_field_vec(din * batch, 22), O.rand_field_vec(din * batch, 23)
