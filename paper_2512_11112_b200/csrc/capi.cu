@@ -11,6 +11,8 @@
 
 #include "field.cuh"
 #include "hostcopy.hpp"
+
+#include <cstdlib>
 #include "internal.hpp"
 
 using namespace spdzb200;
@@ -834,18 +836,30 @@ struct Staging {
         off += (words * 4 + 15) / 16 * 16;
         return p;
     }
-    // large pageable host vectors (the reference Backend's std::vector operands) go through the
-    // pinned staging ring at multi-threaded memcpy speed (hostcopy.cu)
+    // Pageable host vectors (the reference Backend's std::vector operands) are copied by the
+    // driver directly: through the pinned staging ring (hostcopy.cu) the 2^20-lane add measured
+    // 4.0 ms against 2.1 ms (fresh output vectors fault their pages in the copy-out; the ring's
+    // hand-offs cost more than they save at 4-16 MB per call), mask+combine 6.1 against 6.5 ms
+    // (scripts/hostapi_probe.py, profiles/r02i_hostapi.log).  The run-input path keeps the ring
+    // (run.cu: 13.4 -> 5.2 ms per pageable e2e step).
+    // SPDZ_HOST_STAGING (experiments): bit 0 stages pageable H2D copies, bit 1 pageable D2H copies
+    static int staging_mode() {
+        static const int m = [] {
+            const char* e = std::getenv("SPDZ_HOST_STAGING");
+            return e ? std::atoi(e) : 0;
+        }();
+        return m;
+    }
     uint32_t* up(const uint32_t* h, uint64_t words) {
         uint32_t* d = take(words);
-        if (words * 4 >= (1u << 20) && is_pageable(h))
+        if ((staging_mode() & 1) && words * 4 >= (1u << 20) && is_pageable(h))
             cuda_check(staged_h2d(ctx->device, d, h, words * 4, ctx->stream), "staged H2D");
         else if (words)
             cuda_check(cudaMemcpyAsync(d, h, words * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D");
         return d;
     }
     void down(uint32_t* h, const uint32_t* d, uint64_t words) {
-        if (words * 4 >= (1u << 20) && is_pageable(h))
+        if ((staging_mode() & 2) && words * 4 >= (1u << 20) && is_pageable(h))
             cuda_check(staged_d2h(ctx->device, h, d, words * 4, ctx->stream), "staged D2H");
         else if (words)
             cuda_check(cudaMemcpyAsync(h, d, words * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");

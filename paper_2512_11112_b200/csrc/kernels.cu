@@ -844,11 +844,12 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
 // party 0's de, alpha_i de, bias (spdz.cpp:117-123, linear.cpp:59) — then re-zeroes the
 // row's scratch.  Sums stay below 2^64: a segment adds < 2^40 and a row has at most din/4
 // segments.
-__device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (&acc)[5], uint32_t r, uint32_t seg,
-                                          uint32_t din4, unsigned long long* acc_rows, unsigned int* done_rows,
-                                          uint32_t lane) {
+__device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (&lo)[5], unsigned long long (&hi)[5],
+                                          uint32_t r, uint32_t seg, uint32_t din4, unsigned long long* acc_rows,
+                                          unsigned int* done_rows, uint32_t lane) {
+    unsigned long long acc[5];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) acc[q] = warp_sum(fold1(acc[q]));
+    for (int q = 0; q < 5; ++q) acc[q] = warp_sum(fold1((fold1(hi[q]) << 16) + fold1(lo[q])));
     if (lane == 0) {
         unsigned long long* ar = acc_rows + (uint64_t)r * 5;
 #pragma unroll
@@ -880,7 +881,7 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
         }
     }
 #pragma unroll
-    for (int q = 0; q < 5; ++q) acc[q] = 0ull;
+    for (int q = 0; q < 5; ++q) lo[q] = hi[q] = 0ull;
 }
 
 struct MC2Ld {
@@ -901,24 +902,36 @@ __device__ __forceinline__ void mc2_load(const MC2Args& a, uint64_t gg, uint32_t
         L.bv[p] = B4[p][0][c4];
         L.bm[p] = B4[p][1][c4];
     }
-}
+}// The nine products per cell (d e; d B.v, d B.m, A.v e, A.m e of each party) with the shared
+// operands d and e split into 16-bit halves: every product is then < 2^48 and goes straight into a
+// u64 accumulator as one IMAD.WIDE.U32 multiply-add (lo: low halves, hi: high halves, weight
+// 2^16), instead of a 64-bit product, its fold and a 64-bit add.  A lane adds at most 2 din/32
+// products per accumulator between flushes: below 2^64 for din < 2^20 (launcher).
 __device__ __forceinline__ void mc2_compute(const MC2Args& a, uint64_t gg, const MC2Ld& L,
-                                            unsigned long long (&acc)[5]) {
+                                            unsigned long long (&lo)[5], unsigned long long (&hi)[5]) {
+    const uint4 e4 = L.e4, bv[2] = {L.bv[0], L.bv[1]}, bm[2] = {L.bm[0], L.bm[1]};
     const uint32_t d[4] = {fp_add(L.d0.x, fp_reduce32(L.d1.x)), fp_add(L.d0.y, fp_reduce32(L.d1.y)),
                            fp_add(L.d0.z, fp_reduce32(L.d1.z)), fp_add(L.d0.w, fp_reduce32(L.d1.w))};
-    const uint32_t e[4] = {L.e4.x, L.e4.y, L.e4.z, L.e4.w};
+    const uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
-    for (int l = 0; l < 4; ++l) acc[4] += fold1(mul_wide(d[l], e[l]));
+    for (int l = 0; l < 4; ++l) {
+        const uint32_t dl = d[l] & 0xFFFFu, dh = d[l] >> 16, el = e[l] & 0xFFFFu, eh = e[l] >> 16;
+        lo[4] += (unsigned long long)dl * e[l];
+        hi[4] += (unsigned long long)dh * e[l];
+        const uint32_t BV[2] = {l == 0 ? bv[0].x : l == 1 ? bv[0].y : l == 2 ? bv[0].z : bv[0].w,
+                                l == 0 ? bv[1].x : l == 1 ? bv[1].y : l == 2 ? bv[1].z : bv[1].w};
+        const uint32_t BM[2] = {l == 0 ? bm[0].x : l == 1 ? bm[0].y : l == 2 ? bm[0].z : bm[0].w,
+                                l == 0 ? bm[1].x : l == 1 ? bm[1].y : l == 2 ? bm[1].z : bm[1].w};
+        const uint32_t AV[2] = {l == 0 ? L.av[0].x : l == 1 ? L.av[0].y : l == 2 ? L.av[0].z : L.av[0].w,
+                                l == 0 ? L.av[1].x : l == 1 ? L.av[1].y : l == 2 ? L.av[1].z : L.av[1].w};
+        const uint32_t AM[2] = {l == 0 ? L.am[0].x : l == 1 ? L.am[0].y : l == 2 ? L.am[0].z : L.am[0].w,
+                                l == 0 ? L.am[1].x : l == 1 ? L.am[1].y : l == 2 ? L.am[1].z : L.am[1].w};
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        const uint32_t AV[4] = {L.av[p].x, L.av[p].y, L.av[p].z, L.av[p].w};
-        const uint32_t AM[4] = {L.am[p].x, L.am[p].y, L.am[p].z, L.am[p].w};
-        const uint32_t BV[4] = {L.bv[p].x, L.bv[p].y, L.bv[p].z, L.bv[p].w};
-        const uint32_t BM[4] = {L.bm[p].x, L.bm[p].y, L.bm[p].z, L.bm[p].w};
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            acc[2 * p] += fold1(mul_wide(d[l], BV[l])) + fold1(mul_wide(AV[l], e[l]));
-            acc[2 * p + 1] += fold1(mul_wide(d[l], BM[l])) + fold1(mul_wide(AM[l], e[l]));
+        for (int p = 0; p < 2; ++p) {
+            lo[2 * p] += (unsigned long long)dl * BV[p] + (unsigned long long)el * AV[p];
+            hi[2 * p] += (unsigned long long)dh * BV[p] + (unsigned long long)eh * AV[p];
+            lo[2 * p + 1] += (unsigned long long)dl * BM[p] + (unsigned long long)el * AM[p];
+            hi[2 * p + 1] += (unsigned long long)dh * BM[p] + (unsigned long long)eh * AM[p];
         }
     }
     st4(a.opened, gg, d);
@@ -954,23 +967,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_matrix_combine2_flat(MC2Args
         const uint4* const B4[2][2] = {
             {reinterpret_cast<const uint4*>(a.B[0][0] + toff), reinterpret_cast<const uint4*>(a.B[0][1] + toff)},
             {reinterpret_cast<const uint4*>(a.B[1][0] + toff), reinterpret_cast<const uint4*>(a.B[1][1] + toff)}};
-        unsigned long long acc[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
+        unsigned long long lo[5] = {0ull, 0ull, 0ull, 0ull, 0ull}, hi[5] = {0ull, 0ull, 0ull, 0ull, 0ull};  // v0 m0 v1 m1 de
         uint64_t gg = u0 + lane;
         if (UNROLL == 2) {
             for (; gg + 32 < rend; gg += 64) {
                 MC2Ld L0, L1;
                 mc2_load(a, gg, (uint32_t)(gg - rbase), E4, B4, L0);
                 mc2_load(a, gg + 32, (uint32_t)(gg + 32 - rbase), E4, B4, L1);
-                mc2_compute(a, gg, L0, acc);
-                mc2_compute(a, gg + 32, L1, acc);
+                mc2_compute(a, gg, L0, lo, hi);
+                mc2_compute(a, gg + 32, L1, lo, hi);
             }
         }
         for (; gg < rend; gg += 32) {
             MC2Ld L0;
             mc2_load(a, gg, (uint32_t)(gg - rbase), E4, B4, L0);
-            mc2_compute(a, gg, L0, acc);
+            mc2_compute(a, gg, L0, lo, hi);
         }
-        mc2_flush(a, acc, r, (uint32_t)(rend - u0), din4, acc_rows, done_rows, lane);
+        mc2_flush(a, lo, hi, r, (uint32_t)(rend - u0), din4, acc_rows, done_rows, lane);
         u0 = rend;
     }
 }
@@ -1455,7 +1468,7 @@ cudaError_t launch_matrix_combine2(cudaStream_t s, const MC2Args& a, int sms, un
         const char* e = std::getenv("SPDZ_MC2_UNROLL");
         return e && std::atoi(e) == 1 ? 1 : 2;
     }();
-    if (v4 && acc_rows && done_rows && !flat_off) {
+    if (v4 && acc_rows && done_rows && !flat_off && a.din < (1u << 20)) {  // (the flat kernel's u64 bound)
         auto kern = unroll == 2 ? k_matrix_combine2_flat<2, 2> : k_matrix_combine2_flat<1, 3>;
         static int per_sm[2] = {0, 0};
         int& ps = per_sm[unroll - 1];
