@@ -119,10 +119,17 @@ struct SigConsts {
     uint32_t sh30 = 1u << 2, sh27 = 1u << 5, sh31 = 1u << 1, five = 5u;
 };
 
-// z ^= z >> s (s < 32); hm = 2^(32-s): h >> s = umulhi(h, hm) on the fma pipe
+// Which of the three xorshifts take their high-word shift on the ALU pipe (SHF) instead of the
+// fma-heavy pipe (umulhi by 2^(32-s)): bit 0 = >> 30, bit 1 = >> 27, bit 2 = >> 31.  The split
+// that balances the two pipes is measured (scripts/sigma_ceiling.py).
+#ifndef SPDZ_SIGMA_ALU_SHIFTS
+#define SPDZ_SIGMA_ALU_SHIFTS 0
+#endif
+// z ^= z >> s (s < 32); hm = 2^(32-s): h >> s = umulhi(h, hm) on the fma pipe, or a shift
+template <bool kAlu>
 __device__ __forceinline__ void xorshift_r(uint32_t& l, uint32_t& h, int s, uint32_t hm) {
     l ^= __funnelshift_r(l, h, s);
-    h ^= __umulhi(h, hm);
+    h ^= kAlu ? (h >> s) : __umulhi(h, hm);
 }
 __device__ __forceinline__ void mul_const(uint32_t& l, uint32_t& h, uint32_t cl, uint32_t ch) {  // z *= c (mod 2^64)
     const uint32_t t1 = h * cl, t2 = l * ch, hw = __umulhi(l, cl);
@@ -138,12 +145,16 @@ __device__ __forceinline__ uint32_t rep_mod_p(uint32_t l, uint32_t h, uint32_t f
 }
 // r' < 2^32 with r' == mix64(h:l) (mod p)  (hash.hpp:21-26, reduce: field.hpp:14)
 __device__ __forceinline__ uint32_t mac_coeff_rep(uint32_t l, uint32_t h, const SigConsts& kc) {
-    xorshift_r(l, h, 30, kc.sh30);
+    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 1) != 0>(l, h, 30, kc.sh30);
     mul_const(l, h, 0x1ce4e5b9u, 0xbf58476du);
-    xorshift_r(l, h, 27, kc.sh27);
+    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 2) != 0>(l, h, 27, kc.sh27);
     mul_const(l, h, 0x133111ebu, 0x94d049bbu);
-    xorshift_r(l, h, 31, kc.sh31);
+    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 4) != 0>(l, h, 31, kc.sh31);
+#ifdef SPDZ_SIGMA_ALU_FIVE
+    return rep_mod_p(l, h, 5u);
+#else
     return rep_mod_p(l, h, kc.five);
+#endif
 }
 #endif  // __CUDACC__
 
