@@ -902,6 +902,10 @@ __global__ void __launch_bounds__(kThreadsTcs, 1) k_modgemm_tcs(const TcsArgs p,
             }
             mma_commit(tfull);
             tl_mark(tl, 4);
+            // every MMA of this CTA is issued: the next kernel in the stream (programmatic dependent
+            // launch) may start its prologue on SMs this grid frees; it reads nothing before its
+            // griddepcontrol.wait, which waits for this whole grid and its memory
+            asm volatile("griddepcontrol.launch_dependents;");
         }
         __syncwarp();
     } else {  // ---- warps 1-16: producers, then epilogue ----
@@ -1084,8 +1088,8 @@ cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint3
     p.KB = KB;
     p.tiles_n = tiles_n;
     p.out = out;
-    const bool pdl = !a_image || bx.e;  // a re-layout kernel runs first
-    if (pdl) {  // re-layout kernel: A (unless prepared) and B limb images
+    const bool relayout = !a_image || bx.e;
+    if (relayout) {  // re-layout kernel: A (unless prepared) and B limb images
         const uint32_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Np = (N + 63) / 64 * 64;
         uint8_t* At = a_image ? nullptr : scratch;
         uint8_t* Bt = a_image ? scratch : scratch + (uint64_t)4 * Mp * KB * TK;
@@ -1119,10 +1123,10 @@ cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint3
     attrs[0].val.clusterDim.x = ks;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
-    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the re-layout kernel
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the previous kernel
     attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = ks > 1 ? attrs : attrs + 1;
-    cfg.numAttrs = (ks > 1 ? 1 : 0) + (pdl ? 1 : 0);
+    cfg.numAttrs = (ks > 1 ? 1 : 0) + 1;  // programmatic dependent launch after whatever precedes it
     cudaError_t e = p.b_image ? cudaLaunchKernelEx(&cfg, k_modgemm_tcs<true>, p, g_tc_tl)
                               : cudaLaunchKernelEx(&cfg, k_modgemm_tcs<false>, p, g_tc_tl);
     ++g_kernel_launches;
