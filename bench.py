@@ -470,10 +470,39 @@ def per_party_block(args, dev, inputs, spot, colocated_step_ms, colocated_kstat)
                     a[f] += st[f]
     r.close()
     step = float(np.mean(ms))
+    # the same per-party kernels as the N-GPU ranks run them: lane chunks on their own streams, one
+    # stream per party, each chunk's MAC check (its own coin after its openings) overlapping the next
+    # chunks' mask/combine (ChunkedRun(mac="per_chunk"), bench's N > 1 path)
+    from paper_2512_11112_b200 import ChunkedRun
+    chunks = 4
+    cr = ChunkedRun(lambda L: chain_graph(args.kind, L), 2, args.lanes, chunks=chunks, devices=[dev, dev],
+                    mac="per_chunk", stream_per_party=True, separate_party_kernels=True, dealer_seed=1)
+    coins = iter(range(0x5000, 0x5000 + 64 * (args.warmup + args.steps)))
+    cms = []
+    for k in range(args.warmup + args.steps):
+        cr.deal(9000 + k)
+        cr.bind_inputs(inputs)
+        cr.share_inputs()
+        torch.cuda.synchronize()
+        sig, span, reps = cr.online(coin_fn=lambda: next(coins))
+        for sg in sig:  # every chunk's check verifies on its own
+            if sum(sg) % P != 0:
+                raise RuntimeError("per-chunk MAC check did not verify")
+        spot(np.concatenate([rp.outputs for rp in reps]), f"chunked per-party step {k}")
+        if k >= args.warmup:
+            cms.append(span)
+    cr.close()
+    cstep = float(np.mean(cms))
     gbs = lambda d: {n: round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1) for n, v in d.items() if v["launches"]}
     return {"placement": "2 parties on 1 GPU, one stream, each party's own kernels (no co-located fusion)",
             "ms_per_step": step, "mult_per_s": N_MUL[args.kind] * args.lanes / (step / 1e3),
-            "vs_colocated_step": step / colocated_step_ms, "kernels_gbs": gbs(kst),
+            "vs_colocated_step": step / colocated_step_ms,
+            "chunked": {"placement": f"{chunks} lane chunks on their own streams, one stream per party, each "
+                                     "party's own kernels, a MAC check per chunk (its coin after its "
+                                     "openings) overlapping later chunks' kernels (the N-GPU ranks' mode)",
+                        "ms_per_step": cstep, "mult_per_s": N_MUL[args.kind] * args.lanes / (cstep / 1e3),
+                        "vs_colocated_step": cstep / colocated_step_ms},
+            "kernels_gbs": gbs(kst),
             "kernel_ms_per_step": {n: round(v["ms"] / args.steps, 4) for n, v in kst.items() if v["launches"]},
             "colocated_kernels_gbs": gbs(colocated_kstat),
             "contracts_bytes": {"mask": "24 per lane", "combine": "48 + 8 (peer d, e) per lane (OpCombine<1>)",

@@ -498,11 +498,12 @@ class ChunkedRun:
 
     def __init__(self, graph_fn, n_parties: int, lanes: int, chunks: int = 4, shard: tuple | None = None,
                  dealer_seed: int = 1, devices=None, single_party: int | None = None, coin: int | None = None,
-                 profile_kernels: bool = False, node_streams: int = 1, mac: str = "joint"):
+                 profile_kernels: bool = False, node_streams: int = 1, mac: str = "joint", **run_kw):
         """mac="joint": one coin after every chunk's openings, per-party partials summed over the
         chunks; mac="per_chunk": chunk c's coin is agreed as soon as its openings are final and its
         sigma kernels launched while later chunks still run (each chunk a full SPDZ check of its
-        own openings), so the issue-bound sigma overlaps the next chunk's HBM-bound kernels."""
+        own openings), so the issue-bound sigma overlaps the next chunk's HBM-bound kernels.
+        run_kw: further LocalRun options for every chunk (stream_per_party, separate_party_kernels)."""
         import torch
         assert mac in ("joint", "per_chunk")
         self.mac = mac
@@ -520,7 +521,8 @@ class ChunkedRun:
         self.n, self.party, self.coin = n_parties, single_party, coin
         self.runs = [LocalRun(graph_fn(L), n_parties, dealer_seed=dealer_seed, devices=devices,
                               shard=(off0 + lo, total), external_mac_verify=True, single_party=single_party,
-                              profile_kernels=profile_kernels, node_streams=node_streams) for lo, L in self.ranges]
+                              profile_kernels=profile_kernels, node_streams=node_streams, **run_kw)
+                     for lo, L in self.ranges]
 
     def close(self):
         for r in self.runs:
