@@ -735,8 +735,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-linear", action="store_true", help="skip the linear-layer block")
     ap.add_argument("--no-per-party", action="store_true", help="skip the per-party-kernel block")
-    ap.add_argument("--exchange-chunks", type=int, default=2,
-                    help="N>1: lane chunks per GPU whose opening exchanges overlap each other's kernels")
+    ap.add_argument("--exchange-chunks", type=int, default=4,
+                    help="N>1: lane chunks per GPU whose opening exchanges and per-chunk MAC checks overlap "
+                         "each other's kernels (4: the per-party block's measured mode)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="lane chunks of the host-streamed e2e run")
     ap.add_argument("--e2e-weights", default="", help="relative lane-chunk sizes of the host-streamed e2e run "
                     "(comma-separated; overrides --e2e-chunks)")
