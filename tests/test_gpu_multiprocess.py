@@ -112,6 +112,35 @@ def test_chunked_run_local_equals_unsharded(gpu):
     cr.close()
 
 
+def test_chunked_per_party_per_chunk_mac(gpu):
+    """bench.py's per-party mode (the N-GPU ranks' mode on one GPU): 4 lane chunks, one stream per
+    party, each party's own kernels, a MAC check per chunk with its own coin.  Outputs equal the
+    unsharded run's; every chunk's sigma set verifies on its own and equals, party by party, the
+    same chunking run with the co-located kernels and the same coins (those kernels are pinned to
+    the oracle elsewhere)."""
+    from paper_2512_11112_b200 import ChunkedRun, LocalRun, chain_graph
+    n = 1 << 18
+    x, y = O.rand_field_vec(n, 3), O.rand_field_vec(n, 4)
+    full = LocalRun(chain_graph("heavy", n), 2, coin=7)
+    full.bind_inputs({"x": x, "y": y})
+    full.share_inputs()
+    want = full.online().outputs
+    full.close()
+    sigs = {}
+    for per_party in (True, False):
+        kw = dict(stream_per_party=True, separate_party_kernels=True) if per_party else {}
+        cr = ChunkedRun(lambda L: chain_graph("heavy", L), 2, n, chunks=4, mac="per_chunk", **kw)
+        cr.bind_inputs({"x": x, "y": y})
+        cr.share_inputs()
+        coins = iter([0x11, 0x22, 0x33, 0x44])
+        sig, ms, reps = cr.online(coin_fn=lambda: next(coins))
+        np.testing.assert_array_equal(np.concatenate([rep.outputs for rep in reps]), want)
+        assert len(sig) == 4 and all(sum(sg) % P == 0 for sg in sig) and ms > 0
+        sigs[per_party] = sig
+        cr.close()
+    assert sigs[True] == sigs[False]
+
+
 def _sharded_party(rank, world, port, kind, n, coin, q, device_of_party):
     """bench.py's N-GPU mapping (parallel.party_layout): party p on ranks [p*G, (p+1)*G),
     rank k of each party holds lane shard k of the n-lane circuit and opens to its peer."""
