@@ -720,9 +720,9 @@ __global__ void __launch_bounds__(256) k_tile_both(RowsArgs ra, ColsArgs ca, uin
 // columns of its K half (twice the epilogue's TMEM reads).  Each CTA recombines its 64 columns mod
 // p, pushes the 32 its peer finalises into the peer's shared memory (st.shared::cluster) and, after
 // one cluster barrier, adds the peer's half to its own 32 columns.  Operands: A (W) always from a
-// limb image by TMA (prepared once for a public W, or by the re-layout launch); X either from the
-// re-layout launch's image by TMA, or — with a prepared W, one launch per call — split into limbs
-// by the 16 worker warps (8 consecutive k of one column per thread, warp-coalesced loads).  The
+// limb image by TMA (prepared once for a public W, or by a re-layout launch of W alone); X split into
+// limbs by the 16 worker warps (8 consecutive k of one column per thread, warp-coalesced loads), or,
+// when B carries the + coef E transform, from the re-layout launch's image by TMA.  The
 // worker warps then drain TMEM, one 16-column chunk each (4 per TMEM lane quarter).
 constexpr int kStagesS = 4;
 constexpr int kWorkWarps = 16;    // producers, then one 16-column epilogue chunk each (4 per TMEM lane quarter)
@@ -1072,8 +1072,10 @@ cudaError_t run_tc(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32
 
 // Narrow problems: k_modgemm_tcs on 128 x 64 tiles, K split over a 2-CTA cluster when both halves
 // get at least one stage and the doubled grid still fits on the SMs (diagnostic bit 11 keeps one CTA).
-// A prepared W image: one launch, X split into limbs by the worker warps.  Otherwise both operands
-// are re-laid out first (k_tile_both, PDL-chained) and every stage is two TMA bulk copies.
+// A prepared W image: one launch, X split into limbs by the worker warps.  W per call: one re-layout
+// launch of W (k_tile_both, PDL-chained), X still split in the kernel (eager 19.3 -> 17.5 us per C3 call
+// against re-laying out both, profiles/r02n); with the E transform both operands are re-laid out and
+// every stage is two TMA bulk copies.
 cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint32_t lda, uint32_t batch,
                     const uint32_t* w0, const uint32_t* w1, const uint32_t* x0, const uint32_t* x1, const TcBx& bx,
                     const uint8_t* a_image, uint8_t* scratch, const TcOut& out, int sms) {
@@ -1088,8 +1090,11 @@ cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint3
     p.KB = KB;
     p.tiles_n = tiles_n;
     p.out = out;
-    const bool relayout = !a_image || bx.e;
-    if (relayout) {  // re-layout kernel: A (unless prepared) and B limb images
+    // Re-layout launch: the A (W) limb image unless prepared, and the B image only when B carries
+    // the + coef E transform (batched secret x secret); otherwise X is split in the kernel's worker
+    // warps, as with a prepared W (diagnostic bit 13: the B image by re-layout as well).
+    const bool b_relayout = bx.e || (!a_image && (g_tc_dbg & 8192));
+    if (!a_image || b_relayout) {
         const uint32_t Mp = (M + 2 * TM - 1) / (2 * TM) * (2 * TM), Np = (N + 63) / 64 * 64;
         uint8_t* At = a_image ? nullptr : scratch;
         uint8_t* Bt = a_image ? scratch : scratch + (uint64_t)4 * Mp * KB * TK;
@@ -1098,12 +1103,13 @@ cudaError_t run_tcs(cudaStream_t s, int mode, uint32_t dout, uint32_t din, uint3
         const RowsArgs ra{w0, mode == 0 ? w0 : w1, mode == 0 ? M : dout, M, din, Mp, KB, At, lda};
         ColsArgs ca = p.b;
         ca.out = Bt;
-        k_tile_both<64><<<row_blocks + KB * (Np / 32), 256, 0, s>>>(ra, ca, row_blocks, KB);
+        const uint32_t col_blocks = b_relayout ? KB * (Np / 32) : 0u;
+        k_tile_both<64><<<row_blocks + col_blocks, 256, 0, s>>>(ra, ca, row_blocks, KB);
         ++g_kernel_launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         p.a_image = a_image ? a_image : At;
-        p.b_image = Bt;
+        p.b_image = b_relayout ? Bt : nullptr;
     }
     static bool attr = false;
     if (!attr) {

@@ -199,7 +199,8 @@ if "--variants" in sys.argv:
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps * 1000
 
-    for flags, name in ((0, "split-K cluster (k_modgemm_tcs, ks=2)"), (2048, "k_modgemm_tcs, ks=1"),
+    for flags, name in ((0, "split-K cluster (k_modgemm_tcs, ks=2)"), (8192, "k_modgemm_tcs, both images re-laid out"),
+                        (2048, "k_modgemm_tcs, ks=1"),
                         (64, "persistent TN=32 + re-layout"), (512, "CTA pair 256x32 + re-layout")):
         lib().spdz_diag_gemm_tc_flags(flags)
         r = [time_eager(plain_call), time_graph(plain_call), time_eager(prep_call), time_graph(prep_call)]
