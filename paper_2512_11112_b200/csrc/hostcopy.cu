@@ -115,11 +115,22 @@ bool is_pageable(const void* p) {
 
 namespace {
 cudaError_t ring_ready(Ring& ring) {
-    if (ring.slot[0]) return cudaSuccess;
+    if (ring.slot[kSlots - 1] && ring.ev[kSlots - 1]) return cudaSuccess;
     for (int s = 0; s < kSlots; ++s) {
-        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&ring.slot[s]), kSlot);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ring.ev[s], cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
+        cudaError_t e = cudaSuccess;
+        if (!ring.slot[s]) {
+            void* p = nullptr;
+            e = cudaMallocHost(&p, kSlot);
+            ring.slot[s] = e == cudaSuccess ? static_cast<char*>(p) : nullptr;
+        }
+        if (e == cudaSuccess && !ring.ev[s]) e = cudaEventCreateWithFlags(&ring.ev[s], cudaEventDisableTiming);
+        if (e != cudaSuccess) {  // a later call retries the missing slots (a null slot is never used)
+            if (ring.slot[s] && !ring.ev[s]) {
+                cudaFreeHost(ring.slot[s]);
+                ring.slot[s] = nullptr;
+            }
+            return e;
+        }
     }
     return cudaSuccess;
 }
