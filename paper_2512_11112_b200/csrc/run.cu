@@ -314,7 +314,7 @@ void share_inputs(spdz_run* r) {
 // a lane-parallel circuit (no linear layers or reductions, whose launchers size scratch
 // buffers and grids at call time), no fault injection, no per-kernel timing.
 bool graphable(spdz_run* r) {
-    if (!r->opts.use_graph || r->cfg || r->any_remote || r->opts.profile_kernels || !r->faults.empty()) return false;
+    if (!r->opts.use_graph || r->cfg || r->any_remote || !r->faults.empty()) return false;
     for (int p = 0; p < r->n; ++p)
         if (!r->parties[p].local || S(r, p) != S(r, 0)) return false;
     return true;
@@ -600,15 +600,18 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
                 const uint64_t l0 = g_kernel_launches;
                 cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "begin capture");
                 cudaGraph_t g = nullptr;
+                r->kt_capturing = true;
                 try {
                     Exec ex{r};
                     ex.run_nodes();
                     ex.open_root();
                 } catch (...) {
+                    r->kt_capturing = false;
                     cudaStreamEndCapture(s, &g);
                     if (g) cudaGraphDestroy(g);
                     throw;
                 }
+                r->kt_capturing = false;
                 cuda_check(cudaStreamEndCapture(s, &g), "end capture");
                 cudaError_t e = cudaGraphInstantiate(&r->online_graph, g, 0);
                 cudaGraphDestroy(g);
@@ -617,10 +620,14 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
                 r->graph_exchanged = r->exchanged;
                 r->graph_maclog.clear();
                 for (auto& P : r->parties) r->graph_maclog.push_back(P.maclog);
+                r->graph_kt_recs = r->kt.recs;
+                r->graph_kt_used = r->kt.used;
             } else {
                 g_kernel_launches += r->graph_launches;
                 r->exchanged = r->graph_exchanged;
                 for (int p = 0; p < r->n; ++p) r->parties[p].maclog = r->graph_maclog[p];
+                r->kt.recs = r->graph_kt_recs;  // the replay re-records the captured event pairs
+                r->kt.used = r->graph_kt_used;
             }
             lk(cudaGraphLaunch(r->online_graph, s), "cudaGraphLaunch");
         } else {

@@ -645,14 +645,17 @@ int ktimer_begin(spdz_run* r, int p) {
     if (!r->opts.profile_kernels) return -1;
     cudaEvent_t a = r->kt.take(r->devices[p]);
     dev(r, p);
-    lk(cudaEventRecord(a, S(r, p)), "record");
+    // inside a graph capture the event becomes an event-record node, re-recorded by every replay
+    lk(r->kt_capturing ? cudaEventRecordWithFlags(a, S(r, p), cudaEventRecordExternal) : cudaEventRecord(a, S(r, p)),
+       "record");
     r->kt.recs.push_back({-1, r->devices[p], a, nullptr, 0});
     return (int)r->kt.recs.size() - 1;
 }
 void ktimer_end(spdz_run* r, int p, int idx, int cls, uint64_t bytes) {
     if (idx < 0) return;
     cudaEvent_t b = r->kt.take(r->devices[p]);
-    lk(cudaEventRecord(b, S(r, p)), "record");
+    lk(r->kt_capturing ? cudaEventRecordWithFlags(b, S(r, p), cudaEventRecordExternal) : cudaEventRecord(b, S(r, p)),
+       "record");
     auto& rec = r->kt.recs[idx];
     rec.cls = cls;
     rec.b = b;

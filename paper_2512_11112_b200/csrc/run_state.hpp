@@ -229,6 +229,10 @@ struct spdz_run {
     cudaGraphExec_t online_graph = nullptr;
     std::vector<std::vector<spdz_mac_segment_t>> graph_maclog;
     uint64_t graph_exchanged = 0, graph_launches = 0;
+    // profile_kernels inside the graph: the captured kernel-class event pairs (event-record nodes)
+    bool kt_capturing = false;
+    std::vector<KTimer::Rec> graph_kt_recs;
+    size_t graph_kt_used = 0;
     // share_inputs: constants uploaded once, reduced public inputs kept alive for async copies
     bool consts_uploaded = false;
     std::map<uint32_t, std::vector<uint32_t>> pub_reduced;

@@ -13,7 +13,8 @@ P = 4294967291
 rng = np.random.default_rng(1)
 x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
 y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
-for name, kw in (("profile_kernels", {"profile_kernels": True}), ("eager", {}), ("graph", {"use_graph": True})):
+for name, kw in (("profile_kernels", {"profile_kernels": True}), ("eager", {}), ("graph", {"use_graph": True}),
+                 ("graph+profile", {"use_graph": True, "profile_kernels": True})):
     run = LocalRun(chain_graph("heavy", lanes), 2, devices=[0, 0], dealer_seed=1, **kw)
     ms = []
     for k in range(13):
@@ -24,4 +25,6 @@ for name, kw in (("profile_kernels", {"profile_kernels": True}), ("eager", {}), 
         if k >= 3:
             ms.append(rep.online_device_ms)
     run.close()
-    print(f"{name:16s} median {np.median(ms):.4f} ms  min {np.min(ms):.4f}  max {np.max(ms):.4f}", flush=True)
+    ks = {k: round(v["ms"], 4) for k, v in (rep.kstat or {}).items() if v["launches"]}
+    print(f"{name:16s} median {np.median(ms):.4f} ms  min {np.min(ms):.4f}  max {np.max(ms):.4f}  kernels {ks}",
+          flush=True)

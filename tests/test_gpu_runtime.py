@@ -361,6 +361,36 @@ def test_graph_replayed_online_phase(gpu, kind):
         r.close()
 
 
+def test_graph_replay_with_kernel_timing(gpu):
+    """profile_kernels inside the replayed graph (event-record nodes captured with the kernels):
+    outputs and sigmas equal the eager profiled run, every kernel class is timed on every
+    replay with the same launches and algorithmic bytes as the eager run, and the times are real."""
+    from paper_2512_11112_b200 import LocalRun, chain_graph
+    n, coin = 1 << 16, 0xC0FFEE
+    x, y = O.rand_field_vec(n, 5), O.rand_field_vec(n, 6)
+    runs = [LocalRun(chain_graph("heavy", n), 2, coin=coin, profile_kernels=True, use_graph=g) for g in (False, True)]
+    want = O.sim_chain("heavy", 2, x, y, 1, coin)
+    for seed in (1, 2, 3):
+        reps = []
+        for r in runs:
+            r.deal(seed)
+            r.bind_inputs({"x": x, "y": y})
+            r.share_inputs()
+            reps.append(r.online())
+        np.testing.assert_array_equal(reps[0].outputs, reps[1].outputs)
+        assert reps[0].sigmas == reps[1].sigmas
+        if seed == 1:
+            np.testing.assert_array_equal(reps[1].outputs, want["outputs"])
+            assert list(reps[1].sigmas) == list(want["sigmas"])
+        for name, st in reps[0].kstat.items():
+            g = reps[1].kstat[name]
+            assert (g["launches"], g["bytes"]) == (st["launches"], st["bytes"]), name
+            if st["launches"]:
+                assert 0.0 < g["ms"] < 1000.0, (name, g)
+    for r in runs:
+        r.close()
+
+
 @pytest.mark.parametrize("n_parties", [2, 3])
 def test_inputs_above_p_are_reduced(gpu, n_parties):
     """preproc.cpp:149: bound inputs are reduced mod p before sharing (2 parties: inline in
