@@ -336,6 +336,17 @@ struct OpOpen {  // net.cpp:170-215
     }
 };
 
+// Root open of two co-located parties: both parties' opened words (identical: z0 + z1) in one
+// pass, 8 bytes read and 8 written per lane instead of two OpOpen<1> launches reading 16.
+struct OpOpen2 {
+    __device__ static constexpr bool is_peer(int k) { return false; }
+    __device__ void prepare() {}
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        o[0] = fp_add(in[0], fp_reduce32(in[1]));
+        o[1] = fp_add(in[1], fp_reduce32(in[0]));
+    }
+};
+
 template <int NP>
 cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, const uint32_t* const* pd,
                        const uint32_t* const* pe, const uint32_t* const tri[6], int party, uint32_t alpha,
@@ -1219,8 +1230,12 @@ __device__ __forceinline__ void linmask_group(const LinMask2Args& m, uint64_t ud
     } else {
         const uint64_t e = g - ud, c4 = e % din4;
         const uint4 x0 = ld4(m.x[0], c4), b0 = ld4(m.b[0], e), x1 = ld4(m.x[1], c4), b1 = ld4(m.b[1], e);
-        reinterpret_cast<uint4*>(m.pay[0] + m.cells)[e] = fp_sub4(x0, b0);
-        reinterpret_cast<uint4*>(m.pay[1] + m.cells)[e] = fp_sub4(x1, b1);
+        const uint4 e0 = fp_sub4(x0, b0), e1 = fp_sub4(x1, b1);
+        reinterpret_cast<uint4*>(m.pay[0] + m.cells)[e] = e0;
+        reinterpret_cast<uint4*>(m.pay[1] + m.cells)[e] = e1;
+        if (m.opened_e)  // both payloads are local: E opened here (net.cpp:170-215 sum) instead of a launch
+            reinterpret_cast<uint4*>(m.opened_e)[e] = make_uint4(fp_add(e0.x, e1.x), fp_add(e0.y, e1.y),
+                                                                 fp_add(e0.z, e1.z), fp_add(e0.w, e1.w));
     }
 }
 __global__ void __launch_bounds__(kThreads) k_linear_mask2(LinMask2Args m) {
@@ -1347,6 +1362,12 @@ cudaError_t launch_open_sum(cudaStream_t s, const uint32_t* own, const uint32_t*
 #undef CASE
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_open_sum2(cudaStream_t s, const uint32_t* z0, const uint32_t* z1, uint32_t* out0, uint32_t* out1,
+                             uint64_t n, int sms) {
+    IO<2, 2> io{{z0, z1}, {out0, out1}};
+    return run_map(s, io, n, OpOpen2{}, sms);
 }
 
 cudaError_t launch_reduce_add(cudaStream_t s, const uint32_t* xv, const uint32_t* xm, uint64_t n,
@@ -1580,6 +1601,7 @@ cudaError_t launch_linear_mask2(cudaStream_t s, const LinMask2Args& m, int sms) 
     bool ok = m.din % 4 == 0 && m.cells % 4 == 0;
     for (int p = 0; p < 2; ++p)
         ok = ok && aligned16(m.w[p]) && aligned16(m.a[p]) && aligned16(m.x[p]) && aligned16(m.b[p]) && aligned16(m.pay[p]);
+    ok = ok && aligned16(m.opened_e);
     if (!ok) return cudaErrorInvalidValue;  // caller falls back to the per-plane kernels
     const uint64_t total = m.cells / 4 + (uint64_t)m.din * m.ntiles / 4;
     if (total == 0) return cudaSuccess;

@@ -132,7 +132,11 @@ struct LinMask2Args {
     uint32_t* pay[2];
     uint64_t cells;
     uint32_t din, ntiles;
+    uint32_t* opened_e;  // optional: the opened E (E_0 + E_1, every tile) written in the same pass
 };
+// both co-located parties' opened words z0 + z1 (the root open) in one pass
+cudaError_t launch_open_sum2(cudaStream_t s, const uint32_t* z0, const uint32_t* z1, uint32_t* out0, uint32_t* out1,
+                             uint64_t n, int sms);
 cudaError_t launch_linear_mask2(cudaStream_t s, const LinMask2Args& m, int sms);
 // E_t = x - B_t for all tiles (B: n_tiles x din)
 cudaError_t launch_tile_e(cudaStream_t s, const uint32_t* xv, const uint32_t* bv, uint32_t din, uint32_t n_tiles,

@@ -780,7 +780,8 @@ struct Exec {
                 auto& P1 = r->parties[1];
                 const Val &w1 = P1.ns[n.operands[1]].out, &x1 = P1.ns[n.operands[0]].out;
                 const LinMask2Args m{{w.v, w1.v}, {st.mA[0], P1.ns[id].mA[0]}, {x.v, x1.v},
-                                     {st.mB[0], P1.ns[id].mB[0]}, {st.payload, P1.ns[id].payload}, cells, din, ntiles};
+                                     {st.mB[0], P1.ns[id].mB[0]}, {st.payload, P1.ns[id].payload}, cells, din, ntiles,
+                                     st.opened + cells};
                 const cudaError_t e = launch_linear_mask2(c->stream, m, c->sms);
                 if (e == cudaSuccess) {
                     e_done = fuse2_masked = true;
@@ -796,7 +797,8 @@ struct Exec {
             }
             if (!e_done)
                 lk(launch_tile_e(c->stream, x.v, st.mB[0], din, ntiles, st.payload + cells, c->sms), "mask E");
-            tend(p, tk, SPDZ_KSTAT_MASK, (fuse2 ? (p == 0 ? 24 * cells : 0) : 12 * cells) + 12 * etot);
+            tend(p, tk, SPDZ_KSTAT_MASK,
+                 (fuse2 ? (p == 0 ? 24 * cells : 0) : 12 * cells) + 12 * etot + (fuse2_masked && p == 0 ? 4 * etot : 0));
             sent[p] = publish(p, slot_of(id, 0));
             if (r->net) net_send_tiles(p, batch0, st.payload, din, lt);
         }
@@ -805,8 +807,10 @@ struct Exec {
             auto &s0 = P0.ns[id], &s1 = P1.ns[id];
             dev(r, 0);
             const int tk = tbegin(0);
-            const uint32_t* peE[1] = {s1.payload + cells};
-            lk(launch_open_sum(S(r, 0), s0.payload + cells, peE, 1, s0.opened + cells, etot, SMS(r, 0)), "open E");
+            if (!fuse2_masked) {  // (the two-party mask kernel opened E in its own pass)
+                const uint32_t* peE[1] = {s1.payload + cells};
+                lk(launch_open_sum(S(r, 0), s0.payload + cells, peE, 1, s0.opened + cells, etot, SMS(r, 0)), "open E");
+            }
             MC2Args a{};
             a.din = din;
             a.rows = dout;
@@ -1152,8 +1156,24 @@ struct Exec {
             }
             return;
         }
-        std::vector<cudaEvent_t> ready(r->n);
         const uint64_t batch = make_batch(r->root, 1, 1);
+        bool pair = colocated2(r);
+        for (auto& f : r->faults) pair = pair && f.node != r->root;
+        if (pair) {  // both local parties' openings (identical words) in one pass
+            auto &P0 = r->parties[0], &P1 = r->parties[1];
+            dev(r, 0);
+            const int tk = tbegin(0);
+            lk(launch_open_sum2(S(r, 0), P0.ns[r->root].out.v, P1.ns[r->root].out.v, P0.outputs, P1.outputs, L,
+                                SMS(r, 0)),
+               "open root (both parties)");
+            tend(0, tk, SPDZ_KSTAT_OPEN, 16ull * L);
+            r->exchanged += 2 * L * 4;
+            for (int p = 0; p < 2; ++p)
+                r->parties[p].maclog.push_back({r->parties[p].outputs, r->parties[p].ns[r->root].out.m, nullptr, L, 0,
+                                                batch, r->shard_off, r->shard_total ? r->shard_total : L});
+            return;
+        }
+        std::vector<cudaEvent_t> ready(r->n);
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             dev(r, p);
