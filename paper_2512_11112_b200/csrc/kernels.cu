@@ -281,6 +281,31 @@ struct OpCombine2 {
     }
 };
 
+// OpCombine2 followed, in the same pass, by the next multiply's mask (OpMask2) when that multiply
+// consumes this one's product: the fresh z.v of each party is masked from registers instead of
+// being re-read by a separate mask launch (runtime.cpp:209-217 for the next node).  ZPOS: which of
+// the next multiply's operands is this product (0 = left x, 1 = right y, 2 = both).  Inputs: the 16
+// of OpCombine2, then per party [other operand .v (ZPOS < 2)], a'.v, b'.v.  Outputs: the 6 of
+// OpCombine2, then d'0 e'0 d'1 e'1.
+template <int ZPOS>
+struct OpCombine2M : OpCombine2 {
+    static constexpr int kPer = ZPOS == 2 ? 2 : 3;  // extra inputs per party
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        OpCombine2::operator()(in, o);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const uint32_t* q = in + 16 + kPer * p;
+            const uint32_t z = o[2 * p];
+            const uint32_t x = ZPOS == 1 ? q[0] : z, y = ZPOS == 0 ? q[0] : z;
+            const uint32_t* ab = q + (ZPOS == 2 ? 0 : 1);
+            o[6 + 2 * p] = fp_sub(x, ab[0]);
+            o[7 + 2 * p] = fp_sub(y, ab[1]);
+        }
+    }
+};
+// (one 4-lane group per iteration: two in flight, as OpCombine2 does, measured 12% slower with the
+// 22 operand streams; profiles/r02u)
+
 // Input sharing of one private input for both parties of a 2-party run on one GPU
 // (preproc.cpp:205-243 with spdz::add_public, spdz.cpp:35-45): x = reduce(raw input),
 // diff = x - r (opened by party 0), party 0: (mask.v + diff, mask.m + alpha_0 diff),
@@ -1344,6 +1369,48 @@ cudaError_t launch_beaver_combine2(cudaStream_t s, const uint32_t* const de[4], 
     io.out[4] = open_d;
     io.out[5] = open_e;
     return run_map(s, io, n, OpCombine2{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]}, sms);
+}
+
+template <int ZPOS>
+static cudaError_t combine2m(cudaStream_t s, const IO<16, 6>& base, const uint32_t* const nx[6],
+                            uint32_t* const nde[4], const OpCombine2& op, uint64_t n, int sms) {
+    constexpr int K = OpCombine2M<ZPOS>::kPer;
+    IO<16 + 2 * K, 10> io;
+    for (int k = 0; k < 16; ++k) io.in[k] = base.in[k];
+    for (int p = 0; p < 2; ++p) {
+        int k = 16 + K * p;
+        if (ZPOS != 2) io.in[k++] = nx[3 * p];  // the next multiply's other operand
+        io.in[k++] = nx[3 * p + 1];             // a'.v
+        io.in[k] = nx[3 * p + 2];               // b'.v
+    }
+    for (int k = 0; k < 6; ++k) io.out[k] = base.out[k];
+    for (int k = 0; k < 4; ++k) io.out[6 + k] = nde[k];
+    OpCombine2M<ZPOS> f;
+    static_cast<OpCombine2&>(f) = op;
+    return run_map(s, io, n, f, sms);
+}
+
+cudaError_t launch_beaver_combine2_mask(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],
+                                        const uint32_t* const tri1[6], const uint32_t alpha[2],
+                                        const uint32_t* const alpha_dev[2], uint32_t* const z[4], uint32_t* open_d,
+                                        uint32_t* open_e, int zpos, const uint32_t* const next[6],
+                                        uint32_t* const next_de[4], uint64_t n, int sms) {
+    IO<16, 6> io;
+    for (int k = 0; k < 4; ++k) io.in[k] = de[k];
+    for (int k = 0; k < 6; ++k) {
+        io.in[4 + k] = tri0[k];
+        io.in[10 + k] = tri1[k];
+    }
+    for (int k = 0; k < 4; ++k) io.out[k] = z[k];
+    io.out[4] = open_d;
+    io.out[5] = open_e;
+    const OpCombine2 op{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]};
+    switch (zpos) {
+        case 0: return combine2m<0>(s, io, next, next_de, op, n, sms);
+        case 1: return combine2m<1>(s, io, next, next_de, op, n, sms);
+        case 2: return combine2m<2>(s, io, next, next_de, op, n, sms);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uint32_t* r_clear,

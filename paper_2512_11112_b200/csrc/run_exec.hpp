@@ -468,12 +468,45 @@ struct Exec {
     // Both parties of a 2-party run on one stream: both masks, then one fused open+combine
     // (payloads read once, opened values logged once).  (Running it in L2-sized lane blocks so
     // the payloads are re-read from L2 measured slower: the per-launch overhead dominated.)
+    // The multiply that runs right after `id` when its mask can be fused into id's combine: the next
+    // live node that launches work is a co-located Beaver multiply of the same lanes (no broadcast)
+    // with this product as an operand, straight-line issue on one stream.  Returns -1 otherwise.
+    int fusable_next_mul(uint32_t id) {
+        static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;  // (A/B experiments)
+        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return -1;
+        const uint64_t L = r->node(id).lanes;
+        for (uint32_t k = id + 1; k < r->nodes.size(); ++k) {
+            if (!r->live[k]) continue;
+            const auto& n = r->nodes[k];
+            if (n.kind == SPDZ_NODE_INPUT || n.kind == SPDZ_NODE_CONST || n.kind == SPDZ_NODE_NOP ||
+                n.kind == SPDZ_NODE_LABEL)
+                continue;
+            if (n.kind == SPDZ_NODE_LOAD && !r->parties[r->ref_party()].ns[k].dyn_load) continue;  // a view
+            if (n.kind != SPDZ_NODE_MUL || n.lanes != L) return -1;
+            for (auto& f : r->faults)
+                if (f.node == k) return -1;
+            for (int p = 0; p < 2; ++p) {
+                const auto &st = r->parties[p].ns[k], &own = r->parties[p].ns[id];
+                const auto& P = r->parties[p];
+                if (st.xa.is_public || st.xb.is_public || P.ns[n.operands[0]].out.lanes != L ||
+                    P.ns[n.operands[1]].out.lanes != L)  // (a broadcast operand is filled by its own node)
+                    return -1;
+                if (st.xa.v != own.out.v && st.xb.v != own.out.v) return -1;
+            }
+            return (int)k;
+        }
+        return -1;
+    }
+
     void beaver_pair(uint32_t id, uint64_t off) {
         const auto& n = r->node(id);
         const uint64_t L = n.lanes;
         auto &P0 = r->parties[0], &P1 = r->parties[1];
         auto &s0 = P0.ns[id], &s1 = P1.ns[id];
         dev(r, 0);
+        if (r->premasked.size() != r->nodes.size()) r->premasked.assign(r->nodes.size(), 0);
+        const bool masked = r->premasked[id];
+        r->premasked[id] = 0;
         for (int p = 0; p < 2; ++p) {
             auto& P = r->parties[p];
             auto& st = P.ns[id];
@@ -483,7 +516,7 @@ struct Exec {
         }
         const uint32_t alpha[2] = {P0.ctx->alpha, P1.ctx->alpha};
         const uint32_t* alpha_dev[2] = {P0.ctx->d_alpha, P1.ctx->d_alpha};
-        {  // both parties' d = x - a, e = y - b in one pass (48 bytes per lane)
+        if (!masked) {  // both parties' d = x - a, e = y - b in one pass (48 bytes per lane)
             const int tk = tbegin(0);
             const uint32_t* xyab[8] = {s0.xa.v, s0.xb.v, P0.pool[0] + off, P0.pool[2] + off,
                                        s1.xa.v, s1.xb.v, P1.pool[0] + off, P1.pool[2] + off};
@@ -499,10 +532,28 @@ struct Exec {
         }
         uint32_t* z[4] = {s0.out.v, s0.out.m, s1.out.v, s1.out.m};
         const int tk = tbegin(0);
-        lk(launch_beaver_combine2(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, L, SMS(r, 0)),
-           "k_combine2");
-        // [d|e] of both parties 16 + two parties' triple planes 48 + two z 16 + one opened log 8
-        tend(0, tk, SPDZ_KSTAT_COMBINE, 88 * L);
+        const int id2 = fusable_next_mul(id);
+        if (id2 >= 0) {  // the next multiply's mask from the fresh products, in the same pass
+            const uint64_t off2 = provisioned(r->scalar, (uint32_t)id2, 0).base;
+            auto &n0 = P0.ns[id2], &n1 = P1.ns[id2];
+            const bool zx = n0.xa.v == s0.out.v, zy = n0.xb.v == s0.out.v;
+            const int zpos = zx && zy ? 2 : (zx ? 0 : 1);
+            const uint32_t* next[6] = {zx ? n0.xb.v : n0.xa.v, P0.pool[0] + off2, P0.pool[2] + off2,
+                                       zx ? n1.xb.v : n1.xa.v, P1.pool[0] + off2, P1.pool[2] + off2};
+            uint32_t* const nde[4] = {n0.payload, n0.payload + L, n1.payload, n1.payload + L};
+            lk(launch_beaver_combine2_mask(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, zpos,
+                                           next, nde, L, SMS(r, 0)),
+               "k_combine2 + next mask");
+            r->premasked[id2] = 1;
+            // + per party the next operand (unless both are this product), a'.v, b'.v read and d', e' written
+            tend(0, tk, SPDZ_KSTAT_COMBINE, (88 + (zpos == 2 ? 32 : 40)) * L);
+        } else {
+            lk(launch_beaver_combine2(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, L,
+                                      SMS(r, 0)),
+               "k_combine2");
+            // [d|e] of both parties 16 + two parties' triple planes 48 + two z 16 + one opened log 8
+            tend(0, tk, SPDZ_KSTAT_COMBINE, 88 * L);
+        }
         r->exchanged += 2 * (2 * L * 4);
     }
 
