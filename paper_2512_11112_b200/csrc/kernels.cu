@@ -287,19 +287,27 @@ struct OpCombine2 {
 // the next multiply's operands is this product (0 = left x, 1 = right y, 2 = both).  Inputs: the 16
 // of OpCombine2, then per party [other operand .v (ZPOS < 2)], a'.v, b'.v.  Outputs: the 6 of
 // OpCombine2, then d'0 e'0 d'1 e'1.
+// ZPOS 3: this product is the circuit's root — its opening (both parties' words, z0 + z1,
+// net.cpp:170-215) is written instead (no extra inputs; outputs: the 6 of OpCombine2, then both
+// parties' opened outputs).
 template <int ZPOS>
 struct OpCombine2M : OpCombine2 {
-    static constexpr int kPer = ZPOS == 2 ? 2 : 3;  // extra inputs per party
+    static constexpr int kPer = ZPOS == 3 ? 0 : (ZPOS == 2 ? 2 : 3);  // extra inputs per party
     __device__ void operator()(const uint32_t* in, uint32_t* o) const {
         OpCombine2::operator()(in, o);
+        if constexpr (ZPOS == 3) {
+            o[6] = fp_add(o[0], fp_reduce32(o[2]));
+            o[7] = fp_add(o[2], fp_reduce32(o[0]));
+        } else {
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const uint32_t* q = in + 16 + kPer * p;
-            const uint32_t z = o[2 * p];
-            const uint32_t x = ZPOS == 1 ? q[0] : z, y = ZPOS == 0 ? q[0] : z;
-            const uint32_t* ab = q + (ZPOS == 2 ? 0 : 1);
-            o[6 + 2 * p] = fp_sub(x, ab[0]);
-            o[7 + 2 * p] = fp_sub(y, ab[1]);
+            for (int p = 0; p < 2; ++p) {
+                const uint32_t* q = in + 16 + kPer * p;
+                const uint32_t z = o[2 * p];
+                const uint32_t x = ZPOS == 1 ? q[0] : z, y = ZPOS == 0 ? q[0] : z;
+                const uint32_t* ab = q + (ZPOS == 2 ? 0 : 1);
+                o[6 + 2 * p] = fp_sub(x, ab[0]);
+                o[7 + 2 * p] = fp_sub(y, ab[1]);
+            }
         }
     }
 };
@@ -1375,16 +1383,18 @@ template <int ZPOS>
 static cudaError_t combine2m(cudaStream_t s, const IO<16, 6>& base, const uint32_t* const nx[6],
                             uint32_t* const nde[4], const OpCombine2& op, uint64_t n, int sms) {
     constexpr int K = OpCombine2M<ZPOS>::kPer;
-    IO<16 + 2 * K, 10> io;
+    IO<16 + 2 * K, ZPOS == 3 ? 8 : 10> io;
     for (int k = 0; k < 16; ++k) io.in[k] = base.in[k];
-    for (int p = 0; p < 2; ++p) {
-        int k = 16 + K * p;
-        if (ZPOS != 2) io.in[k++] = nx[3 * p];  // the next multiply's other operand
-        io.in[k++] = nx[3 * p + 1];             // a'.v
-        io.in[k] = nx[3 * p + 2];               // b'.v
+    if constexpr (K > 0) {
+        for (int p = 0; p < 2; ++p) {
+            int k = 16 + K * p;
+            if (ZPOS != 2) io.in[k++] = nx[3 * p];  // the next multiply's other operand
+            io.in[k++] = nx[3 * p + 1];             // a'.v
+            io.in[k] = nx[3 * p + 2];               // b'.v
+        }
     }
     for (int k = 0; k < 6; ++k) io.out[k] = base.out[k];
-    for (int k = 0; k < 4; ++k) io.out[6 + k] = nde[k];
+    for (int k = 0; k < (ZPOS == 3 ? 2 : 4); ++k) io.out[6 + k] = nde[k];
     OpCombine2M<ZPOS> f;
     static_cast<OpCombine2&>(f) = op;
     return run_map(s, io, n, f, sms);
@@ -1409,6 +1419,7 @@ cudaError_t launch_beaver_combine2_mask(cudaStream_t s, const uint32_t* const de
         case 0: return combine2m<0>(s, io, next, next_de, op, n, sms);
         case 1: return combine2m<1>(s, io, next, next_de, op, n, sms);
         case 2: return combine2m<2>(s, io, next, next_de, op, n, sms);
+        case 3: return combine2m<3>(s, io, next, next_de, op, n, sms);
     }
     return cudaErrorInvalidValue;
 }

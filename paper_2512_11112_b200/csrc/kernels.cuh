@@ -87,7 +87,8 @@ cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uin
 // z0.m, z1.v, z1.m}; the opened d, e (one copy, identical for both parties) -> open_d/open_e.
 // launch_beaver_combine2 plus the next multiply's mask from the fresh products (zpos: the next
 // multiply's operand that is this product — 0 left, 1 right, 2 both; next[3p..3p+2] = party p's other
-// operand .v (unused for zpos 2), a'.v, b'.v; next_de = d'0 e'0 d'1 e'1)
+// operand .v (unused for zpos 2), a'.v, b'.v; next_de = d'0 e'0 d'1 e'1).  zpos 3: the product is the
+// root — next unused, next_de[0..1] = both parties' opened outputs.
 cudaError_t launch_beaver_combine2_mask(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],
                                         const uint32_t* const tri1[6], const uint32_t alpha[2],
                                         const uint32_t* const alpha_dev[2], uint32_t* const z[4], uint32_t* open_d,

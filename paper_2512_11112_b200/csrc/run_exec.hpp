@@ -498,6 +498,22 @@ struct Exec {
         return -1;
     }
 
+    // `id` is the multiply the root opens (the last node of a straight-line run): its combine can
+    // write the opened outputs of both local parties (the root open without its own launch).
+    bool root_fusable(uint32_t id) {
+        static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;
+        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return false;
+        const auto& rn = r->nodes[r->root];
+        if (rn.kind != SPDZ_NODE_ROOT || rn.n_operands == 0 || rn.operands[0] != id) return false;
+        for (auto& f : r->faults)
+            if (f.node == r->root) return false;
+        for (int p = 0; p < 2; ++p) {
+            const Val& rv = r->parties[p].ns[r->root].out;
+            if (rv.is_public || rv.v != r->parties[p].ns[id].out.v || rv.lanes != r->node(id).lanes) return false;
+        }
+        return true;
+    }
+
     void beaver_pair(uint32_t id, uint64_t off) {
         const auto& n = r->node(id);
         const uint64_t L = n.lanes;
@@ -533,7 +549,15 @@ struct Exec {
         uint32_t* z[4] = {s0.out.v, s0.out.m, s1.out.v, s1.out.m};
         const int tk = tbegin(0);
         const int id2 = fusable_next_mul(id);
-        if (id2 >= 0) {  // the next multiply's mask from the fresh products, in the same pass
+        if (id2 < 0 && root_fusable(id)) {  // the root open from the fresh products, in the same pass
+            uint32_t* const outs[4] = {P0.outputs, P1.outputs, nullptr, nullptr};
+            const uint32_t* const none[6] = {};
+            lk(launch_beaver_combine2_mask(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, 3, none,
+                                           outs, L, SMS(r, 0)),
+               "k_combine2 + root open");
+            r->root_opened = true;
+            tend(0, tk, SPDZ_KSTAT_COMBINE, (88 + 8) * L);  // + both parties' opened outputs written
+        } else if (id2 >= 0) {  // the next multiply's mask from the fresh products, in the same pass
             const uint64_t off2 = provisioned(r->scalar, (uint32_t)id2, 0).base;
             auto &n0 = P0.ns[id2], &n1 = P1.ns[id2];
             const bool zx = n0.xa.v == s0.out.v, zy = n0.xb.v == s0.out.v;
@@ -1213,11 +1237,15 @@ struct Exec {
         if (pair) {  // both local parties' openings (identical words) in one pass
             auto &P0 = r->parties[0], &P1 = r->parties[1];
             dev(r, 0);
-            const int tk = tbegin(0);
-            lk(launch_open_sum2(S(r, 0), P0.ns[r->root].out.v, P1.ns[r->root].out.v, P0.outputs, P1.outputs, L,
-                                SMS(r, 0)),
-               "open root (both parties)");
-            tend(0, tk, SPDZ_KSTAT_OPEN, 16ull * L);
+            if (r->root_opened) {  // already written by the root multiply's combine
+                r->root_opened = false;
+            } else {
+                const int tk = tbegin(0);
+                lk(launch_open_sum2(S(r, 0), P0.ns[r->root].out.v, P1.ns[r->root].out.v, P0.outputs, P1.outputs, L,
+                                    SMS(r, 0)),
+                   "open root (both parties)");
+                tend(0, tk, SPDZ_KSTAT_OPEN, 16ull * L);
+            }
             r->exchanged += 2 * L * 4;
             for (int p = 0; p < 2; ++p)
                 r->parties[p].maclog.push_back({r->parties[p].outputs, r->parties[p].ns[r->root].out.m, nullptr, L, 0,
