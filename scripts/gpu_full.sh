@@ -13,9 +13,11 @@ if [ -z "$SKIP_REF" ]; then
 fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-linear --no-per-party > gpurun_out/ncu_launch.log 2>&1
 NB="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-linear --no-per-party"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:OpCombine2 -s 4 -c 1 -o gpurun_out/prof_combine $NB > gpurun_out/ncu_combine.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:OpMask2 -s 4 -c 1 -o gpurun_out/prof_mask $NB > gpurun_out/ncu_mask.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mac_sigma -s 2 -c 1 -o gpurun_out/prof_sigma $NB > gpurun_out/ncu_sigma.log 2>&1
+NC="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
+# the timed step's first combine (the next multiply's mask fused), its mask and its MAC sigma
+timeout 600 $NC -k regex:OpCombine2 -s 4 -c 1 -o gpurun_out/prof_combine $NB > gpurun_out/ncu_combine.log 2>&1
+timeout 600 $NC -k regex:OpMask2 -s 1 -c 1 -o gpurun_out/prof_mask $NB > gpurun_out/ncu_mask.log 2>&1
+timeout 600 $NC -k regex:k_mac_sigma -s 1 -c 1 -o gpurun_out/prof_sigma $NB > gpurun_out/ncu_sigma.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_matrix_combine2 -s 2 -c 1 -o gpurun_out/prof_matrix_combine2 python scripts/linear_probe.py > gpurun_out/ncu_mc2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_modgemm_tcs -s 6 -c 1 -o gpurun_out/prof_gemm_tcs python scripts/gemm_probe.py 1024 256 --tc-only --prepared > gpurun_out/ncu_gemm.log 2>&1
 timeout 600 python scripts/kernel_bench.py > gpurun_out/kernel_bench.json 2> gpurun_out/kernel_bench.err

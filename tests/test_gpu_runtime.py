@@ -561,3 +561,53 @@ def test_separate_party_kernels_equal_fused(gpu, case):
     for p in range(2):
         for k in range(2):
             np.testing.assert_array_equal(got[False][2][p][k], got[True][2][p][k])
+
+
+_FUSION_PROBE = r"""
+import sys, json
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from oracle import oracle as O
+from paper_2512_11112_b200 import LocalRun, chain_graph
+n, coin = 40963, 0xF00D
+x, y = O.rand_field_vec(n, 21), O.rand_field_vec(n, 22)
+out = {}
+for use_graph in (False, True):
+    r = LocalRun(chain_graph("heavy", n), 2, coin=coin, use_graph=use_graph)
+    r.deal(7)
+    r.bind_inputs({"x": x, "y": y})
+    r.share_inputs()
+    rep = r.online()
+    v, m = r.node_share_host(1, 9)
+    out[str(use_graph)] = [int(np.bitwise_xor.reduce(rep.outputs.astype(np.uint64) * 2654435761 % (1 << 61))),
+                           list(rep.sigmas), int(v.astype(np.uint64).sum()), int(m.astype(np.uint64).sum()),
+                           rep.kernel_launches]
+    r.close()
+print(json.dumps(out))
+"""
+
+
+def test_mask_and_root_fusion_equal_unfused(gpu):
+    """The co-located fusions (next multiply's mask and the root open written by the combine,
+    OpCombine2M) give the same outputs, sigmas and node shares as the separate launches
+    (SPDZ_NO_MASK_FUSION=1), eager and graph-replayed, with fewer launches."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for off in (False, True):
+        env = dict(os.environ)
+        env.pop("SPDZ_NO_MASK_FUSION", None)
+        if off:
+            env["SPDZ_NO_MASK_FUSION"] = "1"
+        p = subprocess.run([sys.executable, "-c", _FUSION_PROBE, root], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[off] = json.loads(p.stdout.strip().splitlines()[-1])
+    for g in ("False", "True"):
+        fused, plain = res[False][g], res[True][g]
+        assert fused[:4] == plain[:4]
+        assert fused[4] < plain[4]  # 3 masks and the root open fewer
