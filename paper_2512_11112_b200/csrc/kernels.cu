@@ -414,6 +414,55 @@ cudaError_t combine_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, c
     return run_map(s, io, n, OpCombine<NP, false>{{alpha, alpha_dev}, party}, sms);
 }
 
+// One party's fused open + combine followed by the next multiply's mask from the fresh product
+// (the co-located OpCombine2M, per party: the N-GPU ranks' kernel mix).  Inputs: OpCombine<NP>'s,
+// then [the next multiply's other operand .v (ZPOS < 2)], a'.v, b'.v.  Outputs: z.v z.m open_d
+// open_e d' e'.
+template <int NP, int ZPOS>
+struct OpCombineM : OpCombine<NP, true> {
+    static constexpr int kX = ZPOS == 2 ? 2 : 3;
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        OpCombine<NP, true>::operator()(in, o);
+        const uint32_t* q = in + 8 + 2 * NP;
+        const uint32_t z = o[0];
+        const uint32_t x = ZPOS == 1 ? q[0] : z, y = ZPOS == 0 ? q[0] : z;
+        const uint32_t* ab = q + (ZPOS == 2 ? 0 : 1);
+        o[4] = fp_sub(x, ab[0]);
+        o[5] = fp_sub(y, ab[1]);
+    }
+};
+
+template <int NP, int ZPOS>
+cudaError_t combine_m_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe, const uint32_t* const* pd,
+                         const uint32_t* const* pe, const uint32_t* const tri[6], int party, uint32_t alpha,
+                         uint32_t* zv, uint32_t* zm, uint32_t* open_d, uint32_t* open_e, const uint32_t* const next[3],
+                         uint32_t* const next_de[2], uint64_t n, int sms, const uint32_t* alpha_dev) {
+    constexpr int K = OpCombineM<NP, ZPOS>::kX;
+    IO<8 + 2 * NP + K, 6> io;
+    io.in[0] = od;
+    io.in[1] = oe;
+    for (int p = 0; p < NP; ++p) {
+        io.in[2 + p] = pd[p];
+        io.in[2 + NP + p] = pe[p];
+    }
+    for (int k = 0; k < 6; ++k) io.in[2 + 2 * NP + k] = tri[k];
+    int k = 8 + 2 * NP;
+    if (ZPOS != 2) io.in[k++] = next[0];
+    io.in[k++] = next[1];
+    io.in[k] = next[2];
+    io.out[0] = zv;
+    io.out[1] = zm;
+    io.out[2] = open_d;
+    io.out[3] = open_e;
+    io.out[4] = next_de[0];
+    io.out[5] = next_de[1];
+    OpCombineM<NP, ZPOS> op;
+    op.alpha = alpha;
+    op.ap = alpha_dev;
+    op.party = party;
+    return run_map(s, io, n, op, sms);
+}
+
 template <int NP>
 cudaError_t open_np(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, uint32_t* out, uint64_t n,
                     int sms) {
@@ -1360,6 +1409,21 @@ cudaError_t launch_beaver_combine(cudaStream_t s, const uint32_t* own_d, const u
         CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_beaver_combine_mask(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                       const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
+                                       const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv,
+                                       uint32_t* zm, uint32_t* open_d, uint32_t* open_e, int zpos,
+                                       const uint32_t* const next[3], uint32_t* const next_de[2], uint64_t n, int sms,
+                                       const uint32_t* alpha_dev) {
+#define CASE(NP, Z)                                                                                              \
+    if (n_peers == NP && zpos == Z)                                                                              \
+        return combine_m_np<NP, Z>(s, own_d, own_e, peer_d, peer_e, tri, party, alpha, zv, zm, open_d, open_e, next, \
+                                   next_de, n, sms, alpha_dev);
+    CASE(1, 0) CASE(1, 1) CASE(1, 2) CASE(2, 0) CASE(2, 1) CASE(2, 2) CASE(3, 0) CASE(3, 1) CASE(3, 2)
+#undef CASE
     return cudaErrorInvalidValue;
 }
 

@@ -85,6 +85,15 @@ cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uin
                                 const uint32_t* const alpha_dev[2], uint32_t* const out[4], uint64_t n, int sms);
 // Both parties of a 2-party run on one GPU: de = {d0, e0, d1, e1} payload halves, z = {z0.v,
 // z0.m, z1.v, z1.m}; the opened d, e (one copy, identical for both parties) -> open_d/open_e.
+// launch_beaver_combine (1-3 peers) plus the next multiply's mask from this party's fresh product
+// (zpos as launch_beaver_combine2_mask; next = other operand .v (unused for zpos 2), a'.v, b'.v;
+// next_de = d', e')
+cudaError_t launch_beaver_combine_mask(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                       const uint32_t* const* peer_d, const uint32_t* const* peer_e, int n_peers,
+                                       const uint32_t* const tri[6], int party, uint32_t alpha, uint32_t* zv,
+                                       uint32_t* zm, uint32_t* open_d, uint32_t* open_e, int zpos,
+                                       const uint32_t* const next[3], uint32_t* const next_de[2], uint64_t n, int sms,
+                                       const uint32_t* alpha_dev);
 // launch_beaver_combine2 plus the next multiply's mask from the fresh products (zpos: the next
 // multiply's operand that is this product — 0 left, 1 right, 2 both; next[3p..3p+2] = party p's other
 // operand .v (unused for zpos 2), a'.v, b'.v; next_de = d'0 e'0 d'1 e'1).  zpos 3: the product is the

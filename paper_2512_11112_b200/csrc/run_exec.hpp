@@ -474,6 +474,8 @@ struct Exec {
     int fusable_next_mul(uint32_t id) {
         static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;  // (A/B experiments)
         if (off || r->cfg || r->opts.node_streams > 1 || r->net) return -1;
+        // the per-party kernels: 1-3 peers (launch_beaver_combine_mask), no fault injection
+        if (!colocated2(r) && (r->n < 2 || r->n > 4 || !r->faults.empty())) return -1;
         const uint64_t L = r->node(id).lanes;
         for (uint32_t k = id + 1; k < r->nodes.size(); ++k) {
             if (!r->live[k]) continue;
@@ -485,7 +487,8 @@ struct Exec {
             if (n.kind != SPDZ_NODE_MUL || n.lanes != L) return -1;
             for (auto& f : r->faults)
                 if (f.node == k) return -1;
-            for (int p = 0; p < 2; ++p) {
+            for (int p = 0; p < r->n; ++p) {
+                if (!r->parties[p].local) continue;
                 const auto &st = r->parties[p].ns[k], &own = r->parties[p].ns[id];
                 const auto& P = r->parties[p];
                 if (st.xa.is_public || st.xb.is_public || P.ns[n.operands[0]].out.lanes != L ||
@@ -611,12 +614,19 @@ struct Exec {
             return;
         }
         std::vector<cudaEvent_t> sent(r->n);
+        if (r->premasked.size() != r->nodes.size()) r->premasked.assign(r->nodes.size(), 0);
+        const bool masked = r->premasked[id];  // [d|e] written and published by the previous combine
+        r->premasked[id] = 0;
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
             auto& st = P.ns[id];
             const Val &a = P.ns[n.operands[0]].out, &b = P.ns[n.operands[1]].out;
             dev(r, p);
+            if (masked) {
+                sent[p] = r->premask_ev[p];
+                continue;
+            }
             if (a.lanes != L) bcast_into(p, a, st.xa);
             if (b.lanes != L) bcast_into(p, b, st.xb);
             const int tk = tbegin(p);
@@ -629,6 +639,8 @@ struct Exec {
         }
         const uint64_t batch = make_batch(id, exec, 0);
         const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
+        const int id2 = fusable_next_mul(id);
+        if (r->premask_ev.size() != (size_t)r->n) r->premask_ev.assign(r->n, nullptr);
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
             auto& P = r->parties[p];
@@ -650,15 +662,32 @@ struct Exec {
             const uint32_t* tri[6];
             for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
             const int tk = tbegin(p);
-            lk(launch_beaver_combine(S(r, p), st.payload, st.payload + L, pd, pe, k, tri, P.ctx->party, P.ctx->alpha,
-                                     st.out.v, st.out.m, st.opened, st.opened + L, L, SMS(r, p), P.ctx->d_alpha),
-               "k_combine");
-            // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
-            tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
+            if (id2 >= 0) {  // + the next multiply's mask from this party's fresh product; published at once
+                auto& nx = P.ns[id2];
+                const uint64_t off2 = provisioned(r->scalar, (uint32_t)id2, 0).base;
+                const bool zx = nx.xa.v == st.out.v, zy = nx.xb.v == st.out.v;
+                const int zpos = zx && zy ? 2 : (zx ? 0 : 1);
+                const uint32_t* next[3] = {zx ? nx.xb.v : nx.xa.v, P.pool[0] + off2, P.pool[2] + off2};
+                uint32_t* const nde[2] = {nx.payload, nx.payload + L};
+                lk(launch_beaver_combine_mask(S(r, p), st.payload, st.payload + L, pd, pe, k, tri, P.ctx->party,
+                                              P.ctx->alpha, st.out.v, st.out.m, st.opened, st.opened + L, zpos, next, nde,
+                                              L, SMS(r, p), P.ctx->d_alpha),
+                   "k_combine + next mask");
+                tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k + (zpos == 2 ? 16 : 20)) * L);
+                r->premask_ev[p] = publish(p, slot_of((uint32_t)id2, 0));
+            } else {
+                lk(launch_beaver_combine(S(r, p), st.payload, st.payload + L, pd, pe, k, tri, P.ctx->party,
+                                         P.ctx->alpha, st.out.v, st.out.m, st.opened, st.opened + L, L, SMS(r, p),
+                                         P.ctx->d_alpha),
+                   "k_combine");
+                // own [d|e] 8 + peers 8k + triple planes 24 + z 8 + opened log 8 bytes per lane
+                tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k) * L);
+            }
             // log_open (runtime.cpp:224): records [d | e] with mac shares [x.m - a.m | y.m - b.m]
             P.maclog.push_back({st.opened, mac_slot(p, id, exec, 0), P.pool[1] + off, L, 0, batch, so, 2 * G});
             P.maclog.push_back({st.opened + L, mac_slot(p, id, exec, 1), P.pool[3] + off, L, 0, batch, G + so, 2 * G});
         }
+        if (id2 >= 0) r->premasked[id2] = 1;
     }
 
     // runtime.cpp:242-281

@@ -572,14 +572,14 @@ from paper_2512_11112_b200 import LocalRun, chain_graph
 n, coin = 40963, 0xF00D
 x, y = O.rand_field_vec(n, 21), O.rand_field_vec(n, 22)
 out = {}
-for use_graph in (False, True):
-    r = LocalRun(chain_graph("heavy", n), 2, coin=coin, use_graph=use_graph)
+for use_graph, sep in ((False, False), (True, False), (False, True), (True, True)):
+    r = LocalRun(chain_graph("heavy", n), 2, coin=coin, use_graph=use_graph, separate_party_kernels=sep)
     r.deal(7)
     r.bind_inputs({"x": x, "y": y})
     r.share_inputs()
     rep = r.online()
     v, m = r.node_share_host(1, 9)
-    out[str(use_graph)] = [int(np.bitwise_xor.reduce(rep.outputs.astype(np.uint64) * 2654435761 % (1 << 61))),
+    out[f"{use_graph}/{sep}"] = [int(np.bitwise_xor.reduce(rep.outputs.astype(np.uint64) * 2654435761 % (1 << 61))),
                            list(rep.sigmas), int(v.astype(np.uint64).sum()), int(m.astype(np.uint64).sum()),
                            rep.kernel_launches]
     r.close()
@@ -588,9 +588,9 @@ print(json.dumps(out))
 
 
 def test_mask_and_root_fusion_equal_unfused(gpu):
-    """The co-located fusions (next multiply's mask and the root open written by the combine,
-    OpCombine2M) give the same outputs, sigmas and node shares as the separate launches
-    (SPDZ_NO_MASK_FUSION=1), eager and graph-replayed, with fewer launches."""
+    """The fusions (next multiply's mask written by the combine — co-located OpCombine2M and per-party
+    OpCombineM — and the co-located root open) give the same outputs, sigmas and node shares as the
+    separate launches (SPDZ_NO_MASK_FUSION=1), eager and graph-replayed, with fewer launches."""
     import json
     import os
     import subprocess
@@ -607,7 +607,8 @@ def test_mask_and_root_fusion_equal_unfused(gpu):
                            timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         res[off] = json.loads(p.stdout.strip().splitlines()[-1])
-    for g in ("False", "True"):
-        fused, plain = res[False][g], res[True][g]
-        assert fused[:4] == plain[:4]
-        assert fused[4] < plain[4]  # 3 masks and the root open fewer
+    for mode, fused in res[False].items():
+        plain = res[True][mode]
+        assert fused[:4] == plain[:4], mode
+        assert fused[4] < plain[4], mode  # 3 masks (and, co-located, the root open) fewer
+    assert res[False]["False/False"][:4] == res[False]["False/True"][:4]  # co-located == per-party kernels
