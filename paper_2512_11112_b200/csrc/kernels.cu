@@ -1443,6 +1443,69 @@ cudaError_t launch_beaver_combine2(cudaStream_t s, const uint32_t* const de[4], 
     return run_map(s, io, n, OpCombine2{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]}, sms);
 }
 
+// OpCombine2 followed, in the same pass, by a private add / sub that consumes this product
+// (backend.cpp:25-51 on both planes: w = z + o, z - o or o - z; SM = 0 / 1 / 2) and then,
+// optionally, the multiply after it that consumes w (its mask: NX = 1 w left, 2 w right, 3 both) or
+// the root opening of w (NX = 4).  Inputs: OpCombine2's 16, then per party o.v o.m [the next
+// multiply's other operand .v (NX 1, 2), a'.v, b'.v].  Outputs: OpCombine2's 6, w.v w.m of both
+// parties, then d'0 e'0 d'1 e'1 (NX 1-3) or both parties' opened outputs (NX 4).
+template <int SM, int NX>
+struct OpCombine2A : OpCombine2 {
+    static constexpr int kMask = NX >= 1 && NX <= 3 ? (NX == 3 ? 2 : 3) : 0;
+    static constexpr int kPer = 2 + kMask;  // extra inputs per party
+    static constexpr int kOut = 10 + (kMask ? 4 : NX == 4 ? 2 : 0);
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        OpCombine2::operator()(in, o);
+        uint32_t w[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const uint32_t* q = in + 16 + kPer * p;
+            const uint32_t zv = o[2 * p], zm = o[2 * p + 1];
+            const uint32_t wv = SM == 0 ? fp_add(zv, q[0]) : SM == 1 ? fp_sub(zv, q[0]) : fp_sub(q[0], zv);
+            const uint32_t wm = SM == 0 ? fp_add(zm, q[1]) : SM == 1 ? fp_sub(zm, q[1]) : fp_sub(q[1], zm);
+            o[6 + 2 * p] = wv;
+            o[7 + 2 * p] = wm;
+            w[p] = wv;
+            if constexpr (kMask > 0) {
+                const uint32_t* r = q + 2;
+                const uint32_t x = NX == 2 ? r[0] : wv, y = NX == 1 ? r[0] : wv;
+                const uint32_t* ab = r + (NX == 3 ? 0 : 1);
+                o[10 + 2 * p] = fp_sub(x, ab[0]);
+                o[11 + 2 * p] = fp_sub(y, ab[1]);
+            }
+        }
+        if constexpr (NX == 4) {
+            o[10] = fp_add(w[0], fp_reduce32(w[1]));
+            o[11] = fp_add(w[1], fp_reduce32(w[0]));
+        }
+    }
+};
+
+template <int SM, int NX>
+static cudaError_t combine2a(cudaStream_t s, const IO<16, 6>& base, const uint32_t* const addin[4],
+                            const uint32_t* const nx[6], uint32_t* const w[4], uint32_t* const extra[4],
+                            const OpCombine2& op, uint64_t n, int sms) {
+    using Op = OpCombine2A<SM, NX>;
+    IO<16 + 2 * Op::kPer, Op::kOut> io;
+    for (int k = 0; k < 16; ++k) io.in[k] = base.in[k];
+    for (int p = 0; p < 2; ++p) {
+        int k = 16 + Op::kPer * p;
+        io.in[k++] = addin[2 * p];      // o.v
+        io.in[k++] = addin[2 * p + 1];  // o.m
+        if constexpr (Op::kMask > 0) {
+            if (NX != 3) io.in[k++] = nx[3 * p];
+            io.in[k++] = nx[3 * p + 1];
+            io.in[k] = nx[3 * p + 2];
+        }
+    }
+    for (int k = 0; k < 6; ++k) io.out[k] = base.out[k];
+    for (int k = 0; k < 4; ++k) io.out[6 + k] = w[k];
+    for (int k = 0; k < Op::kOut - 10; ++k) io.out[10 + k] = extra[k];
+    Op f;
+    static_cast<OpCombine2&>(f) = op;
+    return run_map(s, io, n, f, sms);
+}
+
 template <int ZPOS>
 static cudaError_t combine2m(cudaStream_t s, const IO<16, 6>& base, const uint32_t* const nx[6],
                             uint32_t* const nde[4], const OpCombine2& op, uint64_t n, int sms) {
@@ -1462,6 +1525,31 @@ static cudaError_t combine2m(cudaStream_t s, const IO<16, 6>& base, const uint32
     OpCombine2M<ZPOS> f;
     static_cast<OpCombine2&>(f) = op;
     return run_map(s, io, n, f, sms);
+}
+
+cudaError_t launch_beaver_combine2_add(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],
+                                       const uint32_t* const tri1[6], const uint32_t alpha[2],
+                                       const uint32_t* const alpha_dev[2], uint32_t* const z[4], uint32_t* open_d,
+                                       uint32_t* open_e, int sm, const uint32_t* const addin[4], uint32_t* const w[4],
+                                       int nx, const uint32_t* const next[6], uint32_t* const extra[4], uint64_t n,
+                                       int sms) {
+    IO<16, 6> io;
+    for (int k = 0; k < 4; ++k) io.in[k] = de[k];
+    for (int k = 0; k < 6; ++k) {
+        io.in[4 + k] = tri0[k];
+        io.in[10 + k] = tri1[k];
+    }
+    for (int k = 0; k < 4; ++k) io.out[k] = z[k];
+    io.out[4] = open_d;
+    io.out[5] = open_e;
+    const OpCombine2 op{alpha[0], alpha[1], alpha_dev[0], alpha_dev[1]};
+#define CASE(SM, NX) \
+    if (sm == SM && nx == NX) return combine2a<SM, NX>(s, io, addin, next, w, extra, op, n, sms);
+    CASE(0, 0) CASE(0, 1) CASE(0, 2) CASE(0, 3) CASE(0, 4)
+    CASE(1, 0) CASE(1, 1) CASE(1, 2) CASE(1, 3) CASE(1, 4)
+    CASE(2, 0) CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4)
+#undef CASE
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_beaver_combine2_mask(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],

@@ -85,6 +85,17 @@ cudaError_t launch_share_input2(cudaStream_t s, const uint32_t* x_raw, const uin
                                 const uint32_t* const alpha_dev[2], uint32_t* const out[4], uint64_t n, int sms);
 // Both parties of a 2-party run on one GPU: de = {d0, e0, d1, e1} payload halves, z = {z0.v,
 // z0.m, z1.v, z1.m}; the opened d, e (one copy, identical for both parties) -> open_d/open_e.
+// launch_beaver_combine2 plus the private add / sub that consumes the products (sm: 0 w = z + o,
+// 1 w = z - o, 2 w = o - z; addin = o.v o.m of party 0, party 1; w = w.v w.m of party 0, party 1) and
+// then nx: 0 nothing, 1-3 the mask of the multiply consuming w (w left / right / both; next as in
+// launch_beaver_combine2_mask, extra = d'0 e'0 d'1 e'1), 4 the root opening of w (extra = both
+// parties' opened outputs)
+cudaError_t launch_beaver_combine2_add(cudaStream_t s, const uint32_t* const de[4], const uint32_t* const tri0[6],
+                                       const uint32_t* const tri1[6], const uint32_t alpha[2],
+                                       const uint32_t* const alpha_dev[2], uint32_t* const z[4], uint32_t* open_d,
+                                       uint32_t* open_e, int sm, const uint32_t* const addin[4], uint32_t* const w[4],
+                                       int nx, const uint32_t* const next[6], uint32_t* const extra[4], uint64_t n,
+                                       int sms);
 // launch_beaver_combine (1-3 peers) plus the next multiply's mask from this party's fresh product
 // (zpos as launch_beaver_combine2_mask; next = other operand .v (unused for zpos 2), a'.v, b'.v;
 // next_de = d', e')

@@ -595,6 +595,7 @@ int spdz_run_online_begin(spdz_run* r, int reuse) {
         r->kt.recs.clear();
         // fusion hand-offs never outlive a phase (a phase that threw may have left one set)
         r->premasked.assign(r->nodes.size(), 0);
+        r->precomputed.assign(r->nodes.size(), 0);
         r->root_opened = false;
         if (graphable(r)) {
             cudaStream_t s = S(r, 0);

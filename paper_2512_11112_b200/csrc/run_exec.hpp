@@ -468,15 +468,17 @@ struct Exec {
     // Both parties of a 2-party run on one stream: both masks, then one fused open+combine
     // (payloads read once, opened values logged once).  (Running it in L2-sized lane blocks so
     // the payloads are re-read from L2 measured slower: the per-launch overhead dominated.)
-    // The multiply that runs right after `id` when its mask can be fused into id's combine: the next
-    // live node that launches work is a co-located Beaver multiply of the same lanes (no broadcast)
-    // with this product as an operand, straight-line issue on one stream.  Returns -1 otherwise.
-    int fusable_next_mul(uint32_t id) {
+    // ---- launch fusion along straight-line chains (co-located pair: OpCombine2M / OpCombine2A;
+    // per-party kernels: OpCombineM) ----
+    bool fusion_allowed() {
         static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;  // (A/B experiments)
-        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return -1;
+        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return false;
         // the per-party kernels: 1-3 peers (launch_beaver_combine_mask), no fault injection
-        if (!colocated2(r) && (r->n < 2 || r->n > 4 || !r->faults.empty())) return -1;
-        const uint64_t L = r->node(id).lanes;
+        if (!colocated2(r) && (r->n < 2 || r->n > 4 || !r->faults.empty())) return false;
+        return true;
+    }
+    // the next live node after `id` that launches work (static views and markers skipped), or -1
+    int next_work(uint32_t id) {
         for (uint32_t k = id + 1; k < r->nodes.size(); ++k) {
             if (!r->live[k]) continue;
             const auto& n = r->nodes[k];
@@ -484,37 +486,96 @@ struct Exec {
                 n.kind == SPDZ_NODE_LABEL)
                 continue;
             if (n.kind == SPDZ_NODE_LOAD && !r->parties[r->ref_party()].ns[k].dyn_load) continue;  // a view
-            if (n.kind != SPDZ_NODE_MUL || n.lanes != L) return -1;
-            for (auto& f : r->faults)
-                if (f.node == k) return -1;
-            for (int p = 0; p < r->n; ++p) {
-                if (!r->parties[p].local) continue;
-                const auto &st = r->parties[p].ns[k], &own = r->parties[p].ns[id];
-                const auto& P = r->parties[p];
-                if (st.xa.is_public || st.xb.is_public || P.ns[n.operands[0]].out.lanes != L ||
-                    P.ns[n.operands[1]].out.lanes != L)  // (a broadcast operand is filled by its own node)
-                    return -1;
-                if (st.xa.v != own.out.v && st.xb.v != own.out.v) return -1;
-            }
             return (int)k;
         }
         return -1;
+    }
+    // node k is a private Beaver multiply of L lanes (no broadcast operand, not fault-injected) one of
+    // whose operands is node src's value, for every local party
+    bool mul_consumes(int k, uint32_t src, uint64_t L) {
+        if (k < 0) return false;
+        const auto& n = r->nodes[k];
+        if (n.kind != SPDZ_NODE_MUL || n.lanes != L) return false;
+        for (auto& f : r->faults)
+            if (f.node == (uint32_t)k) return false;
+        for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
+            const auto& P = r->parties[p];
+            const auto &st = P.ns[k], &own = P.ns[src];
+            if (st.xa.is_public || st.xb.is_public || P.ns[n.operands[0]].out.lanes != L ||
+                P.ns[n.operands[1]].out.lanes != L)  // (a broadcast operand is filled by its own node)
+                return false;
+            if (st.xa.v != own.out.v && st.xb.v != own.out.v) return false;
+        }
+        return true;
+    }
+    // The multiply that runs right after `id` when its mask can be fused into id's combine: the next
+    // live node that launches work consumes this product.  Returns -1 otherwise.
+    int fusable_next_mul(uint32_t id) {
+        if (!fusion_allowed()) return -1;
+        const int k = next_work(id);
+        return mul_consumes(k, id, r->node(id).lanes) ? k : -1;
+    }
+    // root node opens node src's value (for every local party, no fault on the root)
+    bool root_opens(uint32_t src, uint64_t L) {
+        const auto& rn = r->nodes[r->root];
+        if (rn.kind != SPDZ_NODE_ROOT || rn.n_operands == 0 || rn.operands[0] != src) return false;
+        for (auto& f : r->faults)
+            if (f.node == r->root) return false;
+        for (int p = 0; p < r->n; ++p) {
+            if (!r->parties[p].local) continue;
+            const Val& rv = r->parties[p].ns[r->root].out;
+            if (rv.is_public || rv.v != r->parties[p].ns[src].out.v || rv.lanes != L) return false;
+        }
+        return true;
+    }
+    // Co-located pair: the next node is a private add / sub consuming this product (its other operand
+    // a different value of the same lanes): fused into the combine (sm: 0 z + o, 1 z - o, 2 o - z), and
+    // after it the multiply consuming its result (nx 1-3, its mask) or the root opening it (nx 4).
+    struct AddFuse {
+        int k1 = -1, sm = 0, k2 = -1, nx = 0;
+    };
+    AddFuse fusable_next_add(uint32_t id) {
+        AddFuse f;
+        if (!fusion_allowed() || !colocated2(r)) return f;
+        const uint64_t L = r->node(id).lanes;
+        const int k1 = next_work(id);
+        if (k1 < 0) return f;
+        const auto& n = r->nodes[k1];
+        if ((n.kind != SPDZ_NODE_ADD && n.kind != SPDZ_NODE_SUB) || n.lanes != L) return f;
+        for (auto& ft : r->faults)
+            if (ft.node == (uint32_t)k1) return f;
+        int sm = -1;
+        for (int p = 0; p < 2; ++p) {
+            const auto& P = r->parties[p];
+            const Val &x = P.ns[n.operands[0]].out, &y = P.ns[n.operands[1]].out, &z = P.ns[id].out,
+                      &w = P.ns[k1].out;
+            if (x.is_public || y.is_public || w.is_public || x.lanes != L || y.lanes != L || w.lanes != L) return f;
+            const bool zl = x.v == z.v, zr = y.v == z.v;
+            if (zl == zr) return f;  // neither operand, or z op z
+            const int s = zl ? (n.kind == SPDZ_NODE_SUB ? 1 : 0) : (n.kind == SPDZ_NODE_SUB ? 2 : 0);
+            if (sm >= 0 && s != sm) return f;
+            sm = s;
+        }
+        f.k1 = k1;
+        f.sm = sm;
+        const int k2 = next_work((uint32_t)k1);
+        if (mul_consumes(k2, (uint32_t)k1, L)) {
+            const auto& st = r->parties[0].ns[k2];
+            const Val& w = r->parties[0].ns[k1].out;
+            const bool wx = st.xa.v == w.v, wy = st.xb.v == w.v;
+            f.k2 = k2;
+            f.nx = wx && wy ? 3 : (wx ? 1 : 2);
+        } else if (root_opens((uint32_t)k1, L)) {
+            f.nx = 4;
+        }
+        return f;
     }
 
     // `id` is the multiply the root opens (the last node of a straight-line run): its combine can
     // write the opened outputs of both local parties (the root open without its own launch).
     bool root_fusable(uint32_t id) {
-        static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;
-        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return false;
-        const auto& rn = r->nodes[r->root];
-        if (rn.kind != SPDZ_NODE_ROOT || rn.n_operands == 0 || rn.operands[0] != id) return false;
-        for (auto& f : r->faults)
-            if (f.node == r->root) return false;
-        for (int p = 0; p < 2; ++p) {
-            const Val& rv = r->parties[p].ns[r->root].out;
-            if (rv.is_public || rv.v != r->parties[p].ns[id].out.v || rv.lanes != r->node(id).lanes) return false;
-        }
-        return true;
+        return fusion_allowed() && colocated2(r) && root_opens(id, r->node(id).lanes);
     }
 
     void beaver_pair(uint32_t id, uint64_t off) {
@@ -552,7 +613,47 @@ struct Exec {
         uint32_t* z[4] = {s0.out.v, s0.out.m, s1.out.v, s1.out.m};
         const int tk = tbegin(0);
         const int id2 = fusable_next_mul(id);
-        if (id2 < 0 && root_fusable(id)) {  // the root open from the fresh products, in the same pass
+        const AddFuse af = id2 < 0 ? fusable_next_add(id) : AddFuse{};
+        if (af.k1 >= 0) {  // + the add / sub consuming the products, then the next mask or the root open
+            auto &w0 = P0.ns[af.k1].out, &w1 = P1.ns[af.k1].out;
+            const auto& an = r->node((uint32_t)af.k1);
+            const bool zl = P0.ns[an.operands[0]].out.v == s0.out.v;
+            const Val &o0 = P0.ns[an.operands[zl ? 1 : 0]].out, &o1 = P1.ns[an.operands[zl ? 1 : 0]].out;
+            const uint32_t* addin[4] = {o0.v, o0.m, o1.v, o1.m};
+            uint32_t* const wo[4] = {w0.v, w0.m, w1.v, w1.m};
+            const uint32_t* next[6] = {};
+            uint32_t* extra[4] = {};
+            uint64_t eb = 0;
+            if (af.k2 >= 0) {
+                const uint64_t off2 = provisioned(r->scalar, (uint32_t)af.k2, 0).base;
+                auto &n0 = P0.ns[af.k2], &n1 = P1.ns[af.k2];
+                const bool wx = af.nx != 2;
+                const uint32_t* nx0[3] = {wx ? n0.xb.v : n0.xa.v, P0.pool[0] + off2, P0.pool[2] + off2};
+                const uint32_t* nx1[3] = {wx ? n1.xb.v : n1.xa.v, P1.pool[0] + off2, P1.pool[2] + off2};
+                for (int k = 0; k < 3; ++k) {
+                    next[k] = nx0[k];
+                    next[3 + k] = nx1[k];
+                }
+                extra[0] = n0.payload;
+                extra[1] = n0.payload + L;
+                extra[2] = n1.payload;
+                extra[3] = n1.payload + L;
+                eb = af.nx == 3 ? 32 : 40;
+            } else if (af.nx == 4) {
+                extra[0] = P0.outputs;
+                extra[1] = P1.outputs;
+                eb = 8;
+            }
+            lk(launch_beaver_combine2_add(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, af.sm,
+                                          addin, wo, af.nx, next, extra, L, SMS(r, 0)),
+               "k_combine2 + add");
+            if (r->precomputed.size() != r->nodes.size()) r->precomputed.assign(r->nodes.size(), 0);
+            r->precomputed[af.k1] = 1;
+            if (af.k2 >= 0) r->premasked[af.k2] = 1;
+            if (af.nx == 4) r->root_opened = true;
+            // + both parties' add: o.v o.m read, w.v w.m written (32), then the mask or the opening
+            tend(0, tk, SPDZ_KSTAT_COMBINE, (88 + 32 + eb) * L);
+        } else if (id2 < 0 && root_fusable(id)) {  // the root open from the fresh products, in the same pass
             uint32_t* const outs[4] = {P0.outputs, P1.outputs, nullptr, nullptr};
             const uint32_t* const none[6] = {};
             lk(launch_beaver_combine2_mask(S(r, 0), de, t0, t1, alpha, alpha_dev, z, s0.opened, s0.opened + L, 3, none,
@@ -1172,6 +1273,10 @@ struct Exec {
                     break;
                 case SPDZ_NODE_ADD:
                 case SPDZ_NODE_SUB:
+                    if (id < r->precomputed.size() && r->precomputed[id]) {  // written by the previous combine
+                        r->precomputed[id] = 0;
+                        break;
+                    }
                     for (int p = 0; p < r->n; ++p) {
                         if (!r->parties[p].local) continue;
                         dev(r, p);

@@ -192,6 +192,7 @@ struct spdz_run {
     std::vector<char> live;         // node's value reaches the root (or a branch): executed
     std::vector<char> premasked;    // co-located multiply whose [d|e] the previous combine already wrote
     bool root_opened = false;       // the root multiply's combine wrote the opened outputs
+    std::vector<char> precomputed;  // co-located add / sub already written by the previous combine
     std::vector<cudaEvent_t> premask_ev;  // per party: the event that published a premasked [d|e]
     uint64_t scalar_live = 0, matrix_live = 0;  // triples the live nodes consume (straight-line)
     NetLink* net = nullptr;         // peers across the reference's TCP mesh (spdz_run_attach_net)

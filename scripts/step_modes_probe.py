@@ -9,13 +9,14 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2512_11112_b200 import LocalRun, chain_graph  # noqa: E402
 
 lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
+kind = sys.argv[2] if len(sys.argv) > 2 else "heavy"
 P = 4294967291
 rng = np.random.default_rng(1)
 x = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
 y = rng.integers(0, P, lanes, dtype=np.uint64).astype(np.uint32)
 for name, kw in (("profile_kernels", {"profile_kernels": True}), ("eager", {}), ("graph", {"use_graph": True}),
                  ("graph+profile", {"use_graph": True, "profile_kernels": True})):
-    run = LocalRun(chain_graph("heavy", lanes), 2, devices=[0, 0], dealer_seed=1, **kw)
+    run = LocalRun(chain_graph(kind, lanes), 2, devices=[0, 0], dealer_seed=1, **kw)
     ms = []
     for k in range(13):
         run.deal(100 + k)
