@@ -490,6 +490,12 @@ struct Exec {
         }
         return -1;
     }
+    // a value read by a fused kernel must not be a view into the product it writes (a load at an
+    // offset of z would be read while other threads store z)
+    static bool disjoint(const Val& o, const Val& z, uint64_t L) {
+        auto apart = [L](const uint32_t* a, const uint32_t* b) { return !a || !b || a + L <= b || b + L <= a; };
+        return apart(o.v, z.v) && apart(o.v, z.m) && apart(o.m, z.v) && apart(o.m, z.m);
+    }
     // node k is a private Beaver multiply of L lanes (no broadcast operand, not fault-injected) one of
     // whose operands is node src's value, for every local party
     bool mul_consumes(int k, uint32_t src, uint64_t L) {
@@ -506,6 +512,8 @@ struct Exec {
                 P.ns[n.operands[1]].out.lanes != L)  // (a broadcast operand is filled by its own node)
                 return false;
             if (st.xa.v != own.out.v && st.xb.v != own.out.v) return false;
+            if (st.xa.v != own.out.v && !disjoint(st.xa, own.out, L)) return false;
+            if (st.xb.v != own.out.v && !disjoint(st.xb, own.out, L)) return false;
         }
         return true;
     }
@@ -553,6 +561,7 @@ struct Exec {
             if (x.is_public || y.is_public || w.is_public || x.lanes != L || y.lanes != L || w.lanes != L) return f;
             const bool zl = x.v == z.v, zr = y.v == z.v;
             if (zl == zr) return f;  // neither operand, or z op z
+            if (!disjoint(zl ? y : x, z, L)) return f;
             const int s = zl ? (n.kind == SPDZ_NODE_SUB ? 1 : 0) : (n.kind == SPDZ_NODE_SUB ? 2 : 0);
             if (sm >= 0 && s != sm) return f;
             sm = s;
