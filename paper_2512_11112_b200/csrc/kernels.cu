@@ -911,6 +911,7 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
         }
         if (g == 0) {
             const uint32_t de = fp_reduce64(acc[4]);
+            uint32_t vv[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {  // spdz.cpp:117-123, linear.cpp:59
                 uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(acc[2 * p]));
@@ -923,6 +924,11 @@ __global__ void __launch_bounds__(kThreads, SPDZ_MC2_MINB) k_matrix_combine2(MC2
                 }
                 a.z[p][0][r] = vr;
                 a.z[p][1][r] = mr;
+                vv[p] = vr;
+            }
+            if (a.open_out[0]) {  // the layer is the root: its opening (net.cpp:170-215) for both parties
+                a.open_out[0][r] = fp_add(vv[0], fp_reduce32(vv[1]));
+                a.open_out[1][r] = fp_add(vv[1], fp_reduce32(vv[0]));
             }
         }
     }
@@ -958,6 +964,7 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
             for (int q = 0; q < 5; ++q) sum[q] = atomicExch(ar + q, 0ull);
             done_rows[r] = 0;
             const uint32_t de = fp_reduce64(sum[4]);
+            uint32_t vv[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 uint32_t vr = fp_reduce64((unsigned long long)a.Cc[p][0][r] + fp_reduce64(sum[2 * p]));
@@ -970,6 +977,11 @@ __device__ __forceinline__ void mc2_flush(const MC2Args& a, unsigned long long (
                 }
                 a.z[p][0][r] = vr;
                 a.z[p][1][r] = mr;
+                vv[p] = vr;
+            }
+            if (a.open_out[0]) {  // the layer is the root: its opening (net.cpp:170-215) for both parties
+                a.open_out[0][r] = fp_add(vv[0], fp_reduce32(vv[1]));
+                a.open_out[1][r] = fp_add(vv[1], fp_reduce32(vv[0]));
             }
         }
     }

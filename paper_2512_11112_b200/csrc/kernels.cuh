@@ -73,6 +73,7 @@ struct MC2Args {
     const uint32_t* alpha_dev[2];  // optional: alpha_i read from device memory (CUDA-graph safe)
     uint32_t* z[2][2];
     uint32_t* opened;
+    uint32_t* open_out[2];  // optional: both parties' opened z.v (the layer is the circuit's root)
 };
 // acc_rows (5 u64 per row) / done_rows (u32 per row): zeroed scratch for the balanced kernel
 // (left zeroed); null selects the warp-per-row kernel

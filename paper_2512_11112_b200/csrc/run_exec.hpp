@@ -1046,9 +1046,15 @@ struct Exec {
                 a.z[p][1] = st.out.m;
             }
             a.opened = s0.opened;
+            const bool opens_root = fusion_allowed() && root_opens(id, dout);  // the root open in the row finaliser
+            if (opens_root) {
+                a.open_out[0] = P0.outputs;
+                a.open_out[1] = P1.outputs;
+            }
             auto* acc_rows = reinterpret_cast<unsigned long long*>(s0.mc2_scratch);
             auto* done_rows = reinterpret_cast<unsigned int*>(s0.mc2_scratch + 10ull * dout);
             lk(launch_matrix_combine2(S(r, 0), a, SMS(r, 0), acc_rows, done_rows), "k_matrix_combine2");
+            if (opens_root) r->root_opened = true;
             // D0 4 + D1 4 + two parties' A.v A.m 16 + opened D 4 per cell (B, E from cache)
             tend(0, tk, SPDZ_KSTAT_COMBINE, 28 * cells);
             r->exchanged += 2 * (cells + etot) * 4;

@@ -585,6 +585,18 @@ for kind, use_graph, sep in (("heavy", False, False), ("heavy", True, False), ("
                            list(rep.sigmas), int(v.astype(np.uint64).sum()), int(m.astype(np.uint64).sum()),
                            rep.kernel_launches]
     r.close()
+from paper_2512_11112_b200 import linear_graph
+din, dout = 512, 300
+inp = {"x": O.rand_field_vec(din, 31), "W": O.rand_field_vec(din * dout, 32), "b": O.rand_field_vec(dout, 33)}
+for use_graph in (False, True):
+    r = LocalRun(linear_graph(din, dout), 2, slice_=4096, coin=coin, use_graph=use_graph)
+    r.deal(8)
+    r.bind_inputs(inp)
+    r.share_inputs()
+    rep = r.online()
+    out[f"linear/{use_graph}/False"] = [int(np.bitwise_xor.reduce(rep.outputs.astype(np.uint64) * 2654435761 % (1 << 61))),
+                                        list(rep.sigmas), 0, 0, rep.kernel_launches]
+    r.close()
 print(json.dumps(out))
 """
 
