@@ -143,13 +143,21 @@ __device__ __forceinline__ uint32_t rep_mod_p(uint32_t l, uint32_t h, uint32_t f
     const uint64_t t = (uint64_t)(uint32_t)(s >> 32) * five + (uint32_t)s;
     return (uint32_t)(t >> 32) * five + (uint32_t)t;
 }
+// The single-party kernel (k_mac_sigma<1>, the one-party-per-GPU layout) takes the >> 30 and >> 31
+// high-word shifts on the ALU: measured in the bench's per-party step, 4.36 -> 4.54 TB/s (bits 0+2;
+// all three 4.52; none 4.36), while the co-located two-party kernel keeps all three on the fma
+// pipe (profiles/r02zb)
+#ifndef SPDZ_SIGMA1_ALU_SHIFTS
+#define SPDZ_SIGMA1_ALU_SHIFTS 5
+#endif
 // r' < 2^32 with r' == mix64(h:l) (mod p)  (hash.hpp:21-26, reduce: field.hpp:14)
+template <int ALU = SPDZ_SIGMA_ALU_SHIFTS>
 __device__ __forceinline__ uint32_t mac_coeff_rep(uint32_t l, uint32_t h, const SigConsts& kc) {
-    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 1) != 0>(l, h, 30, kc.sh30);
+    xorshift_r<(ALU & 1) != 0>(l, h, 30, kc.sh30);
     mul_const(l, h, 0x1ce4e5b9u, 0xbf58476du);
-    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 2) != 0>(l, h, 27, kc.sh27);
+    xorshift_r<(ALU & 2) != 0>(l, h, 27, kc.sh27);
     mul_const(l, h, 0x133111ebu, 0x94d049bbu);
-    xorshift_r<(SPDZ_SIGMA_ALU_SHIFTS & 4) != 0>(l, h, 31, kc.sh31);
+    xorshift_r<(ALU & 4) != 0>(l, h, 31, kc.sh31);
 #ifdef SPDZ_SIGMA_ALU_FIVE
     return rep_mod_p(l, h, 5u);
 #else

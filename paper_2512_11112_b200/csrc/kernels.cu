@@ -574,7 +574,7 @@ __device__ __forceinline__ void z_step(uint32_t& zl, uint32_t& zh) {  // z += ga
 }
 __device__ __forceinline__ void sigma_rec(uint32_t zl, uint32_t zh, uint32_t x, uint32_t m, Acc96& sm, Acc96& sx,
                                           const SigConsts& kc) {
-    const uint32_t r = mac_coeff_rep(zl, zh, kc);
+    const uint32_t r = mac_coeff_rep<SPDZ_SIGMA1_ALU_SHIFTS>(zl, zh, kc);  // (single-party kernel only)
     sm.add(mul_wide(r, m));
     sx.add(mul_wide(r, x));
 }
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, SigmaMinBlocks<NP>::value)
                 uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {
-                    const uint32_t r = mac_coeff_rep(zl, zh, kc);
+                    const uint32_t r = mac_coeff_rep<NP == 1 ? SPDZ_SIGMA1_ALU_SHIFTS : SPDZ_SIGMA_ALU_SHIFTS>(zl, zh, kc);
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
                         const uint32_t xl = l == 0 ? x[p].x : l == 1 ? x[p].y : l == 2 ? x[p].z : x[p].w;
@@ -701,7 +701,8 @@ __global__ void __launch_bounds__(kThreads, SigmaMinBlocks<NP>::value)
         }
         for (uint32_t i = done + threadIdx.x; i < count; i += blockDim.x) {
             const uint64_t z = z0 + (uint64_t)i * kGamma;
-            const uint32_t r = mac_coeff_rep((uint32_t)z, (uint32_t)(z >> 32), kc);
+            const uint32_t r = mac_coeff_rep<NP == 1 ? SPDZ_SIGMA1_ALU_SHIFTS : SPDZ_SIGMA_ALU_SHIFTS>(
+                (uint32_t)z, (uint32_t)(z >> 32), kc);
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
                 uint32_t mm = __ldcs(ma[p] + i);
