@@ -569,7 +569,15 @@ struct Exec {
         f.k1 = k1;
         f.sm = sm;
         const int k2 = next_work((uint32_t)k1);
-        if (mul_consumes(k2, (uint32_t)k1, L)) {
+        bool k2_ok = mul_consumes(k2, (uint32_t)k1, L);
+        for (int p = 0; p < 2 && k2_ok; ++p) {  // its other operand is read, so it must not be this product
+            const auto& P = r->parties[p];
+            const auto& st = P.ns[k2];
+            const Val& w = P.ns[k1].out;
+            if (st.xa.v != w.v && !disjoint(st.xa, P.ns[id].out, L)) k2_ok = false;
+            if (st.xb.v != w.v && !disjoint(st.xb, P.ns[id].out, L)) k2_ok = false;
+        }
+        if (k2_ok) {
             const auto& st = r->parties[0].ns[k2];
             const Val& w = r->parties[0].ns[k1].out;
             const bool wx = st.xa.v == w.v, wy = st.xb.v == w.v;

@@ -585,6 +585,33 @@ for kind, use_graph, sep in (("heavy", False, False), ("heavy", True, False), ("
                            list(rep.sigmas), int(v.astype(np.uint64).sum()), int(m.astype(np.uint64).sum()),
                            rep.kernel_launches]
     r.close()
+from paper_2512_11112_b200 import Graph, NodeSpec
+from paper_2512_11112_b200 import runtime as rt
+# mul, add, mul that reads both the add and the first product, then o - z at the root
+g = Graph()
+gx, gy = g.input("x", n, True), g.input("y", n, True)
+c0 = g.add(NodeSpec(rt.CONST, 1, (), False, const_val=0))
+g.add(NodeSpec(rt.NOP))
+a = g.add(NodeSpec(rt.LOAD, n, (gx, c0), True))
+b = g.add(NodeSpec(rt.LOAD, n, (gy, c0), True))
+t1 = g.add(NodeSpec(rt.MUL, n, (a, b), True))
+t2 = g.add(NodeSpec(rt.ADD, n, (t1, a), True))
+t3 = g.add(NodeSpec(rt.MUL, n, (t2, t1), True))
+t4 = g.add(NodeSpec(rt.SUB, n, (b, t3), True))
+g.root = g.add(NodeSpec(rt.ROOT, n, (t4,), True))
+r = LocalRun(g, 2, coin=coin)
+r.deal(9)
+r.bind_inputs({"x": x, "y": y})
+r.share_inputs()
+rep = r.online()
+c1 = O.np_mul(x, y)
+c2 = ((c1.astype(np.uint64) + x) % 4294967291).astype(np.uint32)
+c3 = O.np_mul(c2, c1)
+want = ((y.astype(np.uint64) + 4294967291 - c3) % 4294967291).astype(np.uint32)
+assert (rep.outputs == want).all(), "custom chain vs cleartext"
+out["custom/False/False"] = [int(np.bitwise_xor.reduce(rep.outputs.astype(np.uint64) * 2654435761 % (1 << 61))),
+                             list(rep.sigmas), 0, 0, rep.kernel_launches]
+r.close()
 from paper_2512_11112_b200 import linear_graph
 din, dout = 512, 300
 inp = {"x": O.rand_field_vec(din, 31), "W": O.rand_field_vec(din * dout, 32), "b": O.rand_field_vec(dout, 33)}
