@@ -163,6 +163,19 @@ struct OpSub : NoPeer {  // backend.cpp:39-51
     }
 };
 
+// Both co-located parties' add / sub in one pass: x0.v x0.m y0.v y0.m x1.v x1.m y1.v y1.m -> z0.v z0.m
+// z1.v z1.m (the same bytes as two OpAdd launches, one launch)
+template <bool SUB>
+struct OpAddSub2 : NoPeer {
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = a[k < 2 ? k : k + 2], y = a[k < 2 ? k + 2 : k + 4];
+            o[k] = SUB ? fp_sub(x, y) : fp_add(x, y);
+        }
+    }
+};
+
 // spdz.cpp:35-75; inputs: xv, xm[, k].  KM: 0 vector k, 1 device scalar
 // broadcast (runtime.cpp:36-39), 2 immediate.
 template <int OPC, int KM>
@@ -1362,6 +1375,12 @@ cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const u
                            const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms) {
     IO<4, 2> io{{xv, xm, yv, ym}, {zv, zm}};
     return sub ? run_map(s, io, n, OpSub{}, sms) : run_map(s, io, n, OpAdd{}, sms);
+}
+
+cudaError_t launch_add_sub2(cudaStream_t s, bool sub, const uint32_t* const xy[8], uint32_t* const z[4], uint64_t n,
+                            int sms) {
+    IO<8, 4> io{{xy[0], xy[1], xy[2], xy[3], xy[4], xy[5], xy[6], xy[7]}, {z[0], z[1], z[2], z[3]}};
+    return sub ? run_map(s, io, n, OpAddSub2<true>{}, sms) : run_map(s, io, n, OpAddSub2<false>{}, sms);
 }
 
 template <int OPC>

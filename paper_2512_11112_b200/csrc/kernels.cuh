@@ -38,6 +38,9 @@ struct LaunchInfo {
 extern std::atomic<unsigned long long> g_kernel_launches;  // evidence counter (calls may be concurrent)
 
 // elementwise (backend.cpp:25-51, spdz.cpp:35-75)
+// both co-located parties: xy = x0.v x0.m y0.v y0.m x1.v x1.m y1.v y1.m, z = z0.v z0.m z1.v z1.m
+cudaError_t launch_add_sub2(cudaStream_t s, bool sub, const uint32_t* const xy[8], uint32_t* const z[4], uint64_t n,
+                            int sms);
 cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
                            const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms);
 // op: 0 add_public 1 sub_public 2 rsub_public 3 mul_public 4 share_of_public (xv/xm unused as inputs)

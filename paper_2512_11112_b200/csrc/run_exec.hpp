@@ -41,6 +41,28 @@ struct Exec {
     }
 
     // runtime.cpp:129-162
+    // both co-located parties' private add / sub of L-lane operands in one launch
+    bool add_pair(uint32_t id, bool sub) {
+        if (!colocated2(r)) return false;
+        const auto& n = r->node(id);
+        const uint64_t L = n.lanes;
+        const Val* v[2][3];
+        for (int p = 0; p < 2; ++p) {
+            auto& P = r->parties[p];
+            v[p][0] = &P.ns[n.operands[0]].out;
+            v[p][1] = &P.ns[n.operands[1]].out;
+            v[p][2] = &P.ns[id].out;
+            for (int k = 0; k < 3; ++k)
+                if (v[p][k]->is_public || v[p][k]->lanes != L) return false;
+        }
+        dev(r, 0);
+        const uint32_t* xy[8] = {v[0][0]->v, v[0][0]->m, v[0][1]->v, v[0][1]->m,
+                                 v[1][0]->v, v[1][0]->m, v[1][1]->v, v[1][1]->m};
+        uint32_t* const z[4] = {v[0][2]->v, v[0][2]->m, v[1][2]->v, v[1][2]->m};
+        lk(launch_add_sub2(S(r, 0), sub, xy, z, L, SMS(r, 0)), "add_batch (both parties)");
+        return true;
+    }
+
     void add(int p, uint32_t id, bool sub) {
         auto& P = r->parties[p];
         const auto& n = r->node(id);
@@ -1300,6 +1322,7 @@ struct Exec {
                         r->precomputed[id] = 0;
                         break;
                     }
+                    if (add_pair(id, n.kind == SPDZ_NODE_SUB)) break;
                     for (int p = 0; p < r->n; ++p) {
                         if (!r->parties[p].local) continue;
                         dev(r, p);
