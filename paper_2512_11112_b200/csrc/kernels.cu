@@ -476,6 +476,62 @@ cudaError_t combine_m_np(cudaStream_t s, const uint32_t* od, const uint32_t* oe,
     return run_map(s, io, n, op, sms);
 }
 
+// One party (one peer) of a 2-party run: OpCombine<1> followed by the private add / sub that
+// consumes the product (SM as OpCombine2A) and optionally the mask of the multiply consuming its
+// result (NX 1 w left, 2 w right, 3 both).  Inputs: OpCombine<1>'s 10, o.v o.m, [other .v (NX 1, 2)],
+// a'.v, b'.v (NX > 0).  Outputs: z.v z.m open_d open_e w.v w.m [d' e'].
+template <int SM, int NX>
+struct OpCombineA : OpCombine<1, true> {
+    static constexpr int kX = 2 + (NX == 0 ? 0 : NX == 3 ? 2 : 3);
+    static constexpr int kOut = NX == 0 ? 6 : 8;
+    __device__ void operator()(const uint32_t* in, uint32_t* o) const {
+        OpCombine<1, true>::operator()(in, o);
+        const uint32_t* q = in + 10;
+        const uint32_t zv = o[0], zm = o[1];
+        const uint32_t wv = SM == 0 ? fp_add(zv, q[0]) : SM == 1 ? fp_sub(zv, q[0]) : fp_sub(q[0], zv);
+        const uint32_t wm = SM == 0 ? fp_add(zm, q[1]) : SM == 1 ? fp_sub(zm, q[1]) : fp_sub(q[1], zm);
+        o[4] = wv;
+        o[5] = wm;
+        if constexpr (NX > 0) {
+            const uint32_t* r = q + 2;
+            const uint32_t x = NX == 2 ? r[0] : wv, y = NX == 1 ? r[0] : wv;
+            const uint32_t* ab = r + (NX == 3 ? 0 : 1);
+            o[6] = fp_sub(x, ab[0]);
+            o[7] = fp_sub(y, ab[1]);
+        }
+    }
+};
+
+template <int SM, int NX>
+cudaError_t combine_a(cudaStream_t s, const uint32_t* const in10[10], const uint32_t* const addin[2],
+                      const uint32_t* const next[3], uint32_t* const out4[4], uint32_t* const w[2],
+                      uint32_t* const next_de[2], int party, uint32_t alpha, const uint32_t* alpha_dev, uint64_t n,
+                      int sms) {
+    using Op = OpCombineA<SM, NX>;
+    IO<10 + Op::kX, Op::kOut> io;
+    for (int k = 0; k < 10; ++k) io.in[k] = in10[k];
+    int k = 10;
+    io.in[k++] = addin[0];
+    io.in[k++] = addin[1];
+    if constexpr (NX > 0) {
+        if (NX != 3) io.in[k++] = next[0];
+        io.in[k++] = next[1];
+        io.in[k] = next[2];
+    }
+    for (int j = 0; j < 4; ++j) io.out[j] = out4[j];
+    io.out[4] = w[0];
+    io.out[5] = w[1];
+    if constexpr (NX > 0) {
+        io.out[6] = next_de[0];
+        io.out[7] = next_de[1];
+    }
+    Op op;
+    op.alpha = alpha;
+    op.ap = alpha_dev;
+    op.party = party;
+    return run_map(s, io, n, op, sms);
+}
+
 template <int NP>
 cudaError_t open_np(cudaStream_t s, const uint32_t* own, const uint32_t* const* peers, uint32_t* out, uint64_t n,
                     int sms) {
@@ -1455,6 +1511,23 @@ cudaError_t launch_beaver_combine_mask(cudaStream_t s, const uint32_t* own_d, co
         return combine_m_np<NP, Z>(s, own_d, own_e, peer_d, peer_e, tri, party, alpha, zv, zm, open_d, open_e, next, \
                                    next_de, n, sms, alpha_dev);
     CASE(1, 0) CASE(1, 1) CASE(1, 2) CASE(2, 0) CASE(2, 1) CASE(2, 2) CASE(3, 0) CASE(3, 1) CASE(3, 2)
+#undef CASE
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_beaver_combine_add(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                      const uint32_t* peer_d, const uint32_t* peer_e, const uint32_t* const tri[6],
+                                      int party, uint32_t alpha, uint32_t* zv, uint32_t* zm, uint32_t* open_d,
+                                      uint32_t* open_e, int sm, const uint32_t* const addin[2], uint32_t* const w[2],
+                                      int nx, const uint32_t* const next[3], uint32_t* const next_de[2], uint64_t n,
+                                      int sms, const uint32_t* alpha_dev) {
+    const uint32_t* in10[10] = {own_d, own_e, peer_d, peer_e, tri[0], tri[1], tri[2], tri[3], tri[4], tri[5]};
+    uint32_t* const out4[4] = {zv, zm, open_d, open_e};
+#define CASE(SM, NX) \
+    if (sm == SM && nx == NX) return combine_a<SM, NX>(s, in10, addin, next, out4, w, next_de, party, alpha, alpha_dev, n, sms);
+    CASE(0, 0) CASE(0, 1) CASE(0, 2) CASE(0, 3)
+    CASE(1, 0) CASE(1, 1) CASE(1, 2) CASE(1, 3)
+    CASE(2, 0) CASE(2, 1) CASE(2, 2) CASE(2, 3)
 #undef CASE
     return cudaErrorInvalidValue;
 }

@@ -100,6 +100,15 @@ cudaError_t launch_beaver_combine2_add(cudaStream_t s, const uint32_t* const de[
                                        uint32_t* open_e, int sm, const uint32_t* const addin[4], uint32_t* const w[4],
                                        int nx, const uint32_t* const next[6], uint32_t* const extra[4], uint64_t n,
                                        int sms);
+// launch_beaver_combine of one party of a 2-party run (one peer) plus the private add / sub that
+// consumes the product (sm, addin = o.v o.m, w = w.v w.m) and nx 0 nothing / 1-3 the mask of the
+// multiply consuming its result (next = other operand .v, a'.v, b'.v; next_de = d', e')
+cudaError_t launch_beaver_combine_add(cudaStream_t s, const uint32_t* own_d, const uint32_t* own_e,
+                                      const uint32_t* peer_d, const uint32_t* peer_e, const uint32_t* const tri[6],
+                                      int party, uint32_t alpha, uint32_t* zv, uint32_t* zm, uint32_t* open_d,
+                                      uint32_t* open_e, int sm, const uint32_t* const addin[2], uint32_t* const w[2],
+                                      int nx, const uint32_t* const next[3], uint32_t* const next_de[2], uint64_t n,
+                                      int sms, const uint32_t* alpha_dev);
 // launch_beaver_combine (1-3 peers) plus the next multiply's mask from this party's fresh product
 // (zpos as launch_beaver_combine2_mask; next = other operand .v (unused for zpos 2), a'.v, b'.v;
 // next_de = d', e')

@@ -567,7 +567,8 @@ struct Exec {
     };
     AddFuse fusable_next_add(uint32_t id) {
         AddFuse f;
-        if (!fusion_allowed() || !colocated2(r)) return f;
+        if (!fusion_allowed() || r->n != 2) return f;  // per-party kernels: one peer (launch_beaver_combine_add)
+        const bool pair = colocated2(r);
         const uint64_t L = r->node(id).lanes;
         const int k1 = next_work(id);
         if (k1 < 0) return f;
@@ -578,6 +579,7 @@ struct Exec {
         int sm = -1;
         for (int p = 0; p < 2; ++p) {
             const auto& P = r->parties[p];
+            if (!P.local) continue;
             const Val &x = P.ns[n.operands[0]].out, &y = P.ns[n.operands[1]].out, &z = P.ns[id].out,
                       &w = P.ns[k1].out;
             if (x.is_public || y.is_public || w.is_public || x.lanes != L || y.lanes != L || w.lanes != L) return f;
@@ -594,18 +596,20 @@ struct Exec {
         bool k2_ok = mul_consumes(k2, (uint32_t)k1, L);
         for (int p = 0; p < 2 && k2_ok; ++p) {  // its other operand is read, so it must not be this product
             const auto& P = r->parties[p];
+            if (!P.local) continue;
             const auto& st = P.ns[k2];
             const Val& w = P.ns[k1].out;
             if (st.xa.v != w.v && !disjoint(st.xa, P.ns[id].out, L)) k2_ok = false;
             if (st.xb.v != w.v && !disjoint(st.xb, P.ns[id].out, L)) k2_ok = false;
         }
         if (k2_ok) {
-            const auto& st = r->parties[0].ns[k2];
-            const Val& w = r->parties[0].ns[k1].out;
+            const int rp = r->ref_party();
+            const auto& st = r->parties[rp].ns[k2];
+            const Val& w = r->parties[rp].ns[k1].out;
             const bool wx = st.xa.v == w.v, wy = st.xb.v == w.v;
             f.k2 = k2;
             f.nx = wx && wy ? 3 : (wx ? 1 : 2);
-        } else if (root_opens((uint32_t)k1, L)) {
+        } else if (pair && root_opens((uint32_t)k1, L)) {  // (the root opening needs both parties' words)
             f.nx = 4;
         }
         return f;
@@ -780,6 +784,7 @@ struct Exec {
         const uint64_t batch = make_batch(id, exec, 0);
         const uint64_t G = r->shard_total ? r->shard_total : L, so = r->shard_off;
         const int id2 = fusable_next_mul(id);
+        const AddFuse af = id2 < 0 ? fusable_next_add(id) : AddFuse{};
         if (r->premask_ev.size() != (size_t)r->n) r->premask_ev.assign(r->n, nullptr);
         for (int p = 0; p < r->n; ++p) {
             if (!r->parties[p].local) continue;
@@ -802,7 +807,32 @@ struct Exec {
             const uint32_t* tri[6];
             for (int t = 0; t < 6; ++t) tri[t] = P.pool[t] + off;
             const int tk = tbegin(p);
-            if (id2 >= 0) {  // + the next multiply's mask from this party's fresh product; published at once
+            if (af.k1 >= 0 && k == 1) {  // + the add / sub consuming the product (+ the next mask, published)
+                const auto& an = r->node((uint32_t)af.k1);
+                const bool zl = P.ns[an.operands[0]].out.v == st.out.v;
+                const Val& o = P.ns[an.operands[zl ? 1 : 0]].out;
+                Val& w = P.ns[af.k1].out;
+                const uint32_t* addin[2] = {o.v, o.m};
+                uint32_t* const wo[2] = {w.v, w.m};
+                const uint32_t* next[3] = {nullptr, nullptr, nullptr};
+                uint32_t* nde[2] = {nullptr, nullptr};
+                const int nx = af.k2 >= 0 ? af.nx : 0;
+                if (af.k2 >= 0) {
+                    auto& nxs = P.ns[af.k2];
+                    const uint64_t off2 = provisioned(r->scalar, (uint32_t)af.k2, 0).base;
+                    next[0] = nx == 1 ? nxs.xb.v : nxs.xa.v;
+                    next[1] = P.pool[0] + off2;
+                    next[2] = P.pool[2] + off2;
+                    nde[0] = nxs.payload;
+                    nde[1] = nxs.payload + L;
+                }
+                lk(launch_beaver_combine_add(S(r, p), st.payload, st.payload + L, pd[0], pe[0], tri, P.ctx->party,
+                                             P.ctx->alpha, st.out.v, st.out.m, st.opened, st.opened + L, af.sm, addin, wo,
+                                             nx, next, nde, L, SMS(r, p), P.ctx->d_alpha),
+                   "k_combine + add");
+                tend(p, tk, SPDZ_KSTAT_COMBINE, (48 + 8ull * k + 16 + (nx == 0 ? 0 : nx == 3 ? 16 : 20)) * L);
+                if (af.k2 >= 0) r->premask_ev[p] = publish(p, slot_of((uint32_t)af.k2, 0));
+            } else if (id2 >= 0) {  // + the next multiply's mask from this party's fresh product; published at once
                 auto& nx = P.ns[id2];
                 const uint64_t off2 = provisioned(r->scalar, (uint32_t)id2, 0).base;
                 const bool zx = nx.xa.v == st.out.v, zy = nx.xb.v == st.out.v;
@@ -828,6 +858,11 @@ struct Exec {
             P.maclog.push_back({st.opened + L, mac_slot(p, id, exec, 1), P.pool[3] + off, L, 0, batch, G + so, 2 * G});
         }
         if (id2 >= 0) r->premasked[id2] = 1;
+        if (af.k1 >= 0) {
+            if (r->precomputed.size() != r->nodes.size()) r->precomputed.assign(r->nodes.size(), 0);
+            r->precomputed[af.k1] = 1;
+            if (af.k2 >= 0) r->premasked[af.k2] = 1;
+        }
     }
 
     // runtime.cpp:242-281
