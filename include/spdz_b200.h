@@ -434,6 +434,11 @@ typedef struct spdz_run_options {
      * combine, MAC sigma, input sharing per party), as they would on separate GPUs; 0
      * (default): two such parties' passes are fused (payloads and coefficients read once). */
     int32_t separate_party_kernels;
+    /* 1: no launch fusion along straight-line chains (each node its own kernels); 0 (default): a
+     * multiply's open+combine also writes what the next issued node needs from its product (the
+     * next multiply's [d|e], an add / sub, the root opening) and co-located adds may pair up.
+     * The environment variable SPDZ_NO_MASK_FUSION=1 forces 1 for every run. */
+    int32_t no_fusion;
 } spdz_run_options_t;
 
 /* Per kernel class: launches, summed CUDA-event time and algorithmic bytes

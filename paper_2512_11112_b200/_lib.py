@@ -67,7 +67,7 @@ class RunOptions(C.Structure):  # spdz_run_options_t
                 ("stream_per_party", C.c_int32), ("shard_offset", C.c_uint64), ("shard_total", C.c_uint64),
                 ("external_mac_verify", C.c_int32), ("single_party", C.c_int32), ("entry_label", C.c_uint32),
                 ("loop_iters", C.c_uint64), ("network", C.c_int32), ("node_streams", C.c_int32),
-                ("separate_party_kernels", C.c_int32)]
+                ("separate_party_kernels", C.c_int32), ("no_fusion", C.c_int32)]
 
 
 class KernelStat(C.Structure):  # spdz_kernel_stat_t

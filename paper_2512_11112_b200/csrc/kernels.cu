@@ -176,6 +176,25 @@ struct OpAddSub2 : NoPeer {
     }
 };
 
+// OpAddSub2 followed by the add / sub that consumes its result (SM2: 0 w2 = w + o, 1 w - o, 2 o - w)
+// and, with ROOT, the root opening of w2.  Inputs: OpAddSub2's 8, o0.v o0.m o1.v o1.m.  Outputs: w0.v
+// w0.m w1.v w1.m, w2 of both parties (4), [both parties' opened outputs].
+template <bool SUB, int SM2, bool ROOT>
+struct OpAddSub2X : NoPeer {
+    __device__ void operator()(const uint32_t* a, uint32_t* o) const {
+        OpAddSub2<SUB>{}(a, o);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t w = o[k], q = a[8 + k];
+            o[4 + k] = SM2 == 0 ? fp_add(w, q) : SM2 == 1 ? fp_sub(w, q) : fp_sub(q, w);
+        }
+        if constexpr (ROOT) {
+            o[8] = fp_add(o[4], fp_reduce32(o[6]));
+            o[9] = fp_add(o[6], fp_reduce32(o[4]));
+        }
+    }
+};
+
 // spdz.cpp:35-75; inputs: xv, xm[, k].  KM: 0 vector k, 1 device scalar
 // broadcast (runtime.cpp:36-39), 2 immediate.
 template <int OPC, int KM>
@@ -1437,6 +1456,35 @@ cudaError_t launch_add_sub2(cudaStream_t s, bool sub, const uint32_t* const xy[8
                             int sms) {
     IO<8, 4> io{{xy[0], xy[1], xy[2], xy[3], xy[4], xy[5], xy[6], xy[7]}, {z[0], z[1], z[2], z[3]}};
     return sub ? run_map(s, io, n, OpAddSub2<true>{}, sms) : run_map(s, io, n, OpAddSub2<false>{}, sms);
+}
+
+template <bool SUB, int SM2, bool ROOT>
+static cudaError_t add_sub2x(cudaStream_t s, const uint32_t* const xy[8], const uint32_t* const o[4],
+                             uint32_t* const z[4], uint32_t* const w[4], uint32_t* const out[2], uint64_t n, int sms) {
+    IO<12, ROOT ? 10 : 8> io;
+    for (int k = 0; k < 8; ++k) io.in[k] = xy[k];
+    for (int k = 0; k < 4; ++k) {
+        io.in[8 + k] = o[k];
+        io.out[k] = z[k];
+        io.out[4 + k] = w[k];
+    }
+    if constexpr (ROOT) {
+        io.out[8] = out[0];
+        io.out[9] = out[1];
+    }
+    return run_map(s, io, n, OpAddSub2X<SUB, SM2, ROOT>{}, sms);
+}
+
+cudaError_t launch_add_sub2_chain(cudaStream_t s, bool sub, const uint32_t* const xy[8], uint32_t* const z[4], int sm2,
+                                  const uint32_t* const o[4], uint32_t* const w[4], uint32_t* const out[2], uint64_t n,
+                                  int sms) {
+#define CASE(SB, SM2, R) \
+    if (sub == SB && sm2 == SM2 && (out != nullptr) == R) return add_sub2x<SB, SM2, R>(s, xy, o, z, w, out, n, sms);
+    CASE(false, 0, false) CASE(false, 1, false) CASE(false, 2, false) CASE(true, 0, false) CASE(true, 1, false)
+    CASE(true, 2, false) CASE(false, 0, true) CASE(false, 1, true) CASE(false, 2, true) CASE(true, 0, true)
+    CASE(true, 1, true) CASE(true, 2, true)
+#undef CASE
+    return cudaErrorInvalidValue;
 }
 
 template <int OPC>

@@ -41,6 +41,11 @@ extern std::atomic<unsigned long long> g_kernel_launches;  // evidence counter (
 // both co-located parties: xy = x0.v x0.m y0.v y0.m x1.v x1.m y1.v y1.m, z = z0.v z0.m z1.v z1.m
 cudaError_t launch_add_sub2(cudaStream_t s, bool sub, const uint32_t* const xy[8], uint32_t* const z[4], uint64_t n,
                             int sms);
+// launch_add_sub2 plus the add / sub consuming its result (sm2: 0 w2 = w + o, 1 w - o, 2 o - w; o =
+// o0.v o0.m o1.v o1.m; w = w2 of both parties) and, with out (both parties' outputs), its root opening
+cudaError_t launch_add_sub2_chain(cudaStream_t s, bool sub, const uint32_t* const xy[8], uint32_t* const z[4], int sm2,
+                                  const uint32_t* const o[4], uint32_t* const w[4], uint32_t* const out[2], uint64_t n,
+                                  int sms);
 cudaError_t launch_add_sub(cudaStream_t s, bool sub, const uint32_t* xv, const uint32_t* xm, const uint32_t* yv,
                            const uint32_t* ym, uint32_t* zv, uint32_t* zm, uint64_t n, int sms);
 // op: 0 add_public 1 sub_public 2 rsub_public 3 mul_public 4 share_of_public (xv/xm unused as inputs)

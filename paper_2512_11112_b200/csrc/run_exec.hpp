@@ -59,7 +59,42 @@ struct Exec {
         const uint32_t* xy[8] = {v[0][0]->v, v[0][0]->m, v[0][1]->v, v[0][1]->m,
                                  v[1][0]->v, v[1][0]->m, v[1][1]->v, v[1][1]->m};
         uint32_t* const z[4] = {v[0][2]->v, v[0][2]->m, v[1][2]->v, v[1][2]->m};
-        lk(launch_add_sub2(S(r, 0), sub, xy, z, L, SMS(r, 0)), "add_batch (both parties)");
+        // the next issued node: an add / sub consuming this result, fused (then its root opening)
+        int k1 = fusion_allowed() ? next_work(id) : -1;
+        int sm2 = -1;
+        const Val* o[2] = {nullptr, nullptr};
+        if (k1 >= 0) {
+            const auto& n1 = r->nodes[k1];
+            bool ok = (n1.kind == SPDZ_NODE_ADD || n1.kind == SPDZ_NODE_SUB) && n1.lanes == L;
+            for (auto& f : r->faults) ok = ok && f.node != (uint32_t)k1;
+            for (int p = 0; p < 2 && ok; ++p) {
+                const auto& P = r->parties[p];
+                const Val &a = P.ns[n1.operands[0]].out, &b = P.ns[n1.operands[1]].out, &w2 = P.ns[k1].out;
+                const Val& w = *v[p][2];
+                ok = !a.is_public && !b.is_public && !w2.is_public && a.lanes == L && b.lanes == L && w2.lanes == L;
+                const bool wl = ok && a.v == w.v, wr = ok && b.v == w.v;
+                ok = ok && wl != wr && disjoint(wl ? b : a, w, L);
+                const int s2 = wl ? (n1.kind == SPDZ_NODE_SUB ? 1 : 0) : (n1.kind == SPDZ_NODE_SUB ? 2 : 0);
+                ok = ok && (sm2 < 0 || s2 == sm2);
+                sm2 = s2;
+                o[p] = wl ? &b : &a;
+            }
+            if (!ok) k1 = -1;
+        }
+        if (k1 < 0) {
+            lk(launch_add_sub2(S(r, 0), sub, xy, z, L, SMS(r, 0)), "add_batch (both parties)");
+            return true;
+        }
+        const uint32_t* ov[4] = {o[0]->v, o[0]->m, o[1]->v, o[1]->m};
+        auto &w0 = r->parties[0].ns[k1].out, &w1 = r->parties[1].ns[k1].out;
+        uint32_t* const wo[4] = {w0.v, w0.m, w1.v, w1.m};
+        const bool root = root_opens((uint32_t)k1, L);
+        uint32_t* outs[2] = {r->parties[0].outputs, r->parties[1].outputs};
+        lk(launch_add_sub2_chain(S(r, 0), sub, xy, z, sm2, ov, wo, root ? outs : nullptr, L, SMS(r, 0)),
+           "add_batch + next add (both parties)");
+        if (r->precomputed.size() != r->nodes.size()) r->precomputed.assign(r->nodes.size(), 0);
+        r->precomputed[k1] = 1;
+        if (root) r->root_opened = true;
         return true;
     }
 
@@ -494,7 +529,7 @@ struct Exec {
     // per-party kernels: OpCombineM) ----
     bool fusion_allowed() {
         static const bool off = std::getenv("SPDZ_NO_MASK_FUSION") != nullptr;  // (A/B experiments)
-        if (off || r->cfg || r->opts.node_streams > 1 || r->net) return false;
+        if (off || r->opts.no_fusion || r->cfg || r->opts.node_streams > 1 || r->net) return false;
         // the per-party kernels: 1-3 peers (launch_beaver_combine_mask), no fault injection
         if (!colocated2(r) && (r->n < 2 || r->n > 4 || !r->faults.empty())) return false;
         return true;

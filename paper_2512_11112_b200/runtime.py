@@ -213,7 +213,8 @@ class LocalRun:
                  devices=None, coin: int | None = None, profile_kernels: bool = False,
                  stream_per_party: bool = False, shard: tuple | None = None, external_mac_verify: bool = False,
                  single_party: int | None = None, use_graph: bool = False, loop_iters: int = 64,
-                 network: bool = False, node_streams: int = 1, separate_party_kernels: bool = False):
+                 network: bool = False, node_streams: int = 1, separate_party_kernels: bool = False,
+                 fusion: bool = True):
         self.graph, self.n = graph, n_parties
         o = _lib.RunOptions()
         o.slice = slice_
@@ -231,6 +232,8 @@ class LocalRun:
         o.node_streams = int(node_streams)
         # parties sharing a stream still run their own kernels (the multi-GPU kernel mix on one GPU)
         o.separate_party_kernels = int(separate_party_kernels)
+        # a multiply's combine also writes what the next issued node needs
+        o.no_fusion = int(not fusion)
         if shard is not None:  # (offset, total): this run holds lanes [offset, offset+L) of a total-lane circuit
             o.shard_offset, o.shard_total = int(shard[0]), int(shard[1])
         o.external_mac_verify = int(external_mac_verify or single_party is not None)

@@ -630,8 +630,9 @@ print(json.dumps(out))
 
 def test_mask_and_root_fusion_equal_unfused(gpu):
     """The fusions (next multiply's mask written by the combine — co-located OpCombine2M and per-party
-    OpCombineM —, the co-located add / sub after a multiply with the mask or root opening after it
-    (OpCombine2A) and the co-located root open) give the same outputs, sigmas and node shares as the
+    OpCombineM —, the add / sub after a multiply with the mask or root opening after it (OpCombine2A,
+    OpCombineA), two co-located adds in one pass (OpAddSub2X) and the co-located root open) give the
+    same outputs, sigmas and node shares as the
     separate launches (SPDZ_NO_MASK_FUSION=1), heavy and mixed chains, eager and graph-replayed, with
     fewer launches."""
     import json
@@ -653,8 +654,6 @@ def test_mask_and_root_fusion_equal_unfused(gpu):
     for mode, fused in res[False].items():
         plain = res[True][mode]
         assert fused[:4] == plain[:4], mode
-        assert fused[4] <= plain[4], mode
-        if not mode.startswith("light") and not (mode.startswith("mixed") and mode.endswith("True")):
-            assert fused[4] < plain[4], mode  # masks, adds and the co-located root open fewer
+        assert fused[4] < plain[4], mode  # masks, adds and the co-located root open fewer
     for kind in ("heavy", "mixed"):  # co-located == per-party kernels
         assert res[False][f"{kind}/False/False"][:4] == res[False][f"{kind}/False/True"][:4]
