@@ -667,12 +667,13 @@ def run_ours(args, world, rank, local):
     st = kstat[dom]
     achieved = (st["bytes"] / max(st["launches"], 1)) / ((st["ms"] / max(st["launches"], 1)) / 1e3) / 1e9
     step_ms = total_ms / args.steps
-    shares = {n: round(kstat[n]["ms"] / args.steps / step_ms, 4) for n in kstat}
+    ran = [n for n in kstat if kstat[n]["launches"]]  # (fused classes, e.g. the co-located root open, launch nothing)
+    shares = {n: round(kstat[n]["ms"] / args.steps / step_ms, 4) for n in ran}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": load_traffic(dom), "kernel": dom,
                 "peak_source": peak_kind, "bytes_per_launch": st["bytes"] // max(st["launches"], 1),
                 "launch_ms": round(st["ms"] / max(st["launches"], 1), 4), "step_share": shares,
-                "all_kernels_gbs": {n: round(kstat[n]["bytes"] / max(kstat[n]["ms"], 1e-9) / 1e6, 1) for n in kstat}}
+                "all_kernels_gbs": {n: round(kstat[n]["bytes"] / max(kstat[n]["ms"], 1e-9) / 1e6, 1) for n in ran}}
     per_party = None
     if world == 1 and not args.no_per_party:
         per_party = per_party_block(args, dev, inputs, spot, step_ms, kstat)
